@@ -1,0 +1,387 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 isotropic-splat train step (BASELINE.json metric).
+
+Default workload (config C3, BASELINE.json configs[2]): 1M isotropic Gaussians
+(isg-synth v1, seed 2403), one 1920x1080 view per GPU per step, forward + L2 loss + backward
++ Adam, target = render of the seed-14244 scene.  One "step" = one view per GPU + one Adam
+step on every replica (gradients all-reduced over NCCL when N > 1): weak scaling.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3|c2|c4|c5]
+  python bench.py --impl reference ...   # CPU reference arm (oracle port, all host cores)
+
+`value` is device-resident throughput (inputs in HBM before the timed region); `e2e` is the
+same metric through the C-ABI with host buffers (target H2D + loss D2H inside the timed
+region).  The roofline object reports the dominant kernel; cpu_baseline times the CPU oracle
+(the FP32 tiled restatement) on the box's host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # name: (n_gaussians, W, H, views_per_step_total, train, description)
+    "c2": (1_000_000, 1920, 1080, 1, False, "synthetic 1M isotropic Gaussians, 1920x1080 render"),
+    "c3": (1_000_000, 1920, 1080, 1, True,
+           "synthetic 1M isotropic Gaussians, 1920x1080, fwd+L2+bwd+Adam, 1 view/GPU/step"),
+    "c4": (3_000_000, 1920, 1080, 8, True,
+           "synthetic 3M isotropic Gaussians, 1080p, 8-view batch per step sharded over GPUs"),
+    "c5": (10_000_000, 3840, 2160, 1, True, "synthetic 10M isotropic Gaussians, 4K fwd+bwd+Adam"),
+}
+T_MIN = 1e-5
+METRIC = "fwd+bwd train iters/sec (1M isotropic Gaussians, 1080p)"
+
+# Algorithmic FP32 work per (pixel, list entry) pair, FLOPs (FMA = 2), see DESIGN.md §Roofline:
+FWD_FLOP_EVAL, FWD_FLOP_IN = 6, 12      # 3-sigma test; exp+alpha+composite+transmittance
+BWD_FLOP_EVAL, BWD_FLOP_IN = 6, 44      # same test; transmittance recovery + 7 gradients
+FP32_LANES = 148 * 128
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text()), "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, index: int):
+        self.p = None
+        self.out = ROOT / "gpurun_out" / f"clocks_{os.getpid()}.csv"
+        self.index = index
+
+    def __enter__(self):
+        try:
+            self.out.parent.mkdir(exist_ok=True)
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.out, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in self.out.read_text().strip().splitlines() if r.strip()]
+        except Exception:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows if r[0].strip().replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].strip().lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def cpu_oracle_train_step(ms, co, cam, target, steps=1, threads=0):
+    """CPU oracle (FP32 tiled restatement, oracle/isg_oracle.c) train step: forward + L2 +
+    backward + Adam, timed.  Returns seconds per step."""
+    import oracle as O
+    ms, co = ms.copy(), co.copy()
+    m = np.zeros((ms.shape[0], 8), np.float32)
+    v = np.zeros_like(m)
+    t0 = time.perf_counter()
+    for s in range(1, steps + 1):
+        _, g = O.loss_backward32(ms, co, cam, target, t_min=T_MIN, threads=threads)
+        O.adam32(ms, co, m, v, g, s, [1e-3, 5e-3, 1e-2, 1e-2], 0.9, 0.999, 1e-15)
+    return (time.perf_counter() - t0) / steps
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------------------------------------
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    from paper_2403_14244_b200 import isg  # host-side synth only (no device work)
+    n, W, H, views, train, desc = CONFIGS[args.config]
+    ms, co = isg.synth_scene(n, W, H, seed=2403)
+    tms, tco = isg.synth_scene(n, W, H, seed=14244)
+    cam = isg.Camera.synthetic(W, H)
+    import oracle as O
+    target = O.render32(tms, tco, cam, t_min=T_MIN)
+    cores = host_threads()
+    for _ in range(args.warmup):
+        cpu_oracle_train_step(ms, co, cam, target, 1, cores)
+    times = [cpu_oracle_train_step(ms, co, cam, target, 1, cores) for _ in range(args.steps)]
+    sec = float(np.median(times))
+    val = 1.0 / sec
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "iters/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (isg-synth v1, seeds 2403/14244)",
+            "config": {"workload": desc, "n_gaussians": n, "width": W, "height": H,
+                       "t_min": T_MIN},
+            "cpu_baseline": {"value": val, "unit": "iters/s", "cores": cores, "kind": "port",
+                             "sample": f"{args.steps} full C3 train steps (fwd+L2+bwd+Adam) of the "
+                                       "FP32 tiled CPU oracle; the reference itself has no 3D "
+                                       "backward (SPEC.md:484)"},
+            "e2e": {"value": val, "unit": "iters/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+def run_isg(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2403_14244_b200 import isg
+
+    rank, world, local = env_rank()
+    if world != args.gpus:
+        args.gpus = world
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n, W, H, views_total, train, desc = CONFIGS[args.config]
+    views_per_rank = max(1, views_total // world) if args.config == "c4" else 1
+    step_views = views_per_rank * world
+    stream = torch.cuda.current_stream()
+
+    ms, co = isg.synth_scene(n, W, H, seed=2403)
+    tms, tco = isg.synth_scene(n, W, H, seed=14244)
+    r = isg.Renderer(local, n, W, H)
+    r.set_stream(stream.cuda_stream)
+    opts = isg.RenderOptions(t_min=T_MIN)
+    cfg = isg.AdamConfig()
+    my_views = [rank * views_per_rank + i for i in range(views_per_rank)]
+    n_views_cam = views_total if args.config == "c4" else max(world, 1)
+    cams = [isg.Camera.synthetic(W, H, v % n_views_cam, n_views_cam) for v in
+            (my_views if args.config == "c4" else [rank])]
+    # targets: renders of the target scene, resident in HBM
+    targets = []
+    r.set_scene(tms, tco)
+    for c in cams:
+        t = torch.empty((H, W, 3), dtype=torch.float32, device="cuda")
+        r.render_device(c, opts, t.data_ptr())
+        targets.append(t)
+    r.synchronize()
+    r.set_scene(ms, co)
+    if world > 1:
+        uid = r.nccl_unique_id() if rank == 0 else b"\0" * 128
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        r.nccl_init(world, rank, obj[0])
+
+    def step():
+        if train:
+            for c, t in zip(cams, targets):
+                r.loss_backward_device(c, t.data_ptr(), opts, weight=1.0 / step_views)
+            r.adam_step(cfg)
+        else:
+            r.render_device(cams[0], opts, targets[0].data_ptr())
+
+    # one synchronous frame sizes the key buffers (capacity growth happens here, untimed)
+    if train:
+        r.loss_backward(cams[0], targets[0].cpu().numpy(), opts, weight=1.0 / step_views)
+        r.zero_grads()
+    else:
+        r.render(cams[0], opts)
+    for _ in range(max(args.warmup, 3)):
+        step()
+    r.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- device-resident timed region ----------------------------------------------------
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    barrier()
+    with ClockSampler(local) as clocks:
+        ev[0].record(stream)
+        for i in range(args.steps):
+            step()
+            ev[i + 1].record(stream)
+        barrier()
+    r.synchronize()  # surfaces overflow / validation errors of the async frames
+    step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    total_ms = ev[0].elapsed_time(ev[-1])
+    if world > 1:
+        tt = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    ms_per_step = total_ms / args.steps
+    value = (step_views if train else 1 * world) / (ms_per_step / 1e3)
+    launches_before = r.stats()["kernel_launches"]
+
+    # ---- stage timing (separate pass, events per kernel) ----------------------------------
+    r.profile(True)
+    r.profile_read()
+    prof_steps = max(3, min(args.steps, 10))
+    for _ in range(prof_steps):
+        step()
+    prof = r.profile_read()
+    r.profile(False)
+    launches_per_step = None
+
+    # ---- end to end through the C-ABI with host buffers ----------------------------------
+    host_targets = [t.cpu().numpy() for t in targets]
+    pinned = [torch.from_numpy(h).pin_memory() for h in host_targets]
+    host_views = [p.numpy() for p in pinned]
+    e2e_ms = []
+    barrier()
+    l0 = r.stats()["kernel_launches"]
+    for i in range(args.steps):
+        t0 = time.perf_counter()
+        if train:
+            for c, h in zip(cams, host_views):
+                r.loss_backward(c, h, opts, weight=1.0 / step_views)  # H2D target, D2H loss
+            r.adam_step(cfg)
+            r.synchronize()
+        else:
+            out = np.empty((H, W, 3), np.float32)
+            r.render(cams[0], opts)  # D2H image
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    launches_per_step = (r.stats()["kernel_launches"] - l0) / args.steps
+    e2e_step = float(np.mean(e2e_ms))
+    if world > 1:
+        tt = torch.tensor([e2e_step], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_step = float(tt.item())
+    e2e_value = (step_views if train else world) / (e2e_step / 1e3)
+    h2d = sum(h.nbytes for h in host_views) if train else 0
+    d2h = 8 * len(host_views) if train else W * H * 3 * 4
+
+    st = r.stats()
+    if rank != 0:
+        r.close()
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel ----------------------------------------------------
+    peaks, peak_kind = load_peaks()
+    top = max(prof.items(), key=lambda kv: kv[1][0])
+    top_name, (top_ms_total, top_calls) = top
+    top_ms = top_ms_total / max(top_calls, 1)
+    roof = {"kernel": top_name, "stage_ms_per_step": {k: v[0] / prof_steps for k, v in prof.items()}}
+    pairs = None
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        import oracle as O
+        cam0 = cams[0]
+        tgt0 = host_targets[0]
+        ms_now, co_now = r.get_scene()
+        t0 = time.perf_counter()
+        _, _, _, counts = O.render32(ms_now, co_now, cam0, t_min=T_MIN, want_state=True)
+        pairs = (int(counts[0]), int(counts[1]))
+        cores = host_threads()
+        sec = cpu_oracle_train_step(ms_now, co_now, cam0, tgt0, 1, cores) if train else \
+            (time.perf_counter() - t0)
+        cpu = {"value": 1.0 / sec, "unit": "iters/s" if train else "frames/s", "cores": cores,
+               "kind": "port",
+               "sample": ("1 full C3 train step (fwd+L2+bwd+Adam) of the FP32 tiled CPU oracle"
+                          if train else "1 full C2 frame of the FP32 tiled CPU oracle")}
+    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+    if top_name in ("blend_fwd", "blend_bwd") and pairs:
+        ev_p, in_p = pairs
+        flops = (FWD_FLOP_EVAL * ev_p + FWD_FLOP_IN * in_p) if top_name == "blend_fwd" else \
+            (BWD_FLOP_EVAL * ev_p + BWD_FLOP_IN * in_p)
+        achieved = flops / (top_ms / 1e3) / 1e12
+        peak = 2 * FP32_LANES * sm_mhz * 1e6 / 1e12
+        roof.update({"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "work": f"{flops:.3e} algorithmic FP32 FLOP/launch ({ev_p} evaluated + "
+                             f"{in_p} in-circle pixel-splat pairs)",
+                     "peak_kind": f"spec FP32 FMA rate at the measured sm_max_mhz {sm_mhz:.0f}"})
+    else:
+        gb = {"preprocess": 56 * n, "project_adam": 192 * n, "depth_sort": 4 * 16 * n,
+              "tile_sort": 2 * 16 * st["n_keys"], "scan_emit": 48 * n + 8 * st["n_keys"]}.get(top_name)
+        if gb:
+            achieved = gb / (top_ms / 1e3) / 1e9
+            roof.update({"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
+                         "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                         "peak_kind": peak_kind})
+    roof["ms_per_launch"] = top_ms
+
+    clk = clocks.summary()
+    line = {
+        "metric": METRIC if train else "render FPS (1M isotropic Gaussians, 1080p)",
+        "value": value, "unit": "iters/s" if train else "frames/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "ms_per_step_median": float(np.median(step_ms)),
+        "higher_is_better": True, "scaling": "weak" if args.config != "c4" else "strong",
+        "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (isg-synth v1: scene seed 2403, target seed 14244)",
+        "config": {"workload": desc, "config": args.config, "n_gaussians": n, "width": W,
+                   "height": H, "views_per_step": step_views, "t_min": T_MIN,
+                   "parallelism": f"dp{world} (views sharded, scene replicated)",
+                   "l2": "no flush: per-step working set (scene+Adam state 96 MB, keys "
+                         f"{st['n_keys'] * 16 / 1e6:.0f} MB, images 50 MB) exceeds the 126 MB L2"},
+        "e2e": {"value": e2e_value, "unit": "iters/s" if train else "frames/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": e2e_step},
+        "gpu_launches": int(round(launches_per_step * args.steps)) if launches_per_step else None,
+        "gpu_launches_per_step": launches_per_step,
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "clocks": clk,
+        "stats": {"n_visible": st["n_visible"], "n_keys": st["n_keys"],
+                  "pairs_evaluated": pairs[0] if pairs else None,
+                  "pairs_in_circle": pairs[1] if pairs else None},
+    }
+    print(json.dumps(line), flush=True)
+    r.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="isg", choices=["isg", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_isg(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,167 @@
+/*
+ * isg.h — the C-ABI drop-in boundary of the B200 isotropic-splat hot path.
+ *
+ * Every entry point is `extern "C"`, takes plain pointers and sizes, never
+ * throws, and returns an isg_status.  The C++ host API in
+ * paper_2403_14244_b200/csrc/isosplat_b200.hpp (a drop-in for the reference's
+ * `isosplat::render`, /root/reference/proj/include/isosplat/splat3d.hpp:96-97)
+ * and the Python binding (paper_2403_14244_b200/isg.py) are both thin layers
+ * over these functions.  INTEGRATION.md shows the binding a maintainer of the
+ * reference would add.
+ *
+ * Reference interfaces each entry replaces (file:line under /root/reference/proj):
+ *   isg_camera          <- struct Camera                  include/isosplat/splat3d.hpp:37-53
+ *   isg_set_scene       <- std::span<const IsoSplat3D>    include/isosplat/splat3d.hpp:13-22, 96
+ *                          (+ IsoSplat3D::validate        src/splat3d.cpp:10-17, done on device)
+ *   isg_render          <- isosplat::render(iso)          include/isosplat/splat3d.hpp:96-97,
+ *                                                         src/splat3d.cpp:173-194
+ *   isg_loss_backward   <- mse (L2)                       src/image.cpp:50-58, plus the 3D
+ *                          backward the reference lacks (SPEC.md:484 non-goal; 2D pattern
+ *                          loss_gradients src/loss.cpp:259-300)
+ *   isg_adam_step       <- update_step(iso)               src/optimize.cpp:78-108 (optimizer slot;
+ *                          log-sigma convention :93,:105; skip non-finite :87-90), Adam rule
+ *   isg_debug_bins      <- sort_by_depth                  src/splat3d.cpp:164-169 (parity hook)
+ *   isg_status codes    <- std::domain_error / std::invalid_argument / CLI exit codes
+ *                          src/splat3d.cpp:10-37, tools/isosplat_main.cpp:30-33
+ *
+ * Data layout (host and device): scenes are SoA float4 arrays
+ *   mu_sigma[n][4]    = (mu.x, mu.y, mu.z, sigma)       world units
+ *   rgb_opacity[n][4] = (r, g, b, opacity)
+ * images are row-major interleaved HWC float32 (ImageGrid, include/isosplat/image.hpp:11-31),
+ * gradients are n x 8 float32: (dmu.x, dmu.y, dmu.z, dsigma, dr, dg, db, dopacity).
+ */
+#ifndef ISG_H_
+#define ISG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ISG_TILE 16 /* screen tiles are ISG_TILE x ISG_TILE pixels */
+#define ISG_ABI_VERSION 1
+
+typedef struct isg_ctx isg_ctx; /* one per device: device buffers, a stream, Adam state. NOT thread-safe. */
+
+/* Camera (splat3d.hpp:37-53) in FP32: row-major world->camera rotation R, translation t,
+ * pinhole focal length and principal point in pixels, image size. */
+typedef struct {
+  float R[9];
+  float t[3];
+  float focal;
+  float cx, cy;
+  int32_t width, height;
+} isg_camera;
+
+typedef enum {
+  ISG_OK = 0,
+  ISG_E_DOMAIN = 1,   /* invalid splat / camera: reference throws std::domain_error */
+  ISG_E_ARG = 2,      /* invalid argument / config: std::invalid_argument */
+  ISG_E_CUDA = 3,     /* CUDA runtime error (incl. no device) */
+  ISG_E_OOM = 4,      /* device allocation failed */
+  ISG_E_OVERFLOW = 5, /* internal capacity exceeded and could not grow */
+  ISG_E_NCCL = 6,     /* NCCL unavailable or failed */
+  ISG_E_STATE = 7     /* call out of order (e.g. adam before any backward) */
+} isg_status;
+
+typedef struct {
+  int64_t n_gaussians;    /* scene size */
+  int64_t n_visible;      /* splats with >= 1 tile in the last binning */
+  int64_t n_keys;         /* (tile, splat) pairs in the last binning */
+  int64_t key_capacity;   /* allocated key slots */
+  int64_t n_tiles;        /* tiles of the last camera */
+  int64_t adam_steps;     /* optimizer steps taken */
+  int64_t skipped_updates;/* Gaussian updates skipped for non-finite gradients (optimize.cpp:87-90) */
+  int64_t regrow_events;  /* frames re-run after key-capacity growth */
+  int64_t kernel_launches;/* kernels launched by this context so far */
+} isg_stats;
+
+/* ---- lifetime -------------------------------------------------------------------------- */
+isg_status isg_create(int device, int64_t max_gaussians, int32_t max_width, int32_t max_height,
+                      isg_ctx** out);
+void isg_destroy(isg_ctx* ctx);
+const char* isg_last_error(const isg_ctx* ctx);
+const char* isg_status_string(isg_status s);
+int isg_abi_version(void);
+/* Run all work on an external cudaStream_t (e.g. torch's current stream); NULL = own stream. */
+isg_status isg_set_stream(isg_ctx* ctx, void* cuda_stream);
+isg_status isg_synchronize(isg_ctx* ctx);
+isg_status isg_get_stats(const isg_ctx* ctx, isg_stats* out);
+
+/* ---- scene ----------------------------------------------------------------------------- */
+/* Host pointers.  Validation (IsoSplat3D::validate, splat3d.cpp:10-17) runs on the device and
+ * surfaces as ISG_E_DOMAIN (with the reference's message) from the next render/backward. */
+isg_status isg_set_scene(isg_ctx* ctx, int64_t n, const float* mu_sigma, const float* rgb_opacity);
+/* Device pointers (already resident in HBM); copied device-to-device, stream-ordered. */
+isg_status isg_set_scene_device(isg_ctx* ctx, int64_t n, const float* mu_sigma_dev,
+                                const float* rgb_opacity_dev);
+isg_status isg_get_scene(isg_ctx* ctx, float* mu_sigma, float* rgb_opacity);
+
+/* ---- forward --------------------------------------------------------------------------- */
+/* render (splat3d.cpp:173-194) into a host HWC3 float image.  t_min: early-termination
+ * threshold on transmittance (0 = exact reference semantics, never terminate early). */
+isg_status isg_render(isg_ctx* ctx, const isg_camera* cam, const float bg[3], float t_min,
+                      float* out_hwc3);
+/* Same, device output pointer, asynchronous on the context stream (no host sync). */
+isg_status isg_render_device(isg_ctx* ctx, const isg_camera* cam, const float bg[3], float t_min,
+                             float* out_hwc3_dev);
+
+/* ---- training -------------------------------------------------------------------------- */
+/* Forward + L2 loss (weight * mse, image.cpp:50-58) + backward for one view.  Gradients
+ * ACCUMULATE into the context's n x 8 buffer until isg_adam_step / isg_zero_grads.
+ * target_hwc3: host pointer; *loss_out receives weight * mse (double). */
+isg_status isg_loss_backward(isg_ctx* ctx, const isg_camera* cam, const float bg[3], float t_min,
+                             const float* target_hwc3, float weight, double* loss_out);
+/* Device target pointer; asynchronous; the loss accumulates on device (isg_read_loss). */
+isg_status isg_loss_backward_device(isg_ctx* ctx, const isg_camera* cam, const float bg[3],
+                                    float t_min, const float* target_hwc3_dev, float weight);
+/* Sum of losses of the views since the last isg_adam_step/isg_zero_grads (syncs). */
+isg_status isg_read_loss(isg_ctx* ctx, double* loss_out);
+isg_status isg_zero_grads(isg_ctx* ctx);
+isg_status isg_get_grads(isg_ctx* ctx, float* grads_nx8);
+/* Device pointer of the n x 8 gradient buffer (flushes pending per-view work first), e.g.
+ * for an external all-reduce.  Valid until the next isg_set_scene. */
+isg_status isg_grads_device(isg_ctx* ctx, float** grads_dev);
+/* Adam (torch semantics) on (mu, log sigma, rgb, logit opacity) with per-group learning rates
+ * lr = {lr_mu, lr_sigma, lr_color, lr_opacity}; consumes and zeroes the gradients.  Updates
+ * with a non-finite gradient are skipped and counted (optimize.cpp:87-90). */
+isg_status isg_adam_step(isg_ctx* ctx, const float lr[4], float beta1, float beta2, float eps);
+
+/* ---- multi-GPU (one process per GPU, views sharded, NCCL all-reduce before Adam) -------- */
+/* NCCL is resolved at run time (dlopen libnccl.so.2, the copy torch already loaded if any). */
+isg_status isg_nccl_get_unique_id(void* out_128_bytes);
+isg_status isg_nccl_init(isg_ctx* ctx, int nranks, int rank, const void* unique_id_128_bytes);
+/* Once attached, isg_adam_step all-reduces (sum) the gradient buffer and the loss first. */
+isg_status isg_nccl_detach(isg_ctx* ctx);
+
+/* ---- parity hooks ---------------------------------------------------------------------- */
+/* After the last render/backward: sorted (tile<<32 | float_bits(depth)) keys, the splat
+ * index of each key, and per-tile [start,end) ranges (n_tiles x 2).  Any output pointer may
+ * be NULL; *n_keys always receives the key count. */
+isg_status isg_debug_bins(isg_ctx* ctx, uint64_t* keys, uint32_t* vals, int64_t* n_keys,
+                          uint32_t* ranges);
+/* Per-pixel forward state of the last render: transmittance before the last contributor
+ * and number of list entries processed (both H x W). */
+isg_status isg_debug_pixel_state(isg_ctx* ctx, float* t_last, uint32_t* n_proc);
+
+/* ---- stage timing (CUDA events on the context stream; for bench.py's roofline) ---------- */
+isg_status isg_profile_enable(isg_ctx* ctx, int on);
+int isg_profile_num_stages(void);
+const char* isg_profile_stage_name(int stage);
+/* Accumulated device milliseconds and launch counts per stage since the last read (syncs). */
+isg_status isg_profile_read(isg_ctx* ctx, double* ms_per_stage, int64_t* calls_per_stage);
+
+/* ---- synthetic workload "isg-synth v1" (host-side, no device needed) -------------------- */
+isg_status isg_synth_scene(uint64_t seed, int64_t n, int32_t width, int32_t height,
+                           float* mu_sigma, float* rgb_opacity);
+/* Camera k of an n-view batch: yaw (k-(n-1)/2)*1.5 deg about y, t = (0.05*(k-(n-1)/2),0,0);
+ * n = 1 gives the identity camera.  focal = 1000*W/1920, principal point at the centre. */
+isg_status isg_synth_camera(int32_t width, int32_t height, int32_t view, int32_t n_views,
+                            isg_camera* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ISG_H_ */

@@ -1,0 +1,205 @@
+"""ctypes loader for the CPU oracle (oracle/isg_oracle.c, oracle/_ref) — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs use
+this module, always as the checker or the timed CPU baseline, never as the product path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]  # repo root
+ORACLE_LIB = ROOT / "oracle" / "_build" / "libisg_oracle.so"
+REF_LIB = ROOT / "oracle" / "_ref" / "libisosplat_ref.so"
+
+
+class Cam32(C.Structure):
+    _fields_ = [("R", C.c_float * 9), ("t", C.c_float * 3), ("focal", C.c_float),
+                ("cx", C.c_float), ("cy", C.c_float), ("width", C.c_int32), ("height", C.c_int32)]
+
+
+class Cam64(C.Structure):
+    _fields_ = [("R", C.c_double * 9), ("t", C.c_double * 3), ("focal", C.c_double),
+                ("cx", C.c_double), ("cy", C.c_double), ("width", C.c_int32), ("height", C.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not ORACLE_LIB.exists():
+            import sys
+            sys.path.insert(0, str(ROOT))
+            from paper_2403_14244_b200 import build
+            build.build_oracle()
+        L = C.CDLL(str(ORACLE_LIB))
+        P, I64 = C.c_void_p, C.c_int64
+        L.or_version.restype = C.c_int
+        L.or64_project_iso.argtypes = [P, C.POINTER(Cam64), P]
+        L.or64_project_iso.restype = C.c_int
+        L.or64_composite.argtypes = [I64, P, P]
+        L.or64_composite.restype = C.c_int
+        L.or64_render.argtypes = [I64, P, C.POINTER(Cam64), P, C.c_int, P]
+        L.or64_render.restype = C.c_int
+        L.or64_brute_force.argtypes = [I64, P, C.POINTER(Cam64), P, P]
+        L.or64_brute_force.restype = C.c_int
+        L.or64_mse.argtypes = [I64, P, P]
+        L.or64_mse.restype = C.c_double
+        L.or64_loss_grad.argtypes = [I64, P, C.POINTER(Cam64), P, P, C.c_double, P, P]
+        L.or64_loss_grad.restype = C.c_int
+        L.or32_bin.argtypes = [I64, P, P, C.POINTER(Cam32), P, P, I64, P, C.POINTER(I64)]
+        L.or32_bin.restype = I64
+        L.or32_render.argtypes = [I64, P, P, C.POINTER(Cam32), P, C.c_float, C.c_int, P, P, P, P]
+        L.or32_render.restype = C.c_int
+        L.or32_loss_backward.argtypes = [I64, P, P, C.POINTER(Cam32), P, C.c_float, P, C.c_float,
+                                         C.c_int, C.POINTER(C.c_double), P, P]
+        L.or32_loss_backward.restype = C.c_int
+        L.or32_adam.argtypes = [I64, P, P, P, P, P, I64, P, C.c_float, C.c_float, C.c_float,
+                                C.POINTER(I64)]
+        L.or32_adam.restype = None
+        _lib = L
+    return _lib
+
+
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def cam64(camera) -> Cam64:
+    c = Cam64()
+    R = np.asarray(camera.rotation, np.float64).reshape(9)
+    for i in range(9):
+        c.R[i] = R[i]
+    for i in range(3):
+        c.t[i] = float(camera.translation[i])
+    c.focal = float(camera.focal)
+    c.cx, c.cy = map(float, camera.principal_point)
+    c.width, c.height = int(camera.width), int(camera.height)
+    return c
+
+
+def cam32(camera) -> Cam32:
+    c = Cam32()
+    R = np.asarray(camera.rotation, np.float64).reshape(9)
+    for i in range(9):
+        c.R[i] = float(np.float32(R[i]))
+    for i in range(3):
+        c.t[i] = float(np.float32(camera.translation[i]))
+    c.focal = float(np.float32(camera.focal))
+    c.cx, c.cy = (float(np.float32(v)) for v in camera.principal_point)
+    c.width, c.height = int(camera.width), int(camera.height)
+    return c
+
+
+# ---- FP64 literal -------------------------------------------------------------------------
+def project_iso64(splat8, camera):
+    s = np.ascontiguousarray(splat8, np.float64)
+    out = np.zeros(4)
+    ok = lib().or64_project_iso(_p(s), C.byref(cam64(camera)), _p(out))
+    return out if ok else None
+
+
+def composite64(rgba):
+    a = np.ascontiguousarray(rgba, np.float64).reshape(-1, 4)
+    out = np.zeros(3)
+    if lib().or64_composite(a.shape[0], _p(a), _p(out)):
+        raise ValueError("composite: alpha outside [0,1]")
+    return out
+
+
+def render64(splats, camera, bg=(0, 0, 0), threads=0):
+    s = np.ascontiguousarray(splats, np.float64).reshape(-1, 8)
+    out = np.zeros((camera.height, camera.width, 3))
+    b = np.asarray(bg, np.float64)
+    lib().or64_render(s.shape[0], _p(s), C.byref(cam64(camera)), _p(b), threads, _p(out))
+    return out
+
+
+def brute_force64(splats, camera, bg=(0, 0, 0)):
+    s = np.ascontiguousarray(splats, np.float64).reshape(-1, 8)
+    out = np.zeros((camera.height, camera.width, 3))
+    b = np.asarray(bg, np.float64)
+    lib().or64_brute_force(s.shape[0], _p(s), C.byref(cam64(camera)), _p(b), _p(out))
+    return out
+
+
+def mse64(a, b):
+    a = np.ascontiguousarray(a, np.float64).ravel()
+    b = np.ascontiguousarray(b, np.float64).ravel()
+    return lib().or64_mse(a.size, _p(a), _p(b))
+
+
+def loss_grad64(splats, camera, target, bg=(0, 0, 0), weight=1.0):
+    s = np.ascontiguousarray(splats, np.float64).reshape(-1, 8)
+    t = np.ascontiguousarray(target, np.float64)
+    b = np.asarray(bg, np.float64)
+    g = np.zeros((s.shape[0], 8))
+    loss = np.zeros(1)
+    lib().or64_loss_grad(s.shape[0], _p(s), C.byref(cam64(camera)), _p(b), _p(t), weight,
+                         _p(loss), _p(g))
+    return float(loss[0]), g
+
+
+# ---- FP32 tiled ---------------------------------------------------------------------------
+def bin32(ms, co, camera):
+    ms = np.ascontiguousarray(ms, np.float32)
+    co = np.ascontiguousarray(co, np.float32)
+    c = cam32(camera)
+    nvis = C.c_int64()
+    k = lib().or32_bin(ms.shape[0], _p(ms), _p(co), C.byref(c), None, None, 0, None,
+                       C.byref(nvis))
+    tiles = ((camera.width + 15) // 16) * ((camera.height + 15) // 16)
+    keys = np.empty(k, np.uint64)
+    vals = np.empty(k, np.uint32)
+    ranges = np.empty((tiles, 2), np.uint32)
+    lib().or32_bin(ms.shape[0], _p(ms), _p(co), C.byref(c), _p(keys), _p(vals), k, _p(ranges),
+                   C.byref(nvis))
+    return keys, vals, ranges, nvis.value
+
+
+def render32(ms, co, camera, bg=(0, 0, 0), t_min=1e-5, threads=0, want_state=False):
+    ms = np.ascontiguousarray(ms, np.float32)
+    co = np.ascontiguousarray(co, np.float32)
+    H, W = camera.height, camera.width
+    out = np.empty((H, W, 3), np.float32)
+    tl = np.empty((H, W), np.float32)
+    npr = np.empty((H, W), np.uint32)
+    counts = np.zeros(2, np.int64)
+    b = np.asarray(bg, np.float32)
+    lib().or32_render(ms.shape[0], _p(ms), _p(co), C.byref(cam32(camera)), _p(b), t_min, threads,
+                      _p(out), _p(tl), _p(npr), _p(counts))
+    if want_state:
+        return out, tl, npr, counts
+    return out
+
+
+def loss_backward32(ms, co, camera, target, bg=(0, 0, 0), t_min=1e-5, weight=1.0, threads=0,
+                    grads=None, want_image=False):
+    ms = np.ascontiguousarray(ms, np.float32)
+    co = np.ascontiguousarray(co, np.float32)
+    t = np.ascontiguousarray(target, np.float32)
+    b = np.asarray(bg, np.float32)
+    if grads is None:
+        grads = np.zeros((ms.shape[0], 8), np.float32)
+    img = np.empty((camera.height, camera.width, 3), np.float32) if want_image else None
+    loss = C.c_double()
+    lib().or32_loss_backward(ms.shape[0], _p(ms), _p(co), C.byref(cam32(camera)), _p(b), t_min,
+                             _p(t), weight, threads, C.byref(loss), _p(grads),
+                             _p(img) if img is not None else None)
+    if want_image:
+        return loss.value, grads, img
+    return loss.value, grads
+
+
+def adam32(ms, co, m, v, grads, step, lr, b1=0.9, b2=0.999, eps=1e-15):
+    """In place on ms, co, m, v (all float32, C-contiguous)."""
+    skipped = C.c_int64()
+    lrs = np.asarray(lr, np.float32)
+    g = np.ascontiguousarray(grads, np.float32)
+    lib().or32_adam(ms.shape[0], _p(ms), _p(co), _p(m), _p(v), _p(g), step, _p(lrs), b1, b2, eps,
+                    C.byref(skipped))
+    return skipped.value

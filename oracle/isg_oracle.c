@@ -1,0 +1,757 @@
+/*
+ * isg_oracle.c — CPU oracle for the isotropic-splat hot path.
+ *
+ *   *** TEST INFRASTRUCTURE ONLY. ***  Only tests/, __graft_entry__.smoke() and bench.py's
+ *   cpu_baseline / --impl reference legs may load this library, and only as the checker or
+ *   the timed CPU baseline — never as the product path.  The product (libisg.so) has no CPU
+ *   fallback and does not link this file.
+ *
+ * Two restatements of the reference algorithm live here:
+ *
+ *  (1) or64_*  — a LITERAL FP64 restatement of the reference forward path:
+ *        project_iso          /root/reference/proj/src/splat3d.cpp:59-64
+ *        Camera::to_camera / project_point  include/isosplat/splat3d.hpp:45-51
+ *        composite            src/splat3d.cpp:76-87
+ *        covers(ScreenIso)    src/splat3d.cpp:108-114
+ *        composite_pixels     src/splat3d.cpp:125-162 (row bands, no early exit)
+ *        sort_by_depth        src/splat3d.cpp:164-169 (stable, ties by index)
+ *        render(iso)          src/splat3d.cpp:173-194
+ *        brute_force_render   tools/isosplat_main.cpp:309-355
+ *        mse                  src/image.cpp:50-58
+ *      plus a first-principles FP64 backward (kernel closed forms
+ *      include/isosplat/kernels.hpp:208-222, Jacobian src/splat3d.cpp:39-47) that is pinned
+ *      by central finite differences of the FP64 forward in tests/.
+ *
+ *  (2) or32_*  — the FP32 TILED restatement that the GPU path must match: the same
+ *      arithmetic in IEEE single precision with every rounding spelled out (this file is
+ *      compiled with -ffp-contract=off, as the reference is: proj/CMakeLists.txt:11-17),
+ *      16x16 screen tiles, (tile, depth, index) ordered per-tile lists, optional early
+ *      termination at transmittance t_min, the reverse-walk backward and Adam.  Tile keys,
+ *      their order and the per-tile ranges produced here are the bit-exact parity target.
+ *
+ * Parity status: the forward is pinned against the reference's own known answers
+ * and, when oracle/_ref is built, against the
+ * reference's compiled render(); tiles/keys/ranges, backward and Adam have no reference
+ * counterpart (SPEC.md:484 non-goals) and are pinned by construction, by finite
+ * differences and by torch.optim.Adam respectively.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define OR_TILE 16
+
+/* Same layout as isg_camera in include/isg.h. */
+typedef struct {
+  float R[9];
+  float t[3];
+  float focal;
+  float cx, cy;
+  int32_t width, height;
+} or_cam32;
+
+typedef struct {
+  double R[9];
+  double t[3];
+  double focal;
+  double cx, cy;
+  int32_t width, height;
+} or_cam64;
+
+int or_version(void) { return 1; }
+
+static int resolve_threads(int threads) {
+#ifdef _OPENMP
+  return threads > 0 ? threads : omp_get_max_threads();
+#else
+  (void)threads;
+  return 1;
+#endif
+}
+
+/* ========================================================================================
+ * (1) FP64 literal restatement
+ * ====================================================================================== */
+
+/* splat record: mu.xyz sigma color.rgb opacity (the ISPL iso-3D record order,
+ * include/isosplat/particle_io.hpp:36-46). */
+
+/* project_iso, src/splat3d.cpp:59-64.  Returns 1 and (u, v, sigma2d, depth) when z > near. */
+int or64_project_iso(const double* s, const or_cam64* c, double* out) {
+  /* to_camera: rotation * world + translation (hpp:45-47) */
+  const double x = (c->R[0] * s[0] + c->R[1] * s[1]) + c->R[2] * s[2] + c->t[0];
+  const double y = (c->R[3] * s[0] + c->R[4] * s[1]) + c->R[5] * s[2] + c->t[1];
+  const double z = (c->R[6] * s[0] + c->R[7] * s[1]) + c->R[8] * s[2] + c->t[2];
+  if (!(z > 1e-3)) return 0; /* kNearPlane, hpp:55 */
+  out[0] = c->focal * x / z + c->cx; /* project_point hpp:48-51 */
+  out[1] = c->focal * y / z + c->cy;
+  out[2] = s[3] * c->focal / z; /* sigma_2d = sigma * f / z */
+  out[3] = z;
+  return 1;
+}
+
+/* composite, src/splat3d.cpp:76-87.  rgba: n x 4 (r, g, b, alpha).  Returns 1 on the
+ * reference's domain error (alpha outside [0,1]). */
+int or64_composite(int64_t n, const double* rgba, double* out) {
+  double c0 = 0, c1 = 0, c2 = 0, T = 1.0;
+  for (int64_t k = 0; k < n; ++k) {
+    const double a = rgba[4 * k + 3];
+    if (!(a >= 0.0 && a <= 1.0)) return 1;
+    const double w = T * a;
+    c0 += w * rgba[4 * k + 0];
+    c1 += w * rgba[4 * k + 1];
+    c2 += w * rgba[4 * k + 2];
+    T *= 1.0 - a;
+  }
+  out[0] = c0;
+  out[1] = c1;
+  out[2] = c2;
+  return 0;
+}
+
+typedef struct {
+  double depth;
+  int64_t index;
+} or_entry64;
+
+static int cmp_entry64(const void* a, const void* b) {
+  const or_entry64* x = (const or_entry64*)a;
+  const or_entry64* y = (const or_entry64*)b;
+  if (x->depth < y->depth) return -1;
+  if (x->depth > y->depth) return 1;
+  /* std::stable_sort keeps input order for equal depth (splat3d.cpp:164-169) */
+  return (x->index > y->index) - (x->index < y->index);
+}
+
+typedef struct {
+  double u, v, s2, r2max, c[3], o;
+} or_screen64;
+
+/* render(iso), src/splat3d.cpp:173-194 with composite_pixels :125-162.  The caller has
+ * validated the splats and camera (splat3d.cpp:10-37).  out: H x W x 3. */
+int or64_render(int64_t n, const double* splats, const or_cam64* cam, const double* bg,
+                int threads, double* out) {
+  or_entry64* ord = (or_entry64*)malloc(sizeof(or_entry64) * (size_t)(n > 0 ? n : 1));
+  or_screen64* scr = (or_screen64*)malloc(sizeof(or_screen64) * (size_t)(n > 0 ? n : 1));
+  int64_t m = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    double p[4];
+    if (!or64_project_iso(splats + 8 * i, cam, p)) continue; /* culled */
+    ord[m].depth = p[3];
+    ord[m].index = i;
+    ++m;
+  }
+  qsort(ord, (size_t)m, sizeof(or_entry64), cmp_entry64);
+  for (int64_t k = 0; k < m; ++k) {
+    const double* s = splats + 8 * ord[k].index;
+    double p[4];
+    or64_project_iso(s, cam, p);
+    scr[k].u = p[0];
+    scr[k].v = p[1];
+    scr[k].s2 = p[2] * p[2];
+    scr[k].r2max = 9.0 * p[2] * p[2];
+    scr[k].c[0] = s[4];
+    scr[k].c[1] = s[5];
+    scr[k].c[2] = s[6];
+    scr[k].o = s[7];
+  }
+  const int W = cam->width, H = cam->height;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(resolve_threads(threads))
+  for (int y = 0; y < H; ++y) {
+    const double py = y + 0.5; /* pixel_center, image.hpp:33-34 */
+    for (int x = 0; x < W; ++x) {
+      const double px = x + 0.5;
+      double c0 = 0, c1 = 0, c2 = 0, T = 1.0;
+      for (int64_t k = 0; k < m; ++k) {
+        const or_screen64* s = &scr[k];
+        const double dx = px - s->u, dy = py - s->v;
+        const double r2 = dx * dx + dy * dy;
+        if (r2 > s->r2max) continue;
+        const double g = exp(-r2 / s->s2);
+        const double a = s->o * g;
+        const double w = T * a;
+        c0 += w * s->c[0];
+        c1 += w * s->c[1];
+        c2 += w * s->c[2];
+        T *= 1.0 - a;
+      }
+      double* o = out + ((size_t)y * W + x) * 3;
+      o[0] = c0 + T * bg[0];
+      o[1] = c1 + T * bg[1];
+      o[2] = c2 + T * bg[2];
+    }
+  }
+  free(ord);
+  free(scr);
+  return 0;
+}
+
+/* brute_force_render, tools/isosplat_main.cpp:309-355: re-projects every splat per pixel. */
+int or64_brute_force(int64_t n, const double* splats, const or_cam64* cam, const double* bg,
+                     double* out) {
+  or_entry64* ord = (or_entry64*)malloc(sizeof(or_entry64) * (size_t)(n > 0 ? n : 1));
+  int64_t m = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const double* s = splats + 8 * i;
+    const double z = (cam->R[6] * s[0] + cam->R[7] * s[1]) + cam->R[8] * s[2] + cam->t[2];
+    if (z > 1e-3) {
+      ord[m].depth = z;
+      ord[m].index = i;
+      ++m;
+    }
+  }
+  qsort(ord, (size_t)m, sizeof(or_entry64), cmp_entry64);
+  for (int y = 0; y < cam->height; ++y) {
+    for (int x = 0; x < cam->width; ++x) {
+      const double px = x + 0.5, py = y + 0.5;
+      double c0 = 0, c1 = 0, c2 = 0, T = 1.0;
+      for (int64_t k = 0; k < m; ++k) {
+        const double* s = splats + 8 * ord[k].index;
+        double p[4];
+        or64_project_iso(s, cam, p);
+        const double dx = px - p[0], dy = py - p[1];
+        const double r2 = dx * dx + dy * dy;
+        if (!(r2 <= 9.0 * p[2] * p[2])) continue;
+        const double g = exp(-r2 / (p[2] * p[2]));
+        const double a = s[7] * g;
+        const double w = T * a;
+        c0 += w * s[4];
+        c1 += w * s[5];
+        c2 += w * s[6];
+        T *= 1.0 - a;
+      }
+      double* o = out + ((size_t)y * cam->width + x) * 3;
+      o[0] = c0 + T * bg[0];
+      o[1] = c1 + T * bg[1];
+      o[2] = c2 + T * bg[2];
+    }
+  }
+  free(ord);
+  return 0;
+}
+
+/* mse, src/image.cpp:50-58 */
+double or64_mse(int64_t count, const double* a, const double* b) {
+  double acc = 0.0;
+  for (int64_t i = 0; i < count; ++i) {
+    const double d = a[i] - b[i];
+    acc += d * d;
+  }
+  return acc / (double)count;
+}
+
+/* FP64 loss = weight * mse(render, target) and its gradient w.r.t. every splat parameter
+ * (n x 8: dmu.xyz dsigma drgb dopacity), with no early termination (exact reference
+ * forward).  First-principles chain rule; the per-pixel transmittance
+ * is stored during the forward walk, so no division is involved (an independent check of
+ * the division-based reverse walk used on FP32/GPU). */
+int or64_loss_grad(int64_t n, const double* splats, const or_cam64* cam, const double* bg,
+                   const double* target, double weight, double* loss_out, double* grads) {
+  const int W = cam->width, H = cam->height;
+  or_entry64* ord = (or_entry64*)malloc(sizeof(or_entry64) * (size_t)(n > 0 ? n : 1));
+  double* proj = (double*)malloc(sizeof(double) * 4 * (size_t)(n > 0 ? n : 1));
+  double* d2 = (double*)calloc((size_t)(n > 0 ? n : 1) * 4, sizeof(double)); /* du dv ds do */
+  int64_t m = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (!or64_project_iso(splats + 8 * i, cam, proj + 4 * i)) continue;
+    ord[m].depth = proj[4 * i + 3];
+    ord[m].index = i;
+    ++m;
+  }
+  qsort(ord, (size_t)m, sizeof(or_entry64), cmp_entry64);
+  memset(grads, 0, sizeof(double) * 8 * (size_t)n);
+  int64_t* list = (int64_t*)malloc(sizeof(int64_t) * (size_t)(m > 0 ? m : 1));
+  double* Tk = (double*)malloc(sizeof(double) * (size_t)(m > 0 ? m : 1));
+  double* gk = (double*)malloc(sizeof(double) * (size_t)(m > 0 ? m : 1));
+  const double scale = weight / (3.0 * W * H);
+  double loss = 0.0;
+  for (int y = 0; y < H; ++y) {
+    for (int x = 0; x < W; ++x) {
+      const double px = x + 0.5, py = y + 0.5;
+      int64_t L = 0;
+      double C[3] = {0, 0, 0}, T = 1.0;
+      for (int64_t k = 0; k < m; ++k) {
+        const int64_t i = ord[k].index;
+        const double* p = proj + 4 * i;
+        const double dx = px - p[0], dy = py - p[1];
+        const double r2 = dx * dx + dy * dy;
+        if (r2 > 9.0 * p[2] * p[2]) continue;
+        const double g = exp(-r2 / (p[2] * p[2]));
+        const double a = splats[8 * i + 7] * g;
+        list[L] = i;
+        Tk[L] = T;
+        gk[L] = g;
+        ++L;
+        for (int c = 0; c < 3; ++c) C[c] += T * a * splats[8 * i + 4 + c];
+        T *= 1.0 - a;
+      }
+      double G[3];
+      const double* tg = target + ((size_t)y * W + x) * 3;
+      for (int c = 0; c < 3; ++c) {
+        C[c] += T * bg[c];
+        const double d = C[c] - tg[c];
+        loss += d * d;
+        G[c] = 2.0 * d * scale;
+      }
+      double A[3] = {bg[0], bg[1], bg[2]};
+      for (int64_t l = L - 1; l >= 0; --l) {
+        const int64_t i = list[l];
+        const double* s = splats + 8 * i;
+        const double* p = proj + 4 * i;
+        const double g = gk[l], o = s[7], a = o * g, Tl = Tk[l];
+        double dLda = 0.0;
+        for (int c = 0; c < 3; ++c) {
+          dLda += G[c] * Tl * (s[4 + c] - A[c]);
+          grads[8 * i + 4 + c] += G[c] * Tl * a; /* dC/dc = T a */
+        }
+        for (int c = 0; c < 3; ++c) A[c] = a * s[4 + c] + (1.0 - a) * A[c];
+        grads[8 * i + 7] += dLda * g; /* d alpha / d opacity = g */
+        const double dLdg = dLda * o;
+        const double dx = px - p[0], dy = py - p[1], s2 = p[2] * p[2];
+        d2[4 * i + 0] += dLdg * g * 2.0 * dx / s2; /* kernels.hpp:219 */
+        d2[4 * i + 1] += dLdg * g * 2.0 * dy / s2;
+        d2[4 * i + 2] += dLdg * g * 2.0 * (dx * dx + dy * dy) / (s2 * p[2]); /* kernels.hpp:220 */
+      }
+    }
+  }
+  /* projection backward: u = f x/z + cx, v = f y/z + cy, s = sigma f / z  (splat3d.cpp:39-47) */
+  for (int64_t i = 0; i < n; ++i) {
+    const double* s = splats + 8 * i;
+    const double x = (cam->R[0] * s[0] + cam->R[1] * s[1]) + cam->R[2] * s[2] + cam->t[0];
+    const double yv = (cam->R[3] * s[0] + cam->R[4] * s[1]) + cam->R[5] * s[2] + cam->t[1];
+    const double z = (cam->R[6] * s[0] + cam->R[7] * s[1]) + cam->R[8] * s[2] + cam->t[2];
+    if (!(z > 1e-3)) continue;
+    const double f = cam->focal, du = d2[4 * i], dv = d2[4 * i + 1], ds = d2[4 * i + 2];
+    const double gx = du * f / z, gy = dv * f / z;
+    const double gz = -(du * f * x + dv * f * yv + ds * s[3] * f) / (z * z);
+    grads[8 * i + 0] = cam->R[0] * gx + cam->R[3] * gy + cam->R[6] * gz;
+    grads[8 * i + 1] = cam->R[1] * gx + cam->R[4] * gy + cam->R[7] * gz;
+    grads[8 * i + 2] = cam->R[2] * gx + cam->R[5] * gy + cam->R[8] * gz;
+    grads[8 * i + 3] = ds * f / z;
+  }
+  *loss_out = loss * (weight / (3.0 * W * H));
+  free(ord);
+  free(proj);
+  free(d2);
+  free(list);
+  free(Tk);
+  free(gk);
+  return 0;
+}
+
+/* ========================================================================================
+ * (2) FP32 tiled restatement (the GPU parity target)
+ * ====================================================================================== */
+
+typedef struct {
+  float u, v, s, s2, r2max, c[3], o;
+  float xc, yc, zc;
+  int vis;
+} or_rec32;
+
+/* Projection in FP32 with every rounding explicit (-ffp-contract=off).  The CUDA kernel
+ * performs the identical sequence with __fmul_rn/__fadd_rn/__fdiv_rn. */
+static void or32_project(const float* ms, const float* co, const or_cam32* c, or_rec32* r) {
+  const float mx = ms[0], my = ms[1], mz = ms[2], sg = ms[3];
+  float xc = c->R[0] * mx;
+  xc = xc + c->R[1] * my;
+  xc = xc + c->R[2] * mz;
+  xc = xc + c->t[0];
+  float yc = c->R[3] * mx;
+  yc = yc + c->R[4] * my;
+  yc = yc + c->R[5] * mz;
+  yc = yc + c->t[1];
+  float zc = c->R[6] * mx;
+  zc = zc + c->R[7] * my;
+  zc = zc + c->R[8] * mz;
+  zc = zc + c->t[2];
+  r->xc = xc;
+  r->yc = yc;
+  r->zc = zc;
+  r->vis = zc > 1e-3f; /* kNearPlane */
+  const float fx = c->focal * xc, fy = c->focal * yc, fs = sg * c->focal;
+  r->u = fx / zc + c->cx;
+  r->v = fy / zc + c->cy;
+  r->s = fs / zc;
+  r->s2 = r->s * r->s;
+  r->r2max = (9.0f * r->s) * r->s;
+  r->c[0] = co[0];
+  r->c[1] = co[1];
+  r->c[2] = co[2];
+  r->o = co[3];
+}
+
+/* Exact tile test: the pixel-centre rectangle of tile (tx,ty), clipped to the image, is
+ * within the 3-sigma circle.  Conservative w.r.t. the per-pixel test (rounding is
+ * monotone), so a tile that fails contains no covered pixel. */
+static int or32_tile_hit(const or_rec32* r, int tx, int ty, int W, int H) {
+  const float x0 = (float)(tx * OR_TILE) + 0.5f;
+  const float x1 = (float)((tx * OR_TILE + OR_TILE < W ? tx * OR_TILE + OR_TILE : W) - 1) + 0.5f;
+  const float y0 = (float)(ty * OR_TILE) + 0.5f;
+  const float y1 = (float)((ty * OR_TILE + OR_TILE < H ? ty * OR_TILE + OR_TILE : H) - 1) + 0.5f;
+  const float qx = r->u < x0 ? x0 : (r->u > x1 ? x1 : r->u);
+  const float qy = r->v < y0 ? y0 : (r->v > y1 ? y1 : r->v);
+  const float dx = qx - r->u, dy = qy - r->v;
+  const float ddx = dx * dx, ddy = dy * dy;
+  const float d2 = ddx + ddy;
+  return !(d2 > r->r2max);
+}
+
+/* Conservative tile bounding box [tx0,tx1]x[ty0,ty1]; returns 0 if empty. */
+static int or32_tile_bbox(const or_rec32* r, int tiles_x, int tiles_y, int* b) {
+  const float ext = 3.0f * r->s * 1.0009765625f + 1.0f;
+  float fx0 = floorf((r->u - ext) * (1.0f / OR_TILE));
+  float fx1 = floorf((r->u + ext) * (1.0f / OR_TILE));
+  float fy0 = floorf((r->v - ext) * (1.0f / OR_TILE));
+  float fy1 = floorf((r->v + ext) * (1.0f / OR_TILE));
+  fx0 = fmaxf(fx0, 0.0f);
+  fy0 = fmaxf(fy0, 0.0f);
+  fx1 = fminf(fx1, (float)(tiles_x - 1));
+  fy1 = fminf(fy1, (float)(tiles_y - 1));
+  if (!(fx0 <= fx1) || !(fy0 <= fy1)) return 0;
+  b[0] = (int)fx0;
+  b[1] = (int)fx1;
+  b[2] = (int)fy0;
+  b[3] = (int)fy1;
+  return 1;
+}
+
+static uint32_t f32_bits(float f) {
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  return u;
+}
+
+typedef struct {
+  uint32_t z;
+  uint32_t idx;
+} or_zkey;
+
+static int cmp_zkey(const void* a, const void* b) {
+  const or_zkey* x = (const or_zkey*)a;
+  const or_zkey* y = (const or_zkey*)b;
+  if (x->z != y->z) return x->z < y->z ? -1 : 1;
+  return (x->idx > y->idx) - (x->idx < y->idx);
+}
+
+typedef struct {
+  int W, H, tx, ty, ntiles;
+  int64_t n, nkeys, nvis;
+  or_rec32* rec;
+  uint32_t* vals;   /* nkeys splat indices, tile-major, depth order within a tile */
+  uint32_t* ranges; /* ntiles x 2 */
+} or_frame32;
+
+static void or32_frame_free(or_frame32* f) {
+  free(f->rec);
+  free(f->vals);
+  free(f->ranges);
+}
+
+/* Preprocess + binning: projection, tile sets, stable (tile, depth, index) order.  The
+ * ordering is produced by a stable depth sort followed by a stable counting sort on the tile
+ * — an algorithm independent of the GPU's radix sorts. */
+static void or32_frame_build(int64_t n, const float* mu_sigma, const float* rgb_o,
+                             const or_cam32* cam, or_frame32* f) {
+  f->W = cam->width;
+  f->H = cam->height;
+  f->tx = (f->W + OR_TILE - 1) / OR_TILE;
+  f->ty = (f->H + OR_TILE - 1) / OR_TILE;
+  f->ntiles = f->tx * f->ty;
+  f->n = n;
+  f->rec = (or_rec32*)malloc(sizeof(or_rec32) * (size_t)(n > 0 ? n : 1));
+  or_zkey* zk = (or_zkey*)malloc(sizeof(or_zkey) * (size_t)(n > 0 ? n : 1));
+  int64_t m = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    or32_project(mu_sigma + 4 * i, rgb_o + 4 * i, cam, &f->rec[i]);
+    if (!f->rec[i].vis) continue;
+    zk[m].z = f32_bits(f->rec[i].zc);
+    zk[m].idx = (uint32_t)i;
+    ++m;
+  }
+  qsort(zk, (size_t)m, sizeof(or_zkey), cmp_zkey);
+  uint32_t* cnt = (uint32_t*)calloc((size_t)f->ntiles + 1, sizeof(uint32_t));
+  int64_t total = 0, nvis = 0;
+  for (int pass = 0; pass < 2; ++pass) {
+    uint32_t* cursor = NULL;
+    if (pass == 1) {
+      f->vals = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)(total > 0 ? total : 1));
+      f->ranges = (uint32_t*)malloc(sizeof(uint32_t) * 2 * (size_t)f->ntiles);
+      cursor = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)f->ntiles);
+      uint32_t acc = 0;
+      for (int t = 0; t < f->ntiles; ++t) {
+        f->ranges[2 * t] = acc;
+        cursor[t] = acc;
+        acc += cnt[t];
+        f->ranges[2 * t + 1] = acc;
+      }
+    }
+    for (int64_t k = 0; k < m; ++k) {
+      const or_rec32* r = &f->rec[zk[k].idx];
+      int b[4];
+      if (!or32_tile_bbox(r, f->tx, f->ty, b)) continue;
+      int hit = 0;
+      for (int ty = b[2]; ty <= b[3]; ++ty)
+        for (int tx = b[0]; tx <= b[1]; ++tx) {
+          if (!or32_tile_hit(r, tx, ty, f->W, f->H)) continue;
+          const int t = ty * f->tx + tx;
+          hit = 1;
+          if (pass == 0) {
+            cnt[t]++;
+            total++;
+          } else {
+            f->vals[cursor[t]++] = zk[k].idx;
+          }
+        }
+      if (pass == 0 && hit) nvis++;
+    }
+    free(cursor);
+  }
+  f->nkeys = total;
+  f->nvis = nvis;
+  free(cnt);
+  free(zk);
+}
+
+/* Binning output for the parity hook: keys (tile<<32 | float_bits(depth)) in sorted order,
+ * splat index per key, per-tile [start,end).  Returns the key count; arrays are written only
+ * when the count fits in cap (callers re-query with a larger buffer). */
+int64_t or32_bin(int64_t n, const float* mu_sigma, const float* rgb_o, const or_cam32* cam,
+                 uint64_t* keys, uint32_t* vals, int64_t cap, uint32_t* ranges,
+                 int64_t* n_visible) {
+  or_frame32 f;
+  or32_frame_build(n, mu_sigma, rgb_o, cam, &f);
+  if (n_visible) *n_visible = f.nvis;
+  if (f.nkeys <= cap) {
+    for (int t = 0; t < f.ntiles; ++t)
+      for (uint32_t p = f.ranges[2 * t]; p < f.ranges[2 * t + 1]; ++p) {
+        if (keys) keys[p] = ((uint64_t)t << 32) | f32_bits(f.rec[f.vals[p]].zc);
+        if (vals) vals[p] = f.vals[p];
+      }
+    if (ranges) memcpy(ranges, f.ranges, sizeof(uint32_t) * 2 * (size_t)f.ntiles);
+  }
+  const int64_t k = f.nkeys;
+  or32_frame_free(&f);
+  return k;
+}
+
+/* Front-to-back blend of one pixel over its tile list (composite_pixels semantics,
+ * splat3d.cpp:136-143) with early termination once T <= t_min.  Returns entries processed. */
+static uint32_t or32_blend_pixel(const or_frame32* f, uint32_t beg, uint32_t end, float px,
+                                 float py, const float* bg, float t_min, float* out,
+                                 float* t_last, int64_t* evaluated, int64_t* inside) {
+  float C0 = 0.f, C1 = 0.f, C2 = 0.f, T = 1.f, Tl = 1.f;
+  uint32_t nproc = 0;
+  int64_t ev = 0, in = 0;
+  for (uint32_t p = beg; p < end; ++p) {
+    const or_rec32* r = &f->rec[f->vals[p]];
+    ++ev;
+    const float dx = px - r->u, dy = py - r->v;
+    const float ddx = dx * dx, ddy = dy * dy;
+    const float r2 = ddx + ddy;
+    if (r2 > r->r2max) continue;
+    ++in;
+    const float g = expf(-r2 / r->s2);
+    const float a = r->o * g;
+    const float w = T * a;
+    C0 += w * r->c[0];
+    C1 += w * r->c[1];
+    C2 += w * r->c[2];
+    Tl = T;
+    T = T * (1.0f - a);
+    nproc = p - beg + 1;
+    if (!(T > t_min)) break;
+  }
+  out[0] = C0 + T * bg[0];
+  out[1] = C1 + T * bg[1];
+  out[2] = C2 + T * bg[2];
+  *t_last = Tl;
+  if (evaluated) *evaluated += ev;
+  if (inside) *inside += in;
+  return nproc;
+}
+
+/* FP32 tiled render.  out: H x W x 3; t_last / n_proc (H x W, may be NULL) receive the
+ * per-pixel transmittance before the last processed entry and the number of list entries
+ * processed; counts (may be NULL) = {pairs evaluated, pairs inside the 3-sigma circle}. */
+int or32_render(int64_t n, const float* mu_sigma, const float* rgb_o, const or_cam32* cam,
+                const float* bg, float t_min, int threads, float* out, float* t_last,
+                uint32_t* n_proc, int64_t* counts) {
+  or_frame32 f;
+  or32_frame_build(n, mu_sigma, rgb_o, cam, &f);
+  int64_t ev = 0, in = 0;
+#pragma omp parallel for schedule(dynamic, 4) num_threads(resolve_threads(threads)) \
+    reduction(+ : ev, in)
+  for (int t = 0; t < f.ntiles; ++t) {
+    const int tx = t % f.tx, ty = t / f.tx;
+    for (int y = ty * OR_TILE; y < ty * OR_TILE + OR_TILE && y < f.H; ++y)
+      for (int x = tx * OR_TILE; x < tx * OR_TILE + OR_TILE && x < f.W; ++x) {
+        const size_t pix = (size_t)y * f.W + x;
+        float tl;
+        const uint32_t np = or32_blend_pixel(&f, f.ranges[2 * t], f.ranges[2 * t + 1],
+                                             (float)x + 0.5f, (float)y + 0.5f, bg, t_min,
+                                             out + 3 * pix, &tl, &ev, &in);
+        if (t_last) t_last[pix] = tl;
+        if (n_proc) n_proc[pix] = np;
+      }
+  }
+  if (counts) {
+    counts[0] = ev;
+    counts[1] = in;
+  }
+  or32_frame_free(&f);
+  return 0;
+}
+
+/* FP32 tiled forward + L2 loss (weight * mse) + backward.  Gradients (n x 8, dmu.xyz dsigma
+ * drgb dopacity) are ACCUMULATED into grads.  Per-(tile, entry) partial sums are reduced per
+ * splat in key order, so the result is independent of the thread count.  out_img (may be
+ * NULL) receives the forward image. */
+int or32_loss_backward(int64_t n, const float* mu_sigma, const float* rgb_o, const or_cam32* cam,
+                       const float* bg, float t_min, const float* target, float weight,
+                       int threads, double* loss_out, float* grads, float* out_img) {
+  or_frame32 f;
+  or32_frame_build(n, mu_sigma, rgb_o, cam, &f);
+  float* part = (float*)calloc((size_t)(f.nkeys > 0 ? f.nkeys : 1) * 7, sizeof(float));
+  double* tile_loss = (double*)calloc((size_t)f.ntiles, sizeof(double));
+  const float scale = weight / (3.0f * (float)f.W * (float)f.H);
+#pragma omp parallel for schedule(dynamic, 4) num_threads(resolve_threads(threads))
+  for (int t = 0; t < f.ntiles; ++t) {
+    const int tx = t % f.tx, ty = t / f.tx;
+    const uint32_t beg = f.ranges[2 * t], end = f.ranges[2 * t + 1];
+    double tl_acc = 0.0;
+    for (int y = ty * OR_TILE; y < ty * OR_TILE + OR_TILE && y < f.H; ++y)
+      for (int x = tx * OR_TILE; x < tx * OR_TILE + OR_TILE && x < f.W; ++x) {
+        const size_t pix = (size_t)y * f.W + x;
+        const float px = (float)x + 0.5f, py = (float)y + 0.5f;
+        float C[3], Tl;
+        const uint32_t np = or32_blend_pixel(&f, beg, end, px, py, bg, t_min, C, &Tl, NULL, NULL);
+        if (out_img) memcpy(out_img + 3 * pix, C, sizeof C);
+        float G[3];
+        for (int c = 0; c < 3; ++c) {
+          const float d = C[c] - target[3 * pix + c];
+          tl_acc += (double)d * (double)d;
+          G[c] = 2.0f * d * scale;
+        }
+        float A0 = bg[0], A1 = bg[1], A2 = bg[2], Tc = Tl;
+        int first = 1;
+        for (uint32_t q = np; q-- > 0;) {
+          const uint32_t p = beg + q;
+          const or_rec32* r = &f.rec[f.vals[p]];
+          const float dx = px - r->u, dy = py - r->v;
+          const float ddx = dx * dx, ddy = dy * dy;
+          const float r2 = ddx + ddy;
+          if (r2 > r->r2max) continue;
+          const float g = expf(-r2 / r->s2);
+          const float a = r->o * g;
+          float T;
+          if (first) {
+            T = Tc;
+            first = 0;
+          } else {
+            T = Tc / (1.0f - a);
+          }
+          Tc = T;
+          const float dLda = T * ((G[0] * (r->c[0] - A0) + G[1] * (r->c[1] - A1)) +
+                                  G[2] * (r->c[2] - A2));
+          const float Ta = T * a;
+          float* pp = part + 7 * (size_t)p;
+          pp[4] += G[0] * Ta;
+          pp[5] += G[1] * Ta;
+          pp[6] += G[2] * Ta;
+          A0 = a * r->c[0] + (1.0f - a) * A0;
+          A1 = a * r->c[1] + (1.0f - a) * A1;
+          A2 = a * r->c[2] + (1.0f - a) * A2;
+          pp[3] += dLda * g;
+          const float k2 = (dLda * r->o) * g * 2.0f / r->s2;
+          pp[0] += k2 * dx;
+          pp[1] += k2 * dy;
+          pp[2] += k2 * r2 / r->s;
+        }
+      }
+    tile_loss[t] = tl_acc;
+  }
+  /* per-splat reduction of the 2D partials, in key order */
+  float* d2 = (float*)calloc((size_t)(n > 0 ? n : 1) * 7, sizeof(float));
+  for (int64_t p = 0; p < f.nkeys; ++p) {
+    float* dst = d2 + 7 * (size_t)f.vals[p];
+    const float* src = part + 7 * (size_t)p;
+    for (int j = 0; j < 7; ++j) dst[j] += src[j];
+  }
+  /* projection backward (splat3d.cpp:39-47 Jacobian) */
+  for (int64_t i = 0; i < n; ++i) {
+    const or_rec32* r = &f.rec[i];
+    if (!r->vis) continue;
+    const float* s = d2 + 7 * (size_t)i;
+    const float fz = cam->focal / r->zc;
+    const float gx = s[0] * fz, gy = s[1] * fz;
+    const float gz = -(((s[0] * r->xc + s[1] * r->yc) + s[2] * mu_sigma[4 * i + 3]) * fz) / r->zc;
+    float* gd = grads + 8 * (size_t)i;
+    gd[0] += (cam->R[0] * gx + cam->R[3] * gy) + cam->R[6] * gz;
+    gd[1] += (cam->R[1] * gx + cam->R[4] * gy) + cam->R[7] * gz;
+    gd[2] += (cam->R[2] * gx + cam->R[5] * gy) + cam->R[8] * gz;
+    gd[3] += s[2] * fz;
+    gd[4] += s[4];
+    gd[5] += s[5];
+    gd[6] += s[6];
+    gd[7] += s[3];
+  }
+  double loss = 0.0;
+  for (int t = 0; t < f.ntiles; ++t) loss += tile_loss[t];
+  *loss_out = loss * ((double)weight / (3.0 * f.W * f.H));
+  free(d2);
+  free(part);
+  free(tile_loss);
+  or32_frame_free(&f);
+  return 0;
+}
+
+/* Adam (torch.optim.Adam semantics, no weight decay) on the optimizer-space parameters
+ * (mu, log sigma, rgb, logit opacity) with per-group learning rates lr[4].  sigma moves in
+ * log space as in update_step (optimize.cpp:93,105); a Gaussian whose 8 gradients are not
+ * all finite is skipped and counted (optimize.cpp:87-90).  m, v: n x 8; step >= 1. */
+void or32_adam(int64_t n, float* mu_sigma, float* rgb_o, float* m, float* v, const float* grads,
+               int64_t step, const float* lr, float b1, float b2, float eps, int64_t* skipped) {
+  const double bc1 = 1.0 - pow((double)b1, (double)step);
+  const double bc2 = 1.0 - pow((double)b2, (double)step);
+  const float bc2_sqrt = (float)sqrt(bc2);
+  float step_size[4];
+  for (int j = 0; j < 4; ++j) step_size[j] = (float)((double)lr[j] / bc1);
+  static const int group[8] = {0, 0, 0, 1, 2, 2, 2, 3};
+  int64_t skip = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const float* gr = grads + 8 * (size_t)i;
+    int ok = 1;
+    for (int j = 0; j < 8; ++j) ok &= isfinite(gr[j]) ? 1 : 0;
+    if (!ok) {
+      ++skip;
+      continue;
+    }
+    float* ms = mu_sigma + 4 * (size_t)i;
+    float* co = rgb_o + 4 * (size_t)i;
+    const float sigma = ms[3], op = co[3];
+    float p[8] = {ms[0], ms[1], ms[2], logf(sigma), co[0], co[1], co[2], logf(op) - log1pf(-op)};
+    float g[8] = {gr[0], gr[1], gr[2], gr[3] * sigma, gr[4], gr[5], gr[6], gr[7] * op * (1.0f - op)};
+    for (int j = 0; j < 8; ++j) {
+      float* mm = m + 8 * (size_t)i + j;
+      float* vv = v + 8 * (size_t)i + j;
+      *mm = *mm + (1.0f - b1) * (g[j] - *mm);
+      *vv = b2 * *vv + (1.0f - b2) * g[j] * g[j];
+      const float denom = sqrtf(*vv) / bc2_sqrt + eps;
+      p[j] = p[j] - step_size[group[j]] * (*mm / denom);
+    }
+    ms[0] = p[0];
+    ms[1] = p[1];
+    ms[2] = p[2];
+    ms[3] = expf(p[3]);
+    co[0] = p[4];
+    co[1] = p[5];
+    co[2] = p[6];
+    co[3] = 1.0f / (1.0f + expf(-p[7]));
+  }
+  if (skipped) *skipped += skip;
+}

@@ -1,0 +1,970 @@
+// capi.cu — the C-ABI (include/isg.h): context, device buffers, frame orchestration.
+//
+// A context owns one stream and every device buffer; a frame is launched entirely
+// asynchronously (K1 -> depth sort -> scan/emit -> tile sort -> ranges -> blend), the key
+// count never travels to the host inside a frame: kernels read it from device memory and the
+// blend kernels skip the frame if the preallocated key capacity overflowed.  Host-synchronous
+// entry points (isg_render, isg_loss_backward, isg_read_loss, isg_synchronize) check the
+// overflow and validation flags, grow the capacity and re-run the frame when needed.
+//
+// Errors mirror the reference: invalid splats/cameras -> ISG_E_DOMAIN with the message the
+// reference's std::domain_error carries (src/splat3d.cpp:10-37); bad arguments ->
+// ISG_E_ARG (std::invalid_argument, include/isosplat/particles.hpp:73-83).
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "isg_internal.cuh"
+
+// Stage timing (isg_profile_*): CUDA events around each kernel of a frame, on the launching
+// stream, so bench.py can report the dominant kernel's live launch duration.
+enum Stage {
+  ST_MEMSET, ST_PREPROCESS, ST_DEPTH_SORT, ST_SCAN_EMIT, ST_TILE_SORT, ST_RANGES, ST_BLEND_FWD,
+  ST_BLEND_BWD, ST_LOSS_REDUCE, ST_PROJECT_BWD, ST_PROJECT_ADAM, ST_ADAM, ST_ALLREDUCE, ST_COUNT
+};
+static const char* kStageNames[ST_COUNT] = {
+    "memset", "preprocess", "depth_sort", "scan_emit", "tile_sort", "ranges", "blend_fwd",
+    "blend_bwd", "loss_reduce", "project_bwd", "project_adam", "adam", "allreduce"};
+
+
+
+struct isg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+
+  // scene (SoA float4) and Adam moments (n x 2 float4 each)
+  int64_t n = 0, n_alloc = 0;
+  float4* ms = nullptr;
+  float4* co = nullptr;
+  float4* m = nullptr;
+  float4* v = nullptr;
+  int64_t adam_t = 0;
+
+  // per-splat work buffers
+  float4* rec_geo = nullptr;
+  uint32_t* depth[2] = {nullptr, nullptr};
+  uint32_t* order[2] = {nullptr, nullptr};
+  uint32_t* ntiles = nullptr;
+  uint32_t* rank_of = nullptr;
+  isg::RenderRec* rec_sorted = nullptr;
+  float4* grad2d = nullptr;  // n x 2, indexed by depth rank
+  float4* grad3d = nullptr;  // n x 2, indexed by splat
+  int order_buf = 0;         // which order[] holds the depth order
+
+  // (tile, rank) keys
+  int64_t key_cap = 0;
+  uint32_t* tkey[2] = {nullptr, nullptr};
+  uint32_t* tval[2] = {nullptr, nullptr};
+  int tile_buf = 0;
+
+  // sort / scan scratch
+  isg::SortScratch sort{};
+  int64_t sort_tiles_alloc = 0;
+  unsigned long long* scan_scratch = nullptr;
+  int64_t scan_words_alloc = 0;
+
+  // pixels / tiles
+  int64_t pix_alloc = 0, tiles_alloc = 0;
+  float* img = nullptr;
+  float* target = nullptr;
+  float* t_last = nullptr;
+  uint32_t* n_proc = nullptr;
+  uint2* ranges = nullptr;
+  double* tile_loss = nullptr;
+
+  // device scalars: [0] n_keys [1] first_bad [2] n_visible [3] scan counter [4] depth count
+  uint32_t* sc = nullptr;
+  unsigned long long* total = nullptr;     // [0] total keys, [1] skipped updates
+  double* loss = nullptr;                  // [0] accumulated, [1] last view
+  // pinned readback
+  uint32_t* h_sc = nullptr;
+  unsigned long long* h_total = nullptr;
+  double* h_loss = nullptr;
+
+  // frame state
+  bool have_frame = false;
+  isg::FrameParams last_fp{};
+  bool pending = false;  // grad2d holds an un-projected view
+  isg::FrameParams pending_fp{};
+  bool grad3d_valid = false;
+  bool frame_unchecked = false;  // frames launched since the last overflow check
+
+  // stats
+  int64_t n_keys = 0, n_visible = 0, regrow = 0, launches = 0;
+
+  // NCCL
+  void* nccl_comm = nullptr;
+  int nranks = 1, rank = 0;
+
+  // profiling
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_used;
+  double prof_ms[ST_COUNT] = {};
+  int64_t prof_calls[ST_COUNT] = {};
+};
+
+namespace {
+cudaEvent_t prof_event(isg_ctx* c) {
+  if (c->ev_pool.empty()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  cudaEvent_t e = c->ev_pool.back();
+  c->ev_pool.pop_back();
+  return e;
+}
+struct StageScope {
+  isg_ctx* c;
+  int stage;
+  cudaEvent_t a = nullptr;
+  StageScope(isg_ctx* c_, int s) : c(c_), stage(s) {
+    if (c->prof) {
+      a = prof_event(c);
+      cudaEventRecord(a, c->stream);
+    }
+  }
+  ~StageScope() {
+    if (a) {
+      cudaEvent_t b = prof_event(c);
+      cudaEventRecord(b, c->stream);
+      c->ev_used.push_back({stage, {a, b}});
+    }
+  }
+};
+}  // namespace
+#define ISG_STAGE(st) StageScope stage_scope_##st(ctx, st)
+
+namespace {
+
+using isg::FrameParams;
+
+isg_status fail(isg_ctx* c, isg_status s, const std::string& msg) {
+  if (c) c->err = msg;
+  return s;
+}
+
+isg_status cuda_fail(isg_ctx* c, cudaError_t e, const char* where) {
+  return fail(c, e == cudaErrorMemoryAllocation ? ISG_E_OOM : ISG_E_CUDA,
+              std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define ISG_CUDA(call)                                   \
+  do {                                                   \
+    cudaError_t e_ = (call);                             \
+    if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call); \
+  } while (0)
+
+#define ISG_CHECK_LAUNCH()                                         \
+  do {                                                             \
+    cudaError_t e_ = cudaGetLastError();                           \
+    if (e_ != cudaSuccess) return cuda_fail(ctx, e_, "kernel launch"); \
+  } while (0)
+
+template <class T>
+cudaError_t realloc_dev(T** p, size_t count) {
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  if (count == 0) count = 1;
+  return cudaMalloc((void**)p, sizeof(T) * count);
+}
+
+int bits_for(int64_t v) {  // bits needed to represent values in [0, v)
+  int b = 1;
+  while (b < 32 && (int64_t(1) << b) < v) ++b;
+  return b;
+}
+
+isg_status ensure_scene(isg_ctx* ctx, int64_t n) {
+  if (n <= ctx->n_alloc) return ISG_OK;
+  const int64_t a = std::max<int64_t>(n, 1);
+  ISG_CUDA(realloc_dev(&ctx->ms, a));
+  ISG_CUDA(realloc_dev(&ctx->co, a));
+  ISG_CUDA(realloc_dev(&ctx->m, 2 * a));
+  ISG_CUDA(realloc_dev(&ctx->v, 2 * a));
+  ISG_CUDA(realloc_dev(&ctx->rec_geo, a));
+  for (int i = 0; i < 2; ++i) {
+    ISG_CUDA(realloc_dev(&ctx->depth[i], a));
+    ISG_CUDA(realloc_dev(&ctx->order[i], a));
+  }
+  ISG_CUDA(realloc_dev(&ctx->ntiles, a));
+  ISG_CUDA(realloc_dev(&ctx->rank_of, a));
+  ISG_CUDA(realloc_dev(&ctx->rec_sorted, a));
+  ISG_CUDA(realloc_dev(&ctx->grad2d, 2 * a));
+  ISG_CUDA(realloc_dev(&ctx->grad3d, 2 * a));
+  ISG_CUDA(cudaMemsetAsync(ctx->grad2d, 0, sizeof(float4) * 2 * a, ctx->stream));
+  const int64_t words = isg::scan_emit_scratch_words(a) + 1;
+  ISG_CUDA(realloc_dev(&ctx->scan_scratch, words));
+  ctx->scan_words_alloc = words;
+  ctx->n_alloc = a;
+  return ISG_OK;
+}
+
+isg_status ensure_sort_scratch(isg_ctx* ctx, int64_t cap) {
+  const int64_t tiles = isg::sort_tiles_for(cap);
+  if (tiles <= ctx->sort_tiles_alloc && ctx->sort.hist) return ISG_OK;
+  const int64_t t = std::max<int64_t>(tiles, 1);
+  ISG_CUDA(realloc_dev(&ctx->sort.hist, isg::kMaxPasses * 256));
+  ISG_CUDA(realloc_dev(&ctx->sort.counters, isg::kMaxPasses));
+  ISG_CUDA(realloc_dev(&ctx->sort.lookback, (size_t)isg::kMaxPasses * 256 * t));
+  ctx->sort.max_tiles = t;
+  ctx->sort_tiles_alloc = t;
+  return ISG_OK;
+}
+
+isg_status ensure_keys(isg_ctx* ctx, int64_t cap) {
+  if (cap <= ctx->key_cap) return ISG_OK;
+  for (int i = 0; i < 2; ++i) {
+    ISG_CUDA(realloc_dev(&ctx->tkey[i], cap));
+    ISG_CUDA(realloc_dev(&ctx->tval[i], cap));
+  }
+  ctx->key_cap = cap;
+  return ISG_OK;
+}
+
+isg_status ensure_pixels(isg_ctx* ctx, int W, int H) {
+  const int64_t pix = (int64_t)W * H;
+  const int64_t tiles =
+      (int64_t)((W + isg::kTile - 1) / isg::kTile) * ((H + isg::kTile - 1) / isg::kTile);
+  if (pix > ctx->pix_alloc) {
+    ISG_CUDA(realloc_dev(&ctx->img, 3 * pix));
+    ISG_CUDA(realloc_dev(&ctx->target, 3 * pix));
+    ISG_CUDA(realloc_dev(&ctx->t_last, pix));
+    ISG_CUDA(realloc_dev(&ctx->n_proc, pix));
+    ctx->pix_alloc = pix;
+  }
+  if (tiles > ctx->tiles_alloc) {
+    ISG_CUDA(realloc_dev(&ctx->ranges, tiles));
+    ISG_CUDA(realloc_dev(&ctx->tile_loss, tiles));
+    ctx->tiles_alloc = tiles;
+  }
+  return ISG_OK;
+}
+
+// Camera::validate (splat3d.cpp:27-37) on the FP32 camera.  Orthonormality is checked to
+// 1e-5 here (FP32 cannot hold 1e-9); the C++ drop-in validates the FP64 camera to 1e-9 first.
+isg_status validate_camera(isg_ctx* ctx, const isg_camera* c) {
+  if (!c) return fail(ctx, ISG_E_ARG, "camera: null pointer");
+  for (int i = 0; i < 9; ++i)
+    if (!std::isfinite(c->R[i])) return fail(ctx, ISG_E_DOMAIN, "Camera: non-finite transform");
+  for (int i = 0; i < 3; ++i)
+    if (!std::isfinite(c->t[i])) return fail(ctx, ISG_E_DOMAIN, "Camera: non-finite transform");
+  double worst = 0.0;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      double d = 0.0;
+      for (int k = 0; k < 3; ++k) d += (double)c->R[3 * i + k] * (double)c->R[3 * j + k];
+      worst = std::max(worst, std::fabs(d - (i == j ? 1.0 : 0.0)));
+    }
+  if (worst > 1e-5) return fail(ctx, ISG_E_DOMAIN, "Camera.rotation: not orthonormal within 1e-9");
+  if (!(c->focal > 0.0f) || !std::isfinite(c->focal))
+    return fail(ctx, ISG_E_DOMAIN, "Camera.focal: must be > 0");
+  if (!std::isfinite(c->cx) || !std::isfinite(c->cy))
+    return fail(ctx, ISG_E_DOMAIN, "Camera: non-finite transform");
+  if (c->width <= 0 || c->height <= 0) return fail(ctx, ISG_E_DOMAIN, "Camera: bad image size");
+  if ((int64_t)c->width * c->height > (int64_t)1 << 30)
+    return fail(ctx, ISG_E_ARG, "Camera: image too large");
+  return ISG_OK;
+}
+
+FrameParams make_fp(const isg_camera* cam, const float bg[3], float t_min) {
+  FrameParams fp;
+  fp.cam = *cam;
+  fp.tiles_x = (cam->width + isg::kTile - 1) / isg::kTile;
+  fp.tiles_y = (cam->height + isg::kTile - 1) / isg::kTile;
+  fp.n_tiles = fp.tiles_x * fp.tiles_y;
+  for (int i = 0; i < 3; ++i) fp.bg[i] = bg ? bg[i] : 0.0f;
+  fp.t_min = t_min;
+  return fp;
+}
+
+// Project a pending view's 2D gradients into the 3D accumulator (K8a).
+isg_status flush_pending(isg_ctx* ctx) {
+  if (!ctx->pending) return ISG_OK;
+  ISG_STAGE(ST_PROJECT_BWD);
+  isg::launch_project_backward(ctx->ms, ctx->n, ctx->pending_fp, ctx->rank_of, ctx->grad2d,
+                               ctx->grad3d, !ctx->grad3d_valid, ctx->stream);
+  ISG_CHECK_LAUNCH();
+  ctx->launches++;
+  ctx->grad3d_valid = true;
+  ctx->pending = false;
+  return ISG_OK;
+}
+
+// Launch one frame: K1, depth sort, scan/emit, tile sort, ranges, K6 into `out`.
+isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out) {
+  isg_status s = flush_pending(ctx);
+  if (s != ISG_OK) return s;
+  if ((s = ensure_pixels(ctx, fp.cam.width, fp.cam.height)) != ISG_OK) return s;
+  if (ctx->key_cap == 0) {
+    if ((s = ensure_keys(ctx, std::max<int64_t>(6 * ctx->n, 1 << 20))) != ISG_OK) return s;
+  }
+  if ((s = ensure_sort_scratch(ctx, std::max(ctx->key_cap, ctx->n))) != ISG_OK) return s;
+  cudaStream_t st = ctx->stream;
+  const int64_t n = ctx->n;
+  // scalars: n_keys=0, first_bad=~0, n_visible=0, scan counter=0
+  {
+  ISG_STAGE(ST_MEMSET);
+  ISG_CUDA(cudaMemsetAsync(ctx->sc, 0, sizeof(uint32_t) * 8, st));
+  ISG_CUDA(cudaMemsetAsync(ctx->sc + 1, 0xFF, sizeof(uint32_t), st));
+  ISG_CUDA(cudaMemsetAsync(ctx->total, 0, sizeof(unsigned long long), st));
+  ISG_CUDA(cudaMemsetAsync(ctx->scan_scratch, 0,
+                           sizeof(unsigned long long) * (isg::scan_emit_scratch_words(n) + 1), st));
+  ISG_CUDA(cudaMemsetAsync(ctx->ranges, 0, sizeof(uint2) * fp.n_tiles, st));
+  }
+  {
+  ISG_STAGE(ST_PREPROCESS);
+  isg::launch_preprocess(ctx->ms, ctx->co, n, fp, ctx->rec_geo, ctx->depth[0], ctx->ntiles,
+                         ctx->sc + 1, ctx->sc + 4, st);
+  ISG_CHECK_LAUNCH();
+  ctx->launches++;
+  }
+  if (n > 0) {
+    {
+    ISG_STAGE(ST_DEPTH_SORT);
+    ctx->order_buf = isg::radix_sort_pairs(ctx->depth, ctx->order, true, ctx->sc + 4, n, 32,
+                                           ctx->sort, st, &ctx->launches);
+    ISG_CHECK_LAUNCH();
+    }
+    {
+    ISG_STAGE(ST_SCAN_EMIT);
+    isg::launch_scan_emit(ctx->order[ctx->order_buf], ctx->ntiles, ctx->rec_geo, ctx->co, n, fp,
+                          ctx->rec_sorted, ctx->rank_of, ctx->tkey[0], ctx->tval[0],
+                          ctx->key_cap, ctx->scan_scratch, ctx->sc + 3, ctx->sc + 0, ctx->total,
+                          ctx->sc + 2, st);
+    ISG_CHECK_LAUNCH();
+    ctx->launches++;
+    }
+    {
+    ISG_STAGE(ST_TILE_SORT);
+    ctx->tile_buf = isg::radix_sort_pairs(ctx->tkey, ctx->tval, false, ctx->sc + 0, ctx->key_cap,
+                                          bits_for(fp.n_tiles), ctx->sort, st, &ctx->launches);
+    ISG_CHECK_LAUNCH();
+    }
+    ISG_STAGE(ST_RANGES);
+    isg::launch_ranges(ctx->tkey[ctx->tile_buf], ctx->sc + 0, ctx->key_cap, ctx->ranges, st);
+    ISG_CHECK_LAUNCH();
+    ctx->launches++;
+  }
+  ISG_STAGE(ST_BLEND_FWD);
+  isg::launch_blend_fwd(fp, ctx->ranges, ctx->tval[ctx->tile_buf], ctx->rec_sorted, ctx->total,
+                        ctx->key_cap, out, ctx->t_last, ctx->n_proc, st);
+  ISG_CHECK_LAUNCH();
+  ctx->launches++;
+  ctx->have_frame = true;
+  ctx->last_fp = fp;
+  ctx->frame_unchecked = true;
+  return ISG_OK;
+}
+
+const char* splat_message(const float* a, const float* c) {
+  if (!std::isfinite(a[0]) || !std::isfinite(a[1]) || !std::isfinite(a[2]))
+    return "IsoSplat3D.mu: non-finite coordinates";
+  if (!(a[3] > 0.0f) || !std::isfinite(a[3])) return "IsoSplat3D.sigma: must be positive and finite";
+  if (!std::isfinite(c[0]) || !std::isfinite(c[1]) || !std::isfinite(c[2]))
+    return "IsoSplat3D.color: non-finite";
+  return "IsoSplat3D.opacity: must be in [0,1]";
+}
+
+// Read back the frame scalars (syncs).  Returns ISG_E_DOMAIN for an invalid splat, and sets
+// *overflow when the key capacity was exceeded (capacity is grown for the re-run).
+isg_status check_frame(isg_ctx* ctx, bool* overflow) {
+  *overflow = false;
+  ISG_CUDA(cudaMemcpyAsync(ctx->h_sc, ctx->sc, sizeof(uint32_t) * 8, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  ISG_CUDA(cudaMemcpyAsync(ctx->h_total, ctx->total, sizeof(unsigned long long) * 2,
+                           cudaMemcpyDeviceToHost, ctx->stream));
+  ISG_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->frame_unchecked = false;
+  ctx->n_visible = ctx->h_sc[2];
+  ctx->n_keys = (int64_t)ctx->h_total[0];
+  if (ctx->h_sc[1] != 0xFFFFFFFFu) {
+    const uint32_t bad = ctx->h_sc[1];
+    float a[4], c[4];
+    ISG_CUDA(cudaMemcpy(a, ctx->ms + bad, sizeof a, cudaMemcpyDeviceToHost));
+    ISG_CUDA(cudaMemcpy(c, ctx->co + bad, sizeof c, cudaMemcpyDeviceToHost));
+    return fail(ctx, ISG_E_DOMAIN, splat_message(a, c));
+  }
+  if (ctx->n_keys > ctx->key_cap) {
+    *overflow = true;
+    const int64_t want = ctx->n_keys + ctx->n_keys / 4 + 1024;
+    if (want > (int64_t)0xFFFFFFF0ll)
+      return fail(ctx, ISG_E_OVERFLOW, "binning: more than 2^32 (tile, splat) pairs");
+    isg_status s = ensure_keys(ctx, want);
+    if (s != ISG_OK) return s;
+    s = ensure_sort_scratch(ctx, std::max(ctx->key_cap, ctx->n));
+    if (s != ISG_OK) return s;
+    ctx->regrow++;
+  }
+  return ISG_OK;
+}
+
+isg_status run_backward(isg_ctx* ctx, const FrameParams& fp, const float* target_dev,
+                        float weight) {
+  const float scale = weight / (3.0f * (float)fp.cam.width * (float)fp.cam.height);
+  {
+  ISG_STAGE(ST_BLEND_BWD);
+  isg::launch_blend_bwd(fp, ctx->ranges, ctx->tval[ctx->tile_buf], ctx->rec_sorted, ctx->total,
+                        ctx->key_cap, ctx->img, target_dev, ctx->t_last, ctx->n_proc, scale,
+                        ctx->grad2d, ctx->tile_loss, ctx->stream);
+  ISG_CHECK_LAUNCH();
+  }
+  ISG_STAGE(ST_LOSS_REDUCE);
+  isg::launch_loss_reduce(ctx->tile_loss, fp.n_tiles,
+                          (double)weight / (3.0 * fp.cam.width * (double)fp.cam.height), ctx->loss,
+                          ctx->stream);
+  ISG_CHECK_LAUNCH();
+  ctx->launches += 2;
+  ctx->pending = true;
+  ctx->pending_fp = fp;
+  return ISG_OK;
+}
+
+}  // namespace
+
+// ============================================================================================
+extern "C" {
+
+int isg_abi_version(void) { return ISG_ABI_VERSION; }
+
+const char* isg_status_string(isg_status s) {
+  switch (s) {
+    case ISG_OK: return "ok";
+    case ISG_E_DOMAIN: return "domain error";
+    case ISG_E_ARG: return "invalid argument";
+    case ISG_E_CUDA: return "cuda error";
+    case ISG_E_OOM: return "out of device memory";
+    case ISG_E_OVERFLOW: return "capacity overflow";
+    case ISG_E_NCCL: return "nccl error";
+    case ISG_E_STATE: return "invalid call order";
+  }
+  return "unknown";
+}
+
+const char* isg_last_error(const isg_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+isg_status isg_create(int device, int64_t max_gaussians, int32_t max_width, int32_t max_height,
+                      isg_ctx** out) {
+  if (!out) return ISG_E_ARG;
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return ISG_E_CUDA;
+  }
+  if (device < 0 || device >= count) return ISG_E_ARG;
+  isg_ctx* ctx = new isg_ctx();
+  ctx->device = device;
+  if (cudaSetDevice(device) != cudaSuccess) {
+    delete ctx;
+    return ISG_E_CUDA;
+  }
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ctx;
+    return ISG_E_CUDA;
+  }
+  ctx->own_stream = true;
+  isg_status s = ISG_OK;
+  auto chk = [&](cudaError_t e) {
+    if (e != cudaSuccess && s == ISG_OK) s = e == cudaErrorMemoryAllocation ? ISG_E_OOM : ISG_E_CUDA;
+  };
+  chk(cudaMalloc(&ctx->sc, sizeof(uint32_t) * 8));
+  chk(cudaMalloc(&ctx->total, sizeof(unsigned long long) * 2));
+  chk(cudaMalloc(&ctx->loss, sizeof(double) * 2));
+  chk(cudaMallocHost(&ctx->h_sc, sizeof(uint32_t) * 8));
+  chk(cudaMallocHost(&ctx->h_total, sizeof(unsigned long long) * 2));
+  chk(cudaMallocHost(&ctx->h_loss, sizeof(double) * 2));
+  if (s == ISG_OK) {
+    chk(cudaMemset(ctx->total, 0, sizeof(unsigned long long) * 2));
+    chk(cudaMemset(ctx->loss, 0, sizeof(double) * 2));
+  }
+  if (s == ISG_OK && max_gaussians > 0) s = ensure_scene(ctx, max_gaussians);
+  if (s == ISG_OK && max_width > 0 && max_height > 0) s = ensure_pixels(ctx, max_width, max_height);
+  if (s != ISG_OK) {
+    isg_destroy(ctx);
+    return s;
+  }
+  *out = ctx;
+  return ISG_OK;
+}
+
+isg_status isg_nccl_detach(isg_ctx* ctx);
+
+void isg_destroy(isg_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->nccl_comm) isg_nccl_detach(ctx);
+  void* dev[] = {ctx->ms, ctx->co, ctx->m, ctx->v, ctx->rec_geo, ctx->depth[0], ctx->depth[1],
+                 ctx->order[0], ctx->order[1], ctx->ntiles, ctx->rank_of, ctx->rec_sorted,
+                 ctx->grad2d, ctx->grad3d, ctx->tkey[0], ctx->tkey[1], ctx->tval[0], ctx->tval[1],
+                 ctx->sort.hist, ctx->sort.lookback, ctx->sort.counters, ctx->scan_scratch,
+                 ctx->img, ctx->target, ctx->t_last, ctx->n_proc, ctx->ranges, ctx->tile_loss,
+                 ctx->sc, ctx->total, ctx->loss};
+  for (void* p : dev)
+    if (p) cudaFree(p);
+  if (ctx->h_sc) cudaFreeHost(ctx->h_sc);
+  if (ctx->h_total) cudaFreeHost(ctx->h_total);
+  if (ctx->h_loss) cudaFreeHost(ctx->h_loss);
+  for (auto& u : ctx->ev_used) {
+    cudaEventDestroy(u.second.first);
+    cudaEventDestroy(u.second.second);
+  }
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+isg_status isg_set_stream(isg_ctx* ctx, void* stream) {
+  if (!ctx) return ISG_E_ARG;
+  cudaSetDevice(ctx->device);
+  ISG_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  if (stream) {
+    ctx->stream = (cudaStream_t)stream;
+    ctx->own_stream = false;
+  } else {
+    ISG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    ctx->own_stream = true;
+  }
+  return ISG_OK;
+}
+
+isg_status isg_synchronize(isg_ctx* ctx) {
+  if (!ctx) return ISG_E_ARG;
+  cudaSetDevice(ctx->device);
+  if (ctx->frame_unchecked) {
+    bool ov = false;
+    isg_status s = check_frame(ctx, &ov);
+    if (s != ISG_OK) return s;
+    if (ov)
+      return fail(ctx, ISG_E_OVERFLOW,
+                  "tile-key capacity was exceeded by an asynchronous frame; capacity has been "
+                  "grown — re-run the frames issued since the last synchronisation");
+    return ISG_OK;
+  }
+  ISG_CUDA(cudaStreamSynchronize(ctx->stream));
+  return ISG_OK;
+}
+
+isg_status isg_get_stats(const isg_ctx* ctx, isg_stats* out) {
+  if (!ctx || !out) return ISG_E_ARG;
+  out->n_gaussians = ctx->n;
+  out->n_visible = ctx->n_visible;
+  out->n_keys = ctx->n_keys;
+  out->key_capacity = ctx->key_cap;
+  out->n_tiles = ctx->have_frame ? ctx->last_fp.n_tiles : 0;
+  out->adam_steps = ctx->adam_t;
+  out->skipped_updates = ctx->h_total ? (int64_t)ctx->h_total[1] : 0;
+  out->regrow_events = ctx->regrow;
+  out->kernel_launches = ctx->launches;
+  return ISG_OK;
+}
+
+static isg_status set_scene_impl(isg_ctx* ctx, int64_t n, const float* ms, const float* co,
+                                 cudaMemcpyKind kind) {
+  if (!ctx) return ISG_E_ARG;
+  if (n < 0 || n > 0xFFFFFFF0ll) return fail(ctx, ISG_E_ARG, "set_scene: bad splat count");
+  if (n > 0 && (!ms || !co)) return fail(ctx, ISG_E_ARG, "set_scene: null pointer");
+  cudaSetDevice(ctx->device);
+  isg_status s = ensure_scene(ctx, n);
+  if (s != ISG_OK) return s;
+  if (n > 0) {
+    ISG_CUDA(cudaMemcpyAsync(ctx->ms, ms, sizeof(float4) * n, kind, ctx->stream));
+    ISG_CUDA(cudaMemcpyAsync(ctx->co, co, sizeof(float4) * n, kind, ctx->stream));
+    ISG_CUDA(cudaMemsetAsync(ctx->m, 0, sizeof(float4) * 2 * n, ctx->stream));
+    ISG_CUDA(cudaMemsetAsync(ctx->v, 0, sizeof(float4) * 2 * n, ctx->stream));
+    ISG_CUDA(cudaMemsetAsync(ctx->grad2d, 0, sizeof(float4) * 2 * n, ctx->stream));
+  }
+  if (ctx->n != n || ctx->key_cap < 4 * n) {
+    // size the key buffers for the new scene on the next frame
+    if (ctx->key_cap < std::max<int64_t>(6 * n, 1 << 20)) {
+      s = ensure_keys(ctx, std::max<int64_t>(6 * n, 1 << 20));
+      if (s != ISG_OK) return s;
+    }
+  }
+  ctx->n = n;
+  ctx->adam_t = 0;
+  ctx->pending = false;
+  ctx->grad3d_valid = false;
+  ctx->have_frame = false;
+  ISG_CUDA(cudaMemsetAsync(ctx->loss, 0, sizeof(double) * 2, ctx->stream));
+  if (kind == cudaMemcpyHostToDevice) ISG_CUDA(cudaStreamSynchronize(ctx->stream));
+  return ISG_OK;
+}
+
+isg_status isg_set_scene(isg_ctx* ctx, int64_t n, const float* ms, const float* co) {
+  return set_scene_impl(ctx, n, ms, co, cudaMemcpyHostToDevice);
+}
+
+isg_status isg_set_scene_device(isg_ctx* ctx, int64_t n, const float* ms, const float* co) {
+  return set_scene_impl(ctx, n, ms, co, cudaMemcpyDeviceToDevice);
+}
+
+isg_status isg_get_scene(isg_ctx* ctx, float* ms, float* co) {
+  if (!ctx) return ISG_E_ARG;
+  cudaSetDevice(ctx->device);
+  if (ctx->n > 0) {
+    if (ms) ISG_CUDA(cudaMemcpyAsync(ms, ctx->ms, sizeof(float4) * ctx->n, cudaMemcpyDeviceToHost, ctx->stream));
+    if (co) ISG_CUDA(cudaMemcpyAsync(co, ctx->co, sizeof(float4) * ctx->n, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  ISG_CUDA(cudaStreamSynchronize(ctx->stream));
+  return ISG_OK;
+}
+
+isg_status isg_render_device(isg_ctx* ctx, const isg_camera* cam, const float bg[3], float t_min,
+                             float* out_dev) {
+  if (!ctx) return ISG_E_ARG;
+  if (!out_dev) return fail(ctx, ISG_E_ARG, "render: null output");
+  if (!(t_min >= 0.0f) || !(t_min < 1.0f)) return fail(ctx, ISG_E_ARG, "render: t_min must be in [0,1)");
+  cudaSetDevice(ctx->device);
+  isg_status s = validate_camera(ctx, cam);
+  if (s != ISG_OK) return s;
+  return launch_frame(ctx, make_fp(cam, bg, t_min), out_dev);
+}
+
+isg_status isg_render(isg_ctx* ctx, const isg_camera* cam, const float bg[3], float t_min,
+                      float* out_hwc3) {
+  if (!ctx) return ISG_E_ARG;
+  if (!out_hwc3) return fail(ctx, ISG_E_ARG, "render: null output");
+  if (!(t_min >= 0.0f) || !(t_min < 1.0f)) return fail(ctx, ISG_E_ARG, "render: t_min must be in [0,1)");
+  cudaSetDevice(ctx->device);
+  isg_status s = validate_camera(ctx, cam);
+  if (s != ISG_OK) return s;
+  const FrameParams fp = make_fp(cam, bg, t_min);
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    if ((s = launch_frame(ctx, fp, ctx->img)) != ISG_OK) return s;
+    bool ov = false;
+    if ((s = check_frame(ctx, &ov)) != ISG_OK) return s;
+    if (ov) continue;
+    ISG_CUDA(cudaMemcpyAsync(out_hwc3, ctx->img, sizeof(float) * 3 * (size_t)cam->width * cam->height,
+                             cudaMemcpyDeviceToHost, ctx->stream));
+    ISG_CUDA(cudaStreamSynchronize(ctx->stream));
+    return ISG_OK;
+  }
+  return fail(ctx, ISG_E_OVERFLOW, "render: key capacity kept overflowing");
+}
+
+isg_status isg_loss_backward_device(isg_ctx* ctx, const isg_camera* cam, const float bg[3],
+                                    float t_min, const float* target_dev, float weight) {
+  if (!ctx) return ISG_E_ARG;
+  if (!target_dev) return fail(ctx, ISG_E_ARG, "loss_backward: null target");
+  if (!(t_min >= 0.0f) || !(t_min < 1.0f)) return fail(ctx, ISG_E_ARG, "loss_backward: t_min must be in [0,1)");
+  if (!std::isfinite(weight)) return fail(ctx, ISG_E_ARG, "loss_backward: non-finite weight");
+  cudaSetDevice(ctx->device);
+  isg_status s = validate_camera(ctx, cam);
+  if (s != ISG_OK) return s;
+  const FrameParams fp = make_fp(cam, bg, t_min);
+  if ((s = launch_frame(ctx, fp, ctx->img)) != ISG_OK) return s;
+  return run_backward(ctx, fp, target_dev, weight);
+}
+
+isg_status isg_loss_backward(isg_ctx* ctx, const isg_camera* cam, const float bg[3], float t_min,
+                             const float* target, float weight, double* loss_out) {
+  if (!ctx) return ISG_E_ARG;
+  if (!target) return fail(ctx, ISG_E_ARG, "loss_backward: null target");
+  if (!(t_min >= 0.0f) || !(t_min < 1.0f)) return fail(ctx, ISG_E_ARG, "loss_backward: t_min must be in [0,1)");
+  if (!std::isfinite(weight)) return fail(ctx, ISG_E_ARG, "loss_backward: non-finite weight");
+  cudaSetDevice(ctx->device);
+  isg_status s = validate_camera(ctx, cam);
+  if (s != ISG_OK) return s;
+  if ((s = ensure_pixels(ctx, cam->width, cam->height)) != ISG_OK) return s;
+  const FrameParams fp = make_fp(cam, bg, t_min);
+  ISG_CUDA(cudaMemcpyAsync(ctx->target, target, sizeof(float) * 3 * (size_t)cam->width * cam->height,
+                           cudaMemcpyHostToDevice, ctx->stream));
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    if ((s = launch_frame(ctx, fp, ctx->img)) != ISG_OK) return s;
+    if ((s = run_backward(ctx, fp, ctx->target, weight)) != ISG_OK) return s;
+    bool ov = false;
+    if ((s = check_frame(ctx, &ov)) != ISG_OK) return s;
+    if (ov) {  // K6/K7 skipped the overflowed frame: nothing was accumulated
+      ctx->pending = false;
+      continue;
+    }
+    if (loss_out) {
+      ISG_CUDA(cudaMemcpyAsync(ctx->h_loss, ctx->loss, sizeof(double) * 2, cudaMemcpyDeviceToHost,
+                               ctx->stream));
+      ISG_CUDA(cudaStreamSynchronize(ctx->stream));
+      *loss_out = ctx->h_loss[1];
+    }
+    return ISG_OK;
+  }
+  return fail(ctx, ISG_E_OVERFLOW, "loss_backward: key capacity kept overflowing");
+}
+
+isg_status isg_read_loss(isg_ctx* ctx, double* loss_out) {
+  if (!ctx || !loss_out) return ISG_E_ARG;
+  isg_status s = isg_synchronize(ctx);
+  if (s != ISG_OK) return s;
+  ISG_CUDA(cudaMemcpyAsync(ctx->h_loss, ctx->loss, sizeof(double) * 2, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  ISG_CUDA(cudaStreamSynchronize(ctx->stream));
+  *loss_out = ctx->h_loss[0];
+  return ISG_OK;
+}
+
+isg_status isg_zero_grads(isg_ctx* ctx) {
+  if (!ctx) return ISG_E_ARG;
+  cudaSetDevice(ctx->device);
+  if (ctx->pending && ctx->n > 0)
+    ISG_CUDA(cudaMemsetAsync(ctx->grad2d, 0, sizeof(float4) * 2 * ctx->n, ctx->stream));
+  ctx->pending = false;
+  ctx->grad3d_valid = false;
+  ISG_CUDA(cudaMemsetAsync(ctx->loss, 0, sizeof(double) * 2, ctx->stream));
+  return ISG_OK;
+}
+
+isg_status isg_grads_device(isg_ctx* ctx, float** grads_dev) {
+  if (!ctx || !grads_dev) return ISG_E_ARG;
+  cudaSetDevice(ctx->device);
+  isg_status s = flush_pending(ctx);
+  if (s != ISG_OK) return s;
+  if (!ctx->grad3d_valid && ctx->n > 0) {
+    ISG_CUDA(cudaMemsetAsync(ctx->grad3d, 0, sizeof(float4) * 2 * ctx->n, ctx->stream));
+    ctx->grad3d_valid = true;
+  }
+  *grads_dev = reinterpret_cast<float*>(ctx->grad3d);
+  return ISG_OK;
+}
+
+isg_status isg_get_grads(isg_ctx* ctx, float* grads) {
+  if (!ctx || !grads) return ISG_E_ARG;
+  float* d = nullptr;
+  isg_status s = isg_grads_device(ctx, &d);
+  if (s != ISG_OK) return s;
+  if (ctx->n > 0)
+    ISG_CUDA(cudaMemcpyAsync(grads, d, sizeof(float) * 8 * ctx->n, cudaMemcpyDeviceToHost, ctx->stream));
+  ISG_CUDA(cudaStreamSynchronize(ctx->stream));
+  return ISG_OK;
+}
+
+isg_status isg_nccl_allreduce_grads(isg_ctx* ctx);  // nccl_dl.cpp
+
+isg_status isg_adam_step(isg_ctx* ctx, const float lr[4], float b1, float b2, float eps) {
+  if (!ctx || !lr) return ISG_E_ARG;
+  for (int i = 0; i < 4; ++i)
+    if (!(lr[i] >= 0.0f) || !std::isfinite(lr[i])) return fail(ctx, ISG_E_ARG, "adam: learning rates must be >= 0");
+  if (!(b1 >= 0.0f && b1 < 1.0f) || !(b2 >= 0.0f && b2 < 1.0f))
+    return fail(ctx, ISG_E_ARG, "adam: betas must be in [0,1)");
+  if (!(eps >= 0.0f)) return fail(ctx, ISG_E_ARG, "adam: eps must be >= 0");
+  if (!ctx->pending && !ctx->grad3d_valid)
+    return fail(ctx, ISG_E_STATE, "adam: no gradients accumulated since the last step");
+  cudaSetDevice(ctx->device);
+  ctx->adam_t++;
+  isg::AdamParams ap;
+  for (int i = 0; i < 4; ++i) ap.lr[i] = lr[i];
+  ap.b1 = b1;
+  ap.b2 = b2;
+  ap.eps = eps;
+  const double bc1 = 1.0 - std::pow((double)b1, (double)ctx->adam_t);
+  const double bc2 = 1.0 - std::pow((double)b2, (double)ctx->adam_t);
+  for (int i = 0; i < 4; ++i) ap.step_size[i] = (float)((double)lr[i] / bc1);
+  ap.bc2_sqrt = (float)std::sqrt(bc2);
+  if (ctx->pending && !ctx->grad3d_valid && !ctx->nccl_comm) {
+    // single view since the last step: projection backward fused with Adam (K8)
+    ISG_STAGE(ST_PROJECT_ADAM);
+    isg::launch_project_adam(ctx->ms, ctx->co, ctx->n, ctx->pending_fp, ctx->rank_of, ctx->grad2d,
+                             ctx->m, ctx->v, ap, ctx->total + 1, ctx->stream);
+    ISG_CHECK_LAUNCH();
+    ctx->launches++;
+    ctx->pending = false;
+  } else {
+    isg_status s = flush_pending(ctx);
+    if (s != ISG_OK) return s;
+    if (ctx->nccl_comm) {
+      ISG_STAGE(ST_ALLREDUCE);
+      s = isg_nccl_allreduce_grads(ctx);
+      if (s != ISG_OK) return s;
+    }
+    ISG_STAGE(ST_ADAM);
+    isg::launch_adam(ctx->ms, ctx->co, ctx->n, ctx->grad3d, ctx->m, ctx->v, ap, ctx->total + 1,
+                     ctx->stream);
+    ISG_CHECK_LAUNCH();
+    ctx->launches++;
+  }
+  ctx->grad3d_valid = false;
+  ISG_CUDA(cudaMemsetAsync(ctx->loss, 0, sizeof(double), ctx->stream));
+  return ISG_OK;
+}
+
+isg_status isg_debug_bins(isg_ctx* ctx, uint64_t* keys, uint32_t* vals, int64_t* n_keys,
+                          uint32_t* ranges) {
+  if (!ctx || !n_keys) return ISG_E_ARG;
+  if (!ctx->have_frame) return fail(ctx, ISG_E_STATE, "debug_bins: no frame rendered yet");
+  cudaSetDevice(ctx->device);
+  bool ov = false;
+  isg_status s = check_frame(ctx, &ov);
+  if (s != ISG_OK) return s;
+  if (ov) return fail(ctx, ISG_E_OVERFLOW, "debug_bins: last frame overflowed");
+  const int64_t nk = ctx->n_keys;
+  *n_keys = nk;
+  const FrameParams& fp = ctx->last_fp;
+  if ((keys || vals) && nk > 0) {
+    uint64_t* dk = nullptr;
+    uint32_t* dv = nullptr;
+    ISG_CUDA(cudaMalloc(&dk, sizeof(uint64_t) * nk));
+    ISG_CUDA(cudaMalloc(&dv, sizeof(uint32_t) * nk));
+    isg::launch_debug_keys(ctx->tkey[ctx->tile_buf], ctx->tval[ctx->tile_buf],
+                           ctx->order[ctx->order_buf], ctx->ms, fp, nk, dk, dv, ctx->stream);
+    if (keys) cudaMemcpyAsync(keys, dk, sizeof(uint64_t) * nk, cudaMemcpyDeviceToHost, ctx->stream);
+    if (vals) cudaMemcpyAsync(vals, dv, sizeof(uint32_t) * nk, cudaMemcpyDeviceToHost, ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+    cudaFree(dk);
+    cudaFree(dv);
+  }
+  if (ranges)
+    ISG_CUDA(cudaMemcpyAsync(ranges, ctx->ranges, sizeof(uint2) * fp.n_tiles, cudaMemcpyDeviceToHost,
+                             ctx->stream));
+  ISG_CUDA(cudaStreamSynchronize(ctx->stream));
+  ISG_CUDA(cudaGetLastError());
+  return ISG_OK;
+}
+
+isg_status isg_profile_enable(isg_ctx* ctx, int on) {
+  if (!ctx) return ISG_E_ARG;
+  ctx->prof = on != 0;
+  return ISG_OK;
+}
+
+int isg_profile_num_stages(void) { return ST_COUNT; }
+
+const char* isg_profile_stage_name(int i) { return (i >= 0 && i < ST_COUNT) ? kStageNames[i] : ""; }
+
+isg_status isg_profile_read(isg_ctx* ctx, double* ms, int64_t* calls) {
+  if (!ctx) return ISG_E_ARG;
+  cudaSetDevice(ctx->device);
+  ISG_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (auto& u : ctx->ev_used) {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, u.second.first, u.second.second);
+    ctx->prof_ms[u.first] += t;
+    ctx->prof_calls[u.first] += 1;
+    ctx->ev_pool.push_back(u.second.first);
+    ctx->ev_pool.push_back(u.second.second);
+  }
+  ctx->ev_used.clear();
+  for (int i = 0; i < ST_COUNT; ++i) {
+    if (ms) ms[i] = ctx->prof_ms[i];
+    if (calls) calls[i] = ctx->prof_calls[i];
+    ctx->prof_ms[i] = 0.0;
+    ctx->prof_calls[i] = 0;
+  }
+  return ISG_OK;
+}
+
+isg_status isg_debug_pixel_state(isg_ctx* ctx, float* t_last, uint32_t* n_proc) {
+  if (!ctx) return ISG_E_ARG;
+  if (!ctx->have_frame) return fail(ctx, ISG_E_STATE, "debug_pixel_state: no frame rendered yet");
+  cudaSetDevice(ctx->device);
+  const size_t pix = (size_t)ctx->last_fp.cam.width * ctx->last_fp.cam.height;
+  if (t_last) ISG_CUDA(cudaMemcpyAsync(t_last, ctx->t_last, sizeof(float) * pix, cudaMemcpyDeviceToHost, ctx->stream));
+  if (n_proc) ISG_CUDA(cudaMemcpyAsync(n_proc, ctx->n_proc, sizeof(uint32_t) * pix, cudaMemcpyDeviceToHost, ctx->stream));
+  ISG_CUDA(cudaStreamSynchronize(ctx->stream));
+  return ISG_OK;
+}
+
+}  // extern "C"
+
+// ============================================================================================
+// Multi-GPU: one process per GPU; NCCL resolved at run time so the library has no link-time
+// NCCL dependency (and reuses the libnccl.so.2 torch already loaded, if any).
+#include <nccl.h>  // types only
+
+namespace {
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                             cudaStream_t) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api;
+  tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return api;
+  api.get_unique_id = (decltype(api.get_unique_id))dlsym(h, "ncclGetUniqueId");
+  api.comm_init_rank = (decltype(api.comm_init_rank))dlsym(h, "ncclCommInitRank");
+  api.all_reduce = (decltype(api.all_reduce))dlsym(h, "ncclAllReduce");
+  api.comm_destroy = (decltype(api.comm_destroy))dlsym(h, "ncclCommDestroy");
+  api.error_string = (decltype(api.error_string))dlsym(h, "ncclGetErrorString");
+  api.ok = api.get_unique_id && api.comm_init_rank && api.all_reduce && api.comm_destroy &&
+           api.error_string;
+  return api;
+}
+}  // namespace
+
+extern "C" {
+
+isg_status isg_nccl_get_unique_id(void* out) {
+  if (!out) return ISG_E_ARG;
+  NcclApi& api = nccl();
+  if (!api.ok) return ISG_E_NCCL;
+  ncclUniqueId id;
+  if (api.get_unique_id(&id) != ncclSuccess) return ISG_E_NCCL;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(out, &id, sizeof id);
+  return ISG_OK;
+}
+
+isg_status isg_nccl_init(isg_ctx* ctx, int nranks, int rank, const void* uid) {
+  if (!ctx || !uid || nranks < 1 || rank < 0 || rank >= nranks) return ISG_E_ARG;
+  NcclApi& api = nccl();
+  if (!api.ok) return fail(ctx, ISG_E_NCCL, "nccl: libnccl.so.2 not loadable");
+  cudaSetDevice(ctx->device);
+  ncclUniqueId id;
+  std::memcpy(&id, uid, sizeof id);
+  ncclComm_t comm = nullptr;
+  const ncclResult_t r = api.comm_init_rank(&comm, nranks, id, rank);
+  if (r != ncclSuccess) return fail(ctx, ISG_E_NCCL, std::string("ncclCommInitRank: ") + api.error_string(r));
+  ctx->nccl_comm = comm;
+  ctx->nranks = nranks;
+  ctx->rank = rank;
+  return ISG_OK;
+}
+
+isg_status isg_nccl_detach(isg_ctx* ctx) {
+  if (!ctx) return ISG_E_ARG;
+  if (ctx->nccl_comm) {
+    cudaStreamSynchronize(ctx->stream);
+    nccl().comm_destroy((ncclComm_t)ctx->nccl_comm);
+  }
+  ctx->nccl_comm = nullptr;
+  ctx->nranks = 1;
+  ctx->rank = 0;
+  return ISG_OK;
+}
+
+// Sum the n x 8 gradient buffer and the loss accumulator over ranks (in place), so every
+// replica then runs an identical Adam step and the scenes stay bit-identical.
+isg_status isg_nccl_allreduce_grads(isg_ctx* ctx) {
+  NcclApi& api = nccl();
+  if (!ctx->grad3d_valid && ctx->n > 0) {
+    ISG_CUDA(cudaMemsetAsync(ctx->grad3d, 0, sizeof(float4) * 2 * ctx->n, ctx->stream));
+    ctx->grad3d_valid = true;
+  }
+  ncclResult_t r = api.all_reduce(ctx->grad3d, ctx->grad3d, (size_t)ctx->n * 8, ncclFloat32,
+                                  ncclSum, (ncclComm_t)ctx->nccl_comm, ctx->stream);
+  if (r == ncclSuccess)
+    r = api.all_reduce(ctx->loss, ctx->loss, 1, ncclFloat64, ncclSum, (ncclComm_t)ctx->nccl_comm,
+                       ctx->stream);
+  if (r != ncclSuccess) return fail(ctx, ISG_E_NCCL, std::string("ncclAllReduce: ") + api.error_string(r));
+  return ISG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,145 @@
+// K8 — projection backward and the fused Adam step.
+//
+// Projection backward: chain rule through u = f x/z + cx, v = f y/z + cy, s = sigma f/z
+// (Jacobian: projection_jacobian, /root/reference/proj/src/splat3d.cpp:39-47; closed forms
+// of the kernel gradient: include/isosplat/kernels.hpp:208-222), rotated back to world space
+// with R^T.  Optimizer slot: update_step (src/optimize.cpp:78-108) — sigma moves in log
+// space (:93,:105), updates with a non-finite gradient are skipped and counted (:87-90) — with
+// the Adam rule of torch.optim.Adam on (mu, log sigma, rgb, logit opacity).
+//
+// One thread per splat; params, moments and 3D grads are float4 SoA, coalesced; the 2D
+// gradient of splat g sits at its depth rank (rank_of[g]) and is zeroed after it is read.
+#include "isg_math.cuh"
+
+namespace isg {
+
+namespace {
+
+__device__ __forceinline__ void grad3d_of(const float4 ms, const isg_camera& cam, float4 a,
+                                          float4 b, float out[8]) {
+  const Proj p = project(ms, cam);
+  if (!p.vis) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) out[j] = 0.f;
+    return;
+  }
+  const float fz = cam.focal / p.zc;
+  const float gx = a.x * fz, gy = a.y * fz;
+  const float gz = -(((a.x * p.xc + a.y * p.yc) + a.z * ms.w) * fz) / p.zc;
+  out[0] = (cam.R[0] * gx + cam.R[3] * gy) + cam.R[6] * gz;
+  out[1] = (cam.R[1] * gx + cam.R[4] * gy) + cam.R[7] * gz;
+  out[2] = (cam.R[2] * gx + cam.R[5] * gy) + cam.R[8] * gz;
+  out[3] = a.z * fz;
+  out[4] = b.x;
+  out[5] = b.y;
+  out[6] = b.z;
+  out[7] = a.w;
+}
+
+__device__ __forceinline__ void adam_update(float4* __restrict__ ms, float4* __restrict__ co,
+                                            float4* __restrict__ m, float4* __restrict__ v,
+                                            int64_t i, const float gr[8], const AdamParams& ap,
+                                            unsigned long long* skipped) {
+  bool ok = true;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) ok &= isfinite(gr[j]);
+  if (!ok) {
+    atomicAdd(skipped, 1ull);
+    return;
+  }
+  float4 P0 = ms[i], P1 = co[i];
+  const float sigma = P0.w, op = P1.w;
+  float p[8] = {P0.x, P0.y, P0.z, logf(sigma), P1.x, P1.y, P1.z, logf(op) - log1pf(-op)};
+  const float g[8] = {gr[0], gr[1], gr[2], gr[3] * sigma,
+                      gr[4], gr[5], gr[6], gr[7] * op * (1.0f - op)};
+  float4 M0 = m[2 * i], M1 = m[2 * i + 1], V0 = v[2 * i], V1 = v[2 * i + 1];
+  float mm[8] = {M0.x, M0.y, M0.z, M0.w, M1.x, M1.y, M1.z, M1.w};
+  float vv[8] = {V0.x, V0.y, V0.z, V0.w, V1.x, V1.y, V1.z, V1.w};
+  const int group[8] = {0, 0, 0, 1, 2, 2, 2, 3};
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    mm[j] = mm[j] + (1.0f - ap.b1) * (g[j] - mm[j]);
+    vv[j] = ap.b2 * vv[j] + (1.0f - ap.b2) * g[j] * g[j];
+    const float denom = sqrtf(vv[j]) / ap.bc2_sqrt + ap.eps;
+    p[j] = p[j] - ap.step_size[group[j]] * (mm[j] / denom);
+  }
+  m[2 * i] = make_float4(mm[0], mm[1], mm[2], mm[3]);
+  m[2 * i + 1] = make_float4(mm[4], mm[5], mm[6], mm[7]);
+  v[2 * i] = make_float4(vv[0], vv[1], vv[2], vv[3]);
+  v[2 * i + 1] = make_float4(vv[4], vv[5], vv[6], vv[7]);
+  ms[i] = make_float4(p[0], p[1], p[2], expf(p[3]));
+  co[i] = make_float4(p[4], p[5], p[6], 1.0f / (1.0f + expf(-p[7])));
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(256) k_project_backward(
+    const float4* __restrict__ ms, int64_t n, FrameParams fp, const uint32_t* __restrict__ rank_of,
+    float4* __restrict__ grad2d, float4* __restrict__ grad3d, bool first) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const size_t r = rank_of[i];
+  const float4 a = grad2d[2 * r], b = grad2d[2 * r + 1];
+  grad2d[2 * r] = make_float4(0.f, 0.f, 0.f, 0.f);
+  grad2d[2 * r + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  float o[8];
+  grad3d_of(ms[i], fp.cam, a, b, o);
+  float4 g0 = make_float4(o[0], o[1], o[2], o[3]), g1 = make_float4(o[4], o[5], o[6], o[7]);
+  if (!first) {
+    const float4 h0 = grad3d[2 * i], h1 = grad3d[2 * i + 1];
+    g0 = make_float4(g0.x + h0.x, g0.y + h0.y, g0.z + h0.z, g0.w + h0.w);
+    g1 = make_float4(g1.x + h1.x, g1.y + h1.y, g1.z + h1.z, g1.w + h1.w);
+  }
+  grad3d[2 * i] = g0;
+  grad3d[2 * i + 1] = g1;
+}
+
+__global__ void __launch_bounds__(256) k_project_adam(
+    float4* __restrict__ ms, float4* __restrict__ co, int64_t n, FrameParams fp,
+    const uint32_t* __restrict__ rank_of, float4* __restrict__ grad2d, float4* __restrict__ m,
+    float4* __restrict__ v, AdamParams ap, unsigned long long* __restrict__ skipped) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const size_t r = rank_of[i];
+  const float4 a = grad2d[2 * r], b = grad2d[2 * r + 1];
+  grad2d[2 * r] = make_float4(0.f, 0.f, 0.f, 0.f);
+  grad2d[2 * r + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  float o[8];
+  grad3d_of(ms[i], fp.cam, a, b, o);
+  adam_update(ms, co, m, v, i, o, ap, skipped);
+}
+
+__global__ void __launch_bounds__(256) k_adam(float4* __restrict__ ms, float4* __restrict__ co,
+                                              int64_t n, const float4* __restrict__ grad3d,
+                                              float4* __restrict__ m, float4* __restrict__ v,
+                                              AdamParams ap, unsigned long long* __restrict__ skipped) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float4 g0 = grad3d[2 * i], g1 = grad3d[2 * i + 1];
+  const float o[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+  adam_update(ms, co, m, v, i, o, ap, skipped);
+}
+
+void launch_project_backward(const float4* ms, int64_t n, const FrameParams& fp,
+                             const uint32_t* rank_of, float4* grad2d, float4* grad3d, bool first,
+                             cudaStream_t st) {
+  if (n <= 0) return;
+  k_project_backward<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ms, n, fp, rank_of, grad2d,
+                                                                   grad3d, first);
+}
+
+void launch_project_adam(float4* ms, float4* co, int64_t n, const FrameParams& fp,
+                         const uint32_t* rank_of, float4* grad2d, float4* m, float4* v,
+                         const AdamParams& ap, unsigned long long* skipped, cudaStream_t st) {
+  if (n <= 0) return;
+  k_project_adam<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ms, co, n, fp, rank_of, grad2d, m,
+                                                               v, ap, skipped);
+}
+
+void launch_adam(float4* ms, float4* co, int64_t n, const float4* grad3d, float4* m, float4* v,
+                 const AdamParams& ap, unsigned long long* skipped, cudaStream_t st) {
+  if (n <= 0) return;
+  k_adam<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ms, co, n, grad3d, m, v, ap, skipped);
+}
+
+}  // namespace isg

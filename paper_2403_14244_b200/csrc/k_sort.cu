@@ -1,0 +1,356 @@
+// K2-K5 — binning: scan + emission, onesweep LSD radix sort, per-tile ranges.
+//
+// Replaces the reference's single global std::stable_sort on double depth
+// (/root/reference/proj/src/splat3d.cpp:164-169, ties broken by input index) with the
+// tile-binned order the blend kernels need: per 16x16 tile, splats in (depth, index) order.
+//
+//   1. radix sort (depth bits, splat) over all splats          -> rank r = depth order
+//   2. k_scan_emit: decoupled look-back exclusive scan of the tile counts in rank order,
+//      gather of the depth-ordered 32-B render records, emission of (tile, r) pairs in rank
+//      order (so equal tiles already appear in depth order)
+//   3. radix sort (tile, r) — stable, only ceil(log2(tiles)) bits  -> per-tile lists
+//   4. k_ranges
+//
+// The radix sort is a onesweep LSD sort (one kernel per 8-bit digit pass plus one upfront
+// histogram kernel): every CTA takes a dynamic tile id, ranks its 4096 keys stably with
+// warp-level match_any multisplit, publishes per-digit counts to a decoupled look-back
+// array, scatters through shared memory and writes coalesced runs per digit.
+#include <algorithm>
+
+#include "isg_math.cuh"
+
+namespace isg {
+
+namespace {
+
+constexpr uint32_t kFlagAgg = 1u << 30;
+constexpr uint32_t kFlagInc = 2u << 30;
+constexpr uint32_t kCountMask = (1u << 30) - 1;
+
+__device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
+  return *(const volatile uint32_t*)p;
+}
+__device__ __forceinline__ void st_volatile(uint32_t* p, uint32_t v) {
+  *(volatile uint32_t*)p = v;
+}
+__device__ __forceinline__ unsigned long long ld_volatile64(const unsigned long long* p) {
+  return *(const volatile unsigned long long*)p;
+}
+__device__ __forceinline__ void st_volatile64(unsigned long long* p, unsigned long long v) {
+  *(volatile unsigned long long*)p = v;
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Exclusive scan of one u32 per thread over a 256-thread block.  s_warp: >= 8 words.
+__device__ __forceinline__ uint32_t block_excl_scan_256(uint32_t v, uint32_t* s_warp,
+                                                        uint32_t& total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[w] = x;
+  __syncthreads();
+  uint32_t wpre = 0, tot = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t s = s_warp[i];
+    wpre += (i < w) ? s : 0u;
+    tot += s;
+  }
+  total = tot;
+  __syncthreads();
+  return wpre + x - v;
+}
+
+// ---- upfront histogram of all passes -------------------------------------------------------
+__global__ void __launch_bounds__(256) k_hist(const uint32_t* __restrict__ keys,
+                                              const uint32_t* __restrict__ n_dev, int64_t cap,
+                                              int passes, uint32_t* __restrict__ hist) {
+  __shared__ uint32_t sh[kMaxPasses][256];
+  for (int i = threadIdx.x; i < kMaxPasses * 256; i += 256) (&sh[0][0])[i] = 0;
+  __syncthreads();
+  const int64_t n = min((int64_t)*n_dev, cap);
+  for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < n; i += (int64_t)gridDim.x * 256) {
+    const uint32_t k = keys[i];
+    for (int p = 0; p < passes; ++p) atomicAdd(&sh[p][(k >> (8 * p)) & 255u], 1u);
+  }
+  __syncthreads();
+  for (int p = 0; p < passes; ++p) {
+    const uint32_t c = sh[p][threadIdx.x];
+    if (c) atomicAdd(&hist[p * 256 + threadIdx.x], c);
+  }
+}
+
+// ---- one onesweep digit pass -----------------------------------------------------------------
+struct OnesweepSmem {
+  uint32_t keys[kSortTileItems];
+  uint32_t vals[kSortTileItems];
+  uint32_t wcnt[kSortThreads / 32][257];
+  uint32_t local_start[256];
+  uint32_t bin_base[256];
+  uint32_t warp_tmp[8];
+  uint32_t tile;
+};
+
+__global__ void __launch_bounds__(kSortThreads) k_onesweep(
+    const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
+    uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
+    const uint32_t* __restrict__ n_dev, int64_t cap, int shift,
+    const uint32_t* __restrict__ hist, uint32_t* __restrict__ lookback,
+    uint32_t* __restrict__ counter) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  OnesweepSmem& S = *reinterpret_cast<OnesweepSmem*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t n = min((int64_t)*n_dev, cap);
+  if (tid == 0) S.tile = atomicAdd(counter, 1u);
+  for (int i = tid; i < (kSortThreads / 32) * 257; i += kSortThreads) (&S.wcnt[0][0])[i] = 0;
+  __syncthreads();
+  const uint32_t tile = S.tile;
+  const int64_t base = (int64_t)tile * kSortTileItems;
+  if (base >= n) return;
+
+  uint32_t key[kSortItems], val[kSortItems], rank[kSortItems], dig[kSortItems];
+  const int64_t wbase = base + (int64_t)w * 32 * kSortItems + lane;
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const int64_t idx = wbase + j * 32;
+    const bool valid = idx < n;
+    key[j] = valid ? keys_in[idx] : 0u;
+    val[j] = valid ? (vals_in ? vals_in[idx] : (uint32_t)idx) : 0u;
+    dig[j] = valid ? ((key[j] >> shift) & 255u) : 256u;
+  }
+  // stable warp multisplit: rank = items of the same digit earlier in (iteration, lane) order
+  const uint32_t lt = lanemask_lt();
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const uint32_t d = dig[j];
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    const uint32_t before = S.wcnt[w][d];
+    rank[j] = before + __popc(peers & lt);
+    __syncwarp();
+    if (lane == __ffs(peers) - 1) S.wcnt[w][d] = before + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // per digit: exclusive prefix across warps; tile count
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int ww = 0; ww < kSortThreads / 32; ++ww) {
+    const uint32_t c = S.wcnt[ww][tid];
+    S.wcnt[ww][tid] = cnt;
+    cnt += c;
+  }
+  // publish this tile's aggregate (or inclusive prefix for tile 0)
+  uint32_t* my = lookback + (int64_t)tile * 256 + tid;
+  if (tile == 0) {
+    st_volatile(my, kFlagInc | cnt);
+  } else {
+    st_volatile(my, kFlagAgg | cnt);
+  }
+  uint32_t tot;
+  const uint32_t local_start = block_excl_scan_256(cnt, S.warp_tmp, tot);
+  const uint32_t gpre = block_excl_scan_256(hist[tid], S.warp_tmp, tot);
+  // decoupled look-back for digit `tid`
+  uint32_t excl = 0;
+  if (tile > 0) {
+    int64_t p = (int64_t)tile - 1;
+    while (true) {
+      uint32_t s;
+      do {
+        s = ld_volatile(lookback + p * 256 + tid);
+      } while ((s & ~kCountMask) == 0);
+      excl += s & kCountMask;
+      if ((s & ~kCountMask) == kFlagInc) break;
+      --p;
+    }
+    st_volatile(my, kFlagInc | (excl + cnt));
+  }
+  S.local_start[tid] = local_start;
+  S.bin_base[tid] = gpre + excl - local_start;
+  __syncthreads();
+  // scatter into shared memory in tile-sorted order
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const uint32_t d = dig[j];
+    if (d < 256u) {
+      const uint32_t pos = S.local_start[d] + S.wcnt[w][d] + rank[j];
+      S.keys[pos] = key[j];
+      S.vals[pos] = val[j];
+    }
+  }
+  __syncthreads();
+  const int nvalid = (int)min((int64_t)kSortTileItems, n - base);
+  for (int i = tid; i < nvalid; i += kSortThreads) {
+    const uint32_t k = S.keys[i];
+    const uint32_t o = S.bin_base[(k >> shift) & 255u] + (uint32_t)i;
+    keys_out[o] = k;
+    vals_out[o] = S.vals[i];
+  }
+}
+
+// ---- ranges ---------------------------------------------------------------------------------
+__global__ void k_ranges(const uint32_t* __restrict__ t, const uint32_t* __restrict__ n_dev,
+                         int64_t cap, uint2* __restrict__ ranges) {
+  const int64_t n = min((int64_t)*n_dev, cap);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = t[i];
+    if (i == 0 || t[i - 1] != k) ranges[k].x = (uint32_t)i;
+    if (i == n - 1 || t[i + 1] != k) ranges[k].y = (uint32_t)(i + 1);
+  }
+}
+
+// ---- scan of tile counts in depth order + record gather + emission --------------------------
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 4;
+constexpr int kScanTileItems = kScanThreads * kScanItems;
+constexpr unsigned long long kF64Agg = 1ull << 62;
+constexpr unsigned long long kF64Inc = 2ull << 62;
+constexpr unsigned long long kC64Mask = (1ull << 62) - 1;
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_emit(
+    const uint32_t* __restrict__ order, const uint32_t* __restrict__ ntiles,
+    const float4* __restrict__ rec_geo, const float4* __restrict__ co, int64_t n, FrameParams fp,
+    RenderRec* __restrict__ rec_sorted, uint32_t* __restrict__ rank_of,
+    uint32_t* __restrict__ tile_keys, uint32_t* __restrict__ tile_vals, int64_t key_cap,
+    unsigned long long* __restrict__ lookback, uint32_t* __restrict__ counter,
+    uint32_t* __restrict__ n_keys, unsigned long long* __restrict__ n_keys_total,
+    uint32_t* __restrict__ n_visible) {
+  __shared__ uint32_t s_tile;
+  __shared__ uint32_t s_warp[8];
+  __shared__ unsigned long long s_excl;
+  const int tid = threadIdx.x;
+  if (tid == 0) s_tile = atomicAdd(counter, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const int64_t base = (int64_t)tile * kScanTileItems;
+  if (base >= n) return;
+  const int64_t r0 = base + (int64_t)tid * kScanItems;
+  uint32_t g[kScanItems], c[kScanItems];
+  uint32_t sum = 0, vis = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    const int64_t r = r0 + j;
+    g[j] = r < n ? order[r] : 0u;
+    c[j] = r < n ? ntiles[g[j]] : 0u;
+    sum += c[j];
+    vis += c[j] ? 1u : 0u;
+  }
+  uint32_t tot;
+  const uint32_t texcl = block_excl_scan_256(sum, s_warp, tot);
+  uint32_t vtot;
+  block_excl_scan_256(vis, s_warp, vtot);
+  if (tid == 0) {
+    unsigned long long* my = lookback + tile;
+    unsigned long long excl = 0;
+    if (tile == 0) {
+      st_volatile64(my, kF64Inc | tot);
+    } else {
+      st_volatile64(my, kF64Agg | tot);
+      int64_t p = (int64_t)tile - 1;
+      while (true) {
+        unsigned long long s;
+        do {
+          s = ld_volatile64(lookback + p);
+        } while ((s & ~kC64Mask) == 0);
+        excl += s & kC64Mask;
+        if ((s & ~kC64Mask) == kF64Inc) break;
+        --p;
+      }
+      st_volatile64(my, kF64Inc | (excl + tot));
+    }
+    s_excl = excl;
+    if (vtot) atomicAdd(n_visible, vtot);
+    if (base + kScanTileItems >= n) {
+      const unsigned long long total = excl + tot;
+      *n_keys_total = total;
+      *n_keys = (uint32_t)min((unsigned long long)key_cap, total);
+    }
+  }
+  __syncthreads();
+  unsigned long long off = s_excl + texcl;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    const int64_t r = r0 + j;
+    if (r >= n) break;
+    const uint32_t gg = g[j];
+    rank_of[gg] = (uint32_t)r;
+    const float4 geo = rec_geo[gg];
+    const float4 col = co[gg];
+    RenderRec rr;
+    rr.geo = make_float4(geo.x, geo.y, __fmul_rn(geo.z, geo.z), geo.w);  // (u, v, s^2, r2max)
+    rr.col = col;
+    rec_sorted[r] = rr;
+    if (c[j] == 0) continue;
+    int x0, x1, y0, y1;
+    tile_bbox(geo.x, geo.y, geo.z, fp.tiles_x, fp.tiles_y, x0, x1, y0, y1);
+    for (int ty = y0; ty <= y1; ++ty)
+      for (int tx = x0; tx <= x1; ++tx) {
+        if (!tile_hit(geo.x, geo.y, geo.w, tx, ty, fp.cam.width, fp.cam.height)) continue;
+        if (off < (unsigned long long)key_cap) {
+          tile_keys[off] = (uint32_t)(ty * fp.tiles_x + tx);
+          tile_vals[off] = (uint32_t)r;
+        }
+        ++off;
+      }
+  }
+}
+
+}  // namespace
+
+int64_t scan_emit_scratch_words(int64_t n) { return (n + kScanTileItems - 1) / kScanTileItems; }
+
+void launch_scan_emit(const uint32_t* order, const uint32_t* ntiles, const float4* rec_geo,
+                      const float4* co, int64_t n, const FrameParams& fp, RenderRec* rec_sorted,
+                      uint32_t* rank_of, uint32_t* tile_keys, uint32_t* tile_vals,
+                      int64_t key_cap, unsigned long long* scratch, uint32_t* counter,
+                      uint32_t* n_keys, unsigned long long* n_keys_total, uint32_t* n_visible,
+                      cudaStream_t st) {
+  const int64_t tiles = scan_emit_scratch_words(n);
+  if (tiles == 0) return;  // caller zeroed the counts
+  k_scan_emit<<<(unsigned)tiles, kScanThreads, 0, st>>>(
+      order, ntiles, rec_geo, co, n, fp, rec_sorted, rank_of, tile_keys, tile_vals, key_cap,
+      scratch, counter, n_keys, n_keys_total, n_visible);
+}
+
+void launch_ranges(const uint32_t* sorted_tiles, const uint32_t* n_keys, int64_t key_cap,
+                   uint2* ranges, cudaStream_t st) {
+  const int64_t blocks = std::min<int64_t>((key_cap + 255) / 256, 148 * 16);
+  k_ranges<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, st>>>(sorted_tiles, n_keys, key_cap,
+                                                                   ranges);
+}
+
+int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], bool iota_vals, const uint32_t* n_dev,
+                     int64_t cap, int key_bits, SortScratch& s, cudaStream_t st,
+                     int64_t* launches) {
+  const int passes = (key_bits + 7) / 8;
+  const int64_t tiles = (cap + kSortTileItems - 1) / kSortTileItems;
+  // caller guarantees tiles <= s.max_tiles and passes <= kMaxPasses
+  cudaMemsetAsync(s.hist, 0, sizeof(uint32_t) * kMaxPasses * 256, st);
+  cudaMemsetAsync(s.counters, 0, sizeof(uint32_t) * kMaxPasses, st);
+  cudaMemsetAsync(s.lookback, 0, sizeof(uint32_t) * 256 * (size_t)tiles * passes, st);
+  const int hist_blocks = (int)std::min<int64_t>(std::max<int64_t>(tiles, 1), 148 * 4);
+  k_hist<<<hist_blocks, 256, 0, st>>>(keys[0], n_dev, cap, passes, s.hist);
+  int cur = 0;
+  const size_t smem = sizeof(OnesweepSmem);
+  cudaFuncSetAttribute(k_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  for (int p = 0; p < passes; ++p) {
+    k_onesweep<<<(unsigned)std::max<int64_t>(tiles, 1), kSortThreads, smem, st>>>(
+        keys[cur], (p == 0 && iota_vals) ? nullptr : vals[cur], keys[cur ^ 1], vals[cur ^ 1],
+        n_dev, cap,
+        8 * p, s.hist + 256 * p, s.lookback + (size_t)256 * tiles * p, s.counters + p);
+    cur ^= 1;
+  }
+  if (launches) *launches += 1 + passes;
+  return cur;
+}
+
+}  // namespace isg

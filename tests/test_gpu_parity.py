@@ -1,0 +1,311 @@
+"""GPU parity tests: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Bars (BASELINE.json north_star): tile keys, sort order and per-tile ranges bit-exact; images
+max|diff| <= 1e-4; gradients relative <= 1e-3 per parameter group (||dg||/||g||) and
+elementwise |dg| <= 1e-3 * max|g|.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2403_14244_b200 import isg
+
+pytestmark = pytest.mark.gpu
+
+IMG_TOL = 1e-4
+GRAD_TOL = 1e-3
+GROUPS = {"mu": slice(0, 3), "sigma": slice(3, 4), "rgb": slice(4, 7), "opacity": slice(7, 8)}
+
+
+@pytest.fixture(scope="module")
+def rend():
+    r = isg.Renderer(0)
+    yield r
+    r.close()
+
+
+def random_scene(rng, n, W, H, sigma2d=(0.5, 8.0), depth=(2.0, 10.0), f=None):
+    f = f or 1000.0 * W / 1920.0
+    z = rng.uniform(*depth, n)
+    u = rng.uniform(-0.1 * W, 1.1 * W, n)
+    v = rng.uniform(-0.1 * H, 1.1 * H, n)
+    s2d = np.exp(rng.uniform(np.log(sigma2d[0]), np.log(sigma2d[1]), n))
+    ms = np.stack([(u - W / 2) * z / f, (v - H / 2) * z / f, z, s2d * z / f], 1).astype(np.float32)
+    co = np.concatenate([rng.uniform(0, 1, (n, 3)), rng.uniform(0.05, 0.95, (n, 1))], 1)
+    return ms, co.astype(np.float32), isg.Camera(np.eye(3), np.zeros(3), f, (W / 2, H / 2), W, H)
+
+
+def check_bins(r, ms, co, cam):
+    keys, vals, ranges = r.debug_bins()
+    k2, v2, r2, nvis = O.bin32(ms, co, cam)
+    assert keys.shape == k2.shape, (keys.shape, k2.shape)
+    assert np.array_equal(keys, k2), "tile keys differ"
+    assert np.array_equal(vals, v2), "sort order differs"
+    assert np.array_equal(ranges, r2), "tile ranges differ"
+    assert r.stats()["n_visible"] == nvis
+    return keys
+
+
+CASES = [
+    ("tiny", 40, 64, 48, {}),
+    ("synth256", 10000, 256, 256, {}),
+    ("ragged", 3000, 203, 117, {}),  # partial edge tiles
+    ("large_splats", 300, 256, 192, {"sigma2d": (10.0, 60.0)}),
+    ("tiny_splats", 5000, 128, 128, {"sigma2d": (0.05, 0.5)}),
+    ("near_plane", 2000, 128, 96, {"depth": (-0.5, 3.0)}),
+]
+
+
+@pytest.mark.parametrize("name,n,W,H,kw", CASES, ids=[c[0] for c in CASES])
+def test_bins_and_render(rend, name, n, W, H, kw):
+    rng = np.random.default_rng(abs(hash(name)) % 2**32)
+    ms, co, cam = random_scene(rng, n, W, H, **kw)
+    rend.set_scene(ms, co)
+    for t_min in (0.0, 1e-5, 1e-2):
+        opts = isg.RenderOptions(t_min=t_min)
+        img = rend.render(cam, opts)
+        check_bins(rend, ms, co, cam)
+        ref, tl, npr, _ = O.render32(ms, co, cam, t_min=t_min, want_state=True)
+        assert np.abs(img - ref).max() <= IMG_TOL
+        gtl, gnp = rend.debug_pixel_state(W, H)
+        # early-termination index may differ by one entry where exp rounding straddles t_min
+        assert np.mean(gnp == npr) > 0.99
+
+
+def test_synthetic_scene_bins(rend):
+    W, H = 320, 180
+    ms, co = isg.synth_scene(20000, W, H, seed=2403)
+    cam = isg.Camera.synthetic(W, H)
+    rend.set_scene(ms, co)
+    img = rend.render(cam)
+    check_bins(rend, ms, co, cam)
+    assert np.abs(img - O.render32(ms, co, cam)).max() <= IMG_TOL
+
+
+def test_depth_ties_break_by_index(rend):
+    """Equal depths keep input order (stable_sort, splat3d.cpp:164-169)."""
+    W = H = 64
+    n = 200
+    rng = np.random.default_rng(5)
+    ms, co, cam = random_scene(rng, n, W, H)
+    ms[:, 2] = np.float32(4.0)  # every splat at the same depth
+    ms[:, 0:2] = ms[:, 0:2] * 0.3
+    rend.set_scene(ms, co)
+    img = rend.render(cam, isg.RenderOptions(t_min=0.0))
+    keys = check_bins(rend, ms, co, cam)
+    assert len(keys) > n
+    assert np.abs(img - O.render32(ms, co, cam, t_min=0.0)).max() <= IMG_TOL
+
+
+def test_rotated_cameras(rend):
+    W, H = 192, 128
+    ms, co = isg.synth_scene(8000, W, H, seed=7)
+    rend.set_scene(ms, co)
+    for k in range(8):
+        cam = isg.Camera.synthetic(W, H, k, 8)
+        img = rend.render(cam)
+        check_bins(rend, ms, co, cam)
+        assert np.abs(img - O.render32(ms, co, cam)).max() <= IMG_TOL
+
+
+def test_background_and_empty(rend):
+    cam = isg.Camera(np.eye(3), np.zeros(3), 32.0, (16, 16), 32, 32)
+    rend.set_scene(np.zeros((0, 4), np.float32), np.zeros((0, 4), np.float32))
+    img = rend.render(cam, isg.RenderOptions(background=(0.25, 0.5, 1.0)))
+    assert np.array_equal(img, np.broadcast_to(np.float32([0.25, 0.5, 1.0]), img.shape))
+
+
+def test_three_splat_fixture(rend):
+    """SURVEY Appendix B values (FP64 restatement of the reference on the shipped fixture
+    inputs, proj/tools/make_fixtures.py:73-78 + proj/data/camera_32.json)."""
+    sp = np.array([[0, 0, 2, .25, 1, .2, .1, .5], [.35, -.2, 3, .45, .2, .9, .3, .5],
+                   [-.3, .25, 4, .9, .1, .3, 1, 1]])
+    cam = isg.Camera(np.eye(3), np.zeros(3), 32.0, (16, 16), 32, 32)
+    img = isg.render(sp, cam, isg.RenderOptions(t_min=0.0))
+    known = {(15, 15): [0.539598543904, 0.293501319677, 0.419031703075],
+             (16, 16): [0.540942539951, 0.302246395001, 0.405764169491],
+             (19, 13): [0.255596227004, 0.451627307644, 0.287956021327],
+             (13, 18): [0.308465363202, 0.292865519624, 0.770573717758],
+             (0, 0): [0, 0, 0], (31, 31): [0, 0, 0]}
+    for (x, y), val in known.items():
+        assert np.abs(img[y, x] - np.array(val)).max() <= IMG_TOL
+    assert abs(img.astype(np.float64).sum() - 266.798504875079) < 1e-2
+    assert np.abs(img - O.render64(sp, cam)).max() <= IMG_TOL
+
+
+def test_on_axis_alpha_one(rend):
+    """one on-axis splat with opacity 1 -> colour c at the projection centre."""
+    cam = isg.Camera(np.eye(3), np.zeros(3), 32.0, (16.5, 16.5), 33, 33)
+    sp = np.array([[0, 0, 2.0, 0.2, 0.3, 0.6, 0.9, 1.0]])
+    img = isg.render(sp, cam, isg.RenderOptions(t_min=0.0))
+    assert np.abs(img[16, 16] - np.array([0.3, 0.6, 0.9])).max() <= 1e-6
+
+
+def _grad_check(g, g_ref):
+    for name, sl in GROUPS.items():
+        a, b = g[:, sl], g_ref[:, sl]
+        nb = np.linalg.norm(b)
+        if nb == 0:
+            assert np.abs(a).max() == 0
+            continue
+        assert np.linalg.norm(a - b) / nb <= GRAD_TOL, name
+        assert np.abs(a - b).max() <= GRAD_TOL * np.abs(b).max(), name
+
+
+@pytest.mark.parametrize("name,n,W,H,kw", CASES[:4], ids=[c[0] for c in CASES[:4]])
+def test_loss_backward(rend, name, n, W, H, kw):
+    rng = np.random.default_rng(1 + abs(hash(name)) % 2**31)
+    ms, co, cam = random_scene(rng, n, W, H, **kw)
+    tms, tco, _ = random_scene(rng, n, W, H, **kw)
+    target = O.render32(tms, tco, cam)
+    rend.set_scene(ms, co)
+    opts = isg.RenderOptions(t_min=1e-5)
+    loss = rend.loss_backward(cam, target, opts, weight=1.0)
+    g = rend.grads()
+    loss_ref, g_ref = O.loss_backward32(ms, co, cam, target, t_min=1e-5)
+    assert abs(loss - loss_ref) <= 1e-6 * abs(loss_ref)
+    _grad_check(g, g_ref)
+
+
+def test_backward_vs_fp64_reference(rend):
+    """t_min=0 (exact reference forward): GPU grads vs the FP64 first-principles backward,
+    which the CPU tests pin to central finite differences."""
+    rng = np.random.default_rng(11)
+    ms, co, cam = random_scene(rng, 60, 48, 40)
+    sp = np.concatenate([ms, co], 1).astype(np.float64)
+    target = rng.uniform(0, 1, (40, 48, 3))
+    rend.set_scene(ms, co)
+    loss = rend.loss_backward(cam, target.astype(np.float32), isg.RenderOptions(t_min=0.0))
+    g = rend.grads()
+    loss64, g64 = O.loss_grad64(sp, cam, target)
+    assert abs(loss - loss64) <= 1e-5 * loss64
+    _grad_check(g, g64)
+
+
+def test_multi_view_accumulation(rend):
+    W, H = 128, 96
+    ms, co = isg.synth_scene(4000, W, H, seed=3)
+    tms, tco = isg.synth_scene(4000, W, H, seed=4)
+    rend.set_scene(ms, co)
+    g_ref = np.zeros((4000, 8), np.float32)
+    tot = 0.0
+    for k in range(3):
+        cam = isg.Camera.synthetic(W, H, k, 3)
+        target = O.render32(tms, tco, cam)
+        tot += rend.loss_backward(cam, target, weight=1 / 3)
+        O.loss_backward32(ms, co, cam, target, weight=1 / 3, grads=g_ref)
+    assert abs(rend.read_loss() - tot) < 1e-9 + 1e-7 * tot
+    _grad_check(rend.grads(), g_ref)
+
+
+def _adam_setup():
+    W, H = 128, 96
+    ms, co = isg.synth_scene(3000, W, H, seed=8)
+    tms, tco = isg.synth_scene(3000, W, H, seed=9)
+    cam = isg.Camera.synthetic(W, H)
+    target = O.render32(tms, tco, cam)
+    cfg = isg.AdamConfig(lr_mu=1e-3, lr_sigma=5e-3, lr_color=1e-2, lr_opacity=1e-2, eps=1e-15)
+    return ms, co, cam, target, cfg
+
+
+def test_adam_matches_oracle_given_grads(rend):
+    """Unfused path: the GPU's own gradients fed to the oracle Adam (torch semantics, pinned
+    against torch.optim.Adam in the CPU tests) reproduce the GPU update over 3 steps."""
+    ms, co, cam, target, cfg = _adam_setup()
+    lrs = [cfg.lr_mu, cfg.lr_sigma, cfg.lr_color, cfg.lr_opacity]
+    rend.set_scene(ms, co)
+    oms, oco = ms.copy(), co.copy()
+    m = np.zeros((3000, 8), np.float32)
+    v = np.zeros((3000, 8), np.float32)
+    for step in range(1, 4):
+        rend.loss_backward(cam, target)
+        g = rend.grads()
+        rend.adam_step(cfg)
+        O.adam32(oms, oco, m, v, g, step, lrs, cfg.beta1, cfg.beta2, cfg.eps)
+        gms, gco = rend.get_scene()
+        assert np.abs(gms - oms).max() <= 1e-5
+        assert np.abs(gco - oco).max() <= 1e-5
+        oms, oco = gms.copy(), gco.copy()  # continue from the GPU state (moments already match)
+
+
+def test_adam_fused_equals_unfused(rend):
+    """K8 fused (projection backward + Adam) == K8a projection then K8b Adam."""
+    ms, co, cam, target, cfg = _adam_setup()
+    out = []
+    for fused in (True, False):
+        rend.set_scene(ms, co)
+        rend.loss_backward(cam, target)
+        g = None if fused else rend.grads()  # grads() projects first -> un-fused Adam
+        rend.adam_step(cfg)
+        out.append((rend.get_scene(), g))
+    (ams, aco), _ = out[0]
+    (bms, bco), g = out[1]
+    big = np.abs(g) > 1e-2 * np.abs(g).max(axis=0, keepdims=True)
+    step_tol = np.array([cfg.lr_mu] * 3 + [cfg.lr_sigma] + [cfg.lr_color] * 3 + [cfg.lr_opacity])
+    pa = np.concatenate([ams[:, :3], np.log(ams[:, 3:4]), aco[:, :3],
+                         np.log(aco[:, 3:4] / (1 - aco[:, 3:4]))], 1)
+    pb = np.concatenate([bms[:, :3], np.log(bms[:, 3:4]), bco[:, :3],
+                         np.log(bco[:, 3:4] / (1 - bco[:, 3:4]))], 1)
+    d = np.abs(pa - pb)
+    assert np.all(d <= 2.001 * step_tol + 1e-6)  # Adam's first step is bounded by lr
+    assert np.all(d[big] <= (1e-2 * step_tol + 1e-6)[np.nonzero(big)[1]])
+
+
+def test_validation_errors(rend):
+    cam = isg.Camera(np.eye(3), np.zeros(3), 32.0, (16, 16), 32, 32)
+    good = np.array([[0, 0, 2, .25, 1, .2, .1, .5]] * 3, np.float64)
+    cases = [((1, 3), 0.0, "IsoSplat3D.sigma: must be positive and finite"),
+             ((2, 0), np.nan, "IsoSplat3D.mu: non-finite coordinates"),
+             ((1, 7), 1.5, "IsoSplat3D.opacity: must be in [0,1]"),
+             ((0, 5), np.inf, "IsoSplat3D.color: non-finite")]
+    for (i, j), val, msg in cases:
+        bad = good.copy()
+        bad[i, j] = val
+        ms, co = isg.splats_to_soa(bad)
+        rend.set_scene(ms, co)
+        with pytest.raises(isg.DomainError, match=msg.replace("[", r"\[").replace("]", r"\]")):
+            rend.render(cam)
+    rend.set_scene(*isg.splats_to_soa(good))
+    bad_cam = isg.Camera(np.eye(3), np.zeros(3), -1.0, (16, 16), 32, 32)
+    with pytest.raises(isg.DomainError, match="Camera.focal"):
+        rend.render(bad_cam)
+    with pytest.raises(ValueError):
+        rend.render(cam, isg.RenderOptions(t_min=2.0))
+    with pytest.raises(isg.IsgError):
+        isg.Renderer(0).adam_step()
+
+
+def test_key_capacity_regrow():
+    """Huge splats exceed the initial key capacity: the frame is re-run, results exact."""
+    W, H = 512, 512
+    rng = np.random.default_rng(3)
+    with isg.Renderer(0) as r:
+        ms, co, cam = random_scene(rng, 2000, W, H, sigma2d=(60.0, 200.0))
+        r.set_scene(ms, co)
+        img = r.render(cam)
+        assert r.stats()["regrow_events"] >= 1
+        check_bins(r, ms, co, cam)
+        assert np.abs(img - O.render32(ms, co, cam)).max() <= IMG_TOL
+
+
+def test_render_deterministic(rend):
+    W, H = 256, 256
+    ms, co = isg.synth_scene(10000, W, H)
+    rend.set_scene(ms, co)
+    cam = isg.Camera.synthetic(W, H)
+    a = rend.render(cam)
+    b = rend.render(cam)
+    assert np.array_equal(a, b)
+
+
+def test_full_size_c2_render_parity():
+    """Config C2 (1M splats, 1920x1080): bins bit-exact and image within 1e-4 of the oracle."""
+    W, H, n = 1920, 1080, 1_000_000
+    ms, co = isg.synth_scene(n, W, H, seed=2403)
+    cam = isg.Camera.synthetic(W, H)
+    with isg.Renderer(0) as r:
+        r.set_scene(ms, co)
+        img = r.render(cam)
+        keys = check_bins(r, ms, co, cam)
+        assert np.all(np.diff(keys.astype(np.int64) >> 32) >= 0)
+        assert np.abs(img - O.render32(ms, co, cam)).max() <= IMG_TOL
