@@ -176,7 +176,9 @@ def run_isg(args):
     n, W, H, views_total, train, desc = CONFIGS[args.config]
     views_per_rank = max(1, views_total // world) if args.config == "c4" else 1
     step_views = views_per_rank * world
-    stream = torch.cuda.current_stream()
+    # a real (non-legacy) stream: the context launches on it and the events below time it
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
 
     ms, co = isg.synth_scene(n, W, H, seed=2403)
     tms, tco = isg.synth_scene(n, W, H, seed=14244)

@@ -203,3 +203,66 @@ def adam32(ms, co, m, v, grads, step, lr, b1=0.9, b2=0.999, eps=1e-15):
     lib().or32_adam(ms.shape[0], _p(ms), _p(co), _p(m), _p(v), _p(g), step, _p(lrs), b1, b2, eps,
                     C.byref(skipped))
     return skipped.value
+
+
+# ---- the reference's own code (oracle/_ref, built by oracle/build_ref.sh) -----------------
+_ref = None
+
+
+def ref_lib():
+    global _ref
+    if _ref is None:
+        if not REF_LIB.exists():
+            raise RuntimeError("oracle/_ref/libisosplat_ref.so not built (needs /root/reference)")
+        L = C.CDLL(str(REF_LIB))
+        P, I64 = C.c_void_p, C.c_int64
+        L.ref_render.argtypes = [I64, P, P, C.c_int, C.c_int, P, C.c_int, P, C.c_char_p, C.c_int]
+        L.ref_render.restype = C.c_int
+        L.ref_project_iso.argtypes = [P, P, P, C.c_char_p, C.c_int]
+        L.ref_project_iso.restype = C.c_int
+        L.ref_composite.argtypes = [I64, P, P, C.c_char_p, C.c_int]
+        L.ref_composite.restype = C.c_int
+        L.ref_mse.argtypes = [C.c_int, C.c_int, P, P]
+        L.ref_mse.restype = C.c_double
+        _ref = L
+    return _ref
+
+
+def _ref_cam(camera):
+    return np.concatenate([np.asarray(camera.rotation, np.float64).reshape(9),
+                           np.asarray(camera.translation, np.float64).reshape(3),
+                           [float(camera.focal)], np.asarray(camera.principal_point, np.float64)])
+
+
+def ref_render(splats, camera, bg=(0, 0, 0), threads=1):
+    """The reference's isosplat::render (splat3d.cpp:173-194) on (n, 8) FP64 records."""
+    s = np.ascontiguousarray(splats, np.float64).reshape(-1, 8)
+    c = _ref_cam(camera)
+    b = np.asarray(bg, np.float64)
+    out = np.zeros((camera.height, camera.width, 3))
+    err = C.create_string_buffer(512)
+    st = ref_lib().ref_render(s.shape[0], _p(s), _p(c), camera.width, camera.height, _p(b),
+                              threads, _p(out), err, 512)
+    if st:
+        raise ValueError(err.value.decode())
+    return out
+
+
+def ref_project_iso(splat8, camera):
+    s = np.ascontiguousarray(splat8, np.float64)
+    c = _ref_cam(camera)
+    out = np.zeros(4)
+    err = C.create_string_buffer(512)
+    st = ref_lib().ref_project_iso(_p(s), _p(c), _p(out), err, 512)
+    if st < 0:
+        raise ValueError(err.value.decode())
+    return out if st else None
+
+
+def ref_composite(rgba):
+    a = np.ascontiguousarray(rgba, np.float64).reshape(-1, 4)
+    out = np.zeros(3)
+    err = C.create_string_buffer(512)
+    if ref_lib().ref_composite(a.shape[0], _p(a), _p(out), err, 512):
+        raise ValueError(err.value.decode())
+    return out

@@ -1,0 +1,117 @@
+// ref_capi.cpp — extern "C" wrappers around the REFERENCE's own hot-path code, compiled from
+// /root/reference/proj/src/{splat3d,image}.cpp by oracle/build_ref.sh into
+// oracle/_ref/libisosplat_ref.so.  TEST INFRASTRUCTURE ONLY (checker / CPU baseline).
+//
+// The calls go through the reference's public API unchanged:
+//   isosplat::render(std::span<const IsoSplat3D>, const Camera&, const RenderOptions&)
+//       include/isosplat/splat3d.hpp:96-97, src/splat3d.cpp:173-194
+//   isosplat::project_iso   splat3d.hpp:74, splat3d.cpp:59-64
+//   isosplat::composite     splat3d.hpp:85, splat3d.cpp:76-87
+//   isosplat::mse           image.hpp:40, image.cpp:50-58
+// Exceptions (std::domain_error) become a non-zero return plus the message.
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <span>
+#include <stdexcept>
+#include <utility>
+#include <vector>
+
+#include "isosplat/image.hpp"
+#include "isosplat/splat3d.hpp"
+
+namespace {
+isosplat::Camera make_camera(const double* c, int w, int h) {
+  isosplat::Camera cam;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) cam.rotation(i, j) = c[3 * i + j];
+  for (int i = 0; i < 3; ++i) cam.translation[i] = c[9 + i];
+  cam.focal = c[12];
+  cam.principal_point[0] = c[13];
+  cam.principal_point[1] = c[14];
+  cam.width = w;
+  cam.height = h;
+  return cam;
+}
+
+std::vector<isosplat::IsoSplat3D> make_splats(int64_t n, const double* s) {
+  std::vector<isosplat::IsoSplat3D> v(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) {
+    const double* r = s + 8 * i;
+    v[i].mu = Eigen::Vector3d(r[0], r[1], r[2]);
+    v[i].sigma = r[3];
+    v[i].color = Eigen::Vector3d(r[4], r[5], r[6]);
+    v[i].opacity = r[7];
+  }
+  return v;
+}
+
+int report(const std::exception& e, char* err, int len) {
+  if (err && len > 0) {
+    std::strncpy(err, e.what(), static_cast<size_t>(len) - 1);
+    err[len - 1] = 0;
+  }
+  return dynamic_cast<const std::domain_error*>(&e) ? 1 : 2;
+}
+}  // namespace
+
+extern "C" {
+
+// cam: R (row-major 9), t (3), focal, cx, cy.  out: H x W x 3 doubles.
+int ref_render(int64_t n, const double* splats, const double* cam, int w, int h, const double* bg,
+               int threads, double* out, char* err, int errlen) {
+  try {
+    const auto sp = make_splats(n, splats);
+    isosplat::RenderOptions opt;
+    opt.background = Eigen::Vector3d(bg[0], bg[1], bg[2]);
+    opt.threads = threads;
+    const isosplat::ImageGrid img =
+        isosplat::render(std::span<const isosplat::IsoSplat3D>(sp), make_camera(cam, w, h), opt);
+    std::memcpy(out, img.data.data(), sizeof(double) * img.data.size());
+    return 0;
+  } catch (const std::exception& e) {
+    return report(e, err, errlen);
+  }
+}
+
+// Returns 1 and (u, v, sigma2d, depth) when visible, 0 when culled, -1 on domain error.
+int ref_project_iso(const double* splat, const double* cam, double* out, char* err, int errlen) {
+  try {
+    const auto sp = make_splats(1, splat);
+    const auto p = isosplat::project_iso(sp[0], make_camera(cam, 1, 1));
+    if (!p) return 0;
+    out[0] = p->mu2d[0];
+    out[1] = p->mu2d[1];
+    out[2] = p->sigma2d;
+    out[3] = p->depth;
+    return 1;
+  } catch (const std::exception& e) {
+    report(e, err, errlen);
+    return -1;
+  }
+}
+
+int ref_composite(int64_t n, const double* rgba, double* out, char* err, int errlen) {
+  try {
+    std::vector<std::pair<Eigen::Vector3d, double>> v;
+    for (int64_t i = 0; i < n; ++i)
+      v.emplace_back(Eigen::Vector3d(rgba[4 * i], rgba[4 * i + 1], rgba[4 * i + 2]), rgba[4 * i + 3]);
+    const Eigen::Vector3d c =
+        isosplat::composite(std::span<const std::pair<Eigen::Vector3d, double>>(v));
+    out[0] = c[0];
+    out[1] = c[1];
+    out[2] = c[2];
+    return 0;
+  } catch (const std::exception& e) {
+    return report(e, err, errlen);
+  }
+}
+
+double ref_mse(int w, int h, const double* a, const double* b) {
+  isosplat::ImageGrid x(w, h, 3), y(w, h, 3);
+  std::memcpy(x.data.data(), a, sizeof(double) * x.data.size());
+  std::memcpy(y.data.data(), b, sizeof(double) * y.data.size());
+  return isosplat::mse(x, y);
+}
+
+}  // extern "C"

@@ -299,11 +299,13 @@ isg_status flush_pending(isg_ctx* ctx) {
   return ISG_OK;
 }
 
-// Launch one frame: K1, depth sort, scan/emit, tile sort, ranges, K6 into `out`.
+// Launch one frame: K1, depth sort, scan/emit, tile sort, ranges, K6 into `out` (nullptr =
+// the context's own image buffer, resolved after it is sized for this camera).
 isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out) {
   isg_status s = flush_pending(ctx);
   if (s != ISG_OK) return s;
   if ((s = ensure_pixels(ctx, fp.cam.width, fp.cam.height)) != ISG_OK) return s;
+  if (!out) out = ctx->img;
   if (ctx->key_cap == 0) {
     if ((s = ensure_keys(ctx, std::max<int64_t>(6 * ctx->n, 1 << 20))) != ISG_OK) return s;
   }
@@ -641,7 +643,7 @@ isg_status isg_render(isg_ctx* ctx, const isg_camera* cam, const float bg[3], fl
   if (s != ISG_OK) return s;
   const FrameParams fp = make_fp(cam, bg, t_min);
   for (int attempt = 0; attempt < 3; ++attempt) {
-    if ((s = launch_frame(ctx, fp, ctx->img)) != ISG_OK) return s;
+    if ((s = launch_frame(ctx, fp, nullptr)) != ISG_OK) return s;
     bool ov = false;
     if ((s = check_frame(ctx, &ov)) != ISG_OK) return s;
     if (ov) continue;
@@ -663,7 +665,7 @@ isg_status isg_loss_backward_device(isg_ctx* ctx, const isg_camera* cam, const f
   isg_status s = validate_camera(ctx, cam);
   if (s != ISG_OK) return s;
   const FrameParams fp = make_fp(cam, bg, t_min);
-  if ((s = launch_frame(ctx, fp, ctx->img)) != ISG_OK) return s;
+  if ((s = launch_frame(ctx, fp, nullptr)) != ISG_OK) return s;
   return run_backward(ctx, fp, target_dev, weight);
 }
 
@@ -681,7 +683,7 @@ isg_status isg_loss_backward(isg_ctx* ctx, const isg_camera* cam, const float bg
   ISG_CUDA(cudaMemcpyAsync(ctx->target, target, sizeof(float) * 3 * (size_t)cam->width * cam->height,
                            cudaMemcpyHostToDevice, ctx->stream));
   for (int attempt = 0; attempt < 3; ++attempt) {
-    if ((s = launch_frame(ctx, fp, ctx->img)) != ISG_OK) return s;
+    if ((s = launch_frame(ctx, fp, nullptr)) != ISG_OK) return s;
     if ((s = run_backward(ctx, fp, ctx->target, weight)) != ISG_OK) return s;
     bool ov = false;
     if ((s = check_frame(ctx, &ov)) != ISG_OK) return s;

@@ -30,7 +30,7 @@ def random_scene(rng, n, W, H, sigma2d=(0.5, 8.0), depth=(2.0, 10.0), f=None):
     u = rng.uniform(-0.1 * W, 1.1 * W, n)
     v = rng.uniform(-0.1 * H, 1.1 * H, n)
     s2d = np.exp(rng.uniform(np.log(sigma2d[0]), np.log(sigma2d[1]), n))
-    ms = np.stack([(u - W / 2) * z / f, (v - H / 2) * z / f, z, s2d * z / f], 1).astype(np.float32)
+    ms = np.stack([(u - W / 2) * z / f, (v - H / 2) * z / f, z, s2d * np.maximum(np.abs(z), 0.05) / f], 1).astype(np.float32)
     co = np.concatenate([rng.uniform(0, 1, (n, 3)), rng.uniform(0.05, 0.95, (n, 1))], 1)
     return ms, co.astype(np.float32), isg.Camera(np.eye(3), np.zeros(3), f, (W / 2, H / 2), W, H)
 
