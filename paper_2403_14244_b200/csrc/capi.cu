@@ -52,16 +52,17 @@ struct isg_ctx {
   uint32_t* depth[2] = {nullptr, nullptr};
   uint32_t* order[2] = {nullptr, nullptr};
   uint32_t* ntiles = nullptr;
-  uint32_t* rank_of = nullptr;
+  uint32_t* emit_off = nullptr;  // first emission slot of splat g
   isg::RenderRec* rec_sorted = nullptr;
-  float4* grad2d = nullptr;  // n x 2, indexed by depth rank
   float4* grad3d = nullptr;  // n x 2, indexed by splat
   int order_buf = 0;         // which order[] holds the depth order
 
-  // (tile, rank) keys
+  // (tile, splat) pairs, key_cap slots
   int64_t key_cap = 0;
   uint32_t* tkey[2] = {nullptr, nullptr};
-  uint32_t* tval[2] = {nullptr, nullptr};
+  uint32_t* tval[2] = {nullptr, nullptr};  // emission slots, sorted by (tile, depth, index)
+  uint32_t* emit_rank = nullptr;           // depth rank of the pair in slot e
+  float4* partial = nullptr;               // 2D gradient of the pair in slot e (2 x float4)
   int tile_buf = 0;
 
   // sort / scan scratch
@@ -91,7 +92,7 @@ struct isg_ctx {
   // frame state
   bool have_frame = false;
   isg::FrameParams last_fp{};
-  bool pending = false;  // grad2d holds an un-projected view
+  bool pending = false;  // `partial` holds an un-projected view
   isg::FrameParams pending_fp{};
   bool grad3d_valid = false;
   bool frame_unchecked = false;  // frames launched since the last overflow check
@@ -196,11 +197,9 @@ isg_status ensure_scene(isg_ctx* ctx, int64_t n) {
     ISG_CUDA(realloc_dev(&ctx->order[i], a));
   }
   ISG_CUDA(realloc_dev(&ctx->ntiles, a));
-  ISG_CUDA(realloc_dev(&ctx->rank_of, a));
+  ISG_CUDA(realloc_dev(&ctx->emit_off, a));
   ISG_CUDA(realloc_dev(&ctx->rec_sorted, a));
-  ISG_CUDA(realloc_dev(&ctx->grad2d, 2 * a));
   ISG_CUDA(realloc_dev(&ctx->grad3d, 2 * a));
-  ISG_CUDA(cudaMemsetAsync(ctx->grad2d, 0, sizeof(float4) * 2 * a, ctx->stream));
   const int64_t words = isg::scan_emit_scratch_words(a) + 1;
   ISG_CUDA(realloc_dev(&ctx->scan_scratch, words));
   ctx->scan_words_alloc = words;
@@ -226,6 +225,8 @@ isg_status ensure_keys(isg_ctx* ctx, int64_t cap) {
     ISG_CUDA(realloc_dev(&ctx->tkey[i], cap));
     ISG_CUDA(realloc_dev(&ctx->tval[i], cap));
   }
+  ISG_CUDA(realloc_dev(&ctx->emit_rank, cap));
+  ISG_CUDA(realloc_dev(&ctx->partial, 2 * cap));
   ctx->key_cap = cap;
   return ISG_OK;
 }
@@ -290,8 +291,9 @@ FrameParams make_fp(const isg_camera* cam, const float bg[3], float t_min) {
 isg_status flush_pending(isg_ctx* ctx) {
   if (!ctx->pending) return ISG_OK;
   ISG_STAGE(ST_PROJECT_BWD);
-  isg::launch_project_backward(ctx->ms, ctx->n, ctx->pending_fp, ctx->rank_of, ctx->grad2d,
-                               ctx->grad3d, !ctx->grad3d_valid, ctx->stream);
+  isg::launch_project_backward(ctx->ms, ctx->n, ctx->pending_fp, ctx->emit_off, ctx->ntiles,
+                               ctx->partial, ctx->total, ctx->key_cap, ctx->grad3d,
+                               !ctx->grad3d_valid, ctx->stream);
   ISG_CHECK_LAUNCH();
   ctx->launches++;
   ctx->grad3d_valid = true;
@@ -339,7 +341,7 @@ isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out) {
     {
     ISG_STAGE(ST_SCAN_EMIT);
     isg::launch_scan_emit(ctx->order[ctx->order_buf], ctx->ntiles, ctx->rec_geo, ctx->co, n, fp,
-                          ctx->rec_sorted, ctx->rank_of, ctx->tkey[0], ctx->tval[0],
+                          ctx->rec_sorted, ctx->emit_off, ctx->tkey[0], ctx->emit_rank,
                           ctx->key_cap, ctx->scan_scratch, ctx->sc + 3, ctx->sc + 0, ctx->total,
                           ctx->sc + 2, st);
     ISG_CHECK_LAUNCH();
@@ -347,7 +349,7 @@ isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out) {
     }
     {
     ISG_STAGE(ST_TILE_SORT);
-    ctx->tile_buf = isg::radix_sort_pairs(ctx->tkey, ctx->tval, false, ctx->sc + 0, ctx->key_cap,
+    ctx->tile_buf = isg::radix_sort_pairs(ctx->tkey, ctx->tval, true, ctx->sc + 0, ctx->key_cap,
                                           bits_for(fp.n_tiles), ctx->sort, st, &ctx->launches);
     ISG_CHECK_LAUNCH();
     }
@@ -357,8 +359,9 @@ isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out) {
     ctx->launches++;
   }
   ISG_STAGE(ST_BLEND_FWD);
-  isg::launch_blend_fwd(fp, ctx->ranges, ctx->tval[ctx->tile_buf], ctx->rec_sorted, ctx->total,
-                        ctx->key_cap, out, ctx->t_last, ctx->n_proc, st);
+  isg::launch_blend_fwd(fp, ctx->ranges, ctx->tval[ctx->tile_buf], ctx->emit_rank,
+                        ctx->rec_sorted, ctx->total, ctx->key_cap, out, ctx->t_last, ctx->n_proc,
+                        st);
   ISG_CHECK_LAUNCH();
   ctx->launches++;
   ctx->have_frame = true;
@@ -414,9 +417,10 @@ isg_status run_backward(isg_ctx* ctx, const FrameParams& fp, const float* target
   const float scale = weight / (3.0f * (float)fp.cam.width * (float)fp.cam.height);
   {
   ISG_STAGE(ST_BLEND_BWD);
-  isg::launch_blend_bwd(fp, ctx->ranges, ctx->tval[ctx->tile_buf], ctx->rec_sorted, ctx->total,
-                        ctx->key_cap, ctx->img, target_dev, ctx->t_last, ctx->n_proc, scale,
-                        ctx->grad2d, ctx->tile_loss, ctx->stream);
+  isg::launch_blend_bwd(fp, ctx->ranges, ctx->tval[ctx->tile_buf], ctx->emit_rank,
+                        ctx->rec_sorted, ctx->total, ctx->key_cap, ctx->img, target_dev,
+                        ctx->t_last, ctx->n_proc, scale, ctx->partial, ctx->tile_loss,
+                        ctx->stream);
   ISG_CHECK_LAUNCH();
   }
   ISG_STAGE(ST_LOSS_REDUCE);
@@ -506,8 +510,9 @@ void isg_destroy(isg_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->nccl_comm) isg_nccl_detach(ctx);
   void* dev[] = {ctx->ms, ctx->co, ctx->m, ctx->v, ctx->rec_geo, ctx->depth[0], ctx->depth[1],
-                 ctx->order[0], ctx->order[1], ctx->ntiles, ctx->rank_of, ctx->rec_sorted,
-                 ctx->grad2d, ctx->grad3d, ctx->tkey[0], ctx->tkey[1], ctx->tval[0], ctx->tval[1],
+                 ctx->order[0], ctx->order[1], ctx->ntiles, ctx->emit_off, ctx->rec_sorted,
+                 ctx->emit_rank, ctx->partial, ctx->grad3d, ctx->tkey[0], ctx->tkey[1],
+                 ctx->tval[0], ctx->tval[1],
                  ctx->sort.hist, ctx->sort.lookback, ctx->sort.counters, ctx->scan_scratch,
                  ctx->img, ctx->target, ctx->t_last, ctx->n_proc, ctx->ranges, ctx->tile_loss,
                  ctx->sc, ctx->total, ctx->loss};
@@ -584,7 +589,6 @@ static isg_status set_scene_impl(isg_ctx* ctx, int64_t n, const float* ms, const
     ISG_CUDA(cudaMemcpyAsync(ctx->co, co, sizeof(float4) * n, kind, ctx->stream));
     ISG_CUDA(cudaMemsetAsync(ctx->m, 0, sizeof(float4) * 2 * n, ctx->stream));
     ISG_CUDA(cudaMemsetAsync(ctx->v, 0, sizeof(float4) * 2 * n, ctx->stream));
-    ISG_CUDA(cudaMemsetAsync(ctx->grad2d, 0, sizeof(float4) * 2 * n, ctx->stream));
   }
   if (ctx->n != n || ctx->key_cap < 4 * n) {
     // size the key buffers for the new scene on the next frame
@@ -716,9 +720,7 @@ isg_status isg_read_loss(isg_ctx* ctx, double* loss_out) {
 isg_status isg_zero_grads(isg_ctx* ctx) {
   if (!ctx) return ISG_E_ARG;
   cudaSetDevice(ctx->device);
-  if (ctx->pending && ctx->n > 0)
-    ISG_CUDA(cudaMemsetAsync(ctx->grad2d, 0, sizeof(float4) * 2 * ctx->n, ctx->stream));
-  ctx->pending = false;
+  ctx->pending = false;  // the pending view's per-pair slots are simply dropped
   ctx->grad3d_valid = false;
   ISG_CUDA(cudaMemsetAsync(ctx->loss, 0, sizeof(double) * 2, ctx->stream));
   return ISG_OK;
@@ -773,8 +775,9 @@ isg_status isg_adam_step(isg_ctx* ctx, const float lr[4], float b1, float b2, fl
   if (ctx->pending && !ctx->grad3d_valid && !ctx->nccl_comm) {
     // single view since the last step: projection backward fused with Adam (K8)
     ISG_STAGE(ST_PROJECT_ADAM);
-    isg::launch_project_adam(ctx->ms, ctx->co, ctx->n, ctx->pending_fp, ctx->rank_of, ctx->grad2d,
-                             ctx->m, ctx->v, ap, ctx->total + 1, ctx->stream);
+    isg::launch_project_adam(ctx->ms, ctx->co, ctx->n, ctx->pending_fp, ctx->emit_off,
+                             ctx->ntiles, ctx->partial, ctx->total, ctx->key_cap, ctx->m, ctx->v,
+                             ap, ctx->total + 1, ctx->stream);
     ISG_CHECK_LAUNCH();
     ctx->launches++;
     ctx->pending = false;
@@ -814,7 +817,7 @@ isg_status isg_debug_bins(isg_ctx* ctx, uint64_t* keys, uint32_t* vals, int64_t*
     uint32_t* dv = nullptr;
     ISG_CUDA(cudaMalloc(&dk, sizeof(uint64_t) * nk));
     ISG_CUDA(cudaMalloc(&dv, sizeof(uint32_t) * nk));
-    isg::launch_debug_keys(ctx->tkey[ctx->tile_buf], ctx->tval[ctx->tile_buf],
+    isg::launch_debug_keys(ctx->tkey[ctx->tile_buf], ctx->tval[ctx->tile_buf], ctx->emit_rank,
                            ctx->order[ctx->order_buf], ctx->ms, fp, nk, dk, dv, ctx->stream);
     if (keys) cudaMemcpyAsync(keys, dk, sizeof(uint64_t) * nk, cudaMemcpyDeviceToHost, ctx->stream);
     if (vals) cudaMemcpyAsync(vals, dv, sizeof(uint32_t) * nk, cudaMemcpyDeviceToHost, ctx->stream);

@@ -65,12 +65,14 @@ void launch_preprocess(const float4* ms, const float4* co, int64_t n, const Fram
                        float4* rec_geo, uint32_t* depth_key, uint32_t* ntiles,
                        uint32_t* first_bad, uint32_t* n_dev, cudaStream_t st);
 
-// K2/K3: scan of ntiles in depth order, record gather, (tile, rank) emission.
+// K2/K3: scan of ntiles in depth order, record gather, emission of the (tile, splat) pairs.
+// Pair e (the emission slot) gets tile_keys[e] = tile and emit_rank[e] = depth rank; splat g's
+// pairs occupy slots [emit_off[g], emit_off[g] + ntiles[g]).
 // scratch: scan_emit_scratch_words(n) + 1 zeroed u64 words; counter: zeroed u32.
 int64_t scan_emit_scratch_words(int64_t n);
 void launch_scan_emit(const uint32_t* order, const uint32_t* ntiles, const float4* rec_geo,
                       const float4* co, int64_t n, const FrameParams& fp, RenderRec* rec_sorted,
-                      uint32_t* rank_of, uint32_t* tile_keys, uint32_t* tile_vals,
+                      uint32_t* emit_off, uint32_t* tile_keys, uint32_t* emit_rank,
                       int64_t key_cap, unsigned long long* scratch, uint32_t* counter,
                       uint32_t* n_keys, unsigned long long* n_keys_total, uint32_t* n_visible,
                       cudaStream_t st);
@@ -78,15 +80,18 @@ void launch_scan_emit(const uint32_t* order, const uint32_t* ntiles, const float
 void launch_ranges(const uint32_t* sorted_tiles, const uint32_t* n_keys, int64_t key_cap,
                    uint2* ranges, cudaStream_t st);
 
+// K6.  vals: emission slots sorted by (tile, depth, index).
 void launch_blend_fwd(const FrameParams& fp, const uint2* ranges, const uint32_t* vals,
-                      const RenderRec* rec, const unsigned long long* total, int64_t key_cap,
-                      float* out, float* t_last, uint32_t* n_proc, cudaStream_t st);
+                      const uint32_t* emit_rank, const RenderRec* rec,
+                      const unsigned long long* total, int64_t key_cap, float* out, float* t_last,
+                      uint32_t* n_proc, cudaStream_t st);
 
+// K7.  Writes every pair's 2D gradient to partial[2e], partial[2e+1] (emission slot e).
 void launch_blend_bwd(const FrameParams& fp, const uint2* ranges, const uint32_t* vals,
-                      const RenderRec* rec, const unsigned long long* total, int64_t key_cap,
-                      const float* img, const float* target, const float* t_last,
-                      const uint32_t* n_proc, float loss_scale, float4* grad2d,
-                      double* tile_loss, cudaStream_t st);
+                      const uint32_t* emit_rank, const RenderRec* rec,
+                      const unsigned long long* total, int64_t key_cap, const float* img,
+                      const float* target, const float* t_last, const uint32_t* n_proc,
+                      float loss_scale, float4* partial, double* tile_loss, cudaStream_t st);
 
 // loss[0] += scale * sum(tile_loss), loss[1] = scale * sum(tile_loss)
 void launch_loss_reduce(const double* tile_loss, int n_tiles, double scale, double* loss,
@@ -101,18 +106,20 @@ struct AdamParams {
 
 // K8a: 2D grads of one view -> 3D grads (overwrite when `first`, else accumulate).
 void launch_project_backward(const float4* ms, int64_t n, const FrameParams& fp,
-                             const uint32_t* rank_of, float4* grad2d, float4* grad3d, bool first,
-                             cudaStream_t st);
+                             const uint32_t* emit_off, const uint32_t* ntiles,
+                             const float4* partial, const unsigned long long* total, int64_t cap,
+                             float4* grad3d, bool first, cudaStream_t st);
 // K8 fused: 2D grads of one view -> 3D -> Adam.
 void launch_project_adam(float4* ms, float4* co, int64_t n, const FrameParams& fp,
-                         const uint32_t* rank_of, float4* grad2d, float4* m, float4* v,
+                         const uint32_t* emit_off, const uint32_t* ntiles, const float4* partial,
+                         const unsigned long long* total, int64_t cap, float4* m, float4* v,
                          const AdamParams& ap, unsigned long long* skipped, cudaStream_t st);
 // K8b: Adam from accumulated 3D grads.
 void launch_adam(float4* ms, float4* co, int64_t n, const float4* grad3d, float4* m, float4* v,
                  const AdamParams& ap, unsigned long long* skipped, cudaStream_t st);
 
-void launch_debug_keys(const uint32_t* tiles, const uint32_t* ranks, const uint32_t* order,
-                       const float4* ms, const FrameParams& fp, int64_t nkeys, uint64_t* keys,
-                       uint32_t* gids, cudaStream_t st);
+void launch_debug_keys(const uint32_t* tiles, const uint32_t* slots, const uint32_t* emit_rank,
+                       const uint32_t* order, const float4* ms, const FrameParams& fp,
+                       int64_t nkeys, uint64_t* keys, uint32_t* gids, cudaStream_t st);
 
 }  // namespace isg

@@ -1,19 +1,39 @@
 // K8 — projection backward and the fused Adam step.
 //
-// Projection backward: chain rule through u = f x/z + cx, v = f y/z + cy, s = sigma f/z
-// (Jacobian: projection_jacobian, /root/reference/proj/src/splat3d.cpp:39-47; closed forms
-// of the kernel gradient: include/isosplat/kernels.hpp:208-222), rotated back to world space
-// with R^T.  Optimizer slot: update_step (src/optimize.cpp:78-108) — sigma moves in log
-// space (:93,:105), updates with a non-finite gradient are skipped and counted (:87-90) — with
-// the Adam rule of torch.optim.Adam on (mu, log sigma, rgb, logit opacity).
+// Each splat's 2D gradient (du, dv, dsigma2d, dopacity, drgb) is the sum of its (tile, splat)
+// slots written by K7; they are contiguous in emission order ([emit_off[g], + ntiles[g]) ) and
+// summed in that fixed order, so gradients are bitwise deterministic (no atomics anywhere).
 //
-// One thread per splat; params, moments and 3D grads are float4 SoA, coalesced; the 2D
-// gradient of splat g sits at its depth rank (rank_of[g]) and is zeroed after it is read.
+// Projection backward: chain rule through u = f x/z + cx, v = f y/z + cy, s = sigma f/z
+// (Jacobian: projection_jacobian, /root/reference/proj/src/splat3d.cpp:39-47; closed forms of
+// the kernel gradient: include/isosplat/kernels.hpp:208-222), rotated back to world space with
+// R^T.  Optimizer slot: update_step (src/optimize.cpp:78-108) — sigma moves in log space
+// (:93,:105), updates with a non-finite gradient are skipped and counted (:87-90) — with the
+// Adam rule of torch.optim.Adam on (mu, log sigma, rgb, logit opacity).
+//
+// One thread per splat; params, moments and 3D grads are float4 SoA, coalesced.
 #include "isg_math.cuh"
 
 namespace isg {
 
 namespace {
+
+__device__ __forceinline__ void sum_slots(const float4* __restrict__ partial, uint32_t off,
+                                          uint32_t cnt, float4& a, float4& b) {
+  a = make_float4(0.f, 0.f, 0.f, 0.f);
+  b = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (uint32_t k = 0; k < cnt; ++k) {
+    const float4 x = partial[2 * (size_t)(off + k)];
+    const float4 y = partial[2 * (size_t)(off + k) + 1];
+    a.x += x.x;
+    a.y += x.y;
+    a.z += x.z;
+    a.w += x.w;
+    b.x += y.x;
+    b.y += y.y;
+    b.z += y.z;
+  }
+}
 
 __device__ __forceinline__ void grad3d_of(const float4 ms, const isg_camera& cam, float4 a,
                                           float4 b, float out[8]) {
@@ -74,14 +94,15 @@ __device__ __forceinline__ void adam_update(float4* __restrict__ ms, float4* __r
 }  // namespace
 
 __global__ void __launch_bounds__(256) k_project_backward(
-    const float4* __restrict__ ms, int64_t n, FrameParams fp, const uint32_t* __restrict__ rank_of,
-    float4* __restrict__ grad2d, float4* __restrict__ grad3d, bool first) {
+    const float4* __restrict__ ms, int64_t n, FrameParams fp, const uint32_t* __restrict__ emit_off,
+    const uint32_t* __restrict__ ntiles, const float4* __restrict__ partial,
+    const unsigned long long* __restrict__ total, int64_t cap, float4* __restrict__ grad3d,
+    bool first) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const size_t r = rank_of[i];
-  const float4 a = grad2d[2 * r], b = grad2d[2 * r + 1];
-  grad2d[2 * r] = make_float4(0.f, 0.f, 0.f, 0.f);
-  grad2d[2 * r + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const bool ov = *total > (unsigned long long)cap;  // frame was skipped: contributes nothing
+  float4 a, b;
+  sum_slots(partial, emit_off[i], ov ? 0u : ntiles[i], a, b);
   float o[8];
   grad3d_of(ms[i], fp.cam, a, b, o);
   float4 g0 = make_float4(o[0], o[1], o[2], o[3]), g1 = make_float4(o[4], o[5], o[6], o[7]);
@@ -96,14 +117,15 @@ __global__ void __launch_bounds__(256) k_project_backward(
 
 __global__ void __launch_bounds__(256) k_project_adam(
     float4* __restrict__ ms, float4* __restrict__ co, int64_t n, FrameParams fp,
-    const uint32_t* __restrict__ rank_of, float4* __restrict__ grad2d, float4* __restrict__ m,
-    float4* __restrict__ v, AdamParams ap, unsigned long long* __restrict__ skipped) {
+    const uint32_t* __restrict__ emit_off, const uint32_t* __restrict__ ntiles,
+    const float4* __restrict__ partial, const unsigned long long* __restrict__ total, int64_t cap,
+    float4* __restrict__ m, float4* __restrict__ v, AdamParams ap,
+    unsigned long long* __restrict__ skipped) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const size_t r = rank_of[i];
-  const float4 a = grad2d[2 * r], b = grad2d[2 * r + 1];
-  grad2d[2 * r] = make_float4(0.f, 0.f, 0.f, 0.f);
-  grad2d[2 * r + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (*total > (unsigned long long)cap) return;  // overflowed frame: no update (host re-runs)
+  float4 a, b;
+  sum_slots(partial, emit_off[i], ntiles[i], a, b);
   float o[8];
   grad3d_of(ms[i], fp.cam, a, b, o);
   adam_update(ms, co, m, v, i, o, ap, skipped);
@@ -121,19 +143,23 @@ __global__ void __launch_bounds__(256) k_adam(float4* __restrict__ ms, float4* _
 }
 
 void launch_project_backward(const float4* ms, int64_t n, const FrameParams& fp,
-                             const uint32_t* rank_of, float4* grad2d, float4* grad3d, bool first,
-                             cudaStream_t st) {
+                             const uint32_t* emit_off, const uint32_t* ntiles,
+                             const float4* partial, const unsigned long long* total, int64_t cap,
+                             float4* grad3d, bool first, cudaStream_t st) {
   if (n <= 0) return;
-  k_project_backward<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ms, n, fp, rank_of, grad2d,
-                                                                   grad3d, first);
+  k_project_backward<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ms, n, fp, emit_off, ntiles,
+                                                                   partial, total, cap, grad3d,
+                                                                   first);
 }
 
 void launch_project_adam(float4* ms, float4* co, int64_t n, const FrameParams& fp,
-                         const uint32_t* rank_of, float4* grad2d, float4* m, float4* v,
+                         const uint32_t* emit_off, const uint32_t* ntiles, const float4* partial,
+                         const unsigned long long* total, int64_t cap, float4* m, float4* v,
                          const AdamParams& ap, unsigned long long* skipped, cudaStream_t st) {
   if (n <= 0) return;
-  k_project_adam<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ms, co, n, fp, rank_of, grad2d, m,
-                                                               v, ap, skipped);
+  k_project_adam<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ms, co, n, fp, emit_off, ntiles,
+                                                               partial, total, cap, m, v, ap,
+                                                               skipped);
 }
 
 void launch_adam(float4* ms, float4* co, int64_t n, const float4* grad3d, float4* m, float4* v,

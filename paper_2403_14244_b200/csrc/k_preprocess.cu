@@ -55,24 +55,25 @@ void launch_preprocess(const float4* ms, const float4* co, int64_t n, const Fram
 
 // Parity hook: (tile << 32 | float_bits(depth)) and splat index for each sorted key.
 __global__ void k_debug_keys(const uint32_t* __restrict__ tiles,
-                             const uint32_t* __restrict__ ranks,
+                             const uint32_t* __restrict__ slots,
+                             const uint32_t* __restrict__ emit_rank,
                              const uint32_t* __restrict__ order, const float4* __restrict__ ms,
                              FrameParams fp, int64_t nkeys, uint64_t* __restrict__ keys,
                              uint32_t* __restrict__ gids) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nkeys) return;
-  const uint32_t g = order[ranks[i]];
+  const uint32_t g = order[emit_rank[slots[i]]];
   const Proj p = project(ms[g], fp.cam);
   keys[i] = ((uint64_t)tiles[i] << 32) | __float_as_uint(p.zc);
   gids[i] = g;
 }
 
-void launch_debug_keys(const uint32_t* tiles, const uint32_t* ranks, const uint32_t* order,
-                       const float4* ms, const FrameParams& fp, int64_t nkeys, uint64_t* keys,
-                       uint32_t* gids, cudaStream_t st) {
+void launch_debug_keys(const uint32_t* tiles, const uint32_t* slots, const uint32_t* emit_rank,
+                       const uint32_t* order, const float4* ms, const FrameParams& fp,
+                       int64_t nkeys, uint64_t* keys, uint32_t* gids, cudaStream_t st) {
   if (nkeys <= 0) return;
-  k_debug_keys<<<(unsigned)((nkeys + 255) / 256), 256, 0, st>>>(tiles, ranks, order, ms, fp,
-                                                                 nkeys, keys, gids);
+  k_debug_keys<<<(unsigned)((nkeys + 255) / 256), 256, 0, st>>>(tiles, slots, emit_rank, order,
+                                                                 ms, fp, nkeys, keys, gids);
 }
 
 }  // namespace isg

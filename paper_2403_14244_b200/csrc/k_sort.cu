@@ -219,8 +219,8 @@ constexpr unsigned long long kC64Mask = (1ull << 62) - 1;
 __global__ void __launch_bounds__(kScanThreads) k_scan_emit(
     const uint32_t* __restrict__ order, const uint32_t* __restrict__ ntiles,
     const float4* __restrict__ rec_geo, const float4* __restrict__ co, int64_t n, FrameParams fp,
-    RenderRec* __restrict__ rec_sorted, uint32_t* __restrict__ rank_of,
-    uint32_t* __restrict__ tile_keys, uint32_t* __restrict__ tile_vals, int64_t key_cap,
+    RenderRec* __restrict__ rec_sorted, uint32_t* __restrict__ emit_off,
+    uint32_t* __restrict__ tile_keys, uint32_t* __restrict__ emit_rank, int64_t key_cap,
     unsigned long long* __restrict__ lookback, uint32_t* __restrict__ counter,
     uint32_t* __restrict__ n_keys, unsigned long long* __restrict__ n_keys_total,
     uint32_t* __restrict__ n_visible) {
@@ -282,14 +282,13 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(
     const int64_t r = r0 + j;
     if (r >= n) break;
     const uint32_t gg = g[j];
-    rank_of[gg] = (uint32_t)r;
-    const float4 geo = rec_geo[gg];
-    const float4 col = co[gg];
-    RenderRec rr;
-    rr.geo = make_float4(geo.x, geo.y, __fmul_rn(geo.z, geo.z), geo.w);  // (u, v, s^2, r2max)
-    rr.col = col;
-    rec_sorted[r] = rr;
+    emit_off[gg] = (uint32_t)min(off, (unsigned long long)0xFFFFFFFFu);
     if (c[j] == 0) continue;
+    const float4 geo = rec_geo[gg];
+    RenderRec rr;  // (u, v, r2max, -log2(e)/sigma2d^2), (r, g, b, opacity)
+    rr.geo = make_float4(geo.x, geo.y, geo.w, __fdiv_rn(-1.4426950408889634f, __fmul_rn(geo.z, geo.z)));
+    rr.col = co[gg];
+    rec_sorted[r] = rr;
     int x0, x1, y0, y1;
     tile_bbox(geo.x, geo.y, geo.z, fp.tiles_x, fp.tiles_y, x0, x1, y0, y1);
     for (int ty = y0; ty <= y1; ++ty)
@@ -297,7 +296,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(
         if (!tile_hit(geo.x, geo.y, geo.w, tx, ty, fp.cam.width, fp.cam.height)) continue;
         if (off < (unsigned long long)key_cap) {
           tile_keys[off] = (uint32_t)(ty * fp.tiles_x + tx);
-          tile_vals[off] = (uint32_t)r;
+          emit_rank[off] = (uint32_t)r;
         }
         ++off;
       }
@@ -310,14 +309,14 @@ int64_t scan_emit_scratch_words(int64_t n) { return (n + kScanTileItems - 1) / k
 
 void launch_scan_emit(const uint32_t* order, const uint32_t* ntiles, const float4* rec_geo,
                       const float4* co, int64_t n, const FrameParams& fp, RenderRec* rec_sorted,
-                      uint32_t* rank_of, uint32_t* tile_keys, uint32_t* tile_vals,
+                      uint32_t* emit_off, uint32_t* tile_keys, uint32_t* emit_rank,
                       int64_t key_cap, unsigned long long* scratch, uint32_t* counter,
                       uint32_t* n_keys, unsigned long long* n_keys_total, uint32_t* n_visible,
                       cudaStream_t st) {
   const int64_t tiles = scan_emit_scratch_words(n);
   if (tiles == 0) return;  // caller zeroed the counts
   k_scan_emit<<<(unsigned)tiles, kScanThreads, 0, st>>>(
-      order, ntiles, rec_geo, co, n, fp, rec_sorted, rank_of, tile_keys, tile_vals, key_cap,
+      order, ntiles, rec_geo, co, n, fp, rec_sorted, emit_off, tile_keys, emit_rank, key_cap,
       scratch, counter, n_keys, n_keys_total, n_visible);
 }
 
