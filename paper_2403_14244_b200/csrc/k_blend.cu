@@ -4,13 +4,15 @@
 // inclusion test covers(ScreenIso) (:108-114).  Instead of every pixel visiting every splat
 // (O(W*H*N)), one CTA owns one tile and walks only that tile's depth-ordered list.
 //
-// Mapping (both kernels): 64 threads per tile; warp w covers the 16x8 half-tile w, each lane a
-// 2x2 pixel quad, so one shared-memory record feeds four pixels and the squared distances
-// share two dx^2 and two dy^2.  Per list entry the warp first tests the splat's 3-sigma circle
-// against its half-tile rectangle (warp-uniform; skips ~half the entries at no divergence).
-// Records are staged 64 at a time into shared memory with cp.async, double-buffered: the
-// next batch's copy is in flight while the current one is blended.  The forward stops once
-// every pixel of the tile has transmittance <= t_min (__syncthreads_count per batch).
+// Mapping (both kernels): 128 threads per tile; warp w owns the 8x8 quarter-tile w and each
+// lane a vertical pixel pair, so one shared-memory record feeds two pixels that share dx.
+// Records are staged 128 at a time into shared memory with cp.async, double-buffered (the
+// next batch's copy is in flight while the current one is blended).  The staging thread also
+// tests the splat's 3-sigma circle against the four quarter-tiles (conservative closest-point
+// test, exact rounding) and stores a 4-bit mask; each warp turns the masks into a 128-bit
+// ballot and iterates only over the entries that can touch its quarter — culling costs ~nothing
+// and non-overlapping entries cost no issue slots at all.  Compositing is branch-free.
+// The forward stops once every pixel of the tile has transmittance <= t_min.
 //
 // The 3-sigma test is bit-identical to the FP32 oracle (explicit _rn arithmetic); exp uses
 // ex2.approx on a per-splat precomputed -log2(e)/sigma2d^2.
@@ -18,8 +20,8 @@
 // K7 is the backward the reference does not have: the same walk in reverse from
 // each pixel's last processed entry, the L2 gradient dL/dC = 2 w (C - target) / (3 W H)
 // (mse, src/image.cpp:50-58) fused in the prologue, transmittance recovered by division, and
-// the 7 per-splat 2D gradients (du, dv, dsigma2d, dopacity, drgb) summed per thread over its
-// quad, reduce-scattered across the warp in 9 shuffles, combined across the two warps in
+// the 7 per-splat 2D gradients (du, dv, dsigma2d, dopacity, drgb) summed per thread over its two
+// pixels, reduce-scattered across the warp in 9 shuffles, combined across the four warps in
 // shared memory and written (no atomics) to the (tile, splat) pair's own slot in emission
 // order; K8 then sums each splat's slots in a fixed order -> deterministic gradients.
 #include "isg_math.cuh"
@@ -27,8 +29,9 @@
 namespace isg {
 
 namespace {
-constexpr int kBT = 64;     // threads per tile CTA (2 warps x 32 quads)
-constexpr int kBatch = 64;  // records staged per batch
+constexpr int kBT = 128;     // threads per tile CTA (4 warps x 32 pixel pairs)
+constexpr int kBatch = 128;  // records staged per batch (one per thread)
+constexpr int kWarps = kBT / 32;
 constexpr float kLn2 = 0.6931471805599453f;
 
 __device__ __forceinline__ bool overflowed(const unsigned long long* total, int64_t cap) {
@@ -43,12 +46,41 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
 struct Stage {
-  float4 geo[kBatch];  // u, v, r2max, -log2e / sigma2d^2
-  float4 col[kBatch];  // r, g, b, opacity
+  float4 geo[kBatch];     // u, v, r2max, -log2e / sigma2d^2
+  float4 col[kBatch];     // r, g, b, opacity
   uint32_t slot[kBatch];  // emission index of the (tile, splat) pair
 };
 
+// Pixel-centre rectangle of this warp's quarter-tile, clipped to the image.
+struct TileGeom {
+  float qx0, qx1, qy0, qy1;
+  bool qvalid;
+};
+
+__device__ __forceinline__ TileGeom tile_geom(const FrameParams& fp, int tile) {
+  TileGeom t;
+  const int w = threadIdx.x >> 5;
+  const int tx = tile % fp.tiles_x, ty = tile / fp.tiles_x;
+  const int W = fp.cam.width, H = fp.cam.height;
+  const int x0 = tx * kTile + (w & 1) * 8, y0 = ty * kTile + (w >> 1) * 8;
+  t.qvalid = x0 < W && y0 < H;
+  t.qx0 = (float)x0 + 0.5f;
+  t.qx1 = (float)(min(x0 + 8, W) - 1) + 0.5f;
+  t.qy0 = (float)y0 + 0.5f;
+  t.qy1 = (float)(min(y0 + 8, H) - 1) + 0.5f;
+  return t;
+}
+
+// 3-sigma circle vs pixel-centre rectangle (conservative, exact rounding like tile_hit).
+__device__ __forceinline__ bool rect_hit(float x0, float x1, float y0, float y1, float u, float v,
+                                         float r2max) {
+  const float cx = fminf(fmaxf(u, x0), x1);
+  const float cy = fminf(fmaxf(v, y0), y1);
+  return !(dist2_rn(__fsub_rn(cx, u), __fsub_rn(cy, v)) > r2max);
+}
+
 // Stage list entries [beg, beg+cnt) of the sorted key array into `st` (thread t: entry t).
+// The record fetch is a dependent gather (slot -> rank -> record), issued as cp.async.
 __device__ __forceinline__ void stage_batch(Stage& st, const uint32_t* __restrict__ vals,
                                             const uint32_t* __restrict__ emit_rank,
                                             const RenderRec* __restrict__ rec, uint32_t beg,
@@ -64,45 +96,22 @@ __device__ __forceinline__ void stage_batch(Stage& st, const uint32_t* __restric
   cp_async_commit();
 }
 
-// Per-thread quad geometry.
-struct Quad {
-  float px0, px1, py0, py1;
-  bool valid[4];  // (x0,y0) (x1,y0) (x0,y1) (x1,y1)
-  float wx0, wx1, wy0, wy1;  // pixel-centre rectangle of the warp's half tile (clipped)
-  bool warp_empty;
-  int x0, y0;
-};
-
-__device__ __forceinline__ Quad make_quad(const FrameParams& fp, int tile) {
-  Quad q;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int tx = tile % fp.tiles_x, ty = tile / fp.tiles_x;
-  const int W = fp.cam.width, H = fp.cam.height;
-  q.x0 = tx * kTile + 2 * (lane & 7);
-  q.y0 = ty * kTile + w * 8 + 2 * (lane >> 3);
-  q.px0 = (float)q.x0 + 0.5f;
-  q.px1 = q.px0 + 1.0f;
-  q.py0 = (float)q.y0 + 0.5f;
-  q.py1 = q.py0 + 1.0f;
-  q.valid[0] = q.x0 < W && q.y0 < H;
-  q.valid[1] = q.x0 + 1 < W && q.y0 < H;
-  q.valid[2] = q.x0 < W && q.y0 + 1 < H;
-  q.valid[3] = q.x0 + 1 < W && q.y0 + 1 < H;
-  const int wy = ty * kTile + w * 8;
-  q.warp_empty = wy >= H;
-  q.wx0 = (float)(tx * kTile) + 0.5f;
-  q.wx1 = (float)(min(tx * kTile + kTile, W) - 1) + 0.5f;
-  q.wy0 = (float)wy + 0.5f;
-  q.wy1 = (float)(min(wy + 8, H) - 1) + 0.5f;
-  return q;
-}
-
-// Does the 3-sigma circle reach the warp's pixel-centre rectangle?  (conservative, exact
-// rounding like tile_hit, so no covered pixel is ever skipped)
-__device__ __forceinline__ bool warp_hit(const Quad& q, float u, float v, float r2max) {
-  const float cx = u < q.wx0 ? q.wx0 : (u > q.wx1 ? q.wx1 : u);
-  const float cy = v < q.wy0 ? q.wy0 : (v > q.wy1 ? q.wy1 : v);
-  return !(dist2_rn(__fsub_rn(cx, u), __fsub_rn(cy, v)) > r2max);
+// 128-bit relevance mask of the staged batch for warp w: bit j <=> entry j's 3-sigma circle can
+// reach the warp's quarter-tile.  Lane l tests entries l, l+32, l+64, l+96.
+__device__ __forceinline__ void warp_relevance(const Stage& st, const TileGeom& tg, int w,
+                                               int cnt, uint32_t rel[4]) {
+  (void)w;
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int j = 32 * k + lane;
+    bool hit = false;
+    if (j < cnt && tg.qvalid) {
+      const float4 g = st.geo[j];
+      hit = rect_hit(tg.qx0, tg.qx1, tg.qy0, tg.qy1, g.x, g.y, g.z);
+    }
+    rel[k] = __ballot_sync(0xffffffffu, hit);
+  }
 }
 
 // reduce-scatter of 8 values over the warp in 9 shuffles: lane L returns the warp-wide sum of
@@ -131,6 +140,26 @@ __device__ __forceinline__ float reduce_scatter8(const float v[8]) {
   return y;
 }
 
+struct PixPair {
+  int x, y0;        // pixels (x, y0) and (x, y0 + 1)
+  float px, py0, py1;
+  bool valid0, valid1;
+};
+
+__device__ __forceinline__ PixPair pix_pair(const FrameParams& fp, int tile) {
+  PixPair p;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int tx = tile % fp.tiles_x, ty = tile / fp.tiles_x;
+  p.x = tx * kTile + (w & 1) * 8 + (lane & 7);
+  p.y0 = ty * kTile + (w >> 1) * 8 + 2 * (lane >> 3);
+  p.px = (float)p.x + 0.5f;
+  p.py0 = (float)p.y0 + 0.5f;
+  p.py1 = p.py0 + 1.0f;
+  p.valid0 = p.x < fp.cam.width && p.y0 < fp.cam.height;
+  p.valid1 = p.x < fp.cam.width && p.y0 + 1 < fp.cam.height;
+  return p;
+}
+
 }  // namespace
 
 // =============================================================================================
@@ -142,85 +171,118 @@ __global__ void __launch_bounds__(kBT) k_blend_fwd(
   __shared__ Stage st[2];
   if (overflowed(total, key_cap)) return;
   const int tile = blockIdx.x;
-  const Quad q = make_quad(fp, tile);
+  const int w = threadIdx.x >> 5;
+  const TileGeom tg = tile_geom(fp, tile);
+  const PixPair pp = pix_pair(fp, tile);
   const uint2 rg = ranges[tile];
   const int n = (int)(rg.y - rg.x);
-
-  float T[4], Tl[4], C[4][3];
-  uint32_t np[4];
-  bool done[4];
-#pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    T[p] = 1.0f;
-    Tl[p] = 1.0f;
-    C[p][0] = C[p][1] = C[p][2] = 0.0f;
-    np[p] = 0;
-    done[p] = !q.valid[p];
-  }
   const float t_min = fp.t_min;
+
+  // invalid pixels start "terminated" (T = 0 <= t_min) and never contribute
+  float T0 = pp.valid0 ? 1.0f : 0.0f, T1 = pp.valid1 ? 1.0f : 0.0f;
+  float Tl0 = 1.0f, Tl1 = 1.0f;
+  float C0r = 0.f, C0g = 0.f, C0b = 0.f, C1r = 0.f, C1g = 0.f, C1b = 0.f;
+  uint32_t np0 = 0, np1 = 0;
+
   if (n > 0) stage_batch(st[0], vals, emit_rank, rec, rg.x, min(kBatch, n));
   for (int b = 0, it = 0; b < n; b += kBatch, ++it) {
     Stage& cur = st[it & 1];
     cp_async_wait_all();
-    const bool tdone = done[0] && done[1] && done[2] && done[3];
+    const bool tdone = !(T0 > t_min) && !(T1 > t_min);
     if (__syncthreads_count(tdone) == kBT) break;  // barrier: batch visible, previous consumed
-    if (b + kBatch < n) stage_batch(st[(it + 1) & 1], vals, emit_rank, rec, rg.x + b + kBatch,
-                                    min(kBatch, n - b - kBatch));
-    if (tdone || q.warp_empty) continue;
-    const int cnt = min(kBatch, n - b);
-    for (int j = 0; j < cnt; ++j) {
-      const float4 g = cur.geo[j];
-      if (!warp_hit(q, g.x, g.y, g.z)) continue;
-      const float dx0 = __fsub_rn(q.px0, g.x), dx1 = __fsub_rn(q.px1, g.x);
-      const float dy0 = __fsub_rn(q.py0, g.y), dy1 = __fsub_rn(q.py1, g.y);
-      const float ax0 = __fmul_rn(dx0, dx0), ax1 = __fmul_rn(dx1, dx1);
-      const float ay0 = __fmul_rn(dy0, dy0), ay1 = __fmul_rn(dy1, dy1);
-      float r2[4];
-      r2[0] = __fadd_rn(ax0, ay0);
-      r2[1] = __fadd_rn(ax1, ay0);
-      r2[2] = __fadd_rn(ax0, ay1);
-      r2[3] = __fadd_rn(ax1, ay1);
-      bool in[4];
-      bool any = false;
+    if (b + kBatch < n)
+      stage_batch(st[(it + 1) & 1], vals, emit_rank, rec, rg.x + b + kBatch,
+                  min(kBatch, n - b - kBatch));
+    uint32_t rel[4];
+    warp_relevance(cur, tg, w, min(kBatch, n - b), rel);
 #pragma unroll
-      for (int p = 0; p < 4; ++p) {
-        in[p] = !(r2[p] > g.z) && !done[p];
-        any |= in[p];
+    for (int k = 0; k < 4; ++k) {
+      uint32_t m = rel[k];
+      while (m) {
+        const int jj = 32 * k + __ffs(m) - 1;
+        m &= m - 1;
+        const float4 g = cur.geo[jj];
+        const float4 c = cur.col[jj];
+        const float dx = __fsub_rn(pp.px, g.x);
+        const float ax = __fmul_rn(dx, dx);
+        const float dy0 = __fsub_rn(pp.py0, g.y), dy1 = __fsub_rn(pp.py1, g.y);
+        const float r20 = __fadd_rn(ax, __fmul_rn(dy0, dy0));
+        const float r21 = __fadd_rn(ax, __fmul_rn(dy1, dy1));
+        const bool in0 = !(r20 > g.z) && (T0 > t_min);
+        const bool in1 = !(r21 > g.z) && (T1 > t_min);
+        const uint32_t idx = (uint32_t)(b + jj + 1);
+        const float a0 = in0 ? c.w * fast_exp2(r20 * g.w) : 0.0f;
+        const float a1 = in1 ? c.w * fast_exp2(r21 * g.w) : 0.0f;
+        const float w0 = T0 * a0, w1 = T1 * a1;
+        C0r += w0 * c.x;
+        C0g += w0 * c.y;
+        C0b += w0 * c.z;
+        C1r += w1 * c.x;
+        C1g += w1 * c.y;
+        C1b += w1 * c.z;
+        Tl0 = in0 ? T0 : Tl0;
+        Tl1 = in1 ? T1 : Tl1;
+        np0 = in0 ? idx : np0;
+        np1 = in1 ? idx : np1;
+        T0 = T0 * (1.0f - a0);
+        T1 = T1 * (1.0f - a1);
       }
-      if (!any) continue;
-      const float4 c = cur.col[j];
-#pragma unroll
-      for (int p = 0; p < 4; ++p) {
-        if (!in[p]) continue;
-        const float e = fast_exp2(r2[p] * g.w);
-        const float a = c.w * e;
-        const float wgt = T[p] * a;
-        C[p][0] += wgt * c.x;
-        C[p][1] += wgt * c.y;
-        C[p][2] += wgt * c.z;
-        Tl[p] = T[p];
-        T[p] = T[p] * (1.0f - a);
-        np[p] = (uint32_t)(b + j + 1);
-        done[p] = !(T[p] > t_min);
-      }
-      if (done[0] && done[1] && done[2] && done[3]) break;
     }
   }
   cp_async_wait_all();
   const int W = fp.cam.width;
-#pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    if (!q.valid[p]) continue;
-    const size_t pix = (size_t)(q.y0 + (p >> 1)) * W + q.x0 + (p & 1);
-    out[3 * pix + 0] = C[p][0] + T[p] * fp.bg[0];
-    out[3 * pix + 1] = C[p][1] + T[p] * fp.bg[1];
-    out[3 * pix + 2] = C[p][2] + T[p] * fp.bg[2];
-    t_last[pix] = Tl[p];
-    n_proc[pix] = np[p];
+  if (pp.valid0) {
+    const size_t pix = (size_t)pp.y0 * W + pp.x;
+    out[3 * pix + 0] = C0r + T0 * fp.bg[0];
+    out[3 * pix + 1] = C0g + T0 * fp.bg[1];
+    out[3 * pix + 2] = C0b + T0 * fp.bg[2];
+    t_last[pix] = Tl0;
+    n_proc[pix] = np0;
+  }
+  if (pp.valid1) {
+    const size_t pix = (size_t)(pp.y0 + 1) * W + pp.x;
+    out[3 * pix + 0] = C1r + T1 * fp.bg[0];
+    out[3 * pix + 1] = C1g + T1 * fp.bg[1];
+    out[3 * pix + 2] = C1b + T1 * fp.bg[2];
+    t_last[pix] = Tl1;
+    n_proc[pix] = np1;
   }
 }
 
 // =============================================================================================
+// One pixel of the reverse walk (branch-free; inactive pixels contribute exact zeros).
+struct BwdPix {
+  float G0, G1, G2;  // dL/dC
+  float T;           // transmittance before the most recently processed (later) entry
+  float A0, A1, A2;  // colour behind, normalised
+  uint32_t np;
+  bool first;
+};
+
+__device__ __forceinline__ void bwd_pixel(BwdPix& p, bool act, float dx, float dy, float r2,
+                                          const float4 g, const float4 c, float two_inv_s2,
+                                          float inv_s, float acc[8]) {
+  const float e = fast_exp2(r2 * g.w);
+  const float a = act ? c.w * e : 0.0f;
+  const float Tk = p.first ? p.T : __fdividef(p.T, 1.0f - a);
+  p.first = p.first && !act;
+  p.T = act ? Tk : p.T;
+  const float Tg = act ? Tk : 0.0f;
+  const float dLda = Tg * (p.G0 * (c.x - p.A0) + p.G1 * (c.y - p.A1) + p.G2 * (c.z - p.A2));
+  const float Ta = Tg * a;
+  acc[4] += p.G0 * Ta;
+  acc[5] += p.G1 * Ta;
+  acc[6] += p.G2 * Ta;
+  p.A0 = a * c.x + (1.0f - a) * p.A0;
+  p.A1 = a * c.y + (1.0f - a) * p.A1;
+  p.A2 = a * c.z + (1.0f - a) * p.A2;
+  acc[3] += dLda * e;
+  const float k2 = dLda * c.w * e * two_inv_s2;
+  acc[0] += k2 * dx;
+  acc[1] += k2 * dy;
+  acc[2] += k2 * r2 * inv_s;
+}
+
 __global__ void __launch_bounds__(kBT) k_blend_bwd(
     FrameParams fp, const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals,
     const uint32_t* __restrict__ emit_rank, const RenderRec* __restrict__ rec,
@@ -229,45 +291,47 @@ __global__ void __launch_bounds__(kBT) k_blend_bwd(
     const uint32_t* __restrict__ n_proc, float loss_scale, float4* __restrict__ partial,
     double* __restrict__ tile_loss) {
   __shared__ Stage st[2];
-  __shared__ float s_part[2][8][kBatch];  // [warp][value][entry]
-  __shared__ float s_red[2];
-  __shared__ uint32_t s_max[2];
+  __shared__ float s_part[kWarps][8][kBatch];  // [warp][value][entry]
+  __shared__ uint32_t s_rel[kWarps][4];
+  __shared__ float s_red[kWarps];
+  __shared__ uint32_t s_max[kWarps];
   const int tile = blockIdx.x;
   if (overflowed(total, key_cap)) {
     if (threadIdx.x == 0) tile_loss[tile] = 0.0;
     return;
   }
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const Quad q = make_quad(fp, tile);
+  const TileGeom tg = tile_geom(fp, tile);
+  const PixPair pp = pix_pair(fp, tile);
   const uint2 rg = ranges[tile];
   const int n = (int)(rg.y - rg.x);
   const int W = fp.cam.width;
 
-  float G[4][3], T[4], A[4][3];
-  uint32_t np[4];
-  bool first[4];
+  BwdPix P[2];
   float dsq = 0.0f;
   uint32_t npmax = 0;
 #pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    G[p][0] = G[p][1] = G[p][2] = 0.0f;
-    T[p] = 0.0f;
-    np[p] = 0;
-    first[p] = true;
-    A[p][0] = fp.bg[0];
-    A[p][1] = fp.bg[1];
-    A[p][2] = fp.bg[2];
-    if (q.valid[p]) {
-      const size_t pix = (size_t)(q.y0 + (p >> 1)) * W + q.x0 + (p & 1);
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const float d = img[3 * pix + c] - target[3 * pix + c];
-        dsq += d * d;
-        G[p][c] = 2.0f * d * loss_scale;
-      }
-      T[p] = t_last[pix];
-      np[p] = n_proc[pix];
-      npmax = max(npmax, np[p]);
+  for (int q = 0; q < 2; ++q) {
+    BwdPix& p = P[q];
+    p.G0 = p.G1 = p.G2 = 0.0f;
+    p.T = 0.0f;
+    p.np = 0;
+    p.first = true;
+    p.A0 = fp.bg[0];
+    p.A1 = fp.bg[1];
+    p.A2 = fp.bg[2];
+    if (q == 0 ? pp.valid0 : pp.valid1) {
+      const size_t pix = (size_t)(pp.y0 + q) * W + pp.x;
+      const float d0 = img[3 * pix + 0] - target[3 * pix + 0];
+      const float d1 = img[3 * pix + 1] - target[3 * pix + 1];
+      const float d2 = img[3 * pix + 2] - target[3 * pix + 2];
+      dsq += d0 * d0 + d1 * d1 + d2 * d2;
+      p.G0 = 2.0f * d0 * loss_scale;
+      p.G1 = 2.0f * d1 * loss_scale;
+      p.G2 = 2.0f * d2 * loss_scale;
+      p.T = t_last[pix];
+      p.np = n_proc[pix];
+      npmax = max(npmax, p.np);
     }
   }
 #pragma unroll
@@ -280,9 +344,14 @@ __global__ void __launch_bounds__(kBT) k_blend_bwd(
     s_max[w] = npmax;
   }
   __syncthreads();
-  if (threadIdx.x == 0) tile_loss[tile] = (double)s_red[0] + (double)s_red[1];
-  const int m = (int)max(s_max[0], s_max[1]);  // entries [0, m) are walked
-
+  int m = 0;
+#pragma unroll
+  for (int i = 0; i < kWarps; ++i) m = max(m, (int)s_max[i]);
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < kWarps; ++i) t += (double)s_red[i];
+    tile_loss[tile] = t;
+  }
   // entries never reached by any pixel get zero gradient slots
   for (int j = m + (int)threadIdx.x; j < n; j += kBT) {
     const uint32_t e = vals[rg.x + j];
@@ -303,68 +372,53 @@ __global__ void __launch_bounds__(kBT) k_blend_bwd(
       const int nlo = max(0, lo - kBatch);
       stage_batch(st[(it + 1) & 1], vals, emit_rank, rec, rg.x + nlo, lo - nlo);
     }
-    for (int jj = cnt - 1; jj >= 0; --jj) {
-      const int j = lo + jj;
-      const float4 g = cur.geo[jj];
-      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      bool contrib = false;
-      if (!q.warp_empty && warp_hit(q, g.x, g.y, g.z)) {
-        const float dx[2] = {__fsub_rn(q.px0, g.x), __fsub_rn(q.px1, g.x)};
-        const float dy[2] = {__fsub_rn(q.py0, g.y), __fsub_rn(q.py1, g.y)};
-        const float ax[2] = {__fmul_rn(dx[0], dx[0]), __fmul_rn(dx[1], dx[1])};
-        const float ay[2] = {__fmul_rn(dy[0], dy[0]), __fmul_rn(dy[1], dy[1])};
-        bool act[4];
-        float r2[4];
+    uint32_t rel[4];
+    warp_relevance(cur, tg, w, cnt, rel);
 #pragma unroll
-        for (int p = 0; p < 4; ++p) {
-          r2[p] = __fadd_rn(ax[p & 1], ay[p >> 1]);
-          act[p] = (uint32_t)j < np[p] && !(r2[p] > g.z);
-          contrib |= act[p];
-        }
-        if (contrib) {
-          const float4 c = cur.col[jj];
-          const float two_inv_s2 = g.w * (-2.0f * kLn2);  // 2 / sigma2d^2
-          const float inv_s = sqrtf(two_inv_s2 * 0.5f);   // 1 / sigma2d
-#pragma unroll
-          for (int p = 0; p < 4; ++p) {
-            if (!act[p]) continue;
-            const float e = fast_exp2(r2[p] * g.w);
-            const float a = c.w * e;
-            const float Tk = first[p] ? T[p] : __fdividef(T[p], 1.0f - a);
-            first[p] = false;
-            T[p] = Tk;
-            const float dLda =
-                Tk * (G[p][0] * (c.x - A[p][0]) + G[p][1] * (c.y - A[p][1]) +
-                      G[p][2] * (c.z - A[p][2]));
-            const float Ta = Tk * a;
-            acc[4] += G[p][0] * Ta;
-            acc[5] += G[p][1] * Ta;
-            acc[6] += G[p][2] * Ta;
-            A[p][0] = a * c.x + (1.0f - a) * A[p][0];
-            A[p][1] = a * c.y + (1.0f - a) * A[p][1];
-            A[p][2] = a * c.z + (1.0f - a) * A[p][2];
-            acc[3] += dLda * e;
-            const float k2 = dLda * c.w * e * two_inv_s2;
-            acc[0] += k2 * dx[p & 1];
-            acc[1] += k2 * dy[p >> 1];
-            acc[2] += k2 * r2[p] * inv_s;
-          }
-        }
-      }
-      if (__any_sync(0xffffffffu, contrib)) {
+    for (int k = 3; k >= 0; --k) {
+      uint32_t msk = rel[k];
+      while (msk) {
+        const int bit = 31 - __clz(msk);
+        msk &= ~(1u << bit);
+        const int jj = 32 * k + bit;
+        const int j = lo + jj;
+        const float4 g = cur.geo[jj];
+        const float4 c = cur.col[jj];
+        const float dx = __fsub_rn(pp.px, g.x);
+        const float ax = __fmul_rn(dx, dx);
+        const float dy0 = __fsub_rn(pp.py0, g.y), dy1 = __fsub_rn(pp.py1, g.y);
+        const float r20 = __fadd_rn(ax, __fmul_rn(dy0, dy0));
+        const float r21 = __fadd_rn(ax, __fmul_rn(dy1, dy1));
+        const bool act0 = (uint32_t)j < P[0].np && !(r20 > g.z);
+        const bool act1 = (uint32_t)j < P[1].np && !(r21 > g.z);
+        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        const float two_inv_s2 = g.w * (-2.0f * kLn2);  // 2 / sigma2d^2
+        const float inv_s = sqrtf(two_inv_s2 * 0.5f);   // 1 / sigma2d
+        bwd_pixel(P[0], act0, dx, dy0, r20, g, c, two_inv_s2, inv_s, acc);
+        bwd_pixel(P[1], act1, dx, dy1, r21, g, c, two_inv_s2, inv_s, acc);
         const float y = reduce_scatter8(acc);
         if ((lane & 3) == 0) s_part[w][lane >> 2][jj] = y;
-      } else if (lane < 8) {
-        s_part[w][lane][jj] = 0.0f;
       }
     }
+    // fix the relevance words: lanes 0..3 of warp w hold rel[k] only for k == lane
+    if (lane < 4) {
+      uint32_t r = rel[0];
+      r = lane == 1 ? rel[1] : r;
+      r = lane == 2 ? rel[2] : r;
+      r = lane == 3 ? rel[3] : r;
+      s_rel[w][lane] = r;
+    }
     __syncthreads();
-    // combine the two warps and write each (tile, splat) pair's gradient slot
+    // combine the warps and write each (tile, splat) pair's gradient slot
     if ((int)threadIdx.x < cnt) {
       const int jj = threadIdx.x;
-      float v[8];
+      float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int k = 0; k < 8; ++k) v[k] = s_part[0][k][jj] + s_part[1][k][jj];
+      for (int ww = 0; ww < kWarps; ++ww) {
+        if (!((s_rel[ww][jj >> 5] >> (jj & 31)) & 1u)) continue;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] += s_part[ww][k][jj];
+      }
       const size_t e = cur.slot[jj];
       partial[2 * e] = make_float4(v[0], v[1], v[2], v[3]);
       partial[2 * e + 1] = make_float4(v[4], v[5], v[6], 0.0f);
@@ -403,6 +457,11 @@ void launch_blend_bwd(const FrameParams& fp, const uint2* ranges, const uint32_t
                       const unsigned long long* total, int64_t key_cap, const float* img,
                       const float* target, const float* t_last, const uint32_t* n_proc,
                       float loss_scale, float4* partial, double* tile_loss, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_blend_bwd, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    attr = true;
+  }
   k_blend_bwd<<<fp.n_tiles, kBT, 0, st>>>(fp, ranges, vals, emit_rank, rec, total, key_cap, img,
                                           target, t_last, n_proc, loss_scale, partial, tile_loss);
 }
