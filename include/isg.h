@@ -146,6 +146,15 @@ isg_status isg_debug_bins(isg_ctx* ctx, uint64_t* keys, uint32_t* vals, int64_t*
  * and number of list entries processed (both H x W). */
 isg_status isg_debug_pixel_state(isg_ctx* ctx, float* t_last, uint32_t* n_proc);
 
+/* ---- binning strategy (both produce bit-identical tile lists) ----------------------------
+ * TILE_BUCKET (default): per-tile counters + bucket fill + per-tile bitonic sort by
+ *   (depth bits, splat index) in shared memory.
+ * RADIX: onesweep LSD radix sort of (depth, splat), tile-key emission in depth order and a
+ *   stable onesweep radix sort of (tile, pair). */
+#define ISG_BINNING_TILE_BUCKET 0
+#define ISG_BINNING_RADIX 1
+isg_status isg_set_binning(isg_ctx* ctx, int mode);
+
 /* ---- stage timing (CUDA events on the context stream; for bench.py's roofline) ---------- */
 isg_status isg_profile_enable(isg_ctx* ctx, int on);
 int isg_profile_num_stages(void);

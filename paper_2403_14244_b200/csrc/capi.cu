@@ -24,12 +24,14 @@
 // Stage timing (isg_profile_*): CUDA events around each kernel of a frame, on the launching
 // stream, so bench.py can report the dominant kernel's live launch duration.
 enum Stage {
-  ST_MEMSET, ST_PREPROCESS, ST_DEPTH_SORT, ST_SCAN_EMIT, ST_TILE_SORT, ST_RANGES, ST_BLEND_FWD,
-  ST_BLEND_BWD, ST_LOSS_REDUCE, ST_PROJECT_BWD, ST_PROJECT_ADAM, ST_ADAM, ST_ALLREDUCE, ST_COUNT
+  ST_MEMSET, ST_PREPROCESS, ST_DEPTH_SORT, ST_SCAN_EMIT, ST_TILE_SCAN, ST_FILL, ST_TILE_SORT,
+  ST_RANGES, ST_BLEND_FWD, ST_BLEND_BWD, ST_LOSS_REDUCE, ST_PROJECT_BWD, ST_PROJECT_ADAM, ST_ADAM,
+  ST_ALLREDUCE, ST_COUNT
 };
 static const char* kStageNames[ST_COUNT] = {
-    "memset", "preprocess", "depth_sort", "scan_emit", "tile_sort", "ranges", "blend_fwd",
-    "blend_bwd", "loss_reduce", "project_bwd", "project_adam", "adam", "allreduce"};
+    "memset", "preprocess", "depth_sort", "scan_emit", "tile_scan", "fill", "tile_sort",
+    "ranges", "blend_fwd", "blend_bwd", "loss_reduce", "project_bwd", "project_adam", "adam",
+    "allreduce"};
 
 
 
@@ -48,28 +50,31 @@ struct isg_ctx {
   int64_t adam_t = 0;
 
   // per-splat work buffers
-  float4* rec_geo = nullptr;
-  uint32_t* depth[2] = {nullptr, nullptr};
+  isg::RenderRec* rec = nullptr;  // 32-B render record per splat
+  uint32_t* ntiles = nullptr;     // tiles touched per splat
+  uint32_t* slot_off = nullptr;   // start of splat g's gradient-slot list
+  float4* grad3d = nullptr;       // n x 2, indexed by splat
+  uint32_t* depth[2] = {nullptr, nullptr};  // radix mode: depth keys / depth order
   uint32_t* order[2] = {nullptr, nullptr};
-  uint32_t* ntiles = nullptr;
-  uint32_t* emit_off = nullptr;  // first emission slot of splat g
-  isg::RenderRec* rec_sorted = nullptr;
-  float4* grad3d = nullptr;  // n x 2, indexed by splat
-  int order_buf = 0;         // which order[] holds the depth order
+  int order_buf = 0;
 
   // (tile, splat) pairs, key_cap slots
+  int binning = isg::kBinTileBucket;
   int64_t key_cap = 0;
-  uint32_t* tkey[2] = {nullptr, nullptr};
-  uint32_t* tval[2] = {nullptr, nullptr};  // emission slots, sorted by (tile, depth, index)
-  uint32_t* emit_rank = nullptr;           // depth rank of the pair in slot e
-  float4* partial = nullptr;               // 2D gradient of the pair in slot e (2 x float4)
+  uint2* sorted = nullptr;                  // per list entry: (splat, gradient slot)
+  float4* partial = nullptr;                // gradient slot: 2D grads of one pair (2 x float4)
+  unsigned long long* bucket = nullptr;     // tile-bucket mode: (depth << 32 | splat), unsorted
+  uint32_t* slot_of = nullptr;              // tile-bucket mode: slot lists per splat
+  uint32_t* tkey[2] = {nullptr, nullptr};   // radix mode: tile keys
+  uint32_t* tval[2] = {nullptr, nullptr};   // radix mode: emission indices
+  uint32_t* emit_gid = nullptr;             // radix mode: splat of emission index e
   int tile_buf = 0;
+  bool radix_alloc = false;
 
   // sort / scan scratch
   isg::SortScratch sort{};
   int64_t sort_tiles_alloc = 0;
   unsigned long long* scan_scratch = nullptr;
-  int64_t scan_words_alloc = 0;
 
   // pixels / tiles
   int64_t pix_alloc = 0, tiles_alloc = 0;
@@ -78,9 +83,11 @@ struct isg_ctx {
   float* t_last = nullptr;
   uint32_t* n_proc = nullptr;
   uint2* ranges = nullptr;
+  uint32_t* tile_cnt = nullptr;
+  uint32_t* cursor = nullptr;
   double* tile_loss = nullptr;
 
-  // device scalars: [0] n_keys [1] first_bad [2] n_visible [3] scan counter [4] depth count
+  // device scalars: [0] n_keys [1] first_bad [2] n_visible [3] scan tile counter [4] n
   uint32_t* sc = nullptr;
   unsigned long long* total = nullptr;     // [0] total keys, [1] skipped updates
   double* loss = nullptr;                  // [0] accumulated, [1] last view
@@ -191,18 +198,19 @@ isg_status ensure_scene(isg_ctx* ctx, int64_t n) {
   ISG_CUDA(realloc_dev(&ctx->co, a));
   ISG_CUDA(realloc_dev(&ctx->m, 2 * a));
   ISG_CUDA(realloc_dev(&ctx->v, 2 * a));
-  ISG_CUDA(realloc_dev(&ctx->rec_geo, a));
-  for (int i = 0; i < 2; ++i) {
-    ISG_CUDA(realloc_dev(&ctx->depth[i], a));
-    ISG_CUDA(realloc_dev(&ctx->order[i], a));
-  }
+  ISG_CUDA(realloc_dev(&ctx->rec, a));
   ISG_CUDA(realloc_dev(&ctx->ntiles, a));
-  ISG_CUDA(realloc_dev(&ctx->emit_off, a));
-  ISG_CUDA(realloc_dev(&ctx->rec_sorted, a));
+  ISG_CUDA(realloc_dev(&ctx->slot_off, a));
   ISG_CUDA(realloc_dev(&ctx->grad3d, 2 * a));
-  const int64_t words = isg::scan_emit_scratch_words(a) + 1;
+  if (ctx->radix_alloc) {
+    for (int i = 0; i < 2; ++i) {
+      ISG_CUDA(realloc_dev(&ctx->depth[i], a));
+      ISG_CUDA(realloc_dev(&ctx->order[i], a));
+    }
+  }
+  const int64_t words =
+      std::max(isg::scan_emit_scratch_words(a), isg::fill_scratch_words(a)) + 1;
   ISG_CUDA(realloc_dev(&ctx->scan_scratch, words));
-  ctx->scan_words_alloc = words;
   ctx->n_alloc = a;
   return ISG_OK;
 }
@@ -221,13 +229,38 @@ isg_status ensure_sort_scratch(isg_ctx* ctx, int64_t cap) {
 
 isg_status ensure_keys(isg_ctx* ctx, int64_t cap) {
   if (cap <= ctx->key_cap) return ISG_OK;
-  for (int i = 0; i < 2; ++i) {
-    ISG_CUDA(realloc_dev(&ctx->tkey[i], cap));
-    ISG_CUDA(realloc_dev(&ctx->tval[i], cap));
-  }
-  ISG_CUDA(realloc_dev(&ctx->emit_rank, cap));
+  ISG_CUDA(realloc_dev(&ctx->sorted, cap));
   ISG_CUDA(realloc_dev(&ctx->partial, 2 * cap));
+  ISG_CUDA(realloc_dev(&ctx->bucket, cap));
+  ISG_CUDA(realloc_dev(&ctx->slot_of, cap));
+  if (ctx->radix_alloc) {
+    for (int i = 0; i < 2; ++i) {
+      ISG_CUDA(realloc_dev(&ctx->tkey[i], cap));
+      ISG_CUDA(realloc_dev(&ctx->tval[i], cap));
+    }
+    ISG_CUDA(realloc_dev(&ctx->emit_gid, cap));
+  }
   ctx->key_cap = cap;
+  return ISG_OK;
+}
+
+// Radix binning needs its own buffers (allocated on first use).
+isg_status ensure_radix(isg_ctx* ctx) {
+  if (ctx->radix_alloc) return ISG_OK;
+  ctx->radix_alloc = true;
+  const int64_t a = ctx->n_alloc, cap = ctx->key_cap;
+  if (a > 0)
+    for (int i = 0; i < 2; ++i) {
+      ISG_CUDA(realloc_dev(&ctx->depth[i], a));
+      ISG_CUDA(realloc_dev(&ctx->order[i], a));
+    }
+  if (cap > 0) {
+    for (int i = 0; i < 2; ++i) {
+      ISG_CUDA(realloc_dev(&ctx->tkey[i], cap));
+      ISG_CUDA(realloc_dev(&ctx->tval[i], cap));
+    }
+    ISG_CUDA(realloc_dev(&ctx->emit_gid, cap));
+  }
   return ISG_OK;
 }
 
@@ -244,6 +277,8 @@ isg_status ensure_pixels(isg_ctx* ctx, int W, int H) {
   }
   if (tiles > ctx->tiles_alloc) {
     ISG_CUDA(realloc_dev(&ctx->ranges, tiles));
+    ISG_CUDA(realloc_dev(&ctx->tile_cnt, tiles));
+    ISG_CUDA(realloc_dev(&ctx->cursor, tiles));
     ISG_CUDA(realloc_dev(&ctx->tile_loss, tiles));
     ctx->tiles_alloc = tiles;
   }
@@ -287,12 +322,17 @@ FrameParams make_fp(const isg_camera* cam, const float bg[3], float t_min) {
   return fp;
 }
 
+// Splat slot lists: explicit in tile-bucket mode, contiguous (null) in radix mode.
+const uint32_t* slot_list(const isg_ctx* ctx) {
+  return ctx->binning == isg::kBinRadix ? nullptr : ctx->slot_of;
+}
+
 // Project a pending view's 2D gradients into the 3D accumulator (K8a).
 isg_status flush_pending(isg_ctx* ctx) {
   if (!ctx->pending) return ISG_OK;
   ISG_STAGE(ST_PROJECT_BWD);
-  isg::launch_project_backward(ctx->ms, ctx->n, ctx->pending_fp, ctx->emit_off, ctx->ntiles,
-                               ctx->partial, ctx->total, ctx->key_cap, ctx->grad3d,
+  isg::launch_project_backward(ctx->ms, ctx->n, ctx->pending_fp, ctx->slot_off, slot_list(ctx),
+                               ctx->ntiles, ctx->partial, ctx->total, ctx->key_cap, ctx->grad3d,
                                !ctx->grad3d_valid, ctx->stream);
   ISG_CHECK_LAUNCH();
   ctx->launches++;
@@ -312,26 +352,32 @@ isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out) {
     if ((s = ensure_keys(ctx, std::max<int64_t>(6 * ctx->n, 1 << 20))) != ISG_OK) return s;
   }
   if ((s = ensure_sort_scratch(ctx, std::max(ctx->key_cap, ctx->n))) != ISG_OK) return s;
+  const bool radix = ctx->binning == isg::kBinRadix;
+  if (radix && (s = ensure_radix(ctx)) != ISG_OK) return s;
   cudaStream_t st = ctx->stream;
   const int64_t n = ctx->n;
-  // scalars: n_keys=0, first_bad=~0, n_visible=0, scan counter=0
   {
   ISG_STAGE(ST_MEMSET);
+  // scalars: n_keys=0, first_bad=~0, n_visible=0, scan counter=0
   ISG_CUDA(cudaMemsetAsync(ctx->sc, 0, sizeof(uint32_t) * 8, st));
   ISG_CUDA(cudaMemsetAsync(ctx->sc + 1, 0xFF, sizeof(uint32_t), st));
   ISG_CUDA(cudaMemsetAsync(ctx->total, 0, sizeof(unsigned long long), st));
-  ISG_CUDA(cudaMemsetAsync(ctx->scan_scratch, 0,
-                           sizeof(unsigned long long) * (isg::scan_emit_scratch_words(n) + 1), st));
-  ISG_CUDA(cudaMemsetAsync(ctx->ranges, 0, sizeof(uint2) * fp.n_tiles, st));
+  const int64_t words =
+      (radix ? isg::scan_emit_scratch_words(n) : isg::fill_scratch_words(n)) + 1;
+  ISG_CUDA(cudaMemsetAsync(ctx->scan_scratch, 0, sizeof(unsigned long long) * words, st));
+  if (radix)
+    ISG_CUDA(cudaMemsetAsync(ctx->ranges, 0, sizeof(uint2) * fp.n_tiles, st));
+  else
+    ISG_CUDA(cudaMemsetAsync(ctx->tile_cnt, 0, sizeof(uint32_t) * fp.n_tiles, st));
   }
   {
   ISG_STAGE(ST_PREPROCESS);
-  isg::launch_preprocess(ctx->ms, ctx->co, n, fp, ctx->rec_geo, ctx->depth[0], ctx->ntiles,
-                         ctx->sc + 1, ctx->sc + 4, st);
+  isg::launch_preprocess(ctx->ms, ctx->co, n, fp, ctx->rec, radix ? ctx->depth[0] : nullptr,
+                         ctx->ntiles, radix ? nullptr : ctx->tile_cnt, ctx->sc, st);
   ISG_CHECK_LAUNCH();
   ctx->launches++;
   }
-  if (n > 0) {
+  if (radix && n > 0) {
     {
     ISG_STAGE(ST_DEPTH_SORT);
     ctx->order_buf = isg::radix_sort_pairs(ctx->depth, ctx->order, true, ctx->sc + 4, n, 32,
@@ -340,10 +386,9 @@ isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out) {
     }
     {
     ISG_STAGE(ST_SCAN_EMIT);
-    isg::launch_scan_emit(ctx->order[ctx->order_buf], ctx->ntiles, ctx->rec_geo, ctx->co, n, fp,
-                          ctx->rec_sorted, ctx->emit_off, ctx->tkey[0], ctx->emit_rank,
-                          ctx->key_cap, ctx->scan_scratch, ctx->sc + 3, ctx->sc + 0, ctx->total,
-                          ctx->sc + 2, st);
+    isg::launch_scan_emit(ctx->order[ctx->order_buf], ctx->ntiles, ctx->ms, n, fp, ctx->slot_off,
+                          ctx->tkey[0], ctx->emit_gid, ctx->key_cap, ctx->scan_scratch,
+                          ctx->sc + 3, ctx->sc + 0, ctx->total, st);
     ISG_CHECK_LAUNCH();
     ctx->launches++;
     }
@@ -354,14 +399,36 @@ isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out) {
     ISG_CHECK_LAUNCH();
     }
     ISG_STAGE(ST_RANGES);
-    isg::launch_ranges(ctx->tkey[ctx->tile_buf], ctx->sc + 0, ctx->key_cap, ctx->ranges, st);
+    isg::launch_ranges(ctx->tkey[ctx->tile_buf], ctx->tval[ctx->tile_buf], ctx->emit_gid,
+                       ctx->sc + 0, ctx->key_cap, ctx->ranges, ctx->sorted, st);
     ISG_CHECK_LAUNCH();
     ctx->launches++;
+  } else if (!radix) {
+    {
+    ISG_STAGE(ST_TILE_SCAN);
+    isg::launch_tile_scan(ctx->tile_cnt, fp.n_tiles, ctx->key_cap, ctx->ranges, ctx->cursor,
+                          ctx->sc + 0, ctx->total, st);
+    ISG_CHECK_LAUNCH();
+    ctx->launches++;
+    }
+    if (n > 0) {
+      ISG_STAGE(ST_FILL);
+      isg::launch_fill(ctx->ms, ctx->ntiles, n, fp, ctx->cursor, ctx->bucket, ctx->slot_of,
+                       ctx->slot_off, ctx->key_cap, ctx->scan_scratch, ctx->sc + 3, st);
+      ISG_CHECK_LAUNCH();
+      ctx->launches++;
+    }
+    {
+    ISG_STAGE(ST_TILE_SORT);
+    isg::launch_tile_sort(fp, ctx->ranges, ctx->bucket, ctx->total, ctx->key_cap, ctx->sorted,
+                          ctx->partial, st);
+    ISG_CHECK_LAUNCH();
+    ctx->launches++;
+    }
   }
   ISG_STAGE(ST_BLEND_FWD);
-  isg::launch_blend_fwd(fp, ctx->ranges, ctx->tval[ctx->tile_buf], ctx->emit_rank,
-                        ctx->rec_sorted, ctx->total, ctx->key_cap, out, ctx->t_last, ctx->n_proc,
-                        st);
+  isg::launch_blend_fwd(fp, ctx->ranges, ctx->sorted, ctx->rec, ctx->total, ctx->key_cap, out,
+                        ctx->t_last, ctx->n_proc, st);
   ISG_CHECK_LAUNCH();
   ctx->launches++;
   ctx->have_frame = true;
@@ -417,10 +484,9 @@ isg_status run_backward(isg_ctx* ctx, const FrameParams& fp, const float* target
   const float scale = weight / (3.0f * (float)fp.cam.width * (float)fp.cam.height);
   {
   ISG_STAGE(ST_BLEND_BWD);
-  isg::launch_blend_bwd(fp, ctx->ranges, ctx->tval[ctx->tile_buf], ctx->emit_rank,
-                        ctx->rec_sorted, ctx->total, ctx->key_cap, ctx->img, target_dev,
-                        ctx->t_last, ctx->n_proc, scale, ctx->partial, ctx->tile_loss,
-                        ctx->stream);
+  isg::launch_blend_bwd(fp, ctx->ranges, ctx->sorted, ctx->rec, ctx->total, ctx->key_cap,
+                        ctx->img, target_dev, ctx->t_last, ctx->n_proc, scale, ctx->partial,
+                        ctx->tile_loss, ctx->stream);
   ISG_CHECK_LAUNCH();
   }
   ISG_STAGE(ST_LOSS_REDUCE);
@@ -509,13 +575,13 @@ void isg_destroy(isg_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->nccl_comm) isg_nccl_detach(ctx);
-  void* dev[] = {ctx->ms, ctx->co, ctx->m, ctx->v, ctx->rec_geo, ctx->depth[0], ctx->depth[1],
-                 ctx->order[0], ctx->order[1], ctx->ntiles, ctx->emit_off, ctx->rec_sorted,
-                 ctx->emit_rank, ctx->partial, ctx->grad3d, ctx->tkey[0], ctx->tkey[1],
-                 ctx->tval[0], ctx->tval[1],
-                 ctx->sort.hist, ctx->sort.lookback, ctx->sort.counters, ctx->scan_scratch,
-                 ctx->img, ctx->target, ctx->t_last, ctx->n_proc, ctx->ranges, ctx->tile_loss,
-                 ctx->sc, ctx->total, ctx->loss};
+  void* dev[] = {ctx->ms, ctx->co, ctx->m, ctx->v, ctx->rec, ctx->ntiles, ctx->slot_off,
+                 ctx->grad3d, ctx->depth[0], ctx->depth[1], ctx->order[0], ctx->order[1],
+                 ctx->sorted, ctx->partial, ctx->bucket, ctx->slot_of, ctx->tkey[0], ctx->tkey[1],
+                 ctx->tval[0], ctx->tval[1], ctx->emit_gid, ctx->sort.hist, ctx->sort.lookback,
+                 ctx->sort.counters, ctx->scan_scratch, ctx->img, ctx->target, ctx->t_last,
+                 ctx->n_proc, ctx->ranges, ctx->tile_cnt, ctx->cursor, ctx->tile_loss, ctx->sc,
+                 ctx->total, ctx->loss};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (ctx->h_sc) cudaFreeHost(ctx->h_sc);
@@ -775,9 +841,9 @@ isg_status isg_adam_step(isg_ctx* ctx, const float lr[4], float b1, float b2, fl
   if (ctx->pending && !ctx->grad3d_valid && !ctx->nccl_comm) {
     // single view since the last step: projection backward fused with Adam (K8)
     ISG_STAGE(ST_PROJECT_ADAM);
-    isg::launch_project_adam(ctx->ms, ctx->co, ctx->n, ctx->pending_fp, ctx->emit_off,
-                             ctx->ntiles, ctx->partial, ctx->total, ctx->key_cap, ctx->m, ctx->v,
-                             ap, ctx->total + 1, ctx->stream);
+    isg::launch_project_adam(ctx->ms, ctx->co, ctx->n, ctx->pending_fp, ctx->slot_off,
+                             slot_list(ctx), ctx->ntiles, ctx->partial, ctx->total, ctx->key_cap,
+                             ctx->m, ctx->v, ap, ctx->total + 1, ctx->stream);
     ISG_CHECK_LAUNCH();
     ctx->launches++;
     ctx->pending = false;
@@ -817,8 +883,7 @@ isg_status isg_debug_bins(isg_ctx* ctx, uint64_t* keys, uint32_t* vals, int64_t*
     uint32_t* dv = nullptr;
     ISG_CUDA(cudaMalloc(&dk, sizeof(uint64_t) * nk));
     ISG_CUDA(cudaMalloc(&dv, sizeof(uint32_t) * nk));
-    isg::launch_debug_keys(ctx->tkey[ctx->tile_buf], ctx->tval[ctx->tile_buf], ctx->emit_rank,
-                           ctx->order[ctx->order_buf], ctx->ms, fp, nk, dk, dv, ctx->stream);
+    isg::launch_debug_keys(ctx->ranges, ctx->sorted, ctx->ms, fp, dk, dv, ctx->stream);
     if (keys) cudaMemcpyAsync(keys, dk, sizeof(uint64_t) * nk, cudaMemcpyDeviceToHost, ctx->stream);
     if (vals) cudaMemcpyAsync(vals, dv, sizeof(uint32_t) * nk, cudaMemcpyDeviceToHost, ctx->stream);
     cudaStreamSynchronize(ctx->stream);
@@ -830,6 +895,18 @@ isg_status isg_debug_bins(isg_ctx* ctx, uint64_t* keys, uint32_t* vals, int64_t*
                              ctx->stream));
   ISG_CUDA(cudaStreamSynchronize(ctx->stream));
   ISG_CUDA(cudaGetLastError());
+  return ISG_OK;
+}
+
+isg_status isg_set_binning(isg_ctx* ctx, int mode) {
+  if (!ctx) return ISG_E_ARG;
+  if (mode != ISG_BINNING_TILE_BUCKET && mode != ISG_BINNING_RADIX)
+    return fail(ctx, ISG_E_ARG, "set_binning: unknown mode");
+  cudaSetDevice(ctx->device);
+  isg_status s = flush_pending(ctx);  // slot lists of a pending view are mode-specific
+  if (s != ISG_OK) return s;
+  ctx->binning = mode;
+  ctx->have_frame = false;
   return ISG_OK;
 }
 

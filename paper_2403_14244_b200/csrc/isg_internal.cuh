@@ -1,15 +1,16 @@
 // isg_internal.cuh — shared definitions of the sm_100a kernels and the C-ABI layer.
 //
 // Pipeline of one view (all on one stream, no host sync inside a frame):
-//   K1  k_preprocess      per splat: validate, project, 3-sigma radius, tile count, depth key
-//   K4a radix sort        (depth key, splat) over all splats           -> depth order
-//   K2/3 k_scan_emit      decoupled look-back scan of tile counts in depth order, gather of
-//                         the depth-ordered render records, emission of (tile, rank) pairs
-//   K4b radix sort        (tile, rank) pairs, stable                   -> per-tile depth order
-//   K5  k_ranges          per-tile [start, end)
+//   K1  k_preprocess      per splat: validate, project, 3-sigma radius, tile count, 32-B record
+//   binning (two interchangeable modes, identical output):
+//     tile-bucket (default)  K2 k_tile_scan -> K3 k_fill -> K4 k_tile_sort   (k_bin.cu)
+//     radix                  onesweep depth sort -> k_scan_emit -> onesweep tile sort ->
+//                            k_ranges                                        (k_sort.cu)
+//     output: per-tile ranges and, per list entry, (splat, gradient slot) in (depth, index)
+//     order; per splat, the list of its gradient slots.
 //   K6  k_blend_fwd       16x16-tile front-to-back blend with early termination
-//   K7  k_blend_bwd       reverse walk + fused L2 gradient, per-splat 2D grads
-//   K8  k_project_adam    projection backward (+ Adam when fused)
+//   K7  k_blend_bwd       reverse walk + fused L2 gradient -> per-(tile, splat) gradient slots
+//   K8  k_project_adam    per-splat slot sum, projection backward (+ Adam when fused)
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -22,6 +23,8 @@ constexpr int kTile = ISG_TILE;
 constexpr int kTilePixels = kTile * kTile;
 constexpr float kNearPlane = 1e-3f;  // splat3d.hpp:55
 
+enum BinningMode { kBinTileBucket = 0, kBinRadix = 1 };
+
 // ---- per-frame constant parameters --------------------------------------------------------
 struct FrameParams {
   isg_camera cam;
@@ -30,8 +33,8 @@ struct FrameParams {
   float t_min;
 };
 
-// Render record of one visible splat, gathered into depth order (32 B, two float4):
-//   geo = (u, v, sigma2d, r2max = (9*sigma2d)*sigma2d),   col = (r, g, b, opacity)
+// Render record of one splat, indexed by splat (32 B, two float4):
+//   geo = (u, v, r2max = (9*sigma2d)*sigma2d, -log2(e)/sigma2d^2),  col = (r, g, b, opacity)
 struct __align__(16) RenderRec {
   float4 geo;
   float4 col;
@@ -59,44 +62,54 @@ int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], bool iota_vals, const
                      int64_t cap, int key_bits, SortScratch& s, cudaStream_t st,
                      int64_t* launches);
 
-// ---- launchers ----------------------------------------------------------------------------
-// K1.  Also writes *n_dev = n (device-side count for the depth sort).
+// ---- K1 ------------------------------------------------------------------------------------
+// sc: [1] first invalid splat (atomicMin), [2] visible splats, [4] n.  depth_key (radix mode)
+// and tile_cnt (tile-bucket mode) may be null.
 void launch_preprocess(const float4* ms, const float4* co, int64_t n, const FrameParams& fp,
-                       float4* rec_geo, uint32_t* depth_key, uint32_t* ntiles,
-                       uint32_t* first_bad, uint32_t* n_dev, cudaStream_t st);
+                       RenderRec* rec, uint32_t* depth_key, uint32_t* ntiles, uint32_t* tile_cnt,
+                       uint32_t* sc, cudaStream_t st);
 
-// K2/K3: scan of ntiles in depth order, record gather, emission of the (tile, splat) pairs.
-// Pair e (the emission slot) gets tile_keys[e] = tile and emit_rank[e] = depth rank; splat g's
-// pairs occupy slots [emit_off[g], emit_off[g] + ntiles[g]).
-// scratch: scan_emit_scratch_words(n) + 1 zeroed u64 words; counter: zeroed u32.
-int64_t scan_emit_scratch_words(int64_t n);
-void launch_scan_emit(const uint32_t* order, const uint32_t* ntiles, const float4* rec_geo,
-                      const float4* co, int64_t n, const FrameParams& fp, RenderRec* rec_sorted,
-                      uint32_t* emit_off, uint32_t* tile_keys, uint32_t* emit_rank,
-                      int64_t key_cap, unsigned long long* scratch, uint32_t* counter,
-                      uint32_t* n_keys, unsigned long long* n_keys_total, uint32_t* n_visible,
+// ---- tile-bucket binning (k_bin.cu) -------------------------------------------------------
+int64_t fill_scratch_words(int64_t n);  // + 1 zeroed u64 words of look-back scratch
+void launch_tile_scan(const uint32_t* cnt, int n_tiles, int64_t cap, uint2* ranges,
+                      uint32_t* cursor, uint32_t* n_keys, unsigned long long* total,
+                      cudaStream_t st);
+void launch_fill(const float4* ms, const uint32_t* ntiles, int64_t n, const FrameParams& fp,
+                 uint32_t* cursor, unsigned long long* bucket, uint32_t* slot_of,
+                 uint32_t* slot_off, int64_t cap, unsigned long long* lookback, uint32_t* counter,
+                 cudaStream_t st);
+// scratch: the gradient-slot buffer (2 float4 per key), used only for tiles > 2048 entries.
+void launch_tile_sort(const FrameParams& fp, const uint2* ranges, const unsigned long long* bucket,
+                      const unsigned long long* total, int64_t cap, uint2* sorted, float4* scratch,
                       cudaStream_t st);
 
-void launch_ranges(const uint32_t* sorted_tiles, const uint32_t* n_keys, int64_t key_cap,
-                   uint2* ranges, cudaStream_t st);
+// ---- radix binning (k_sort.cu) ------------------------------------------------------------
+int64_t scan_emit_scratch_words(int64_t n);  // + 1 zeroed u64 words
+void launch_scan_emit(const uint32_t* order, const uint32_t* ntiles, const float4* ms, int64_t n,
+                      const FrameParams& fp, uint32_t* slot_off, uint32_t* tile_keys,
+                      uint32_t* emit_gid, int64_t key_cap, unsigned long long* scratch,
+                      uint32_t* counter, uint32_t* n_keys, unsigned long long* n_keys_total,
+                      cudaStream_t st);
+void launch_ranges(const uint32_t* sorted_tiles, const uint32_t* e_sorted,
+                   const uint32_t* emit_gid, const uint32_t* n_keys, int64_t key_cap,
+                   uint2* ranges, uint2* sorted, cudaStream_t st);
 
-// K6.  vals: emission slots sorted by (tile, depth, index).
-void launch_blend_fwd(const FrameParams& fp, const uint2* ranges, const uint32_t* vals,
-                      const uint32_t* emit_rank, const RenderRec* rec,
-                      const unsigned long long* total, int64_t key_cap, float* out, float* t_last,
-                      uint32_t* n_proc, cudaStream_t st);
-
-// K7.  Writes every pair's 2D gradient to partial[2e], partial[2e+1] (emission slot e).
-void launch_blend_bwd(const FrameParams& fp, const uint2* ranges, const uint32_t* vals,
-                      const uint32_t* emit_rank, const RenderRec* rec,
-                      const unsigned long long* total, int64_t key_cap, const float* img,
-                      const float* target, const float* t_last, const uint32_t* n_proc,
-                      float loss_scale, float4* partial, double* tile_loss, cudaStream_t st);
-
+// ---- blending (k_blend.cu) ----------------------------------------------------------------
+// sorted: per list entry (splat, gradient slot), tile-major, (depth, index) order per tile.
+void launch_blend_fwd(const FrameParams& fp, const uint2* ranges, const uint2* sorted,
+                      const RenderRec* rec, const unsigned long long* total, int64_t key_cap,
+                      float* out, float* t_last, uint32_t* n_proc, cudaStream_t st);
+// Writes every pair's 2D gradient to partial[2 slot], partial[2 slot + 1].
+void launch_blend_bwd(const FrameParams& fp, const uint2* ranges, const uint2* sorted,
+                      const RenderRec* rec, const unsigned long long* total, int64_t key_cap,
+                      const float* img, const float* target, const float* t_last,
+                      const uint32_t* n_proc, float loss_scale, float4* partial,
+                      double* tile_loss, cudaStream_t st);
 // loss[0] += scale * sum(tile_loss), loss[1] = scale * sum(tile_loss)
 void launch_loss_reduce(const double* tile_loss, int n_tiles, double scale, double* loss,
                         cudaStream_t st);
 
+// ---- optimizer (k_adam.cu) ----------------------------------------------------------------
 struct AdamParams {
   float lr[4];
   float b1, b2, eps;
@@ -104,22 +117,25 @@ struct AdamParams {
   float bc2_sqrt;      // sqrt(1 - b2^t)
 };
 
+// Splat g's slots: slot_of[slot_off[g] + k] (or slot_off[g] + k when slot_of is null).
 // K8a: 2D grads of one view -> 3D grads (overwrite when `first`, else accumulate).
 void launch_project_backward(const float4* ms, int64_t n, const FrameParams& fp,
-                             const uint32_t* emit_off, const uint32_t* ntiles,
-                             const float4* partial, const unsigned long long* total, int64_t cap,
-                             float4* grad3d, bool first, cudaStream_t st);
+                             const uint32_t* slot_off, const uint32_t* slot_of,
+                             const uint32_t* ntiles, const float4* partial,
+                             const unsigned long long* total, int64_t cap, float4* grad3d,
+                             bool first, cudaStream_t st);
 // K8 fused: 2D grads of one view -> 3D -> Adam.
 void launch_project_adam(float4* ms, float4* co, int64_t n, const FrameParams& fp,
-                         const uint32_t* emit_off, const uint32_t* ntiles, const float4* partial,
+                         const uint32_t* slot_off, const uint32_t* slot_of,
+                         const uint32_t* ntiles, const float4* partial,
                          const unsigned long long* total, int64_t cap, float4* m, float4* v,
                          const AdamParams& ap, unsigned long long* skipped, cudaStream_t st);
 // K8b: Adam from accumulated 3D grads.
 void launch_adam(float4* ms, float4* co, int64_t n, const float4* grad3d, float4* m, float4* v,
                  const AdamParams& ap, unsigned long long* skipped, cudaStream_t st);
 
-void launch_debug_keys(const uint32_t* tiles, const uint32_t* slots, const uint32_t* emit_rank,
-                       const uint32_t* order, const float4* ms, const FrameParams& fp,
-                       int64_t nkeys, uint64_t* keys, uint32_t* gids, cudaStream_t st);
+// ---- parity hook -------------------------------------------------------------------------
+void launch_debug_keys(const uint2* ranges, const uint2* sorted, const float4* ms,
+                       const FrameParams& fp, uint64_t* keys, uint32_t* gids, cudaStream_t st);
 
 }  // namespace isg

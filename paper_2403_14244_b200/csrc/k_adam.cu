@@ -1,8 +1,10 @@
 // K8 — projection backward and the fused Adam step.
 //
 // Each splat's 2D gradient (du, dv, dsigma2d, dopacity, drgb) is the sum of its (tile, splat)
-// slots written by K7; they are contiguous in emission order ([emit_off[g], + ntiles[g]) ) and
-// summed in that fixed order, so gradients are bitwise deterministic (no atomics anywhere).
+// gradient slots written by K7.  Splat g's slots are listed at slot_of[slot_off[g] + k],
+// k < ntiles[g], in emission (row-major tile) order — or are the contiguous range
+// [slot_off[g], + ntiles[g]) when slot_of is null (radix binning) — and are summed in that
+// fixed order, so gradients are bitwise deterministic (no atomics anywhere).
 //
 // Projection backward: chain rule through u = f x/z + cx, v = f y/z + cy, s = sigma f/z
 // (Jacobian: projection_jacobian, /root/reference/proj/src/splat3d.cpp:39-47; closed forms of
@@ -18,13 +20,15 @@ namespace isg {
 
 namespace {
 
-__device__ __forceinline__ void sum_slots(const float4* __restrict__ partial, uint32_t off,
+__device__ __forceinline__ void sum_slots(const float4* __restrict__ partial,
+                                          const uint32_t* __restrict__ slot_of, uint32_t off,
                                           uint32_t cnt, float4& a, float4& b) {
   a = make_float4(0.f, 0.f, 0.f, 0.f);
   b = make_float4(0.f, 0.f, 0.f, 0.f);
   for (uint32_t k = 0; k < cnt; ++k) {
-    const float4 x = partial[2 * (size_t)(off + k)];
-    const float4 y = partial[2 * (size_t)(off + k) + 1];
+    const size_t e = slot_of ? slot_of[off + k] : (size_t)(off + k);
+    const float4 x = partial[2 * e];
+    const float4 y = partial[2 * e + 1];
     a.x += x.x;
     a.y += x.y;
     a.z += x.z;
@@ -94,15 +98,16 @@ __device__ __forceinline__ void adam_update(float4* __restrict__ ms, float4* __r
 }  // namespace
 
 __global__ void __launch_bounds__(256) k_project_backward(
-    const float4* __restrict__ ms, int64_t n, FrameParams fp, const uint32_t* __restrict__ emit_off,
-    const uint32_t* __restrict__ ntiles, const float4* __restrict__ partial,
+    const float4* __restrict__ ms, int64_t n, FrameParams fp, const uint32_t* __restrict__ slot_off,
+    const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ ntiles,
+    const float4* __restrict__ partial,
     const unsigned long long* __restrict__ total, int64_t cap, float4* __restrict__ grad3d,
     bool first) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const bool ov = *total > (unsigned long long)cap;  // frame was skipped: contributes nothing
   float4 a, b;
-  sum_slots(partial, emit_off[i], ov ? 0u : ntiles[i], a, b);
+  sum_slots(partial, slot_of, slot_off[i], ov ? 0u : ntiles[i], a, b);
   float o[8];
   grad3d_of(ms[i], fp.cam, a, b, o);
   float4 g0 = make_float4(o[0], o[1], o[2], o[3]), g1 = make_float4(o[4], o[5], o[6], o[7]);
@@ -117,15 +122,16 @@ __global__ void __launch_bounds__(256) k_project_backward(
 
 __global__ void __launch_bounds__(256) k_project_adam(
     float4* __restrict__ ms, float4* __restrict__ co, int64_t n, FrameParams fp,
-    const uint32_t* __restrict__ emit_off, const uint32_t* __restrict__ ntiles,
-    const float4* __restrict__ partial, const unsigned long long* __restrict__ total, int64_t cap,
-    float4* __restrict__ m, float4* __restrict__ v, AdamParams ap,
+    const uint32_t* __restrict__ slot_off, const uint32_t* __restrict__ slot_of,
+    const uint32_t* __restrict__ ntiles, const float4* __restrict__ partial,
+    const unsigned long long* __restrict__ total, int64_t cap, float4* __restrict__ m,
+    float4* __restrict__ v, AdamParams ap,
     unsigned long long* __restrict__ skipped) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (*total > (unsigned long long)cap) return;  // overflowed frame: no update (host re-runs)
   float4 a, b;
-  sum_slots(partial, emit_off[i], ntiles[i], a, b);
+  sum_slots(partial, slot_of, slot_off[i], ntiles[i], a, b);
   float o[8];
   grad3d_of(ms[i], fp.cam, a, b, o);
   adam_update(ms, co, m, v, i, o, ap, skipped);
@@ -143,23 +149,23 @@ __global__ void __launch_bounds__(256) k_adam(float4* __restrict__ ms, float4* _
 }
 
 void launch_project_backward(const float4* ms, int64_t n, const FrameParams& fp,
-                             const uint32_t* emit_off, const uint32_t* ntiles,
-                             const float4* partial, const unsigned long long* total, int64_t cap,
-                             float4* grad3d, bool first, cudaStream_t st) {
+                             const uint32_t* slot_off, const uint32_t* slot_of,
+                             const uint32_t* ntiles, const float4* partial,
+                             const unsigned long long* total, int64_t cap, float4* grad3d,
+                             bool first, cudaStream_t st) {
   if (n <= 0) return;
-  k_project_backward<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ms, n, fp, emit_off, ntiles,
-                                                                   partial, total, cap, grad3d,
-                                                                   first);
+  k_project_backward<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+      ms, n, fp, slot_off, slot_of, ntiles, partial, total, cap, grad3d, first);
 }
 
 void launch_project_adam(float4* ms, float4* co, int64_t n, const FrameParams& fp,
-                         const uint32_t* emit_off, const uint32_t* ntiles, const float4* partial,
+                         const uint32_t* slot_off, const uint32_t* slot_of,
+                         const uint32_t* ntiles, const float4* partial,
                          const unsigned long long* total, int64_t cap, float4* m, float4* v,
                          const AdamParams& ap, unsigned long long* skipped, cudaStream_t st) {
   if (n <= 0) return;
-  k_project_adam<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ms, co, n, fp, emit_off, ntiles,
-                                                               partial, total, cap, m, v, ap,
-                                                               skipped);
+  k_project_adam<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+      ms, co, n, fp, slot_off, slot_of, ntiles, partial, total, cap, m, v, ap, skipped);
 }
 
 void launch_adam(float4* ms, float4* co, int64_t n, const float4* grad3d, float4* m, float4* v,

@@ -79,19 +79,17 @@ __device__ __forceinline__ bool rect_hit(float x0, float x1, float y0, float y1,
   return !(dist2_rn(__fsub_rn(cx, u), __fsub_rn(cy, v)) > r2max);
 }
 
-// Stage list entries [beg, beg+cnt) of the sorted key array into `st` (thread t: entry t).
-// The record fetch is a dependent gather (slot -> rank -> record), issued as cp.async.
-__device__ __forceinline__ void stage_batch(Stage& st, const uint32_t* __restrict__ vals,
-                                            const uint32_t* __restrict__ emit_rank,
+// Stage list entries [beg, beg+cnt) of the sorted (splat, slot) array into `st` (thread t:
+// entry t).  The 32-B record gather is issued as cp.async.
+__device__ __forceinline__ void stage_batch(Stage& st, const uint2* __restrict__ sorted,
                                             const RenderRec* __restrict__ rec, uint32_t beg,
                                             int cnt) {
   const int t = threadIdx.x;
   if (t < cnt) {
-    const uint32_t e = vals[beg + t];
-    const uint32_t r = emit_rank[e];
-    st.slot[t] = e;
-    cp_async16(&st.geo[t], &rec[r].geo);
-    cp_async16(&st.col[t], &rec[r].col);
+    const uint2 gs = sorted[beg + t];  // (splat, gradient slot)
+    st.slot[t] = gs.y;
+    cp_async16(&st.geo[t], &rec[gs.x].geo);
+    cp_async16(&st.col[t], &rec[gs.x].col);
   }
   cp_async_commit();
 }
@@ -164,8 +162,8 @@ __device__ __forceinline__ PixPair pix_pair(const FrameParams& fp, int tile) {
 
 // =============================================================================================
 __global__ void __launch_bounds__(kBT) k_blend_fwd(
-    FrameParams fp, const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals,
-    const uint32_t* __restrict__ emit_rank, const RenderRec* __restrict__ rec,
+    FrameParams fp, const uint2* __restrict__ ranges, const uint2* __restrict__ sorted,
+    const RenderRec* __restrict__ rec,
     const unsigned long long* __restrict__ total, int64_t key_cap, float* __restrict__ out,
     float* __restrict__ t_last, uint32_t* __restrict__ n_proc) {
   __shared__ Stage st[2];
@@ -184,14 +182,14 @@ __global__ void __launch_bounds__(kBT) k_blend_fwd(
   float C0r = 0.f, C0g = 0.f, C0b = 0.f, C1r = 0.f, C1g = 0.f, C1b = 0.f;
   uint32_t np0 = 0, np1 = 0;
 
-  if (n > 0) stage_batch(st[0], vals, emit_rank, rec, rg.x, min(kBatch, n));
+  if (n > 0) stage_batch(st[0], sorted, rec, rg.x, min(kBatch, n));
   for (int b = 0, it = 0; b < n; b += kBatch, ++it) {
     Stage& cur = st[it & 1];
     cp_async_wait_all();
     const bool tdone = !(T0 > t_min) && !(T1 > t_min);
     if (__syncthreads_count(tdone) == kBT) break;  // barrier: batch visible, previous consumed
     if (b + kBatch < n)
-      stage_batch(st[(it + 1) & 1], vals, emit_rank, rec, rg.x + b + kBatch,
+      stage_batch(st[(it + 1) & 1], sorted, rec, rg.x + b + kBatch,
                   min(kBatch, n - b - kBatch));
     uint32_t rel[4];
     warp_relevance(cur, tg, w, min(kBatch, n - b), rel);
@@ -259,33 +257,46 @@ struct BwdPix {
   bool first;
 };
 
+__device__ __forceinline__ float fast_rcp(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float fast_sqrt(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// acc: [0] sum go*dx, [1] sum go*dy, [2] sum go*r2 (scaled per entry by the caller into
+// du, dv, dsigma2d), [3] dopacity, [4..6] drgb;  go = dL/dalpha * g.
 __device__ __forceinline__ void bwd_pixel(BwdPix& p, bool act, float dx, float dy, float r2,
-                                          const float4 g, const float4 c, float two_inv_s2,
-                                          float inv_s, float acc[8]) {
+                                          const float4 g, const float4 c, float acc[8]) {
   const float e = fast_exp2(r2 * g.w);
   const float a = act ? c.w * e : 0.0f;
-  const float Tk = p.first ? p.T : __fdividef(p.T, 1.0f - a);
+  const float Tk = p.first ? p.T : p.T * fast_rcp(1.0f - a);
   p.first = p.first && !act;
   p.T = act ? Tk : p.T;
   const float Tg = act ? Tk : 0.0f;
-  const float dLda = Tg * (p.G0 * (c.x - p.A0) + p.G1 * (c.y - p.A1) + p.G2 * (c.z - p.A2));
+  const float d0 = c.x - p.A0, d1 = c.y - p.A1, d2 = c.z - p.A2;
+  const float dLda = Tg * (p.G0 * d0 + p.G1 * d1 + p.G2 * d2);
   const float Ta = Tg * a;
   acc[4] += p.G0 * Ta;
   acc[5] += p.G1 * Ta;
   acc[6] += p.G2 * Ta;
-  p.A0 = a * c.x + (1.0f - a) * p.A0;
-  p.A1 = a * c.y + (1.0f - a) * p.A1;
-  p.A2 = a * c.z + (1.0f - a) * p.A2;
-  acc[3] += dLda * e;
-  const float k2 = dLda * c.w * e * two_inv_s2;
-  acc[0] += k2 * dx;
-  acc[1] += k2 * dy;
-  acc[2] += k2 * r2 * inv_s;
+  p.A0 += a * d0;  // A <- a c + (1 - a) A
+  p.A1 += a * d1;
+  p.A2 += a * d2;
+  const float go = dLda * e;
+  acc[3] += go;
+  acc[0] += go * dx;
+  acc[1] += go * dy;
+  acc[2] += go * r2;
 }
 
 __global__ void __launch_bounds__(kBT) k_blend_bwd(
-    FrameParams fp, const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals,
-    const uint32_t* __restrict__ emit_rank, const RenderRec* __restrict__ rec,
+    FrameParams fp, const uint2* __restrict__ ranges, const uint2* __restrict__ sorted,
+    const RenderRec* __restrict__ rec,
     const unsigned long long* __restrict__ total, int64_t key_cap, const float* __restrict__ img,
     const float* __restrict__ target, const float* __restrict__ t_last,
     const uint32_t* __restrict__ n_proc, float loss_scale, float4* __restrict__ partial,
@@ -354,14 +365,14 @@ __global__ void __launch_bounds__(kBT) k_blend_bwd(
   }
   // entries never reached by any pixel get zero gradient slots
   for (int j = m + (int)threadIdx.x; j < n; j += kBT) {
-    const uint32_t e = vals[rg.x + j];
+    const uint32_t e = sorted[rg.x + j].y;
     partial[2 * (size_t)e] = make_float4(0.f, 0.f, 0.f, 0.f);
     partial[2 * (size_t)e + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   if (m == 0) return;
 
   int hi = m;
-  stage_batch(st[0], vals, emit_rank, rec, rg.x + max(0, hi - kBatch), min(kBatch, hi));
+  stage_batch(st[0], sorted, rec, rg.x + max(0, hi - kBatch), min(kBatch, hi));
   for (int it = 0; hi > 0; ++it) {
     const int lo = max(0, hi - kBatch);
     const int cnt = hi - lo;
@@ -370,7 +381,7 @@ __global__ void __launch_bounds__(kBT) k_blend_bwd(
     __syncthreads();  // batch visible; previous batch's flush finished reading s_part
     if (lo > 0) {
       const int nlo = max(0, lo - kBatch);
-      stage_batch(st[(it + 1) & 1], vals, emit_rank, rec, rg.x + nlo, lo - nlo);
+      stage_batch(st[(it + 1) & 1], sorted, rec, rg.x + nlo, lo - nlo);
     }
     uint32_t rel[4];
     warp_relevance(cur, tg, w, cnt, rel);
@@ -392,10 +403,14 @@ __global__ void __launch_bounds__(kBT) k_blend_bwd(
         const bool act0 = (uint32_t)j < P[0].np && !(r20 > g.z);
         const bool act1 = (uint32_t)j < P[1].np && !(r21 > g.z);
         float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        const float two_inv_s2 = g.w * (-2.0f * kLn2);  // 2 / sigma2d^2
-        const float inv_s = sqrtf(two_inv_s2 * 0.5f);   // 1 / sigma2d
-        bwd_pixel(P[0], act0, dx, dy0, r20, g, c, two_inv_s2, inv_s, acc);
-        bwd_pixel(P[1], act1, dx, dy1, r21, g, c, two_inv_s2, inv_s, acc);
+        bwd_pixel(P[0], act0, dx, dy0, r20, g, c, acc);
+        bwd_pixel(P[1], act1, dx, dy1, r21, g, c, acc);
+        // kernels.hpp:219-220 closed forms: dg/du = g 2 dx/s^2, dg/ds = g 2 r^2/s^3, times opacity
+        const float inv_s2 = g.w * -kLn2;          // 1 / sigma2d^2
+        const float k = 2.0f * c.w * inv_s2;       // 2 o / s^2
+        acc[0] *= k;
+        acc[1] *= k;
+        acc[2] *= k * fast_sqrt(inv_s2);           // 2 o / s^3
         const float y = reduce_scatter8(acc);
         if ((lane & 3) == 0) s_part[w][lane >> 2][jj] = y;
       }
@@ -444,17 +459,16 @@ __global__ void k_loss_reduce(const double* __restrict__ tile_loss, int n_tiles,
   }
 }
 
-void launch_blend_fwd(const FrameParams& fp, const uint2* ranges, const uint32_t* vals,
-                      const uint32_t* emit_rank, const RenderRec* rec,
-                      const unsigned long long* total, int64_t key_cap, float* out, float* t_last,
-                      uint32_t* n_proc, cudaStream_t st) {
-  k_blend_fwd<<<fp.n_tiles, kBT, 0, st>>>(fp, ranges, vals, emit_rank, rec, total, key_cap, out,
-                                          t_last, n_proc);
+void launch_blend_fwd(const FrameParams& fp, const uint2* ranges, const uint2* sorted,
+                      const RenderRec* rec, const unsigned long long* total, int64_t key_cap,
+                      float* out, float* t_last, uint32_t* n_proc, cudaStream_t st) {
+  k_blend_fwd<<<fp.n_tiles, kBT, 0, st>>>(fp, ranges, sorted, rec, total, key_cap, out, t_last,
+                                          n_proc);
 }
 
-void launch_blend_bwd(const FrameParams& fp, const uint2* ranges, const uint32_t* vals,
-                      const uint32_t* emit_rank, const RenderRec* rec,
-                      const unsigned long long* total, int64_t key_cap, const float* img,
+void launch_blend_bwd(const FrameParams& fp, const uint2* ranges, const uint2* sorted,
+                      const RenderRec* rec, const unsigned long long* total, int64_t key_cap,
+                      const float* img,
                       const float* target, const float* t_last, const uint32_t* n_proc,
                       float loss_scale, float4* partial, double* tile_loss, cudaStream_t st) {
   static bool attr = false;
@@ -462,7 +476,7 @@ void launch_blend_bwd(const FrameParams& fp, const uint2* ranges, const uint32_t
     cudaFuncSetAttribute(k_blend_bwd, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     attr = true;
   }
-  k_blend_bwd<<<fp.n_tiles, kBT, 0, st>>>(fp, ranges, vals, emit_rank, rec, total, key_cap, img,
+  k_blend_bwd<<<fp.n_tiles, kBT, 0, st>>>(fp, ranges, sorted, rec, total, key_cap, img,
                                           target, t_last, n_proc, loss_scale, partial, tile_loss);
 }
 

@@ -2,78 +2,84 @@
 // (/root/reference/proj/src/splat3d.cpp:176-188 -> project_iso :59-64) and the per-splat
 // validation (IsoSplat3D::validate, splat3d.cpp:10-17).
 //
-// One thread per splat, coalesced float4 SoA loads (32 B/splat read), writes
-// rec_geo (16 B), depth key (4 B) and tile count (4 B).  Isotropic shortcut: the screen
-// radius is 3*sigma*f/z directly — no 3x3 covariance, no eigen-solve.  Splats that are
-// culled (z <= near) or touch no tile get the depth key 0xFFFFFFFF and count 0, so they sort
-// last and emit nothing.
+// One thread per splat, coalesced float4 SoA loads (32 B/splat read), writes the 32-B render
+// record, the tile count (4 B) and, in radix binning mode, the depth key (4 B); in tile-bucket
+// mode it instead bumps one per-tile counter per touched tile.  Isotropic shortcut: the screen
+// radius is 3*sigma*f/z directly — no 3x3 covariance, no eigen-solve.  Splats that are culled
+// (z <= near) or touch no tile get count 0 (and depth key 0xFFFFFFFF: they sort last and emit
+// nothing).
 #include "isg_math.cuh"
 
 namespace isg {
 
 __global__ void __launch_bounds__(256) k_preprocess(const float4* __restrict__ ms,
                                                     const float4* __restrict__ co, int64_t n,
-                                                    FrameParams fp, float4* __restrict__ rec_geo,
+                                                    FrameParams fp, RenderRec* __restrict__ rec,
                                                     uint32_t* __restrict__ depth_key,
                                                     uint32_t* __restrict__ ntiles,
-                                                    uint32_t* __restrict__ first_bad,
-                                                    uint32_t* __restrict__ n_dev) {
+                                                    uint32_t* __restrict__ tile_cnt,
+                                                    uint32_t* __restrict__ sc) {
+  // sc: [1] first invalid splat (atomicMin), [2] visible splats, [4] n (device count)
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i == 0) *n_dev = (uint32_t)n;
-  if (i >= n) return;
-  const float4 a = ms[i];
-  const float4 c = co[i];
-  // IsoSplat3D::validate (splat3d.cpp:10-17): finite mu, sigma > 0 finite, finite color,
-  // opacity in [0,1].  The host reports the first offending index with the reference message.
-  const bool ok = isfinite(a.x) && isfinite(a.y) && isfinite(a.z) && a.w > 0.0f &&
-                  isfinite(a.w) && isfinite(c.x) && isfinite(c.y) && isfinite(c.z) &&
-                  c.w >= 0.0f && c.w <= 1.0f;
-  if (!ok) atomicMin(first_bad, (uint32_t)i);
-
-  const Proj p = project(a, fp.cam);
+  if (i == 0) sc[4] = (uint32_t)n;
   uint32_t count = 0;
-  if (p.vis && ok) {
-    int x0, x1, y0, y1;
-    if (tile_bbox(p.u, p.v, p.s, fp.tiles_x, fp.tiles_y, x0, x1, y0, y1)) {
-      for (int ty = y0; ty <= y1; ++ty)
-        for (int tx = x0; tx <= x1; ++tx)
-          count += tile_hit(p.u, p.v, p.r2max, tx, ty, fp.cam.width, fp.cam.height) ? 1u : 0u;
+  if (i < n) {
+    const float4 a = ms[i];
+    const float4 c = co[i];
+    // IsoSplat3D::validate (splat3d.cpp:10-17): finite mu, sigma > 0 finite, finite color,
+    // opacity in [0,1].  The host reports the first offending index with the reference message.
+    const bool ok = isfinite(a.x) && isfinite(a.y) && isfinite(a.z) && a.w > 0.0f &&
+                    isfinite(a.w) && isfinite(c.x) && isfinite(c.y) && isfinite(c.z) &&
+                    c.w >= 0.0f && c.w <= 1.0f;
+    if (!ok) atomicMin(&sc[1], (uint32_t)i);
+    const Proj p = project(a, fp.cam);
+    if (p.vis && ok) {
+      int x0, x1, y0, y1;
+      if (tile_bbox(p.u, p.v, p.s, fp.tiles_x, fp.tiles_y, x0, x1, y0, y1)) {
+        for (int ty = y0; ty <= y1; ++ty)
+          for (int tx = x0; tx <= x1; ++tx) {
+            if (!tile_hit(p.u, p.v, p.r2max, tx, ty, fp.cam.width, fp.cam.height)) continue;
+            ++count;
+            if (tile_cnt) atomicAdd(&tile_cnt[ty * fp.tiles_x + tx], 1u);
+          }
+      }
     }
+    RenderRec r;  // (u, v, r2max, -log2(e)/sigma2d^2), (r, g, b, opacity)
+    r.geo = make_float4(p.u, p.v, p.r2max, __fdiv_rn(-1.4426950408889634f, __fmul_rn(p.s, p.s)));
+    r.col = c;
+    rec[i] = r;
+    if (depth_key) depth_key[i] = count ? __float_as_uint(p.zc) : 0xFFFFFFFFu;
+    ntiles[i] = count;
   }
-  rec_geo[i] = make_float4(p.u, p.v, p.s, p.r2max);
-  depth_key[i] = count ? __float_as_uint(p.zc) : 0xFFFFFFFFu;
-  ntiles[i] = count;
+  // visible-splat count, one atomic per warp
+  const unsigned vis = __ballot_sync(0xffffffffu, count > 0);
+  if ((threadIdx.x & 31) == 0 && vis) atomicAdd(&sc[2], (uint32_t)__popc(vis));
 }
 
 void launch_preprocess(const float4* ms, const float4* co, int64_t n, const FrameParams& fp,
-                       float4* rec_geo, uint32_t* depth_key, uint32_t* ntiles,
-                       uint32_t* first_bad, uint32_t* n_dev, cudaStream_t st) {
+                       RenderRec* rec, uint32_t* depth_key, uint32_t* ntiles, uint32_t* tile_cnt,
+                       uint32_t* sc, cudaStream_t st) {
   const int64_t blocks = n > 0 ? (n + 255) / 256 : 1;
-  k_preprocess<<<(unsigned)blocks, 256, 0, st>>>(ms, co, n, fp, rec_geo, depth_key, ntiles,
-                                                 first_bad, n_dev);
+  k_preprocess<<<(unsigned)blocks, 256, 0, st>>>(ms, co, n, fp, rec, depth_key, ntiles, tile_cnt,
+                                                 sc);
 }
 
-// Parity hook: (tile << 32 | float_bits(depth)) and splat index for each sorted key.
-__global__ void k_debug_keys(const uint32_t* __restrict__ tiles,
-                             const uint32_t* __restrict__ slots,
-                             const uint32_t* __restrict__ emit_rank,
-                             const uint32_t* __restrict__ order, const float4* __restrict__ ms,
-                             FrameParams fp, int64_t nkeys, uint64_t* __restrict__ keys,
-                             uint32_t* __restrict__ gids) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nkeys) return;
-  const uint32_t g = order[emit_rank[slots[i]]];
-  const Proj p = project(ms[g], fp.cam);
-  keys[i] = ((uint64_t)tiles[i] << 32) | __float_as_uint(p.zc);
-  gids[i] = g;
+// Parity hook: (tile << 32 | float_bits(depth)) and splat index for each sorted entry.
+__global__ void k_debug_keys(const uint2* __restrict__ ranges, const uint2* __restrict__ sorted,
+                             const float4* __restrict__ ms, FrameParams fp,
+                             uint64_t* __restrict__ keys, uint32_t* __restrict__ gids) {
+  const uint2 rg = ranges[blockIdx.x];
+  for (uint32_t i = rg.x + threadIdx.x; i < rg.y; i += blockDim.x) {
+    const uint32_t g = sorted[i].x;
+    const Proj p = project(ms[g], fp.cam);
+    keys[i] = ((uint64_t)blockIdx.x << 32) | __float_as_uint(p.zc);
+    gids[i] = g;
+  }
 }
 
-void launch_debug_keys(const uint32_t* tiles, const uint32_t* slots, const uint32_t* emit_rank,
-                       const uint32_t* order, const float4* ms, const FrameParams& fp,
-                       int64_t nkeys, uint64_t* keys, uint32_t* gids, cudaStream_t st) {
-  if (nkeys <= 0) return;
-  k_debug_keys<<<(unsigned)((nkeys + 255) / 256), 256, 0, st>>>(tiles, slots, emit_rank, order,
-                                                                 ms, fp, nkeys, keys, gids);
+void launch_debug_keys(const uint2* ranges, const uint2* sorted, const float4* ms,
+                       const FrameParams& fp, uint64_t* keys, uint32_t* gids, cudaStream_t st) {
+  k_debug_keys<<<fp.n_tiles, 128, 0, st>>>(ranges, sorted, ms, fp, keys, gids);
 }
 
 }  // namespace isg

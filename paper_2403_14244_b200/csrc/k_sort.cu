@@ -197,14 +197,19 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
 }
 
 // ---- ranges ---------------------------------------------------------------------------------
-__global__ void k_ranges(const uint32_t* __restrict__ t, const uint32_t* __restrict__ n_dev,
-                         int64_t cap, uint2* __restrict__ ranges) {
+// Per-tile [start, end) from the sorted tile keys, and the blend kernels' (splat, slot) pairs
+// (slot = the pair's emission index, which also keys its gradient slot).
+__global__ void k_ranges(const uint32_t* __restrict__ t, const uint32_t* __restrict__ e_sorted,
+                         const uint32_t* __restrict__ emit_gid, const uint32_t* __restrict__ n_dev,
+                         int64_t cap, uint2* __restrict__ ranges, uint2* __restrict__ sorted) {
   const int64_t n = min((int64_t)*n_dev, cap);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t k = t[i];
     if (i == 0 || t[i - 1] != k) ranges[k].x = (uint32_t)i;
     if (i == n - 1 || t[i + 1] != k) ranges[k].y = (uint32_t)(i + 1);
+    const uint32_t e = e_sorted[i];
+    sorted[i] = make_uint2(emit_gid[e], e);
   }
 }
 
@@ -218,12 +223,10 @@ constexpr unsigned long long kC64Mask = (1ull << 62) - 1;
 
 __global__ void __launch_bounds__(kScanThreads) k_scan_emit(
     const uint32_t* __restrict__ order, const uint32_t* __restrict__ ntiles,
-    const float4* __restrict__ rec_geo, const float4* __restrict__ co, int64_t n, FrameParams fp,
-    RenderRec* __restrict__ rec_sorted, uint32_t* __restrict__ emit_off,
-    uint32_t* __restrict__ tile_keys, uint32_t* __restrict__ emit_rank, int64_t key_cap,
+    const float4* __restrict__ ms, int64_t n, FrameParams fp, uint32_t* __restrict__ slot_off,
+    uint32_t* __restrict__ tile_keys, uint32_t* __restrict__ emit_gid, int64_t key_cap,
     unsigned long long* __restrict__ lookback, uint32_t* __restrict__ counter,
-    uint32_t* __restrict__ n_keys, unsigned long long* __restrict__ n_keys_total,
-    uint32_t* __restrict__ n_visible) {
+    uint32_t* __restrict__ n_keys, unsigned long long* __restrict__ n_keys_total) {
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_warp[8];
   __shared__ unsigned long long s_excl;
@@ -235,19 +238,16 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(
   if (base >= n) return;
   const int64_t r0 = base + (int64_t)tid * kScanItems;
   uint32_t g[kScanItems], c[kScanItems];
-  uint32_t sum = 0, vis = 0;
+  uint32_t sum = 0;
 #pragma unroll
   for (int j = 0; j < kScanItems; ++j) {
     const int64_t r = r0 + j;
     g[j] = r < n ? order[r] : 0u;
     c[j] = r < n ? ntiles[g[j]] : 0u;
     sum += c[j];
-    vis += c[j] ? 1u : 0u;
   }
   uint32_t tot;
   const uint32_t texcl = block_excl_scan_256(sum, s_warp, tot);
-  uint32_t vtot;
-  block_excl_scan_256(vis, s_warp, vtot);
   if (tid == 0) {
     unsigned long long* my = lookback + tile;
     unsigned long long excl = 0;
@@ -268,7 +268,6 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(
       st_volatile64(my, kF64Inc | (excl + tot));
     }
     s_excl = excl;
-    if (vtot) atomicAdd(n_visible, vtot);
     if (base + kScanTileItems >= n) {
       const unsigned long long total = excl + tot;
       *n_keys_total = total;
@@ -282,21 +281,17 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(
     const int64_t r = r0 + j;
     if (r >= n) break;
     const uint32_t gg = g[j];
-    emit_off[gg] = (uint32_t)min(off, (unsigned long long)0xFFFFFFFFu);
+    slot_off[gg] = (uint32_t)min(off, (unsigned long long)0xFFFFFFFFu);
     if (c[j] == 0) continue;
-    const float4 geo = rec_geo[gg];
-    RenderRec rr;  // (u, v, r2max, -log2(e)/sigma2d^2), (r, g, b, opacity)
-    rr.geo = make_float4(geo.x, geo.y, geo.w, __fdiv_rn(-1.4426950408889634f, __fmul_rn(geo.z, geo.z)));
-    rr.col = co[gg];
-    rec_sorted[r] = rr;
+    const Proj p = project(ms[gg], fp.cam);  // bit-identical to K1's projection
     int x0, x1, y0, y1;
-    tile_bbox(geo.x, geo.y, geo.z, fp.tiles_x, fp.tiles_y, x0, x1, y0, y1);
+    tile_bbox(p.u, p.v, p.s, fp.tiles_x, fp.tiles_y, x0, x1, y0, y1);
     for (int ty = y0; ty <= y1; ++ty)
       for (int tx = x0; tx <= x1; ++tx) {
-        if (!tile_hit(geo.x, geo.y, geo.w, tx, ty, fp.cam.width, fp.cam.height)) continue;
+        if (!tile_hit(p.u, p.v, p.r2max, tx, ty, fp.cam.width, fp.cam.height)) continue;
         if (off < (unsigned long long)key_cap) {
           tile_keys[off] = (uint32_t)(ty * fp.tiles_x + tx);
-          emit_rank[off] = (uint32_t)r;
+          emit_gid[off] = gg;
         }
         ++off;
       }
@@ -307,24 +302,24 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(
 
 int64_t scan_emit_scratch_words(int64_t n) { return (n + kScanTileItems - 1) / kScanTileItems; }
 
-void launch_scan_emit(const uint32_t* order, const uint32_t* ntiles, const float4* rec_geo,
-                      const float4* co, int64_t n, const FrameParams& fp, RenderRec* rec_sorted,
-                      uint32_t* emit_off, uint32_t* tile_keys, uint32_t* emit_rank,
-                      int64_t key_cap, unsigned long long* scratch, uint32_t* counter,
-                      uint32_t* n_keys, unsigned long long* n_keys_total, uint32_t* n_visible,
+void launch_scan_emit(const uint32_t* order, const uint32_t* ntiles, const float4* ms, int64_t n,
+                      const FrameParams& fp, uint32_t* slot_off, uint32_t* tile_keys,
+                      uint32_t* emit_gid, int64_t key_cap, unsigned long long* scratch,
+                      uint32_t* counter, uint32_t* n_keys, unsigned long long* n_keys_total,
                       cudaStream_t st) {
   const int64_t tiles = scan_emit_scratch_words(n);
   if (tiles == 0) return;  // caller zeroed the counts
-  k_scan_emit<<<(unsigned)tiles, kScanThreads, 0, st>>>(
-      order, ntiles, rec_geo, co, n, fp, rec_sorted, emit_off, tile_keys, emit_rank, key_cap,
-      scratch, counter, n_keys, n_keys_total, n_visible);
+  k_scan_emit<<<(unsigned)tiles, kScanThreads, 0, st>>>(order, ntiles, ms, n, fp, slot_off,
+                                                        tile_keys, emit_gid, key_cap, scratch,
+                                                        counter, n_keys, n_keys_total);
 }
 
-void launch_ranges(const uint32_t* sorted_tiles, const uint32_t* n_keys, int64_t key_cap,
-                   uint2* ranges, cudaStream_t st) {
+void launch_ranges(const uint32_t* sorted_tiles, const uint32_t* e_sorted,
+                   const uint32_t* emit_gid, const uint32_t* n_keys, int64_t key_cap,
+                   uint2* ranges, uint2* sorted, cudaStream_t st) {
   const int64_t blocks = std::min<int64_t>((key_cap + 255) / 256, 148 * 16);
-  k_ranges<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, st>>>(sorted_tiles, n_keys, key_cap,
-                                                                   ranges);
+  k_ranges<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, st>>>(
+      sorted_tiles, e_sorted, emit_gid, n_keys, key_cap, ranges, sorted);
 }
 
 int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], bool iota_vals, const uint32_t* n_dev,

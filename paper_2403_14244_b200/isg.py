@@ -82,6 +82,7 @@ def lib() -> C.CDLL:
         "isg_nccl_detach": ([P], C.c_int),
         "isg_debug_bins": ([P, P, P, C.POINTER(I64), P], C.c_int),
         "isg_debug_pixel_state": ([P, P, P], C.c_int),
+        "isg_set_binning": ([P, C.c_int], C.c_int),
         "isg_profile_enable": ([P, C.c_int], C.c_int),
         "isg_profile_num_stages": ([], C.c_int),
         "isg_profile_stage_name": ([C.c_int], C.c_char_p),
@@ -104,7 +105,8 @@ C_ABI_SYMBOLS = (
     "isg_get_scene", "isg_render", "isg_render_device", "isg_loss_backward",
     "isg_loss_backward_device", "isg_read_loss", "isg_zero_grads", "isg_get_grads",
     "isg_grads_device", "isg_adam_step", "isg_nccl_get_unique_id", "isg_nccl_init",
-    "isg_nccl_detach", "isg_debug_bins", "isg_debug_pixel_state", "isg_profile_enable",
+    "isg_nccl_detach", "isg_debug_bins", "isg_debug_pixel_state", "isg_set_binning",
+    "isg_profile_enable",
     "isg_profile_num_stages", "isg_profile_stage_name", "isg_profile_read", "isg_synth_scene",
     "isg_synth_camera",
 )
@@ -361,6 +363,12 @@ class Renderer:
 
     def nccl_detach(self):
         _check(self._h, lib().isg_nccl_detach(self._h))
+
+    BINNING_TILE_BUCKET, BINNING_RADIX = 0, 1
+
+    def set_binning(self, mode: int):
+        """0 = tile-bucket (default), 1 = onesweep radix; bit-identical tile lists."""
+        _check(self._h, lib().isg_set_binning(self._h, int(mode)))
 
     # -- stage timing -----------------------------------------------------------------------
     def profile(self, on: bool = True):

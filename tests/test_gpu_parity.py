@@ -309,3 +309,61 @@ def test_full_size_c2_render_parity():
         keys = check_bins(r, ms, co, cam)
         assert np.all(np.diff(keys.astype(np.int64) >> 32) >= 0)
         assert np.abs(img - O.render32(ms, co, cam)).max() <= IMG_TOL
+
+
+def test_binning_modes_bit_identical(rend):
+    """Tile-bucket and onesweep-radix binning give identical lists, images and gradients."""
+    W, H = 320, 200
+    ms, co = isg.synth_scene(30000, W, H, seed=21)
+    tms, tco = isg.synth_scene(30000, W, H, seed=22)
+    cam = isg.Camera.synthetic(W, H, 2, 8)
+    target = O.render32(tms, tco, cam)
+    out = []
+    for mode in (isg.Renderer.BINNING_TILE_BUCKET, isg.Renderer.BINNING_RADIX):
+        rend.set_binning(mode)
+        rend.set_scene(ms, co)
+        img = rend.render(cam)
+        bins = check_bins(rend, ms, co, cam)
+        loss = rend.loss_backward(cam, target)
+        out.append((img, bins, loss, rend.grads()))
+    rend.set_binning(isg.Renderer.BINNING_TILE_BUCKET)
+    (i0, b0, l0, g0), (i1, b1, l1, g1) = out
+    assert np.array_equal(i0, i1) and np.array_equal(b0, b1)
+    assert l0 == l1 and np.array_equal(g0, g1)
+
+
+def test_gradients_bitwise_deterministic(rend):
+    W, H = 256, 160
+    ms, co = isg.synth_scene(20000, W, H, seed=31)
+    tms, tco = isg.synth_scene(20000, W, H, seed=32)
+    cam = isg.Camera.synthetic(W, H)
+    target = O.render32(tms, tco, cam)
+    rend.set_scene(ms, co)
+    runs = []
+    for _ in range(3):
+        rend.zero_grads()
+        runs.append((rend.loss_backward(cam, target), rend.grads()))
+    for loss, g in runs[1:]:
+        assert loss == runs[0][0] and np.array_equal(g, runs[0][1])
+
+
+@pytest.mark.parametrize("mode", [0, 1], ids=["tile_bucket", "radix"])
+def test_long_tile_lists(mode):
+    """Tiles with > 2048 entries take the global-memory merge path of the tile sort."""
+    W, H = 96, 80
+    rng = np.random.default_rng(9)
+    with isg.Renderer(0) as r:
+        r.set_binning(mode)
+        ms, co, cam = random_scene(rng, 5000, W, H, sigma2d=(40.0, 80.0))
+        r.set_scene(ms, co)
+        img = r.render(cam, isg.RenderOptions(t_min=0.0))
+        keys, vals, ranges = r.debug_bins()
+        assert (ranges[:, 1] - ranges[:, 0]).max() > 2048
+        check_bins(r, ms, co, cam)
+        assert np.abs(img - O.render32(ms, co, cam, t_min=0.0)).max() <= IMG_TOL
+        tms, tco, _ = random_scene(rng, 5000, W, H, sigma2d=(40.0, 80.0))
+        target = O.render32(tms, tco, cam)
+        loss = r.loss_backward(cam, target, isg.RenderOptions(t_min=0.0))
+        loss_ref, g_ref = O.loss_backward32(ms, co, cam, target, t_min=0.0)
+        assert abs(loss - loss_ref) <= 1e-6 * abs(loss_ref)
+        _grad_check(r.grads(), g_ref)
