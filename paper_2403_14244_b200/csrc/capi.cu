@@ -59,7 +59,7 @@ struct isg_ctx {
   int order_buf = 0;
 
   // (tile, splat) pairs, key_cap slots
-  int binning = isg::kBinTileBucket;
+  int binning = isg::kBinRadix;
   int64_t key_cap = 0;
   uint2* sorted = nullptr;                  // per list entry: (splat, gradient slot)
   float4* partial = nullptr;                // gradient slot: 2D grads of one pair (2 x float4)

@@ -42,7 +42,7 @@ struct __align__(16) RenderRec {
 
 // ---- radix sort (onesweep, 8-bit digits, u32 keys + u32 values) ---------------------------
 constexpr int kSortThreads = 256;
-constexpr int kSortItems = 16;  // items per thread
+constexpr int kSortItems = 8;  // items per thread
 constexpr int kSortTileItems = kSortThreads * kSortItems;
 constexpr int kMaxPasses = 4;
 

@@ -18,6 +18,7 @@
 #include <algorithm>
 
 #include "isg_math.cuh"
+#include "lookback.cuh"
 
 namespace isg {
 
@@ -27,17 +28,6 @@ constexpr int kScanThreads = 1024;
 constexpr int kFillThreads = 256;
 constexpr int kFillItems = 4;
 constexpr int kFillTile = kFillThreads * kFillItems;
-constexpr unsigned long long kF64Agg = 1ull << 62;
-constexpr unsigned long long kF64Inc = 2ull << 62;
-constexpr unsigned long long kC64Mask = (1ull << 62) - 1;
-
-__device__ __forceinline__ unsigned long long ld_volatile64(const unsigned long long* p) {
-  return *(const volatile unsigned long long*)p;
-}
-__device__ __forceinline__ void st_volatile64(unsigned long long* p, unsigned long long v) {
-  *(volatile unsigned long long*)p = v;
-}
-
 // inclusive warp scan + block exclusive scan (blockDim.x threads, <= 32 warps)
 __device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long v,
                                                               unsigned long long* s_warp,
@@ -124,26 +114,9 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(
   }
   unsigned long long tot;
   const unsigned long long texcl = block_excl_scan(sum, s_warp, tot);
-  if (tid == 0) {
-    unsigned long long* my = lookback + tile;
-    unsigned long long excl = 0;
-    if (tile == 0) {
-      st_volatile64(my, kF64Inc | tot);
-    } else {
-      st_volatile64(my, kF64Agg | tot);
-      int64_t p = (int64_t)tile - 1;
-      while (true) {
-        unsigned long long s;
-        do {
-          s = ld_volatile64(lookback + p);
-        } while ((s & ~kC64Mask) == 0);
-        excl += s & kC64Mask;
-        if ((s & ~kC64Mask) == kF64Inc) break;
-        --p;
-      }
-      st_volatile64(my, kF64Inc | (excl + tot));
-    }
-    s_excl = excl;
+  if (tid < 32) {
+    const unsigned long long excl = lookback_warp(lookback, tile, tot);
+    if (tid == 0) s_excl = excl;
   }
   __syncthreads();
   unsigned long long off = s_excl + texcl;

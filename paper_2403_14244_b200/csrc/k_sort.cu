@@ -18,6 +18,7 @@
 #include <algorithm>
 
 #include "isg_math.cuh"
+#include "lookback.cuh"
 
 namespace isg {
 
@@ -32,12 +33,6 @@ __device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
 }
 __device__ __forceinline__ void st_volatile(uint32_t* p, uint32_t v) {
   *(volatile uint32_t*)p = v;
-}
-__device__ __forceinline__ unsigned long long ld_volatile64(const unsigned long long* p) {
-  return *(const volatile unsigned long long*)p;
-}
-__device__ __forceinline__ void st_volatile64(unsigned long long* p, unsigned long long v) {
-  *(volatile unsigned long long*)p = v;
 }
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -161,15 +156,23 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
   // decoupled look-back for digit `tid`
   uint32_t excl = 0;
   if (tile > 0) {
+    // walk back 4 predecessors per round trip (statuses only move 0 -> AGG -> INC, so a stale
+    // aggregate is still a correct partial sum)
     int64_t p = (int64_t)tile - 1;
-    while (true) {
-      uint32_t s;
-      do {
-        s = ld_volatile(lookback + p * 256 + tid);
-      } while ((s & ~kCountMask) == 0);
-      excl += s & kCountMask;
-      if ((s & ~kCountMask) == kFlagInc) break;
-      --p;
+    bool found = false;
+    while (!found) {
+      uint32_t s[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        s[q] = p - q >= 0 ? ld_volatile(lookback + (p - q) * 256 + tid) : kFlagInc;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (found) break;
+        while ((s[q] & ~kCountMask) == 0) s[q] = ld_volatile(lookback + (p - q) * 256 + tid);
+        excl += s[q] & kCountMask;
+        found = (s[q] & ~kCountMask) == kFlagInc;
+      }
+      p -= 4;
     }
     st_volatile(my, kFlagInc | (excl + cnt));
   }
@@ -217,9 +220,6 @@ __global__ void k_ranges(const uint32_t* __restrict__ t, const uint32_t* __restr
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 4;
 constexpr int kScanTileItems = kScanThreads * kScanItems;
-constexpr unsigned long long kF64Agg = 1ull << 62;
-constexpr unsigned long long kF64Inc = 2ull << 62;
-constexpr unsigned long long kC64Mask = (1ull << 62) - 1;
 
 __global__ void __launch_bounds__(kScanThreads) k_scan_emit(
     const uint32_t* __restrict__ order, const uint32_t* __restrict__ ntiles,
@@ -248,30 +248,15 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(
   }
   uint32_t tot;
   const uint32_t texcl = block_excl_scan_256(sum, s_warp, tot);
-  if (tid == 0) {
-    unsigned long long* my = lookback + tile;
-    unsigned long long excl = 0;
-    if (tile == 0) {
-      st_volatile64(my, kF64Inc | tot);
-    } else {
-      st_volatile64(my, kF64Agg | tot);
-      int64_t p = (int64_t)tile - 1;
-      while (true) {
-        unsigned long long s;
-        do {
-          s = ld_volatile64(lookback + p);
-        } while ((s & ~kC64Mask) == 0);
-        excl += s & kC64Mask;
-        if ((s & ~kC64Mask) == kF64Inc) break;
-        --p;
+  if (tid < 32) {
+    const unsigned long long excl = lookback_warp(lookback, tile, tot);
+    if (tid == 0) {
+      s_excl = excl;
+      if (base + kScanTileItems >= n) {
+        const unsigned long long total = excl + tot;
+        *n_keys_total = total;
+        *n_keys = (uint32_t)min((unsigned long long)key_cap, total);
       }
-      st_volatile64(my, kF64Inc | (excl + tot));
-    }
-    s_excl = excl;
-    if (base + kScanTileItems >= n) {
-      const unsigned long long total = excl + tot;
-      *n_keys_total = total;
-      *n_keys = (uint32_t)min((unsigned long long)key_cap, total);
     }
   }
   __syncthreads();
