@@ -128,6 +128,8 @@ isg_status isg_grads_device(isg_ctx* ctx, float** grads_dev);
  * lr = {lr_mu, lr_sigma, lr_color, lr_opacity}; consumes and zeroes the gradients.  Updates
  * with a non-finite gradient are skipped and counted (optimize.cpp:87-90). */
 isg_status isg_adam_step(isg_ctx* ctx, const float lr[4], float beta1, float beta2, float eps);
+/* Loss of the last Adam step's views (all-reduced over ranks when NCCL is attached; syncs). */
+isg_status isg_last_step_loss(isg_ctx* ctx, double* loss_out);
 
 /* ---- multi-GPU (one process per GPU, views sharded, NCCL all-reduce before Adam) -------- */
 /* NCCL is resolved at run time (dlopen libnccl.so.2, the copy torch already loaded if any). */

@@ -86,10 +86,29 @@ def build_ref(force: bool = False) -> Path | None:
     return REF_LIB if REF_LIB.exists() else None
 
 
+DROPIN_SRC = ROOT / "tests" / "cpp" / "test_dropin.cpp"
+DROPIN_BIN = ROOT / "build" / "test_dropin"
+
+
+def build_dropin_test(force: bool = False) -> Path:
+    """The C++ drop-in (csrc/isosplat_b200.hpp) used the way the reference's caller uses it."""
+    deps = [DROPIN_SRC, CSRC / "isosplat_b200.hpp", ROOT / "include" / "isg.h"]
+    stamp = DROPIN_BIN.with_suffix(".sha256")
+    digest = _digest(deps)
+    if not force and DROPIN_BIN.exists() and stamp.exists() and stamp.read_text() == digest:
+        return DROPIN_BIN
+    DROPIN_BIN.parent.mkdir(parents=True, exist_ok=True)
+    _run(["g++", "-std=c++20", "-O2", "-Wall", "-I", ROOT / "include", "-I", CSRC, DROPIN_SRC,
+          "-L", PKG, "-lisg", "-Wl,-rpath,$ORIGIN/../paper_2403_14244_b200", "-o", DROPIN_BIN])
+    stamp.write_text(digest)
+    return DROPIN_BIN
+
+
 def build_all(force: bool = False) -> None:
     build_isg(force)
     build_oracle(force)
     build_ref(force)
+    build_dropin_test(force)
 
 
 if __name__ == "__main__":

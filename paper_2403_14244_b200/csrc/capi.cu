@@ -90,7 +90,7 @@ struct isg_ctx {
   // device scalars: [0] n_keys [1] first_bad [2] n_visible [3] scan tile counter [4] n
   uint32_t* sc = nullptr;
   unsigned long long* total = nullptr;     // [0] total keys, [1] skipped updates
-  double* loss = nullptr;                  // [0] accumulated, [1] last view
+  double* loss = nullptr;                  // [0] accumulated, [1] last view, [2] last step
   // pinned readback
   uint32_t* h_sc = nullptr;
   unsigned long long* h_total = nullptr;
@@ -550,13 +550,13 @@ isg_status isg_create(int device, int64_t max_gaussians, int32_t max_width, int3
   };
   chk(cudaMalloc(&ctx->sc, sizeof(uint32_t) * 8));
   chk(cudaMalloc(&ctx->total, sizeof(unsigned long long) * 2));
-  chk(cudaMalloc(&ctx->loss, sizeof(double) * 2));
+  chk(cudaMalloc(&ctx->loss, sizeof(double) * 3));
   chk(cudaMallocHost(&ctx->h_sc, sizeof(uint32_t) * 8));
   chk(cudaMallocHost(&ctx->h_total, sizeof(unsigned long long) * 2));
-  chk(cudaMallocHost(&ctx->h_loss, sizeof(double) * 2));
+  chk(cudaMallocHost(&ctx->h_loss, sizeof(double) * 3));
   if (s == ISG_OK) {
     chk(cudaMemset(ctx->total, 0, sizeof(unsigned long long) * 2));
-    chk(cudaMemset(ctx->loss, 0, sizeof(double) * 2));
+    chk(cudaMemset(ctx->loss, 0, sizeof(double) * 3));
   }
   if (s == ISG_OK && max_gaussians > 0) s = ensure_scene(ctx, max_gaussians);
   if (s == ISG_OK && max_width > 0 && max_height > 0) s = ensure_pixels(ctx, max_width, max_height);
@@ -862,7 +862,21 @@ isg_status isg_adam_step(isg_ctx* ctx, const float lr[4], float b1, float b2, fl
     ctx->launches++;
   }
   ctx->grad3d_valid = false;
+  // the step's (all-reduced) loss moves to loss[2]; the accumulator restarts at zero
+  ISG_CUDA(cudaMemcpyAsync(ctx->loss + 2, ctx->loss, sizeof(double), cudaMemcpyDeviceToDevice,
+                           ctx->stream));
   ISG_CUDA(cudaMemsetAsync(ctx->loss, 0, sizeof(double), ctx->stream));
+  return ISG_OK;
+}
+
+isg_status isg_last_step_loss(isg_ctx* ctx, double* loss_out) {
+  if (!ctx || !loss_out) return ISG_E_ARG;
+  isg_status s = isg_synchronize(ctx);
+  if (s != ISG_OK) return s;
+  ISG_CUDA(cudaMemcpyAsync(ctx->h_loss, ctx->loss, sizeof(double) * 3, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  ISG_CUDA(cudaStreamSynchronize(ctx->stream));
+  *loss_out = ctx->h_loss[2];
   return ISG_OK;
 }
 

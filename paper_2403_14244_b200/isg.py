@@ -77,6 +77,7 @@ def lib() -> C.CDLL:
         "isg_get_grads": ([P, P], C.c_int),
         "isg_grads_device": ([P, C.POINTER(P)], C.c_int),
         "isg_adam_step": ([P, fp, F, F, F], C.c_int),
+        "isg_last_step_loss": ([P, C.POINTER(C.c_double)], C.c_int),
         "isg_nccl_get_unique_id": ([P], C.c_int),
         "isg_nccl_init": ([P, C.c_int, C.c_int, P], C.c_int),
         "isg_nccl_detach": ([P], C.c_int),
@@ -104,7 +105,8 @@ C_ABI_SYMBOLS = (
     "isg_set_stream", "isg_synchronize", "isg_get_stats", "isg_set_scene", "isg_set_scene_device",
     "isg_get_scene", "isg_render", "isg_render_device", "isg_loss_backward",
     "isg_loss_backward_device", "isg_read_loss", "isg_zero_grads", "isg_get_grads",
-    "isg_grads_device", "isg_adam_step", "isg_nccl_get_unique_id", "isg_nccl_init",
+    "isg_grads_device", "isg_adam_step", "isg_last_step_loss", "isg_nccl_get_unique_id",
+    "isg_nccl_init",
     "isg_nccl_detach", "isg_debug_bins", "isg_debug_pixel_state", "isg_set_binning",
     "isg_profile_enable",
     "isg_profile_num_stages", "isg_profile_stage_name", "isg_profile_read", "isg_synth_scene",
@@ -349,6 +351,11 @@ class Renderer:
 
     def adam_step(self, cfg: AdamConfig = AdamConfig()):
         _check(self._h, lib().isg_adam_step(self._h, cfg.lrs(), cfg.beta1, cfg.beta2, cfg.eps))
+
+    def last_step_loss(self) -> float:
+        v = C.c_double()
+        _check(self._h, lib().isg_last_step_loss(self._h, C.byref(v)))
+        return v.value
 
     # -- multi-GPU --------------------------------------------------------------------------
     @staticmethod

@@ -93,3 +93,29 @@ def test_device_calls_fail_loudly_without_gpu():
         pytest.skip("a GPU is present")
     with pytest.raises(isg.IsgError):
         isg.Renderer(0)
+
+
+def _dropin(mode):
+    from paper_2403_14244_b200 import build
+    exe = build.build_dropin_test()
+    return subprocess.run([str(exe), mode], capture_output=True, text=True, timeout=300)
+
+
+def test_cpp_dropin_host_side():
+    """Reference-style C++ caller code compiles against isosplat_b200.hpp; validation throws
+    the reference's std::domain_error messages before any device call."""
+    r = _dropin("validate")
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "OK validate" in r.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_dropin_render_on_gpu():
+    r = _dropin("render")
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_cpp_dropin_train_on_gpu():
+    r = _dropin("train")
+    assert r.returncode == 0, r.stdout + r.stderr
