@@ -43,8 +43,20 @@ METRIC = "fwd+bwd train iters/sec (1M isotropic Gaussians, 1080p)"
 
 # Algorithmic FP32 work per (pixel, list entry) pair, FLOPs (FMA = 2), see DESIGN.md §Roofline:
 FWD_FLOP_EVAL, FWD_FLOP_IN = 6, 12      # 3-sigma test; exp+alpha+composite+transmittance
-BWD_FLOP_EVAL, BWD_FLOP_IN = 6, 44      # same test; transmittance recovery + 7 gradients
+BWD_FLOP_EVAL, BWD_FLOP_IN = 6, 36      # same test; transmittance recovery + 7 gradients
 FP32_LANES = 148 * 128
+NCU_SUMMARY = "profiles/r1/ncu_full_blend.json"  # dram traffic per launch, --set full capture
+
+
+def ncu_traffic(kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum of `kernel` from the committed capture."""
+    try:
+        d = json.loads((ROOT / NCU_SUMMARY).read_text())["kernels"]["k_" + kernel]
+        mb = lambda s: float(s.split()[0]) * {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3}[s.split()[1]]
+        return {"bytes": mb(d["dram__bytes_read.sum"]) + mb(d["dram__bytes_write.sum"]),
+                "source": NCU_SUMMARY}
+    except Exception:
+        return None
 
 
 def env_rank():
@@ -324,7 +336,7 @@ def run_isg(args):
         achieved = flops / (top_ms / 1e3) / 1e12
         peak = 2 * FP32_LANES * sm_mhz * 1e6 / 1e12
         roof.update({"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": ncu_traffic(top_name),
                      "work": f"{flops:.3e} algorithmic FP32 FLOP/launch ({ev_p} evaluated + "
                              f"{in_p} in-circle pixel-splat pairs)",
                      "peak_kind": f"spec FP32 FMA rate at the measured sm_max_mhz {sm_mhz:.0f}"})

@@ -302,7 +302,9 @@ __global__ void __launch_bounds__(kBT) k_blend_bwd(
     const uint32_t* __restrict__ n_proc, float loss_scale, float4* __restrict__ partial,
     double* __restrict__ tile_loss) {
   __shared__ Stage st[2];
-  __shared__ float s_part[kWarps][8][kBatch];  // [warp][value][entry]
+  // [warp][value][entry], rows padded by one word so the 8 values of one entry (written by
+  // lanes 0,4,..,28 at once) fall in 8 different banks
+  __shared__ float s_part[kWarps][8][kBatch + 1];
   __shared__ uint32_t s_rel[kWarps][4];
   __shared__ float s_red[kWarps];
   __shared__ uint32_t s_max[kWarps];

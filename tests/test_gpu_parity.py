@@ -66,10 +66,14 @@ def test_bins_and_render(rend, name, n, W, H, kw):
         img = rend.render(cam, opts)
         check_bins(rend, ms, co, cam)
         ref, tl, npr, _ = O.render32(ms, co, cam, t_min=t_min, want_state=True)
-        assert np.abs(img - ref).max() <= IMG_TOL
         gtl, gnp = rend.debug_pixel_state(W, H)
-        # early-termination index may differ by one entry where exp rounding straddles t_min
-        assert np.mean(gnp == npr) > 0.99
+        same = gnp == npr
+        # Where transmittance lands within one rounding of t_min, ex2.approx (GPU) and libm
+        # expf (oracle) may stop one entry apart; that entry is worth at most ~t_min * max|c|.
+        # Everywhere else the images agree to IMG_TOL.
+        assert np.mean(same) > 0.99
+        assert np.abs(img - ref)[same].max(initial=0.0) <= IMG_TOL
+        assert np.abs(img - ref).max() <= IMG_TOL + 2.0 * t_min
 
 
 def test_synthetic_scene_bins(rend):
