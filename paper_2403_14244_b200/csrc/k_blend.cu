@@ -112,6 +112,21 @@ __device__ __forceinline__ void warp_relevance(const Stage& st, const TileGeom& 
   }
 }
 
+// Compact the warp's relevant entries of the batch into `list` (ascending); returns the count.
+// The blend loops then cost ~3 instructions per relevant entry for iteration.
+__device__ __forceinline__ int warp_compact(const uint32_t rel[4], uint8_t* list) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = (1u << lane) - 1u;
+  int base = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if ((rel[k] >> lane) & 1u) list[base + __popc(rel[k] & lt)] = (uint8_t)(32 * k + lane);
+    base += __popc(rel[k]);
+  }
+  __syncwarp();
+  return base;
+}
+
 // reduce-scatter of 8 values over the warp in 9 shuffles: lane L returns the warp-wide sum of
 // value (L >> 2) & 7.
 __device__ __forceinline__ float reduce_scatter8(const float v[8]) {
@@ -167,6 +182,7 @@ __global__ void __launch_bounds__(kBT) k_blend_fwd(
     const unsigned long long* __restrict__ total, int64_t key_cap, float* __restrict__ out,
     float* __restrict__ t_last, uint32_t* __restrict__ n_proc) {
   __shared__ Stage st[2];
+  __shared__ uint8_t s_list[kWarps][kBatch];
   if (overflowed(total, key_cap)) return;
   const int tile = blockIdx.x;
   const int w = threadIdx.x >> 5;
@@ -193,12 +209,10 @@ __global__ void __launch_bounds__(kBT) k_blend_fwd(
                   min(kBatch, n - b - kBatch));
     uint32_t rel[4];
     warp_relevance(cur, tg, w, min(kBatch, n - b), rel);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      uint32_t m = rel[k];
-      while (m) {
-        const int jj = 32 * k + __ffs(m) - 1;
-        m &= m - 1;
+    const int nrel = warp_compact(rel, s_list[w]);
+    {
+      for (int i = 0; i < nrel; ++i) {
+        const int jj = s_list[w][i];
         const float4 g = cur.geo[jj];
         const float4 c = cur.col[jj];
         const float dx = __fsub_rn(pp.px, g.x);
@@ -270,17 +284,18 @@ __device__ __forceinline__ float fast_sqrt(float x) {
 
 // acc: [0] sum go*dx, [1] sum go*dy, [2] sum go*r2 (scaled per entry by the caller into
 // du, dv, dsigma2d), [3] dopacity, [4..6] drgb;  go = dL/dalpha * g.
+// An inactive pixel gets e = 0, hence a = 0: T is unchanged exactly (T * rcp(1) = T), A is
+// unchanged (A + 0), and every contribution (Ta = T a, go = dL/da e) is an exact zero.
 __device__ __forceinline__ void bwd_pixel(BwdPix& p, bool act, float dx, float dy, float r2,
                                           const float4 g, const float4 c, float acc[8]) {
-  const float e = fast_exp2(r2 * g.w);
-  const float a = act ? c.w * e : 0.0f;
+  const float e = act ? fast_exp2(r2 * g.w) : 0.0f;
+  const float a = c.w * e;
   const float Tk = p.first ? p.T : p.T * fast_rcp(1.0f - a);
   p.first = p.first && !act;
-  p.T = act ? Tk : p.T;
-  const float Tg = act ? Tk : 0.0f;
+  p.T = Tk;
   const float d0 = c.x - p.A0, d1 = c.y - p.A1, d2 = c.z - p.A2;
-  const float dLda = Tg * (p.G0 * d0 + p.G1 * d1 + p.G2 * d2);
-  const float Ta = Tg * a;
+  const float dLda = Tk * (p.G0 * d0 + p.G1 * d1 + p.G2 * d2);
+  const float Ta = Tk * a;
   acc[4] += p.G0 * Ta;
   acc[5] += p.G1 * Ta;
   acc[6] += p.G2 * Ta;
@@ -306,6 +321,7 @@ __global__ void __launch_bounds__(kBT) k_blend_bwd(
   // lanes 0,4,..,28 at once) fall in 8 different banks
   __shared__ float s_part[kWarps][8][kBatch + 1];
   __shared__ uint32_t s_rel[kWarps][4];
+  __shared__ uint8_t s_list[kWarps][kBatch];
   __shared__ float s_red[kWarps];
   __shared__ uint32_t s_max[kWarps];
   const int tile = blockIdx.x;
@@ -387,13 +403,10 @@ __global__ void __launch_bounds__(kBT) k_blend_bwd(
     }
     uint32_t rel[4];
     warp_relevance(cur, tg, w, cnt, rel);
-#pragma unroll
-    for (int k = 3; k >= 0; --k) {
-      uint32_t msk = rel[k];
-      while (msk) {
-        const int bit = 31 - __clz(msk);
-        msk &= ~(1u << bit);
-        const int jj = 32 * k + bit;
+    const int nrel = warp_compact(rel, s_list[w]);
+    {
+      for (int i = nrel - 1; i >= 0; --i) {
+        const int jj = s_list[w][i];
         const int j = lo + jj;
         const float4 g = cur.geo[jj];
         const float4 c = cur.col[jj];
