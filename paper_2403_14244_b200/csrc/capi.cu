@@ -39,6 +39,8 @@ struct isg_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  cudaStream_t copy_stream = nullptr;  // host<->device uploads overlapped with compute
+  cudaEvent_t ev_main = nullptr, ev_copy = nullptr;
   std::string err;
 
   // scene (SoA float4) and Adam moments (n x 2 float4 each)
@@ -448,12 +450,16 @@ const char* splat_message(const float* a, const float* c) {
 
 // Read back the frame scalars (syncs).  Returns ISG_E_DOMAIN for an invalid splat, and sets
 // *overflow when the key capacity was exceeded (capacity is grown for the re-run).
-isg_status check_frame(isg_ctx* ctx, bool* overflow) {
+// with_loss: also read the loss scalars back in the same synchronisation.
+isg_status check_frame(isg_ctx* ctx, bool* overflow, bool with_loss = false) {
   *overflow = false;
   ISG_CUDA(cudaMemcpyAsync(ctx->h_sc, ctx->sc, sizeof(uint32_t) * 8, cudaMemcpyDeviceToHost,
                            ctx->stream));
   ISG_CUDA(cudaMemcpyAsync(ctx->h_total, ctx->total, sizeof(unsigned long long) * 2,
                            cudaMemcpyDeviceToHost, ctx->stream));
+  if (with_loss)
+    ISG_CUDA(cudaMemcpyAsync(ctx->h_loss, ctx->loss, sizeof(double) * 3, cudaMemcpyDeviceToHost,
+                             ctx->stream));
   ISG_CUDA(cudaStreamSynchronize(ctx->stream));
   ctx->frame_unchecked = false;
   ctx->n_visible = ctx->h_sc[2];
@@ -548,6 +554,9 @@ isg_status isg_create(int device, int64_t max_gaussians, int32_t max_width, int3
   auto chk = [&](cudaError_t e) {
     if (e != cudaSuccess && s == ISG_OK) s = e == cudaErrorMemoryAllocation ? ISG_E_OOM : ISG_E_CUDA;
   };
+  chk(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+  chk(cudaEventCreateWithFlags(&ctx->ev_main, cudaEventDisableTiming));
+  chk(cudaEventCreateWithFlags(&ctx->ev_copy, cudaEventDisableTiming));
   chk(cudaMalloc(&ctx->sc, sizeof(uint32_t) * 8));
   chk(cudaMalloc(&ctx->total, sizeof(unsigned long long) * 2));
   chk(cudaMalloc(&ctx->loss, sizeof(double) * 3));
@@ -592,6 +601,12 @@ void isg_destroy(isg_ctx* ctx) {
     cudaEventDestroy(u.second.second);
   }
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  if (ctx->ev_main) cudaEventDestroy(ctx->ev_main);
+  if (ctx->ev_copy) cudaEventDestroy(ctx->ev_copy);
+  if (ctx->copy_stream) {
+    cudaStreamSynchronize(ctx->copy_stream);
+    cudaStreamDestroy(ctx->copy_stream);
+  }
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -714,12 +729,12 @@ isg_status isg_render(isg_ctx* ctx, const isg_camera* cam, const float bg[3], fl
   const FrameParams fp = make_fp(cam, bg, t_min);
   for (int attempt = 0; attempt < 3; ++attempt) {
     if ((s = launch_frame(ctx, fp, nullptr)) != ISG_OK) return s;
-    bool ov = false;
-    if ((s = check_frame(ctx, &ov)) != ISG_OK) return s;
-    if (ov) continue;
+    // image read-back queued behind the frame; one synchronisation covers both
     ISG_CUDA(cudaMemcpyAsync(out_hwc3, ctx->img, sizeof(float) * 3 * (size_t)cam->width * cam->height,
                              cudaMemcpyDeviceToHost, ctx->stream));
-    ISG_CUDA(cudaStreamSynchronize(ctx->stream));
+    bool ov = false;
+    if ((s = check_frame(ctx, &ov)) != ISG_OK) return s;
+    if (ov) continue;  // the copied image is stale: re-run with grown buffers
     return ISG_OK;
   }
   return fail(ctx, ISG_E_OVERFLOW, "render: key capacity kept overflowing");
@@ -750,23 +765,25 @@ isg_status isg_loss_backward(isg_ctx* ctx, const isg_camera* cam, const float bg
   if (s != ISG_OK) return s;
   if ((s = ensure_pixels(ctx, cam->width, cam->height)) != ISG_OK) return s;
   const FrameParams fp = make_fp(cam, bg, t_min);
+  // The target upload runs on the copy stream, overlapped with binning and the forward blend;
+  // only K7 consumes it.  It first waits for earlier work on the main stream (a previous K7
+  // may still read the buffer).
+  ISG_CUDA(cudaEventRecord(ctx->ev_main, ctx->stream));
+  ISG_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_main, 0));
   ISG_CUDA(cudaMemcpyAsync(ctx->target, target, sizeof(float) * 3 * (size_t)cam->width * cam->height,
-                           cudaMemcpyHostToDevice, ctx->stream));
+                           cudaMemcpyHostToDevice, ctx->copy_stream));
+  ISG_CUDA(cudaEventRecord(ctx->ev_copy, ctx->copy_stream));
   for (int attempt = 0; attempt < 3; ++attempt) {
     if ((s = launch_frame(ctx, fp, nullptr)) != ISG_OK) return s;
+    ISG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_copy, 0));
     if ((s = run_backward(ctx, fp, ctx->target, weight)) != ISG_OK) return s;
     bool ov = false;
-    if ((s = check_frame(ctx, &ov)) != ISG_OK) return s;
+    if ((s = check_frame(ctx, &ov, true)) != ISG_OK) return s;
     if (ov) {  // K6/K7 skipped the overflowed frame: nothing was accumulated
       ctx->pending = false;
       continue;
     }
-    if (loss_out) {
-      ISG_CUDA(cudaMemcpyAsync(ctx->h_loss, ctx->loss, sizeof(double) * 2, cudaMemcpyDeviceToHost,
-                               ctx->stream));
-      ISG_CUDA(cudaStreamSynchronize(ctx->stream));
-      *loss_out = ctx->h_loss[1];
-    }
+    if (loss_out) *loss_out = ctx->h_loss[1];
     return ISG_OK;
   }
   return fail(ctx, ISG_E_OVERFLOW, "loss_backward: key capacity kept overflowing");

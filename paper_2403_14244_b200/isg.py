@@ -298,10 +298,15 @@ class Renderer:
     def _bg(options: RenderOptions):
         return (C.c_float * 3)(*[float(b) for b in options.background])
 
-    def render(self, camera, options: RenderOptions = RenderOptions()) -> np.ndarray:
-        """render(iso) (splat3d.cpp:173-194): (H, W, 3) float32 image."""
+    def render(self, camera, options: RenderOptions = RenderOptions(),
+               out: Optional[np.ndarray] = None) -> np.ndarray:
+        """render(iso) (splat3d.cpp:173-194): (H, W, 3) float32 image (into `out` if given,
+        e.g. a pinned buffer)."""
         c = self._cam(camera)
-        out = np.empty((c.height, c.width, 3), np.float32)
+        if out is None:
+            out = np.empty((c.height, c.width, 3), np.float32)
+        elif out.dtype != np.float32 or out.size != c.height * c.width * 3 or not out.flags.c_contiguous:
+            raise ValueError("render: out must be a C-contiguous float32 (H, W, 3) array")
         _check(self._h, lib().isg_render(self._h, C.byref(c), self._bg(options),
                                          float(options.t_min), _ptr(out)))
         return out
