@@ -1,0 +1,284 @@
+// K7 — per-16x16-tile backward of the alpha blend, with the L2 loss gradient fused in.
+//
+// The backward the reference does not have (its 2D analogue is loss_gradients,
+// /root/reference/proj/src/loss.cpp:259-300).  Per pixel it walks the tile's depth-ordered
+// list in reverse from the last processed entry (n_proc - 1), recovering the transmittance
+// T_k = T_{k+1} / (1 - a_k) (the forward stores T *before* the last contributor, so a = 1 is
+// never divided by), and accumulating with A = colour behind:
+//     dL/da_k = T_k G.(c_k - A_k),  dL/dc_k = G T_k a_k,  A <- a c + (1 - a) A
+// with G = dL/dC = 2 w (C - target) / (3 W H) (mse, src/image.cpp:50-58) computed in the
+// prologue, and the kernel closed forms of include/isosplat/kernels.hpp:208-222.
+//
+// Mapping: 64 threads per tile.  Each HALF-warp owns one 8x8 quarter-tile and each lane a 2x2
+// pixel quad.  Per staged batch every half-warp compacts the entries whose 3-sigma circle can
+// reach its quarter into its own list; the two halves of a warp then walk their OWN lists in
+// lockstep — two different splats per warp step — so culling stays at 8x8 granularity while
+// the per-step costs (iteration, warp reduction) are shared by two (region, splat) pairs of four
+// pixels per lane.  The 7 gradients of a pair are summed over the lane's 4 pixels, reduce-
+// scattered over the 16 lanes in 8 shuffles, combined over the four quarters in shared memory
+// and written — no atomics — to the pair's gradient slot; K8 sums each splat's slots in a fixed
+// order, so gradients are bitwise deterministic.
+#include "blend_common.cuh"
+
+namespace isg {
+
+namespace {
+using namespace blend;
+
+constexpr int kBT = 64;     // threads per tile CTA: 2 warps = 4 half-warps = 4 quarter-tiles
+constexpr int kBatch = 64;  // records staged per batch (one per thread)
+
+struct BwdPix {
+  float G0, G1, G2;  // dL/dC
+  float T;           // transmittance before the most recently processed (later) entry
+  float A0, A1, A2;  // colour behind, normalised
+  int np;            // list entries the forward processed for this pixel
+};
+
+// acc: [0] sum go*dx, [1] sum go*dy, [2] sum go*r2 (scaled per entry into du, dv, dsigma2d),
+// [3] dopacity, [4..6] drgb;  go = dL/dalpha * g.  An inactive pixel gets e = 0, hence a = 0:
+// T and A stay exactly unchanged and every contribution is an exact zero.
+__device__ __forceinline__ void bwd_pixel(BwdPix& p, bool act, int j, float dx, float dy,
+                                          float r2, const float4 g, const float4 c,
+                                          float acc[8]) {
+  const float e = act ? fast_exp2(r2 * g.w) : 0.0f;
+  const float a = c.w * e;
+  const float Tk = (j == p.np - 1) ? p.T : p.T * fast_rcp(1.0f - a);
+  p.T = Tk;
+  const float d0 = c.x - p.A0, d1 = c.y - p.A1, d2 = c.z - p.A2;
+  const float dLda = Tk * (p.G0 * d0 + p.G1 * d1 + p.G2 * d2);
+  const float Ta = Tk * a;
+  acc[4] += p.G0 * Ta;
+  acc[5] += p.G1 * Ta;
+  acc[6] += p.G2 * Ta;
+  p.A0 += a * d0;
+  p.A1 += a * d1;
+  p.A2 += a * d2;
+  const float go = dLda * e;
+  acc[3] += go;
+  acc[0] += go * dx;
+  acc[1] += go * dy;
+  acc[2] += go * r2;
+}
+
+// reduce-scatter of 8 values over a 16-lane half-warp in 8 shuffles: lane l returns the sum
+// over its half of value (l >> 1) & 7.
+__device__ __forceinline__ float reduce_scatter8_half(const float v[8]) {
+  const int lane = threadIdx.x & 31;
+  const bool b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+  float w[4], x[2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float send = b3 ? v[i] : v[i + 4];
+    const float keep = b3 ? v[i + 4] : v[i];
+    w[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float send = b2 ? w[i] : w[i + 2];
+    const float keep = b2 ? w[i + 2] : w[i];
+    x[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  const float send = b1 ? x[0] : x[1];
+  const float keep = b1 ? x[1] : x[0];
+  float y = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  y += __shfl_xor_sync(0xffffffffu, y, 1);
+  return y;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kBT) k_blend_bwd(
+    FrameParams fp, const uint2* __restrict__ ranges, const uint2* __restrict__ sorted,
+    const RenderRec* __restrict__ rec, const unsigned long long* __restrict__ total,
+    int64_t key_cap, const float* __restrict__ img, const float* __restrict__ target,
+    const float* __restrict__ t_last, const uint32_t* __restrict__ n_proc, float loss_scale,
+    float4* __restrict__ partial, double* __restrict__ tile_loss) {
+  __shared__ Stage<kBatch> st[2];
+  // [quarter][value][entry]; rows padded so one entry's 8 values hit 8 different banks
+  __shared__ float s_part[4][8][kBatch + 1];
+  __shared__ uint32_t s_rel[4][kBatch / 32];
+  __shared__ uint8_t s_list[4][kBatch];
+  __shared__ float s_red[2];
+  __shared__ int s_max[2];
+  const int tile = blockIdx.x;
+  if (overflowed(total, key_cap)) {
+    if (threadIdx.x == 0) tile_loss[tile] = 0.0;
+    return;
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int h = lane >> 4, l16 = lane & 15;
+  const int q = 2 * w + h;  // this half-warp's quarter-tile
+  const int tx = tile % fp.tiles_x, ty = tile / fp.tiles_x;
+  const int W = fp.cam.width, H = fp.cam.height;
+  const int x0 = tx * kTile + (q & 1) * 8 + 2 * (l16 & 3);
+  const int y0 = ty * kTile + (q >> 1) * 8 + 2 * (l16 >> 2);
+  const float px[2] = {(float)x0 + 0.5f, (float)x0 + 1.5f};
+  const float py[2] = {(float)y0 + 0.5f, (float)y0 + 1.5f};
+  const Region regA = region_rect(fp, tile, 2 * w), regB = region_rect(fp, tile, 2 * w + 1);
+  const uint2 rg = ranges[tile];
+  const int n = (int)(rg.y - rg.x);
+
+  BwdPix P[4];
+  float dsq = 0.0f;
+  int npmax = 0;
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    BwdPix& s = P[p];
+    s.G0 = s.G1 = s.G2 = 0.0f;
+    s.T = 0.0f;
+    s.np = 0;
+    s.A0 = fp.bg[0];
+    s.A1 = fp.bg[1];
+    s.A2 = fp.bg[2];
+    const int x = x0 + (p & 1), y = y0 + (p >> 1);
+    if (x < W && y < H) {
+      const size_t pix = (size_t)y * W + x;
+      const float d0 = img[3 * pix + 0] - target[3 * pix + 0];
+      const float d1 = img[3 * pix + 1] - target[3 * pix + 1];
+      const float d2 = img[3 * pix + 2] - target[3 * pix + 2];
+      dsq += d0 * d0 + d1 * d1 + d2 * d2;
+      s.G0 = 2.0f * d0 * loss_scale;
+      s.G1 = 2.0f * d1 * loss_scale;
+      s.G2 = 2.0f * d2 * loss_scale;
+      s.T = t_last[pix];
+      s.np = (int)n_proc[pix];
+      npmax = max(npmax, s.np);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    dsq += __shfl_xor_sync(0xffffffffu, dsq, o);
+    npmax = max(npmax, __shfl_xor_sync(0xffffffffu, npmax, o));
+  }
+  if (lane == 0) {
+    s_red[w] = dsq;
+    s_max[w] = npmax;
+  }
+  __syncthreads();
+  const int m = max(s_max[0], s_max[1]);  // entries [0, m) are walked
+  if (threadIdx.x == 0) tile_loss[tile] = (double)s_red[0] + (double)s_red[1];
+  // entries never reached by any pixel get zero gradient slots
+  for (int j = m + (int)threadIdx.x; j < n; j += kBT) {
+    const uint32_t e = sorted[rg.x + j].y;
+    partial[2 * (size_t)e] = make_float4(0.f, 0.f, 0.f, 0.f);
+    partial[2 * (size_t)e + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  if (m == 0) return;
+
+  const uint32_t lt = (1u << lane) - 1u;
+  int hi = m;
+  stage_batch(st[0], sorted, rec, rg.x + max(0, hi - kBatch), min(kBatch, hi));
+  for (int it = 0; hi > 0; ++it) {
+    const int lo = max(0, hi - kBatch);
+    const int cnt = hi - lo;
+    Stage<kBatch>& cur = st[it & 1];
+    cp_async_wait_all();
+    __syncthreads();  // batch visible; previous batch's flush finished reading s_part
+    if (lo > 0) {
+      const int nlo = max(0, lo - kBatch);
+      stage_batch(st[(it + 1) & 1], sorted, rec, rg.x + nlo, lo - nlo);
+    }
+    // relevance of the batch for this warp's two quarters -> two compacted lists
+    int cntA = 0, cntB = 0;
+#pragma unroll
+    for (int k = 0; k < kBatch / 32; ++k) {
+      const int j = 32 * k + lane;
+      bool ha = false, hb = false;
+      if (j < cnt) {
+        const float4 g = cur.geo[j];
+        ha = regA.valid && rect_hit(regA, g.x, g.y, g.z);
+        hb = regB.valid && rect_hit(regB, g.x, g.y, g.z);
+      }
+      const uint32_t ma = __ballot_sync(0xffffffffu, ha);
+      const uint32_t mb = __ballot_sync(0xffffffffu, hb);
+      if (ha) s_list[2 * w][cntA + __popc(ma & lt)] = (uint8_t)j;
+      if (hb) s_list[2 * w + 1][cntB + __popc(mb & lt)] = (uint8_t)j;
+      cntA += __popc(ma);
+      cntB += __popc(mb);
+      if (lane == 0) {
+        s_rel[2 * w][k] = ma;
+        s_rel[2 * w + 1][k] = mb;
+      }
+    }
+    __syncwarp();
+    const int my_cnt = h ? cntB : cntA;
+    const int steps = max(cntA, cntB);
+    for (int s = 0; s < steps; ++s) {
+      const int i = my_cnt - 1 - s;  // reverse depth order
+      const bool has = i >= 0;
+      const int jj = has ? s_list[q][i] : 0;
+      const int j = lo + jj;
+      const float4 g = cur.geo[jj];
+      const float4 c = cur.col[jj];
+      const float dx[2] = {__fsub_rn(px[0], g.x), __fsub_rn(px[1], g.x)};
+      const float dy[2] = {__fsub_rn(py[0], g.y), __fsub_rn(py[1], g.y)};
+      const float ax[2] = {__fmul_rn(dx[0], dx[0]), __fmul_rn(dx[1], dx[1])};
+      const float ay[2] = {__fmul_rn(dy[0], dy[0]), __fmul_rn(dy[1], dy[1])};
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const float r2 = __fadd_rn(ax[p & 1], ay[p >> 1]);
+        const bool act = has && j < P[p].np && !(r2 > g.z);
+        bwd_pixel(P[p], act, j, dx[p & 1], dy[p >> 1], r2, g, c, acc);
+      }
+      // kernels.hpp:219-220: dg/du = g 2 dx / s^2, dg/ds = g 2 r^2 / s^3, times opacity
+      const float inv_s2 = g.w * -kLn2;     // 1 / sigma2d^2
+      const float k2 = 2.0f * c.w * inv_s2;  // 2 o / s^2
+      acc[0] *= k2;
+      acc[1] *= k2;
+      acc[2] *= k2 * fast_sqrt(inv_s2);      // 2 o / s^3
+      const float y = reduce_scatter8_half(acc);
+      if (has && (l16 & 1) == 0) s_part[q][l16 >> 1][jj] = y;
+    }
+    __syncthreads();
+    // combine the quarters and write each (tile, splat) pair's gradient slot
+    if ((int)threadIdx.x < cnt) {
+      const int jj = threadIdx.x;
+      float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        if (!((s_rel[r][jj >> 5] >> (jj & 31)) & 1u)) continue;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] += s_part[r][k][jj];
+      }
+      const size_t e = cur.slot[jj];
+      partial[2 * e] = make_float4(v[0], v[1], v[2], v[3]);
+      partial[2 * e + 1] = make_float4(v[4], v[5], v[6], 0.0f);
+    }
+    hi = lo;
+  }
+}
+
+__global__ void k_loss_reduce(const double* __restrict__ tile_loss, int n_tiles, double scale,
+                              double* __restrict__ loss) {
+  __shared__ double s[256];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n_tiles; i += 256) acc += tile_loss[i];
+  s[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    loss[0] += s[0] * scale;  // accumulated over views
+    loss[1] = s[0] * scale;   // this view
+  }
+}
+
+void launch_blend_bwd(const FrameParams& fp, const uint2* ranges, const uint2* sorted,
+                      const RenderRec* rec, const unsigned long long* total, int64_t key_cap,
+                      const float* img, const float* target, const float* t_last,
+                      const uint32_t* n_proc, float loss_scale, float4* partial,
+                      double* tile_loss, cudaStream_t st) {
+  k_blend_bwd<<<fp.n_tiles, kBT, 0, st>>>(fp, ranges, sorted, rec, total, key_cap, img, target,
+                                          t_last, n_proc, loss_scale, partial, tile_loss);
+}
+
+void launch_loss_reduce(const double* tile_loss, int n_tiles, double scale, double* loss,
+                        cudaStream_t st) {
+  k_loss_reduce<<<1, 256, 0, st>>>(tile_loss, n_tiles, scale, loss);
+}
+
+}  // namespace isg
