@@ -56,7 +56,8 @@ struct isg_ctx {
   uint32_t* ntiles = nullptr;     // tiles touched per splat
   uint32_t* slot_off = nullptr;   // start of splat g's gradient-slot list
   float4* grad3d = nullptr;       // n x 2, indexed by splat
-  uint32_t* depth[2] = {nullptr, nullptr};  // radix mode: depth keys / depth order
+  uint2* tilebox = nullptr;                 // compact tile bbox + hit mask per splat
+  uint32_t* depth[2] = {nullptr, nullptr};  // depth keys (+ radix ping-pong) / depth order
   uint32_t* order[2] = {nullptr, nullptr};
   int order_buf = 0;
 
@@ -204,11 +205,10 @@ isg_status ensure_scene(isg_ctx* ctx, int64_t n) {
   ISG_CUDA(realloc_dev(&ctx->ntiles, a));
   ISG_CUDA(realloc_dev(&ctx->slot_off, a));
   ISG_CUDA(realloc_dev(&ctx->grad3d, 2 * a));
-  if (ctx->radix_alloc) {
-    for (int i = 0; i < 2; ++i) {
-      ISG_CUDA(realloc_dev(&ctx->depth[i], a));
-      ISG_CUDA(realloc_dev(&ctx->order[i], a));
-    }
+  ISG_CUDA(realloc_dev(&ctx->tilebox, a));
+  for (int i = 0; i < 2; ++i) {
+    ISG_CUDA(realloc_dev(&ctx->depth[i], a));
+    ISG_CUDA(realloc_dev(&ctx->order[i], a));
   }
   const int64_t words =
       std::max(isg::scan_emit_scratch_words(a), isg::fill_scratch_words(a)) + 1;
@@ -250,12 +250,7 @@ isg_status ensure_keys(isg_ctx* ctx, int64_t cap) {
 isg_status ensure_radix(isg_ctx* ctx) {
   if (ctx->radix_alloc) return ISG_OK;
   ctx->radix_alloc = true;
-  const int64_t a = ctx->n_alloc, cap = ctx->key_cap;
-  if (a > 0)
-    for (int i = 0; i < 2; ++i) {
-      ISG_CUDA(realloc_dev(&ctx->depth[i], a));
-      ISG_CUDA(realloc_dev(&ctx->order[i], a));
-    }
+  const int64_t cap = ctx->key_cap;
   if (cap > 0) {
     for (int i = 0; i < 2; ++i) {
       ISG_CUDA(realloc_dev(&ctx->tkey[i], cap));
@@ -374,8 +369,8 @@ isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out) {
   }
   {
   ISG_STAGE(ST_PREPROCESS);
-  isg::launch_preprocess(ctx->ms, ctx->co, n, fp, ctx->rec, radix ? ctx->depth[0] : nullptr,
-                         ctx->ntiles, radix ? nullptr : ctx->tile_cnt, ctx->sc, st);
+  isg::launch_preprocess(ctx->ms, ctx->co, n, fp, ctx->rec, ctx->depth[0], ctx->ntiles,
+                         ctx->tilebox, radix ? nullptr : ctx->tile_cnt, ctx->sc, st);
   ISG_CHECK_LAUNCH();
   ctx->launches++;
   }
@@ -388,9 +383,9 @@ isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out) {
     }
     {
     ISG_STAGE(ST_SCAN_EMIT);
-    isg::launch_scan_emit(ctx->order[ctx->order_buf], ctx->ntiles, ctx->ms, n, fp, ctx->slot_off,
-                          ctx->tkey[0], ctx->emit_gid, ctx->key_cap, ctx->scan_scratch,
-                          ctx->sc + 3, ctx->sc + 0, ctx->total, st);
+    isg::launch_scan_emit(ctx->order[ctx->order_buf], ctx->ntiles, ctx->tilebox, ctx->ms, n, fp,
+                          ctx->slot_off, ctx->tkey[0], ctx->emit_gid, ctx->key_cap,
+                          ctx->scan_scratch, ctx->sc + 3, ctx->sc + 0, ctx->total, st);
     ISG_CHECK_LAUNCH();
     ctx->launches++;
     }
@@ -415,8 +410,9 @@ isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out) {
     }
     if (n > 0) {
       ISG_STAGE(ST_FILL);
-      isg::launch_fill(ctx->ms, ctx->ntiles, n, fp, ctx->cursor, ctx->bucket, ctx->slot_of,
-                       ctx->slot_off, ctx->key_cap, ctx->scan_scratch, ctx->sc + 3, st);
+      isg::launch_fill(ctx->ms, ctx->ntiles, ctx->tilebox, ctx->depth[0], n, fp, ctx->cursor,
+                       ctx->bucket, ctx->slot_of, ctx->slot_off, ctx->key_cap, ctx->scan_scratch,
+                       ctx->sc + 3, st);
       ISG_CHECK_LAUNCH();
       ctx->launches++;
     }
@@ -584,7 +580,7 @@ void isg_destroy(isg_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->nccl_comm) isg_nccl_detach(ctx);
-  void* dev[] = {ctx->ms, ctx->co, ctx->m, ctx->v, ctx->rec, ctx->ntiles, ctx->slot_off,
+  void* dev[] = {ctx->ms, ctx->co, ctx->m, ctx->v, ctx->rec, ctx->ntiles, ctx->slot_off, ctx->tilebox,
                  ctx->grad3d, ctx->depth[0], ctx->depth[1], ctx->order[0], ctx->order[1],
                  ctx->sorted, ctx->partial, ctx->bucket, ctx->slot_of, ctx->tkey[0], ctx->tkey[1],
                  ctx->tval[0], ctx->tval[1], ctx->emit_gid, ctx->sort.hist, ctx->sort.lookback,

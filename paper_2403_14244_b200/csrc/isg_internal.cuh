@@ -63,21 +63,21 @@ int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], bool iota_vals, const
                      int64_t* launches);
 
 // ---- K1 ------------------------------------------------------------------------------------
-// sc: [1] first invalid splat (atomicMin), [2] visible splats, [4] n.  depth_key (radix mode)
-// and tile_cnt (tile-bucket mode) may be null.
+// sc: [1] first invalid splat (atomicMin), [2] visible splats, [4] n.  tilebox: compact tile
+// bbox + hit mask per splat (see for_each_tile).  tile_cnt (tile-bucket mode) may be null.
 void launch_preprocess(const float4* ms, const float4* co, int64_t n, const FrameParams& fp,
-                       RenderRec* rec, uint32_t* depth_key, uint32_t* ntiles, uint32_t* tile_cnt,
-                       uint32_t* sc, cudaStream_t st);
+                       RenderRec* rec, uint32_t* depth_key, uint32_t* ntiles, uint2* tilebox,
+                       uint32_t* tile_cnt, uint32_t* sc, cudaStream_t st);
 
 // ---- tile-bucket binning (k_bin.cu) -------------------------------------------------------
 int64_t fill_scratch_words(int64_t n);  // + 1 zeroed u64 words of look-back scratch
 void launch_tile_scan(const uint32_t* cnt, int n_tiles, int64_t cap, uint2* ranges,
                       uint32_t* cursor, uint32_t* n_keys, unsigned long long* total,
                       cudaStream_t st);
-void launch_fill(const float4* ms, const uint32_t* ntiles, int64_t n, const FrameParams& fp,
-                 uint32_t* cursor, unsigned long long* bucket, uint32_t* slot_of,
-                 uint32_t* slot_off, int64_t cap, unsigned long long* lookback, uint32_t* counter,
-                 cudaStream_t st);
+void launch_fill(const float4* ms, const uint32_t* ntiles, const uint2* tilebox,
+                 const uint32_t* depth_key, int64_t n, const FrameParams& fp, uint32_t* cursor,
+                 unsigned long long* bucket, uint32_t* slot_of, uint32_t* slot_off, int64_t cap,
+                 unsigned long long* lookback, uint32_t* counter, cudaStream_t st);
 // scratch: the gradient-slot buffer (2 float4 per key), used only for tiles > 2048 entries.
 void launch_tile_sort(const FrameParams& fp, const uint2* ranges, const unsigned long long* bucket,
                       const unsigned long long* total, int64_t cap, uint2* sorted, float4* scratch,
@@ -85,11 +85,11 @@ void launch_tile_sort(const FrameParams& fp, const uint2* ranges, const unsigned
 
 // ---- radix binning (k_sort.cu) ------------------------------------------------------------
 int64_t scan_emit_scratch_words(int64_t n);  // + 1 zeroed u64 words
-void launch_scan_emit(const uint32_t* order, const uint32_t* ntiles, const float4* ms, int64_t n,
-                      const FrameParams& fp, uint32_t* slot_off, uint32_t* tile_keys,
-                      uint32_t* emit_gid, int64_t key_cap, unsigned long long* scratch,
-                      uint32_t* counter, uint32_t* n_keys, unsigned long long* n_keys_total,
-                      cudaStream_t st);
+void launch_scan_emit(const uint32_t* order, const uint32_t* ntiles, const uint2* tilebox,
+                      const float4* ms, int64_t n, const FrameParams& fp, uint32_t* slot_off,
+                      uint32_t* tile_keys, uint32_t* emit_gid, int64_t key_cap,
+                      unsigned long long* scratch, uint32_t* counter, uint32_t* n_keys,
+                      unsigned long long* n_keys_total, cudaStream_t st);
 void launch_ranges(const uint32_t* sorted_tiles, const uint32_t* e_sorted,
                    const uint32_t* emit_gid, const uint32_t* n_keys, int64_t key_cap,
                    uint2* ranges, uint2* sorted, cudaStream_t st);

@@ -79,6 +79,34 @@ __device__ __forceinline__ bool tile_bbox(float u, float v, float s, int tiles_x
   return true;
 }
 
+// Visit the tiles a splat touches, in row-major order (the order K1 counted them).  `box` is
+// K1's compact record: x0 | y0 << 12 | bw << 24 and a hit mask over the (<= 32-tile) bbox; for
+// bigger boxes (bw == 0) the projection and the exact tile tests are recomputed from `ms`.
+template <class F>
+__device__ __forceinline__ void for_each_tile(uint2 box, const float4& ms, const FrameParams& fp,
+                                              F&& f) {
+  const uint32_t bw = box.x >> 24;
+  if (bw) {
+    const uint32_t x0 = box.x & 0xFFFu, y0 = (box.x >> 12) & 0xFFFu;
+    const uint32_t inv = (65536u + bw - 1u) / bw;  // exact floor(b / bw) for b < 32
+    uint32_t m = box.y;
+    while (m) {
+      const uint32_t b = __ffs(m) - 1;
+      m &= m - 1;
+      const uint32_t r = (b * inv) >> 16;
+      f((int)((y0 + r) * (uint32_t)fp.tiles_x + x0 + (b - r * bw)));
+    }
+    return;
+  }
+  const Proj p = project(ms, fp.cam);
+  int x0, x1, y0, y1;
+  if (!p.vis || !tile_bbox(p.u, p.v, p.s, fp.tiles_x, fp.tiles_y, x0, x1, y0, y1)) return;
+  for (int ty = y0; ty <= y1; ++ty)
+    for (int tx = x0; tx <= x1; ++tx)
+      if (tile_hit(p.u, p.v, p.r2max, tx, ty, fp.cam.width, fp.cam.height))
+        f(ty * fp.tiles_x + tx);
+}
+
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

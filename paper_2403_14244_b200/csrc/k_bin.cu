@@ -91,8 +91,9 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_scan(const uint32_t* __re
 
 // ---- K3: per-splat slot lists + bucket fill ---------------------------------------------------
 __global__ void __launch_bounds__(kFillThreads) k_fill(
-    const float4* __restrict__ ms, const uint32_t* __restrict__ ntiles, int64_t n, FrameParams fp,
-    uint32_t* __restrict__ cursor, unsigned long long* __restrict__ bucket,
+    const float4* __restrict__ ms, const uint32_t* __restrict__ ntiles,
+    const uint2* __restrict__ tilebox, const uint32_t* __restrict__ depth_key, int64_t n,
+    FrameParams fp, uint32_t* __restrict__ cursor, unsigned long long* __restrict__ bucket,
     uint32_t* __restrict__ slot_of, uint32_t* __restrict__ slot_off, int64_t cap,
     unsigned long long* __restrict__ lookback, uint32_t* __restrict__ counter) {
   __shared__ uint32_t s_tile;
@@ -126,18 +127,15 @@ __global__ void __launch_bounds__(kFillThreads) k_fill(
     if (g >= n) break;
     slot_off[g] = (uint32_t)min(off, (unsigned long long)0xFFFFFFFFull);
     if (c[j] == 0) continue;
-    const Proj p = project(ms[g], fp.cam);
-    const unsigned long long key = ((unsigned long long)__float_as_uint(p.zc) << 32) | (uint32_t)g;
-    int x0, x1, y0, y1;
-    tile_bbox(p.u, p.v, p.s, fp.tiles_x, fp.tiles_y, x0, x1, y0, y1);
-    for (int ty = y0; ty <= y1; ++ty)
-      for (int tx = x0; tx <= x1; ++tx) {
-        if (!tile_hit(p.u, p.v, p.r2max, tx, ty, fp.cam.width, fp.cam.height)) continue;
-        const uint32_t slot = atomicAdd(&cursor[ty * fp.tiles_x + tx], 1u);
-        if (slot < (uint64_t)cap) bucket[slot] = key;
-        if (off < (unsigned long long)cap) slot_of[off] = slot;
-        ++off;
-      }
+    const unsigned long long key = ((unsigned long long)depth_key[g] << 32) | (uint32_t)g;
+    const uint2 box = tilebox[g];
+    const float4 m = (box.x >> 24) ? make_float4(0.f, 0.f, 0.f, 0.f) : ms[g];
+    for_each_tile(box, m, fp, [&](int t) {
+      const uint32_t slot = atomicAdd(&cursor[t], 1u);
+      if (slot < (uint64_t)cap) bucket[slot] = key;
+      if (off < (unsigned long long)cap) slot_of[off] = slot;
+      ++off;
+    });
   }
 }
 
@@ -257,14 +255,15 @@ void launch_tile_scan(const uint32_t* cnt, int n_tiles, int64_t cap, uint2* rang
   k_tile_scan<<<1, kScanThreads, 0, st>>>(cnt, n_tiles, cap, ranges, cursor, n_keys, total);
 }
 
-void launch_fill(const float4* ms, const uint32_t* ntiles, int64_t n, const FrameParams& fp,
-                 uint32_t* cursor, unsigned long long* bucket, uint32_t* slot_of,
-                 uint32_t* slot_off, int64_t cap, unsigned long long* lookback, uint32_t* counter,
-                 cudaStream_t st) {
+void launch_fill(const float4* ms, const uint32_t* ntiles, const uint2* tilebox,
+                 const uint32_t* depth_key, int64_t n, const FrameParams& fp, uint32_t* cursor,
+                 unsigned long long* bucket, uint32_t* slot_of, uint32_t* slot_off, int64_t cap,
+                 unsigned long long* lookback, uint32_t* counter, cudaStream_t st) {
   const int64_t tiles = fill_scratch_words(n);
   if (tiles == 0) return;
-  k_fill<<<(unsigned)tiles, kFillThreads, 0, st>>>(ms, ntiles, n, fp, cursor, bucket, slot_of,
-                                                   slot_off, cap, lookback, counter);
+  k_fill<<<(unsigned)tiles, kFillThreads, 0, st>>>(ms, ntiles, tilebox, depth_key, n, fp, cursor,
+                                                   bucket, slot_of, slot_off, cap, lookback,
+                                                   counter);
 }
 
 void launch_tile_sort(const FrameParams& fp, const uint2* ranges, const unsigned long long* bucket,

@@ -17,6 +17,7 @@ __global__ void __launch_bounds__(256) k_preprocess(const float4* __restrict__ m
                                                     FrameParams fp, RenderRec* __restrict__ rec,
                                                     uint32_t* __restrict__ depth_key,
                                                     uint32_t* __restrict__ ntiles,
+                                                    uint2* __restrict__ tilebox,
                                                     uint32_t* __restrict__ tile_cnt,
                                                     uint32_t* __restrict__ sc) {
   // sc: [1] first invalid splat (atomicMin), [2] visible splats, [4] n (device count)
@@ -24,6 +25,7 @@ __global__ void __launch_bounds__(256) k_preprocess(const float4* __restrict__ m
   if (i == 0) sc[4] = (uint32_t)n;
   uint32_t count = 0;
   if (i < n) {
+    uint2 box = make_uint2(0u, 0u);
     const float4 a = ms[i];
     const float4 c = co[i];
     // IsoSplat3D::validate (splat3d.cpp:10-17): finite mu, sigma > 0 finite, finite color,
@@ -36,19 +38,26 @@ __global__ void __launch_bounds__(256) k_preprocess(const float4* __restrict__ m
     if (p.vis && ok) {
       int x0, x1, y0, y1;
       if (tile_bbox(p.u, p.v, p.s, fp.tiles_x, fp.tiles_y, x0, x1, y0, y1)) {
+        const int bw = x1 - x0 + 1;
+        const bool small = bw * (y1 - y0 + 1) <= 32 && bw < 256 && x0 < 4096 && y0 < 4096;
+        uint32_t mask = 0;
         for (int ty = y0; ty <= y1; ++ty)
           for (int tx = x0; tx <= x1; ++tx) {
             if (!tile_hit(p.u, p.v, p.r2max, tx, ty, fp.cam.width, fp.cam.height)) continue;
+            if (small) mask |= 1u << ((ty - y0) * bw + (tx - x0));
             ++count;
             if (tile_cnt) atomicAdd(&tile_cnt[ty * fp.tiles_x + tx], 1u);
           }
+        // emission kernels iterate the hit bits instead of re-projecting (bw == 0: re-project)
+        if (small) box = make_uint2((uint32_t)x0 | ((uint32_t)y0 << 12) | ((uint32_t)bw << 24), mask);
       }
     }
+    tilebox[i] = box;
     RenderRec r;  // (u, v, r2max, -log2(e)/sigma2d^2), (r, g, b, opacity)
     r.geo = make_float4(p.u, p.v, p.r2max, __fdiv_rn(-1.4426950408889634f, __fmul_rn(p.s, p.s)));
     r.col = c;
     rec[i] = r;
-    if (depth_key) depth_key[i] = count ? __float_as_uint(p.zc) : 0xFFFFFFFFu;
+    depth_key[i] = count ? __float_as_uint(p.zc) : 0xFFFFFFFFu;
     ntiles[i] = count;
   }
   // visible-splat count, one atomic per warp
@@ -57,11 +66,11 @@ __global__ void __launch_bounds__(256) k_preprocess(const float4* __restrict__ m
 }
 
 void launch_preprocess(const float4* ms, const float4* co, int64_t n, const FrameParams& fp,
-                       RenderRec* rec, uint32_t* depth_key, uint32_t* ntiles, uint32_t* tile_cnt,
-                       uint32_t* sc, cudaStream_t st) {
+                       RenderRec* rec, uint32_t* depth_key, uint32_t* ntiles, uint2* tilebox,
+                       uint32_t* tile_cnt, uint32_t* sc, cudaStream_t st) {
   const int64_t blocks = n > 0 ? (n + 255) / 256 : 1;
-  k_preprocess<<<(unsigned)blocks, 256, 0, st>>>(ms, co, n, fp, rec, depth_key, ntiles, tile_cnt,
-                                                 sc);
+  k_preprocess<<<(unsigned)blocks, 256, 0, st>>>(ms, co, n, fp, rec, depth_key, ntiles, tilebox,
+                                                 tile_cnt, sc);
 }
 
 // Parity hook: (tile << 32 | float_bits(depth)) and splat index for each sorted entry.

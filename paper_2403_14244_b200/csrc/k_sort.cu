@@ -156,23 +156,25 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
   // decoupled look-back for digit `tid`
   uint32_t excl = 0;
   if (tile > 0) {
-    // walk back 4 predecessors per round trip (statuses only move 0 -> AGG -> INC, so a stale
-    // aggregate is still a correct partial sum)
+    // walk back kWin predecessors per round trip, all loads in flight at once (statuses only
+    // move 0 -> AGG -> INC, so a stale aggregate is still a correct partial sum); the
+    // inclusive-prefix frontier then advances kWin tiles per L2 round trip
+    constexpr int kWin = 16;
     int64_t p = (int64_t)tile - 1;
     bool found = false;
     while (!found) {
-      uint32_t s[4];
+      uint32_t s[kWin];
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < kWin; ++q)
         s[q] = p - q >= 0 ? ld_volatile(lookback + (p - q) * 256 + tid) : kFlagInc;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < kWin; ++q) {
         if (found) break;
         while ((s[q] & ~kCountMask) == 0) s[q] = ld_volatile(lookback + (p - q) * 256 + tid);
         excl += s[q] & kCountMask;
         found = (s[q] & ~kCountMask) == kFlagInc;
       }
-      p -= 4;
+      p -= kWin;
     }
     st_volatile(my, kFlagInc | (excl + cnt));
   }
@@ -223,8 +225,9 @@ constexpr int kScanTileItems = kScanThreads * kScanItems;
 
 __global__ void __launch_bounds__(kScanThreads) k_scan_emit(
     const uint32_t* __restrict__ order, const uint32_t* __restrict__ ntiles,
-    const float4* __restrict__ ms, int64_t n, FrameParams fp, uint32_t* __restrict__ slot_off,
-    uint32_t* __restrict__ tile_keys, uint32_t* __restrict__ emit_gid, int64_t key_cap,
+    const uint2* __restrict__ tilebox, const float4* __restrict__ ms, int64_t n, FrameParams fp,
+    uint32_t* __restrict__ slot_off, uint32_t* __restrict__ tile_keys,
+    uint32_t* __restrict__ emit_gid, int64_t key_cap,
     unsigned long long* __restrict__ lookback, uint32_t* __restrict__ counter,
     uint32_t* __restrict__ n_keys, unsigned long long* __restrict__ n_keys_total) {
   __shared__ uint32_t s_tile;
@@ -268,18 +271,15 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(
     const uint32_t gg = g[j];
     slot_off[gg] = (uint32_t)min(off, (unsigned long long)0xFFFFFFFFu);
     if (c[j] == 0) continue;
-    const Proj p = project(ms[gg], fp.cam);  // bit-identical to K1's projection
-    int x0, x1, y0, y1;
-    tile_bbox(p.u, p.v, p.s, fp.tiles_x, fp.tiles_y, x0, x1, y0, y1);
-    for (int ty = y0; ty <= y1; ++ty)
-      for (int tx = x0; tx <= x1; ++tx) {
-        if (!tile_hit(p.u, p.v, p.r2max, tx, ty, fp.cam.width, fp.cam.height)) continue;
-        if (off < (unsigned long long)key_cap) {
-          tile_keys[off] = (uint32_t)(ty * fp.tiles_x + tx);
-          emit_gid[off] = gg;
-        }
-        ++off;
+    const uint2 box = tilebox[gg];
+    const float4 m = (box.x >> 24) ? make_float4(0.f, 0.f, 0.f, 0.f) : ms[gg];
+    for_each_tile(box, m, fp, [&](int t) {
+      if (off < (unsigned long long)key_cap) {
+        tile_keys[off] = (uint32_t)t;
+        emit_gid[off] = gg;
       }
+      ++off;
+    });
   }
 }
 
@@ -287,16 +287,16 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(
 
 int64_t scan_emit_scratch_words(int64_t n) { return (n + kScanTileItems - 1) / kScanTileItems; }
 
-void launch_scan_emit(const uint32_t* order, const uint32_t* ntiles, const float4* ms, int64_t n,
-                      const FrameParams& fp, uint32_t* slot_off, uint32_t* tile_keys,
-                      uint32_t* emit_gid, int64_t key_cap, unsigned long long* scratch,
-                      uint32_t* counter, uint32_t* n_keys, unsigned long long* n_keys_total,
-                      cudaStream_t st) {
+void launch_scan_emit(const uint32_t* order, const uint32_t* ntiles, const uint2* tilebox,
+                      const float4* ms, int64_t n, const FrameParams& fp, uint32_t* slot_off,
+                      uint32_t* tile_keys, uint32_t* emit_gid, int64_t key_cap,
+                      unsigned long long* scratch, uint32_t* counter, uint32_t* n_keys,
+                      unsigned long long* n_keys_total, cudaStream_t st) {
   const int64_t tiles = scan_emit_scratch_words(n);
   if (tiles == 0) return;  // caller zeroed the counts
-  k_scan_emit<<<(unsigned)tiles, kScanThreads, 0, st>>>(order, ntiles, ms, n, fp, slot_off,
-                                                        tile_keys, emit_gid, key_cap, scratch,
-                                                        counter, n_keys, n_keys_total);
+  k_scan_emit<<<(unsigned)tiles, kScanThreads, 0, st>>>(order, ntiles, tilebox, ms, n, fp,
+                                                        slot_off, tile_keys, emit_gid, key_cap,
+                                                        scratch, counter, n_keys, n_keys_total);
 }
 
 void launch_ranges(const uint32_t* sorted_tiles, const uint32_t* e_sorted,
