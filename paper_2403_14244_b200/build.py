@@ -92,7 +92,8 @@ DROPIN_BIN = ROOT / "build" / "test_dropin"
 
 def build_dropin_test(force: bool = False) -> Path:
     """The C++ drop-in (csrc/isosplat_b200.hpp) used the way the reference's caller uses it."""
-    deps = [DROPIN_SRC, CSRC / "isosplat_b200.hpp", ROOT / "include" / "isg.h"]
+    deps = [DROPIN_SRC, CSRC / "isosplat_b200.hpp", CSRC / "isosplat_io.hpp",
+            ROOT / "include" / "isg.h"]
     stamp = DROPIN_BIN.with_suffix(".sha256")
     digest = _digest(deps)
     if not force and DROPIN_BIN.exists() and stamp.exists() and stamp.read_text() == digest:

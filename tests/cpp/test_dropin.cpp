@@ -4,15 +4,23 @@
 //   test_dropin validate   host-only checks (no GPU needed)
 //   test_dropin render     3-splat fixture on the GPU vs known answers
 //   test_dropin train      Trainer: loss decreases over Adam steps
+//   test_dropin io DIR     ISPL binary/JSON + camera JSON round trips (host only)
+//   test_dropin render3d SCENE CAMERA OUT.png   the reference's run_render3d flow
+//                          (tools/isosplat_main.cpp:357-398) on the B200 path
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <fstream>
+#include <iostream>
 #include <stdexcept>
 #include <vector>
 
 #include "isosplat_b200.hpp"
+#include "isosplat_io.hpp"
 
 using namespace isosplat;
+
+constexpr int kExitBadInput = 2;  // tools/isosplat_main.cpp:30
 
 static std::vector<IsoSplat3D> three_splats() {  // proj/tools/make_fixtures.py:73-78
   std::vector<IsoSplat3D> s(3);
@@ -103,6 +111,69 @@ int main(int argc, char** argv) {
     std::printf("loss %.6g -> %.6g\n", first, last);
     if (!(last < 0.5 * first)) return fail("loss did not decrease");
     std::printf("OK train\n");
+    return 0;
+  }
+  if (!std::strcmp(mode, "io") && argc > 2) {
+    const std::string dir = argv[2];
+    ParticleSet set;
+    set.iso3d = three_splats();
+    set.metadata_json = "{\"name\":\"three_splats\"}";
+    save_particles(dir + "/cpp_scene.ispl", set, false);
+    save_particles(dir + "/cpp_scene.json", set, true);
+    for (const char* f : {"/cpp_scene.ispl", "/cpp_scene.json"}) {
+      const ParticleSet back = load_particles(dir + f);
+      if (back.count() != 3) return fail("round trip count");
+      for (int i = 0; i < 3; ++i)
+        if (back.iso3d[i].mu[0] != set.iso3d[i].mu[0] || back.iso3d[i].sigma != set.iso3d[i].sigma ||
+            back.iso3d[i].color[2] != set.iso3d[i].color[2] || back.iso3d[i].opacity != set.iso3d[i].opacity)
+          return fail("round trip values");
+    }
+    std::ofstream(dir + "/cpp_camera.json")
+        << "{\"rotation\": [[1,0,0],[0,1,0],[0,0,1]], \"translation\": [0,0,0], \"focal\": 32,"
+           " \"principal_point\": [16, 16], \"image_size\": [32, 32]}\n";
+    const Camera c = load_camera(dir + "/cpp_camera.json");
+    if (c.focal != 32 || c.width != 32 || c.principal_point[1] != 16) return fail("camera");
+    std::ofstream(dir + "/bad_quat.json")
+        << "{\"quaternion\": [1, 0.1, 0, 0], \"translation\": [0,0,0], \"focal\": 1,"
+           " \"principal_point\": [0, 0], \"image_size\": [4, 4]}\n";
+    try {
+      load_camera(dir + "/bad_quat.json");
+      return fail("bad quaternion accepted");
+    } catch (const std::runtime_error& e) {
+      if (std::strcmp(e.what(), "camera: quaternion norm must be 1 within 1e-9")) return fail(e.what());
+    }
+    // files written by the Python side (tests/test_scene_io.py), if present
+    for (const char* f : {"/py_scene.ispl", "/py_scene.json"}) {
+      std::ifstream probe(dir + f);
+      if (!probe) continue;
+      const ParticleSet py = load_particles(dir + f);
+      if (py.count() != 3 || py.iso3d[2].sigma != 0.9) return fail("python-written scene");
+    }
+    std::printf("OK io\n");
+    return 0;
+  }
+  if (!std::strcmp(mode, "render3d") && argc > 4) {
+    // run_render3d, tools/isosplat_main.cpp:357-398
+    ParticleSet scene;
+    Camera cam;
+    try {
+      scene = load_particles(argv[2]);
+      cam = load_camera(argv[3]);
+      if (scene.dimension != 3) throw std::runtime_error("scene file must hold 3D splats (dimension=3)");
+    } catch (const std::exception& e) {
+      std::cerr << "error: " << e.what() << "\n";
+      return kExitBadInput;
+    }
+    RenderOptions options;
+    ImageGrid img;
+    try {
+      img = render(std::span<const IsoSplat3D>(scene.iso3d), cam, options);
+    } catch (const std::domain_error& e) {
+      std::cerr << "error: " << e.what() << "\n";
+      return kExitBadInput;
+    }
+    write_png(argv[4], img);
+    std::cout << "rendered " << scene.count() << " splats to " << argv[4] << "\n";
     return 0;
   }
   return fail("unknown mode");
