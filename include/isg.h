@@ -130,6 +130,14 @@ isg_status isg_grads_device(isg_ctx* ctx, float** grads_dev);
 isg_status isg_adam_step(isg_ctx* ctx, const float lr[4], float beta1, float beta2, float eps);
 /* Loss of the last Adam step's views (all-reduced over ranks when NCCL is attached; syncs). */
 isg_status isg_last_step_loss(isg_ctx* ctx, double* loss_out);
+/* weight * mse of one view without gradients (forward + loss only; device target; syncs).
+ * Pending per-view gradients are preserved. */
+isg_status isg_eval_loss(isg_ctx* ctx, const isg_camera* cam, const float bg[3], float t_min,
+                         const float* target_hwc3_dev, float weight, double* loss_out);
+/* Save / restore the scene, Adam moments and step count (the reject-and-halve step of the
+ * reference's fit loop, src/optimize.cpp:333-340, needs the pre-step state back). */
+isg_status isg_snapshot(isg_ctx* ctx);
+isg_status isg_restore(isg_ctx* ctx);
 
 /* ---- multi-GPU (one process per GPU, views sharded, NCCL all-reduce before Adam) -------- */
 /* NCCL is resolved at run time (dlopen libnccl.so.2, the copy torch already loaded if any). */

@@ -110,6 +110,11 @@ struct isg_ctx {
   // stats
   int64_t n_keys = 0, n_visible = 0, regrow = 0, launches = 0;
 
+  // snapshot of (scene, Adam moments, step) for reject-and-retry optimisation
+  float4* snap = nullptr;  // ms | co | m (2n) | v (2n)
+  int64_t snap_n = 0, snap_t = 0;
+  bool snap_valid = false;
+
   // NCCL
   void* nccl_comm = nullptr;
   int nranks = 1, rank = 0;
@@ -454,7 +459,7 @@ isg_status check_frame(isg_ctx* ctx, bool* overflow, bool with_loss = false) {
   ISG_CUDA(cudaMemcpyAsync(ctx->h_total, ctx->total, sizeof(unsigned long long) * 2,
                            cudaMemcpyDeviceToHost, ctx->stream));
   if (with_loss)
-    ISG_CUDA(cudaMemcpyAsync(ctx->h_loss, ctx->loss, sizeof(double) * 3, cudaMemcpyDeviceToHost,
+    ISG_CUDA(cudaMemcpyAsync(ctx->h_loss, ctx->loss, sizeof(double) * 4, cudaMemcpyDeviceToHost,
                              ctx->stream));
   ISG_CUDA(cudaStreamSynchronize(ctx->stream));
   ctx->frame_unchecked = false;
@@ -494,7 +499,7 @@ isg_status run_backward(isg_ctx* ctx, const FrameParams& fp, const float* target
   ISG_STAGE(ST_LOSS_REDUCE);
   isg::launch_loss_reduce(ctx->tile_loss, fp.n_tiles,
                           (double)weight / (3.0 * fp.cam.width * (double)fp.cam.height), ctx->loss,
-                          ctx->stream);
+                          ctx->loss + 1, ctx->stream);
   ISG_CHECK_LAUNCH();
   ctx->launches += 2;
   ctx->pending = true;
@@ -555,13 +560,13 @@ isg_status isg_create(int device, int64_t max_gaussians, int32_t max_width, int3
   chk(cudaEventCreateWithFlags(&ctx->ev_copy, cudaEventDisableTiming));
   chk(cudaMalloc(&ctx->sc, sizeof(uint32_t) * 8));
   chk(cudaMalloc(&ctx->total, sizeof(unsigned long long) * 2));
-  chk(cudaMalloc(&ctx->loss, sizeof(double) * 3));
+  chk(cudaMalloc(&ctx->loss, sizeof(double) * 4));
   chk(cudaMallocHost(&ctx->h_sc, sizeof(uint32_t) * 8));
   chk(cudaMallocHost(&ctx->h_total, sizeof(unsigned long long) * 2));
-  chk(cudaMallocHost(&ctx->h_loss, sizeof(double) * 3));
+  chk(cudaMallocHost(&ctx->h_loss, sizeof(double) * 4));
   if (s == ISG_OK) {
     chk(cudaMemset(ctx->total, 0, sizeof(unsigned long long) * 2));
-    chk(cudaMemset(ctx->loss, 0, sizeof(double) * 3));
+    chk(cudaMemset(ctx->loss, 0, sizeof(double) * 4));
   }
   if (s == ISG_OK && max_gaussians > 0) s = ensure_scene(ctx, max_gaussians);
   if (s == ISG_OK && max_width > 0 && max_height > 0) s = ensure_pixels(ctx, max_width, max_height);
@@ -586,7 +591,7 @@ void isg_destroy(isg_ctx* ctx) {
                  ctx->tval[0], ctx->tval[1], ctx->emit_gid, ctx->sort.hist, ctx->sort.lookback,
                  ctx->sort.counters, ctx->scan_scratch, ctx->img, ctx->target, ctx->t_last,
                  ctx->n_proc, ctx->ranges, ctx->tile_cnt, ctx->cursor, ctx->tile_loss, ctx->sc,
-                 ctx->total, ctx->loss};
+                 ctx->total, ctx->loss, ctx->snap};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (ctx->h_sc) cudaFreeHost(ctx->h_sc);
@@ -676,6 +681,7 @@ static isg_status set_scene_impl(isg_ctx* ctx, int64_t n, const float* ms, const
   }
   ctx->n = n;
   ctx->adam_t = 0;
+  ctx->snap_valid = false;
   ctx->pending = false;
   ctx->grad3d_valid = false;
   ctx->have_frame = false;
@@ -890,6 +896,68 @@ isg_status isg_last_step_loss(isg_ctx* ctx, double* loss_out) {
                            ctx->stream));
   ISG_CUDA(cudaStreamSynchronize(ctx->stream));
   *loss_out = ctx->h_loss[2];
+  return ISG_OK;
+}
+
+isg_status isg_eval_loss(isg_ctx* ctx, const isg_camera* cam, const float bg[3], float t_min,
+                         const float* target_dev, float weight, double* loss_out) {
+  if (!ctx || !loss_out) return ISG_E_ARG;
+  if (!target_dev) return fail(ctx, ISG_E_ARG, "eval_loss: null target");
+  if (!(t_min >= 0.0f) || !(t_min < 1.0f)) return fail(ctx, ISG_E_ARG, "eval_loss: t_min must be in [0,1)");
+  cudaSetDevice(ctx->device);
+  isg_status s = validate_camera(ctx, cam);
+  if (s != ISG_OK) return s;
+  const FrameParams fp = make_fp(cam, bg, t_min);
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    if ((s = launch_frame(ctx, fp, nullptr)) != ISG_OK) return s;
+    isg::launch_l2_tiles(fp, ctx->img, target_dev, ctx->tile_loss, ctx->stream);
+    isg::launch_loss_reduce(ctx->tile_loss, fp.n_tiles,
+                            (double)weight / (3.0 * fp.cam.width * (double)fp.cam.height),
+                            nullptr, ctx->loss + 3, ctx->stream);
+    ISG_CHECK_LAUNCH();
+    ctx->launches += 2;
+    bool ov = false;
+    if ((s = check_frame(ctx, &ov, true)) != ISG_OK) return s;
+    if (ov) continue;
+    *loss_out = ctx->h_loss[3];
+    return ISG_OK;
+  }
+  return fail(ctx, ISG_E_OVERFLOW, "eval_loss: key capacity kept overflowing");
+}
+
+isg_status isg_snapshot(isg_ctx* ctx) {
+  if (!ctx) return ISG_E_ARG;
+  cudaSetDevice(ctx->device);
+  if (ctx->snap_n < ctx->n) {
+    ISG_CUDA(realloc_dev(&ctx->snap, 6 * std::max<int64_t>(ctx->n, 1)));
+    ctx->snap_n = ctx->n;
+  }
+  const size_t n = (size_t)ctx->n;
+  if (n) {
+    ISG_CUDA(cudaMemcpyAsync(ctx->snap, ctx->ms, sizeof(float4) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    ISG_CUDA(cudaMemcpyAsync(ctx->snap + n, ctx->co, sizeof(float4) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    ISG_CUDA(cudaMemcpyAsync(ctx->snap + 2 * n, ctx->m, sizeof(float4) * 2 * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    ISG_CUDA(cudaMemcpyAsync(ctx->snap + 4 * n, ctx->v, sizeof(float4) * 2 * n, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  ctx->snap_t = ctx->adam_t;
+  ctx->snap_valid = true;
+  return ISG_OK;
+}
+
+isg_status isg_restore(isg_ctx* ctx) {
+  if (!ctx) return ISG_E_ARG;
+  if (!ctx->snap_valid || ctx->snap_n < ctx->n)
+    return fail(ctx, ISG_E_STATE, "restore: no snapshot of the current scene");
+  cudaSetDevice(ctx->device);
+  const size_t n = (size_t)ctx->n;
+  if (n) {
+    ISG_CUDA(cudaMemcpyAsync(ctx->ms, ctx->snap, sizeof(float4) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    ISG_CUDA(cudaMemcpyAsync(ctx->co, ctx->snap + n, sizeof(float4) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    ISG_CUDA(cudaMemcpyAsync(ctx->m, ctx->snap + 2 * n, sizeof(float4) * 2 * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    ISG_CUDA(cudaMemcpyAsync(ctx->v, ctx->snap + 4 * n, sizeof(float4) * 2 * n, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  ctx->adam_t = ctx->snap_t;
+  ctx->have_frame = false;
   return ISG_OK;
 }
 

@@ -105,9 +105,12 @@ void launch_blend_bwd(const FrameParams& fp, const uint2* ranges, const uint2* s
                       const float* img, const float* target, const float* t_last,
                       const uint32_t* n_proc, float loss_scale, float4* partial,
                       double* tile_loss, cudaStream_t st);
-// loss[0] += scale * sum(tile_loss), loss[1] = scale * sum(tile_loss)
-void launch_loss_reduce(const double* tile_loss, int n_tiles, double scale, double* loss,
-                        cudaStream_t st);
+// s = scale * sum(tile_loss) (fixed order); *accum += s (if accum), *set = s
+void launch_loss_reduce(const double* tile_loss, int n_tiles, double scale, double* accum,
+                        double* set, cudaStream_t st);
+// tile_loss[t] = sum over tile t of |img - target|^2 (evaluation without gradients)
+void launch_l2_tiles(const FrameParams& fp, const float* img, const float* target,
+                     double* tile_loss, cudaStream_t st);
 
 // ---- optimizer (k_adam.cu) ----------------------------------------------------------------
 struct AdamParams {

@@ -250,8 +250,38 @@ __global__ void __launch_bounds__(kBT) k_blend_bwd(
   }
 }
 
+// Loss without gradients (evaluation): per-tile sum of squared differences, same tiling and
+// summation order as the backward's prologue.
+__global__ void __launch_bounds__(kTilePixels) k_l2_tiles(FrameParams fp,
+                                                          const float* __restrict__ img,
+                                                          const float* __restrict__ target,
+                                                          double* __restrict__ tile_loss) {
+  __shared__ float s_red[kTilePixels / 32];
+  const int tile = blockIdx.x;
+  const int tx = tile % fp.tiles_x, ty = tile / fp.tiles_x;
+  const int x = tx * kTile + (threadIdx.x & (kTile - 1)), y = ty * kTile + threadIdx.x / kTile;
+  float d2 = 0.0f;
+  if (x < fp.cam.width && y < fp.cam.height) {
+    const size_t pix = (size_t)y * fp.cam.width + x;
+    for (int c = 0; c < 3; ++c) {
+      const float d = img[3 * pix + c] - target[3 * pix + c];
+      d2 += d * d;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) d2 += __shfl_xor_sync(0xffffffffu, d2, o);
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = d2;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < kTilePixels / 32; ++i) t += (double)s_red[i];
+    tile_loss[tile] = t;
+  }
+}
+
+// scale * sum(tile_loss) in a fixed order: added to *accum (if not null), stored to *set.
 __global__ void k_loss_reduce(const double* __restrict__ tile_loss, int n_tiles, double scale,
-                              double* __restrict__ loss) {
+                              double* __restrict__ accum, double* __restrict__ set) {
   __shared__ double s[256];
   double acc = 0.0;
   for (int i = threadIdx.x; i < n_tiles; i += 256) acc += tile_loss[i];
@@ -262,8 +292,8 @@ __global__ void k_loss_reduce(const double* __restrict__ tile_loss, int n_tiles,
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    loss[0] += s[0] * scale;  // accumulated over views
-    loss[1] = s[0] * scale;   // this view
+    if (accum) *accum += s[0] * scale;
+    *set = s[0] * scale;
   }
 }
 
@@ -276,9 +306,14 @@ void launch_blend_bwd(const FrameParams& fp, const uint2* ranges, const uint2* s
                                           t_last, n_proc, loss_scale, partial, tile_loss);
 }
 
-void launch_loss_reduce(const double* tile_loss, int n_tiles, double scale, double* loss,
-                        cudaStream_t st) {
-  k_loss_reduce<<<1, 256, 0, st>>>(tile_loss, n_tiles, scale, loss);
+void launch_loss_reduce(const double* tile_loss, int n_tiles, double scale, double* accum,
+                        double* set, cudaStream_t st) {
+  k_loss_reduce<<<1, 256, 0, st>>>(tile_loss, n_tiles, scale, accum, set);
+}
+
+void launch_l2_tiles(const FrameParams& fp, const float* img, const float* target,
+                     double* tile_loss, cudaStream_t st) {
+  k_l2_tiles<<<fp.n_tiles, kTilePixels, 0, st>>>(fp, img, target, tile_loss);
 }
 
 }  // namespace isg

@@ -78,6 +78,9 @@ def lib() -> C.CDLL:
         "isg_grads_device": ([P, C.POINTER(P)], C.c_int),
         "isg_adam_step": ([P, fp, F, F, F], C.c_int),
         "isg_last_step_loss": ([P, C.POINTER(C.c_double)], C.c_int),
+        "isg_eval_loss": ([P, C.POINTER(CameraT), fp, F, P, F, C.POINTER(C.c_double)], C.c_int),
+        "isg_snapshot": ([P], C.c_int),
+        "isg_restore": ([P], C.c_int),
         "isg_nccl_get_unique_id": ([P], C.c_int),
         "isg_nccl_init": ([P, C.c_int, C.c_int, P], C.c_int),
         "isg_nccl_detach": ([P], C.c_int),
@@ -105,7 +108,8 @@ C_ABI_SYMBOLS = (
     "isg_set_stream", "isg_synchronize", "isg_get_stats", "isg_set_scene", "isg_set_scene_device",
     "isg_get_scene", "isg_render", "isg_render_device", "isg_loss_backward",
     "isg_loss_backward_device", "isg_read_loss", "isg_zero_grads", "isg_get_grads",
-    "isg_grads_device", "isg_adam_step", "isg_last_step_loss", "isg_nccl_get_unique_id",
+    "isg_grads_device", "isg_adam_step", "isg_last_step_loss", "isg_eval_loss", "isg_snapshot",
+    "isg_restore", "isg_nccl_get_unique_id",
     "isg_nccl_init",
     "isg_nccl_detach", "isg_debug_bins", "isg_debug_pixel_state", "isg_set_binning",
     "isg_profile_enable",
@@ -356,6 +360,22 @@ class Renderer:
 
     def adam_step(self, cfg: AdamConfig = AdamConfig()):
         _check(self._h, lib().isg_adam_step(self._h, cfg.lrs(), cfg.beta1, cfg.beta2, cfg.eps))
+
+    def eval_loss_device(self, camera, target_ptr: int, options: RenderOptions = RenderOptions(),
+                         weight: float = 1.0) -> float:
+        """weight * mse of one view, no gradients (pending gradients are kept)."""
+        c = self._cam(camera)
+        v = C.c_double()
+        _check(self._h, lib().isg_eval_loss(self._h, C.byref(c), self._bg(options),
+                                            float(options.t_min), C.c_void_p(target_ptr),
+                                            float(weight), C.byref(v)))
+        return v.value
+
+    def snapshot(self):
+        _check(self._h, lib().isg_snapshot(self._h))
+
+    def restore(self):
+        _check(self._h, lib().isg_restore(self._h))
 
     def last_step_loss(self) -> float:
         v = C.c_double()

@@ -1,0 +1,220 @@
+"""3D training driver (paper_2403_14244_b200/fit3d.py), fit_impl semantics of the reference
+(/root/reference/proj/src/optimize.cpp:298-358; tests/test_optimize.cpp's properties):
+
+  * loss decreases on a fit toward a target scene; loss_history has one entry per epoch,
+  * with backoff the recorded loss never increases and rejected steps halve rate_scale,
+  * a non-finite loss raises DivergenceError(epoch, particle) with the reference's message,
+  * outputs: particles.ispl (metadata epoch/final_loss), loss.csv, state.json.
+
+CPU tests drive the loop with the CPU oracle; the GPU tests run it on libisg and compare the
+trajectory with the oracle's.
+"""
+import json
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2403_14244_b200 import isg, scene_io
+from paper_2403_14244_b200.fit3d import (DivergenceError, FitConfig3D, RendererBackend, fit,
+                                         offending_particle, save_fit_outputs)
+
+W, H, N, VIEWS = 64, 48, 300, 3
+
+
+class OracleFitBackend:
+    """CPU stand-in for fit3d.RendererBackend (same step semantics as libisg)."""
+
+    def __init__(self, ms, co, cams, targets, cfg: FitConfig3D):
+        self.ms, self.co = ms.copy(), co.copy()
+        self.m = np.zeros((ms.shape[0], 8), np.float32)
+        self.v = np.zeros_like(self.m)
+        self.g = np.zeros_like(self.m)
+        self.cams, self.targets, self.cfg = cams, targets, cfg
+        self.n_views = len(cams)
+        self.loss, self.t, self.skipped, self.snap = 0.0, 0, 0, None
+
+    def count(self):
+        return self.ms.shape[0]
+
+    def params(self):
+        return np.concatenate([self.ms, self.co], 1).astype(np.float64)
+
+    def eval_loss(self, view, weight):
+        loss, _ = O.loss_backward32(self.ms, self.co, self.cams[view], self.targets[view],
+                                    t_min=self.cfg.t_min, weight=weight, threads=1)
+        return loss
+
+    def loss_backward(self, view, weight):
+        loss, _ = O.loss_backward32(self.ms, self.co, self.cams[view], self.targets[view],
+                                    t_min=self.cfg.t_min, weight=weight, grads=self.g, threads=1)
+        self.loss += loss
+
+    def step(self, rate_scale):
+        a = self.cfg.adam
+        lr = [a.lr_mu * rate_scale, a.lr_sigma * rate_scale, a.lr_color * rate_scale,
+              a.lr_opacity * rate_scale]
+        self.t += 1
+        self.skipped += O.adam32(self.ms, self.co, self.m, self.v, self.g, self.t, lr,
+                                 a.beta1, a.beta2, a.eps)
+        self.g[:] = 0
+        loss, self.loss = self.loss, 0.0
+        return loss
+
+    def snapshot(self):
+        self.snap = (self.ms.copy(), self.co.copy(), self.m.copy(), self.v.copy(), self.t)
+
+    def restore(self):
+        ms, co, m, v, self.t = self.snap
+        self.ms[:], self.co[:], self.m[:], self.v[:] = ms, co, m, v
+
+    def skipped_updates(self):
+        return self.skipped
+
+
+def problem(n=N, views=VIEWS):
+    ms, co = isg.synth_scene(n, W, H, seed=2403)
+    tms, tco = isg.synth_scene(n, W, H, seed=14244)
+    cams = [isg.Camera.synthetic(W, H, k, views) for k in range(views)]
+    targets = [O.render32(tms, tco, c) for c in cams]
+    return ms, co, cams, targets
+
+
+def test_fit_decreases_loss_and_history():
+    ms, co, cams, targets = problem()
+    cfg = FitConfig3D(epochs=6)
+    st = fit(OracleFitBackend(ms, co, cams, targets, cfg), cfg)
+    assert st.epoch == 6 and len(st.loss_history) == 6
+    assert st.particle_count_history == [N] * 6
+    assert st.final_loss == st.loss_history[-1]
+    assert st.loss_history[-1] < st.initial_loss
+    assert st.rate_scale == 1.0
+
+
+def test_backoff_never_increases_and_halves():
+    ms, co, cams, targets = problem()
+    # a learning rate large enough that some steps overshoot
+    cfg = FitConfig3D(epochs=8, backoff=True,
+                      adam=isg.AdamConfig(lr_mu=0.5, lr_sigma=1.0, lr_color=1.0, lr_opacity=2.0))
+    st = fit(OracleFitBackend(ms, co, cams, targets, cfg), cfg)
+    hist = [st.initial_loss] + st.loss_history
+    assert all(b <= a for a, b in zip(hist, hist[1:]))
+    assert st.rate_scale < 1.0  # at least one rejected step
+    n_rejected = round(-np.log2(st.rate_scale))
+    assert sum(b == a for a, b in zip(hist, hist[1:])) >= n_rejected
+
+
+def test_divergence_error_non_finite_target():
+    ms, co, cams, targets = problem(views=1)
+    bad = targets[0].copy()
+    bad[3, 5, 1] = np.nan
+    cfg = FitConfig3D(epochs=2)
+    with pytest.raises(DivergenceError) as ei:
+        fit(OracleFitBackend(ms, co, cams, [bad], cfg), cfg)
+    assert ei.value.epoch == 0
+    assert str(ei.value) == f"fit diverged at epoch 0 (particle {ei.value.particle_index})"
+
+
+def test_offending_particle_and_config_validation():
+    p = np.tile(np.array([0, 0, 1, 0.1, 0.5, 0.5, 0.5, 0.5]), (4, 1))
+    assert offending_particle(p) == -1
+    p[2, 3] = -1.0
+    p[3, 0] = np.inf
+    assert offending_particle(p) == 2
+    with pytest.raises(ValueError, match="epochs"):
+        FitConfig3D(epochs=-1).validate()
+    with pytest.raises(ValueError, match="lr_mu"):
+        FitConfig3D(adam=isg.AdamConfig(lr_mu=0.0)).validate()
+
+
+def test_outputs(tmp_path):
+    ms, co, cams, targets = problem(views=1)
+    cfg = FitConfig3D(epochs=3)
+    be = OracleFitBackend(ms, co, cams, targets, cfg)
+    st = fit(be, cfg)
+    save_fit_outputs(tmp_path, st, cfg, be.params())
+    ps = scene_io.load_particles(tmp_path / "particles.ispl")
+    assert ps.count() == N
+    assert ps.metadata["epoch"] == 3
+    assert ps.metadata["final_loss"] == pytest.approx(st.final_loss)
+    lines = (tmp_path / "loss.csv").read_text().splitlines()
+    assert lines[0] == "epoch,loss,particles" and len(lines) == 1 + 1 + 3
+    sidecar = json.loads((tmp_path / "state.json").read_text())
+    for k in ("epoch", "initial_loss", "final_loss", "rate_scale", "skipped_updates", "particles",
+              "config", "loss_history", "particle_count_history"):
+        assert k in sidecar
+    assert sidecar["loss_history"] == st.loss_history
+
+
+# ---- GPU ------------------------------------------------------------------------------------
+def _gpu_backend(ms, co, cams, targets, cfg):
+    import torch
+    r = isg.Renderer(max_gaussians=ms.shape[0], max_width=W, max_height=H)
+    r.set_scene(ms, co)
+    dev = [torch.from_numpy(t).cuda() for t in targets]
+    torch.cuda.synchronize()
+    be = RendererBackend(r, cams, [t.data_ptr() for t in dev], cfg)
+    be._keep = dev
+    return be
+
+
+@pytest.mark.gpu
+def test_gpu_fit_matches_oracle_trajectory():
+    ms, co, cams, targets = problem()
+    cfg = FitConfig3D(epochs=5)
+    st_o = fit(OracleFitBackend(ms, co, cams, targets, cfg), cfg)
+    st_g = fit(_gpu_backend(ms, co, cams, targets, cfg), cfg)
+    assert st_g.initial_loss == pytest.approx(st_o.initial_loss, rel=1e-5)
+    np.testing.assert_allclose(st_g.loss_history, st_o.loss_history, rtol=1e-3)
+    assert st_g.final_loss < st_g.initial_loss
+
+
+@pytest.mark.gpu
+def test_gpu_backoff_matches_oracle():
+    ms, co, cams, targets = problem()
+    cfg = FitConfig3D(epochs=8, backoff=True,
+                      adam=isg.AdamConfig(lr_mu=0.5, lr_sigma=1.0, lr_color=1.0, lr_opacity=2.0))
+    st_o = fit(OracleFitBackend(ms, co, cams, targets, cfg), cfg)
+    st_g = fit(_gpu_backend(ms, co, cams, targets, cfg), cfg)
+    hist = [st_g.initial_loss] + st_g.loss_history
+    assert all(b <= a for a, b in zip(hist, hist[1:]))
+    assert st_g.rate_scale == st_o.rate_scale
+    np.testing.assert_allclose(st_g.loss_history, st_o.loss_history, rtol=1e-3)
+
+
+@pytest.mark.gpu
+def test_gpu_eval_loss_keeps_pending_grads_and_restore():
+    ms, co, cams, targets = problem(views=2)
+    cfg = FitConfig3D()
+    be = _gpu_backend(ms, co, cams, targets, cfg)
+    be.loss_backward(0, 0.5)
+    g0 = be.r.grads().copy()
+    l1 = be.eval_loss(1, 0.5)
+    lo, _ = O.loss_backward32(ms, co, cams[1], targets[1], weight=0.5)
+    assert l1 == pytest.approx(lo, rel=1e-5)
+    np.testing.assert_array_equal(be.r.grads(), g0)
+    be.snapshot()
+    p0 = be.params()
+    be.step(1.0)
+    assert not np.array_equal(be.params(), p0)
+    be.restore()
+    np.testing.assert_array_equal(be.params(), p0)
+    # the restored Adam state reproduces the same step
+    be.loss_backward(0, 0.5)
+    be.step(1.0)
+    p1 = be.params()
+    be.restore()
+    be.loss_backward(0, 0.5)
+    be.step(1.0)
+    np.testing.assert_array_equal(be.params(), p1)
+
+
+@pytest.mark.gpu
+def test_gpu_divergence_on_nan_target():
+    ms, co, cams, targets = problem(views=1)
+    bad = targets[0].copy()
+    bad[3, 5, 1] = np.nan
+    cfg = FitConfig3D(epochs=2)
+    with pytest.raises(DivergenceError) as ei:
+        fit(_gpu_backend(ms, co, cams, [bad], cfg), cfg)
+    assert ei.value.epoch == 0
