@@ -8,6 +8,7 @@ step on every replica (gradients all-reduced over NCCL when N > 1): weak scaling
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3|c2|c4|c5]
   python bench.py --impl reference ...   # CPU reference arm (oracle port, all host cores)
+  python bench.py --loss l1_dssim        # train with the paper's 0.8 L1 + 0.2 D-SSIM loss
 
 `value` is device-resident throughput (inputs in HBM before the timed region); `e2e` is the
 same metric through the C-ABI with host buffers (target H2D + loss D2H inside the timed
@@ -196,6 +197,8 @@ def run_isg(args):
     tms, tco = isg.synth_scene(n, W, H, seed=14244)
     r = isg.Renderer(local, n, W, H)
     r.set_stream(stream.cuda_stream)
+    if args.loss == "l1_dssim":
+        r.set_loss(isg.LOSS_L1_DSSIM, 0.2)
     opts = isg.RenderOptions(t_min=T_MIN)
     cfg = isg.AdamConfig()
     my_views = [rank * views_per_rank + i for i in range(views_per_rank)]
@@ -361,6 +364,7 @@ def run_isg(args):
         "data": "synthetic (isg-synth v1: scene seed 2403, target seed 14244)",
         "config": {"workload": desc, "config": args.config, "n_gaussians": n, "width": W,
                    "height": H, "views_per_step": step_views, "t_min": T_MIN,
+                   "loss": "L2 (mse)" if args.loss == "l2" else "0.8 L1 + 0.2 D-SSIM",
                    "parallelism": f"dp{world} (views sharded, scene replicated)",
                    "l2": "no flush: per-step working set (scene+Adam state 96 MB, keys "
                          f"{st['n_keys'] * 16 / 1e6:.0f} MB, images 50 MB) exceeds the 126 MB L2"},
@@ -390,6 +394,8 @@ def main():
     ap.add_argument("--impl", default="isg", choices=["isg", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--loss", default="l2", choices=["l2", "l1_dssim"],
+                    help="training loss (BASELINE configs use L2; l1_dssim = the paper's loss)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

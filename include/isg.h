@@ -139,6 +139,23 @@ isg_status isg_eval_loss(isg_ctx* ctx, const isg_camera* cam, const float bg[3],
 isg_status isg_snapshot(isg_ctx* ctx);
 isg_status isg_restore(isg_ctx* ctx);
 
+/* ---- image loss (the loss the training entry points use) --------------------------------
+ * ISG_LOSS_L2 (default): weight * mse                          (image.cpp:50-58)
+ * ISG_LOSS_L1_DSSIM:     weight * ((1-lambda) L1 + lambda (1 - SSIM)), 11-tap sigma-1.5
+ *                        window on valid positions, and its pixel gradient
+ *                        (loss <- loss.cpp:184-190, ssim :119-141, dL/dfhat :201-213,
+ *                        ssim_gradient_wrt_second :143-182).  lambda outside [0,1] ->
+ *                        ISG_E_DOMAIN "loss: lambda must be in [0,1]"; lambda > 0 needs
+ *                        W, H >= 11 (ISG_E_DOMAIN "ssim: image smaller than the 11x11 window"). */
+#define ISG_LOSS_L2 0
+#define ISG_LOSS_L1_DSSIM 1
+isg_status isg_set_loss(isg_ctx* ctx, int kind, float lambda);
+/* The configured loss of a device image fhat against target (both HWC3), and optionally its
+ * gradient dL/dfhat into dldc_dev (HWC3; NULL = loss only).  Syncs. */
+isg_status isg_image_loss_device(isg_ctx* ctx, int32_t width, int32_t height,
+                                 const float* fhat_dev, const float* target_dev, float weight,
+                                 double* loss_out, float* dldc_dev);
+
 /* ---- multi-GPU (one process per GPU, views sharded, NCCL all-reduce before Adam) -------- */
 /* NCCL is resolved at run time (dlopen libnccl.so.2, the copy torch already loaded if any). */
 isg_status isg_nccl_get_unique_id(void* out_128_bytes);

@@ -61,6 +61,11 @@ def lib():
         L.or32_adam.argtypes = [I64, P, P, P, P, P, I64, P, C.c_float, C.c_float, C.c_float,
                                 C.POINTER(I64)]
         L.or32_adam.restype = None
+        L.or32_backward_dldc.argtypes = [I64, P, P, C.POINTER(Cam32), P, C.c_float, P, C.c_int, P]
+        L.or32_backward_dldc.restype = C.c_int
+        L.or64_image_loss.argtypes = [C.c_int, C.c_int, P, P, C.c_double, C.c_double,
+                                      C.POINTER(C.c_double), P]
+        L.or64_image_loss.restype = C.c_int
         _lib = L
     return _lib
 
@@ -205,6 +210,35 @@ def adam32(ms, co, m, v, grads, step, lr, b1=0.9, b2=0.999, eps=1e-15):
     return skipped.value
 
 
+def backward_dldc32(ms, co, camera, dldc, bg=(0, 0, 0), t_min=1e-5, threads=0, grads=None):
+    """FP32 tiled backward for a given pixel gradient dL/dC (HWC3); accumulates into grads."""
+    ms = np.ascontiguousarray(ms, np.float32)
+    co = np.ascontiguousarray(co, np.float32)
+    g = np.ascontiguousarray(dldc, np.float32)
+    b = np.asarray(bg, np.float32)
+    if grads is None:
+        grads = np.zeros((ms.shape[0], 8), np.float32)
+    lib().or32_backward_dldc(ms.shape[0], _p(ms), _p(co), C.byref(cam32(camera)), _p(b), t_min,
+                             _p(g), threads, _p(grads))
+    return grads
+
+
+def image_loss64(target, fhat, lam=0.2, weight=1.0, grad=False):
+    """weight * loss(target, fhat, lam) (loss.cpp:184-190) and optionally weight * dL/dfhat."""
+    f = np.ascontiguousarray(target, np.float64)
+    fh = np.ascontiguousarray(fhat, np.float64)
+    H, W = f.shape[:2]
+    g = np.zeros_like(f) if grad else None
+    v = C.c_double()
+    st = lib().or64_image_loss(W, H, _p(f), _p(fh), lam, weight, C.byref(v),
+                               _p(g) if grad else None)
+    if st == -1:
+        raise ValueError("loss: lambda must be in [0,1]")
+    if st == -2:
+        raise ValueError("ssim: image smaller than the 11x11 window")
+    return (v.value, g) if grad else v.value
+
+
 # ---- the reference's own code (oracle/_ref, built by oracle/build_ref.sh) -----------------
 _ref = None
 
@@ -224,6 +258,9 @@ def ref_lib():
         L.ref_composite.restype = C.c_int
         L.ref_mse.argtypes = [C.c_int, C.c_int, P, P]
         L.ref_mse.restype = C.c_double
+        L.ref_image_loss.argtypes = [C.c_int, C.c_int, P, P, C.c_double, P, P, C.c_char_p,
+                                     C.c_int]
+        L.ref_image_loss.restype = C.c_int
         _ref = L
     return _ref
 
@@ -266,3 +303,18 @@ def ref_composite(rgba):
     if ref_lib().ref_composite(a.shape[0], _p(a), _p(out), err, 512):
         raise ValueError(err.value.decode())
     return out
+
+
+def ref_image_loss(target, fhat, lam=0.2, grad=False):
+    """The reference's loss(), l1_term(), ssim() and ssim_gradient_wrt_second()
+    (loss.cpp:112-190) -> (loss, l1, ssim[, dssim/dfhat])."""
+    f = np.ascontiguousarray(target, np.float64)
+    fh = np.ascontiguousarray(fhat, np.float64)
+    H, W = f.shape[:2]
+    out = np.full(3, np.nan)
+    g = np.zeros_like(f) if grad else None
+    err = C.create_string_buffer(512)
+    if ref_lib().ref_image_loss(W, H, _p(f), _p(fh), lam, _p(out), _p(g) if grad else None,
+                                err, 512):
+        raise ValueError(err.value.decode())
+    return (out[0], out[1], out[2], g) if grad else (out[0], out[1], out[2])

@@ -22,6 +22,10 @@
  *      include/isosplat/kernels.hpp:208-222, Jacobian src/splat3d.cpp:39-47) that is pinned
  *      by central finite differences of the FP64 forward in tests/.
  *
+ *  (3) or64_image_loss — FP64 restatement of the paper's L1 + D-SSIM loss and its pixel
+ *      gradient (src/loss.cpp:16-213), pinned against the reference's own compiled loss(),
+ *      ssim() and ssim_gradient_wrt_second() (oracle/_ref) in tests/.
+ *
  *  (2) or32_*  — the FP32 TILED restatement that the GPU path must match: the same
  *      arithmetic in IEEE single precision with every rounding spelled out (this file is
  *      compiled with -ffp-contract=off, as the reference is: proj/CMakeLists.txt:11-17),
@@ -611,9 +615,10 @@ int or32_render(int64_t n, const float* mu_sigma, const float* rgb_o, const or_c
  * drgb dopacity) are ACCUMULATED into grads.  Per-(tile, entry) partial sums are reduced per
  * splat in key order, so the result is independent of the thread count.  out_img (may be
  * NULL) receives the forward image. */
-int or32_loss_backward(int64_t n, const float* mu_sigma, const float* rgb_o, const or_cam32* cam,
-                       const float* bg, float t_min, const float* target, float weight,
-                       int threads, double* loss_out, float* grads, float* out_img) {
+static int or32_backward_impl(int64_t n, const float* mu_sigma, const float* rgb_o,
+                              const or_cam32* cam, const float* bg, float t_min,
+                              const float* target, const float* dldc, float weight, int threads,
+                              double* loss_out, float* grads, float* out_img) {
   or_frame32 f;
   or32_frame_build(n, mu_sigma, rgb_o, cam, &f);
   float* part = (float*)calloc((size_t)(f.nkeys > 0 ? f.nkeys : 1) * 7, sizeof(float));
@@ -633,9 +638,13 @@ int or32_loss_backward(int64_t n, const float* mu_sigma, const float* rgb_o, con
         if (out_img) memcpy(out_img + 3 * pix, C, sizeof C);
         float G[3];
         for (int c = 0; c < 3; ++c) {
-          const float d = C[c] - target[3 * pix + c];
-          tl_acc += (double)d * (double)d;
-          G[c] = 2.0f * d * scale;
+          if (dldc) {
+            G[c] = dldc[3 * pix + c];
+          } else {
+            const float d = C[c] - target[3 * pix + c];
+            tl_acc += (double)d * (double)d;
+            G[c] = 2.0f * d * scale;
+          }
         }
         float A0 = bg[0], A1 = bg[1], A2 = bg[2], Tc = Tl;
         int first = 1;
@@ -702,11 +711,147 @@ int or32_loss_backward(int64_t n, const float* mu_sigma, const float* rgb_o, con
   }
   double loss = 0.0;
   for (int t = 0; t < f.ntiles; ++t) loss += tile_loss[t];
-  *loss_out = loss * ((double)weight / (3.0 * f.W * f.H));
+  if (loss_out) *loss_out = loss * ((double)weight / (3.0 * f.W * f.H));
   free(d2);
   free(part);
   free(tile_loss);
   or32_frame_free(&f);
+  return 0;
+}
+
+int or32_loss_backward(int64_t n, const float* mu_sigma, const float* rgb_o, const or_cam32* cam,
+                       const float* bg, float t_min, const float* target, float weight,
+                       int threads, double* loss_out, float* grads, float* out_img) {
+  return or32_backward_impl(n, mu_sigma, rgb_o, cam, bg, t_min, target, NULL, weight, threads,
+                            loss_out, grads, out_img);
+}
+
+/* The same backward with a given pixel gradient dL/dC (HWC3, weight included), e.g. of the
+ * L1 + D-SSIM loss below.  Gradients are ACCUMULATED into grads. */
+int or32_backward_dldc(int64_t n, const float* mu_sigma, const float* rgb_o, const or_cam32* cam,
+                       const float* bg, float t_min, const float* dldc, int threads,
+                       float* grads) {
+  return or32_backward_impl(n, mu_sigma, rgb_o, cam, bg, t_min, NULL, dldc, 1.0f, threads, NULL,
+                            grads, NULL);
+}
+
+/* ============================================================================================
+ * (3) L1 + D-SSIM image loss, FP64 — a literal restatement of /root/reference/proj/src/loss.cpp
+ * ============================================================================================ */
+#define OR_WIN 11
+#define OR_HALF 5
+
+static void or_ssim_taps(double t[OR_WIN]) { /* window_taps, loss.cpp:22-35 */
+  double sum = 0.0;
+  for (int i = 0; i < OR_WIN; ++i) {
+    const double d = i - OR_HALF;
+    t[i] = exp(-d * d / (2.0 * 1.5 * 1.5));
+    sum += t[i];
+  }
+  for (int i = 0; i < OR_WIN; ++i) t[i] /= sum;
+}
+
+/* filter, loss.cpp:49-72: separable correlation, zero padded (clipped tap range) */
+static void or_filter(const double* w, const double* in, int W, int H, double* tmp, double* out) {
+  for (int y = 0; y < H; ++y)
+    for (int x = 0; x < W; ++x) {
+      double acc = 0.0;
+      const int d0 = x - OR_HALF < 0 ? -x : -OR_HALF;
+      const int d1 = W - 1 - x < OR_HALF ? W - 1 - x : OR_HALF;
+      for (int d = d0; d <= d1; ++d) acc += w[d + OR_HALF] * in[(size_t)y * W + x + d];
+      tmp[(size_t)y * W + x] = acc;
+    }
+  memset(out, 0, sizeof(double) * (size_t)W * H);
+  for (int y = 0; y < H; ++y) {
+    const int d0 = y - OR_HALF < 0 ? -y : -OR_HALF;
+    const int d1 = H - 1 - y < OR_HALF ? H - 1 - y : OR_HALF;
+    for (int d = d0; d <= d1; ++d) {
+      const double wd = w[d + OR_HALF];
+      for (int x = 0; x < W; ++x) out[(size_t)y * W + x] += wd * tmp[(size_t)(y + d) * W + x];
+    }
+  }
+}
+
+/* loss(f, fhat, lambda) (loss.cpp:184-190) of HWC3 images f (target) and fhat, times weight,
+ * and optionally dL/dfhat (loss_pixel_gradient :201-213 with ssim_gradient_wrt_second
+ * :143-182), times weight.  Returns 0, -1 for lambda outside [0,1], -2 for an image smaller
+ * than the window when lambda > 0. */
+int or64_image_loss(int W, int H, const double* f, const double* fhat, double lambda,
+                    double weight, double* loss_out, double* dldfhat) {
+  if (!(lambda >= 0.0 && lambda <= 1.0)) return -1;
+  const size_t P = (size_t)W * H, N = 3 * P;
+  double l1 = 0.0;
+  for (size_t i = 0; i < N; ++i) l1 += fabs(f[i] - fhat[i]);
+  l1 /= (double)N;
+  if (dldfhat) {
+    const double w1 = (1.0 - lambda) / (double)N;
+    for (size_t i = 0; i < N; ++i) {
+      const double r = fhat[i] - f[i];
+      dldfhat[i] = r > 0.0 ? w1 : (r < 0.0 ? -w1 : 0.0);
+    }
+  }
+  if (lambda == 0.0) {
+    *loss_out = weight * l1;
+    if (dldfhat)
+      for (size_t i = 0; i < N; ++i) dldfhat[i] *= weight;
+    return 0;
+  }
+  if (W < OR_WIN || H < OR_WIN) return -2;
+  double w[OR_WIN];
+  or_ssim_taps(w);
+  const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;
+  double* buf = (double*)malloc(sizeof(double) * P * 16);
+  double *a = buf, *b = buf + P, *m1 = buf + 2 * P, *m2 = buf + 3 * P, *t1 = buf + 4 * P,
+         *t2 = buf + 5 * P, *t12 = buf + 6 * P, *tmp = buf + 7 * P, *prod = buf + 8 * P,
+         *gm2 = buf + 9 * P, *gt2 = buf + 10 * P, *gt12 = buf + 11 * P, *f1 = buf + 12 * P,
+         *f2 = buf + 13 * P, *f3 = buf + 14 * P;
+  const double norm = 1.0 / ((double)(W - 2 * OR_HALF) * (H - 2 * OR_HALF) * 3);
+  double total = 0.0;
+  for (int c = 0; c < 3; ++c) {
+    for (size_t i = 0; i < P; ++i) {
+      a[i] = f[3 * i + c];
+      b[i] = fhat[3 * i + c];
+    }
+    /* ssim_terms, loss.cpp:86-102 */
+    or_filter(w, a, W, H, tmp, m1);
+    or_filter(w, b, W, H, tmp, m2);
+    for (size_t i = 0; i < P; ++i) prod[i] = a[i] * a[i];
+    or_filter(w, prod, W, H, tmp, t1);
+    for (size_t i = 0; i < P; ++i) prod[i] = b[i] * b[i];
+    or_filter(w, prod, W, H, tmp, t2);
+    for (size_t i = 0; i < P; ++i) prod[i] = a[i] * b[i];
+    or_filter(w, prod, W, H, tmp, t12);
+    double acc = 0.0;
+    memset(gm2, 0, sizeof(double) * P * 3);
+    for (int y = OR_HALF; y < H - OR_HALF; ++y)
+      for (int x = OR_HALF; x < W - OR_HALF; ++x) {
+        const size_t i = (size_t)y * W + x;
+        const double s11 = t1[i] - m1[i] * m1[i], s22 = t2[i] - m2[i] * m2[i],
+                     s12 = t12[i] - m1[i] * m2[i];
+        const double nl = 2.0 * m1[i] * m2[i] + C1, dl = m1[i] * m1[i] + m2[i] * m2[i] + C1;
+        const double nc = 2.0 * s12 + C2, dc = s11 + s22 + C2;
+        acc += (nl * nc) / (dl * dc); /* ssim, :128-137 */
+        const double lum = nl / dl, cs = nc / dc; /* :159-170 */
+        const double d_s22 = -lum * nc / (dc * dc), d_s12 = lum * 2.0 / dc;
+        const double d_lum_m2 = (2.0 * m1[i] * dl - nl * 2.0 * m2[i]) / (dl * dl);
+        gm2[i] = cs * d_lum_m2 + d_s22 * (-2.0 * m2[i]) + d_s12 * (-m1[i]);
+        gt2[i] = d_s22;
+        gt12[i] = d_s12;
+      }
+    total += acc / ((double)(W - 2 * OR_HALF) * (H - 2 * OR_HALF));
+    if (dldfhat) {
+      or_filter(w, gm2, W, H, tmp, f1);
+      or_filter(w, gt2, W, H, tmp, f2);
+      or_filter(w, gt12, W, H, tmp, f3);
+      for (size_t i = 0; i < P; ++i) /* :174-179, then loss_pixel_gradient :210 */
+        dldfhat[3 * i + c] -= lambda * (norm * (f1[i] + 2.0 * b[i] * f2[i] + a[i] * f3[i]));
+    }
+  }
+  free(buf);
+  const double ssim = total / 3.0;
+  *loss_out = weight * ((1.0 - lambda) * l1 + lambda * (1.0 - ssim));
+  if (dldfhat)
+    for (size_t i = 0; i < N; ++i) dldfhat[i] *= weight;
   return 0;
 }
 

@@ -1,5 +1,5 @@
 // ref_capi.cpp — extern "C" wrappers around the REFERENCE's own hot-path code, compiled from
-// /root/reference/proj/src/{splat3d,image}.cpp by oracle/build_ref.sh into
+// /root/reference/proj/src/{splat3d,image,loss,reconstruct}.cpp by oracle/build_ref.sh into
 // oracle/_ref/libisosplat_ref.so.  TEST INFRASTRUCTURE ONLY (checker / CPU baseline).
 //
 // The calls go through the reference's public API unchanged:
@@ -8,6 +8,8 @@
 //   isosplat::project_iso   splat3d.hpp:74, splat3d.cpp:59-64
 //   isosplat::composite     splat3d.hpp:85, splat3d.cpp:76-87
 //   isosplat::mse           image.hpp:40, image.cpp:50-58
+//   isosplat::loss / ssim / l1_term / ssim_gradient_wrt_second
+//                           loss.hpp:12-24, loss.cpp:112-190
 // Exceptions (std::domain_error) become a non-zero return plus the message.
 #include <cstdint>
 #include <cstring>
@@ -18,6 +20,7 @@
 #include <vector>
 
 #include "isosplat/image.hpp"
+#include "isosplat/loss.hpp"
 #include "isosplat/splat3d.hpp"
 
 namespace {
@@ -112,6 +115,35 @@ double ref_mse(int w, int h, const double* a, const double* b) {
   std::memcpy(x.data.data(), a, sizeof(double) * x.data.size());
   std::memcpy(y.data.data(), b, sizeof(double) * y.data.size());
   return isosplat::mse(x, y);
+}
+
+namespace {
+isosplat::ImageGrid grid_of(int w, int h, const double* d) {
+  isosplat::ImageGrid g(w, h, 3);
+  std::memcpy(g.data.data(), d, sizeof(double) * g.data.size());
+  return g;
+}
+}  // namespace
+
+// out[0] = loss(f, fhat, lambda), out[1] = l1_term, out[2] = ssim (when lambda != 0 and the
+// window fits).  grad (may be null): d ssim / d fhat (ssim_gradient_wrt_second).
+int ref_image_loss(int w, int h, const double* f, const double* fhat, double lambda, double* out,
+                   double* grad, char* err, int errlen) {
+  try {
+    const auto a = grid_of(w, h, f), b = grid_of(w, h, fhat);
+    out[0] = isosplat::loss(a, b, lambda);
+    out[1] = isosplat::l1_term(a, b);
+    if (lambda != 0.0) {
+      out[2] = isosplat::ssim(a, b);
+      if (grad) {
+        const auto g = isosplat::ssim_gradient_wrt_second(a, b);
+        std::memcpy(grad, g.data.data(), sizeof(double) * g.data.size());
+      }
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return report(e, err, errlen);
+  }
 }
 
 }  // extern "C"

@@ -24,7 +24,7 @@ REF_LIB = ORACLE_DIR / "_ref" / "libisosplat_ref.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["capi.cu", "k_preprocess.cu", "k_bin.cu", "k_sort.cu", "k_blend.cu",
-              "k_blend_bwd.cu", "k_adam.cu", "synth.cu"]
+              "k_blend_bwd.cu", "k_ssim.cu", "k_adam.cu", "synth.cu"]
 
 
 def _digest(paths) -> str:

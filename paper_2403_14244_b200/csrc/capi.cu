@@ -26,13 +26,12 @@
 enum Stage {
   ST_MEMSET, ST_PREPROCESS, ST_DEPTH_SORT, ST_SCAN_EMIT, ST_TILE_SCAN, ST_FILL, ST_TILE_SORT,
   ST_RANGES, ST_BLEND_FWD, ST_BLEND_BWD, ST_LOSS_REDUCE, ST_PROJECT_BWD, ST_PROJECT_ADAM, ST_ADAM,
-  ST_ALLREDUCE, ST_COUNT
+  ST_ALLREDUCE, ST_IMAGE_LOSS, ST_COUNT
 };
 static const char* kStageNames[ST_COUNT] = {
     "memset", "preprocess", "depth_sort", "scan_emit", "tile_scan", "fill", "tile_sort",
     "ranges", "blend_fwd", "blend_bwd", "loss_reduce", "project_bwd", "project_adam", "adam",
-    "allreduce"};
-
+    "allreduce", "image_loss"};
 
 
 struct isg_ctx {
@@ -89,6 +88,14 @@ struct isg_ctx {
   uint32_t* tile_cnt = nullptr;
   uint32_t* cursor = nullptr;
   double* tile_loss = nullptr;
+
+  // image loss: ISG_LOSS_L2 (fused into K7) or ISG_LOSS_L1_DSSIM (k_ssim.cu -> dL/dC -> K7)
+  int loss_kind = ISG_LOSS_L2;
+  float lambda = 0.2f;
+  int64_t ssim_pix_alloc = 0, ssim_part_alloc = 0;
+  float* coef = nullptr;       // 9 W H gradient-coefficient planes
+  float* dldc = nullptr;       // dL/dC, HWC3
+  double2* ssim_part = nullptr;
 
   // device scalars: [0] n_keys [1] first_bad [2] n_visible [3] scan tile counter [4] n
   uint32_t* sc = nullptr;
@@ -486,22 +493,65 @@ isg_status check_frame(isg_ctx* ctx, bool* overflow, bool with_loss = false) {
   return ISG_OK;
 }
 
+// Buffers of the L1 + D-SSIM loss for a W x H image.
+isg_status ensure_image_loss(isg_ctx* ctx, int W, int H) {
+  const int64_t pix = (int64_t)W * H;
+  if (pix > ctx->ssim_pix_alloc) {
+    ISG_CUDA(realloc_dev(&ctx->coef, 9 * pix));
+    ISG_CUDA(realloc_dev(&ctx->dldc, 3 * pix));
+    ctx->ssim_pix_alloc = pix;
+  }
+  const int64_t parts = isg::ssim_part_count(W, H);
+  if (parts > ctx->ssim_part_alloc) {
+    ISG_CUDA(realloc_dev(&ctx->ssim_part, parts));
+    ctx->ssim_part_alloc = parts;
+  }
+  return ISG_OK;
+}
+
+// ssim (loss.cpp:104-108) needs the 11x11 window to fit.
+isg_status check_loss_size(isg_ctx* ctx, int W, int H) {
+  if (ctx->loss_kind == ISG_LOSS_L1_DSSIM && ctx->lambda != 0.0f &&
+      (W < 2 * isg::kSsimHalf + 1 || H < 2 * isg::kSsimHalf + 1))
+    return fail(ctx, ISG_E_DOMAIN, "ssim: image smaller than the 11x11 window");
+  return ISG_OK;
+}
+
 isg_status run_backward(isg_ctx* ctx, const FrameParams& fp, const float* target_dev,
                         float weight) {
-  const float scale = weight / (3.0f * (float)fp.cam.width * (float)fp.cam.height);
-  {
-  ISG_STAGE(ST_BLEND_BWD);
-  isg::launch_blend_bwd(fp, ctx->ranges, ctx->sorted, ctx->rec, ctx->total, ctx->key_cap,
-                        ctx->img, target_dev, ctx->t_last, ctx->n_proc, scale, ctx->partial,
-                        ctx->tile_loss, ctx->stream);
-  ISG_CHECK_LAUNCH();
+  const int W = fp.cam.width, H = fp.cam.height;
+  if (ctx->loss_kind == ISG_LOSS_L1_DSSIM) {
+    isg_status s = ensure_image_loss(ctx, W, H);
+    if (s != ISG_OK) return s;
+    {
+    ISG_STAGE(ST_IMAGE_LOSS);
+    ctx->launches += isg::launch_image_loss(W, H, ctx->img, target_dev, ctx->lambda,
+                                            (double)weight, true, ctx->coef, ctx->ssim_part,
+                                            ctx->dldc, ctx->total, ctx->key_cap, ctx->loss,
+                                            ctx->loss + 1, ctx->stream);
+    ISG_CHECK_LAUNCH();
+    }
+    ISG_STAGE(ST_BLEND_BWD);
+    isg::launch_blend_bwd(fp, ctx->ranges, ctx->sorted, ctx->rec, ctx->total, ctx->key_cap,
+                          ctx->img, ctx->dldc, ctx->t_last, ctx->n_proc, 1.0f, ctx->partial,
+                          ctx->tile_loss, true, ctx->stream);
+    ISG_CHECK_LAUNCH();
+    ctx->launches += 1;
+  } else {
+    const float scale = weight / (3.0f * (float)W * (float)H);
+    {
+    ISG_STAGE(ST_BLEND_BWD);
+    isg::launch_blend_bwd(fp, ctx->ranges, ctx->sorted, ctx->rec, ctx->total, ctx->key_cap,
+                          ctx->img, target_dev, ctx->t_last, ctx->n_proc, scale, ctx->partial,
+                          ctx->tile_loss, false, ctx->stream);
+    ISG_CHECK_LAUNCH();
+    }
+    ISG_STAGE(ST_LOSS_REDUCE);
+    isg::launch_loss_reduce(ctx->tile_loss, fp.n_tiles, (double)weight / (3.0 * W * (double)H),
+                            ctx->loss, ctx->loss + 1, ctx->stream);
+    ISG_CHECK_LAUNCH();
+    ctx->launches += 2;
   }
-  ISG_STAGE(ST_LOSS_REDUCE);
-  isg::launch_loss_reduce(ctx->tile_loss, fp.n_tiles,
-                          (double)weight / (3.0 * fp.cam.width * (double)fp.cam.height), ctx->loss,
-                          ctx->loss + 1, ctx->stream);
-  ISG_CHECK_LAUNCH();
-  ctx->launches += 2;
   ctx->pending = true;
   ctx->pending_fp = fp;
   return ISG_OK;
@@ -591,7 +641,7 @@ void isg_destroy(isg_ctx* ctx) {
                  ctx->tval[0], ctx->tval[1], ctx->emit_gid, ctx->sort.hist, ctx->sort.lookback,
                  ctx->sort.counters, ctx->scan_scratch, ctx->img, ctx->target, ctx->t_last,
                  ctx->n_proc, ctx->ranges, ctx->tile_cnt, ctx->cursor, ctx->tile_loss, ctx->sc,
-                 ctx->total, ctx->loss, ctx->snap};
+                 ctx->total, ctx->loss, ctx->snap, ctx->coef, ctx->dldc, ctx->ssim_part};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (ctx->h_sc) cudaFreeHost(ctx->h_sc);
@@ -751,6 +801,7 @@ isg_status isg_loss_backward_device(isg_ctx* ctx, const isg_camera* cam, const f
   cudaSetDevice(ctx->device);
   isg_status s = validate_camera(ctx, cam);
   if (s != ISG_OK) return s;
+  if ((s = check_loss_size(ctx, cam->width, cam->height)) != ISG_OK) return s;
   const FrameParams fp = make_fp(cam, bg, t_min);
   if ((s = launch_frame(ctx, fp, nullptr)) != ISG_OK) return s;
   return run_backward(ctx, fp, target_dev, weight);
@@ -765,6 +816,7 @@ isg_status isg_loss_backward(isg_ctx* ctx, const isg_camera* cam, const float bg
   cudaSetDevice(ctx->device);
   isg_status s = validate_camera(ctx, cam);
   if (s != ISG_OK) return s;
+  if ((s = check_loss_size(ctx, cam->width, cam->height)) != ISG_OK) return s;
   if ((s = ensure_pixels(ctx, cam->width, cam->height)) != ISG_OK) return s;
   const FrameParams fp = make_fp(cam, bg, t_min);
   // The target upload runs on the copy stream, overlapped with binning and the forward blend;
@@ -907,15 +959,25 @@ isg_status isg_eval_loss(isg_ctx* ctx, const isg_camera* cam, const float bg[3],
   cudaSetDevice(ctx->device);
   isg_status s = validate_camera(ctx, cam);
   if (s != ISG_OK) return s;
+  if ((s = check_loss_size(ctx, cam->width, cam->height)) != ISG_OK) return s;
   const FrameParams fp = make_fp(cam, bg, t_min);
+  const int W = cam->width, H = cam->height;
+  if (ctx->loss_kind == ISG_LOSS_L1_DSSIM && (s = ensure_image_loss(ctx, W, H)) != ISG_OK) return s;
   for (int attempt = 0; attempt < 3; ++attempt) {
     if ((s = launch_frame(ctx, fp, nullptr)) != ISG_OK) return s;
-    isg::launch_l2_tiles(fp, ctx->img, target_dev, ctx->tile_loss, ctx->stream);
-    isg::launch_loss_reduce(ctx->tile_loss, fp.n_tiles,
-                            (double)weight / (3.0 * fp.cam.width * (double)fp.cam.height),
-                            nullptr, ctx->loss + 3, ctx->stream);
+    if (ctx->loss_kind == ISG_LOSS_L1_DSSIM) {
+      ISG_STAGE(ST_IMAGE_LOSS);
+      ctx->launches += isg::launch_image_loss(W, H, ctx->img, target_dev, ctx->lambda,
+                                              (double)weight, false, ctx->coef, ctx->ssim_part,
+                                              nullptr, ctx->total, ctx->key_cap, nullptr,
+                                              ctx->loss + 3, ctx->stream);
+    } else {
+      isg::launch_l2_tiles(fp, ctx->img, target_dev, ctx->tile_loss, ctx->stream);
+      isg::launch_loss_reduce(ctx->tile_loss, fp.n_tiles, (double)weight / (3.0 * W * (double)H),
+                              nullptr, ctx->loss + 3, ctx->stream);
+      ctx->launches += 2;
+    }
     ISG_CHECK_LAUNCH();
-    ctx->launches += 2;
     bool ov = false;
     if ((s = check_frame(ctx, &ov, true)) != ISG_OK) return s;
     if (ov) continue;
@@ -958,6 +1020,63 @@ isg_status isg_restore(isg_ctx* ctx) {
   }
   ctx->adam_t = ctx->snap_t;
   ctx->have_frame = false;
+  return ISG_OK;
+}
+
+isg_status isg_set_loss(isg_ctx* ctx, int kind, float lambda) {
+  if (!ctx) return ISG_E_ARG;
+  if (kind != ISG_LOSS_L2 && kind != ISG_LOSS_L1_DSSIM)
+    return fail(ctx, ISG_E_ARG, "set_loss: unknown loss kind");
+  if (kind == ISG_LOSS_L1_DSSIM && !(lambda >= 0.0f && lambda <= 1.0f))
+    return fail(ctx, ISG_E_DOMAIN, "loss: lambda must be in [0,1]");  // loss.cpp:186
+  ctx->loss_kind = kind;
+  if (kind == ISG_LOSS_L1_DSSIM) ctx->lambda = lambda;
+  return ISG_OK;
+}
+
+isg_status isg_image_loss_device(isg_ctx* ctx, int32_t width, int32_t height,
+                                 const float* fhat_dev, const float* target_dev, float weight,
+                                 double* loss_out, float* dldc_dev) {
+  if (!ctx || !loss_out || !fhat_dev || !target_dev) return ISG_E_ARG;
+  if (width <= 0 || height <= 0) return fail(ctx, ISG_E_ARG, "image_loss: bad image size");
+  if (!std::isfinite(weight)) return fail(ctx, ISG_E_ARG, "image_loss: non-finite weight");
+  cudaSetDevice(ctx->device);
+  isg_status s = check_loss_size(ctx, width, height);
+  if (s != ISG_OK) return s;
+  if ((s = isg_synchronize(ctx)) != ISG_OK) return s;
+  if (ctx->loss_kind == ISG_LOSS_L1_DSSIM) {
+    if ((s = ensure_image_loss(ctx, width, height)) != ISG_OK) return s;
+    ISG_STAGE(ST_IMAGE_LOSS);
+    ctx->launches += isg::launch_image_loss(width, height, fhat_dev, target_dev, ctx->lambda,
+                                            (double)weight, dldc_dev != nullptr, ctx->coef,
+                                            ctx->ssim_part, dldc_dev, nullptr, 0, nullptr,
+                                            ctx->loss + 3, ctx->stream);
+    ISG_CHECK_LAUNCH();
+  } else {
+    // mse (image.cpp:50-58) on the 16x16 tiling of the frame kernels
+    if ((s = ensure_pixels(ctx, width, height)) != ISG_OK) return s;
+    isg_camera cam{};
+    cam.width = width;
+    cam.height = height;
+    const FrameParams fp = make_fp(&cam, nullptr, 0.0f);
+    isg::launch_l2_tiles(fp, fhat_dev, target_dev, ctx->tile_loss, ctx->stream);
+    isg::launch_loss_reduce(ctx->tile_loss, fp.n_tiles,
+                            (double)weight / (3.0 * width * (double)height), nullptr,
+                            ctx->loss + 3, ctx->stream);
+    ISG_CHECK_LAUNCH();
+    ctx->launches += 2;
+    if (dldc_dev) {
+      isg::launch_l2_grad(width, height, fhat_dev, target_dev,
+                          2.0f * weight / (3.0f * (float)width * (float)height), dldc_dev,
+                          ctx->stream);
+      ISG_CHECK_LAUNCH();
+      ctx->launches += 1;
+    }
+  }
+  ISG_CUDA(cudaMemcpyAsync(ctx->h_loss + 3, ctx->loss + 3, sizeof(double), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  ISG_CUDA(cudaStreamSynchronize(ctx->stream));
+  *loss_out = ctx->h_loss[3];
   return ISG_OK;
 }
 

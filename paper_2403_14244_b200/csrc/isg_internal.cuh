@@ -100,11 +100,29 @@ void launch_blend_fwd(const FrameParams& fp, const uint2* ranges, const uint2* s
                       const RenderRec* rec, const unsigned long long* total, int64_t key_cap,
                       float* out, float* t_last, uint32_t* n_proc, cudaStream_t st);
 // Writes every pair's 2D gradient to partial[2 slot], partial[2 slot + 1].
+// given_dldc: `target` is dL/dC (G = loss_scale * target) and tile_loss is not meaningful;
+// otherwise G = 2 loss_scale (img - target) and tile_loss[t] = sum over the tile of |d|^2.
 void launch_blend_bwd(const FrameParams& fp, const uint2* ranges, const uint2* sorted,
                       const RenderRec* rec, const unsigned long long* total, int64_t key_cap,
                       const float* img, const float* target, const float* t_last,
                       const uint32_t* n_proc, float loss_scale, float4* partial,
-                      double* tile_loss, cudaStream_t st);
+                      double* tile_loss, bool given_dldc, cudaStream_t st);
+
+// ---- L1 + D-SSIM image loss (k_ssim.cu) ---------------------------------------------------
+constexpr int kSsimHalf = 5;  // 11-tap window
+int64_t ssim_part_count(int W, int H);  // double2 partials per frame
+// loss = weight ((1-lambda) L1 + lambda (1 - SSIM)) of fhat against target: *accum += loss
+// (if not null), *set = loss.  grad: also dL/dfhat (weight included) into dldc (HWC3), using
+// coef (9 W H floats) as scratch.  lambda == 0 skips SSIM (needs W, H >= 11 otherwise).
+// total/key_cap (may be null): a frame whose key capacity overflowed contributes nothing.
+// Returns the number of kernels launched.
+int launch_image_loss(int W, int H, const float* fhat, const float* target, float lambda,
+                       double weight, bool grad, float* coef, double2* part, float* dldc,
+                       const unsigned long long* total, int64_t key_cap, double* accum,
+                       double* set, cudaStream_t st);
+// dldc = scale (fhat - target) elementwise (the mse pixel gradient, scale = 2 w / (3 W H))
+void launch_l2_grad(int W, int H, const float* fhat, const float* target, float scale,
+                    float* dldc, cudaStream_t st);
 // s = scale * sum(tile_loss) (fixed order); *accum += s (if accum), *set = s
 void launch_loss_reduce(const double* tile_loss, int n_tiles, double scale, double* accum,
                         double* set, cudaStream_t st);

@@ -7,7 +7,8 @@
 // never divided by), and accumulating with A = colour behind:
 //     dL/da_k = T_k G.(c_k - A_k),  dL/dc_k = G T_k a_k,  A <- a c + (1 - a) A
 // with G = dL/dC = 2 w (C - target) / (3 W H) (mse, src/image.cpp:50-58) computed in the
-// prologue, and the kernel closed forms of include/isosplat/kernels.hpp:208-222.
+// prologue — or, for the L1 + D-SSIM loss, read from the dL/dC image k_ssim.cu wrote — and the
+// kernel closed forms of include/isosplat/kernels.hpp:208-222.
 //
 // Mapping: 64 threads per tile.  Each HALF-warp owns one 8x8 quarter-tile and each lane a 2x2
 // pixel quad.  Per staged batch every half-warp compacts the entries whose 3-sigma circle can
@@ -88,6 +89,7 @@ __device__ __forceinline__ float reduce_scatter8_half(const float v[8]) {
 
 }  // namespace
 
+template <bool kGivenG>
 __global__ void __launch_bounds__(kBT) k_blend_bwd(
     FrameParams fp, const uint2* __restrict__ ranges, const uint2* __restrict__ sorted,
     const RenderRec* __restrict__ rec, const unsigned long long* __restrict__ total,
@@ -134,13 +136,19 @@ __global__ void __launch_bounds__(kBT) k_blend_bwd(
     const int x = x0 + (p & 1), y = y0 + (p >> 1);
     if (x < W && y < H) {
       const size_t pix = (size_t)y * W + x;
-      const float d0 = img[3 * pix + 0] - target[3 * pix + 0];
-      const float d1 = img[3 * pix + 1] - target[3 * pix + 1];
-      const float d2 = img[3 * pix + 2] - target[3 * pix + 2];
-      dsq += d0 * d0 + d1 * d1 + d2 * d2;
-      s.G0 = 2.0f * d0 * loss_scale;
-      s.G1 = 2.0f * d1 * loss_scale;
-      s.G2 = 2.0f * d2 * loss_scale;
+      if (kGivenG) {  // `target` holds dL/dC (e.g. L1 + D-SSIM, k_ssim.cu)
+        s.G0 = target[3 * pix + 0] * loss_scale;
+        s.G1 = target[3 * pix + 1] * loss_scale;
+        s.G2 = target[3 * pix + 2] * loss_scale;
+      } else {
+        const float d0 = img[3 * pix + 0] - target[3 * pix + 0];
+        const float d1 = img[3 * pix + 1] - target[3 * pix + 1];
+        const float d2 = img[3 * pix + 2] - target[3 * pix + 2];
+        dsq += d0 * d0 + d1 * d1 + d2 * d2;
+        s.G0 = 2.0f * d0 * loss_scale;
+        s.G1 = 2.0f * d1 * loss_scale;
+        s.G2 = 2.0f * d2 * loss_scale;
+      }
       s.T = t_last[pix];
       s.np = (int)n_proc[pix];
       npmax = max(npmax, s.np);
@@ -301,9 +309,15 @@ void launch_blend_bwd(const FrameParams& fp, const uint2* ranges, const uint2* s
                       const RenderRec* rec, const unsigned long long* total, int64_t key_cap,
                       const float* img, const float* target, const float* t_last,
                       const uint32_t* n_proc, float loss_scale, float4* partial,
-                      double* tile_loss, cudaStream_t st) {
-  k_blend_bwd<<<fp.n_tiles, kBT, 0, st>>>(fp, ranges, sorted, rec, total, key_cap, img, target,
-                                          t_last, n_proc, loss_scale, partial, tile_loss);
+                      double* tile_loss, bool given_dldc, cudaStream_t st) {
+  if (given_dldc)
+    k_blend_bwd<true><<<fp.n_tiles, kBT, 0, st>>>(fp, ranges, sorted, rec, total, key_cap, img,
+                                                  target, t_last, n_proc, loss_scale, partial,
+                                                  tile_loss);
+  else
+    k_blend_bwd<false><<<fp.n_tiles, kBT, 0, st>>>(fp, ranges, sorted, rec, total, key_cap, img,
+                                                   target, t_last, n_proc, loss_scale, partial,
+                                                   tile_loss);
 }
 
 void launch_loss_reduce(const double* tile_loss, int n_tiles, double scale, double* accum,

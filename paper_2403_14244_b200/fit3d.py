@@ -28,7 +28,7 @@ from typing import List, Optional, Protocol, Sequence
 import numpy as np
 
 from . import scene_io
-from .isg import AdamConfig, DomainError, RenderOptions
+from .isg import LOSS_L1_DSSIM, LOSS_L2, AdamConfig, DomainError, RenderOptions
 
 
 class DivergenceError(RuntimeError):
@@ -47,10 +47,16 @@ class FitConfig3D:
     t_min: float = 1e-5
     background: tuple = (0.0, 0.0, 0.0)
     backoff: bool = False  # reject-and-halve steps that increase the loss
+    loss: str = "l2"       # "l2" (mse) or "l1_dssim" ((1-lam) L1 + lam (1 - SSIM), loss.cpp:184)
+    lam: float = 0.2       # FitConfig::lambda (the paper's 0.2)
 
     def validate(self):  # particles.hpp:73-83 style
         if self.epochs < 0:
             raise ValueError("epochs: must be >= 0")
+        if self.loss not in ("l2", "l1_dssim"):
+            raise ValueError("loss: must be 'l2' or 'l1_dssim'")
+        if not 0.0 <= self.lam <= 1.0:
+            raise ValueError("lambda: must be in [0,1]")
         for name in ("lr_mu", "lr_sigma", "lr_color", "lr_opacity"):
             if not getattr(self.adam, name) > 0:
                 raise ValueError(f"{name}: must be > 0")
@@ -166,6 +172,7 @@ class RendererBackend:
         self.n_views = len(self.cameras)
         self.opts = RenderOptions(background=config.background, t_min=config.t_min)
         self.adam = config.adam
+        renderer.set_loss(LOSS_L1_DSSIM if config.loss == "l1_dssim" else LOSS_L2, config.lam)
 
     def count(self) -> int:
         return self.r.n

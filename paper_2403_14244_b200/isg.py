@@ -20,6 +20,7 @@ _PKG = Path(__file__).resolve().parent
 LIB_PATH = _PKG / "libisg.so"
 
 ISG_OK, ISG_E_DOMAIN, ISG_E_ARG, ISG_E_CUDA, ISG_E_OOM, ISG_E_OVERFLOW, ISG_E_NCCL, ISG_E_STATE = range(8)
+LOSS_L2, LOSS_L1_DSSIM = 0, 1  # ISG_LOSS_* (include/isg.h)
 
 
 class IsgError(RuntimeError):
@@ -81,6 +82,8 @@ def lib() -> C.CDLL:
         "isg_eval_loss": ([P, C.POINTER(CameraT), fp, F, P, F, C.POINTER(C.c_double)], C.c_int),
         "isg_snapshot": ([P], C.c_int),
         "isg_restore": ([P], C.c_int),
+        "isg_set_loss": ([P, C.c_int, F], C.c_int),
+        "isg_image_loss_device": ([P, I32, I32, P, P, F, C.POINTER(C.c_double), P], C.c_int),
         "isg_nccl_get_unique_id": ([P], C.c_int),
         "isg_nccl_init": ([P, C.c_int, C.c_int, P], C.c_int),
         "isg_nccl_detach": ([P], C.c_int),
@@ -109,7 +112,7 @@ C_ABI_SYMBOLS = (
     "isg_get_scene", "isg_render", "isg_render_device", "isg_loss_backward",
     "isg_loss_backward_device", "isg_read_loss", "isg_zero_grads", "isg_get_grads",
     "isg_grads_device", "isg_adam_step", "isg_last_step_loss", "isg_eval_loss", "isg_snapshot",
-    "isg_restore", "isg_nccl_get_unique_id",
+    "isg_restore", "isg_set_loss", "isg_image_loss_device", "isg_nccl_get_unique_id",
     "isg_nccl_init",
     "isg_nccl_detach", "isg_debug_bins", "isg_debug_pixel_state", "isg_set_binning",
     "isg_profile_enable",
@@ -376,6 +379,20 @@ class Renderer:
 
     def restore(self):
         _check(self._h, lib().isg_restore(self._h))
+
+    def set_loss(self, kind: int = LOSS_L2, lam: float = 0.2):
+        """Training/eval loss: LOSS_L2 (mse) or LOSS_L1_DSSIM ((1-lam) L1 + lam (1 - SSIM),
+        loss.cpp:184-190)."""
+        _check(self._h, lib().isg_set_loss(self._h, int(kind), float(lam)))
+
+    def image_loss_device(self, width: int, height: int, fhat_ptr: int, target_ptr: int,
+                          weight: float = 1.0, dldc_ptr: Optional[int] = None) -> float:
+        """The configured loss of a device image against a device target (+ dL/dfhat)."""
+        v = C.c_double()
+        _check(self._h, lib().isg_image_loss_device(
+            self._h, int(width), int(height), C.c_void_p(fhat_ptr), C.c_void_p(target_ptr),
+            float(weight), C.byref(v), C.c_void_p(dldc_ptr) if dldc_ptr else None))
+        return v.value
 
     def last_step_loss(self) -> float:
         v = C.c_double()

@@ -11,6 +11,9 @@ The fixtures are small and committed, so the GPU box (no /root/reference) can us
   reference_scenes.npz  8 randomised scenes (<= 48x40 px, <= 120 splats, rotated cameras,
                         non-zero backgrounds, splats behind the camera / off screen, opacity 1)
                         and the reference renders
+  image_loss.npz        image pairs (11x11 up to 64x48, equal pixels, saturated values) with the
+                        reference's loss(), l1_term(), ssim() and ssim_gradient_wrt_second()
+                        (proj/src/loss.cpp:112-190) for several lambdas
 """
 import sys
 from pathlib import Path
@@ -65,7 +68,36 @@ def main():
         scenes[f"s{k}_bg"] = bg
         scenes[f"s{k}_image"] = img
     np.savez_compressed(OUT / "reference_scenes.npz", **scenes)
+    image_loss_fixture()
     print("golden fixtures written:", sorted(p.name for p in OUT.glob("*.npz")))
+
+
+IMAGE_LOSS_CASES = [(11, 11, 0.2), (17, 13, 0.2), (40, 24, 0.0), (33, 29, 1.0), (64, 48, 0.5)]
+
+
+def image_loss_fixture():
+    rng = np.random.default_rng(14244)
+    out = {}
+    for k, (W, H, lam) in enumerate(IMAGE_LOSS_CASES):
+        f = rng.random((H, W, 3))
+        fhat = np.clip(f + 0.15 * rng.standard_normal(f.shape), 0.0, 1.0)  # saturated values
+        eq = rng.random((H, W)) < 0.1
+        fhat[eq] = f[eq]  # equal pixels: L1 subgradient 0
+        loss, l1, ssim, g = O.ref_image_loss(f, fhat, lam, grad=True)
+        out[f"c{k}_f"], out[f"c{k}_fhat"] = f, fhat
+        out[f"c{k}_meta"] = np.array([W, H, lam, loss, l1, ssim])
+        out[f"c{k}_dssim"] = g if g is not None else np.zeros(0)
+    np.savez_compressed(OUT / "image_loss.npz", **out)
+
+
+def load_image_loss():
+    g = np.load(OUT / "image_loss.npz")
+    cases = []
+    for k in range(len(IMAGE_LOSS_CASES)):
+        W, H, lam, loss, l1, ssim = g[f"c{k}_meta"]
+        cases.append(dict(f=g[f"c{k}_f"], fhat=g[f"c{k}_fhat"], lam=float(lam), loss=float(loss),
+                          l1=float(l1), ssim=float(ssim), dssim=g[f"c{k}_dssim"]))
+    return cases
 
 
 def load_scenes():

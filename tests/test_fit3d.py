@@ -40,14 +40,26 @@ class OracleFitBackend:
     def params(self):
         return np.concatenate([self.ms, self.co], 1).astype(np.float64)
 
+    def _dssim(self, view, weight, grad):
+        img = O.render32(self.ms, self.co, self.cams[view], t_min=self.cfg.t_min, threads=1)
+        return O.image_loss64(self.targets[view], img, self.cfg.lam, weight, grad=grad)
+
     def eval_loss(self, view, weight):
+        if self.cfg.loss == "l1_dssim":
+            return self._dssim(view, weight, False)
         loss, _ = O.loss_backward32(self.ms, self.co, self.cams[view], self.targets[view],
                                     t_min=self.cfg.t_min, weight=weight, threads=1)
         return loss
 
     def loss_backward(self, view, weight):
-        loss, _ = O.loss_backward32(self.ms, self.co, self.cams[view], self.targets[view],
-                                    t_min=self.cfg.t_min, weight=weight, grads=self.g, threads=1)
+        if self.cfg.loss == "l1_dssim":
+            loss, dldc = self._dssim(view, weight, True)
+            O.backward_dldc32(self.ms, self.co, self.cams[view], dldc.astype(np.float32),
+                              t_min=self.cfg.t_min, threads=1, grads=self.g)
+        else:
+            loss, _ = O.loss_backward32(self.ms, self.co, self.cams[view], self.targets[view],
+                                        t_min=self.cfg.t_min, weight=weight, grads=self.g,
+                                        threads=1)
         self.loss += loss
 
     def step(self, rate_scale):
@@ -115,6 +127,13 @@ def test_divergence_error_non_finite_target():
     assert str(ei.value) == f"fit diverged at epoch 0 (particle {ei.value.particle_index})"
 
 
+def test_fit_l1_dssim_decreases_loss():
+    ms, co, cams, targets = problem()
+    cfg = FitConfig3D(epochs=5, loss="l1_dssim", lam=0.2)
+    st = fit(OracleFitBackend(ms, co, cams, targets, cfg), cfg)
+    assert st.loss_history[-1] < st.initial_loss
+
+
 def test_offending_particle_and_config_validation():
     p = np.tile(np.array([0, 0, 1, 0.1, 0.5, 0.5, 0.5, 0.5]), (4, 1))
     assert offending_particle(p) == -1
@@ -125,6 +144,10 @@ def test_offending_particle_and_config_validation():
         FitConfig3D(epochs=-1).validate()
     with pytest.raises(ValueError, match="lr_mu"):
         FitConfig3D(adam=isg.AdamConfig(lr_mu=0.0)).validate()
+    with pytest.raises(ValueError, match="lambda"):
+        FitConfig3D(loss="l1_dssim", lam=1.5).validate()
+    with pytest.raises(ValueError, match="loss"):
+        FitConfig3D(loss="ssim").validate()
 
 
 def test_outputs(tmp_path):
@@ -162,6 +185,17 @@ def _gpu_backend(ms, co, cams, targets, cfg):
 def test_gpu_fit_matches_oracle_trajectory():
     ms, co, cams, targets = problem()
     cfg = FitConfig3D(epochs=5)
+    st_o = fit(OracleFitBackend(ms, co, cams, targets, cfg), cfg)
+    st_g = fit(_gpu_backend(ms, co, cams, targets, cfg), cfg)
+    assert st_g.initial_loss == pytest.approx(st_o.initial_loss, rel=1e-5)
+    np.testing.assert_allclose(st_g.loss_history, st_o.loss_history, rtol=1e-3)
+    assert st_g.final_loss < st_g.initial_loss
+
+
+@pytest.mark.gpu
+def test_gpu_fit_l1_dssim_matches_oracle_trajectory():
+    ms, co, cams, targets = problem()
+    cfg = FitConfig3D(epochs=4, loss="l1_dssim", lam=0.2)
     st_o = fit(OracleFitBackend(ms, co, cams, targets, cfg), cfg)
     st_g = fit(_gpu_backend(ms, co, cams, targets, cfg), cfg)
     assert st_g.initial_loss == pytest.approx(st_o.initial_loss, rel=1e-5)
