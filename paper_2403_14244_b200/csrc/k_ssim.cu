@@ -12,9 +12,10 @@
 //   dL/dfhat     (1-l)/N sign(fhat - f) - l dSSIM/dfhat, sign(0) = 0           :201-213
 // with f = target, fhat = rendered image; everything here is scaled by the view weight w.
 //
-// Two kernels over 32x16-pixel output tiles (all three channels per CTA):
-//   k_ssim_fwd  stages the tile's 42x26 halo region of both images in shared memory (channel-
-//               planar), runs the 11-tap horizontal then vertical pass for the five moments,
+// Two kernels over 32x32-pixel output tiles (all three channels per CTA, one at a time):
+//   k_ssim_fwd  stages the tile's 42x42 halo region of both images in shared memory (RGB
+//               interleaved, as in HBM), runs the 11-tap horizontal then vertical pass for the
+//               five moments (each thread 4 consecutive outputs per pass, register-blocked),
 //               and at every valid position evaluates S and the three gradient coefficients
 //               (written as 9 planes, zero outside the valid region); per-CTA partial sums of
 //               |f - fhat| and S go to `part` (reduced in a fixed order, deterministic).
@@ -31,10 +32,17 @@ namespace isg {
 
 namespace {
 
-constexpr int kSX = 32, kSY = 16;  // output tile
+constexpr int kT = 32;  // output tile kT x kT, all three channels
 constexpr int kHalf = kSsimHalf, kWin = 2 * kSsimHalf + 1;
-constexpr int kRX = kSX + 2 * kHalf, kRY = kSY + 2 * kHalf;  // 42 x 26 halo region
-constexpr int kThreads = 256;                                // 32 x 8: 2 output rows each
+constexpr int kR = kT + 2 * kHalf;  // 42: halo region side
+constexpr int kThreads = 256;       // 8 warps
+constexpr int kG = 4;               // outputs per thread in each 1D pass (register blocking)
+constexpr int kIn = kG + kWin - 1;  // 14 inputs cover kG outputs
+constexpr int kHItems = kR * (kT / kG);  // horizontal-pass work items per plane (336)
+// Shared-memory pitches (odd / +1 so that lanes walking different rows hit different banks)
+constexpr int kPitchI = 3 * kR + 1;  // interleaved RGB rows of the images (127)
+constexpr int kPitchP = kR + 1;      // planar coefficient rows (43)
+constexpr int kPitchH = kT + 1;      // horizontal-pass results (33)
 constexpr float kC1 = 0.01f * 0.01f, kC2 = 0.03f * 0.03f;
 
 struct Taps {
@@ -54,6 +62,22 @@ Taps make_taps() {  // loss.cpp:22-35, in FP64 then rounded
 }
 
 __device__ __forceinline__ float sgn(float r) { return r > 0.0f ? 1.0f : (r < 0.0f ? -1.0f : 0.0f); }
+
+// 4-byte asynchronous global->shared copy; src_ok == false zero-fills (src not read).
+__device__ __forceinline__ void cp_async4(float* dst, const float* src, bool src_ok) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(src),
+               "r"(src_ok ? 4 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 // Block-wide sum of two floats per thread into double2 (fixed order).
 __device__ void block_sum2(float a, float b, double2* out) {
@@ -83,12 +107,12 @@ __global__ void __launch_bounds__(kThreads) k_l1(int W, int H, const float* __re
                                                  const float* __restrict__ f, float w1,
                                                  double2* __restrict__ part,
                                                  float* __restrict__ dldc) {
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int bx = blockIdx.x * kSX, by = blockIdx.y * kSY;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gx = blockIdx.x * kT + lane;
   float l1 = 0.0f;
 #pragma unroll
-  for (int o = 0; o < 2; ++o) {
-    const int gx = bx + tx, gy = by + 2 * ty + o;
+  for (int o = 0; o < kG; ++o) {
+    const int gy = blockIdx.y * kT + warp * kG + o;
     if (gx < W && gy < H) {
       const size_t p = 3 * ((size_t)gy * W + gx);
 #pragma unroll
@@ -102,93 +126,126 @@ __global__ void __launch_bounds__(kThreads) k_l1(int W, int H, const float* __re
   block_sum2(l1, 0.0f, part + blockIdx.y * gridDim.x + blockIdx.x);
 }
 
+struct FwdSmem {
+  float a[kR][kPitchI];  // target f, interleaved RGB, halo region
+  float b[kR][kPitchI];  // render fhat
+  float h[5][kR][kPitchH];
+};
+
+// Moments of one channel -> S and the gradient coefficients at the tile's valid positions.
 template <bool kGrad>
 __global__ void __launch_bounds__(kThreads) k_ssim_fwd(int W, int H, const float* __restrict__ fhat,
                                                        const float* __restrict__ f, Taps tp,
                                                        float* __restrict__ coef,
                                                        double2* __restrict__ part) {
-  __shared__ float sa[3][kRY][kRX];
-  __shared__ float sb[3][kRY][kRX];
-  __shared__ float hs[5][kRY][kSX];
-  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
-  const int bx = blockIdx.x * kSX, by = blockIdx.y * kSY;
-  const int blk = blockIdx.y * gridDim.x + blockIdx.x;
+  extern __shared__ float4 smem_raw[];
+  FwdSmem& S = *reinterpret_cast<FwdSmem*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int bx = blockIdx.x * kT, by = blockIdx.y * kT;
   const size_t HW = (size_t)W * H;
-  float l1 = 0.0f, ssum = 0.0f;
-  // stage the halo region, de-interleaving channels (zero outside the image = zero padding)
-  for (int i = tid; i < kRY * kRX * 3; i += kThreads) {
-    const int r = i / (kRX * 3), k = i - r * (kRX * 3);
-    const int px = k / 3, c = k - px * 3;
-    const int gy = by - kHalf + r, gx = bx - kHalf + px;
-    float va = 0.0f, vb = 0.0f;
-    if (gy >= 0 && gy < H && gx >= 0 && gx < W) {
-      const size_t o = 3 * ((size_t)gy * W + gx) + c;
-      va = f[o];
-      vb = fhat[o];
-    }
-    sa[c][r][px] = va;
-    sb[c][r][px] = vb;
-  }
-  __syncthreads();
+  const int row_len = 3 * W;
+  // stage the halo region as it lies in HBM (interleaved RGB rows), all copies in flight at
+  // once; zero outside the image
+  for (int r = warp; r < kR; r += kThreads / 32) {
+    const int gy = by - kHalf + r;
+    const bool row_ok = gy >= 0 && gy < H;
+    const size_t roff = row_ok ? (size_t)gy * row_len : 0;
 #pragma unroll
-  for (int o = 0; o < 2; ++o) {
-    const int gx = bx + tx, gy = by + 2 * ty + o;
-    if (gx < W && gy < H) {
+    for (int k0 = 0; k0 < 3 * kR; k0 += 32) {
+      const int k = k0 + lane;
+      if (k < 3 * kR) {
+        const int gx3 = 3 * (bx - kHalf) + k;
+        const bool ok = row_ok && gx3 >= 0 && gx3 < row_len;
+        const size_t o = ok ? roff + gx3 : 0;
+        cp_async4(&S.a[r][k], f + o, ok);
+        cp_async4(&S.b[r][k], fhat + o, ok);
+      }
+    }
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  // L1 over the tile's own pixels (thread: column lane, rows warp*kG ..)
+  float l1 = 0.0f, ssum = 0.0f;
+  const int x = lane, y0 = warp * kG;
+#pragma unroll
+  for (int o = 0; o < kG; ++o)
+    if (bx + x < W && by + y0 + o < H) {
 #pragma unroll
       for (int c = 0; c < 3; ++c)
-        l1 += fabsf(sa[c][2 * ty + o + kHalf][tx + kHalf] - sb[c][2 * ty + o + kHalf][tx + kHalf]);
+        l1 += fabsf(S.a[y0 + o + kHalf][3 * (x + kHalf) + c] - S.b[y0 + o + kHalf][3 * (x + kHalf) + c]);
     }
-  }
   for (int c = 0; c < 3; ++c) {
-    // horizontal pass: 5 moments at every region row, output columns
-    for (int i = tid; i < kRY * kSX; i += kThreads) {
-      const int r = i / kSX, x = i - r * kSX;
-      float m1 = 0.f, m2 = 0.f, t1 = 0.f, t2 = 0.f, t12 = 0.f;
+    // horizontal pass: item = (row, kG consecutive outputs); lanes walk different rows
+    for (int i = tid; i < kHItems; i += kThreads) {
+      const int g = i / kR, r = i - g * kR;
+      const float* pa = &S.a[r][3 * g * kG + c];
+      const float* pb = &S.b[r][3 * g * kG + c];
+      float acc[kG][5];
 #pragma unroll
-      for (int d = 0; d < kWin; ++d) {
-        const float a = sa[c][r][x + d], b = sb[c][r][x + d], w = tp.w[d];
-        m1 = fmaf(w, a, m1);
-        m2 = fmaf(w, b, m2);
-        t1 = fmaf(w * a, a, t1);
-        t2 = fmaf(w * b, b, t2);
-        t12 = fmaf(w * a, b, t12);
+      for (int o = 0; o < kG; ++o)
+#pragma unroll
+        for (int k = 0; k < 5; ++k) acc[o][k] = 0.0f;
+#pragma unroll
+      for (int j = 0; j < kIn; ++j) {
+        const float a = pa[3 * j], b = pb[3 * j];
+        const float v[5] = {a, b, a * a, b * b, a * b};
+#pragma unroll
+        for (int o = 0; o < kG; ++o) {
+          const int d = j - o;
+          if (d >= 0 && d < kWin) {
+#pragma unroll
+            for (int k = 0; k < 5; ++k) acc[o][k] = fmaf(tp.w[d], v[k], acc[o][k]);
+          }
+        }
       }
-      hs[0][r][x] = m1;
-      hs[1][r][x] = m2;
-      hs[2][r][x] = t1;
-      hs[3][r][x] = t2;
-      hs[4][r][x] = t12;
+#pragma unroll
+      for (int o = 0; o < kG; ++o)
+#pragma unroll
+        for (int k = 0; k < 5; ++k) S.h[k][r][g * kG + o] = acc[o][k];
     }
     __syncthreads();
-    // vertical pass: two output rows per thread share 10 of their 11 taps
-    float v[2][5] = {};
+    // vertical pass: thread = (column lane, kG consecutive output rows)
+    float acc[kG][5];
 #pragma unroll
-    for (int j = 0; j < kWin + 1; ++j) {
+    for (int o = 0; o < kG; ++o)
 #pragma unroll
-      for (int k = 0; k < 5; ++k) {
-        const float h = hs[k][2 * ty + j][tx];
-        if (j < kWin) v[0][k] = fmaf(tp.w[j], h, v[0][k]);
-        if (j >= 1) v[1][k] = fmaf(tp.w[j - 1], h, v[1][k]);
+      for (int k = 0; k < 5; ++k) acc[o][k] = 0.0f;
+#pragma unroll
+    for (int j = 0; j < kIn; ++j) {
+      float v[5];
+#pragma unroll
+      for (int k = 0; k < 5; ++k) v[k] = S.h[k][y0 + j][x];
+#pragma unroll
+      for (int o = 0; o < kG; ++o) {
+        const int d = j - o;
+        if (d >= 0 && d < kWin) {
+#pragma unroll
+          for (int k = 0; k < 5; ++k) acc[o][k] = fmaf(tp.w[d], v[k], acc[o][k]);
+        }
       }
     }
+    const int gx = bx + x;
 #pragma unroll
-    for (int o = 0; o < 2; ++o) {
-      const int gx = bx + tx, gy = by + 2 * ty + o;
+    for (int o = 0; o < kG; ++o) {
+      const int gy = by + y0 + o;
       if (gx >= W || gy >= H) continue;
       const bool valid = gx >= kHalf && gx < W - kHalf && gy >= kHalf && gy < H - kHalf;
       float g_m2 = 0.f, g_t2 = 0.f, g_t12 = 0.f;
       if (valid) {
-        const float m1 = v[o][0], m2 = v[o][1];
-        const float s11 = v[o][2] - m1 * m1, s22 = v[o][3] - m2 * m2, s12 = v[o][4] - m1 * m2;
+        const float m1 = acc[o][0], m2 = acc[o][1];
+        const float s11 = acc[o][2] - m1 * m1, s22 = acc[o][3] - m2 * m2;
+        const float s12 = acc[o][4] - m1 * m2;
         const float nl = 2.0f * m1 * m2 + kC1, dl = m1 * m1 + m2 * m2 + kC1;
         const float nc = 2.0f * s12 + kC2, dc = s11 + s22 + kC2;
-        const float lum = nl / dl, cs = nc / dc;
+        const float idl = rcp_approx(dl), idc = rcp_approx(dc);
+        const float lum = nl * idl, cs = nc * idc;
         ssum += lum * cs;
-        if (kGrad) {
-          const float d_s22 = -lum * nc / (dc * dc);
-          const float d_s12 = lum * 2.0f / dc;
-          const float d_lum_m2 = (2.0f * m1 * dl - nl * 2.0f * m2) / (dl * dl);
-          g_m2 = cs * d_lum_m2 + d_s22 * (-2.0f * m2) + d_s12 * (-m1);
+        if (kGrad) {  // loss.cpp:164-170
+          const float d_s22 = -lum * cs * idc;
+          const float d_s12 = 2.0f * lum * idc;
+          const float d_lum_m2 = 2.0f * (m1 * dl - nl * m2) * (idl * idl);
+          g_m2 = cs * d_lum_m2 - 2.0f * m2 * d_s22 - m1 * d_s12;
           g_t2 = d_s22;
           g_t12 = d_s12;
         }
@@ -200,67 +257,102 @@ __global__ void __launch_bounds__(kThreads) k_ssim_fwd(int W, int H, const float
         coef[(3 * c + 2) * HW + p] = g_t12;
       }
     }
-    __syncthreads();  // hs is rewritten by the next channel
+    __syncthreads();  // S.h is rewritten by the next channel
   }
-  block_sum2(l1, ssum, part + blk);
+  block_sum2(l1, ssum, part + blockIdx.y * gridDim.x + blockIdx.x);
 }
 
-// dL/dfhat = w1 sign(fhat - f) - wl norm (F1 + 2 fhat F2 + f F3), F = window-filtered coefficients.
+struct BwdSmem {
+  float c[3][3][kR][kPitchP];  // [channel][coefficient] planes, halo region
+  float h[3][kR][kPitchH];
+};
+
+// dL/dfhat = w1 sign(fhat - f) - wln (F1 + 2 fhat F2 + f F3), F = window-filtered coefficients.
 __global__ void __launch_bounds__(kThreads) k_ssim_bwd(int W, int H, const float* __restrict__ fhat,
                                                        const float* __restrict__ f,
                                                        const float* __restrict__ coef, Taps tp,
                                                        float w1, float wln,
                                                        float* __restrict__ dldc) {
-  __shared__ float sc[3][kRY][kRX];
-  __shared__ float hs[3][kRY][kSX];
-  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
-  const int bx = blockIdx.x * kSX, by = blockIdx.y * kSY;
+  extern __shared__ float4 smem_raw[];
+  BwdSmem& S = *reinterpret_cast<BwdSmem*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int bx = blockIdx.x * kT, by = blockIdx.y * kT;
   const size_t HW = (size_t)W * H;
+  const int x = lane, y0 = warp * kG;
+  // all nine coefficient planes in flight at once, one commit group per channel
   for (int c = 0; c < 3; ++c) {
-    for (int i = tid; i < 3 * kRY * kRX; i += kThreads) {
-      const int k = i / (kRY * kRX), rem = i - k * (kRY * kRX);
-      const int r = rem / kRX, px = rem - r * kRX;
-      const int gy = by - kHalf + r, gx = bx - kHalf + px;
-      float val = 0.0f;
-      if (gy >= 0 && gy < H && gx >= 0 && gx < W) val = coef[(3 * c + k) * HW + (size_t)gy * W + gx];
-      sc[k][r][px] = val;
-    }
-    __syncthreads();
-    for (int i = tid; i < kRY * kSX; i += kThreads) {
-      const int r = i / kSX, x = i - r * kSX;
-      float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+    for (int rr = warp; rr < 3 * kR; rr += kThreads / 32) {
+      const int k = rr / kR, r = rr - k * kR;
+      const int gy = by - kHalf + r;
+      const bool row_ok = gy >= 0 && gy < H;
+      const float* src = coef + (3 * c + k) * HW + (row_ok ? (size_t)gy * W : 0);
 #pragma unroll
-      for (int d = 0; d < kWin; ++d) {
-        const float w = tp.w[d];
-        a0 = fmaf(w, sc[0][r][x + d], a0);
-        a1 = fmaf(w, sc[1][r][x + d], a1);
-        a2 = fmaf(w, sc[2][r][x + d], a2);
-      }
-      hs[0][r][x] = a0;
-      hs[1][r][x] = a1;
-      hs[2][r][x] = a2;
-    }
-    __syncthreads();
-    float v[2][3] = {};
-#pragma unroll
-    for (int j = 0; j < kWin + 1; ++j) {
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const float h = hs[k][2 * ty + j][tx];
-        if (j < kWin) v[0][k] = fmaf(tp.w[j], h, v[0][k]);
-        if (j >= 1) v[1][k] = fmaf(tp.w[j - 1], h, v[1][k]);
+      for (int px0 = 0; px0 < kR; px0 += 32) {
+        const int px = px0 + lane;
+        if (px < kR) {
+          const int gx = bx - kHalf + px;
+          const bool ok = row_ok && gx >= 0 && gx < W;
+          cp_async4(&S.c[c][k][r][px], ok ? src + gx : coef, ok);
+        }
       }
     }
+    cp_async_commit();
+  }
+  for (int c = 0; c < 3; ++c) {
+    if (c == 0) cp_async_wait<2>();
+    else if (c == 1) cp_async_wait<1>();
+    else cp_async_wait<0>();
+    __syncthreads();
+    for (int i = tid; i < kHItems; i += kThreads) {
+      const int g = i / kR, r = i - g * kR;
+      float acc[kG][3];
 #pragma unroll
-    for (int o = 0; o < 2; ++o) {
-      const int gx = bx + tx, gy = by + 2 * ty + o;
+      for (int o = 0; o < kG; ++o) acc[o][0] = acc[o][1] = acc[o][2] = 0.0f;
+#pragma unroll
+      for (int j = 0; j < kIn; ++j) {
+        const float v[3] = {S.c[c][0][r][g * kG + j], S.c[c][1][r][g * kG + j],
+                            S.c[c][2][r][g * kG + j]};
+#pragma unroll
+        for (int o = 0; o < kG; ++o) {
+          const int d = j - o;
+          if (d >= 0 && d < kWin) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) acc[o][k] = fmaf(tp.w[d], v[k], acc[o][k]);
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 0; o < kG; ++o)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) S.h[k][r][g * kG + o] = acc[o][k];
+    }
+    __syncthreads();
+    float acc[kG][3];
+#pragma unroll
+    for (int o = 0; o < kG; ++o) acc[o][0] = acc[o][1] = acc[o][2] = 0.0f;
+#pragma unroll
+    for (int j = 0; j < kIn; ++j) {
+      const float v[3] = {S.h[0][y0 + j][x], S.h[1][y0 + j][x], S.h[2][y0 + j][x]};
+#pragma unroll
+      for (int o = 0; o < kG; ++o) {
+        const int d = j - o;
+        if (d >= 0 && d < kWin) {
+#pragma unroll
+          for (int k = 0; k < 3; ++k) acc[o][k] = fmaf(tp.w[d], v[k], acc[o][k]);
+        }
+      }
+    }
+    const int gx = bx + x;
+#pragma unroll
+    for (int o = 0; o < kG; ++o) {
+      const int gy = by + y0 + o;
       if (gx >= W || gy >= H) continue;
       const size_t p = 3 * ((size_t)gy * W + gx) + c;
       const float a = f[p], b = fhat[p];
-      const float g = v[o][0] + 2.0f * b * v[o][1] + a * v[o][2];
+      const float g = acc[o][0] + 2.0f * b * acc[o][1] + a * acc[o][2];
       dldc[p] = w1 * sgn(b - a) - wln * g;
     }
-    __syncthreads();  // sc / hs are rewritten by the next channel
+    __syncthreads();  // S.h is rewritten by the next channel
   }
 }
 
@@ -296,7 +388,7 @@ __global__ void k_ssim_reduce(const double2* __restrict__ part, int n, double l1
   }
 }
 
-dim3 ssim_grid(int W, int H) { return dim3((W + kSX - 1) / kSX, (H + kSY - 1) / kSY); }
+dim3 ssim_grid(int W, int H) { return dim3((W + kT - 1) / kT, (H + kT - 1) / kT); }
 
 __global__ void k_l2_grad(int64_t n, const float* __restrict__ fhat, const float* __restrict__ f,
                           float scale, float* __restrict__ dldc) {
@@ -324,6 +416,16 @@ int launch_image_loss(int W, int H, const float* fhat, const float* target, floa
                        const unsigned long long* total, int64_t key_cap, double* accum,
                        double* set, cudaStream_t st) {
   static const Taps tp = make_taps();
+  static const bool attr = [] {
+    cudaFuncSetAttribute(k_ssim_fwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(FwdSmem));
+    cudaFuncSetAttribute(k_ssim_fwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(FwdSmem));
+    cudaFuncSetAttribute(k_ssim_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(BwdSmem));
+    return true;
+  }();
+  (void)attr;
   const dim3 grid = ssim_grid(W, H);
   const bool ssim = lambda != 0.0f;
   const double N = 3.0 * W * (double)H;
@@ -334,10 +436,11 @@ int launch_image_loss(int W, int H, const float* fhat, const float* target, floa
   if (!ssim) {
     k_l1<<<grid, kThreads, 0, st>>>(W, H, fhat, target, w1, part, grad ? dldc : nullptr);
   } else if (grad) {
-    k_ssim_fwd<true><<<grid, kThreads, 0, st>>>(W, H, fhat, target, tp, coef, part);
-    k_ssim_bwd<<<grid, kThreads, 0, st>>>(W, H, fhat, target, coef, tp, w1, wln, dldc);
+    k_ssim_fwd<true><<<grid, kThreads, sizeof(FwdSmem), st>>>(W, H, fhat, target, tp, coef, part);
+    k_ssim_bwd<<<grid, kThreads, sizeof(BwdSmem), st>>>(W, H, fhat, target, coef, tp, w1, wln,
+                                                         dldc);
   } else {
-    k_ssim_fwd<false><<<grid, kThreads, 0, st>>>(W, H, fhat, target, tp, coef, part);
+    k_ssim_fwd<false><<<grid, kThreads, sizeof(FwdSmem), st>>>(W, H, fhat, target, tp, coef, part);
   }
   k_ssim_reduce<<<1, 256, 0, st>>>(part, (int)(grid.x * grid.y), weight * (1.0 - lam) / N,
                                    ssim ? weight * lam : 0.0, ssim ? weight * lam / valid : 0.0,

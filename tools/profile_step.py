@@ -1,7 +1,8 @@
 #!/usr/bin/env python3
 """Minimal driver for ncu captures: C3 (1M splats, 1080p) train steps through the C-ABI with
 device-resident inputs, no timing and no CPU work, so `ncu -k regex:...` sees only our
-kernels.  Usage: python tools/profile_step.py [--steps 3] [--config c3|c2|c5] [--render]"""
+kernels.  Usage: python tools/profile_step.py [--steps 3] [--config c3|c2|c5] [--render]
+[--loss l2|l1_dssim]"""
 import argparse
 import sys
 from pathlib import Path
@@ -22,6 +23,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--config", default="c3", choices=sorted(SIZES))
     ap.add_argument("--render", action="store_true", help="forward only")
+    ap.add_argument("--loss", default="l2", choices=["l2", "l1_dssim"])
     a = ap.parse_args()
     n, W, H = SIZES[a.config]
     ms, co = isg.synth_scene(n, W, H, seed=2403)
@@ -32,6 +34,8 @@ def main():
     torch.cuda.set_stream(stream)
     r = isg.Renderer(0, n, W, H)
     r.set_stream(stream.cuda_stream)
+    if a.loss == "l1_dssim":
+        r.set_loss(isg.LOSS_L1_DSSIM, 0.2)
     target = torch.empty((H, W, 3), dtype=torch.float32, device="cuda")
     r.set_scene(tms, tco)
     r.render_device(cam, opts, target.data_ptr())
