@@ -70,17 +70,22 @@ __global__ void __launch_bounds__(kBT) k_blend_fwd(
   const int n = (int)(rg.y - rg.x);
   const float t_min = fp.t_min;
 
-  // invalid pixels start "terminated" (T = 0 <= t_min) and never contribute
-  float T0 = valid0 ? 1.0f : 0.0f, T1 = valid1 ? 1.0f : 0.0f;
+  // The pixel pair is processed as packed f32x2 (FFMA2/FMUL2/FADD2: one issue slot for both
+  // pixels); .x = pixel (px, py), .y = pixel (px, py + 1).  Every packed op rounds per lane
+  // exactly like its scalar counterpart, so the 3-sigma test stays bit-identical to the oracle.
+  // Invalid pixels start "terminated" (T = 0 <= t_min) and never contribute.
+  const float2 PY = make_float2(py0, py1);
+  float2 T = make_float2(valid0 ? 1.0f : 0.0f, valid1 ? 1.0f : 0.0f);
   float Tl0 = 1.0f, Tl1 = 1.0f;
-  float C0r = 0.f, C0g = 0.f, C0b = 0.f, C1r = 0.f, C1g = 0.f, C1b = 0.f;
+  float2 Cr = make_float2(0.f, 0.f), Cg = Cr, Cb = Cr;
   uint32_t np0 = 0, np1 = 0;
+  const float2 kOne = make_float2(1.0f, 1.0f), kMinusOne = make_float2(-1.0f, -1.0f);
 
   if (n > 0) stage_batch(st[0], sorted, rec, rg.x, min(kBatch, n));
   for (int b = 0, it = 0; b < n; b += kBatch, ++it) {
     Stage<kBatch>& cur = st[it & 1];
     cp_async_wait_all();
-    const bool tdone = !(T0 > t_min) && !(T1 > t_min);
+    const bool tdone = !(T.x > t_min) && !(T.y > t_min);
     if (__syncthreads_count(tdone) == kBT) break;  // barrier: batch visible, previous consumed
     if (b + kBatch < n)
       stage_batch(st[(it + 1) & 1], sorted, rec, rg.x + b + kBatch, min(kBatch, n - b - kBatch));
@@ -91,29 +96,30 @@ __global__ void __launch_bounds__(kBT) k_blend_fwd(
       const float4 c = cur.col[jj];
       const float dx = __fsub_rn(px, g.x);
       const float ax = __fmul_rn(dx, dx);
-      const float dy0 = __fsub_rn(py0, g.y), dy1 = __fsub_rn(py1, g.y);
-      const float r20 = __fadd_rn(ax, __fmul_rn(dy0, dy0));
-      const float r21 = __fadd_rn(ax, __fmul_rn(dy1, dy1));
-      const bool in0 = !(r20 > g.z) && (T0 > t_min);
-      const bool in1 = !(r21 > g.z) && (T1 > t_min);
+      const float2 dy = __fadd2_rn(PY, make_float2(-g.y, -g.y));
+      // scalar: ptxas would contract a packed mul.rn + add.rn into FFMA2 (one rounding), and
+      // the 3-sigma test must round exactly like the oracle's (and K1's) dist2_rn
+      const float2 r2 = make_float2(__fadd_rn(ax, __fmul_rn(dy.x, dy.x)),
+                                    __fadd_rn(ax, __fmul_rn(dy.y, dy.y)));
+      const bool in0 = !(r2.x > g.z) && (T.x > t_min);
+      const bool in1 = !(r2.y > g.z) && (T.y > t_min);
       const uint32_t idx = (uint32_t)(b + jj + 1);
-      const float a0 = in0 ? c.w * fast_exp2(r20 * g.w) : 0.0f;
-      const float a1 = in1 ? c.w * fast_exp2(r21 * g.w) : 0.0f;
-      const float w0 = T0 * a0, w1 = T1 * a1;
-      C0r += w0 * c.x;
-      C0g += w0 * c.y;
-      C0b += w0 * c.z;
-      C1r += w1 * c.x;
-      C1g += w1 * c.y;
-      C1b += w1 * c.z;
-      Tl0 = in0 ? T0 : Tl0;
-      Tl1 = in1 ? T1 : Tl1;
+      const float2 q = __fmul2_rn(r2, make_float2(g.w, g.w));
+      const float2 e = __fmul2_rn(make_float2(c.w, c.w), make_float2(fast_exp2(q.x), fast_exp2(q.y)));
+      const float2 a = make_float2(in0 ? e.x : 0.0f, in1 ? e.y : 0.0f);
+      const float2 wgt = __fmul2_rn(T, a);
+      Cr = __ffma2_rn(wgt, make_float2(c.x, c.x), Cr);
+      Cg = __ffma2_rn(wgt, make_float2(c.y, c.y), Cg);
+      Cb = __ffma2_rn(wgt, make_float2(c.z, c.z), Cb);
+      Tl0 = in0 ? T.x : Tl0;
+      Tl1 = in1 ? T.y : Tl1;
       np0 = in0 ? idx : np0;
       np1 = in1 ? idx : np1;
-      T0 = T0 * (1.0f - a0);
-      T1 = T1 * (1.0f - a1);
+      T = __fmul2_rn(T, __ffma2_rn(a, kMinusOne, kOne));  // T (1 - a)
     }
   }
+  const float T0 = T.x, T1 = T.y;
+  const float C0r = Cr.x, C0g = Cg.x, C0b = Cb.x, C1r = Cr.y, C1g = Cg.y, C1b = Cb.y;
   cp_async_wait_all();
   if (valid0) {
     const size_t pix = (size_t)py_i * W + px_i;

@@ -29,37 +29,48 @@ using namespace blend;
 constexpr int kBT = 64;     // threads per tile CTA: 2 warps = 4 half-warps = 4 quarter-tiles
 constexpr int kBatch = 64;  // records staged per batch (one per thread)
 
-struct BwdPix {
-  float G0, G1, G2;  // dL/dC
-  float T;           // transmittance before the most recently processed (later) entry
-  float A0, A1, A2;  // colour behind, normalised
-  int np;            // list entries the forward processed for this pixel
+// Two horizontally adjacent pixels (same row) as packed f32x2 lanes: .x = (x0, y), .y = (x0+1, y).
+// Packed FFMA2/FMUL2/FADD2 issue once for both pixels.
+struct BwdPair {
+  float2 G0, G1, G2;  // dL/dC
+  float2 T;           // transmittance before the most recently processed (later) entry
+  float2 A0, A1, A2;  // colour behind, normalised
+  int np0, np1;       // list entries the forward processed for each pixel
 };
 
+__device__ __forceinline__ float2 bc(float v) { return make_float2(v, v); }
+
 // acc: [0] sum go*dx, [1] sum go*dy, [2] sum go*r2 (scaled per entry into du, dv, dsigma2d),
-// [3] dopacity, [4..6] drgb;  go = dL/dalpha * g.  An inactive pixel gets e = 0, hence a = 0:
-// T and A stay exactly unchanged and every contribution is an exact zero.
-__device__ __forceinline__ void bwd_pixel(BwdPix& p, bool act, int j, float dx, float dy,
-                                          float r2, const float4 g, const float4 c,
-                                          float acc[8]) {
-  const float e = act ? fast_exp2(r2 * g.w) : 0.0f;
-  const float a = c.w * e;
-  const float Tk = (j == p.np - 1) ? p.T : p.T * fast_rcp(1.0f - a);
+// [3] dopacity, [4..6] drgb;  go = dL/dalpha * g; summed per lane of the pair.  An inactive
+// pixel gets e = 0, hence a = 0: T and A stay exactly unchanged and every contribution is an
+// exact zero.
+__device__ __forceinline__ void bwd_pair(BwdPair& p, bool act0, bool act1, int j, float2 dx,
+                                         float dy, float2 r2, const float4 g, const float4 c,
+                                         float2 acc[8]) {
+  const float2 q = __fmul2_rn(r2, bc(g.w));
+  const float2 e = make_float2(act0 ? fast_exp2(q.x) : 0.0f, act1 ? fast_exp2(q.y) : 0.0f);
+  const float2 a = __fmul2_rn(bc(c.w), e);
+  const float2 om = __ffma2_rn(a, bc(-1.0f), bc(1.0f));  // 1 - a
+  const float2 Tr = __fmul2_rn(p.T, make_float2(fast_rcp(om.x), fast_rcp(om.y)));
+  const float2 Tk = make_float2(j == p.np0 - 1 ? p.T.x : Tr.x, j == p.np1 - 1 ? p.T.y : Tr.y);
   p.T = Tk;
-  const float d0 = c.x - p.A0, d1 = c.y - p.A1, d2 = c.z - p.A2;
-  const float dLda = Tk * (p.G0 * d0 + p.G1 * d1 + p.G2 * d2);
-  const float Ta = Tk * a;
-  acc[4] += p.G0 * Ta;
-  acc[5] += p.G1 * Ta;
-  acc[6] += p.G2 * Ta;
-  p.A0 += a * d0;
-  p.A1 += a * d1;
-  p.A2 += a * d2;
-  const float go = dLda * e;
-  acc[3] += go;
-  acc[0] += go * dx;
-  acc[1] += go * dy;
-  acc[2] += go * r2;
+  const float2 d0 = __fadd2_rn(bc(c.x), make_float2(-p.A0.x, -p.A0.y));
+  const float2 d1 = __fadd2_rn(bc(c.y), make_float2(-p.A1.x, -p.A1.y));
+  const float2 d2 = __fadd2_rn(bc(c.z), make_float2(-p.A2.x, -p.A2.y));
+  const float2 gd = __ffma2_rn(p.G2, d2, __ffma2_rn(p.G1, d1, __fmul2_rn(p.G0, d0)));
+  const float2 dLda = __fmul2_rn(Tk, gd);
+  const float2 Ta = __fmul2_rn(Tk, a);
+  acc[4] = __ffma2_rn(p.G0, Ta, acc[4]);
+  acc[5] = __ffma2_rn(p.G1, Ta, acc[5]);
+  acc[6] = __ffma2_rn(p.G2, Ta, acc[6]);
+  p.A0 = __ffma2_rn(a, d0, p.A0);
+  p.A1 = __ffma2_rn(a, d1, p.A1);
+  p.A2 = __ffma2_rn(a, d2, p.A2);
+  const float2 go = __fmul2_rn(dLda, e);
+  acc[3] = __fadd2_rn(acc[3], go);
+  acc[0] = __ffma2_rn(go, dx, acc[0]);
+  acc[1] = __ffma2_rn(go, bc(dy), acc[1]);
+  acc[2] = __ffma2_rn(go, r2, acc[2]);
 }
 
 // reduce-scatter of 8 values over a 16-lane half-warp in 8 shuffles: lane l returns the sum
@@ -115,44 +126,50 @@ __global__ void __launch_bounds__(kBT) k_blend_bwd(
   const int W = fp.cam.width, H = fp.cam.height;
   const int x0 = tx * kTile + (q & 1) * 8 + 2 * (l16 & 3);
   const int y0 = ty * kTile + (q >> 1) * 8 + 2 * (l16 >> 2);
-  const float px[2] = {(float)x0 + 0.5f, (float)x0 + 1.5f};
-  const float py[2] = {(float)y0 + 0.5f, (float)y0 + 1.5f};
+  const float2 PX = make_float2((float)x0 + 0.5f, (float)x0 + 1.5f);
+  const float2 PY = make_float2((float)y0 + 0.5f, (float)y0 + 1.5f);
   const Region regA = region_rect(fp, tile, 2 * w), regB = region_rect(fp, tile, 2 * w + 1);
   const uint2 rg = ranges[tile];
   const int n = (int)(rg.y - rg.x);
 
-  BwdPix P[4];
+  BwdPair P[2];  // P[k]: the quad's row k
   float dsq = 0.0f;
   int npmax = 0;
 #pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    BwdPix& s = P[p];
-    s.G0 = s.G1 = s.G2 = 0.0f;
-    s.T = 0.0f;
-    s.np = 0;
-    s.A0 = fp.bg[0];
-    s.A1 = fp.bg[1];
-    s.A2 = fp.bg[2];
-    const int x = x0 + (p & 1), y = y0 + (p >> 1);
-    if (x < W && y < H) {
-      const size_t pix = (size_t)y * W + x;
-      if (kGivenG) {  // `target` holds dL/dC (e.g. L1 + D-SSIM, k_ssim.cu)
-        s.G0 = target[3 * pix + 0] * loss_scale;
-        s.G1 = target[3 * pix + 1] * loss_scale;
-        s.G2 = target[3 * pix + 2] * loss_scale;
-      } else {
-        const float d0 = img[3 * pix + 0] - target[3 * pix + 0];
-        const float d1 = img[3 * pix + 1] - target[3 * pix + 1];
-        const float d2 = img[3 * pix + 2] - target[3 * pix + 2];
-        dsq += d0 * d0 + d1 * d1 + d2 * d2;
-        s.G0 = 2.0f * d0 * loss_scale;
-        s.G1 = 2.0f * d1 * loss_scale;
-        s.G2 = 2.0f * d2 * loss_scale;
+  for (int k = 0; k < 2; ++k) {
+    float G[2][3] = {}, T[2] = {0.f, 0.f};
+    int np[2] = {0, 0};
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int x = x0 + i, y = y0 + k;
+      if (x < W && y < H) {
+        const size_t pix = (size_t)y * W + x;
+        if (kGivenG) {  // `target` holds dL/dC (e.g. L1 + D-SSIM, k_ssim.cu)
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) G[i][ch] = target[3 * pix + ch] * loss_scale;
+        } else {
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) {
+            const float d = img[3 * pix + ch] - target[3 * pix + ch];
+            dsq += d * d;
+            G[i][ch] = 2.0f * d * loss_scale;
+          }
+        }
+        T[i] = t_last[pix];
+        np[i] = (int)n_proc[pix];
+        npmax = max(npmax, np[i]);
       }
-      s.T = t_last[pix];
-      s.np = (int)n_proc[pix];
-      npmax = max(npmax, s.np);
     }
+    BwdPair& s = P[k];
+    s.G0 = make_float2(G[0][0], G[1][0]);
+    s.G1 = make_float2(G[0][1], G[1][1]);
+    s.G2 = make_float2(G[0][2], G[1][2]);
+    s.T = make_float2(T[0], T[1]);
+    s.np0 = np[0];
+    s.np1 = np[1];
+    s.A0 = bc(fp.bg[0]);
+    s.A1 = bc(fp.bg[1]);
+    s.A2 = bc(fp.bg[2]);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -219,17 +236,26 @@ __global__ void __launch_bounds__(kBT) k_blend_bwd(
       const int j = lo + jj;
       const float4 g = cur.geo[jj];
       const float4 c = cur.col[jj];
-      const float dx[2] = {__fsub_rn(px[0], g.x), __fsub_rn(px[1], g.x)};
-      const float dy[2] = {__fsub_rn(py[0], g.y), __fsub_rn(py[1], g.y)};
-      const float ax[2] = {__fmul_rn(dx[0], dx[0]), __fmul_rn(dx[1], dx[1])};
-      const float ay[2] = {__fmul_rn(dy[0], dy[0]), __fmul_rn(dy[1], dy[1])};
-      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      const float2 dx = __fadd2_rn(PX, bc(-g.x));
+      const float2 dy = __fadd2_rn(PY, bc(-g.y));
+      // r2 in scalar: ptxas would contract a packed mul.rn + add.rn into FFMA2 (one rounding),
+      // and the 3-sigma test must round exactly like the oracle's (and the forward's)
+      const float ax0 = __fmul_rn(dx.x, dx.x), ax1 = __fmul_rn(dx.y, dx.y);
+      float2 acc2[8];
 #pragma unroll
-      for (int p = 0; p < 4; ++p) {
-        const float r2 = __fadd_rn(ax[p & 1], ay[p >> 1]);
-        const bool act = has && j < P[p].np && !(r2 > g.z);
-        bwd_pixel(P[p], act, j, dx[p & 1], dy[p >> 1], r2, g, c, acc);
+      for (int k = 0; k < 8; ++k) acc2[k] = bc(0.0f);
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const float dyk = k ? dy.y : dy.x;
+        const float ay = __fmul_rn(dyk, dyk);
+        const float2 r2 = make_float2(__fadd_rn(ax0, ay), __fadd_rn(ax1, ay));
+        const bool act0 = has && j < P[k].np0 && !(r2.x > g.z);
+        const bool act1 = has && j < P[k].np1 && !(r2.y > g.z);
+        bwd_pair(P[k], act0, act1, j, dx, dyk, r2, g, c, acc2);
       }
+      float acc[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[k] = acc2[k].x + acc2[k].y;
       // kernels.hpp:219-220: dg/du = g 2 dx / s^2, dg/ds = g 2 r^2 / s^3, times opacity
       const float inv_s2 = g.w * -kLn2;     // 1 / sigma2d^2
       const float k2 = 2.0f * c.w * inv_s2;  // 2 o / s^2
