@@ -42,7 +42,10 @@ struct __align__(16) RenderRec {
 
 // ---- radix sort (onesweep, 8-bit digits, u32 keys + u32 values) ---------------------------
 constexpr int kSortThreads = 256;
-constexpr int kSortItems = 8;  // items per thread
+#ifndef ISG_SORT_ITEMS
+#define ISG_SORT_ITEMS 8
+#endif
+constexpr int kSortItems = ISG_SORT_ITEMS;  // items per thread
 constexpr int kSortTileItems = kSortThreads * kSortItems;
 constexpr int kMaxPasses = 4;
 

@@ -20,6 +20,13 @@
 #include "isg_math.cuh"
 #include "lookback.cuh"
 
+#ifndef ISG_HIST_MODE
+#define ISG_HIST_MODE 2
+#endif
+#ifndef ISG_LOOKBACK_WIN
+#define ISG_LOOKBACK_WIN 16
+#endif
+
 namespace isg {
 
 namespace {
@@ -73,9 +80,31 @@ __global__ void __launch_bounds__(256) k_hist(const uint32_t* __restrict__ keys,
   for (int i = threadIdx.x; i < kMaxPasses * 256; i += 256) (&sh[0][0])[i] = 0;
   __syncthreads();
   const int64_t n = min((int64_t)*n_dev, cap);
-  for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < n; i += (int64_t)gridDim.x * 256) {
-    const uint32_t k = keys[i];
-    for (int p = 0; p < passes; ++p) atomicAdd(&sh[p][(k >> (8 * p)) & 255u], 1u);
+  const uint32_t lt = lanemask_lt();
+  // grid-stride over whole warps.  A digit shared by the whole warp (the skewed high bytes:
+  // e.g. the exponent byte of positive depths, the top bits of tile ids) costs one shared
+  // atomic per warp instead of 32 serialised ones.
+  const int64_t stride = (int64_t)gridDim.x * 256;
+  for (int64_t i0 = (int64_t)blockIdx.x * 256 + (threadIdx.x & ~31); i0 < n; i0 += stride) {
+    const int64_t i = i0 + (threadIdx.x & 31);
+    const bool valid = i < n;
+    const uint32_t k = valid ? keys[i] : 0u;
+    const bool full = __all_sync(0xffffffffu, valid);
+    for (int p = 0; p < passes; ++p) {
+      const uint32_t d = (k >> (8 * p)) & 255u;
+#if ISG_HIST_MODE == 1
+      const uint32_t dv = valid ? d : 256u;
+      const uint32_t peers = __match_any_sync(0xffffffffu, dv);
+      if (dv < 256u && (peers & lt) == 0) atomicAdd(&sh[p][dv], (uint32_t)__popc(peers));
+#else
+      const uint32_t d0 = __shfl_sync(0xffffffffu, d, 0);
+      if (full && __all_sync(0xffffffffu, d == d0)) {
+        if ((threadIdx.x & 31) == 0) atomicAdd(&sh[p][d0], 32u);
+      } else if (valid) {
+        atomicAdd(&sh[p][d], 1u);
+      }
+#endif
+    }
   }
   __syncthreads();
   for (int p = 0; p < passes; ++p) {
@@ -143,45 +172,15 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
     S.wcnt[ww][tid] = cnt;
     cnt += c;
   }
-  // publish this tile's aggregate (or inclusive prefix for tile 0)
+  // publish this tile's aggregate (or inclusive prefix for tile 0) as early as possible
   uint32_t* my = lookback + (int64_t)tile * 256 + tid;
-  if (tile == 0) {
-    st_volatile(my, kFlagInc | cnt);
-  } else {
-    st_volatile(my, kFlagAgg | cnt);
-  }
+  st_volatile(my, (tile == 0 ? kFlagInc : kFlagAgg) | cnt);
   uint32_t tot;
   const uint32_t local_start = block_excl_scan_256(cnt, S.warp_tmp, tot);
-  const uint32_t gpre = block_excl_scan_256(hist[tid], S.warp_tmp, tot);
-  // decoupled look-back for digit `tid`
-  uint32_t excl = 0;
-  if (tile > 0) {
-    // walk back kWin predecessors per round trip, all loads in flight at once (statuses only
-    // move 0 -> AGG -> INC, so a stale aggregate is still a correct partial sum); the
-    // inclusive-prefix frontier then advances kWin tiles per L2 round trip
-    constexpr int kWin = 16;
-    int64_t p = (int64_t)tile - 1;
-    bool found = false;
-    while (!found) {
-      uint32_t s[kWin];
-#pragma unroll
-      for (int q = 0; q < kWin; ++q)
-        s[q] = p - q >= 0 ? ld_volatile(lookback + (p - q) * 256 + tid) : kFlagInc;
-#pragma unroll
-      for (int q = 0; q < kWin; ++q) {
-        if (found) break;
-        while ((s[q] & ~kCountMask) == 0) s[q] = ld_volatile(lookback + (p - q) * 256 + tid);
-        excl += s[q] & kCountMask;
-        found = (s[q] & ~kCountMask) == kFlagInc;
-      }
-      p -= kWin;
-    }
-    st_volatile(my, kFlagInc | (excl + cnt));
-  }
   S.local_start[tid] = local_start;
-  S.bin_base[tid] = gpre + excl - local_start;
   __syncthreads();
-  // scatter into shared memory in tile-sorted order
+  // scatter into shared memory in tile-sorted order (independent of the global offsets, so the
+  // per-item registers are dead before the look-back)
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
     const uint32_t d = dig[j];
@@ -191,6 +190,33 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
       S.vals[pos] = val[j];
     }
   }
+  const uint32_t gpre = block_excl_scan_256(hist[tid], S.warp_tmp, tot);
+  // decoupled look-back for digit `tid`
+  uint32_t excl = 0;
+  if (tile > 0) {
+    // walk back kWin predecessors per round trip, all loads in flight at once (statuses only
+    // move 0 -> AGG -> INC, so a stale aggregate is still a correct partial sum); the
+    // inclusive-prefix frontier then advances kWin tiles per L2 round trip
+    constexpr int kWin = ISG_LOOKBACK_WIN;
+    int64_t p = (int64_t)tile - 1;
+    bool found = false;
+    while (!found) {
+      uint32_t sw[kWin];
+#pragma unroll
+      for (int q = 0; q < kWin; ++q)
+        sw[q] = p - q >= 0 ? ld_volatile(lookback + (p - q) * 256 + tid) : kFlagInc;
+#pragma unroll
+      for (int q = 0; q < kWin; ++q) {
+        if (found) break;
+        while ((sw[q] & ~kCountMask) == 0) sw[q] = ld_volatile(lookback + (p - q) * 256 + tid);
+        excl += sw[q] & kCountMask;
+        found = (sw[q] & ~kCountMask) == kFlagInc;
+      }
+      p -= kWin;
+    }
+    st_volatile(my, kFlagInc | (excl + cnt));
+  }
+  S.bin_base[tid] = gpre + excl - local_start;
   __syncthreads();
   const int nvalid = (int)min((int64_t)kSortTileItems, n - base);
   for (int i = tid; i < nvalid; i += kSortThreads) {
