@@ -156,6 +156,32 @@ isg_status isg_image_loss_device(isg_ctx* ctx, int32_t width, int32_t height,
                                  const float* fhat_dev, const float* target_dev, float weight,
                                  double* loss_out, float* dldc_dev);
 
+/* ---- adaptive control (prune / merge / split of the splat set) ----------------------------
+ * adaptive_control (src/optimize.cpp:221-284) for isotropic 3D splats, on the device:
+ *   prune  opacity < prune_threshold (the first splat of maximal opacity always survives)
+ *   merge  pairs with |mu_i - mu_j| < merge_distance_factor * min(sigma) and max colour
+ *          difference < merge_color_tol, greedily nearest-first on (dist, i, j), one merge per
+ *          splat; weights w = opacity * sigma^2, mu / sigma^2 / colour w-weighted, opacity =
+ *          min(1, (w1 + w2) / sigma^2)
+ *   split  sigma > split_sigma_max (world units), widest first, while count <= max_particles
+ *          (<= 0: twice the current count); children at mu +- d sigma/2, sigma / sqrt(2), d a
+ *          unit direction from (seed, round, parent index)
+ * Parameter checks and messages follow AdaptiveControlParams::validate
+ * (include/isosplat/optimize.hpp:21-27).  Adam moments and step restart at zero (the
+ * reference clears its momentum, optimize.cpp:344).  Synchronises. */
+typedef struct {
+  double prune_threshold;       /* 1e-3 in the reference */
+  double merge_distance_factor; /* 0.5 */
+  double merge_color_tol;       /* 0.05 */
+  double split_sigma_max;       /* world units */
+  int64_t max_particles;        /* effective cap; <= 0: 2 x the current count */
+} isg_adapt_params;
+typedef struct {
+  int64_t n_before, n_pruned, n_merged, n_split, n_after;
+} isg_adapt_result;
+isg_status isg_adaptive_control(isg_ctx* ctx, const isg_adapt_params* params, uint64_t seed,
+                                uint64_t round, isg_adapt_result* out);
+
 /* ---- multi-GPU (one process per GPU, views sharded, NCCL all-reduce before Adam) -------- */
 /* NCCL is resolved at run time (dlopen libnccl.so.2, the copy torch already loaded if any). */
 isg_status isg_nccl_get_unique_id(void* out_128_bytes);

@@ -66,6 +66,11 @@ def lib():
         L.or64_image_loss.argtypes = [C.c_int, C.c_int, P, P, C.c_double, C.c_double,
                                       C.POINTER(C.c_double), P]
         L.or64_image_loss.restype = C.c_int
+        L.or_adaptive_control.argtypes = [C.c_int, I64, P, P, C.c_int, C.c_uint64, C.c_uint64, P,
+                                          I64, P]
+        L.or_adaptive_control.restype = I64
+        L.or_split_direction.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, P]
+        L.or_split_direction.restype = None
         _lib = L
     return _lib
 
@@ -239,6 +244,32 @@ def image_loss64(target, fhat, lam=0.2, weight=1.0, grad=False):
     return (v.value, g) if grad else v.value
 
 
+class AdaptParams(C.Structure):
+    """AdaptiveControlParams (optimize.hpp:14-28) with the effective particle cap."""
+    _fields_ = [("prune_threshold", C.c_double), ("merge_distance_factor", C.c_double),
+                ("merge_color_tol", C.c_double), ("split_sigma_max", C.c_double),
+                ("max_particles", C.c_int64)]
+
+
+def adaptive_control(records, params: AdaptParams, dims=3, channels=3, seed=0, round_=0):
+    """Oracle prune -> merge -> split (optimize.cpp:150-284); dims 2 = the reference's 2D
+    rules, dims 3 = the 3D splat rules.  Returns (records, (pruned, merged, split))."""
+    R = 8 if dims == 3 else 6
+    a = np.ascontiguousarray(records, np.float64).reshape(-1, R)
+    cap = max(int(params.max_particles), a.shape[0]) + 1
+    out = np.zeros((cap, R))
+    counts = np.zeros(3, np.int64)
+    m = lib().or_adaptive_control(dims, a.shape[0], _p(a), C.byref(params), channels, seed,
+                                  round_, _p(out), cap, _p(counts))
+    return out[:m].copy(), tuple(int(c) for c in counts)
+
+
+def split_direction(seed, round_, index):
+    d = np.zeros(3)
+    lib().or_split_direction(seed, round_, index, _p(d))
+    return d
+
+
 # ---- the reference's own code (oracle/_ref, built by oracle/build_ref.sh) -----------------
 _ref = None
 
@@ -261,6 +292,9 @@ def ref_lib():
         L.ref_image_loss.argtypes = [C.c_int, C.c_int, P, P, C.c_double, P, P, C.c_char_p,
                                      C.c_int]
         L.ref_image_loss.restype = C.c_int
+        L.ref_adaptive_control_2d.argtypes = [I64, P, P, C.c_int, C.c_int, C.c_uint64, P, I64,
+                                              C.c_char_p, C.c_int]
+        L.ref_adaptive_control_2d.restype = I64
         _ref = L
     return _ref
 
@@ -318,3 +352,19 @@ def ref_image_loss(target, fhat, lam=0.2, grad=False):
                                 err, 512):
         raise ValueError(err.value.decode())
     return (out[0], out[1], out[2], g) if grad else (out[0], out[1], out[2])
+
+
+def ref_adaptive_control_2d(records, prune_threshold=1e-3, merge_distance_factor=0.5,
+                            merge_color_tol=0.05, split_sigma_max=15.0, max_particles=0,
+                            channels=3, seed=0):
+    """The reference's adaptive_control on IsoParticle2D records (n, 6)."""
+    a = np.ascontiguousarray(records, np.float64).reshape(-1, 6)
+    prm = np.array([prune_threshold, merge_distance_factor, merge_color_tol, split_sigma_max])
+    cap = max(max_particles, a.shape[0]) + 1
+    out = np.zeros((cap, 6))
+    err = C.create_string_buffer(512)
+    m = ref_lib().ref_adaptive_control_2d(a.shape[0], _p(a), _p(prm), max_particles, channels,
+                                          seed, _p(out), cap, err, 512)
+    if m < 0:
+        raise ValueError(err.value.decode())
+    return out[:m].copy()

@@ -6,6 +6,7 @@
 #   /root/reference/proj/src/image.cpp     ImageGrid, mse
 #   /root/reference/proj/src/loss.cpp      L1 + D-SSIM loss, ssim gradient (+ reconstruct.cpp,
 #                                          which loss.cpp's 2D overloads link against)
+#   /root/reference/proj/src/optimize.cpp  adaptive_control (prune / merge / split), 2D
 #
 # The reference's build system is not used (it needs cmake + Eigen + libpng + vendored
 # CLI11/json, none of which exist here).  Eigen is replaced by oracle/eigen_shim, a minimal
@@ -20,6 +21,7 @@ mkdir -p "$OUT"
 g++ -std=c++20 -O2 -ffp-contract=off -fPIC -shared -pthread \
     -I "$HERE/eigen_shim" -I "$REF/include" \
     "$REF/src/splat3d.cpp" "$REF/src/image.cpp" "$REF/src/loss.cpp" "$REF/src/reconstruct.cpp" \
+    "$REF/src/optimize.cpp" \
     "$HERE/ref_capi.cpp" \
     -o "$OUT/libisosplat_ref.so"
 echo "built $OUT/libisosplat_ref.so"

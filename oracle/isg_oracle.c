@@ -900,3 +900,261 @@ void or32_adam(int64_t n, float* mu_sigma, float* rgb_o, float* m, float* v, con
   }
   if (skipped) *skipped += skip;
 }
+
+/* ============================================================================================
+ * (4) Adaptive control (prune / merge / split), /root/reference/proj/src/optimize.cpp:150-284.
+ *
+ * One control flow (prune_impl :153-174, adaptive_control :221-284), two rule sets:
+ *   dims == 2  the reference's IsoParticle2D rules verbatim (records mu.x mu.y sigma A0 A1 A2):
+ *              prune on max-channel |A| (:47-51), merge weights luminance(A) pi sigma^2 with
+ *              per-channel zeroth-moment conservation (:200-219, luminance :19-22)
+ *   dims == 3  the isotropic 3D splat rules the GPU implements (records mu.xyz sigma r g b o):
+ *              prune on opacity; merge weights w = o sigma^2 (screen-footprint mass),
+ *              mu / sigma^2 / colour w-weighted, o = min(1, (w1 + w2) / sigma^2) (footprint mass
+ *              conserved); split children at mu +- (sigma/2) d, sigma / sqrt(2), colour and
+ *              opacity kept, d a unit direction from Marsaglia's method on a splitmix64 stream
+ *              keyed by (seed, round, parent index) — no transcendental functions, so the GPU
+ *              reproduces it bit for bit; every 3D result is rounded to FP32 at the end.
+ * Pairs qualify when |mu_i - mu_j| < gamma min(sigma) and the max colour difference < tol
+ * (:232-244); they are taken greedily nearest-first on (dist, i, j) (:246-259), one merge per
+ * particle, a refused merge still consumes both; splits go widest first, ties by higher index,
+ * while the count stays <= max_particles (:266-281).  Returns the new count (<= out_cap).
+ * ============================================================================================ */
+typedef struct {
+  double prune_threshold, merge_distance_factor, merge_color_tol, split_sigma_max;
+  int64_t max_particles;
+} or_adapt_params;
+
+typedef struct {
+  double dist;
+  int64_t i, j;
+} or_pair;
+
+static int cmp_pair(const void* a, const void* b) {
+  const or_pair *x = (const or_pair*)a, *y = (const or_pair*)b;
+  if (x->dist != y->dist) return x->dist < y->dist ? -1 : 1;
+  if (x->i != y->i) return x->i < y->i ? -1 : 1;
+  if (x->j != y->j) return x->j < y->j ? -1 : 1;
+  return 0;
+}
+
+static uint64_t or_splitmix(uint64_t* s) {
+  uint64_t z = (*s += 0x9E3779B97F4A7C15ull);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+/* Unit direction for splitting parent `index` (Marsaglia 1972). */
+void or_split_direction(uint64_t seed, uint64_t round, uint64_t index, double d[3]) {
+  uint64_t s = seed ^ (round * 0xD1B54A32D192ED03ull) ^ (index * 0xA24BAED4963EE407ull);
+  for (;;) {
+    const double u1 = (double)(or_splitmix(&s) >> 11) * 0x1.0p-52 - 1.0;
+    const double u2 = (double)(or_splitmix(&s) >> 11) * 0x1.0p-52 - 1.0;
+    const double q = u1 * u1 + u2 * u2;
+    if (q >= 1.0 || q == 0.0) continue;
+    const double f = 2.0 * sqrt(1.0 - q);
+    d[0] = u1 * f;
+    d[1] = u2 * f;
+    d[2] = 1.0 - 2.0 * q;
+    return;
+  }
+}
+
+static double or_lum(const double* a, int channels) {
+  if (channels == 1) return a[0];
+  return 0.2126 * a[0] + 0.7152 * a[1] + 0.0722 * a[2];
+}
+
+static double or_prune_score(int dims, const double* r, int channels) {
+  if (dims == 3) return r[7];
+  double m = fabs(r[3]);
+  for (int c = 1; c < channels; ++c) m = fabs(r[3 + c]) > m ? fabs(r[3 + c]) : m;
+  return m;
+}
+
+static double or_color_diff(int dims, const double* a, const double* b, int channels) {
+  const int off = dims == 3 ? 4 : 3, nc = dims == 3 ? 3 : channels;
+  double m = 0.0;
+  for (int c = 0; c < nc; ++c) {
+    const double d = fabs(a[off + c] - b[off + c]);
+    m = d > m ? d : m;
+  }
+  return m;
+}
+
+static double or_dist(int dims, const double* a, const double* b) {
+  double s = 0.0;
+  for (int k = 0; k < dims; ++k) {
+    const double d = a[k] - b[k];
+    s = s + d * d;
+  }
+  return sqrt(s);
+}
+
+static float f32(double x) { return (float)x; }
+
+/* merge (optimize.cpp:200-219 for 2D; the 3D rule above).  Returns 0 when refused. */
+static int or_merge(int dims, const double* p1, const double* p2, int channels, double* out) {
+  if (dims == 2) {
+    const double PI = 3.14159265358979323846;
+    const double w1 = or_lum(p1 + 3, channels) * PI * p1[2] * p1[2];
+    const double w2 = or_lum(p2 + 3, channels) * PI * p2[2] * p2[2];
+    const double total = w1 + w2;
+    if (fabs(total) < 1e-12) return 0;
+    const double mx = (w1 * p1[0] + w2 * p2[0]) / total, my = (w1 * p1[1] + w2 * p2[1]) / total;
+    const double s2 = (w1 * p1[2] * p1[2] + w2 * p2[2] * p2[2]) / total;
+    if (!(s2 > 0.0) || !isfinite(s2) || !isfinite(mx) || !isfinite(my)) return 0;
+    out[0] = mx;
+    out[1] = my;
+    out[2] = sqrt(s2);
+    for (int c = 0; c < 3; ++c) out[3 + c] = 0.0;
+    for (int c = 0; c < channels; ++c) {
+      const double m1 = p1[3 + c] * PI * p1[2] * p1[2];
+      const double m2 = p2[3 + c] * PI * p2[2] * p2[2];
+      out[3 + c] = (m1 + m2) / (PI * s2);
+    }
+    return 1;
+  }
+  const double w1 = p1[7] * (p1[3] * p1[3]), w2 = p2[7] * (p2[3] * p2[3]);
+  const double total = w1 + w2;
+  if (fabs(total) < 1e-12) return 0;
+  double mu[3];
+  for (int k = 0; k < 3; ++k) mu[k] = (w1 * p1[k] + w2 * p2[k]) / total;
+  const double s2 = (w1 * (p1[3] * p1[3]) + w2 * (p2[3] * p2[3])) / total;
+  if (!(s2 > 0.0) || !isfinite(s2) || !isfinite(mu[0]) || !isfinite(mu[1]) || !isfinite(mu[2]))
+    return 0;
+  for (int k = 0; k < 3; ++k) out[k] = f32(mu[k]);
+  out[3] = f32(sqrt(s2));
+  for (int c = 0; c < 3; ++c) out[4 + c] = f32((w1 * p1[4 + c] + w2 * p2[4 + c]) / total);
+  const double o = total / s2;
+  out[7] = f32(o < 1.0 ? o : 1.0);
+  if (!(out[3] > 0.0)) return 0; /* sigma underflowed in FP32 */
+  return 1;
+}
+
+typedef struct {
+  double sigma;
+  int64_t idx;
+} or_cand;
+
+static int cmp_cand(const void* a, const void* b) { /* sigma desc, then index desc */
+  const or_cand *x = (const or_cand*)a, *y = (const or_cand*)b;
+  if (x->sigma != y->sigma) return x->sigma > y->sigma ? -1 : 1;
+  if (x->idx != y->idx) return x->idx > y->idx ? -1 : 1;
+  return 0;
+}
+
+int64_t or_adaptive_control(int dims, int64_t n, const double* in, const or_adapt_params* p,
+                            int channels, uint64_t seed, uint64_t round, double* out,
+                            int64_t out_cap, int64_t* counts /* pruned, merged, split */) {
+  const int R = dims == 3 ? 8 : 6;
+  const int sig = dims == 3 ? 3 : 2;
+  if (n <= 0) return 0;
+  /* prune (keep the best-scoring first index if nothing survives) */
+  double* a = (double*)malloc(sizeof(double) * R * (size_t)n);
+  int64_t m = 0, best = 0;
+  double best_s = -1.0;
+  for (int64_t i = 0; i < n; ++i) {
+    const double s = or_prune_score(dims, in + R * i, channels);
+    if (s > best_s) {
+      best_s = s;
+      best = i;
+    }
+  }
+  for (int64_t i = 0; i < n; ++i)
+    if (or_prune_score(dims, in + R * i, channels) >= p->prune_threshold)
+      memcpy(a + R * m++, in + R * i, sizeof(double) * R);
+  if (m == 0) memcpy(a + R * m++, in + R * best, sizeof(double) * R);
+  if (counts) counts[0] = n - m;
+  /* merge: all qualifying pairs, greedy nearest-first */
+  int64_t np = 0, pcap = 1024;
+  or_pair* pairs = (or_pair*)malloc(sizeof(or_pair) * pcap);
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = i + 1; j < m; ++j) {
+      const double* pi = a + R * i;
+      const double* pj = a + R * j;
+      const double dist = or_dist(dims, pi, pj);
+      const double smin = pi[sig] < pj[sig] ? pi[sig] : pj[sig];
+      if (dist >= p->merge_distance_factor * smin) continue;
+      if (or_color_diff(dims, pi, pj, channels) >= p->merge_color_tol) continue;
+      if (np == pcap) pairs = (or_pair*)realloc(pairs, sizeof(or_pair) * (pcap *= 2));
+      pairs[np].dist = dist;
+      pairs[np].i = i;
+      pairs[np].j = j;
+      ++np;
+    }
+  qsort(pairs, (size_t)np, sizeof(or_pair), cmp_pair);
+  char* used = (char*)calloc((size_t)m, 1);
+  char* drop = (char*)calloc((size_t)m, 1);
+  int64_t merged = 0;
+  double tmp[8];
+  for (int64_t k = 0; k < np; ++k) {
+    const int64_t i = pairs[k].i, j = pairs[k].j;
+    if (used[i] || used[j]) continue;
+    used[i] = used[j] = 1;
+    if (or_merge(dims, a + R * i, a + R * j, channels, tmp)) {
+      memcpy(a + R * i, tmp, sizeof(double) * R);
+      drop[j] = 1;
+      ++merged;
+    }
+  }
+  if (counts) counts[1] = merged;
+  int64_t c = 0;
+  for (int64_t i = 0; i < m; ++i)
+    if (!drop[i] && c < out_cap) memcpy(out + R * c++, a + R * i, sizeof(double) * R);
+  /* split: widest first while the budget allows */
+  int64_t nc = 0;
+  or_cand* cand = (or_cand*)malloc(sizeof(or_cand) * (size_t)(c > 0 ? c : 1));
+  for (int64_t i = 0; i < c; ++i)
+    if (out[R * i + sig] > p->split_sigma_max) {
+      cand[nc].sigma = out[R * i + sig];
+      cand[nc].idx = i;
+      ++nc;
+    }
+  qsort(cand, (size_t)nc, sizeof(or_cand), cmp_cand);
+  int64_t splits = 0;
+  const int64_t base = c;
+  for (int64_t k = 0; k < nc; ++k) {
+    if (c + 1 > p->max_particles || c + 1 > out_cap) break;
+    const int64_t i = cand[k].idx;
+    double* par = out + R * i;
+    double* ch = out + R * c;
+    memcpy(ch, par, sizeof(double) * R);
+    if (dims == 3) {
+      double d[3];
+      or_split_direction(seed, round, (uint64_t)i, d);
+      const double h = 0.5 * par[3];
+      for (int q = 0; q < 3; ++q) {
+        const double off = h * d[q];
+        ch[q] = f32(par[q] - off);
+        par[q] = f32(par[q] + off);
+      }
+      par[3] = ch[3] = f32(par[3] * sqrt(0.5));
+    } else {
+      /* 2D: the reference draws phi from std::mt19937_64 (optimize.cpp:188-198); here the
+       * direction is the 3D stream's (x, y) normalised — structure only, not the reference's
+       * random numbers */
+      double d[3];
+      or_split_direction(seed, round, (uint64_t)i, d);
+      const double nrm = sqrt(d[0] * d[0] + d[1] * d[1]);
+      const double h = par[2] / 2.0;
+      const double ox = nrm > 0 ? h * d[0] / nrm : h, oy = nrm > 0 ? h * d[1] / nrm : 0.0;
+      ch[0] = par[0] - ox;
+      ch[1] = par[1] - oy;
+      par[0] = par[0] + ox;
+      par[1] = par[1] + oy;
+      par[2] = ch[2] = par[2] * sqrt(0.5);
+    }
+    ++c;
+    ++splits;
+  }
+  (void)base;
+  if (counts) counts[2] = splits;
+  free(cand);
+  free(used);
+  free(drop);
+  free(pairs);
+  free(a);
+  return c;
+}

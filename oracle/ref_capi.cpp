@@ -1,5 +1,5 @@
 // ref_capi.cpp — extern "C" wrappers around the REFERENCE's own hot-path code, compiled from
-// /root/reference/proj/src/{splat3d,image,loss,reconstruct}.cpp by oracle/build_ref.sh into
+// /root/reference/proj/src/{splat3d,image,loss,reconstruct,optimize}.cpp by oracle/build_ref.sh into
 // oracle/_ref/libisosplat_ref.so.  TEST INFRASTRUCTURE ONLY (checker / CPU baseline).
 //
 // The calls go through the reference's public API unchanged:
@@ -10,6 +10,7 @@
 //   isosplat::mse           image.hpp:40, image.cpp:50-58
 //   isosplat::loss / ssim / l1_term / ssim_gradient_wrt_second
 //                           loss.hpp:12-24, loss.cpp:112-190
+//   isosplat::adaptive_control (IsoParticle2D)   optimize.cpp:221-284
 // Exceptions (std::domain_error) become a non-zero return plus the message.
 #include <cstdint>
 #include <cstring>
@@ -21,6 +22,7 @@
 
 #include "isosplat/image.hpp"
 #include "isosplat/loss.hpp"
+#include "isosplat/optimize.hpp"
 #include "isosplat/splat3d.hpp"
 
 namespace {
@@ -143,6 +145,44 @@ int ref_image_loss(int w, int h, const double* f, const double* fhat, double lam
     return 0;
   } catch (const std::exception& e) {
     return report(e, err, errlen);
+  }
+}
+
+// adaptive_control on IsoParticle2D (optimize.cpp:221-284).  recs: n x 6 (mu.x mu.y sigma A0 A1
+// A2); params: prune_threshold, merge_distance_factor, merge_color_tol, split_sigma_max.
+// Returns the new count (written to out, capacity out_cap) or -1 on error.
+int64_t ref_adaptive_control_2d(int64_t n, const double* recs, const double* params,
+                                int max_particles, int channels, uint64_t seed, double* out,
+                                int64_t out_cap, char* err, int errlen) {
+  try {
+    std::vector<isosplat::IsoParticle2D> v(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) {
+      const double* r = recs + 6 * i;
+      v[i].mu = Eigen::Vector2d(r[0], r[1]);
+      v[i].sigma = r[2];
+      v[i].amplitude = {r[3], r[4], r[5]};
+    }
+    isosplat::AdaptiveControlParams a;
+    a.prune_threshold = params[0];
+    a.merge_distance_factor = params[1];
+    a.merge_color_tol = params[2];
+    a.split_sigma_max = params[3];
+    std::mt19937_64 rng(seed);
+    const auto res = isosplat::adaptive_control(std::move(v), a, max_particles, channels, rng);
+    const int64_t m = static_cast<int64_t>(res.size());
+    for (int64_t i = 0; i < m && i < out_cap; ++i) {
+      double* r = out + 6 * i;
+      r[0] = res[i].mu[0];
+      r[1] = res[i].mu[1];
+      r[2] = res[i].sigma;
+      r[3] = res[i].amplitude[0];
+      r[4] = res[i].amplitude[1];
+      r[5] = res[i].amplitude[2];
+    }
+    return m;
+  } catch (const std::exception& e) {
+    report(e, err, errlen);
+    return -1;
   }
 }
 

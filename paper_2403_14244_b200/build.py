@@ -24,7 +24,9 @@ REF_LIB = ORACLE_DIR / "_ref" / "libisosplat_ref.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["capi.cu", "k_preprocess.cu", "k_bin.cu", "k_sort.cu", "k_blend.cu",
-              "k_blend_bwd.cu", "k_ssim.cu", "k_adam.cu", "synth.cu"]
+              "k_blend_bwd.cu", "k_ssim.cu", "k_adam.cu", "k_adapt.cu", "synth.cu"]
+# per-file flags: adaptive control rounds every FP64 product/sum like the oracle (no FMA)
+CU_EXTRA = {"k_adapt.cu": ["-fmad=false"]}
 
 
 def _digest(paths) -> str:
@@ -42,7 +44,7 @@ def _run(cmd, cwd=None):
 
 def build_isg(force: bool = False) -> Path:
     srcs = [CSRC / s for s in CU_SOURCES]
-    deps = srcs + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "isg.h"]
+    deps = srcs + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "isg.h", Path(__file__)]
     stamp = PKG / ".libisg.sha256"
     digest = _digest(deps)
     if not force and LIB.exists() and stamp.exists() and stamp.read_text() == digest:
@@ -53,7 +55,8 @@ def build_isg(force: bool = False) -> Path:
     for s in srcs:
         o = objdir / (s.stem + ".o")
         _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fopenmp",
-              "-Xptxas", "-v", "-I", ROOT / "include", "-c", s, "-o", o])
+              "-Xptxas", "-v", *CU_EXTRA.get(s.name, []), "-I", ROOT / "include", "-c", s,
+              "-o", o])
         objs.append(o)
     _run([NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC,-fopenmp", "-o", LIB, *objs,
           "-ldl", "-lgomp"])

@@ -1023,6 +1023,80 @@ isg_status isg_restore(isg_ctx* ctx) {
   return ISG_OK;
 }
 
+isg_status isg_adaptive_control(isg_ctx* ctx, const isg_adapt_params* prm, uint64_t seed,
+                                uint64_t round, isg_adapt_result* out) {
+  if (!ctx || !prm) return ISG_E_ARG;
+  // AdaptiveControlParams::validate (include/isosplat/optimize.hpp:21-27)
+  if (!(prm->prune_threshold >= 0.0)) return fail(ctx, ISG_E_ARG, "prune_threshold: must be >= 0");
+  if (!(prm->merge_distance_factor > 0.0))
+    return fail(ctx, ISG_E_ARG, "merge_distance_factor: must be > 0");
+  if (!(prm->merge_color_tol >= 0.0)) return fail(ctx, ISG_E_ARG, "merge_color_tol: must be >= 0");
+  if (!(prm->split_sigma_max > 0.0)) return fail(ctx, ISG_E_ARG, "split_sigma_max: must be > 0");
+  cudaSetDevice(ctx->device);
+  isg_status s = isg_synchronize(ctx);
+  if (s != ISG_OK) return s;
+  const int64_t n = ctx->n;
+  const int64_t cap = prm->max_particles > 0 ? prm->max_particles : 2 * n;
+  if (cap > 0xFFFFFFF0ll) return fail(ctx, ISG_E_ARG, "max_particles: too large");
+  // grow the scene buffers (preserving the splats) so the appended split children fit
+  if (cap > ctx->n_alloc) {
+    float4 *ms_keep = nullptr, *co_keep = nullptr;
+    ISG_CUDA(cudaMalloc(&ms_keep, sizeof(float4) * std::max<int64_t>(n, 1)));
+    ISG_CUDA(cudaMalloc(&co_keep, sizeof(float4) * std::max<int64_t>(n, 1)));
+    if (n) {
+      ISG_CUDA(cudaMemcpyAsync(ms_keep, ctx->ms, sizeof(float4) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+      ISG_CUDA(cudaMemcpyAsync(co_keep, ctx->co, sizeof(float4) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    ISG_CUDA(cudaStreamSynchronize(ctx->stream));
+    s = ensure_scene(ctx, cap);
+    if (s == ISG_OK && n) {
+      cudaMemcpyAsync(ctx->ms, ms_keep, sizeof(float4) * n, cudaMemcpyDeviceToDevice, ctx->stream);
+      cudaMemcpyAsync(ctx->co, co_keep, sizeof(float4) * n, cudaMemcpyDeviceToDevice, ctx->stream);
+      cudaStreamSynchronize(ctx->stream);
+    }
+    cudaFree(ms_keep);
+    cudaFree(co_keep);
+    if (s != ISG_OK) return s;
+  }
+  if ((s = ensure_sort_scratch(ctx, std::max(ctx->key_cap, ctx->n_alloc))) != ISG_OK) return s;
+  float4 *ms_tmp = nullptr, *co_tmp = nullptr;
+  ISG_CUDA(cudaMalloc(&ms_tmp, sizeof(float4) * ctx->n_alloc));
+  ISG_CUDA(cudaMalloc(&co_tmp, sizeof(float4) * ctx->n_alloc));
+  isg::AdaptParamsDev p{prm->prune_threshold, prm->merge_distance_factor, prm->merge_color_tol,
+                        prm->split_sigma_max, cap};
+  isg::AdaptCounts c{};
+  const cudaError_t e = isg::adaptive_control(ctx->ms, ctx->co, n, p, seed, round, ctx->sort,
+                                              ctx->depth, ctx->order, ms_tmp, co_tmp, &c,
+                                              ctx->stream, &ctx->launches);
+  cudaFree(ms_tmp);  // the buffers not in use after the (possible) swaps
+  cudaFree(co_tmp);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "adaptive_control");
+  // the optimizer restarts on the new set (the reference clears its momentum, optimize.cpp:344)
+  ctx->n = c.n_after;
+  if (ctx->n > 0) {
+    ISG_CUDA(cudaMemsetAsync(ctx->m, 0, sizeof(float4) * 2 * ctx->n, ctx->stream));
+    ISG_CUDA(cudaMemsetAsync(ctx->v, 0, sizeof(float4) * 2 * ctx->n, ctx->stream));
+  }
+  ctx->adam_t = 0;
+  ctx->snap_valid = false;
+  ctx->pending = false;
+  ctx->grad3d_valid = false;
+  ctx->have_frame = false;
+  ISG_CUDA(cudaMemsetAsync(ctx->loss, 0, sizeof(double) * 2, ctx->stream));
+  ISG_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (ctx->key_cap < std::max<int64_t>(6 * ctx->n, 1 << 20)) {
+    if ((s = ensure_keys(ctx, std::max<int64_t>(6 * ctx->n, 1 << 20))) != ISG_OK) return s;
+  }
+  if (out) {
+    out->n_before = c.n_before;
+    out->n_pruned = c.n_pruned;
+    out->n_merged = c.n_merged;
+    out->n_split = c.n_split;
+    out->n_after = c.n_after;
+  }
+  return ISG_OK;
+}
+
 isg_status isg_set_loss(isg_ctx* ctx, int kind, float lambda) {
   if (!ctx) return ISG_E_ARG;
   if (kind != ISG_LOSS_L2 && kind != ISG_LOSS_L1_DSSIM)

@@ -158,6 +158,22 @@ void launch_project_adam(float4* ms, float4* co, int64_t n, const FrameParams& f
 void launch_adam(float4* ms, float4* co, int64_t n, const float4* grad3d, float4* m, float4* v,
                  const AdamParams& ap, unsigned long long* skipped, cudaStream_t st);
 
+// ---- adaptive control (k_adapt.cu) ----------------------------------------------------------
+struct AdaptParamsDev {
+  double prune_threshold, merge_distance_factor, merge_color_tol, split_sigma_max;
+  int64_t max_particles;  // effective cap
+};
+struct AdaptCounts {
+  int64_t n_before, n_pruned, n_merged, n_split, n_after;
+};
+// Prune -> merge -> split of the n splats in (ms, co), in place; ms/co may be swapped with
+// ms_tmp/co_tmp (all four hold >= max(n, max_particles) records).  keys/vals: two ping-pong
+// pairs of >= n words; sort: radix scratch for >= n items.  Synchronises the stream.
+cudaError_t adaptive_control(float4*& ms, float4*& co, int64_t n, const AdaptParamsDev& p,
+                             uint64_t seed, uint64_t round, SortScratch& sort, uint32_t* keys[2],
+                             uint32_t* vals[2], float4* ms_tmp, float4* co_tmp,
+                             AdaptCounts* counts, cudaStream_t st, int64_t* launches);
+
 // ---- parity hook -------------------------------------------------------------------------
 void launch_debug_keys(const uint2* ranges, const uint2* sorted, const float4* ms,
                        const FrameParams& fp, uint64_t* keys, uint32_t* gids, cudaStream_t st);

@@ -9,6 +9,9 @@ Follows fit_impl (/root/reference/proj/src/optimize.cpp:298-358) for isotropic 3
     snapshot, rate_scale halved) when it would increase the loss (:327-340) — the recorded loss
     then never increases;
     non-finite loss -> DivergenceError(epoch, offending particle) (:319, :330-332)
+  adapt=True: adaptive control (prune / merge / split, k_adapt.cu) every adapt_every epochs,
+    then the loss is re-evaluated (:341-351); the particle cap is max(max_particles, n0), or
+    2 n0 when max_particles is 0 (:309-312)
   history: loss_history, particle_count_history, epoch, rate_scale, skipped_updates
 
 Outputs like run_fit_typed (tools/isosplat_main.cpp:116-137): particles.ispl|.json (metadata
@@ -28,7 +31,7 @@ from typing import List, Optional, Protocol, Sequence
 import numpy as np
 
 from . import scene_io
-from .isg import LOSS_L1_DSSIM, LOSS_L2, AdamConfig, DomainError, RenderOptions
+from .isg import LOSS_L1_DSSIM, LOSS_L2, AdamConfig, AdaptParams, DomainError, RenderOptions
 
 
 class DivergenceError(RuntimeError):
@@ -49,6 +52,10 @@ class FitConfig3D:
     backoff: bool = False  # reject-and-halve steps that increase the loss
     loss: str = "l2"       # "l2" (mse) or "l1_dssim" ((1-lam) L1 + lam (1 - SSIM), loss.cpp:184)
     lam: float = 0.2       # FitConfig::lambda (the paper's 0.2)
+    adapt: bool = False    # adaptive control every adapt_every epochs (optimize.cpp:341-351)
+    adapt_every: int = 100
+    adapt_params: AdaptParams = field(default_factory=AdaptParams)
+    rng_seed: int = 0
 
     def validate(self):  # particles.hpp:73-83 style
         if self.epochs < 0:
@@ -57,6 +64,19 @@ class FitConfig3D:
             raise ValueError("loss: must be 'l2' or 'l1_dssim'")
         if not 0.0 <= self.lam <= 1.0:
             raise ValueError("lambda: must be in [0,1]")
+        if self.adapt_every < 1:
+            raise ValueError("adapt_every: must be >= 1")
+        a = self.adapt_params  # AdaptiveControlParams::validate (optimize.hpp:21-27)
+        if not a.prune_threshold >= 0:
+            raise ValueError("prune_threshold: must be >= 0")
+        if not a.merge_distance_factor > 0:
+            raise ValueError("merge_distance_factor: must be > 0")
+        if not a.merge_color_tol >= 0:
+            raise ValueError("merge_color_tol: must be >= 0")
+        if not a.split_sigma_max > 0:
+            raise ValueError("split_sigma_max: must be > 0")
+        if a.max_particles < 0:
+            raise ValueError("max_particles: must be >= 0")
         for name in ("lr_mu", "lr_sigma", "lr_color", "lr_opacity"):
             if not getattr(self.adam, name) > 0:
                 raise ValueError(f"{name}: must be > 0")
@@ -86,6 +106,7 @@ class FitBackend(Protocol):
     def snapshot(self) -> None: ...
     def restore(self) -> None: ...
     def skipped_updates(self) -> int: ...
+    def adaptive_control(self, params: AdaptParams, seed: int, round_: int) -> dict: ...
 
 
 def offending_particle(params: np.ndarray) -> int:
@@ -112,6 +133,10 @@ def fit(be: FitBackend, config: FitConfig3D) -> FitState3D:
         raise ValueError("init_particles: must be nonempty")
     st = FitState3D()
     w = 1.0 / be.n_views
+    n0 = be.count()
+    a = config.adapt_params  # particle cap, optimize.cpp:309-312
+    cap = max(a.max_particles, n0) if a.max_particles > 0 else 2 * n0
+    adapt_round = 0
     current = _batch_loss(be, w, 0)
     st.initial_loss = current
     for e in range(config.epochs):
@@ -134,6 +159,12 @@ def fit(be: FitBackend, config: FitConfig3D) -> FitState3D:
                 current = loss
         except DomainError:
             raise DivergenceError(e, offending_particle(be.params())) from None
+        if config.adapt and (e + 1) % config.adapt_every == 0:
+            be.adaptive_control(AdaptParams(a.prune_threshold, a.merge_distance_factor,
+                                            a.merge_color_tol, a.split_sigma_max, cap),
+                                config.rng_seed, adapt_round)
+            adapt_round += 1
+            current = _batch_loss(be, w, e)
         st.loss_history.append(current)
         st.particle_count_history.append(be.count())
         st.epoch = e + 1
@@ -202,3 +233,6 @@ class RendererBackend:
 
     def skipped_updates(self) -> int:
         return int(self.r.stats()["skipped_updates"])
+
+    def adaptive_control(self, params: AdaptParams, seed: int, round_: int) -> dict:
+        return self.r.adaptive_control(params, seed, round_)

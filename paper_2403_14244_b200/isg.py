@@ -38,6 +38,18 @@ class CameraT(C.Structure):
                 ("cx", C.c_float), ("cy", C.c_float), ("width", C.c_int32), ("height", C.c_int32)]
 
 
+class AdaptParamsT(C.Structure):
+    """isg_adapt_params: AdaptiveControlParams (optimize.hpp:14-28) for 3D splats."""
+    _fields_ = [("prune_threshold", C.c_double), ("merge_distance_factor", C.c_double),
+                ("merge_color_tol", C.c_double), ("split_sigma_max", C.c_double),
+                ("max_particles", C.c_int64)]
+
+
+class AdaptResultT(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("n_before", "n_pruned", "n_merged", "n_split",
+                                         "n_after")]
+
+
 class StatsT(C.Structure):
     _fields_ = [(n, C.c_int64) for n in ("n_gaussians", "n_visible", "n_keys", "key_capacity",
                                          "n_tiles", "adam_steps", "skipped_updates",
@@ -83,6 +95,8 @@ def lib() -> C.CDLL:
         "isg_snapshot": ([P], C.c_int),
         "isg_restore": ([P], C.c_int),
         "isg_set_loss": ([P, C.c_int, F], C.c_int),
+        "isg_adaptive_control": ([P, C.POINTER(AdaptParamsT), C.c_uint64, C.c_uint64,
+                                  C.POINTER(AdaptResultT)], C.c_int),
         "isg_image_loss_device": ([P, I32, I32, P, P, F, C.POINTER(C.c_double), P], C.c_int),
         "isg_nccl_get_unique_id": ([P], C.c_int),
         "isg_nccl_init": ([P, C.c_int, C.c_int, P], C.c_int),
@@ -112,7 +126,7 @@ C_ABI_SYMBOLS = (
     "isg_get_scene", "isg_render", "isg_render_device", "isg_loss_backward",
     "isg_loss_backward_device", "isg_read_loss", "isg_zero_grads", "isg_get_grads",
     "isg_grads_device", "isg_adam_step", "isg_last_step_loss", "isg_eval_loss", "isg_snapshot",
-    "isg_restore", "isg_set_loss", "isg_image_loss_device", "isg_nccl_get_unique_id",
+    "isg_restore", "isg_set_loss", "isg_image_loss_device", "isg_adaptive_control", "isg_nccl_get_unique_id",
     "isg_nccl_init",
     "isg_nccl_detach", "isg_debug_bins", "isg_debug_pixel_state", "isg_set_binning",
     "isg_profile_enable",
@@ -183,6 +197,18 @@ class RenderOptions:
     background: tuple = (0.0, 0.0, 0.0)
     threads: int = 1
     t_min: float = 1e-5
+
+
+@dataclass
+class AdaptParams:
+    """AdaptiveControlParams (optimize.hpp:14-28); split_sigma_max in world units (the
+    reference's 15 px is a 2D pixel scale).  max_particles: effective cap (0: twice the
+    current count)."""
+    prune_threshold: float = 1e-3
+    merge_distance_factor: float = 0.5
+    merge_color_tol: float = 0.05
+    split_sigma_max: float = float("inf")
+    max_particles: int = 0
 
 
 @dataclass
@@ -393,6 +419,18 @@ class Renderer:
             self._h, int(width), int(height), C.c_void_p(fhat_ptr), C.c_void_p(target_ptr),
             float(weight), C.byref(v), C.c_void_p(dldc_ptr) if dldc_ptr else None))
         return v.value
+
+    def adaptive_control(self, params: "AdaptParams", seed: int = 0, round_: int = 0) -> dict:
+        """Prune / merge / split the resident splat set (optimize.cpp:221-284); returns the
+        counts.  Adam state restarts."""
+        p = AdaptParamsT(params.prune_threshold, params.merge_distance_factor,
+                         params.merge_color_tol, params.split_sigma_max,
+                         int(params.max_particles))
+        res = AdaptResultT()
+        _check(self._h, lib().isg_adaptive_control(self._h, C.byref(p), int(seed), int(round_),
+                                                   C.byref(res)))
+        self.n = int(res.n_after)
+        return {k: int(getattr(res, k)) for k, _ in AdaptResultT._fields_}
 
     def last_step_loss(self) -> float:
         v = C.c_double()

@@ -83,6 +83,20 @@ class OracleFitBackend:
     def skipped_updates(self):
         return self.skipped
 
+    def adaptive_control(self, prm, seed, round_):
+        rec = np.concatenate([self.ms, self.co], 1).astype(np.float64)
+        out, counts = O.adaptive_control(
+            rec, O.AdaptParams(prm.prune_threshold, prm.merge_distance_factor,
+                               prm.merge_color_tol, prm.split_sigma_max, prm.max_particles),
+            dims=3, seed=seed, round_=round_)
+        self.ms = np.ascontiguousarray(out[:, :4], np.float32)
+        self.co = np.ascontiguousarray(out[:, 4:], np.float32)
+        self.m = np.zeros((self.ms.shape[0], 8), np.float32)
+        self.v = np.zeros_like(self.m)
+        self.g = np.zeros_like(self.m)
+        self.t = 0
+        return dict(zip(("n_pruned", "n_merged", "n_split"), counts))
+
 
 def problem(n=N, views=VIEWS):
     ms, co = isg.synth_scene(n, W, H, seed=2403)
@@ -134,6 +148,19 @@ def test_fit_l1_dssim_decreases_loss():
     assert st.loss_history[-1] < st.initial_loss
 
 
+ADAPT_CFG = dict(epochs=6, adapt=True, adapt_every=2, rng_seed=5,
+                 adapt_params=isg.AdaptParams(0.02, 1.0, 0.2, 0.01, 0))
+
+
+def test_fit_with_adaptive_control_changes_count():
+    ms, co, cams, targets = problem()
+    cfg = FitConfig3D(**ADAPT_CFG)
+    st = fit(OracleFitBackend(ms, co, cams, targets, cfg), cfg)
+    assert len(set(st.particle_count_history)) > 1
+    assert max(st.particle_count_history) <= 2 * N
+    assert np.isfinite(st.final_loss)
+
+
 def test_offending_particle_and_config_validation():
     p = np.tile(np.array([0, 0, 1, 0.1, 0.5, 0.5, 0.5, 0.5]), (4, 1))
     assert offending_particle(p) == -1
@@ -148,6 +175,10 @@ def test_offending_particle_and_config_validation():
         FitConfig3D(loss="l1_dssim", lam=1.5).validate()
     with pytest.raises(ValueError, match="loss"):
         FitConfig3D(loss="ssim").validate()
+    with pytest.raises(ValueError, match="adapt_every"):
+        FitConfig3D(adapt_every=0).validate()
+    with pytest.raises(ValueError, match="merge_distance_factor"):
+        FitConfig3D(adapt_params=isg.AdaptParams(merge_distance_factor=0.0)).validate()
 
 
 def test_outputs(tmp_path):
@@ -201,6 +232,17 @@ def test_gpu_fit_l1_dssim_matches_oracle_trajectory():
     assert st_g.initial_loss == pytest.approx(st_o.initial_loss, rel=1e-5)
     np.testing.assert_allclose(st_g.loss_history, st_o.loss_history, rtol=1e-3)
     assert st_g.final_loss < st_g.initial_loss
+
+
+@pytest.mark.gpu
+def test_gpu_fit_with_adaptive_control_matches_oracle():
+    ms, co, cams, targets = problem()
+    cfg = FitConfig3D(**ADAPT_CFG)
+    st_o = fit(OracleFitBackend(ms, co, cams, targets, cfg), cfg)
+    st_g = fit(_gpu_backend(ms, co, cams, targets, cfg), cfg)
+    # the counts agree exactly while the parameters stay within the trajectory tolerance
+    assert st_g.particle_count_history == st_o.particle_count_history
+    np.testing.assert_allclose(st_g.loss_history, st_o.loss_history, rtol=2e-3)
 
 
 @pytest.mark.gpu
