@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from dataclasses import dataclass, field
 from pathlib import Path
 from typing import Optional, Sequence
@@ -17,7 +18,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libisg.so"
+LIB_PATH = Path(os.environ.get("ISG_LIB_PATH", _PKG / "libisg.so"))  # override: A/B builds
 
 ISG_OK, ISG_E_DOMAIN, ISG_E_ARG, ISG_E_CUDA, ISG_E_OOM, ISG_E_OVERFLOW, ISG_E_NCCL, ISG_E_STATE = range(8)
 LOSS_L2, LOSS_L1_DSSIM = 0, 1  # ISG_LOSS_* (include/isg.h)
