@@ -34,16 +34,17 @@ constexpr int kBatch = 64;  // records staged per batch (one per thread)
 struct BwdPair {
   float2 G0, G1, G2;  // dL/dC
   float2 T;           // transmittance before the most recently processed (later) entry
-  float2 A0, A1, A2;  // colour behind, normalised
+  float2 GA;          // G . A, A = colour behind (normalised): only its projection on G is used
   int np0, np1;       // list entries the forward processed for each pixel
 };
 
 __device__ __forceinline__ float2 bc(float v) { return make_float2(v, v); }
 
 // acc: [0] sum go*dx, [1] sum go*dy, [2] sum go*r2 (scaled per entry into du, dv, dsigma2d),
-// [3] dopacity, [4..6] drgb;  go = dL/dalpha * g; summed per lane of the pair.  An inactive
-// pixel gets e = 0, hence a = 0: T and A stay exactly unchanged and every contribution is an
-// exact zero.
+// [3] dopacity, [4..6] drgb;  go = dL/dalpha * g; summed per lane of the pair.
+//   dL/da_k = T_k G.(c_k - A_k);  A <- a c + (1 - a) A  =>  G.A <- G.A + a (G.c - G.A)
+// so the colour behind is carried as the single scalar G.A per pixel.  An inactive pixel gets
+// e = 0, hence a = 0: T and G.A stay exactly unchanged and every contribution is an exact zero.
 __device__ __forceinline__ void bwd_pair(BwdPair& p, bool act0, bool act1, int j, float2 dx,
                                          float dy, float2 r2, const float4 g, const float4 c,
                                          float2 acc[8]) {
@@ -54,18 +55,14 @@ __device__ __forceinline__ void bwd_pair(BwdPair& p, bool act0, bool act1, int j
   const float2 Tr = __fmul2_rn(p.T, make_float2(fast_rcp(om.x), fast_rcp(om.y)));
   const float2 Tk = make_float2(j == p.np0 - 1 ? p.T.x : Tr.x, j == p.np1 - 1 ? p.T.y : Tr.y);
   p.T = Tk;
-  const float2 d0 = __fadd2_rn(bc(c.x), make_float2(-p.A0.x, -p.A0.y));
-  const float2 d1 = __fadd2_rn(bc(c.y), make_float2(-p.A1.x, -p.A1.y));
-  const float2 d2 = __fadd2_rn(bc(c.z), make_float2(-p.A2.x, -p.A2.y));
-  const float2 gd = __ffma2_rn(p.G2, d2, __ffma2_rn(p.G1, d1, __fmul2_rn(p.G0, d0)));
+  const float2 Gc = __ffma2_rn(p.G2, bc(c.z), __ffma2_rn(p.G1, bc(c.y), __fmul2_rn(p.G0, bc(c.x))));
+  const float2 gd = __fadd2_rn(Gc, make_float2(-p.GA.x, -p.GA.y));  // G.(c - A)
+  p.GA = __ffma2_rn(a, gd, p.GA);
   const float2 dLda = __fmul2_rn(Tk, gd);
   const float2 Ta = __fmul2_rn(Tk, a);
   acc[4] = __ffma2_rn(p.G0, Ta, acc[4]);
   acc[5] = __ffma2_rn(p.G1, Ta, acc[5]);
   acc[6] = __ffma2_rn(p.G2, Ta, acc[6]);
-  p.A0 = __ffma2_rn(a, d0, p.A0);
-  p.A1 = __ffma2_rn(a, d1, p.A1);
-  p.A2 = __ffma2_rn(a, d2, p.A2);
   const float2 go = __fmul2_rn(dLda, e);
   acc[3] = __fadd2_rn(acc[3], go);
   acc[0] = __ffma2_rn(go, dx, acc[0]);
@@ -169,9 +166,8 @@ __global__ void __launch_bounds__(kBT) k_blend_bwd(
     s.T = make_float2(T[0], T[1]);
     s.np0 = np[0];
     s.np1 = np[1];
-    s.A0 = bc(fp.bg[0]);
-    s.A1 = bc(fp.bg[1]);
-    s.A2 = bc(fp.bg[2]);
+    s.GA = make_float2(G[0][0] * fp.bg[0] + G[0][1] * fp.bg[1] + G[0][2] * fp.bg[2],
+                       G[1][0] * fp.bg[0] + G[1][1] * fp.bg[1] + G[1][2] * fp.bg[2]);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -242,7 +238,9 @@ __global__ void __launch_bounds__(kBT) k_blend_bwd(
       const float2 dy = __fadd2_rn(PY, bc(-g.y));
       // r2 in scalar: ptxas would contract a packed mul.rn + add.rn into FFMA2 (one rounding),
       // and the 3-sigma test must round exactly like the oracle's (and the forward's)
-      const float ax0 = __fmul_rn(dx.x, dx.x), ax1 = __fmul_rn(dx.y, dx.y);
+      // dx^2 as fma(dx, dx, -0) = round(dx^2): one FFMA2 that ptxas does not contract with
+      // the following add (a packed mul.rn + add.rn pair it would)
+      const float2 ax = __ffma2_rn(dx, dx, bc(-0.0f));
       float2 acc2[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) acc2[k] = bc(0.0f);
@@ -250,7 +248,7 @@ __global__ void __launch_bounds__(kBT) k_blend_bwd(
       for (int k = 0; k < 2; ++k) {
         const float dyk = k ? dy.y : dy.x;
         const float ay = __fmul_rn(dyk, dyk);
-        const float2 r2 = make_float2(__fadd_rn(ax0, ay), __fadd_rn(ax1, ay));
+        const float2 r2 = __fadd2_rn(ax, bc(ay));
         const bool act0 = has && j < P[k].np0 && !(r2.x > g.z);
         const bool act1 = has && j < P[k].np1 && !(r2.y > g.z);
         bwd_pair(P[k], act0, act1, j, dx, dyk, r2, g, c, acc2);
@@ -259,12 +257,12 @@ __global__ void __launch_bounds__(kBT) k_blend_bwd(
 #pragma unroll
       for (int k = 0; k < 8; ++k) acc[k] = acc2[k].x + acc2[k].y;
       // kernels.hpp:219-220: dg/du = g 2 dx / s^2, dg/ds = g 2 r^2 / s^3, times opacity
-      const float inv_s2 = g.w * -kLn2;     // 1 / sigma2d^2
-      const float k2 = 2.0f * c.w * inv_s2;  // 2 o / s^2
-      acc[0] *= k2;
-      acc[1] *= k2;
-      acc[2] *= k2 * fast_sqrt(inv_s2);      // 2 o / s^3
-      const float y = reduce_scatter8_half(acc);
+      // lane l ends with value (l >> 1) & 7; du, dv scale by 2 o / s^2, dsigma2d by 2 o / s^3
+      const float inv_s2 = g.w * -kLn2;  // 1 / sigma2d^2
+      const int vi = (l16 >> 1) & 7;
+      const float k2 = 2.0f * c.w * inv_s2;
+      const float scale = vi < 2 ? k2 : (vi == 2 ? k2 * fast_sqrt(inv_s2) : 1.0f);
+      const float y = reduce_scatter8_half(acc) * scale;
       if (has && (l16 & 1) == 0) s_part[q][l16 >> 1][jj] = y;
     }
     __syncthreads();
