@@ -199,6 +199,8 @@ def run_isg(args):
     r.set_stream(stream.cuda_stream)
     if args.loss == "l1_dssim":
         r.set_loss(isg.LOSS_L1_DSSIM, 0.2)
+    if args.binning == "bucket":
+        r.set_binning(r.BINNING_TILE_BUCKET)
     opts = isg.RenderOptions(t_min=T_MIN)
     cfg = isg.AdamConfig()
     my_views = [rank * views_per_rank + i for i in range(views_per_rank)]
@@ -365,6 +367,7 @@ def run_isg(args):
         "config": {"workload": desc, "config": args.config, "n_gaussians": n, "width": W,
                    "height": H, "views_per_step": step_views, "t_min": T_MIN,
                    "loss": "L2 (mse)" if args.loss == "l2" else "0.8 L1 + 0.2 D-SSIM",
+                   "binning": args.binning,
                    "parallelism": f"dp{world} (views sharded, scene replicated)",
                    "l2": "no flush: per-step working set (scene+Adam state 96 MB, keys "
                          f"{st['n_keys'] * 16 / 1e6:.0f} MB, images 50 MB) exceeds the 126 MB L2"},
@@ -394,6 +397,8 @@ def main():
     ap.add_argument("--impl", default="isg", choices=["isg", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--binning", default="radix", choices=["radix", "bucket"],
+                    help="binning strategy (identical tile lists)")
     ap.add_argument("--loss", default="l2", choices=["l2", "l1_dssim"],
                     help="training loss (BASELINE configs use L2; l1_dssim = the paper's loss)")
     args = ap.parse_args()

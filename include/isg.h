@@ -200,10 +200,10 @@ isg_status isg_debug_bins(isg_ctx* ctx, uint64_t* keys, uint32_t* vals, int64_t*
 isg_status isg_debug_pixel_state(isg_ctx* ctx, float* t_last, uint32_t* n_proc);
 
 /* ---- binning strategy (both produce bit-identical tile lists) ----------------------------
- * TILE_BUCKET (default): per-tile counters + bucket fill + per-tile bitonic sort by
- *   (depth bits, splat index) in shared memory.
- * RADIX: onesweep LSD radix sort of (depth, splat), tile-key emission in depth order and a
- *   stable onesweep radix sort of (tile, pair). */
+ * TILE_BUCKET: per-tile counters + bucket fill + per-tile bitonic sort by (depth bits, splat
+ *   index) in shared memory.
+ * RADIX (default): onesweep LSD radix sort of (depth, splat), tile-key emission in depth order
+ *   and a stable onesweep radix sort of (tile, pair). */
 #define ISG_BINNING_TILE_BUCKET 0
 #define ISG_BINNING_RADIX 1
 isg_status isg_set_binning(isg_ctx* ctx, int mode);

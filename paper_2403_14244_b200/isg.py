@@ -455,7 +455,7 @@ class Renderer:
     BINNING_TILE_BUCKET, BINNING_RADIX = 0, 1
 
     def set_binning(self, mode: int):
-        """0 = tile-bucket (default), 1 = onesweep radix; bit-identical tile lists."""
+        """0 = tile-bucket, 1 = onesweep radix (default); bit-identical tile lists."""
         _check(self._h, lib().isg_set_binning(self._h, int(mode)))
 
     # -- stage timing -----------------------------------------------------------------------
