@@ -239,6 +239,20 @@ def run_isg(args):
     for _ in range(max(args.warmup, 3)):
         step()
     r.synchronize()
+    step_eager = step
+    graph = None
+    if not args.no_graph:
+        # the whole step (every view's frame + backward, the all-reduce, Adam) as one CUDA
+        # graph launch; a replay re-runs every kernel on the live buffers
+        r.graph_begin()
+        step_eager()
+        graph = r.graph_end()
+
+        def step():
+            graph.launch()
+        for _ in range(2):
+            step()
+        r.synchronize()
 
     def barrier():
         if world > 1:
@@ -248,6 +262,7 @@ def run_isg(args):
     # ---- device-resident timed region ----------------------------------------------------
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     barrier()
+    launches_t0 = r.stats()["kernel_launches"]
     with ClockSampler(local) as clocks:
         ev[0].record(stream)
         for i in range(args.steps):
@@ -263,14 +278,14 @@ def run_isg(args):
         total_ms = float(tt.item())
     ms_per_step = total_ms / args.steps
     value = (step_views if train else 1 * world) / (ms_per_step / 1e3)
-    launches_before = r.stats()["kernel_launches"]
+    launches_timed = r.stats()["kernel_launches"] - launches_t0
 
-    # ---- stage timing (separate pass, events per kernel) ----------------------------------
+    # ---- stage timing (separate pass, events per kernel, kernel by kernel) ----------------
     r.profile(True)
     r.profile_read()
     prof_steps = max(3, min(args.steps, 10))
     for _ in range(prof_steps):
-        step()
+        step_eager()
     prof = r.profile_read()
     r.profile(False)
     launches_per_step = None
@@ -368,14 +383,16 @@ def run_isg(args):
                    "height": H, "views_per_step": step_views, "t_min": T_MIN,
                    "loss": "L2 (mse)" if args.loss == "l2" else "0.8 L1 + 0.2 D-SSIM",
                    "binning": args.binning,
+                   "launch": "eager" if args.no_graph else "cuda_graph (one graph launch per step)",
                    "parallelism": f"dp{world} (views sharded, scene replicated)",
                    "l2": "no flush: per-step working set (scene+Adam state 96 MB, keys "
                          f"{st['n_keys'] * 16 / 1e6:.0f} MB, images 50 MB) exceeds the 126 MB L2"},
         "e2e": {"value": e2e_value, "unit": "iters/s" if train else "frames/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_step},
-        "gpu_launches": int(round(launches_per_step * args.steps)) if launches_per_step else None,
-        "gpu_launches_per_step": launches_per_step,
+        "gpu_launches": int(launches_timed),
+        "gpu_launches_per_step": launches_timed / args.steps,
+        "e2e_gpu_launches_per_step": launches_per_step,
         "roofline": roof,
         "cpu_baseline": cpu,
         "clocks": clk,
@@ -397,6 +414,8 @@ def main():
     ap.add_argument("--impl", default="isg", choices=["isg", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="launch the device-resident step kernel by kernel (no CUDA graph)")
     ap.add_argument("--binning", default="radix", choices=["radix", "bucket"],
                     help="binning strategy (identical tile lists)")
     ap.add_argument("--loss", default="l2", choices=["l2", "l1_dssim"],

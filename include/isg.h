@@ -182,6 +182,20 @@ typedef struct {
 isg_status isg_adaptive_control(isg_ctx* ctx, const isg_adapt_params* params, uint64_t seed,
                                 uint64_t round, isg_adapt_result* out);
 
+/* ---- CUDA graphs ------------------------------------------------------------------------
+ * Capture the asynchronous calls of one train step (isg_loss_backward_device per view +
+ * isg_adam_step, or isg_render_device) on the context stream and replay them with one launch.
+ * Capture after a warm-up step (buffers must not grow inside the capture).  Synchronising
+ * entry points return ISG_E_STATE while capturing.  The Adam step counter lives on the device,
+ * so replays apply the correct bias corrections; the learning rates, cameras and device
+ * pointers are the captured ones.  A replayed frame that overflows the key capacity is skipped
+ * and reported by the next synchronising call (re-capture after it grows the buffers). */
+typedef struct isg_graph isg_graph;
+isg_status isg_graph_begin(isg_ctx* ctx);
+isg_status isg_graph_end(isg_ctx* ctx, isg_graph** out);
+isg_status isg_graph_launch(isg_ctx* ctx, isg_graph* graph);
+void isg_graph_destroy(isg_graph* graph);
+
 /* ---- multi-GPU (one process per GPU, views sharded, NCCL all-reduce before Adam) -------- */
 /* NCCL is resolved at run time (dlopen libnccl.so.2, the copy torch already loaded if any). */
 isg_status isg_nccl_get_unique_id(void* out_128_bytes);

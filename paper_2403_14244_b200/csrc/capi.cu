@@ -101,6 +101,7 @@ struct isg_ctx {
   uint32_t* sc = nullptr;
   unsigned long long* total = nullptr;     // [0] total keys, [1] skipped updates
   double* loss = nullptr;                  // [0] accumulated, [1] last view, [2] last step
+  isg::AdamState* adam_state = nullptr;    // [0] live, [1] snapshot (step counter on device)
   // pinned readback
   uint32_t* h_sc = nullptr;
   unsigned long long* h_total = nullptr;
@@ -126,6 +127,10 @@ struct isg_ctx {
   void* nccl_comm = nullptr;
   int nranks = 1, rank = 0;
 
+  // CUDA-graph capture of the context stream (isg_graph_*)
+  bool capturing = false;
+  int64_t capture_launches0 = 0;
+
   // profiling
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -150,7 +155,7 @@ struct StageScope {
   int stage;
   cudaEvent_t a = nullptr;
   StageScope(isg_ctx* c_, int s) : c(c_), stage(s) {
-    if (c->prof) {
+    if (c->prof && !c->capturing) {
       a = prof_event(c);
       cudaEventRecord(a, c->stream);
     }
@@ -174,6 +179,13 @@ isg_status fail(isg_ctx* c, isg_status s, const std::string& msg) {
   if (c) c->err = msg;
   return s;
 }
+
+// Host-synchronising entry points cannot run inside a stream capture.
+#define ISG_NO_CAPTURE(name)                                                               \
+  do {                                                                                     \
+    if (ctx->capturing)                                                                    \
+      return fail(ctx, ISG_E_STATE, name ": synchronising call inside isg_graph_begin/end"); \
+  } while (0)
 
 isg_status cuda_fail(isg_ctx* c, cudaError_t e, const char* where) {
   return fail(c, e == cudaErrorMemoryAllocation ? ISG_E_OOM : ISG_E_CUDA,
@@ -374,10 +386,7 @@ isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out) {
   const int64_t words =
       (radix ? isg::scan_emit_scratch_words(n) : isg::fill_scratch_words(n)) + 1;
   ISG_CUDA(cudaMemsetAsync(ctx->scan_scratch, 0, sizeof(unsigned long long) * words, st));
-  if (radix)
-    ISG_CUDA(cudaMemsetAsync(ctx->ranges, 0, sizeof(uint2) * fp.n_tiles, st));
-  else
-    ISG_CUDA(cudaMemsetAsync(ctx->tile_cnt, 0, sizeof(uint32_t) * fp.n_tiles, st));
+  if (!radix) ISG_CUDA(cudaMemsetAsync(ctx->tile_cnt, 0, sizeof(uint32_t) * fp.n_tiles, st));
   }
   {
   ISG_STAGE(ST_PREPROCESS);
@@ -409,7 +418,7 @@ isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out) {
     }
     ISG_STAGE(ST_RANGES);
     isg::launch_ranges(ctx->tkey[ctx->tile_buf], ctx->tval[ctx->tile_buf], ctx->emit_gid,
-                       ctx->sc + 0, ctx->key_cap, ctx->ranges, ctx->sorted, st);
+                       ctx->sc + 0, ctx->key_cap, fp.n_tiles, ctx->ranges, ctx->sorted, st);
     ISG_CHECK_LAUNCH();
     ctx->launches++;
   } else if (!radix) {
@@ -435,6 +444,8 @@ isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out) {
     ISG_CHECK_LAUNCH();
     ctx->launches++;
     }
+  } else {  // radix, empty scene: every tile empty at 0
+    ISG_CUDA(cudaMemsetAsync(ctx->ranges, 0, sizeof(uint2) * fp.n_tiles, st));
   }
   ISG_STAGE(ST_BLEND_FWD);
   isg::launch_blend_fwd(fp, ctx->ranges, ctx->sorted, ctx->rec, ctx->total, ctx->key_cap, out,
@@ -611,12 +622,14 @@ isg_status isg_create(int device, int64_t max_gaussians, int32_t max_width, int3
   chk(cudaMalloc(&ctx->sc, sizeof(uint32_t) * 8));
   chk(cudaMalloc(&ctx->total, sizeof(unsigned long long) * 2));
   chk(cudaMalloc(&ctx->loss, sizeof(double) * 4));
+  chk(cudaMalloc(&ctx->adam_state, sizeof(isg::AdamState) * 2));
   chk(cudaMallocHost(&ctx->h_sc, sizeof(uint32_t) * 8));
   chk(cudaMallocHost(&ctx->h_total, sizeof(unsigned long long) * 2));
   chk(cudaMallocHost(&ctx->h_loss, sizeof(double) * 4));
   if (s == ISG_OK) {
     chk(cudaMemset(ctx->total, 0, sizeof(unsigned long long) * 2));
     chk(cudaMemset(ctx->loss, 0, sizeof(double) * 4));
+    chk(cudaMemset(ctx->adam_state, 0, sizeof(isg::AdamState) * 2));
   }
   if (s == ISG_OK && max_gaussians > 0) s = ensure_scene(ctx, max_gaussians);
   if (s == ISG_OK && max_width > 0 && max_height > 0) s = ensure_pixels(ctx, max_width, max_height);
@@ -641,7 +654,8 @@ void isg_destroy(isg_ctx* ctx) {
                  ctx->tval[0], ctx->tval[1], ctx->emit_gid, ctx->sort.hist, ctx->sort.lookback,
                  ctx->sort.counters, ctx->scan_scratch, ctx->img, ctx->target, ctx->t_last,
                  ctx->n_proc, ctx->ranges, ctx->tile_cnt, ctx->cursor, ctx->tile_loss, ctx->sc,
-                 ctx->total, ctx->loss, ctx->snap, ctx->coef, ctx->dldc, ctx->ssim_part};
+                 ctx->total, ctx->loss, ctx->snap, ctx->coef, ctx->dldc, ctx->ssim_part,
+                 ctx->adam_state};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (ctx->h_sc) cudaFreeHost(ctx->h_sc);
@@ -664,6 +678,7 @@ void isg_destroy(isg_ctx* ctx) {
 
 isg_status isg_set_stream(isg_ctx* ctx, void* stream) {
   if (!ctx) return ISG_E_ARG;
+  ISG_NO_CAPTURE("isg_set_stream");
   cudaSetDevice(ctx->device);
   ISG_CUDA(cudaStreamSynchronize(ctx->stream));
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
@@ -679,6 +694,7 @@ isg_status isg_set_stream(isg_ctx* ctx, void* stream) {
 
 isg_status isg_synchronize(isg_ctx* ctx) {
   if (!ctx) return ISG_E_ARG;
+  ISG_NO_CAPTURE("isg_synchronize");
   cudaSetDevice(ctx->device);
   if (ctx->frame_unchecked) {
     bool ov = false;
@@ -711,6 +727,7 @@ isg_status isg_get_stats(const isg_ctx* ctx, isg_stats* out) {
 static isg_status set_scene_impl(isg_ctx* ctx, int64_t n, const float* ms, const float* co,
                                  cudaMemcpyKind kind) {
   if (!ctx) return ISG_E_ARG;
+  if (kind == cudaMemcpyHostToDevice) ISG_NO_CAPTURE("isg_set_scene");
   if (n < 0 || n > 0xFFFFFFF0ll) return fail(ctx, ISG_E_ARG, "set_scene: bad splat count");
   if (n > 0 && (!ms || !co)) return fail(ctx, ISG_E_ARG, "set_scene: null pointer");
   cudaSetDevice(ctx->device);
@@ -731,6 +748,7 @@ static isg_status set_scene_impl(isg_ctx* ctx, int64_t n, const float* ms, const
   }
   ctx->n = n;
   ctx->adam_t = 0;
+  ISG_CUDA(cudaMemsetAsync(ctx->adam_state, 0, sizeof(isg::AdamState), ctx->stream));
   ctx->snap_valid = false;
   ctx->pending = false;
   ctx->grad3d_valid = false;
@@ -750,6 +768,7 @@ isg_status isg_set_scene_device(isg_ctx* ctx, int64_t n, const float* ms, const 
 
 isg_status isg_get_scene(isg_ctx* ctx, float* ms, float* co) {
   if (!ctx) return ISG_E_ARG;
+  ISG_NO_CAPTURE("isg_get_scene");
   cudaSetDevice(ctx->device);
   if (ctx->n > 0) {
     if (ms) ISG_CUDA(cudaMemcpyAsync(ms, ctx->ms, sizeof(float4) * ctx->n, cudaMemcpyDeviceToHost, ctx->stream));
@@ -773,6 +792,7 @@ isg_status isg_render_device(isg_ctx* ctx, const isg_camera* cam, const float bg
 isg_status isg_render(isg_ctx* ctx, const isg_camera* cam, const float bg[3], float t_min,
                       float* out_hwc3) {
   if (!ctx) return ISG_E_ARG;
+  ISG_NO_CAPTURE("isg_render");
   if (!out_hwc3) return fail(ctx, ISG_E_ARG, "render: null output");
   if (!(t_min >= 0.0f) || !(t_min < 1.0f)) return fail(ctx, ISG_E_ARG, "render: t_min must be in [0,1)");
   cudaSetDevice(ctx->device);
@@ -810,6 +830,7 @@ isg_status isg_loss_backward_device(isg_ctx* ctx, const isg_camera* cam, const f
 isg_status isg_loss_backward(isg_ctx* ctx, const isg_camera* cam, const float bg[3], float t_min,
                              const float* target, float weight, double* loss_out) {
   if (!ctx) return ISG_E_ARG;
+  ISG_NO_CAPTURE("isg_loss_backward");
   if (!target) return fail(ctx, ISG_E_ARG, "loss_backward: null target");
   if (!(t_min >= 0.0f) || !(t_min < 1.0f)) return fail(ctx, ISG_E_ARG, "loss_backward: t_min must be in [0,1)");
   if (!std::isfinite(weight)) return fail(ctx, ISG_E_ARG, "loss_backward: non-finite weight");
@@ -899,44 +920,33 @@ isg_status isg_adam_step(isg_ctx* ctx, const float lr[4], float b1, float b2, fl
   if (!ctx->pending && !ctx->grad3d_valid)
     return fail(ctx, ISG_E_STATE, "adam: no gradients accumulated since the last step");
   cudaSetDevice(ctx->device);
-  ctx->adam_t++;
-  isg::AdamParams ap;
-  for (int i = 0; i < 4; ++i) ap.lr[i] = lr[i];
-  ap.b1 = b1;
-  ap.b2 = b2;
-  ap.eps = eps;
-  const double bc1 = 1.0 - std::pow((double)b1, (double)ctx->adam_t);
-  const double bc2 = 1.0 - std::pow((double)b2, (double)ctx->adam_t);
-  for (int i = 0; i < 4; ++i) ap.step_size[i] = (float)((double)lr[i] / bc1);
-  ap.bc2_sqrt = (float)std::sqrt(bc2);
+  ctx->adam_t++;  // host mirror (stats); the device counter drives the bias corrections
   if (ctx->pending && !ctx->grad3d_valid && !ctx->nccl_comm) {
     // single view since the last step: projection backward fused with Adam (K8)
     ISG_STAGE(ST_PROJECT_ADAM);
+    isg::launch_adam_tick(lr, b1, b2, eps, ctx->adam_state, ctx->loss, ctx->stream);
     isg::launch_project_adam(ctx->ms, ctx->co, ctx->n, ctx->pending_fp, ctx->slot_off,
                              slot_list(ctx), ctx->ntiles, ctx->partial, ctx->total, ctx->key_cap,
-                             ctx->m, ctx->v, ap, ctx->total + 1, ctx->stream);
+                             ctx->m, ctx->v, ctx->adam_state, ctx->total + 1, ctx->stream);
     ISG_CHECK_LAUNCH();
-    ctx->launches++;
+    ctx->launches += 2;
     ctx->pending = false;
   } else {
     isg_status s = flush_pending(ctx);
     if (s != ISG_OK) return s;
     if (ctx->nccl_comm) {
       ISG_STAGE(ST_ALLREDUCE);
-      s = isg_nccl_allreduce_grads(ctx);
+      s = isg_nccl_allreduce_grads(ctx);  // gradients and the step's loss, before the tick
       if (s != ISG_OK) return s;
     }
     ISG_STAGE(ST_ADAM);
-    isg::launch_adam(ctx->ms, ctx->co, ctx->n, ctx->grad3d, ctx->m, ctx->v, ap, ctx->total + 1,
-                     ctx->stream);
+    isg::launch_adam_tick(lr, b1, b2, eps, ctx->adam_state, ctx->loss, ctx->stream);
+    isg::launch_adam(ctx->ms, ctx->co, ctx->n, ctx->grad3d, ctx->m, ctx->v, ctx->adam_state,
+                     ctx->total + 1, ctx->stream);
     ISG_CHECK_LAUNCH();
-    ctx->launches++;
+    ctx->launches += 2;
   }
   ctx->grad3d_valid = false;
-  // the step's (all-reduced) loss moves to loss[2]; the accumulator restarts at zero
-  ISG_CUDA(cudaMemcpyAsync(ctx->loss + 2, ctx->loss, sizeof(double), cudaMemcpyDeviceToDevice,
-                           ctx->stream));
-  ISG_CUDA(cudaMemsetAsync(ctx->loss, 0, sizeof(double), ctx->stream));
   return ISG_OK;
 }
 
@@ -954,6 +964,7 @@ isg_status isg_last_step_loss(isg_ctx* ctx, double* loss_out) {
 isg_status isg_eval_loss(isg_ctx* ctx, const isg_camera* cam, const float bg[3], float t_min,
                          const float* target_dev, float weight, double* loss_out) {
   if (!ctx || !loss_out) return ISG_E_ARG;
+  ISG_NO_CAPTURE("isg_eval_loss");
   if (!target_dev) return fail(ctx, ISG_E_ARG, "eval_loss: null target");
   if (!(t_min >= 0.0f) || !(t_min < 1.0f)) return fail(ctx, ISG_E_ARG, "eval_loss: t_min must be in [0,1)");
   cudaSetDevice(ctx->device);
@@ -1001,6 +1012,8 @@ isg_status isg_snapshot(isg_ctx* ctx) {
     ISG_CUDA(cudaMemcpyAsync(ctx->snap + 2 * n, ctx->m, sizeof(float4) * 2 * n, cudaMemcpyDeviceToDevice, ctx->stream));
     ISG_CUDA(cudaMemcpyAsync(ctx->snap + 4 * n, ctx->v, sizeof(float4) * 2 * n, cudaMemcpyDeviceToDevice, ctx->stream));
   }
+  ISG_CUDA(cudaMemcpyAsync(ctx->adam_state + 1, ctx->adam_state, sizeof(isg::AdamState),
+                           cudaMemcpyDeviceToDevice, ctx->stream));
   ctx->snap_t = ctx->adam_t;
   ctx->snap_valid = true;
   return ISG_OK;
@@ -1018,6 +1031,8 @@ isg_status isg_restore(isg_ctx* ctx) {
     ISG_CUDA(cudaMemcpyAsync(ctx->m, ctx->snap + 2 * n, sizeof(float4) * 2 * n, cudaMemcpyDeviceToDevice, ctx->stream));
     ISG_CUDA(cudaMemcpyAsync(ctx->v, ctx->snap + 4 * n, sizeof(float4) * 2 * n, cudaMemcpyDeviceToDevice, ctx->stream));
   }
+  ISG_CUDA(cudaMemcpyAsync(ctx->adam_state, ctx->adam_state + 1, sizeof(isg::AdamState),
+                           cudaMemcpyDeviceToDevice, ctx->stream));
   ctx->adam_t = ctx->snap_t;
   ctx->have_frame = false;
   return ISG_OK;
@@ -1026,6 +1041,7 @@ isg_status isg_restore(isg_ctx* ctx) {
 isg_status isg_adaptive_control(isg_ctx* ctx, const isg_adapt_params* prm, uint64_t seed,
                                 uint64_t round, isg_adapt_result* out) {
   if (!ctx || !prm) return ISG_E_ARG;
+  ISG_NO_CAPTURE("isg_adaptive_control");
   // AdaptiveControlParams::validate (include/isosplat/optimize.hpp:21-27)
   if (!(prm->prune_threshold >= 0.0)) return fail(ctx, ISG_E_ARG, "prune_threshold: must be >= 0");
   if (!(prm->merge_distance_factor > 0.0))
@@ -1078,6 +1094,7 @@ isg_status isg_adaptive_control(isg_ctx* ctx, const isg_adapt_params* prm, uint6
     ISG_CUDA(cudaMemsetAsync(ctx->v, 0, sizeof(float4) * 2 * ctx->n, ctx->stream));
   }
   ctx->adam_t = 0;
+  ISG_CUDA(cudaMemsetAsync(ctx->adam_state, 0, sizeof(isg::AdamState), ctx->stream));
   ctx->snap_valid = false;
   ctx->pending = false;
   ctx->grad3d_valid = false;
@@ -1097,6 +1114,60 @@ isg_status isg_adaptive_control(isg_ctx* ctx, const isg_adapt_params* prm, uint6
   return ISG_OK;
 }
 
+struct isg_graph {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int64_t launches = 0;
+};
+
+isg_status isg_graph_begin(isg_ctx* ctx) {
+  if (!ctx) return ISG_E_ARG;
+  if (ctx->capturing) return fail(ctx, ISG_E_STATE, "graph_begin: already capturing");
+  cudaSetDevice(ctx->device);
+  isg_status s = isg_synchronize(ctx);  // pending overflow checks happen before the capture
+  if (s != ISG_OK) return s;
+  ISG_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  ctx->capturing = true;
+  ctx->capture_launches0 = ctx->launches;
+  return ISG_OK;
+}
+
+isg_status isg_graph_end(isg_ctx* ctx, isg_graph** out) {
+  if (!ctx || !out) return ISG_E_ARG;
+  if (!ctx->capturing) return fail(ctx, ISG_E_STATE, "graph_end: not capturing");
+  cudaSetDevice(ctx->device);
+  ctx->capturing = false;
+  isg_graph* g = new isg_graph();
+  cudaError_t e = cudaStreamEndCapture(ctx->stream, &g->graph);
+  if (e == cudaSuccess) e = cudaGraphInstantiate(&g->exec, g->graph, 0);
+  if (e != cudaSuccess) {
+    if (g->graph) cudaGraphDestroy(g->graph);
+    delete g;
+    cudaGetLastError();
+    return cuda_fail(ctx, e, "graph capture");
+  }
+  g->launches = ctx->launches - ctx->capture_launches0;
+  *out = g;
+  return ISG_OK;
+}
+
+isg_status isg_graph_launch(isg_ctx* ctx, isg_graph* g) {
+  if (!ctx || !g) return ISG_E_ARG;
+  if (ctx->capturing) return fail(ctx, ISG_E_STATE, "graph_launch: inside a capture");
+  cudaSetDevice(ctx->device);
+  ISG_CUDA(cudaGraphLaunch(g->exec, ctx->stream));
+  ctx->launches += g->launches;
+  ctx->frame_unchecked = true;  // replayed frames are checked at the next synchronisation
+  return ISG_OK;
+}
+
+void isg_graph_destroy(isg_graph* g) {
+  if (!g) return;
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->graph) cudaGraphDestroy(g->graph);
+  delete g;
+}
+
 isg_status isg_set_loss(isg_ctx* ctx, int kind, float lambda) {
   if (!ctx) return ISG_E_ARG;
   if (kind != ISG_LOSS_L2 && kind != ISG_LOSS_L1_DSSIM)
@@ -1112,6 +1183,7 @@ isg_status isg_image_loss_device(isg_ctx* ctx, int32_t width, int32_t height,
                                  const float* fhat_dev, const float* target_dev, float weight,
                                  double* loss_out, float* dldc_dev) {
   if (!ctx || !loss_out || !fhat_dev || !target_dev) return ISG_E_ARG;
+  ISG_NO_CAPTURE("isg_image_loss_device");
   if (width <= 0 || height <= 0) return fail(ctx, ISG_E_ARG, "image_loss: bad image size");
   if (!std::isfinite(weight)) return fail(ctx, ISG_E_ARG, "image_loss: non-finite weight");
   cudaSetDevice(ctx->device);

@@ -93,8 +93,9 @@ void launch_scan_emit(const uint32_t* order, const uint32_t* ntiles, const uint2
                       uint32_t* tile_keys, uint32_t* emit_gid, int64_t key_cap,
                       unsigned long long* scratch, uint32_t* counter, uint32_t* n_keys,
                       unsigned long long* n_keys_total, cudaStream_t st);
+// (splat, slot) pairs in sorted order + per-tile ranges (empty tiles: (start, start))
 void launch_ranges(const uint32_t* sorted_tiles, const uint32_t* e_sorted,
-                   const uint32_t* emit_gid, const uint32_t* n_keys, int64_t key_cap,
+                   const uint32_t* emit_gid, const uint32_t* n_keys, int64_t key_cap, int n_tiles,
                    uint2* ranges, uint2* sorted, cudaStream_t st);
 
 // ---- blending (k_blend.cu) ----------------------------------------------------------------
@@ -134,12 +135,23 @@ void launch_l2_tiles(const FrameParams& fp, const float* img, const float* targe
                      double* tile_loss, cudaStream_t st);
 
 // ---- optimizer (k_adam.cu) ----------------------------------------------------------------
+// Adam scalars live in device memory (AdamState), written by k_adam_tick once per step from
+// the step counter on the device, so a captured CUDA graph replays correct bias corrections.
 struct AdamParams {
   float lr[4];
   float b1, b2, eps;
   float step_size[4];  // lr / (1 - b1^t)
   float bc2_sqrt;      // sqrt(1 - b2^t)
 };
+struct AdamState {
+  AdamParams p;
+  long long t;  // steps taken
+};
+
+// t += 1, bias corrections of step t into st->p; moves the step's accumulated loss
+// (loss[0]) to loss[2] and restarts the accumulator.
+void launch_adam_tick(const float lr[4], float b1, float b2, float eps, AdamState* st_dev,
+                      double* loss, cudaStream_t st);
 
 // Splat g's slots: slot_of[slot_off[g] + k] (or slot_off[g] + k when slot_of is null).
 // K8a: 2D grads of one view -> 3D grads (overwrite when `first`, else accumulate).
@@ -153,10 +165,10 @@ void launch_project_adam(float4* ms, float4* co, int64_t n, const FrameParams& f
                          const uint32_t* slot_off, const uint32_t* slot_of,
                          const uint32_t* ntiles, const float4* partial,
                          const unsigned long long* total, int64_t cap, float4* m, float4* v,
-                         const AdamParams& ap, unsigned long long* skipped, cudaStream_t st);
+                         const AdamState* ap, unsigned long long* skipped, cudaStream_t st);
 // K8b: Adam from accumulated 3D grads.
 void launch_adam(float4* ms, float4* co, int64_t n, const float4* grad3d, float4* m, float4* v,
-                 const AdamParams& ap, unsigned long long* skipped, cudaStream_t st);
+                 const AdamState* ap, unsigned long long* skipped, cudaStream_t st);
 
 // ---- adaptive control (k_adapt.cu) ----------------------------------------------------------
 struct AdaptParamsDev {

@@ -97,6 +97,21 @@ __device__ __forceinline__ void adam_update(float4* __restrict__ ms, float4* __r
 
 }  // namespace
 
+// One thread: step counter, bias corrections (torch.optim.Adam: step_size = lr / (1 - b1^t),
+// denominator sqrt(v) / sqrt(1 - b2^t) + eps) and the loss hand-over of the step.
+__global__ void k_adam_tick(AdamParams in, AdamState* __restrict__ st, double* __restrict__ loss) {
+  const long long t = st->t + 1;
+  st->t = t;
+  const double bc1 = 1.0 - pow((double)in.b1, (double)t);
+  const double bc2 = 1.0 - pow((double)in.b2, (double)t);
+  AdamParams p = in;
+  for (int i = 0; i < 4; ++i) p.step_size[i] = (float)((double)in.lr[i] / bc1);
+  p.bc2_sqrt = (float)sqrt(bc2);
+  st->p = p;
+  loss[2] = loss[0];
+  loss[0] = 0.0;
+}
+
 __global__ void __launch_bounds__(256) k_project_backward(
     const float4* __restrict__ ms, int64_t n, FrameParams fp, const uint32_t* __restrict__ slot_off,
     const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ ntiles,
@@ -125,11 +140,12 @@ __global__ void __launch_bounds__(256) k_project_adam(
     const uint32_t* __restrict__ slot_off, const uint32_t* __restrict__ slot_of,
     const uint32_t* __restrict__ ntiles, const float4* __restrict__ partial,
     const unsigned long long* __restrict__ total, int64_t cap, float4* __restrict__ m,
-    float4* __restrict__ v, AdamParams ap,
+    float4* __restrict__ v, const AdamState* __restrict__ state,
     unsigned long long* __restrict__ skipped) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (*total > (unsigned long long)cap) return;  // overflowed frame: no update (host re-runs)
+  const AdamParams ap = state->p;
   float4 a, b;
   sum_slots(partial, slot_of, slot_off[i], ntiles[i], a, b);
   float o[8];
@@ -140,9 +156,11 @@ __global__ void __launch_bounds__(256) k_project_adam(
 __global__ void __launch_bounds__(256) k_adam(float4* __restrict__ ms, float4* __restrict__ co,
                                               int64_t n, const float4* __restrict__ grad3d,
                                               float4* __restrict__ m, float4* __restrict__ v,
-                                              AdamParams ap, unsigned long long* __restrict__ skipped) {
+                                              const AdamState* __restrict__ state,
+                                              unsigned long long* __restrict__ skipped) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  const AdamParams ap = state->p;
   const float4 g0 = grad3d[2 * i], g1 = grad3d[2 * i + 1];
   const float o[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
   adam_update(ms, co, m, v, i, o, ap, skipped);
@@ -162,16 +180,26 @@ void launch_project_adam(float4* ms, float4* co, int64_t n, const FrameParams& f
                          const uint32_t* slot_off, const uint32_t* slot_of,
                          const uint32_t* ntiles, const float4* partial,
                          const unsigned long long* total, int64_t cap, float4* m, float4* v,
-                         const AdamParams& ap, unsigned long long* skipped, cudaStream_t st) {
+                         const AdamState* ap, unsigned long long* skipped, cudaStream_t st) {
   if (n <= 0) return;
   k_project_adam<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
       ms, co, n, fp, slot_off, slot_of, ntiles, partial, total, cap, m, v, ap, skipped);
 }
 
 void launch_adam(float4* ms, float4* co, int64_t n, const float4* grad3d, float4* m, float4* v,
-                 const AdamParams& ap, unsigned long long* skipped, cudaStream_t st) {
+                 const AdamState* ap, unsigned long long* skipped, cudaStream_t st) {
   if (n <= 0) return;
   k_adam<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ms, co, n, grad3d, m, v, ap, skipped);
+}
+
+void launch_adam_tick(const float lr[4], float b1, float b2, float eps, AdamState* st_dev,
+                      double* loss, cudaStream_t st) {
+  AdamParams in{};
+  for (int i = 0; i < 4; ++i) in.lr[i] = lr[i];
+  in.b1 = b1;
+  in.b2 = b2;
+  in.eps = eps;
+  k_adam_tick<<<1, 1, 0, st>>>(in, st_dev, loss);
 }
 
 }  // namespace isg

@@ -228,19 +228,35 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
 }
 
 // ---- ranges ---------------------------------------------------------------------------------
-// Per-tile [start, end) from the sorted tile keys, and the blend kernels' (splat, slot) pairs
-// (slot = the pair's emission index, which also keys its gradient slot).
+// Per-tile [start, end) from the sorted tile keys and the blend kernels' (splat, slot) pairs
+// (slot = the pair's emission index, which also keys its gradient slot).  The thread at each
+// key change also fills the empty tiles in the gap with (i, i), so an empty tile gets
+// (start, start) at the position it would occupy, exactly like the oracle.
 __global__ void k_ranges(const uint32_t* __restrict__ t, const uint32_t* __restrict__ e_sorted,
                          const uint32_t* __restrict__ emit_gid, const uint32_t* __restrict__ n_dev,
-                         int64_t cap, uint2* __restrict__ ranges, uint2* __restrict__ sorted) {
+                         int64_t cap, int n_tiles, uint2* __restrict__ ranges,
+                         uint2* __restrict__ sorted) {
   const int64_t n = min((int64_t)*n_dev, cap);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+  if (n == 0) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n_tiles; k += gridDim.x * blockDim.x)
+      ranges[k] = make_uint2(0u, 0u);
+    return;
+  }
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t k = t[i];
-    if (i == 0 || t[i - 1] != k) ranges[k].x = (uint32_t)i;
-    if (i == n - 1 || t[i + 1] != k) ranges[k].y = (uint32_t)(i + 1);
-    const uint32_t e = e_sorted[i];
-    sorted[i] = make_uint2(emit_gid[e], e);
+    // boundary between item i-1 and item i (i = 0: before the first, i = n: after the last)
+    const uint32_t prev = i > 0 ? t[i - 1] : 0xFFFFFFFFu;
+    const uint32_t next = i < n ? t[i] : (uint32_t)n_tiles;
+    if (i == 0 || prev != next) {
+      const uint32_t lo = i > 0 ? prev + 1 : 0u;  // empty tiles lo .. next-1
+      for (uint32_t k = lo; k < next; ++k) ranges[k] = make_uint2((uint32_t)i, (uint32_t)i);
+      if (i > 0) ranges[prev].y = (uint32_t)i;
+      if (i < n) ranges[next].x = (uint32_t)i;
+    }
+    if (i < n) {
+      const uint32_t e = e_sorted[i];
+      sorted[i] = make_uint2(emit_gid[e], e);
+    }
   }
 }
 
@@ -326,11 +342,11 @@ void launch_scan_emit(const uint32_t* order, const uint32_t* ntiles, const uint2
 }
 
 void launch_ranges(const uint32_t* sorted_tiles, const uint32_t* e_sorted,
-                   const uint32_t* emit_gid, const uint32_t* n_keys, int64_t key_cap,
+                   const uint32_t* emit_gid, const uint32_t* n_keys, int64_t key_cap, int n_tiles,
                    uint2* ranges, uint2* sorted, cudaStream_t st) {
-  const int64_t blocks = std::min<int64_t>((key_cap + 255) / 256, 148 * 16);
+  const int64_t blocks = std::min<int64_t>((key_cap + 256) / 256, 148 * 16);
   k_ranges<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, st>>>(
-      sorted_tiles, e_sorted, emit_gid, n_keys, key_cap, ranges, sorted);
+      sorted_tiles, e_sorted, emit_gid, n_keys, key_cap, n_tiles, ranges, sorted);
 }
 
 int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], bool iota_vals, const uint32_t* n_dev,
@@ -346,7 +362,11 @@ int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], bool iota_vals, const
   k_hist<<<hist_blocks, 256, 0, st>>>(keys[0], n_dev, cap, passes, s.hist);
   int cur = 0;
   const size_t smem = sizeof(OnesweepSmem);
-  cudaFuncSetAttribute(k_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static const bool attr_set = [&] {  // once, outside any graph capture
+    cudaFuncSetAttribute(k_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return true;
+  }();
+  (void)attr_set;
   for (int p = 0; p < passes; ++p) {
     k_onesweep<<<(unsigned)std::max<int64_t>(tiles, 1), kSortThreads, smem, st>>>(
         keys[cur], (p == 0 && iota_vals) ? nullptr : vals[cur], keys[cur ^ 1], vals[cur ^ 1],

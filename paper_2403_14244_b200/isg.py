@@ -96,6 +96,10 @@ def lib() -> C.CDLL:
         "isg_snapshot": ([P], C.c_int),
         "isg_restore": ([P], C.c_int),
         "isg_set_loss": ([P, C.c_int, F], C.c_int),
+        "isg_graph_begin": ([P], C.c_int),
+        "isg_graph_end": ([P, C.POINTER(P)], C.c_int),
+        "isg_graph_launch": ([P, P], C.c_int),
+        "isg_graph_destroy": ([P], None),
         "isg_adaptive_control": ([P, C.POINTER(AdaptParamsT), C.c_uint64, C.c_uint64,
                                   C.POINTER(AdaptResultT)], C.c_int),
         "isg_image_loss_device": ([P, I32, I32, P, P, F, C.POINTER(C.c_double), P], C.c_int),
@@ -127,7 +131,8 @@ C_ABI_SYMBOLS = (
     "isg_get_scene", "isg_render", "isg_render_device", "isg_loss_backward",
     "isg_loss_backward_device", "isg_read_loss", "isg_zero_grads", "isg_get_grads",
     "isg_grads_device", "isg_adam_step", "isg_last_step_loss", "isg_eval_loss", "isg_snapshot",
-    "isg_restore", "isg_set_loss", "isg_image_loss_device", "isg_adaptive_control", "isg_nccl_get_unique_id",
+    "isg_restore", "isg_set_loss", "isg_image_loss_device", "isg_adaptive_control",
+    "isg_graph_begin", "isg_graph_end", "isg_graph_launch", "isg_graph_destroy", "isg_nccl_get_unique_id",
     "isg_nccl_init",
     "isg_nccl_detach", "isg_debug_bins", "isg_debug_pixel_state", "isg_set_binning",
     "isg_profile_enable",
@@ -237,6 +242,27 @@ def _check(ctx, status: int) -> None:
     if status == ISG_E_ARG:
         raise ValueError(msg)
     raise IsgError(status, f"{L.isg_status_string(status).decode()}: {msg}")
+
+
+class Graph:
+    """A captured sequence of asynchronous calls (isg_graph), replayed with launch()."""
+
+    def __init__(self, renderer, handle):
+        self._r, self._h = renderer, handle
+
+    def launch(self):
+        _check(self._r._h, lib().isg_graph_launch(self._r._h, self._h))
+
+    def close(self):
+        if self._h:
+            lib().isg_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def splats_to_soa(splats: np.ndarray):
@@ -432,6 +458,16 @@ class Renderer:
                                                    C.byref(res)))
         self.n = int(res.n_after)
         return {k: int(getattr(res, k)) for k, _ in AdaptResultT._fields_}
+
+    # -- CUDA graphs -------------------------------------------------------------------------
+    def graph_begin(self):
+        """Start capturing the asynchronous calls on the context stream."""
+        _check(self._h, lib().isg_graph_begin(self._h))
+
+    def graph_end(self) -> "Graph":
+        g = C.c_void_p()
+        _check(self._h, lib().isg_graph_end(self._h, C.byref(g)))
+        return Graph(self, g)
 
     def last_step_loss(self) -> float:
         v = C.c_double()

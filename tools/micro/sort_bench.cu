@@ -75,7 +75,12 @@ int main() {
     float z = uz(rng);
     std::memcpy(&d, &z, 4);
   }
-  run("depth", depth, true, 32, 20);
+  for (int64_t m : {32768L, 131072L, 262144L, 1000000L}) {
+    std::vector<uint32_t> d(depth.begin(), depth.begin() + m);
+    char name[32];
+    snprintf(name, sizeof name, "d%lld", (long long)m);
+    run(name, d, true, 32, 20);
+  }
   // tile ids in depth order: each splat touches a few neighbouring tiles
   std::vector<uint32_t> tile;
   std::uniform_int_distribution<int> ut(0, 8159), nt(1, 7);
