@@ -81,29 +81,34 @@ __global__ void __launch_bounds__(256) k_hist(const uint32_t* __restrict__ keys,
   __syncthreads();
   const int64_t n = min((int64_t)*n_dev, cap);
   const uint32_t lt = lanemask_lt();
-  // grid-stride over whole warps.  A digit shared by the whole warp (the skewed high bytes:
-  // e.g. the exponent byte of positive depths, the top bits of tile ids) costs one shared
-  // atomic per warp instead of 32 serialised ones.
-  const int64_t stride = (int64_t)gridDim.x * 256;
-  for (int64_t i0 = (int64_t)blockIdx.x * 256 + (threadIdx.x & ~31); i0 < n; i0 += stride) {
-    const int64_t i = i0 + (threadIdx.x & 31);
-    const bool valid = i < n;
-    const uint32_t k = valid ? keys[i] : 0u;
-    const bool full = __all_sync(0xffffffffu, valid);
-    for (int p = 0; p < passes; ++p) {
-      const uint32_t d = (k >> (8 * p)) & 255u;
-#if ISG_HIST_MODE == 1
-      const uint32_t dv = valid ? d : 256u;
-      const uint32_t peers = __match_any_sync(0xffffffffu, dv);
-      if (dv < 256u && (peers & lt) == 0) atomicAdd(&sh[p][dv], (uint32_t)__popc(peers));
-#else
-      const uint32_t d0 = __shfl_sync(0xffffffffu, d, 0);
-      if (full && __all_sync(0xffffffffu, d == d0)) {
-        if ((threadIdx.x & 31) == 0) atomicAdd(&sh[p][d0], 32u);
-      } else if (valid) {
-        atomicAdd(&sh[p][d], 1u);
+  // grid-stride over whole warps, kHistUnroll keys per thread in flight at once.  A digit
+  // shared by the whole warp (the skewed high bytes: e.g. the exponent byte of positive
+  // depths, the top bits of tile ids) costs one shared atomic per warp instead of 32
+  // serialised ones.
+  constexpr int kHistUnroll = 8;
+  const int64_t stride = (int64_t)gridDim.x * 256 * kHistUnroll;
+  for (int64_t i0 = ((int64_t)blockIdx.x * 256 + (threadIdx.x & ~31)) * kHistUnroll; i0 < n;
+       i0 += stride) {
+    uint32_t k[kHistUnroll];
+    bool valid[kHistUnroll];
+#pragma unroll
+    for (int u = 0; u < kHistUnroll; ++u) {
+      const int64_t i = i0 + 32 * u + (threadIdx.x & 31);
+      valid[u] = i < n;
+      k[u] = valid[u] ? keys[i] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < kHistUnroll; ++u) {
+      const bool full = __all_sync(0xffffffffu, valid[u]);
+      for (int p = 0; p < passes; ++p) {
+        const uint32_t d = (k[u] >> (8 * p)) & 255u;
+        const uint32_t d0 = __shfl_sync(0xffffffffu, d, 0);
+        if (full && __all_sync(0xffffffffu, d == d0)) {
+          if ((threadIdx.x & 31) == 0) atomicAdd(&sh[p][d0], 32u);
+        } else if (valid[u]) {
+          atomicAdd(&sh[p][d], 1u);
+        }
       }
-#endif
     }
   }
   __syncthreads();
@@ -262,7 +267,10 @@ __global__ void k_ranges(const uint32_t* __restrict__ t, const uint32_t* __restr
 
 // ---- scan of tile counts in depth order + record gather + emission --------------------------
 constexpr int kScanThreads = 256;
-constexpr int kScanItems = 4;
+#ifndef ISG_SCAN_ITEMS
+#define ISG_SCAN_ITEMS 4
+#endif
+constexpr int kScanItems = ISG_SCAN_ITEMS;
 constexpr int kScanTileItems = kScanThreads * kScanItems;
 
 __global__ void __launch_bounds__(kScanThreads) k_scan_emit(
@@ -283,12 +291,16 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(
   if (base >= n) return;
   const int64_t r0 = base + (int64_t)tid * kScanItems;
   uint32_t g[kScanItems], c[kScanItems];
+  uint2 box[kScanItems];
   uint32_t sum = 0;
+  // all gathers of the thread's splats in flight before the scan (the emission needs them)
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) g[j] = r0 + j < n ? order[r0 + j] : 0u;
 #pragma unroll
   for (int j = 0; j < kScanItems; ++j) {
-    const int64_t r = r0 + j;
-    g[j] = r < n ? order[r] : 0u;
-    c[j] = r < n ? ntiles[g[j]] : 0u;
+    const bool ok = r0 + j < n;
+    c[j] = ok ? ntiles[g[j]] : 0u;
+    box[j] = ok ? tilebox[g[j]] : make_uint2(0u, 0u);
     sum += c[j];
   }
   uint32_t tot;
@@ -313,9 +325,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(
     const uint32_t gg = g[j];
     slot_off[gg] = (uint32_t)min(off, (unsigned long long)0xFFFFFFFFu);
     if (c[j] == 0) continue;
-    const uint2 box = tilebox[gg];
-    const float4 m = (box.x >> 24) ? make_float4(0.f, 0.f, 0.f, 0.f) : ms[gg];
-    for_each_tile(box, m, fp, [&](int t) {
+    const float4 m = (box[j].x >> 24) ? make_float4(0.f, 0.f, 0.f, 0.f) : ms[gg];
+    for_each_tile(box[j], m, fp, [&](int t) {
       if (off < (unsigned long long)key_cap) {
         tile_keys[off] = (uint32_t)t;
         emit_gid[off] = gg;
