@@ -32,6 +32,7 @@ sys.path.insert(0, str(ROOT))
 
 CONFIGS = {
     # name: (n_gaussians, W, H, views_per_step_total, train, description)
+    "c1": (10_000, 256, 256, 1, True, "synthetic 10K isotropic Gaussians, 256x256, fwd+L2+bwd+Adam"),
     "c2": (1_000_000, 1920, 1080, 1, False, "synthetic 1M isotropic Gaussians, 1920x1080 render"),
     "c3": (1_000_000, 1920, 1080, 1, True,
            "synthetic 1M isotropic Gaussians, 1920x1080, fwd+L2+bwd+Adam, 1 view/GPU/step"),
@@ -133,6 +134,42 @@ def cpu_oracle_train_step(ms, co, cam, target, steps=1, threads=0):
     return (time.perf_counter() - t0) / steps
 
 
+def reference_render_fps(ms, co, cam, cores):
+    """The reference's OWN render() (oracle/_ref: src/splat3d.cpp:173-194 compiled unmodified;
+    rows split into `threads` bands, :148-160) timed on a bounded sample and extrapolated to the
+    full frame.  A sub-image is the same camera with the principal point shifted, so its pixels
+    are exactly the frame's.  F = a 1x1 image (projection + sort of every splat, the per-call
+    fixed cost); B = a band of `cores` rows (every thread composites one full row); the full
+    frame is F + (B - F) * H / cores (each thread then composites H / cores rows).
+    Returns (frames/s, sample description) or None when oracle/_ref is not built."""
+    import oracle as O
+    try:
+        O.ref_lib()
+    except Exception:
+        return None
+    from paper_2403_14244_b200 import isg
+    sp = np.concatenate([ms, co], 1).astype(np.float64)
+    W, H = cam.width, cam.height
+    cx, cy = cam.principal_point
+    rows = max(1, min(cores, H))
+
+    def sub(w, h, x0, y0):
+        c = isg.Camera(np.asarray(cam.rotation), np.asarray(cam.translation), cam.focal,
+                       (cx - x0, cy - y0), w, h)
+        t0 = time.perf_counter()
+        O.ref_render(sp, c, threads=cores)
+        return time.perf_counter() - t0
+
+    fixed = sub(1, 1, W // 2, H // 2)
+    band = sub(W, rows, 0, H // 2 - rows // 2)
+    full = fixed + max(band - fixed, 0.0) * H / rows
+    return 1.0 / full, (f"the reference's own render() (oracle/_ref, src/splat3d.cpp:173-194, "
+                        f"FP64, every pixel tests every splat) with threads={cores}: a 1x1 image "
+                        f"({fixed:.2f} s, projection + sort) and a {rows}-row band "
+                        f"({band:.2f} s, one row per thread); full {W}x{H} frame extrapolated "
+                        f"to {full:.1f} s")
+
+
 def host_threads():
     try:
         return len(os.sched_getaffinity(0))
@@ -151,8 +188,24 @@ def run_reference(args):
     tms, tco = isg.synth_scene(n, W, H, seed=14244)
     cam = isg.Camera.synthetic(W, H)
     import oracle as O
-    target = O.render32(tms, tco, cam, t_min=T_MIN)
     cores = host_threads()
+    if not train:
+        res = reference_render_fps(ms, co, cam, cores)
+        if res is not None:
+            fps, sample = res
+            line = {"impl": "reference", "metric": "render FPS (1M isotropic Gaussians, 1080p)",
+                    "value": fps, "unit": "frames/s", "n_gpus": world, "steps": 1, "warmup": 0,
+                    "ms_per_step": 1e3 / fps, "higher_is_better": True, "scaling": "weak",
+                    "vs_baseline": None, "dtype": "f64",
+                    "data": "synthetic (isg-synth v1, seed 2403)",
+                    "config": {"workload": desc, "n_gaussians": n, "width": W, "height": H},
+                    "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores,
+                                     "kind": "reference", "sample": sample},
+                    "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                            "d2h_bytes_per_step": 0}}
+            print(json.dumps(line), flush=True)
+            return
+    target = O.render32(tms, tco, cam, t_min=T_MIN)
     for _ in range(args.warmup):
         cpu_oracle_train_step(ms, co, cam, target, 1, cores)
     times = [cpu_oracle_train_step(ms, co, cam, target, 1, cores) for _ in range(args.steps)]
@@ -348,6 +401,12 @@ def run_isg(args):
                "kind": "port",
                "sample": ("1 full C3 train step (fwd+L2+bwd+Adam) of the FP32 tiled CPU oracle"
                           if train else "1 full C2 frame of the FP32 tiled CPU oracle")}
+        if not train:  # the reference's own renderer exists: it is the baseline, the port aside
+            res = reference_render_fps(ms_now, co_now, cam0, cores)
+            if res is not None:
+                port = cpu
+                cpu = {"value": res[0], "unit": "frames/s", "cores": cores, "kind": "reference",
+                       "sample": res[1], "port": port}
     sm_mhz = peaks.get("sm_max_mhz", 1965.0)
     if top_name in ("blend_fwd", "blend_bwd") and pairs:
         ev_p, in_p = pairs
