@@ -218,7 +218,8 @@ def run_reference(args):
             "config": {"workload": desc, "n_gaussians": n, "width": W, "height": H,
                        "t_min": T_MIN},
             "cpu_baseline": {"value": val, "unit": "iters/s", "cores": cores, "kind": "port",
-                             "sample": f"{args.steps} full C3 train steps (fwd+L2+bwd+Adam) of the "
+                             "sample": f"{args.steps} full {args.config.upper()} train steps "
+                                       "(fwd+L2+bwd+Adam) of the "
                                        "FP32 tiled CPU oracle; the reference itself has no 3D "
                                        "backward (SPEC.md:484)"},
             "e2e": {"value": val, "unit": "iters/s", "h2d_bytes_per_step": 0,
@@ -399,8 +400,9 @@ def run_isg(args):
             (time.perf_counter() - t0)
         cpu = {"value": 1.0 / sec, "unit": "iters/s" if train else "frames/s", "cores": cores,
                "kind": "port",
-               "sample": ("1 full C3 train step (fwd+L2+bwd+Adam) of the FP32 tiled CPU oracle"
-                          if train else "1 full C2 frame of the FP32 tiled CPU oracle")}
+               "sample": (f"1 full {args.config.upper()} train step (fwd+L2+bwd+Adam) of the FP32 "
+                          "tiled CPU oracle" if train else
+                          f"1 full {args.config.upper()} frame of the FP32 tiled CPU oracle")}
         if not train:  # the reference's own renderer exists: it is the baseline, the port aside
             res = reference_render_fps(ms_now, co_now, cam0, cores)
             if res is not None:
