@@ -375,26 +375,33 @@ def test_long_tile_lists(mode):
         _grad_check(r.grads(), g_ref)
 
 
-def test_cuda_graph_replay_matches_stream_execution():
-    """A captured train step (loss_backward_device + fused Adam) replayed K times gives the
+@pytest.mark.parametrize("views,loss_kind", [(1, isg.LOSS_L2), (3, isg.LOSS_L2),
+                                             (2, isg.LOSS_L1_DSSIM)])
+def test_cuda_graph_replay_matches_stream_execution(views, loss_kind):
+    """A captured train step (loss_backward_device per view + Adam) replayed K times gives the
     bitwise-identical trajectory of K ordinary steps (device-side Adam step counter)."""
     import torch
     W, H, n, K = 128, 96, 4000, 5
     ms, co = isg.synth_scene(n, W, H, seed=31)
     tms, tco = isg.synth_scene(n, W, H, seed=32)
-    cam = isg.Camera.synthetic(W, H, 1, 3)
-    target = torch.from_numpy(O.render32(tms, tco, cam)).cuda()
+    cams = [isg.Camera.synthetic(W, H, k, views) for k in range(views)]
+    targets = [torch.from_numpy(O.render32(tms, tco, c)).cuda() for c in cams]
     torch.cuda.synchronize()
+
+    def step(r):
+        for c, t in zip(cams, targets):
+            r.loss_backward_device(c, t.data_ptr(), weight=1.0 / views)
+        r.adam_step()
+
     results = []
     for use_graph in (False, True):
         r = isg.Renderer(0)
+        r.set_loss(loss_kind, 0.2)
         r.set_scene(ms, co)
-        r.loss_backward_device(cam, target.data_ptr())  # warm-up step sizes every buffer
-        r.adam_step()
+        step(r)  # warm-up step sizes every buffer
         if use_graph:
             r.graph_begin()
-            r.loss_backward_device(cam, target.data_ptr())
-            r.adam_step()
+            step(r)
             with pytest.raises(isg.IsgError):
                 r.read_loss()  # synchronising call inside a capture
             g = r.graph_end()
@@ -403,12 +410,41 @@ def test_cuda_graph_replay_matches_stream_execution():
             g.close()
         else:
             for _ in range(K):
-                r.loss_backward_device(cam, target.data_ptr())
-                r.adam_step()
+                step(r)
         loss = r.last_step_loss()
         results.append((r.get_scene(), loss))
         r.close()
     (a, la), (b, lb) = results
+    np.testing.assert_array_equal(a[0], b[0])
+    np.testing.assert_array_equal(a[1], b[1])
+    assert la == lb
+
+
+def test_nccl_single_rank_path_matches_local_adam():
+    """The multi-GPU step on one rank: NCCL (dlopen'd) all-reduce of the gradient buffer and the
+    loss, then the un-fused Adam — identical to the fused single-GPU step."""
+    W, H, n = 96, 64, 2000
+    ms, co = isg.synth_scene(n, W, H, seed=41)
+    tms, tco = isg.synth_scene(n, W, H, seed=42)
+    cams = [isg.Camera.synthetic(W, H, k, 2) for k in range(2)]
+    targets = [O.render32(tms, tco, c) for c in cams]
+    out = []
+    for use_nccl in (False, True):
+        r = isg.Renderer(0)
+        r.set_scene(ms, co)
+        if use_nccl:
+            r.nccl_init(1, 0, isg.Renderer.nccl_unique_id())
+        losses = []
+        for _ in range(3):
+            for c, t in zip(cams, targets):
+                r.loss_backward(c, t, weight=0.5)
+            r.adam_step()
+            losses.append(r.last_step_loss())
+        if use_nccl:
+            r.nccl_detach()
+        out.append((r.get_scene(), losses))
+        r.close()
+    (a, la), (b, lb) = out
     np.testing.assert_array_equal(a[0], b[0])
     np.testing.assert_array_equal(a[1], b[1])
     assert la == lb
