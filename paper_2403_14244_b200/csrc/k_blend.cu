@@ -4,13 +4,15 @@
 // test covers(ScreenIso) (:108-114).  Instead of every pixel visiting every splat
 // (O(W*H*N)), one CTA owns one tile and walks only that tile's depth-ordered list.
 //
-// Mapping: 128 threads per tile; warp w owns the 8x8 quarter-tile w and each lane a vertical
-// pixel pair, so one shared-memory record feeds two pixels that share dx.  Records are
-// staged 128 at a time into shared memory with cp.async, double-buffered (the next batch's
-// copy is in flight while the current one is blended).  After each batch barrier every warp
-// tests the staged splats' 3-sigma circles against its quarter (conservative closest-point
-// test, exact rounding), ballots, and compacts the relevant entry indices into a per-warp list
-// — culling costs a few instructions per batch and irrelevant entries cost no issue slots.
+// Mapping: 128 threads per tile; warp w owns the 8x8 quarter-tile w, each 8-lane group one 4x4
+// sub-quarter and each lane a vertical pixel pair, so one shared-memory record feeds two pixels
+// that share dx.  Records are staged 128 at a time into shared memory with cp.async,
+// double-buffered (the next batch's copy is in flight while the current one is blended).
+// After each batch barrier every warp tests the staged splats' 3-sigma circles against its
+// quarter and then its four sub-quarters (conservative closest-point tests, exact rounding),
+// ballots, and compacts the relevant entry indices into four lists; the groups walk their own
+// lists in lockstep.  The 4x4 culling cuts the pixel-entry slots a circle does not cover
+// (a circle of the typical 6-px 3-sigma radius covers a 4x4 region far better than an 8x8).
 // Compositing is branch-free; the CTA stops once every pixel has transmittance <= t_min.
 //
 // The 3-sigma test is bit-identical to the FP32 oracle (explicit _rn arithmetic); exp uses
@@ -24,27 +26,60 @@ using namespace blend;
 
 constexpr int kBT = 128;     // threads per tile CTA (4 warps x 32 pixel pairs)
 constexpr int kBatch = 128;  // records staged per batch (one per thread)
+constexpr int kListPitch = kBatch + 4;  // sub-quarter lists start in different banks
 
-// Compact the warp's relevant entries of the batch into `list` (ascending); returns the count.
-__device__ __forceinline__ int warp_relevant_list(const Stage<kBatch>& st, const Region& rg,
-                                                  int cnt, uint8_t* list) {
+// 4x4 sub-quarter s (0..3) of quarter-tile w, pixel-centre rectangle clipped to the image.
+__device__ __forceinline__ Region sub_rect(const FrameParams& fp, int tile, int w, int s) {
+  Region g;
+  const int tx = tile % fp.tiles_x, ty = tile / fp.tiles_x;
+  const int W = fp.cam.width, H = fp.cam.height;
+  const int x0 = tx * kTile + (w & 1) * 8 + (s & 1) * 4, y0 = ty * kTile + (w >> 1) * 8 + (s >> 1) * 4;
+  g.valid = x0 < W && y0 < H;
+  g.x0 = (float)x0 + 0.5f;
+  g.x1 = (float)(min(x0 + 4, W) - 1) + 0.5f;
+  g.y0 = (float)y0 + 0.5f;
+  g.y1 = (float)(min(y0 + 4, H) - 1) + 0.5f;
+  return g;
+}
+
+// Compact the batch's entries relevant to each of the warp's four 4x4 sub-quarters into
+// list[s] (ascending); count[s] receives the lengths.  The four closest-point tests share their
+// per-axis terms: the rounded squares of the x distances to the left / right sub-quarter
+// columns and of the y distances to the top / bottom rows are computed once, and each test
+// adds one pair exactly as rect_hit's dist2_rn would (bit-identical decisions).
+__device__ __forceinline__ void warp_relevant_lists(const Stage<kBatch>& st, const Region rs[4],
+                                                    int cnt, uint8_t (*list)[kListPitch],
+                                                    int count[4]) {
   const int lane = threadIdx.x & 31;
   const uint32_t lt = (1u << lane) - 1u;
-  int base = 0;
+  int base[4] = {0, 0, 0, 0};
 #pragma unroll
   for (int k = 0; k < kBatch / 32; ++k) {
     const int j = 32 * k + lane;
-    bool hit = false;
-    if (j < cnt && rg.valid) {
+    bool h[4] = {false, false, false, false};
+    if (j < cnt) {
       const float4 g = st.geo[j];
-      hit = rect_hit(rg, g.x, g.y, g.z);
+      float ax[2], ay[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const float dx = __fsub_rn(fminf(fmaxf(g.x, rs[i].x0), rs[i].x1), g.x);
+        const float dy = __fsub_rn(fminf(fmaxf(g.y, rs[2 * i].y0), rs[2 * i].y1), g.y);
+        ax[i] = __fmul_rn(dx, dx);
+        ay[i] = __fmul_rn(dy, dy);
+      }
+#pragma unroll
+      for (int s = 0; s < 4; ++s) h[s] = rs[s].valid && !(__fadd_rn(ax[s & 1], ay[s >> 1]) > g.z);
     }
-    const uint32_t m = __ballot_sync(0xffffffffu, hit);
-    if (hit) list[base + __popc(m & lt)] = (uint8_t)j;
-    base += __popc(m);
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const uint32_t m = __ballot_sync(0xffffffffu, h[s]);
+      if (h[s]) list[s][base[s] + __popc(m & lt)] = (uint8_t)j;
+      base[s] += __popc(m);
+    }
   }
   __syncwarp();
-  return base;
+#pragma unroll
+  for (int s = 0; s < 4; ++s) count[s] = base[s];
 }
 
 }  // namespace
@@ -55,14 +90,17 @@ __global__ void __launch_bounds__(kBT) k_blend_fwd(
     int64_t key_cap, float* __restrict__ out, float* __restrict__ t_last,
     uint32_t* __restrict__ n_proc) {
   __shared__ Stage<kBatch> st[2];
-  __shared__ uint8_t s_list[kBT / 32][kBatch];
+  __shared__ uint8_t s_list[kBT / 32][4][kListPitch];
   if (overflowed(total, key_cap)) return;
   const int tile = blockIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const Region reg = region_rect(fp, tile, w);
+  const int sq = lane >> 3, l8 = lane & 7;  // 8-lane group = 4x4 sub-quarter, lane = pixel pair
+  Region sub[4];
+#pragma unroll
+  for (int s = 0; s < 4; ++s) sub[s] = sub_rect(fp, tile, w, s);
   const int tx = tile % fp.tiles_x, ty = tile / fp.tiles_x;
-  const int px_i = tx * kTile + (w & 1) * 8 + (lane & 7);
-  const int py_i = ty * kTile + (w >> 1) * 8 + 2 * (lane >> 3);  // pixels (px_i, py_i + {0,1})
+  const int px_i = tx * kTile + (w & 1) * 8 + (sq & 1) * 4 + (l8 & 3);
+  const int py_i = ty * kTile + (w >> 1) * 8 + (sq >> 1) * 4 + 2 * (l8 >> 2);  // (px, py+{0,1})
   const int W = fp.cam.width, H = fp.cam.height;
   const bool valid0 = px_i < W && py_i < H, valid1 = px_i < W && py_i + 1 < H;
   const float px = (float)px_i + 0.5f, py0 = (float)py_i + 0.5f, py1 = py0 + 1.0f;
@@ -89,11 +127,22 @@ __global__ void __launch_bounds__(kBT) k_blend_fwd(
     if (__syncthreads_count(tdone) == kBT) break;  // barrier: batch visible, previous consumed
     if (b + kBatch < n)
       stage_batch(st[(it + 1) & 1], sorted, rec, rg.x + b + kBatch, min(kBatch, n - b - kBatch));
-    const int nrel = warp_relevant_list(cur, reg, min(kBatch, n - b), s_list[w]);
-    for (int i = 0; i < nrel; ++i) {
-      const int jj = s_list[w][i];
-      const float4 g = cur.geo[jj];
-      const float4 c = cur.col[jj];
+    int cnt[4];
+    warp_relevant_lists(cur, sub, min(kBatch, n - b), s_list[w], cnt);
+    const int steps = max(max(cnt[0], cnt[1]), max(cnt[2], cnt[3]));
+    const int my_cnt = sq == 0 ? cnt[0] : (sq == 1 ? cnt[1] : (sq == 2 ? cnt[2] : cnt[3]));
+    // the four 8-lane groups walk their own sub-quarter lists in lockstep; the next entry's
+    // index and record are loaded one iteration ahead (hides the shared-memory latency chain)
+    const uint8_t* my_list = s_list[w][sq];
+    int jn = my_cnt > 0 ? my_list[0] : 0;
+    float4 gn = cur.geo[jn], cn = cur.col[jn];
+    for (int i = 0; i < steps; ++i) {
+      const bool has = i < my_cnt;
+      const int jj = jn;
+      const float4 g = gn, c = cn;
+      jn = i + 1 < my_cnt ? my_list[i + 1] : 0;
+      gn = cur.geo[jn];
+      cn = cur.col[jn];
       const float dx = __fsub_rn(px, g.x);
       const float ax = __fmul_rn(dx, dx);
       const float2 dy = __fadd2_rn(PY, make_float2(-g.y, -g.y));
@@ -101,8 +150,8 @@ __global__ void __launch_bounds__(kBT) k_blend_fwd(
       // the 3-sigma test must round exactly like the oracle's (and K1's) dist2_rn
       const float2 r2 = make_float2(__fadd_rn(ax, __fmul_rn(dy.x, dy.x)),
                                     __fadd_rn(ax, __fmul_rn(dy.y, dy.y)));
-      const bool in0 = !(r2.x > g.z) && (T.x > t_min);
-      const bool in1 = !(r2.y > g.z) && (T.y > t_min);
+      const bool in0 = has && !(r2.x > g.z) && (T.x > t_min);
+      const bool in1 = has && !(r2.y > g.z) && (T.y > t_min);
       const uint32_t idx = (uint32_t)(b + jj + 1);
       const float2 q = __fmul2_rn(r2, make_float2(g.w, g.w));
       const float2 e = __fmul2_rn(make_float2(c.w, c.w), make_float2(fast_exp2(q.x), fast_exp2(q.y)));
