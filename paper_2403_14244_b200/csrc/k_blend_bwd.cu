@@ -10,15 +10,16 @@
 // prologue — or, for the L1 + D-SSIM loss, read from the dL/dC image k_ssim.cu wrote — and the
 // kernel closed forms of include/isosplat/kernels.hpp:208-222.
 //
-// Mapping: 64 threads per tile.  Each HALF-warp owns one 8x8 quarter-tile and each lane a 2x2
-// pixel quad.  Per staged batch every half-warp compacts the entries whose 3-sigma circle can
-// reach its quarter into its own list; the two halves of a warp then walk their OWN lists in
-// lockstep — two different splats per warp step — so culling stays at 8x8 granularity while
-// the per-step costs (iteration, warp reduction) are shared by two (region, splat) pairs of four
-// pixels per lane.  The 7 gradients of a pair are summed over the lane's 4 pixels, reduce-
-// scattered over the 16 lanes in 8 shuffles, combined over the four quarters in shared memory
-// and written — no atomics — to the pair's gradient slot; K8 sums each splat's slots in a fixed
-// order, so gradients are bitwise deterministic.
+// Mapping: 64 threads per tile.  Each four-lane group owns one 4x4 sub-quarter and each lane a
+// 2x2 pixel quad (two packed f32x2 pixel pairs).  Per staged batch of 32 records every warp
+// tests the records against its 8 sub-quarters (shared per-axis terms), ballots, and compacts 8
+// relevance lists; the 8 groups then walk their OWN lists in lockstep in reverse — eight
+// different splats per warp step — so culling is at 4x4 granularity (a typical 6-px 3-sigma
+// circle covers a 4x4 region far better than an 8x8 one) and the per-entry reduction runs
+// over only 4 lanes.  The 7 gradients of a pair are summed over the lane's 4 pixels,
+// reduce-scattered over the group in 6 shuffles, combined over the 16 sub-quarters in shared
+// memory in a fixed order and written — no atomics — to the pair's gradient slot; K8 sums each
+// splat's slots in a fixed order, so gradients are bitwise deterministic.
 #include "blend_common.cuh"
 
 namespace isg {
@@ -26,8 +27,10 @@ namespace isg {
 namespace {
 using namespace blend;
 
-constexpr int kBT = 64;     // threads per tile CTA: 2 warps = 4 half-warps = 4 quarter-tiles
-constexpr int kBatch = 64;  // records staged per batch (one per thread)
+constexpr int kBT = 64;      // threads per tile CTA: 2 warps x 8 four-lane groups
+constexpr int kBatch = 32;   // records staged per batch (one relevance ballot per sub-quarter)
+constexpr int kSubs = 16;    // 4x4 sub-quarters per tile (one per four-lane group)
+constexpr int kListPitch = kBatch + 4;  // sub-quarter lists start in different banks
 
 // Two horizontally adjacent pixels (same row) as packed f32x2 lanes: .x = (x0, y), .y = (x0+1, y).
 // Packed FFMA2/FMUL2/FADD2 issue once for both pixels.
@@ -70,29 +73,24 @@ __device__ __forceinline__ void bwd_pair(BwdPair& p, bool act0, bool act1, int j
   acc[2] = __ffma2_rn(go, r2, acc[2]);
 }
 
-// reduce-scatter of 8 values over a 16-lane half-warp in 8 shuffles: lane l returns the sum
-// over its half of value (l >> 1) & 7.
-__device__ __forceinline__ float reduce_scatter8_half(const float v[8]) {
+// reduce-scatter of 8 values over a 4-lane group in 6 shuffles: lane l (l4 = l & 3) returns the
+// group sums of values 4*(l4>>1) + 2*(l4&1) + {0, 1} in out[0], out[1].
+__device__ __forceinline__ void reduce_scatter8_quad(const float v[8], float out[2]) {
   const int lane = threadIdx.x & 31;
-  const bool b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
-  float w[4], x[2];
+  const bool b1 = lane & 2, b0 = lane & 1;
+  float w[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const float send = b3 ? v[i] : v[i + 4];
-    const float keep = b3 ? v[i + 4] : v[i];
-    w[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    const float send = b1 ? v[i] : v[i + 4];
+    const float keep = b1 ? v[i + 4] : v[i];
+    w[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
   }
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
-    const float send = b2 ? w[i] : w[i + 2];
-    const float keep = b2 ? w[i + 2] : w[i];
-    x[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    const float send = b0 ? w[i] : w[i + 2];
+    const float keep = b0 ? w[i + 2] : w[i];
+    out[i] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
   }
-  const float send = b1 ? x[0] : x[1];
-  const float keep = b1 ? x[1] : x[0];
-  float y = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-  y += __shfl_xor_sync(0xffffffffu, y, 1);
-  return y;
 }
 
 }  // namespace
@@ -107,10 +105,10 @@ __global__ void __launch_bounds__(kBT) k_blend_bwd(
     const float* __restrict__ t_last, const uint32_t* __restrict__ n_proc, float loss_scale,
     float4* __restrict__ partial, double* __restrict__ tile_loss) {
   __shared__ Stage<kBatch> st[2];
-  // [quarter][value][entry]; rows padded so one entry's 8 values hit 8 different banks
-  __shared__ float s_part[4][8][kBatch + 1];
-  __shared__ uint32_t s_rel[4][kBatch / 32];
-  __shared__ uint8_t s_list[4][kBatch];
+  // [sub-quarter][value][entry]; rows padded so one entry's 8 values hit 8 different banks
+  __shared__ float s_part[kSubs][8][kBatch + 1];
+  __shared__ uint32_t s_rel[kSubs];  // relevance ballot of the batch per sub-quarter
+  __shared__ uint8_t s_list[kSubs][kListPitch];
   __shared__ float s_red[2];
   __shared__ int s_max[2];
   const int tile = blockIdx.x;
@@ -119,15 +117,32 @@ __global__ void __launch_bounds__(kBT) k_blend_bwd(
     return;
   }
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int h = lane >> 4, l16 = lane & 15;
-  const int q = 2 * w + h;  // this half-warp's quarter-tile
+  const int gq = lane >> 2, l4 = lane & 3;  // four-lane group = one 4x4 sub-quarter
+  const int sub = 8 * w + gq;               // q = sub >> 2 (quarter), sub & 3 within it
+  const int q = sub >> 2, sq = sub & 3;
   const int tx = tile % fp.tiles_x, ty = tile / fp.tiles_x;
   const int W = fp.cam.width, H = fp.cam.height;
-  const int x0 = tx * kTile + (q & 1) * 8 + 2 * (l16 & 3);
-  const int y0 = ty * kTile + (q >> 1) * 8 + 2 * (l16 >> 2);
+  const int x0 = tx * kTile + (q & 1) * 8 + (sq & 1) * 4 + 2 * (l4 & 1);
+  const int y0 = ty * kTile + (q >> 1) * 8 + (sq >> 1) * 4 + 2 * (l4 >> 1);
   const float2 PX = make_float2((float)x0 + 0.5f, (float)x0 + 1.5f);
   const float2 PY = make_float2((float)y0 + 0.5f, (float)y0 + 1.5f);
-  const Region regA = region_rect(fp, tile, 2 * w), regB = region_rect(fp, tile, 2 * w + 1);
+  // the warp's 8 sub-quarters: 4 columns of the tile (x = 4c) x 2 rows (y = 8w + 4r)
+  float cx0[4], cx1[4], ry0[2], ry1[2];
+  bool cv[4], rv[2];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int xs = tx * kTile + 4 * c;
+    cv[c] = xs < W;
+    cx0[c] = (float)xs + 0.5f;
+    cx1[c] = (float)(min(xs + 4, W) - 1) + 0.5f;
+  }
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int ys = ty * kTile + 8 * w + 4 * r;
+    rv[r] = ys < H;
+    ry0[r] = (float)ys + 0.5f;
+    ry1[r] = (float)(min(ys + 4, H) - 1) + 0.5f;
+  }
   const uint2 rg = ranges[tile];
   const int n = (int)(rg.y - rg.x);
 
@@ -202,44 +217,55 @@ __global__ void __launch_bounds__(kBT) k_blend_bwd(
       const int nlo = max(0, lo - kBatch);
       stage_batch(st[(it + 1) & 1], sorted, rec, rg.x + nlo, lo - nlo);
     }
-    // relevance of the batch for this warp's two quarters -> two compacted lists
-    int cntA = 0, cntB = 0;
+    // relevance of the batch for the warp's 8 sub-quarters -> 8 compacted lists.  The tests
+    // share their per-axis terms (rounded squares of the distances to the 4 columns and 2
+    // rows) and add one pair exactly as rect_hit's dist2_rn would.
+    bool hs[8];
+    {
+      const int j = lane;
+      const bool in = j < cnt;
+      const float4 g = cur.geo[in ? j : 0];
+      float ax4[4], ay2[2];
 #pragma unroll
-    for (int k = 0; k < kBatch / 32; ++k) {
-      const int j = 32 * k + lane;
-      bool ha = false, hb = false;
-      if (j < cnt) {
-        const float4 g = cur.geo[j];
-        ha = regA.valid && rect_hit(regA, g.x, g.y, g.z);
-        hb = regB.valid && rect_hit(regB, g.x, g.y, g.z);
+      for (int c = 0; c < 4; ++c) {
+        const float d = __fsub_rn(fminf(fmaxf(g.x, cx0[c]), cx1[c]), g.x);
+        ax4[c] = __fmul_rn(d, d);
       }
-      const uint32_t ma = __ballot_sync(0xffffffffu, ha);
-      const uint32_t mb = __ballot_sync(0xffffffffu, hb);
-      if (ha) s_list[2 * w][cntA + __popc(ma & lt)] = (uint8_t)j;
-      if (hb) s_list[2 * w + 1][cntB + __popc(mb & lt)] = (uint8_t)j;
-      cntA += __popc(ma);
-      cntB += __popc(mb);
-      if (lane == 0) {
-        s_rel[2 * w][k] = ma;
-        s_rel[2 * w + 1][k] = mb;
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const float d = __fsub_rn(fminf(fmaxf(g.y, ry0[r]), ry1[r]), g.y);
+        ay2[r] = __fmul_rn(d, d);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {  // group k: quarter 2w + (k >> 2), sub (k & 3)
+        const int c = (k >> 2) * 2 + (k & 1), r = (k >> 1) & 1;
+        hs[k] = in && cv[c] && rv[r] && !(__fadd_rn(ax4[c], ay2[r]) > g.z);
       }
     }
+    int my_cnt = 0, steps = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t mk = __ballot_sync(0xffffffffu, hs[k]);
+      if (hs[k]) s_list[8 * w + k][__popc(mk & lt)] = (uint8_t)lane;
+      if (lane == 0) s_rel[8 * w + k] = mk;
+      const int ck = __popc(mk);
+      steps = max(steps, ck);
+      if (k == gq) my_cnt = ck;
+    }
     __syncwarp();
-    const int my_cnt = h ? cntB : cntA;
-    const int steps = max(cntA, cntB);
+    const uint8_t* my_list = s_list[sub];
     for (int s = 0; s < steps; ++s) {
       const int i = my_cnt - 1 - s;  // reverse depth order
       const bool has = i >= 0;
-      const int jj = has ? s_list[q][i] : 0;
+      const int jj = has ? my_list[i] : 0;
       const int j = lo + jj;
       const float4 g = cur.geo[jj];
       const float4 c = cur.col[jj];
       const float2 dx = __fadd2_rn(PX, bc(-g.x));
       const float2 dy = __fadd2_rn(PY, bc(-g.y));
-      // r2 in scalar: ptxas would contract a packed mul.rn + add.rn into FFMA2 (one rounding),
-      // and the 3-sigma test must round exactly like the oracle's (and the forward's)
-      // dx^2 as fma(dx, dx, -0) = round(dx^2): one FFMA2 that ptxas does not contract with
-      // the following add (a packed mul.rn + add.rn pair it would)
+      // r2 keeps the oracle's rounding: dx^2 as fma(dx, dx, -0) = round(dx^2), which ptxas
+      // emits as an FMUL2 it does not contract with the following add (a packed mul.rn +
+      // add.rn pair it would contract into one FFMA2)
       const float2 ax = __ffma2_rn(dx, dx, bc(-0.0f));
       float2 acc2[8];
 #pragma unroll
@@ -256,23 +282,29 @@ __global__ void __launch_bounds__(kBT) k_blend_bwd(
       float acc[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) acc[k] = acc2[k].x + acc2[k].y;
-      // kernels.hpp:219-220: dg/du = g 2 dx / s^2, dg/ds = g 2 r^2 / s^3, times opacity
-      // lane l ends with value (l >> 1) & 7; du, dv scale by 2 o / s^2, dsigma2d by 2 o / s^3
+      float y[2];
+      reduce_scatter8_quad(acc, y);
+      // kernels.hpp:219-220: dg/du = g 2 dx / s^2, dg/ds = g 2 r^2 / s^3, times opacity.  The
+      // lane holds values vb, vb + 1 with vb = 4 (l4 >> 1) + 2 (l4 & 1): lane 0 (du, dv) scales
+      // both by 2 o / s^2, lane 1 (dsigma2d, dopacity) the first by 2 o / s^3.
       const float inv_s2 = g.w * -kLn2;  // 1 / sigma2d^2
-      const int vi = (l16 >> 1) & 7;
       const float k2 = 2.0f * c.w * inv_s2;
-      const float scale = vi < 2 ? k2 : (vi == 2 ? k2 * fast_sqrt(inv_s2) : 1.0f);
-      const float y = reduce_scatter8_half(acc) * scale;
-      if (has && (l16 & 1) == 0) s_part[q][l16 >> 1][jj] = y;
+      const int vb = 4 * (l4 >> 1) + 2 * (l4 & 1);
+      const float s0 = vb == 0 ? k2 : (vb == 2 ? k2 * fast_sqrt(inv_s2) : 1.0f);
+      const float s1 = vb == 0 ? k2 : 1.0f;
+      if (has) {
+        s_part[sub][vb][jj] = y[0] * s0;
+        s_part[sub][vb + 1][jj] = y[1] * s1;
+      }
     }
     __syncthreads();
-    // combine the quarters and write each (tile, splat) pair's gradient slot
+    // combine the sub-quarters in a fixed order and write each (tile, splat) pair's slot
     if ((int)threadIdx.x < cnt) {
       const int jj = threadIdx.x;
       float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        if (!((s_rel[r][jj >> 5] >> (jj & 31)) & 1u)) continue;
+#pragma unroll 4
+      for (int r = 0; r < kSubs; ++r) {
+        if (!((s_rel[r] >> jj) & 1u)) continue;
 #pragma unroll
         for (int k = 0; k < 8; ++k) v[k] += s_part[r][k][jj];
       }
