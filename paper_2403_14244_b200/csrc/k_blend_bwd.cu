@@ -28,7 +28,11 @@ namespace {
 using namespace blend;
 
 constexpr int kBT = 64;      // threads per tile CTA: 2 warps x 8 four-lane groups
-constexpr int kBatch = 32;   // records staged per batch (one relevance ballot per sub-quarter)
+#ifndef ISG_BWD_BATCH
+#define ISG_BWD_BATCH 32
+#endif
+constexpr int kBatch = ISG_BWD_BATCH;  // records staged per batch (32: one ballot per sub-quarter)
+constexpr int kWords = kBatch / 32;
 constexpr int kSubs = 16;    // 4x4 sub-quarters per tile (one per four-lane group)
 constexpr int kListPitch = kBatch + 4;  // sub-quarter lists start in different banks
 
@@ -107,7 +111,7 @@ __global__ void __launch_bounds__(kBT) k_blend_bwd(
   __shared__ Stage<kBatch> st[2];
   // [sub-quarter][value][entry]; rows padded so one entry's 8 values hit 8 different banks
   __shared__ float s_part[kSubs][8][kBatch + 1];
-  __shared__ uint32_t s_rel[kSubs];  // relevance ballot of the batch per sub-quarter
+  __shared__ uint32_t s_rel[kSubs][kWords];  // relevance ballots of the batch per sub-quarter
   __shared__ uint8_t s_list[kSubs][kListPitch];
   __shared__ float s_red[2];
   __shared__ int s_max[2];
@@ -220,9 +224,11 @@ __global__ void __launch_bounds__(kBT) k_blend_bwd(
     // relevance of the batch for the warp's 8 sub-quarters -> 8 compacted lists.  The tests
     // share their per-axis terms (rounded squares of the distances to the 4 columns and 2
     // rows) and add one pair exactly as rect_hit's dist2_rn would.
-    bool hs[8];
-    {
-      const int j = lane;
+    int my_cnt = 0, steps = 0;
+    int base[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int wd = 0; wd < kWords; ++wd) {
+      const int j = 32 * wd + lane;
       const bool in = j < cnt;
       const float4 g = cur.geo[in ? j : 0];
       float ax4[4], ay2[2];
@@ -239,18 +245,17 @@ __global__ void __launch_bounds__(kBT) k_blend_bwd(
 #pragma unroll
       for (int k = 0; k < 8; ++k) {  // group k: quarter 2w + (k >> 2), sub (k & 3)
         const int c = (k >> 2) * 2 + (k & 1), r = (k >> 1) & 1;
-        hs[k] = in && cv[c] && rv[r] && !(__fadd_rn(ax4[c], ay2[r]) > g.z);
+        const bool hk = in && cv[c] && rv[r] && !(__fadd_rn(ax4[c], ay2[r]) > g.z);
+        const uint32_t mk = __ballot_sync(0xffffffffu, hk);
+        if (hk) s_list[8 * w + k][base[k] + __popc(mk & lt)] = (uint8_t)j;
+        if (lane == 0) s_rel[8 * w + k][wd] = mk;
+        base[k] += __popc(mk);
       }
     }
-    int my_cnt = 0, steps = 0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const uint32_t mk = __ballot_sync(0xffffffffu, hs[k]);
-      if (hs[k]) s_list[8 * w + k][__popc(mk & lt)] = (uint8_t)lane;
-      if (lane == 0) s_rel[8 * w + k] = mk;
-      const int ck = __popc(mk);
-      steps = max(steps, ck);
-      if (k == gq) my_cnt = ck;
+      steps = max(steps, base[k]);
+      if (k == gq) my_cnt = base[k];
     }
     __syncwarp();
     const uint8_t* my_list = s_list[sub];
@@ -304,7 +309,7 @@ __global__ void __launch_bounds__(kBT) k_blend_bwd(
       float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll 4
       for (int r = 0; r < kSubs; ++r) {
-        if (!((s_rel[r] >> jj) & 1u)) continue;
+        if (!((s_rel[r][jj >> 5] >> (jj & 31)) & 1u)) continue;
 #pragma unroll
         for (int k = 0; k < 8; ++k) v[k] += s_part[r][k][jj];
       }
