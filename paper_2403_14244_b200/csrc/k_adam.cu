@@ -25,17 +25,31 @@ __device__ __forceinline__ void sum_slots(const float4* __restrict__ partial,
                                           uint32_t cnt, float4& a, float4& b) {
   a = make_float4(0.f, 0.f, 0.f, 0.f);
   b = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (uint32_t k = 0; k < cnt; ++k) {
-    const size_t e = slot_of ? slot_of[off + k] : (size_t)(off + k);
-    const float4 x = partial[2 * e];
-    const float4 y = partial[2 * e + 1];
-    a.x += x.x;
-    a.y += x.y;
-    a.z += x.z;
-    a.w += x.w;
-    b.x += y.x;
-    b.y += y.y;
-    b.z += y.z;
+  // kUnroll slots' loads in flight at once, then summed in slot order (same order as a plain
+  // loop, so the result is unchanged and deterministic)
+  constexpr uint32_t kUnroll = 4;
+  for (uint32_t k0 = 0; k0 < cnt; k0 += kUnroll) {
+    float4 x[kUnroll], y[kUnroll];
+#pragma unroll
+    for (uint32_t u = 0; u < kUnroll; ++u) {
+      if (k0 + u < cnt) {
+        const size_t e = slot_of ? slot_of[off + k0 + u] : (size_t)(off + k0 + u);
+        x[u] = partial[2 * e];
+        y[u] = partial[2 * e + 1];
+      }
+    }
+#pragma unroll
+    for (uint32_t u = 0; u < kUnroll; ++u) {
+      if (k0 + u < cnt) {
+        a.x += x[u].x;
+        a.y += x[u].y;
+        a.z += x[u].z;
+        a.w += x[u].w;
+        b.x += y[u].x;
+        b.y += y[u].y;
+        b.z += y[u].z;
+      }
+    }
   }
 }
 
