@@ -74,9 +74,17 @@ struct isg_ctx {
   bool radix_alloc = false;
 
   // sort / scan scratch
-  isg::SortScratch sort{};
+  isg::SortScratch sort{};  // adaptive control (zeroed per call)
   int64_t sort_tiles_alloc = 0;
-  unsigned long long* scan_scratch = nullptr;
+  // per-frame scratch, ONE allocation zeroed by ONE memset per frame: [scan look-back words |
+  // depth-sort hist+counters | tile-sort hist+counters | depth-sort look-back | tile-sort
+  // look-back]
+  unsigned char* arena = nullptr;
+  size_t arena_bytes = 0;
+  int64_t arena_n = -1, arena_cap = -1;
+  size_t arena_depth_end = 0;  // bytes to zero when only the depth sort runs (tile-bucket)
+  unsigned long long* scan_scratch = nullptr;  // = arena
+  isg::SortScratch sort_depth{}, sort_tile{};
 
   // pixels / tiles
   int64_t pix_alloc = 0, tiles_alloc = 0;
@@ -234,10 +242,39 @@ isg_status ensure_scene(isg_ctx* ctx, int64_t n) {
     ISG_CUDA(realloc_dev(&ctx->depth[i], a));
     ISG_CUDA(realloc_dev(&ctx->order[i], a));
   }
-  const int64_t words =
-      std::max(isg::scan_emit_scratch_words(a), isg::fill_scratch_words(a)) + 1;
-  ISG_CUDA(realloc_dev(&ctx->scan_scratch, words));
   ctx->n_alloc = a;
+  return ISG_OK;
+}
+
+// The per-frame scratch arena for a scene of n_alloc splats and key_cap pairs.
+isg_status ensure_arena(isg_ctx* ctx) {
+  if (ctx->arena && ctx->arena_n == ctx->n_alloc && ctx->arena_cap == ctx->key_cap) return ISG_OK;
+  const int64_t a = std::max<int64_t>(ctx->n_alloc, 1), cap = std::max<int64_t>(ctx->key_cap, 1);
+  auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t scan = align(sizeof(unsigned long long) *
+                            (std::max(isg::scan_emit_scratch_words(a), isg::fill_scratch_words(a)) + 1));
+  const size_t hist = align(sizeof(uint32_t) * (isg::kMaxPasses * 256 + isg::kMaxPasses));
+  const size_t lb_depth = align(isg::sort_lookback_bytes(a, isg::kMaxPasses));
+  const size_t lb_tile = align(isg::sort_lookback_bytes(cap, isg::kMaxPasses));
+  const size_t bytes = scan + 2 * hist + lb_depth + lb_tile;
+  if (ctx->arena) cudaFree(ctx->arena);
+  ctx->arena = nullptr;
+  ISG_CUDA(cudaMalloc(&ctx->arena, bytes));
+  ISG_CUDA(cudaMemset(ctx->arena, 0, bytes));
+  ctx->arena_bytes = bytes;
+  ctx->arena_n = ctx->n_alloc;
+  ctx->arena_cap = ctx->key_cap;
+  unsigned char* p = ctx->arena;
+  ctx->scan_scratch = reinterpret_cast<unsigned long long*>(p);
+  auto carve = [&](isg::SortScratch& ss, size_t hist_off, size_t lb_off, int64_t items) {
+    ss.hist = reinterpret_cast<uint32_t*>(p + hist_off);
+    ss.counters = ss.hist + isg::kMaxPasses * 256;
+    ss.lookback = reinterpret_cast<uint32_t*>(p + lb_off);
+    ss.max_tiles = std::max<int64_t>(isg::sort_tiles_for(items), 1);
+  };
+  carve(ctx->sort_depth, scan, scan + 2 * hist, a);
+  carve(ctx->sort_tile, scan + hist, scan + 2 * hist + lb_depth, cap);
+  ctx->arena_depth_end = scan + 2 * hist + lb_depth;
   return ISG_OK;
 }
 
@@ -372,20 +409,20 @@ isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out) {
   if (ctx->key_cap == 0) {
     if ((s = ensure_keys(ctx, std::max<int64_t>(6 * ctx->n, 1 << 20))) != ISG_OK) return s;
   }
-  if ((s = ensure_sort_scratch(ctx, std::max(ctx->key_cap, ctx->n))) != ISG_OK) return s;
+  if ((s = ensure_arena(ctx)) != ISG_OK) return s;
   const bool radix = ctx->binning == isg::kBinRadix;
   if (radix && (s = ensure_radix(ctx)) != ISG_OK) return s;
   cudaStream_t st = ctx->stream;
   const int64_t n = ctx->n;
   {
   ISG_STAGE(ST_MEMSET);
-  // scalars: n_keys=0, first_bad=~0, n_visible=0, scan counter=0
-  ISG_CUDA(cudaMemsetAsync(ctx->sc, 0, sizeof(uint32_t) * 8, st));
-  ISG_CUDA(cudaMemsetAsync(ctx->sc + 1, 0xFF, sizeof(uint32_t), st));
-  ISG_CUDA(cudaMemsetAsync(ctx->total, 0, sizeof(unsigned long long), st));
-  const int64_t words =
-      (radix ? isg::scan_emit_scratch_words(n) : isg::fill_scratch_words(n)) + 1;
-  ISG_CUDA(cudaMemsetAsync(ctx->scan_scratch, 0, sizeof(unsigned long long) * words, st));
+  // scalars sc[0..7] and the frame's key total (contiguous): all zero
+  ISG_CUDA(cudaMemsetAsync(ctx->sc, 0, sizeof(uint32_t) * 8 + sizeof(unsigned long long), st));
+  // scan look-back + both sorts' histograms, counters and look-back statuses: one memset
+  const size_t zero = radix ? (size_t)((unsigned char*)ctx->sort_tile.lookback - ctx->arena) +
+                                  isg::sort_lookback_bytes(ctx->key_cap, 2)
+                            : ctx->arena_depth_end;
+  ISG_CUDA(cudaMemsetAsync(ctx->arena, 0, zero, st));
   if (!radix) ISG_CUDA(cudaMemsetAsync(ctx->tile_cnt, 0, sizeof(uint32_t) * fp.n_tiles, st));
   }
   {
@@ -399,7 +436,7 @@ isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out) {
     {
     ISG_STAGE(ST_DEPTH_SORT);
     ctx->order_buf = isg::radix_sort_pairs(ctx->depth, ctx->order, true, ctx->sc + 4, n, 32,
-                                           ctx->sort, st, &ctx->launches);
+                                           ctx->sort_depth, st, &ctx->launches, true);
     ISG_CHECK_LAUNCH();
     }
     {
@@ -413,7 +450,8 @@ isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out) {
     {
     ISG_STAGE(ST_TILE_SORT);
     ctx->tile_buf = isg::radix_sort_pairs(ctx->tkey, ctx->tval, true, ctx->sc + 0, ctx->key_cap,
-                                          bits_for(fp.n_tiles), ctx->sort, st, &ctx->launches);
+                                          bits_for(fp.n_tiles), ctx->sort_tile, st,
+                                          &ctx->launches, true);
     ISG_CHECK_LAUNCH();
     }
     ISG_STAGE(ST_RANGES);
@@ -483,8 +521,8 @@ isg_status check_frame(isg_ctx* ctx, bool* overflow, bool with_loss = false) {
   ctx->frame_unchecked = false;
   ctx->n_visible = ctx->h_sc[2];
   ctx->n_keys = (int64_t)ctx->h_total[0];
-  if (ctx->h_sc[1] != 0xFFFFFFFFu) {
-    const uint32_t bad = ctx->h_sc[1];
+  if (ctx->h_sc[1] != 0u) {
+    const uint32_t bad = 0xFFFFFFFFu - ctx->h_sc[1];
     float a[4], c[4];
     ISG_CUDA(cudaMemcpy(a, ctx->ms + bad, sizeof a, cudaMemcpyDeviceToHost));
     ISG_CUDA(cudaMemcpy(c, ctx->co + bad, sizeof c, cudaMemcpyDeviceToHost));
@@ -497,9 +535,7 @@ isg_status check_frame(isg_ctx* ctx, bool* overflow, bool with_loss = false) {
       return fail(ctx, ISG_E_OVERFLOW, "binning: more than 2^32 (tile, splat) pairs");
     isg_status s = ensure_keys(ctx, want);
     if (s != ISG_OK) return s;
-    s = ensure_sort_scratch(ctx, std::max(ctx->key_cap, ctx->n));
-    if (s != ISG_OK) return s;
-    ctx->regrow++;
+    ctx->regrow++;  // the frame arena follows the new capacity at the next launch
   }
   return ISG_OK;
 }
@@ -619,8 +655,9 @@ isg_status isg_create(int device, int64_t max_gaussians, int32_t max_width, int3
   chk(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
   chk(cudaEventCreateWithFlags(&ctx->ev_main, cudaEventDisableTiming));
   chk(cudaEventCreateWithFlags(&ctx->ev_copy, cudaEventDisableTiming));
-  chk(cudaMalloc(&ctx->sc, sizeof(uint32_t) * 8));
-  chk(cudaMalloc(&ctx->total, sizeof(unsigned long long) * 2));
+  // sc[0..7] followed by total[0..1] (one allocation: the per-frame part is zeroed at once)
+  chk(cudaMalloc(&ctx->sc, sizeof(uint32_t) * 8 + sizeof(unsigned long long) * 2));
+  if (s == ISG_OK) ctx->total = reinterpret_cast<unsigned long long*>(ctx->sc + 8);
   chk(cudaMalloc(&ctx->loss, sizeof(double) * 4));
   chk(cudaMalloc(&ctx->adam_state, sizeof(isg::AdamState) * 2));
   chk(cudaMallocHost(&ctx->h_sc, sizeof(uint32_t) * 8));
@@ -652,9 +689,9 @@ void isg_destroy(isg_ctx* ctx) {
                  ctx->grad3d, ctx->depth[0], ctx->depth[1], ctx->order[0], ctx->order[1],
                  ctx->sorted, ctx->partial, ctx->bucket, ctx->slot_of, ctx->tkey[0], ctx->tkey[1],
                  ctx->tval[0], ctx->tval[1], ctx->emit_gid, ctx->sort.hist, ctx->sort.lookback,
-                 ctx->sort.counters, ctx->scan_scratch, ctx->img, ctx->target, ctx->t_last,
+                 ctx->sort.counters, ctx->arena, ctx->img, ctx->target, ctx->t_last,
                  ctx->n_proc, ctx->ranges, ctx->tile_cnt, ctx->cursor, ctx->tile_loss, ctx->sc,
-                 ctx->total, ctx->loss, ctx->snap, ctx->coef, ctx->dldc, ctx->ssim_part,
+                 ctx->loss, ctx->snap, ctx->coef, ctx->dldc, ctx->ssim_part,
                  ctx->adam_state};
   for (void* p : dev)
     if (p) cudaFree(p);

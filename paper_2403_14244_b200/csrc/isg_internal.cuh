@@ -15,6 +15,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "../../include/isg.h"
 
 namespace isg {
@@ -61,12 +63,18 @@ inline int64_t sort_tiles_for(int64_t cap) { return (cap + kSortTileItems - 1) /
 // Stable LSD sort of n (device count *n_dev, <= cap) pairs on bits [0, key_bits).  keys/vals
 // are ping-pong buffers; returns the index (0/1) of the buffer holding the result.  With
 // iota_vals the first pass uses the item index as the value (vals[0] is not read).
+// scratch_zeroed: the caller zeroed s (hist, counters, the passes' look-back) on the stream.
 int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], bool iota_vals, const uint32_t* n_dev,
                      int64_t cap, int key_bits, SortScratch& s, cudaStream_t st,
-                     int64_t* launches);
+                     int64_t* launches, bool scratch_zeroed = false);
+
+// Byte size of a sort's look-back region for `passes` passes over up to `cap` items.
+inline size_t sort_lookback_bytes(int64_t cap, int passes) {
+  return sizeof(uint32_t) * 256 * (size_t)std::max<int64_t>(sort_tiles_for(cap), 1) * passes;
+}
 
 // ---- K1 ------------------------------------------------------------------------------------
-// sc: [1] first invalid splat (atomicMin), [2] visible splats, [4] n.  tilebox: compact tile
+// sc: [1] 0xFFFFFFFF - first invalid splat (atomicMax; 0 = none), [2] visible splats, [4] n.  tilebox: compact tile
 // bbox + hit mask per splat (see for_each_tile).  tile_cnt (tile-bucket mode) may be null.
 void launch_preprocess(const float4* ms, const float4* co, int64_t n, const FrameParams& fp,
                        RenderRec* rec, uint32_t* depth_key, uint32_t* ntiles, uint2* tilebox,

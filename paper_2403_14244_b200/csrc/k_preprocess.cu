@@ -20,7 +20,8 @@ __global__ void __launch_bounds__(256) k_preprocess(const float4* __restrict__ m
                                                     uint2* __restrict__ tilebox,
                                                     uint32_t* __restrict__ tile_cnt,
                                                     uint32_t* __restrict__ sc) {
-  // sc: [1] first invalid splat (atomicMin), [2] visible splats, [4] n (device count)
+  // sc: [1] 0xFFFFFFFF - first invalid splat (atomicMax, 0 = none: zero-initialised with the
+  // other scalars), [2] visible splats, [4] n (device count)
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i == 0) sc[4] = (uint32_t)n;
   uint32_t count = 0;
@@ -33,7 +34,7 @@ __global__ void __launch_bounds__(256) k_preprocess(const float4* __restrict__ m
     const bool ok = isfinite(a.x) && isfinite(a.y) && isfinite(a.z) && a.w > 0.0f &&
                     isfinite(a.w) && isfinite(c.x) && isfinite(c.y) && isfinite(c.z) &&
                     c.w >= 0.0f && c.w <= 1.0f;
-    if (!ok) atomicMin(&sc[1], (uint32_t)i);
+    if (!ok) atomicMax(&sc[1], 0xFFFFFFFFu - (uint32_t)i);
     const Proj p = project(a, fp.cam);
     if (p.vis && ok) {
       int x0, x1, y0, y1;

@@ -362,13 +362,15 @@ void launch_ranges(const uint32_t* sorted_tiles, const uint32_t* e_sorted,
 
 int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], bool iota_vals, const uint32_t* n_dev,
                      int64_t cap, int key_bits, SortScratch& s, cudaStream_t st,
-                     int64_t* launches) {
+                     int64_t* launches, bool scratch_zeroed) {
   const int passes = (key_bits + 7) / 8;
   const int64_t tiles = (cap + kSortTileItems - 1) / kSortTileItems;
   // caller guarantees tiles <= s.max_tiles and passes <= kMaxPasses
-  cudaMemsetAsync(s.hist, 0, sizeof(uint32_t) * kMaxPasses * 256, st);
-  cudaMemsetAsync(s.counters, 0, sizeof(uint32_t) * kMaxPasses, st);
-  cudaMemsetAsync(s.lookback, 0, sizeof(uint32_t) * 256 * (size_t)tiles * passes, st);
+  if (!scratch_zeroed) {
+    cudaMemsetAsync(s.hist, 0, sizeof(uint32_t) * kMaxPasses * 256, st);
+    cudaMemsetAsync(s.counters, 0, sizeof(uint32_t) * kMaxPasses, st);
+    cudaMemsetAsync(s.lookback, 0, sizeof(uint32_t) * 256 * (size_t)tiles * passes, st);
+  }
   const int hist_blocks = (int)std::min<int64_t>(std::max<int64_t>(tiles, 1), 148 * 4);
   k_hist<<<hist_blocks, 256, 0, st>>>(keys[0], n_dev, cap, passes, s.hist);
   int cur = 0;
