@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -1373,9 +1374,13 @@ NcclApi& nccl() {
   static bool tried = false;
   if (tried) return api;
   tried = true;
+  // 1. an NCCL already in the process (e.g. the one torch loaded) — sharing it avoids two
+  //    NCCL versions under one SONAME; 2. $ISG_NCCL_LIB; 3. the loader's search path.
   void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
-  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  const char* env = std::getenv("ISG_NCCL_LIB");
+  if (!h && env && *env) h = dlopen(env, RTLD_NOW | RTLD_LOCAL);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_LOCAL);
   if (!h) return api;
   api.get_unique_id = (decltype(api.get_unique_id))dlsym(h, "ncclGetUniqueId");
   api.comm_init_rank = (decltype(api.comm_init_rank))dlsym(h, "ncclCommInitRank");

@@ -231,6 +231,17 @@ class AdamConfig:
         return (C.c_float * 4)(self.lr_mu, self.lr_sigma, self.lr_color, self.lr_opacity)
 
 
+def _process_nccl() -> None:
+    """libisg resolves NCCL at run time and prefers one already loaded in the process.  Load
+    torch's bundled NCCL first (importing torch does) so that the process holds one NCCL —
+    otherwise an older system libnccl.so.2 loaded here would later shadow torch's (same
+    SONAME) and break `import torch`."""
+    try:
+        import torch  # noqa: F401
+    except Exception:
+        pass
+
+
 def _check(ctx, status: int) -> None:
     if status == ISG_OK:
         return
@@ -477,11 +488,13 @@ class Renderer:
     # -- multi-GPU --------------------------------------------------------------------------
     @staticmethod
     def nccl_unique_id() -> bytes:
+        _process_nccl()
         buf = (C.c_char * 128)()
         _check(None, lib().isg_nccl_get_unique_id(buf))
         return bytes(buf)
 
     def nccl_init(self, nranks: int, rank: int, uid: bytes):
+        _process_nccl()
         buf = (C.c_char * 128).from_buffer_copy(uid)
         _check(self._h, lib().isg_nccl_init(self._h, nranks, rank, buf))
 

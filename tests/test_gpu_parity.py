@@ -448,3 +448,40 @@ def test_nccl_single_rank_path_matches_local_adam():
     np.testing.assert_array_equal(a[0], b[0])
     np.testing.assert_array_equal(a[1], b[1])
     assert la == lb
+
+
+def test_cuda_graph_with_nccl_single_rank():
+    """The multi-GPU step (NCCL all-reduce + un-fused Adam) captured in a CUDA graph replays
+    like kernel-by-kernel execution (one rank)."""
+    import torch
+    W, H, n, K = 96, 64, 2000, 4
+    ms, co = isg.synth_scene(n, W, H, seed=51)
+    tms, tco = isg.synth_scene(n, W, H, seed=52)
+    cam = isg.Camera.synthetic(W, H)
+    target = torch.from_numpy(O.render32(tms, tco, cam)).cuda()
+    torch.cuda.synchronize()
+    out = []
+    for use_graph in (False, True):
+        r = isg.Renderer(0)
+        r.set_scene(ms, co)
+        r.nccl_init(1, 0, isg.Renderer.nccl_unique_id())
+        r.loss_backward_device(cam, target.data_ptr())
+        r.adam_step()
+        if use_graph:
+            r.graph_begin()
+            r.loss_backward_device(cam, target.data_ptr())
+            r.adam_step()
+            g = r.graph_end()
+            for _ in range(K):
+                g.launch()
+            g.close()
+        else:
+            for _ in range(K):
+                r.loss_backward_device(cam, target.data_ptr())
+                r.adam_step()
+        out.append((r.get_scene(), r.last_step_loss()))
+        r.nccl_detach()
+        r.close()
+    np.testing.assert_array_equal(out[0][0][0], out[1][0][0])
+    np.testing.assert_array_equal(out[0][0][1], out[1][0][1])
+    assert out[0][1] == out[1][1]
