@@ -206,19 +206,22 @@ def run_reference(args):
             print(json.dumps(line), flush=True)
             return
     target = O.render32(tms, tco, cam, t_min=T_MIN)
-    for _ in range(args.warmup):
-        cpu_oracle_train_step(ms, co, cam, target, 1, cores)
-    times = [cpu_oracle_train_step(ms, co, cam, target, 1, cores) for _ in range(args.steps)]
+    # bounded: at most one warm-up step and ~60 s of timed steps, so that the arm ends within
+    # a few minutes for any --steps (the line reports the steps actually timed)
+    first = cpu_oracle_train_step(ms, co, cam, target, 1, cores)  # the warm-up step
+    steps = max(1, min(args.steps, int(60.0 / max(first, 1e-3))))
+    times = [cpu_oracle_train_step(ms, co, cam, target, 1, cores) for _ in range(steps)]
     sec = float(np.median(times))
     val = 1.0 / sec
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "iters/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
+            "n_gpus": world, "steps": steps, "steps_requested": args.steps, "warmup": 1,
+            "ms_per_step": sec * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (isg-synth v1, seeds 2403/14244)",
             "config": {"workload": desc, "n_gaussians": n, "width": W, "height": H,
                        "t_min": T_MIN},
             "cpu_baseline": {"value": val, "unit": "iters/s", "cores": cores, "kind": "port",
-                             "sample": f"{args.steps} full {args.config.upper()} train steps "
+                             "sample": f"{steps} full {args.config.upper()} train steps "
                                        "(fwd+L2+bwd+Adam) of the "
                                        "FP32 tiled CPU oracle; the reference itself has no 3D "
                                        "backward (SPEC.md:484)"},
