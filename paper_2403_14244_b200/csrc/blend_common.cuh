@@ -53,31 +53,5 @@ __device__ __forceinline__ void stage_batch(Stage<B>& st, const uint2* __restric
   cp_async_commit();
 }
 
-// Pixel-centre rectangle of an 8x8 region, clipped to the image.
-struct Region {
-  float x0, x1, y0, y1;
-  bool valid;
-};
-
-__device__ __forceinline__ Region region_rect(const FrameParams& fp, int tile, int r) {
-  Region g;
-  const int tx = tile % fp.tiles_x, ty = tile / fp.tiles_x;
-  const int W = fp.cam.width, H = fp.cam.height;
-  const int x0 = tx * kTile + (r & 1) * 8, y0 = ty * kTile + (r >> 1) * 8;
-  g.valid = x0 < W && y0 < H;
-  g.x0 = (float)x0 + 0.5f;
-  g.x1 = (float)(min(x0 + 8, W) - 1) + 0.5f;
-  g.y0 = (float)y0 + 0.5f;
-  g.y1 = (float)(min(y0 + 8, H) - 1) + 0.5f;
-  return g;
-}
-
-// 3-sigma circle vs pixel-centre rectangle (conservative, exact rounding like tile_hit).
-__device__ __forceinline__ bool rect_hit(const Region& g, float u, float v, float r2max) {
-  const float cx = fminf(fmaxf(u, g.x0), g.x1);
-  const float cy = fminf(fmaxf(v, g.y0), g.y1);
-  return !(dist2_rn(__fsub_rn(cx, u), __fsub_rn(cy, v)) > r2max);
-}
-
 }  // namespace blend
 }  // namespace isg

@@ -3,13 +3,14 @@
 // Pipeline of one view (all on one stream, no host sync inside a frame):
 //   K1  k_preprocess      per splat: validate, project, 3-sigma radius, tile count, 32-B record
 //   binning (two interchangeable modes, identical output):
-//     tile-bucket (default)  K2 k_tile_scan -> K3 k_fill -> K4 k_tile_sort   (k_bin.cu)
-//     radix                  onesweep depth sort -> k_scan_emit -> onesweep tile sort ->
+//     radix (default)        onesweep depth sort -> k_scan_emit -> onesweep tile sort ->
 //                            k_ranges                                        (k_sort.cu)
+//     tile-bucket            K2 k_tile_scan -> K3 k_fill -> K4 k_tile_sort   (k_bin.cu)
 //     output: per-tile ranges and, per list entry, (splat, gradient slot) in (depth, index)
 //     order; per splat, the list of its gradient slots.
 //   K6  k_blend_fwd       16x16-tile front-to-back blend with early termination
-//   K7  k_blend_bwd       reverse walk + fused L2 gradient -> per-(tile, splat) gradient slots
+//   K7  k_blend_bwd       reverse walk + fused L2 gradient (or a given dL/dC, k_ssim.cu) ->
+//                         per-(tile, splat) gradient slots
 //   K8  k_project_adam    per-splat slot sum, projection backward (+ Adam when fused)
 #pragma once
 #include <cuda_runtime.h>

@@ -28,6 +28,12 @@ constexpr int kBT = 128;     // threads per tile CTA (4 warps x 32 pixel pairs)
 constexpr int kBatch = 128;  // records staged per batch (one per thread)
 constexpr int kListPitch = kBatch + 4;  // sub-quarter lists start in different banks
 
+// Pixel-centre rectangle of a region, clipped to the image.
+struct Region {
+  float x0, x1, y0, y1;
+  bool valid;
+};
+
 // 4x4 sub-quarter s (0..3) of quarter-tile w, pixel-centre rectangle clipped to the image.
 __device__ __forceinline__ Region sub_rect(const FrameParams& fp, int tile, int w, int s) {
   Region g;
@@ -46,7 +52,8 @@ __device__ __forceinline__ Region sub_rect(const FrameParams& fp, int tile, int 
 // list[s] (ascending); count[s] receives the lengths.  The four closest-point tests share their
 // per-axis terms: the rounded squares of the x distances to the left / right sub-quarter
 // columns and of the y distances to the top / bottom rows are computed once, and each test
-// adds one pair exactly as rect_hit's dist2_rn would (bit-identical decisions).
+// adds one pair exactly as dist2_rn (isg_math.cuh) would at the sub-quarter's closest pixel
+// centre (bit-identical decisions; a conservative superset of the per-pixel 3-sigma test).
 __device__ __forceinline__ void warp_relevant_lists(const Stage<kBatch>& st, const Region rs[4],
                                                     int cnt, uint8_t (*list)[kListPitch],
                                                     int count[4]) {

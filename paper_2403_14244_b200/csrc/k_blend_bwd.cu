@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(kBT) k_blend_bwd(
     }
     // relevance of the batch for the warp's 8 sub-quarters -> 8 compacted lists.  The tests
     // share their per-axis terms (rounded squares of the distances to the 4 columns and 2
-    // rows) and add one pair exactly as rect_hit's dist2_rn would.
+    // rows) and add one pair exactly as dist2_rn would at the sub-quarter's closest pixel centre.
     int my_cnt = 0, steps = 0;
     int base[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
