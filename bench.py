@@ -50,6 +50,18 @@ FP32_LANES = 148 * 128
 NCU_SUMMARY = "profiles/r1/ncu_full_blend.json"  # dram traffic per launch, --set full capture
 
 
+def stage_bytes(n, keys, tiles):
+    """Algorithmic DRAM bytes per step of the memory-bound stages:
+    K1 32 B read + 56 B written per splat; onesweep: 4 B histogram read + per pass 8 B read +
+    8 B written per item (depth: 4 passes over n, tiles: 2 passes over the keys); scan/emit:
+    order + tile count + tile box + slot offset (20 B) per splat, tile key + splat (8 B) per
+    key; ranges: 12 B read + 8 B written per key + 8 B per tile; K8: 96 B read + 96 B written
+    per splat + 32 B per gradient slot."""
+    return {"preprocess": 88 * n, "depth_sort": (4 + 4 * 16) * n,
+            "scan_emit": 20 * n + 8 * keys, "tile_sort": (4 + 2 * 16) * keys,
+            "ranges": 20 * keys + 8 * tiles, "project_adam": 192 * n + 32 * keys}
+
+
 def ncu_traffic(kernel: str):
     """dram__bytes_read.sum + dram__bytes_write.sum of `kernel` from the committed capture."""
     try:
@@ -467,13 +479,19 @@ def run_isg(args):
                              f"{in_p} in-circle pixel-splat pairs)",
                      "peak_kind": f"spec FP32 FMA rate at the measured sm_max_mhz {sm_mhz:.0f}"})
     else:
-        gb = {"preprocess": 56 * n, "project_adam": 192 * n, "depth_sort": 4 * 16 * n,
-              "tile_sort": 2 * 16 * st["n_keys"], "scan_emit": 48 * n + 8 * st["n_keys"]}.get(top_name)
+        gb = stage_bytes(n, st["n_keys"], st["n_tiles"]).get(top_name)
         if gb:
             achieved = gb / (top_ms / 1e3) / 1e9
             roof.update({"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
                          "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": None,
                          "peak_kind": peak_kind})
+    # every memory-bound stage against HBM: algorithmic bytes / CUDA-event time per step
+    stage_ms = {k: v[0] / prof_steps for k, v in prof.items()}
+    roof["hbm_stages"] = {
+        k: {"ms": stage_ms[k], "bytes": b, "GB/s": b / (stage_ms[k] / 1e3) / 1e9,
+            "frac": b / (stage_ms[k] / 1e3) / 1e9 / peaks["hbm_gbs"]}
+        for k, b in stage_bytes(n, st["n_keys"], st["n_tiles"]).items()
+        if stage_ms.get(k, 0) > 0}
     roof["ms_per_launch"] = top_ms
 
     clk = clocks.summary()
