@@ -138,18 +138,12 @@ __global__ void __launch_bounds__(kBT) k_blend_fwd(
     warp_relevant_lists(cur, sub, min(kBatch, n - b), s_list[w], cnt);
     const int steps = max(max(cnt[0], cnt[1]), max(cnt[2], cnt[3]));
     const int my_cnt = sq == 0 ? cnt[0] : (sq == 1 ? cnt[1] : (sq == 2 ? cnt[2] : cnt[3]));
-    // the four 8-lane groups walk their own sub-quarter lists in lockstep; the next entry's
-    // index and record are loaded one iteration ahead (hides the shared-memory latency chain)
+    // the four 8-lane groups walk their own sub-quarter lists in lockstep
     const uint8_t* my_list = s_list[w][sq];
-    int jn = my_cnt > 0 ? my_list[0] : 0;
-    float4 gn = cur.geo[jn], cn = cur.col[jn];
     for (int i = 0; i < steps; ++i) {
       const bool has = i < my_cnt;
-      const int jj = jn;
-      const float4 g = gn, c = cn;
-      jn = i + 1 < my_cnt ? my_list[i + 1] : 0;
-      gn = cur.geo[jn];
-      cn = cur.col[jn];
+      const int jj = has ? my_list[i] : 0;
+      const float4 g = cur.geo[jj], c = cur.col[jj];
       const float dx = __fsub_rn(px, g.x);
       const float ax = __fmul_rn(dx, dx);
       const float2 dy = __fadd2_rn(PY, make_float2(-g.y, -g.y));
