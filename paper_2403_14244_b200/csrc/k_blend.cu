@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(kBT) k_blend_fwd(
   float Tl0 = 1.0f, Tl1 = 1.0f;
   float2 Cr = make_float2(0.f, 0.f), Cg = Cr, Cb = Cr;
   uint32_t np0 = 0, np1 = 0;
-  const float2 kOne = make_float2(1.0f, 1.0f), kMinusOne = make_float2(-1.0f, -1.0f);
+  const float2 kOne = make_float2(1.0f, 1.0f);
 
   if (n > 0) stage_batch(st[0], sorted, rec, rg.x, min(kBatch, n));
   for (int b = 0, it = 0; b < n; b += kBatch, ++it) {
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(kBT) k_blend_fwd(
       Tl1 = in1 ? T.y : Tl1;
       np0 = in0 ? idx : np0;
       np1 = in1 ? idx : np1;
-      T = __fmul2_rn(T, __ffma2_rn(a, kMinusOne, kOne));  // T (1 - a)
+      T = __fmul2_rn(T, __fadd2_rn(kOne, make_float2(-a.x, -a.y)));  // T (1 - a)
     }
   }
   const float T0 = T.x, T1 = T.y;

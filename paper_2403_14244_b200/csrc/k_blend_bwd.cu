@@ -58,7 +58,7 @@ __device__ __forceinline__ void bwd_pair(BwdPair& p, bool act0, bool act1, int j
   const float2 q = __fmul2_rn(r2, bc(g.w));
   const float2 e = make_float2(act0 ? fast_exp2(q.x) : 0.0f, act1 ? fast_exp2(q.y) : 0.0f);
   const float2 a = __fmul2_rn(bc(c.w), e);
-  const float2 om = __ffma2_rn(a, bc(-1.0f), bc(1.0f));  // 1 - a
+  const float2 om = __fadd2_rn(bc(1.0f), make_float2(-a.x, -a.y));  // 1 - a (FADD2 imm)
   const float2 Tr = __fmul2_rn(p.T, make_float2(fast_rcp(om.x), fast_rcp(om.y)));
   const float2 Tk = make_float2(j == p.np0 - 1 ? p.T.x : Tr.x, j == p.np1 - 1 ? p.T.y : Tr.y);
   p.T = Tk;
