@@ -48,6 +48,19 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 
+// Lanes of the warp holding the same 9-bit value (digit, or 256 = no item): 9 ballots instead of
+// one match.any (a slow MIO-pipe instruction on this part).
+__device__ __forceinline__ uint32_t warp_match9(uint32_t d) {
+  uint32_t peers = 0xffffffffu;
+#pragma unroll
+  for (int b = 0; b < 9; ++b) {
+    const bool bit = (d >> b) & 1u;
+    const uint32_t m = __ballot_sync(0xffffffffu, bit);
+    peers &= bit ? m : ~m;
+  }
+  return peers;
+}
+
 // Exclusive scan of one u32 per thread over a 256-thread block.  s_warp: >= 8 words.
 __device__ __forceinline__ uint32_t block_excl_scan_256(uint32_t v, uint32_t* s_warp,
                                                         uint32_t& total) {
@@ -161,11 +174,15 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
     const uint32_t d = dig[j];
-    const uint32_t peers = __match_any_sync(0xffffffffu, d);
-    const uint32_t before = S.wcnt[w][d];
+    const uint32_t peers = warp_match9(d);
+    // only each digit's leader lane touches the counter; the others get it by shuffle, so
+    // one __syncwarp per round orders the rounds
+    const int leader = __ffs(peers) - 1;
+    uint32_t before = 0;
+    if (lane == leader) before = S.wcnt[w][d];
+    before = __shfl_sync(0xffffffffu, before, leader);
     rank[j] = before + __popc(peers & lt);
-    __syncwarp();
-    if (lane == __ffs(peers) - 1) S.wcnt[w][d] = before + __popc(peers);
+    if (lane == leader) S.wcnt[w][d] = before + __popc(peers);
     __syncwarp();
   }
   __syncthreads();

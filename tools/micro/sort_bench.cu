@@ -4,6 +4,7 @@
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include \
 //   tools/micro/sort_bench.cu paper_2403_14244_b200/csrc/k_sort.cu -o tools/micro/sort_bench
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <random>
@@ -89,5 +90,14 @@ int main() {
     for (int j = 0; j < c && tile.size() < 3360000; ++j) tile.push_back((t + (j & 1) + 120 * (j >> 1)) % 8160);
   }
   run("tile", tile, false, 13, 20);
+  if (getenv("SORT_BIG")) {  // C5-sized tile sort: 33M keys over 32400 tiles (15 bits)
+    std::vector<uint32_t> big;
+    std::uniform_int_distribution<int> ub(0, 32399);
+    while (big.size() < 33000000) {
+      int t = ub(rng), c = nt(rng);
+      for (int j = 0; j < c && big.size() < 33000000; ++j) big.push_back((t + (j & 1) + 240 * (j >> 1)) % 32400);
+    }
+    run("big", big, false, 15, 5);
+  }
   return 0;
 }
