@@ -254,7 +254,7 @@ isg_status ensure_arena(isg_ctx* ctx) {
   auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
   const size_t scan = align(sizeof(unsigned long long) *
                             (std::max(isg::scan_emit_scratch_words(a), isg::fill_scratch_words(a)) + 1));
-  const size_t hist = align(sizeof(uint32_t) * (isg::kMaxPasses * 256 + isg::kMaxPasses));
+  const size_t hist = align(sizeof(uint32_t) * (isg::kMaxPasses * 256 + isg::kMaxPasses + 1));
   const size_t lb_depth = align(isg::sort_lookback_bytes(a, isg::kMaxPasses));
   const size_t lb_tile = align(isg::sort_lookback_bytes(cap, isg::kMaxPasses));
   const size_t bytes = scan + 2 * hist + lb_depth + lb_tile;
@@ -284,7 +284,7 @@ isg_status ensure_sort_scratch(isg_ctx* ctx, int64_t cap) {
   if (tiles <= ctx->sort_tiles_alloc && ctx->sort.hist) return ISG_OK;
   const int64_t t = std::max<int64_t>(tiles, 1);
   ISG_CUDA(realloc_dev(&ctx->sort.hist, isg::kMaxPasses * 256));
-  ISG_CUDA(realloc_dev(&ctx->sort.counters, isg::kMaxPasses));
+  ISG_CUDA(realloc_dev(&ctx->sort.counters, isg::kMaxPasses + 1));
   ISG_CUDA(realloc_dev(&ctx->sort.lookback, (size_t)isg::kMaxPasses * 256 * t));
   ctx->sort.max_tiles = t;
   ctx->sort_tiles_alloc = t;

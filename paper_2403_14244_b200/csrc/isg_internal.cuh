@@ -53,9 +53,9 @@ constexpr int kSortTileItems = kSortThreads * kSortItems;
 constexpr int kMaxPasses = 4;
 
 struct SortScratch {
-  uint32_t* hist;       // kMaxPasses x 256 global digit histograms
+  uint32_t* hist;       // kMaxPasses x 256 global digit histograms -> exclusive digit offsets
   uint32_t* lookback;   // kMaxPasses x max_tiles x 256 status words
-  uint32_t* counters;   // kMaxPasses dynamic tile counters
+  uint32_t* counters;   // kMaxPasses dynamic tile counters + 1 histogram completion counter
   int64_t max_tiles;    // per pass
 };
 

@@ -88,7 +88,8 @@ __device__ __forceinline__ uint32_t block_excl_scan_256(uint32_t v, uint32_t* s_
 // ---- upfront histogram of all passes -------------------------------------------------------
 __global__ void __launch_bounds__(256) k_hist(const uint32_t* __restrict__ keys,
                                               const uint32_t* __restrict__ n_dev, int64_t cap,
-                                              int passes, uint32_t* __restrict__ hist) {
+                                              int passes, uint32_t* __restrict__ hist,
+                                              uint32_t* __restrict__ done) {
   __shared__ uint32_t sh[kMaxPasses][256];
   for (int i = threadIdx.x; i < kMaxPasses * 256; i += 256) (&sh[0][0])[i] = 0;
   __syncthreads();
@@ -128,6 +129,22 @@ __global__ void __launch_bounds__(256) k_hist(const uint32_t* __restrict__ keys,
   for (int p = 0; p < passes; ++p) {
     const uint32_t c = sh[p][threadIdx.x];
     if (c) atomicAdd(&hist[p * 256 + threadIdx.x], c);
+  }
+  // the last block to finish turns the global histograms into exclusive digit offsets, once
+  // for all onesweep CTAs (done: a zeroed counter)
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  __shared__ uint32_t s_warp[8];
+  for (int p = 0; p < passes; ++p) {
+    const uint32_t c = __ldcg(&hist[p * 256 + threadIdx.x]);
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan_256(c, s_warp, tot);
+    hist[p * 256 + threadIdx.x] = ex;
   }
 }
 
@@ -212,7 +229,7 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
       S.vals[pos] = val[j];
     }
   }
-  const uint32_t gpre = block_excl_scan_256(hist[tid], S.warp_tmp, tot);
+  const uint32_t gpre = hist[tid];  // exclusive digit offset (k_hist's last block scanned)
   // decoupled look-back for digit `tid`
   uint32_t excl = 0;
   if (tile > 0) {
@@ -385,11 +402,12 @@ int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], bool iota_vals, const
   // caller guarantees tiles <= s.max_tiles and passes <= kMaxPasses
   if (!scratch_zeroed) {
     cudaMemsetAsync(s.hist, 0, sizeof(uint32_t) * kMaxPasses * 256, st);
-    cudaMemsetAsync(s.counters, 0, sizeof(uint32_t) * kMaxPasses, st);
+    cudaMemsetAsync(s.counters, 0, sizeof(uint32_t) * (kMaxPasses + 1), st);
     cudaMemsetAsync(s.lookback, 0, sizeof(uint32_t) * 256 * (size_t)tiles * passes, st);
   }
   const int hist_blocks = (int)std::min<int64_t>(std::max<int64_t>(tiles, 1), 148 * 4);
-  k_hist<<<hist_blocks, 256, 0, st>>>(keys[0], n_dev, cap, passes, s.hist);
+  k_hist<<<hist_blocks, 256, 0, st>>>(keys[0], n_dev, cap, passes, s.hist,
+                                      s.counters + kMaxPasses);
   int cur = 0;
   const size_t smem = sizeof(OnesweepSmem);
   static const bool attr_set = [&] {  // once, outside any graph capture

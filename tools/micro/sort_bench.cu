@@ -28,7 +28,7 @@ static void run(const char* name, std::vector<uint32_t>& hk, bool iota, int bits
   isg::SortScratch s{};
   const int64_t tiles = isg::sort_tiles_for(cap);
   cudaMalloc(&s.hist, isg::kMaxPasses * 256 * 4);
-  cudaMalloc(&s.counters, isg::kMaxPasses * 4);
+  cudaMalloc(&s.counters, (isg::kMaxPasses + 1) * 4);
   cudaMalloc(&s.lookback, (size_t)isg::kMaxPasses * 256 * tiles * 4);
   s.max_tiles = tiles;
   cudaStream_t st;
