@@ -371,6 +371,22 @@ def run_isg(args):
     host_out = torch.empty((H, W, 3), dtype=torch.float32).pin_memory().numpy()
     e2e_ms = []
     use_pipe = train and graph is not None
+    use_rpipe = (not train) and graph is not None
+    if use_rpipe:
+        # render: frame i into device image i % 2 (one graph each), its D2H into pinned host
+        # image i % 2 on a copy stream while frame i + 1 renders; frame i's read is complete
+        # (synchronised) before frame i + 2 reuses the buffers
+        rbufs = [torch.empty((H, W, 3), dtype=torch.float32, device="cuda") for _ in range(2)]
+        rhost = [torch.empty((H, W, 3), dtype=torch.float32).pin_memory() for _ in range(2)]
+        rgraphs = []
+        for b in range(2):
+            r.graph_begin()
+            r.render_device(cams[0], opts, rbufs[b].data_ptr())
+            rgraphs.append(r.graph_end())
+        copy_stream = torch.cuda.Stream()
+        ev_done = [torch.cuda.Event() for _ in range(2)]
+        ev_read = [torch.cuda.Event() for _ in range(2)]
+        r.synchronize()
     if use_pipe:
         bufs = [[torch.empty_like(t) for t in targets] for _ in range(2)]
         graphs = []
@@ -415,9 +431,22 @@ def run_isg(args):
                 r.loss_backward(c, h, opts, weight=1.0 / step_views)  # H2D target, D2H loss
             r.adam_step(cfg)
             r.synchronize()
+        elif use_rpipe:
+            b = i & 1
+            if i >= 2:
+                ev_read[b].synchronize()  # frame i - 2 is on the host: its buffers are free
+            rgraphs[b].launch()
+            ev_done[b].record(stream)
+            with torch.cuda.stream(copy_stream):
+                copy_stream.wait_event(ev_done[b])
+                rhost[b].copy_(rbufs[b], non_blocking=True)
+                ev_read[b].record(copy_stream)
         else:
             r.render(cams[0], opts, out=host_out)  # D2H image into pinned memory
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    if use_rpipe:
+        for e in ev_read:
+            e.synchronize()  # the last frames' images are on the host
     e2e_total_ms = (time.perf_counter() - t_start) * 1e3
     launches_per_step = (r.stats()["kernel_launches"] - l0) / args.steps
     e2e_step = e2e_total_ms / args.steps
@@ -516,6 +545,9 @@ def run_isg(args):
                 "ms_per_step": e2e_step,
                 "mode": ("cuda graph per step, next step's targets prefetched from pinned host "
                          "memory on a copy stream, loss read back every step") if use_pipe else
+                        ("cuda graph per frame into a double-buffered device image, each image "
+                         "copied to pinned host memory on a copy stream while the next renders")
+                        if use_rpipe else
                         ("isg_loss_backward with host targets per view + adam_step + sync"
                          if train else "isg_render into pinned host memory")},
         "gpu_launches": int(launches_timed),
