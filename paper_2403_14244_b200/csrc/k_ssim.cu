@@ -298,6 +298,23 @@ __global__ void __launch_bounds__(kThreads) k_ssim_bwd(int W, int H, const float
     }
     cp_async_commit();
   }
+  // the thread's output pixels of both images, loaded while the planes stream in
+  float fa[kG][3], fb[kG][3];
+  {
+    const int gx = bx + x;
+#pragma unroll
+    for (int o = 0; o < kG; ++o) {
+      const int gy = by + y0 + o;
+      const bool ok = gx < W && gy < H;
+      const size_t p = ok ? 3 * ((size_t)gy * W + gx) : 0;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        fa[o][c] = ok ? f[p + c] : 0.0f;
+        fb[o][c] = ok ? fhat[p + c] : 0.0f;
+      }
+    }
+  }
+#pragma unroll
   for (int c = 0; c < 3; ++c) {
     if (c == 0) cp_async_wait<2>();
     else if (c == 1) cp_async_wait<1>();
@@ -348,7 +365,7 @@ __global__ void __launch_bounds__(kThreads) k_ssim_bwd(int W, int H, const float
       const int gy = by + y0 + o;
       if (gx >= W || gy >= H) continue;
       const size_t p = 3 * ((size_t)gy * W + gx) + c;
-      const float a = f[p], b = fhat[p];
+      const float a = fa[o][c], b = fb[o][c];
       const float g = acc[o][0] + 2.0f * b * acc[o][1] + a * acc[o][2];
       dldc[p] = w1 * sgn(b - a) - wln * g;
     }
