@@ -181,49 +181,72 @@ __global__ void __launch_bounds__(kThreads) k_ssim_fwd(int W, int H, const float
       const int g = i / kR, r = i - g * kR;
       const float* pa = &S.a[r][3 * g * kG + c];
       const float* pb = &S.b[r][3 * g * kG + c];
-      float acc[kG][5];
+      // (m1, m2) and (t1, t2) as packed f32x2 pairs (FFMA2), t12 scalar
+      float2 am[kG], at[kG];
+      float ax[kG];
 #pragma unroll
-      for (int o = 0; o < kG; ++o)
-#pragma unroll
-        for (int k = 0; k < 5; ++k) acc[o][k] = 0.0f;
+      for (int o = 0; o < kG; ++o) {
+        am[o] = at[o] = make_float2(0.0f, 0.0f);
+        ax[o] = 0.0f;
+      }
 #pragma unroll
       for (int j = 0; j < kIn; ++j) {
-        const float a = pa[3 * j], b = pb[3 * j];
-        const float v[5] = {a, b, a * a, b * b, a * b};
+        const float2 ab = make_float2(pa[3 * j], pb[3 * j]);
+        const float2 sq = __fmul2_rn(ab, ab);
+        const float x12 = ab.x * ab.y;
 #pragma unroll
         for (int o = 0; o < kG; ++o) {
           const int d = j - o;
           if (d >= 0 && d < kWin) {
-#pragma unroll
-            for (int k = 0; k < 5; ++k) acc[o][k] = fmaf(tp.w[d], v[k], acc[o][k]);
+            const float2 wd = make_float2(tp.w[d], tp.w[d]);
+            am[o] = __ffma2_rn(wd, ab, am[o]);
+            at[o] = __ffma2_rn(wd, sq, at[o]);
+            ax[o] = fmaf(tp.w[d], x12, ax[o]);
           }
         }
       }
 #pragma unroll
-      for (int o = 0; o < kG; ++o)
-#pragma unroll
-        for (int k = 0; k < 5; ++k) S.h[k][r][g * kG + o] = acc[o][k];
+      for (int o = 0; o < kG; ++o) {
+        S.h[0][r][g * kG + o] = am[o].x;
+        S.h[1][r][g * kG + o] = am[o].y;
+        S.h[2][r][g * kG + o] = at[o].x;
+        S.h[3][r][g * kG + o] = at[o].y;
+        S.h[4][r][g * kG + o] = ax[o];
+      }
     }
     __syncthreads();
     // vertical pass: thread = (column lane, kG consecutive output rows)
-    float acc[kG][5];
+    float2 vm[kG], vt[kG];
+    float vx[kG];
 #pragma unroll
-    for (int o = 0; o < kG; ++o)
-#pragma unroll
-      for (int k = 0; k < 5; ++k) acc[o][k] = 0.0f;
+    for (int o = 0; o < kG; ++o) {
+      vm[o] = vt[o] = make_float2(0.0f, 0.0f);
+      vx[o] = 0.0f;
+    }
 #pragma unroll
     for (int j = 0; j < kIn; ++j) {
-      float v[5];
-#pragma unroll
-      for (int k = 0; k < 5; ++k) v[k] = S.h[k][y0 + j][x];
+      const float2 hm = make_float2(S.h[0][y0 + j][x], S.h[1][y0 + j][x]);
+      const float2 ht = make_float2(S.h[2][y0 + j][x], S.h[3][y0 + j][x]);
+      const float hx = S.h[4][y0 + j][x];
 #pragma unroll
       for (int o = 0; o < kG; ++o) {
         const int d = j - o;
         if (d >= 0 && d < kWin) {
-#pragma unroll
-          for (int k = 0; k < 5; ++k) acc[o][k] = fmaf(tp.w[d], v[k], acc[o][k]);
+          const float2 wd = make_float2(tp.w[d], tp.w[d]);
+          vm[o] = __ffma2_rn(wd, hm, vm[o]);
+          vt[o] = __ffma2_rn(wd, ht, vt[o]);
+          vx[o] = fmaf(tp.w[d], hx, vx[o]);
         }
       }
+    }
+    float acc[kG][5];
+#pragma unroll
+    for (int o = 0; o < kG; ++o) {
+      acc[o][0] = vm[o].x;
+      acc[o][1] = vm[o].y;
+      acc[o][2] = vt[o].x;
+      acc[o][3] = vt[o].y;
+      acc[o][4] = vx[o];
     }
     const int gx = bx + x;
 #pragma unroll
