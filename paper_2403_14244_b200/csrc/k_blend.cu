@@ -136,6 +136,11 @@ __global__ void __launch_bounds__(kBT) k_blend_fwd(
       stage_batch(st[(it + 1) & 1], sorted, rec, rg.x + b + kBatch, min(kBatch, n - b - kBatch));
     int cnt[4];
     warp_relevant_lists(cur, sub, min(kBatch, n - b), s_list[w], cnt);
+    // a sub-quarter whose 16 pixels have all terminated walks nothing
+    const uint32_t alive = __ballot_sync(0xffffffffu, T.x > t_min || T.y > t_min);
+#pragma unroll
+    for (int q4 = 0; q4 < 4; ++q4)
+      if (((alive >> (8 * q4)) & 0xFFu) == 0u) cnt[q4] = 0;
     const int steps = max(max(cnt[0], cnt[1]), max(cnt[2], cnt[3]));
     const int my_cnt = sq == 0 ? cnt[0] : (sq == 1 ? cnt[1] : (sq == 2 ? cnt[2] : cnt[3]));
     // the four 8-lane groups walk their own sub-quarter lists in lockstep
