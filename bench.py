@@ -22,6 +22,7 @@ import json
 import os
 import subprocess
 import sys
+import threading
 import time
 from pathlib import Path
 
@@ -86,50 +87,93 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """SM clocks + clock-event (throttle) reasons sampled DURING the timed region.
+
+    NVML polled from a thread every ~1 ms (a C3 timed region is ~140 ms, a C1 one ~12 ms), on
+    the device found by PCI bus id; falls back to `nvidia-smi -lms 20` when NVML is absent."""
+
+    REASONS = [("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40),
+               ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4)]
 
     def __init__(self, index: int):
-        self.p = None
-        self.out = ROOT / "gpurun_out" / f"clocks_{os.getpid()}.csv"
         self.index = index
+        self.rows = []          # (sm_mhz, max_mhz, reasons bitmask)
+        self.p = None
+        self.thread = None
+        self.stop = False
+        self.source = "unavailable"
+        self.out = ROOT / "gpurun_out" / f"clocks_{os.getpid()}.csv"
+
+    def _nvml_handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        try:
+            import torch
+            p = torch.cuda.get_device_properties(self.index)
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
+
+    def _poll(self, pynvml, h):
+        mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        while not self.stop:
+            sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+            rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.rows.append((float(sm), float(mx), int(rs)))
+            time.sleep(0.001)
 
     def __enter__(self):
+        try:
+            pynvml, h = self._nvml_handle()
+            self.rows.append((float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)),
+                              float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)),
+                              int(pynvml.nvmlDeviceGetCurrentClocksEventReasons(h))))
+            self.rows.clear()
+            self.thread = threading.Thread(target=self._poll, args=(pynvml, h), daemon=True)
+            self.thread.start()
+            self.source = "nvml 1 ms"
+            return self
+        except Exception:
+            self.thread = None
         try:
             self.out.parent.mkdir(exist_ok=True)
             self.p = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index),
-                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
                  "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=open(self.out, "w"), stderr=subprocess.DEVNULL)
+            self.source = "nvidia-smi 20 ms"
         except Exception:
             self.p = None
         return self
 
     def __exit__(self, *a):
+        if self.thread is not None:
+            self.stop = True
+            self.thread.join(timeout=5)
         if self.p:
             self.p.terminate()
             try:
                 self.p.wait(timeout=5)
             except Exception:
                 self.p.kill()
+            try:
+                for r in self.out.read_text().strip().splitlines():
+                    f = [x.strip() for x in r.split(",")]
+                    if len(f) >= 3 and f[0].replace(".", "").isdigit():
+                        self.rows.append((float(f[0]), float(f[1]), int(f[2], 16)))
+            except Exception:
+                pass
 
     def summary(self):
-        try:
-            rows = [r.split(",") for r in self.out.read_text().strip().splitlines() if r.strip()]
-        except Exception:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        sm = [float(r[0]) for r in rows if r[0].strip().replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4)
-                          if len(r) > 3 + i and r[3 + i].strip().lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(rows)}
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"],
+                    "source": self.source}
+        reasons = sorted({n for _, _, m in self.rows for n, bit in self.REASONS if m & bit})
+        return {"sm_mhz": float(np.median([r[0] for r in self.rows])),
+                "sm_max_mhz": max(r[1] for r in self.rows), "reasons": reasons,
+                "samples": len(self.rows), "source": self.source}
 
 
 def cpu_oracle_train_step(ms, co, cam, target, steps=1, threads=0):

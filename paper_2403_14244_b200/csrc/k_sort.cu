@@ -306,6 +306,7 @@ constexpr int kScanThreads = 256;
 #endif
 constexpr int kScanItems = ISG_SCAN_ITEMS;
 constexpr int kScanTileItems = kScanThreads * kScanItems;
+constexpr int kEmitWindow = 4096;  // staged keys per window (32 KB of shared memory)
 
 __global__ void __launch_bounds__(kScanThreads) k_scan_emit(
     const uint32_t* __restrict__ order, const uint32_t* __restrict__ ntiles,
@@ -317,6 +318,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_warp[8];
   __shared__ unsigned long long s_excl;
+  __shared__ uint32_t s_emit_key[kEmitWindow];
+  __shared__ uint32_t s_emit_gid[kEmitWindow];
   const int tid = threadIdx.x;
   if (tid == 0) s_tile = atomicAdd(counter, 1u);
   __syncthreads();
@@ -338,7 +341,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(
     sum += c[j];
   }
   uint32_t tot;
-  const uint32_t texcl = block_excl_scan_256(sum, s_warp, tot);
+  uint32_t texcl = block_excl_scan_256(sum, s_warp, tot);
   if (tid < 32) {
     const unsigned long long excl = lookback_warp(lookback, tile, tot);
     if (tid == 0) {
@@ -351,22 +354,49 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(
     }
   }
   __syncthreads();
-  unsigned long long off = s_excl + texcl;
+  // Emission.  The CTA's keys occupy one contiguous range [s_excl, s_excl + tot) of the
+  // output, so they are staged in shared memory window by window and written back coalesced
+  // (per-thread emission straight to global memory scatters every store across 32 lines).
+  // An item straddling a window boundary is enumerated again in the next window.
+  const unsigned long long cta0 = s_excl;
 #pragma unroll
   for (int j = 0; j < kScanItems; ++j) {
-    const int64_t r = r0 + j;
-    if (r >= n) break;
-    const uint32_t gg = g[j];
-    slot_off[gg] = (uint32_t)min(off, (unsigned long long)0xFFFFFFFFu);
-    if (c[j] == 0) continue;
-    const float4 m = (box[j].x >> 24) ? make_float4(0.f, 0.f, 0.f, 0.f) : ms[gg];
-    for_each_tile(box[j], m, fp, [&](int t) {
-      if (off < (unsigned long long)key_cap) {
-        tile_keys[off] = (uint32_t)t;
-        emit_gid[off] = gg;
+    if (r0 + j < n) slot_off[g[j]] = (uint32_t)min(cta0 + texcl, 0xFFFFFFFFull);
+    texcl += c[j];
+  }
+  // texcl is now the end of this thread's range (CTA-relative); its start is end - sum
+  const uint32_t t_end = texcl, t_begin = texcl - sum;
+  for (uint32_t w = 0; w < tot; w += kEmitWindow) {
+    const uint32_t wend = w + kEmitWindow;
+    if (t_begin < wend && t_end > w) {
+      uint32_t pos = t_begin;
+#pragma unroll
+      for (int j = 0; j < kScanItems; ++j) {
+        const uint32_t p0 = pos;
+        pos += c[j];
+        if (c[j] == 0 || pos <= w || p0 >= wend) continue;
+        const float4 m = (box[j].x >> 24) ? make_float4(0.f, 0.f, 0.f, 0.f) : ms[g[j]];
+        uint32_t q = p0;
+        const uint32_t gg = g[j];
+        for_each_tile(box[j], m, fp, [&](int t) {
+          if (q >= w && q < wend) {
+            s_emit_key[q - w] = (uint32_t)t;
+            s_emit_gid[q - w] = gg;
+          }
+          ++q;
+        });
       }
-      ++off;
-    });
+    }
+    __syncthreads();
+    const uint32_t cnt = min(tot - w, (uint32_t)kEmitWindow);
+    const unsigned long long o0 = cta0 + w;
+    for (uint32_t i = tid; i < cnt; i += kScanThreads) {
+      if (o0 + i < (unsigned long long)key_cap) {
+        tile_keys[o0 + i] = s_emit_key[i];
+        emit_gid[o0 + i] = s_emit_gid[i];
+      }
+    }
+    __syncthreads();
   }
 }
 

@@ -317,6 +317,23 @@ def test_full_size_c2_render_parity():
         assert np.abs(img - O.render32(ms, co, cam)).max() <= IMG_TOL
 
 
+def test_full_size_c3_loss_backward():
+    """Config C3 (1M splats, 1920x1080, the bench's train step): L2 loss and all 8M parameter
+    gradients against the oracle at full size, same tolerances as the small cases."""
+    W, H, n = 1920, 1080, 1_000_000
+    ms, co = isg.synth_scene(n, W, H, seed=1)
+    tms, tco = isg.synth_scene(n, W, H, seed=2)
+    cam = isg.Camera.synthetic(W, H)
+    target = O.render32(tms, tco, cam)
+    with isg.Renderer(0) as r:
+        r.set_scene(ms, co)
+        loss = r.loss_backward(cam, target)
+        g = r.grads()
+    loss_ref, g_ref = O.loss_backward32(ms, co, cam, target)
+    assert abs(loss - loss_ref) <= 1e-6 * abs(loss_ref)
+    _grad_check(g, g_ref)
+
+
 def test_binning_modes_bit_identical(rend):
     """Tile-bucket and onesweep-radix binning give identical lists, images and gradients."""
     W, H = 320, 200
