@@ -37,18 +37,21 @@ struct Stage {
   uint32_t slot[B];  // gradient slot of the (tile, splat) pair
 };
 
-// Stage list entries [beg, beg+cnt) of the sorted (splat, slot) array (thread t: entry t).
-// The 32-B record gather is issued as cp.async; the caller waits + barriers before use.
-template <int B>
+// Stage list entries [beg, beg+cnt) of the sorted (splat, slot) array (thread t: entries t,
+// t + NT, ...).  The 32-B record gathers are issued as cp.async; the caller waits + barriers
+// before use.
+template <int NT, int B>
 __device__ __forceinline__ void stage_batch(Stage<B>& st, const uint2* __restrict__ sorted,
                                             const RenderRec* __restrict__ rec, uint32_t beg,
                                             int cnt) {
-  const int t = threadIdx.x;
-  if (t < cnt) {
-    const uint2 gs = sorted[beg + t];  // (splat, gradient slot)
-    st.slot[t] = gs.y;
-    cp_async16(&st.geo[t], &rec[gs.x].geo);
-    cp_async16(&st.col[t], &rec[gs.x].col);
+#pragma unroll
+  for (int t = threadIdx.x; t < B; t += NT) {
+    if (t < cnt) {
+      const uint2 gs = sorted[beg + t];  // (splat, gradient slot)
+      st.slot[t] = gs.y;
+      cp_async16(&st.geo[t], &rec[gs.x].geo);
+      cp_async16(&st.col[t], &rec[gs.x].col);
+    }
   }
   cp_async_commit();
 }

@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(kBT) k_blend_bwd(
 
   const uint32_t lt = (1u << lane) - 1u;
   int hi = m;
-  stage_batch(st[0], sorted, rec, rg.x + max(0, hi - kBatch), min(kBatch, hi));
+  stage_batch<kBT>(st[0], sorted, rec, rg.x + max(0, hi - kBatch), min(kBatch, hi));
   for (int it = 0; hi > 0; ++it) {
     const int lo = max(0, hi - kBatch);
     const int cnt = hi - lo;
@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(kBT) k_blend_bwd(
     __syncthreads();  // batch visible; previous batch's flush finished reading s_part
     if (lo > 0) {
       const int nlo = max(0, lo - kBatch);
-      stage_batch(st[(it + 1) & 1], sorted, rec, rg.x + nlo, lo - nlo);
+      stage_batch<kBT>(st[(it + 1) & 1], sorted, rec, rg.x + nlo, lo - nlo);
     }
     // relevance of the batch for the warp's 8 sub-quarters -> 8 compacted lists.  The tests
     // share their per-axis terms (rounded squares of the distances to the 4 columns and 2
