@@ -6,6 +6,8 @@ namespace isg {
 namespace blend {
 
 constexpr float kLn2 = 0.6931471805599453f;
+// start of an empty tile's range as the tile sort leaves it (isg_debug_bins fixes it up)
+constexpr uint32_t kEmptyRange = 0xFFFFFFFFu;
 
 __device__ __forceinline__ bool overflowed(const unsigned long long* total, int64_t cap) {
   return *total > (unsigned long long)cap;

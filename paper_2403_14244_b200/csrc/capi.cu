@@ -71,7 +71,6 @@ struct isg_ctx {
   uint32_t* tkey[2] = {nullptr, nullptr};   // radix mode: tile keys
   uint32_t* tval[2] = {nullptr, nullptr};   // radix mode: emission indices
   uint32_t* emit_gid = nullptr;             // radix mode: splat of emission index e
-  int tile_buf = 0;
   bool radix_alloc = false;
 
   // sort / scan scratch
@@ -444,22 +443,23 @@ isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out) {
     ISG_STAGE(ST_SCAN_EMIT);
     isg::launch_scan_emit(ctx->order[ctx->order_buf], ctx->ntiles, ctx->tilebox, ctx->ms, n, fp,
                           ctx->slot_off, ctx->tkey[0], ctx->emit_gid, ctx->key_cap,
-                          ctx->scan_scratch, ctx->sc + 3, ctx->sc + 0, ctx->total, st);
+                          ctx->scan_scratch, ctx->sc + 3, ctx->sc + 0, ctx->total, ctx->ranges,
+                          fp.n_tiles, st);
     ISG_CHECK_LAUNCH();
     ctx->launches++;
     }
     {
     ISG_STAGE(ST_TILE_SORT);
-    ctx->tile_buf = isg::radix_sort_pairs(ctx->tkey, ctx->tval, true, ctx->sc + 0, ctx->key_cap,
-                                          bits_for(fp.n_tiles), ctx->sort_tile, st,
-                                          &ctx->launches, true);
+    isg::SortEpilogue epi;
+    epi.emit_gid = ctx->emit_gid;
+    epi.sorted = ctx->sorted;
+    epi.ranges = ctx->ranges;
+    isg::radix_sort_pairs(ctx->tkey, ctx->tval, true, ctx->sc + 0, ctx->key_cap,
+                          bits_for(fp.n_tiles), ctx->sort_tile, st, &ctx->launches, true, epi);
     ISG_CHECK_LAUNCH();
     }
-    ISG_STAGE(ST_RANGES);
-    isg::launch_ranges(ctx->tkey[ctx->tile_buf], ctx->tval[ctx->tile_buf], ctx->emit_gid,
-                       ctx->sc + 0, ctx->key_cap, fp.n_tiles, ctx->ranges, ctx->sorted, st);
-    ISG_CHECK_LAUNCH();
-    ctx->launches++;
+    // empty tiles keep (0xFFFFFFFF, 0): the blend kernels read them as empty, and only the
+    // parity hook (isg_debug_bins) needs their oracle form (s, s)
   } else if (!radix) {
     {
     ISG_STAGE(ST_TILE_SCAN);
@@ -1276,6 +1276,8 @@ isg_status isg_debug_bins(isg_ctx* ctx, uint64_t* keys, uint32_t* vals, int64_t*
   const int64_t nk = ctx->n_keys;
   *n_keys = nk;
   const FrameParams& fp = ctx->last_fp;
+  if (ctx->binning == isg::kBinRadix)
+    isg::launch_ranges_fix(ctx->sc + 0, ctx->key_cap, fp.n_tiles, ctx->ranges, ctx->stream);
   if ((keys || vals) && nk > 0) {
     uint64_t* dk = nullptr;
     uint32_t* dv = nullptr;

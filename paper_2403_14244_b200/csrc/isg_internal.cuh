@@ -65,9 +65,18 @@ inline int64_t sort_tiles_for(int64_t cap) { return (cap + kSortTileItems - 1) /
 // are ping-pong buffers; returns the index (0/1) of the buffer holding the result.  With
 // iota_vals the first pass uses the item index as the value (vals[0] is not read).
 // scratch_zeroed: the caller zeroed s (hist, counters, the passes' look-back) on the stream.
+// Optional epilogue of a sort's last pass (the tile sort): instead of (keys, vals) it writes
+// sorted[o] = (emit_gid[val], val) and the per-tile [start, end) of the key runs into `ranges`
+// (pre-set to (0xFFFFFFFF, 0) per tile; launch_ranges_fix then fills the empty tiles).
+struct SortEpilogue {
+  const uint32_t* emit_gid = nullptr;
+  uint2* sorted = nullptr;
+  uint2* ranges = nullptr;
+};
 int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], bool iota_vals, const uint32_t* n_dev,
                      int64_t cap, int key_bits, SortScratch& s, cudaStream_t st,
-                     int64_t* launches, bool scratch_zeroed = false);
+                     int64_t* launches, bool scratch_zeroed = false,
+                     const SortEpilogue& epi = SortEpilogue());
 
 // Byte size of a sort's look-back region for `passes` passes over up to `cap` items.
 inline size_t sort_lookback_bytes(int64_t cap, int passes) {
@@ -101,11 +110,12 @@ void launch_scan_emit(const uint32_t* order, const uint32_t* ntiles, const uint2
                       const float4* ms, int64_t n, const FrameParams& fp, uint32_t* slot_off,
                       uint32_t* tile_keys, uint32_t* emit_gid, int64_t key_cap,
                       unsigned long long* scratch, uint32_t* counter, uint32_t* n_keys,
-                      unsigned long long* n_keys_total, cudaStream_t st);
-// (splat, slot) pairs in sorted order + per-tile ranges (empty tiles: (start, start))
-void launch_ranges(const uint32_t* sorted_tiles, const uint32_t* e_sorted,
-                   const uint32_t* emit_gid, const uint32_t* n_keys, int64_t key_cap, int n_tiles,
-                   uint2* ranges, uint2* sorted, cudaStream_t st);
+                      unsigned long long* n_keys_total, uint2* ranges, int n_tiles,
+                      cudaStream_t st);
+// Empty tiles of the ranges the tile sort's epilogue wrote get (s, s), s = the start of the
+// next non-empty tile (n if none) — the position the tile would occupy, like the oracle.
+void launch_ranges_fix(const uint32_t* n_keys, int64_t key_cap, int n_tiles, uint2* ranges,
+                       cudaStream_t st);
 
 // ---- blending (k_blend.cu) ----------------------------------------------------------------
 // sorted: per list entry (splat, gradient slot), tile-major, (depth, index) order per tile.

@@ -25,7 +25,13 @@ namespace {
 using namespace blend;
 
 constexpr int kBT = 64;      // threads per tile CTA: 2 warps x 8 four-lane groups
-constexpr int kBatch = 128;  // records staged per batch
+#ifndef ISG_FWD_BATCH
+#define ISG_FWD_BATCH 128
+#endif
+#ifndef ISG_FWD_MINB
+#define ISG_FWD_MINB 1
+#endif
+constexpr int kBatch = ISG_FWD_BATCH;  // records staged per batch
 constexpr int kWords = kBatch / 32;
 constexpr int kListPitch = kBatch + 4;  // sub-quarter lists start in different banks
 
@@ -59,7 +65,7 @@ __device__ __forceinline__ void fwd_pair(FwdPair& p, bool has, float2 r2, const 
 
 }  // namespace
 
-__global__ void __launch_bounds__(kBT) k_blend_fwd(
+__global__ void __launch_bounds__(kBT, ISG_FWD_MINB) k_blend_fwd(
     FrameParams fp, const uint2* __restrict__ ranges, const uint2* __restrict__ sorted,
     const RenderRec* __restrict__ rec, const unsigned long long* __restrict__ total,
     int64_t key_cap, float* __restrict__ out, float* __restrict__ t_last,
@@ -96,7 +102,7 @@ __global__ void __launch_bounds__(kBT) k_blend_fwd(
     ry1[r] = (float)(min(ys + 4, H) - 1) + 0.5f;
   }
   const uint2 rg = ranges[tile];
-  const int n = (int)(rg.y - rg.x);
+  const int n = rg.x == kEmptyRange ? 0 : (int)(rg.y - rg.x);
   const float t_min = fp.t_min;
 
   // Invalid pixels start "terminated" (T = 0 <= t_min) and never contribute.

@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(kBT) k_blend_bwd(
     ry1[r] = (float)(min(ys + 4, H) - 1) + 0.5f;
   }
   const uint2 rg = ranges[tile];
-  const int n = (int)(rg.y - rg.x);
+  const int n = rg.x == kEmptyRange ? 0 : (int)(rg.y - rg.x);
 
   BwdPair P[2];  // P[k]: the quad's row k
   float dsq = 0.0f;

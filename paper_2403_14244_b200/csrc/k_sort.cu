@@ -5,16 +5,17 @@
 // tile-binned order the blend kernels need: per 16x16 tile, splats in (depth, index) order.
 //
 //   1. radix sort (depth bits, splat) over all splats          -> rank r = depth order
-//   2. k_scan_emit: decoupled look-back exclusive scan of the tile counts in rank order,
-//      gather of the depth-ordered 32-B render records, emission of (tile, r) pairs in rank
-//      order (so equal tiles already appear in depth order)
-//   3. radix sort (tile, r) — stable, only ceil(log2(tiles)) bits  -> per-tile lists
-//   4. k_ranges
+//   2. k_scan_emit: decoupled look-back exclusive scan of the tile counts in rank order and
+//      emission of (tile, splat) pairs in rank order (so equal tiles already appear in depth
+//      order), staged per CTA in shared memory and written coalesced
+//   3. radix sort (tile, emission index) — stable, only ceil(log2(tiles)) bits; its last
+//      pass writes the (splat, slot) pairs in final order and the tile runs' bounds
+//   4. k_ranges_fix: empty tiles get (s, s) at the position they would occupy
 //
 // The radix sort is a onesweep LSD sort (one kernel per 8-bit digit pass plus one upfront
-// histogram kernel): every CTA takes a dynamic tile id, ranks its 4096 keys stably with
-// warp-level match_any multisplit, publishes per-digit counts to a decoupled look-back
-// array, scatters through shared memory and writes coalesced runs per digit.
+// histogram kernel): every CTA takes a dynamic tile id, ranks its 2048 keys stably with a
+// ballot-based warp multisplit, publishes per-digit counts to a decoupled look-back array,
+// scatters through shared memory and writes coalesced runs per digit.
 #include <algorithm>
 
 #include "isg_math.cuh"
@@ -22,6 +23,9 @@
 
 #ifndef ISG_HIST_MODE
 #define ISG_HIST_MODE 2
+#endif
+#ifndef ISG_EPI_PREFETCH
+#define ISG_EPI_PREFETCH 1
 #endif
 #ifndef ISG_LOOKBACK_WIN
 #define ISG_LOOKBACK_WIN 16
@@ -157,14 +161,16 @@ struct OnesweepSmem {
   uint32_t bin_base[256];
   uint32_t warp_tmp[8];
   uint32_t tile;
+  uint32_t gids[kSortTileItems];  // epilogue pass only: splat of each item
 };
 
+template <bool kEpi>
 __global__ void __launch_bounds__(kSortThreads) k_onesweep(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
     uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
     const uint32_t* __restrict__ n_dev, int64_t cap, int shift,
     const uint32_t* __restrict__ hist, uint32_t* __restrict__ lookback,
-    uint32_t* __restrict__ counter) {
+    uint32_t* __restrict__ counter, SortEpilogue epi) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   OnesweepSmem& S = *reinterpret_cast<OnesweepSmem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -185,6 +191,13 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
     key[j] = valid ? keys_in[idx] : 0u;
     val[j] = valid ? (vals_in ? vals_in[idx] : (uint32_t)idx) : 0u;
     dig[j] = valid ? ((key[j] >> shift) & 255u) : 256u;
+  }
+  // epilogue: the splat gathers are issued now and land during the ranking and look-back
+  uint32_t gid[kEpi ? kSortItems : 1];
+  if constexpr (kEpi) {
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j)
+      gid[j] = ISG_EPI_PREFETCH && dig[j] < 256u ? epi.emit_gid[val[j]] : 0u;
   }
   // stable warp multisplit: rank = items of the same digit earlier in (iteration, lane) order
   const uint32_t lt = lanemask_lt();
@@ -227,6 +240,7 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
       const uint32_t pos = S.local_start[d] + S.wcnt[w][d] + rank[j];
       S.keys[pos] = key[j];
       S.vals[pos] = val[j];
+      if constexpr (kEpi) S.gids[pos] = gid[j];
     }
   }
   const uint32_t gpre = hist[tid];  // exclusive digit offset (k_hist's last block scanned)
@@ -258,43 +272,65 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
   S.bin_base[tid] = gpre + excl - local_start;
   __syncthreads();
   const int nvalid = (int)min((int64_t)kSortTileItems, n - base);
-  for (int i = tid; i < nvalid; i += kSortThreads) {
-    const uint32_t k = S.keys[i];
-    const uint32_t o = S.bin_base[(k >> shift) & 255u] + (uint32_t)i;
-    keys_out[o] = k;
-    vals_out[o] = S.vals[i];
+  if constexpr (kEpi) {
+    // last pass of the tile sort: (splat, slot) pairs in final order, and the tile runs'
+    // bounds.  Items adjacent in shared memory with the same digit are adjacent in the output,
+    // so a run's first / last item here bounds the tile's range; runs continuing in other
+    // tiles of the sort are merged by the atomics.
+    for (int i = tid; i < nvalid; i += kSortThreads) {
+      const uint32_t k = S.keys[i];
+      const uint32_t o = S.bin_base[(k >> shift) & 255u] + (uint32_t)i;
+      const uint32_t v = S.vals[i];
+      epi.sorted[o] = make_uint2(ISG_EPI_PREFETCH ? S.gids[i] : epi.emit_gid[v], v);
+      if (i == 0 || S.keys[i - 1] != k) atomicMin(&epi.ranges[k].x, o);
+      if (i == nvalid - 1 || S.keys[i + 1] != k) atomicMax(&epi.ranges[k].y, o + 1u);
+    }
+  } else {
+    for (int i = tid; i < nvalid; i += kSortThreads) {
+      const uint32_t k = S.keys[i];
+      const uint32_t o = S.bin_base[(k >> shift) & 255u] + (uint32_t)i;
+      keys_out[o] = k;
+      vals_out[o] = S.vals[i];
+    }
   }
 }
 
-// ---- ranges ---------------------------------------------------------------------------------
-// Per-tile [start, end) from the sorted tile keys and the blend kernels' (splat, slot) pairs
-// (slot = the pair's emission index, which also keys its gradient slot).  The thread at each
-// key change also fills the empty tiles in the gap with (i, i), so an empty tile gets
-// (start, start) at the position it would occupy, exactly like the oracle.
-__global__ void k_ranges(const uint32_t* __restrict__ t, const uint32_t* __restrict__ e_sorted,
-                         const uint32_t* __restrict__ emit_gid, const uint32_t* __restrict__ n_dev,
-                         int64_t cap, int n_tiles, uint2* __restrict__ ranges,
-                         uint2* __restrict__ sorted) {
+// ---- ranges fix-up ---------------------------------------------------------------------------
+// The tile sort's epilogue left empty tiles at (0xFFFFFFFF, 0).  One CTA: each thread takes a
+// contiguous segment of tiles, a block-wide suffix minimum over the segments' smallest starts
+// gives every empty tile the start of the next non-empty tile (n when none follows).
+constexpr int kFixThreads = 1024;
+__global__ void __launch_bounds__(kFixThreads) k_ranges_fix(const uint32_t* __restrict__ n_dev,
+                                                            int64_t cap, int n_tiles,
+                                                            uint2* __restrict__ ranges) {
+  __shared__ uint32_t s_min[kFixThreads];
   const int64_t n = min((int64_t)*n_dev, cap);
+  const int tid = threadIdx.x;
+  const int seg = (n_tiles + kFixThreads - 1) / kFixThreads;
+  const int k0 = min(tid * seg, n_tiles), k1 = min(k0 + seg, n_tiles);
   if (n == 0) {
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n_tiles; k += gridDim.x * blockDim.x)
-      ranges[k] = make_uint2(0u, 0u);
+    for (int k = k0; k < k1; ++k) ranges[k] = make_uint2(0u, 0u);
     return;
   }
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    // boundary between item i-1 and item i (i = 0: before the first, i = n: after the last)
-    const uint32_t prev = i > 0 ? t[i - 1] : 0xFFFFFFFFu;
-    const uint32_t next = i < n ? t[i] : (uint32_t)n_tiles;
-    if (i == 0 || prev != next) {
-      const uint32_t lo = i > 0 ? prev + 1 : 0u;  // empty tiles lo .. next-1
-      for (uint32_t k = lo; k < next; ++k) ranges[k] = make_uint2((uint32_t)i, (uint32_t)i);
-      if (i > 0) ranges[prev].y = (uint32_t)i;
-      if (i < n) ranges[next].x = (uint32_t)i;
-    }
-    if (i < n) {
-      const uint32_t e = e_sorted[i];
-      sorted[i] = make_uint2(emit_gid[e], e);
+  uint32_t m = 0xFFFFFFFFu;
+  for (int k = k0; k < k1; ++k) m = min(m, ranges[k].x);
+  s_min[tid] = m;
+  __syncthreads();
+  // inclusive suffix minimum (Hillis-Steele)
+  for (int o = 1; o < kFixThreads; o <<= 1) {
+    const uint32_t other = tid + o < kFixThreads ? s_min[tid + o] : 0xFFFFFFFFu;
+    __syncthreads();
+    s_min[tid] = min(s_min[tid], other);
+    __syncthreads();
+  }
+  uint32_t next = tid + 1 < kFixThreads ? s_min[tid + 1] : 0xFFFFFFFFu;
+  if (next == 0xFFFFFFFFu) next = (uint32_t)n;
+  for (int k = k1 - 1; k >= k0; --k) {
+    const uint2 r = ranges[k];
+    if (r.x == 0xFFFFFFFFu) {
+      ranges[k] = make_uint2(next, next);
+    } else {
+      next = r.x;
     }
   }
 }
@@ -314,7 +350,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(
     uint32_t* __restrict__ slot_off, uint32_t* __restrict__ tile_keys,
     uint32_t* __restrict__ emit_gid, int64_t key_cap,
     unsigned long long* __restrict__ lookback, uint32_t* __restrict__ counter,
-    uint32_t* __restrict__ n_keys, unsigned long long* __restrict__ n_keys_total) {
+    uint32_t* __restrict__ n_keys, unsigned long long* __restrict__ n_keys_total,
+    uint2* __restrict__ ranges, int n_tiles) {
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_warp[8];
   __shared__ unsigned long long s_excl;
@@ -322,6 +359,9 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(
   __shared__ uint32_t s_emit_gid[kEmitWindow];
   const int tid = threadIdx.x;
   if (tid == 0) s_tile = atomicAdd(counter, 1u);
+  // empty ranges for the tile sort's epilogue (its atomics run after this kernel)
+  for (int k = blockIdx.x * kScanThreads + tid; k < n_tiles; k += gridDim.x * kScanThreads)
+    ranges[k] = make_uint2(0xFFFFFFFFu, 0u);
   __syncthreads();
   const uint32_t tile = s_tile;
   const int64_t base = (int64_t)tile * kScanTileItems;
@@ -408,25 +448,24 @@ void launch_scan_emit(const uint32_t* order, const uint32_t* ntiles, const uint2
                       const float4* ms, int64_t n, const FrameParams& fp, uint32_t* slot_off,
                       uint32_t* tile_keys, uint32_t* emit_gid, int64_t key_cap,
                       unsigned long long* scratch, uint32_t* counter, uint32_t* n_keys,
-                      unsigned long long* n_keys_total, cudaStream_t st) {
+                      unsigned long long* n_keys_total, uint2* ranges, int n_tiles,
+                      cudaStream_t st) {
   const int64_t tiles = scan_emit_scratch_words(n);
   if (tiles == 0) return;  // caller zeroed the counts
   k_scan_emit<<<(unsigned)tiles, kScanThreads, 0, st>>>(order, ntiles, tilebox, ms, n, fp,
                                                         slot_off, tile_keys, emit_gid, key_cap,
-                                                        scratch, counter, n_keys, n_keys_total);
+                                                        scratch, counter, n_keys, n_keys_total,
+                                                        ranges, n_tiles);
 }
 
-void launch_ranges(const uint32_t* sorted_tiles, const uint32_t* e_sorted,
-                   const uint32_t* emit_gid, const uint32_t* n_keys, int64_t key_cap, int n_tiles,
-                   uint2* ranges, uint2* sorted, cudaStream_t st) {
-  const int64_t blocks = std::min<int64_t>((key_cap + 256) / 256, 148 * 16);
-  k_ranges<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, st>>>(
-      sorted_tiles, e_sorted, emit_gid, n_keys, key_cap, n_tiles, ranges, sorted);
+void launch_ranges_fix(const uint32_t* n_keys, int64_t key_cap, int n_tiles, uint2* ranges,
+                       cudaStream_t st) {
+  k_ranges_fix<<<1, kFixThreads, 0, st>>>(n_keys, key_cap, n_tiles, ranges);
 }
 
 int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], bool iota_vals, const uint32_t* n_dev,
                      int64_t cap, int key_bits, SortScratch& s, cudaStream_t st,
-                     int64_t* launches, bool scratch_zeroed) {
+                     int64_t* launches, bool scratch_zeroed, const SortEpilogue& epi) {
   const int passes = (key_bits + 7) / 8;
   const int64_t tiles = (cap + kSortTileItems - 1) / kSortTileItems;
   // caller guarantees tiles <= s.max_tiles and passes <= kMaxPasses
@@ -441,15 +480,20 @@ int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], bool iota_vals, const
   int cur = 0;
   const size_t smem = sizeof(OnesweepSmem);
   static const bool attr_set = [&] {  // once, outside any graph capture
-    cudaFuncSetAttribute(k_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_onesweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    cudaFuncSetAttribute(k_onesweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
     return true;
   }();
   (void)attr_set;
   for (int p = 0; p < passes; ++p) {
-    k_onesweep<<<(unsigned)std::max<int64_t>(tiles, 1), kSortThreads, smem, st>>>(
+    const bool fin = p == passes - 1 && epi.sorted;
+    (fin ? k_onesweep<true> : k_onesweep<false>)<<<(unsigned)std::max<int64_t>(tiles, 1),
+                                                  kSortThreads, smem, st>>>(
         keys[cur], (p == 0 && iota_vals) ? nullptr : vals[cur], keys[cur ^ 1], vals[cur ^ 1],
-        n_dev, cap,
-        8 * p, s.hist + 256 * p, s.lookback + (size_t)256 * tiles * p, s.counters + p);
+        n_dev, cap, 8 * p, s.hist + 256 * p, s.lookback + (size_t)256 * tiles * p,
+        s.counters + p, fin ? epi : SortEpilogue());
     cur ^= 1;
   }
   if (launches) *launches += 1 + passes;
