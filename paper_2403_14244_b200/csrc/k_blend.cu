@@ -28,8 +28,16 @@ constexpr int kBT = 64;      // threads per tile CTA: 2 warps x 8 four-lane grou
 #ifndef ISG_FWD_BATCH
 #define ISG_FWD_BATCH 128
 #endif
+// An explicit minimum of 1 CTA/SM lets ptxas use 106 registers instead of its default 80:
+// measured 4.5% faster (C3 0.263 vs 0.275 ms); capping for occupancy (72 / 64 registers) is
+// slower.
 #ifndef ISG_FWD_MINB
 #define ISG_FWD_MINB 1
+#endif
+#if ISG_FWD_MINB > 0
+#define ISG_FWD_BOUNDS __launch_bounds__(kBT, ISG_FWD_MINB)
+#else
+#define ISG_FWD_BOUNDS __launch_bounds__(kBT)
 #endif
 constexpr int kBatch = ISG_FWD_BATCH;  // records staged per batch
 constexpr int kWords = kBatch / 32;
@@ -65,7 +73,7 @@ __device__ __forceinline__ void fwd_pair(FwdPair& p, bool has, float2 r2, const 
 
 }  // namespace
 
-__global__ void __launch_bounds__(kBT, ISG_FWD_MINB) k_blend_fwd(
+__global__ void ISG_FWD_BOUNDS k_blend_fwd(
     FrameParams fp, const uint2* __restrict__ ranges, const uint2* __restrict__ sorted,
     const RenderRec* __restrict__ rec, const unsigned long long* __restrict__ total,
     int64_t key_cap, float* __restrict__ out, float* __restrict__ t_last,

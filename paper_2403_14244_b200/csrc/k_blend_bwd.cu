@@ -99,10 +99,18 @@ __device__ __forceinline__ void reduce_scatter8_quad(const float v[8], float out
 
 }  // namespace
 
+#ifndef ISG_BWD_MINB
+#define ISG_BWD_MINB 0
+#endif
+#if ISG_BWD_MINB > 0
+#define ISG_BWD_BOUNDS __launch_bounds__(kBT, ISG_BWD_MINB)
+#else
+#define ISG_BWD_BOUNDS __launch_bounds__(kBT)
+#endif
 template <bool kGivenG>
 // (a minimum-blocks bound that caps registers for more resident warps — 10, 12, 14 or 16 CTAs
 // per SM — measured 12-27% slower: ptxas then trades ILP for registers)
-__global__ void __launch_bounds__(kBT) k_blend_bwd(
+__global__ void ISG_BWD_BOUNDS k_blend_bwd(
     FrameParams fp, const uint2* __restrict__ ranges, const uint2* __restrict__ sorted,
     const RenderRec* __restrict__ rec, const unsigned long long* __restrict__ total,
     int64_t key_cap, const float* __restrict__ img, const float* __restrict__ target,
