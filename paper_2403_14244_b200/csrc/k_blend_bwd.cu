@@ -297,17 +297,12 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
       for (int k = 0; k < 8; ++k) acc[k] = acc2[k].x + acc2[k].y;
       float y[2];
       reduce_scatter8_quad(acc, y);
-      // kernels.hpp:219-220: dg/du = g 2 dx / s^2, dg/ds = g 2 r^2 / s^3, times opacity.  The
-      // lane holds values vb, vb + 1 with vb = 4 (l4 >> 1) + 2 (l4 & 1): lane 0 (du, dv) scales
-      // both by 2 o / s^2, lane 1 (dsigma2d, dopacity) the first by 2 o / s^3.
-      const float inv_s2 = g.w * -kLn2;  // 1 / sigma2d^2
-      const float k2 = 2.0f * c.w * inv_s2;
+      // the lane holds values vb, vb + 1 (vb = 4 (l4 >> 1) + 2 (l4 & 1)); the per-splat
+      // scale factors are applied once per entry in the flush
       const int vb = 4 * (l4 >> 1) + 2 * (l4 & 1);
-      const float s0 = vb == 0 ? k2 : (vb == 2 ? k2 * fast_sqrt(inv_s2) : 1.0f);
-      const float s1 = vb == 0 ? k2 : 1.0f;
       if (has) {
-        s_part[sub][vb][jj] = y[0] * s0;
-        s_part[sub][vb + 1][jj] = y[1] * s1;
+        s_part[sub][vb][jj] = y[0];
+        s_part[sub][vb + 1][jj] = y[1];
       }
     }
     __syncthreads();
@@ -321,6 +316,13 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
 #pragma unroll
         for (int k = 0; k < 8; ++k) v[k] += s_part[r][k][jj];
       }
+      // kernels.hpp:219-220: dg/du = g 2 dx / s^2, dg/ds = g 2 r^2 / s^3, times opacity:
+      // (du, dv) scale by 2 o / s^2, dsigma2d by 2 o / s^3
+      const float inv_s2 = cur.geo[jj].w * -kLn2;  // 1 / sigma2d^2
+      const float k2 = 2.0f * cur.col[jj].w * inv_s2;
+      v[0] *= k2;
+      v[1] *= k2;
+      v[2] *= k2 * fast_sqrt(inv_s2);
       const size_t e = cur.slot[jj];
       partial[2 * e] = make_float4(v[0], v[1], v[2], v[3]);
       partial[2 * e + 1] = make_float4(v[4], v[5], v[6], 0.0f);
