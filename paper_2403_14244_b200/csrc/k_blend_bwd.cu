@@ -306,26 +306,28 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
       }
     }
     __syncthreads();
-    // combine the sub-quarters in a fixed order and write each (tile, splat) pair's slot
-    if ((int)threadIdx.x < cnt) {
-      const int jj = threadIdx.x;
-      float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    // combine the sub-quarters in a fixed order and write each (tile, splat) pair's slot:
+    // warp h sums values 4h .. 4h+3 of entry `lane` (h = 1: drgb; value 7 is unused)
+    static_assert(kBatch == 32 && kBT == 64, "flush maps entry = lane, half = warp");
+    if (lane < cnt) {
+      const int jj = lane;
+      float v[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 4
       for (int r = 0; r < kSubs; ++r) {
-        if (!((s_rel[r][jj >> 5] >> (jj & 31)) & 1u)) continue;
+        if (!((s_rel[r][0] >> jj) & 1u)) continue;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] += s_part[r][k][jj];
+        for (int k = 0; k < 4; ++k) v[k] += s_part[r][4 * w + k][jj];
       }
-      // kernels.hpp:219-220: dg/du = g 2 dx / s^2, dg/ds = g 2 r^2 / s^3, times opacity:
-      // (du, dv) scale by 2 o / s^2, dsigma2d by 2 o / s^3
-      const float inv_s2 = cur.geo[jj].w * -kLn2;  // 1 / sigma2d^2
-      const float k2 = 2.0f * cur.col[jj].w * inv_s2;
-      v[0] *= k2;
-      v[1] *= k2;
-      v[2] *= k2 * fast_sqrt(inv_s2);
       const size_t e = cur.slot[jj];
-      partial[2 * e] = make_float4(v[0], v[1], v[2], v[3]);
-      partial[2 * e + 1] = make_float4(v[4], v[5], v[6], 0.0f);
+      if (w == 0) {
+        // kernels.hpp:219-220: dg/du = g 2 dx / s^2, dg/ds = g 2 r^2 / s^3, times opacity:
+        // (du, dv) scale by 2 o / s^2, dsigma2d by 2 o / s^3
+        const float inv_s2 = cur.geo[jj].w * -kLn2;  // 1 / sigma2d^2
+        const float k2 = 2.0f * cur.col[jj].w * inv_s2;
+        partial[2 * e] = make_float4(v[0] * k2, v[1] * k2, v[2] * (k2 * fast_sqrt(inv_s2)), v[3]);
+      } else {
+        partial[2 * e + 1] = make_float4(v[0], v[1], v[2], 0.0f);
+      }
     }
     hi = lo;
   }
