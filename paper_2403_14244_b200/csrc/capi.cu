@@ -427,16 +427,22 @@ isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out) {
   }
   {
   ISG_STAGE(ST_PREPROCESS);
+  // radix mode: K1 also builds the depth sort's digit histograms
   isg::launch_preprocess(ctx->ms, ctx->co, n, fp, ctx->rec, ctx->depth[0], ctx->ntiles,
-                         ctx->tilebox, radix ? nullptr : ctx->tile_cnt, ctx->sc, st);
+                         ctx->tilebox, radix ? nullptr : ctx->tile_cnt, ctx->sc,
+                         radix ? ctx->sort_depth.hist : nullptr,
+                         radix ? ctx->sort_depth.counters + isg::kMaxPasses : nullptr, st);
   ISG_CHECK_LAUNCH();
   ctx->launches++;
   }
   if (radix && n > 0) {
+    const int tile_passes = (bits_for(fp.n_tiles) + 7) / 8;
     {
     ISG_STAGE(ST_DEPTH_SORT);
+    isg::SortOptions dopt;
+    dopt.scratch_zeroed = dopt.hist_ready = true;
     ctx->order_buf = isg::radix_sort_pairs(ctx->depth, ctx->order, true, ctx->sc + 4, n, 32,
-                                           ctx->sort_depth, st, &ctx->launches, true);
+                                           ctx->sort_depth, st, &ctx->launches, dopt);
     ISG_CHECK_LAUNCH();
     }
     {
@@ -444,18 +450,20 @@ isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out) {
     isg::launch_scan_emit(ctx->order[ctx->order_buf], ctx->ntiles, ctx->tilebox, ctx->ms, n, fp,
                           ctx->slot_off, ctx->tkey[0], ctx->emit_gid, ctx->key_cap,
                           ctx->scan_scratch, ctx->sc + 3, ctx->sc + 0, ctx->total, ctx->ranges,
-                          fp.n_tiles, st);
+                          fp.n_tiles, tile_passes, ctx->sort_tile.hist,
+                          ctx->sort_tile.counters + isg::kMaxPasses, st);
     ISG_CHECK_LAUNCH();
     ctx->launches++;
     }
     {
     ISG_STAGE(ST_TILE_SORT);
-    isg::SortEpilogue epi;
-    epi.emit_gid = ctx->emit_gid;
-    epi.sorted = ctx->sorted;
-    epi.ranges = ctx->ranges;
+    isg::SortOptions topt;
+    topt.scratch_zeroed = topt.hist_ready = true;  // k_scan_emit built the histograms
+    topt.epi.emit_gid = ctx->emit_gid;
+    topt.epi.sorted = ctx->sorted;
+    topt.epi.ranges = ctx->ranges;
     isg::radix_sort_pairs(ctx->tkey, ctx->tval, true, ctx->sc + 0, ctx->key_cap,
-                          bits_for(fp.n_tiles), ctx->sort_tile, st, &ctx->launches, true, epi);
+                          bits_for(fp.n_tiles), ctx->sort_tile, st, &ctx->launches, topt);
     ISG_CHECK_LAUNCH();
     }
     // empty tiles keep (0xFFFFFFFF, 0): the blend kernels read them as empty, and only the

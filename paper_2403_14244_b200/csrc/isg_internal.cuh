@@ -73,10 +73,15 @@ struct SortEpilogue {
   uint2* sorted = nullptr;
   uint2* ranges = nullptr;
 };
+struct SortOptions {
+  bool scratch_zeroed = false;  // hist / counters / look-back already zero (one frame memset)
+  bool hist_ready = false;      // hist already holds the exclusive digit offsets (the keys'
+                                // producer built them: radix_hist.cuh); no k_hist launch
+  SortEpilogue epi;
+};
 int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], bool iota_vals, const uint32_t* n_dev,
                      int64_t cap, int key_bits, SortScratch& s, cudaStream_t st,
-                     int64_t* launches, bool scratch_zeroed = false,
-                     const SortEpilogue& epi = SortEpilogue());
+                     int64_t* launches, const SortOptions& opt = SortOptions());
 
 // Byte size of a sort's look-back region for `passes` passes over up to `cap` items.
 inline size_t sort_lookback_bytes(int64_t cap, int passes) {
@@ -88,7 +93,8 @@ inline size_t sort_lookback_bytes(int64_t cap, int passes) {
 // bbox + hit mask per splat (see for_each_tile).  tile_cnt (tile-bucket mode) may be null.
 void launch_preprocess(const float4* ms, const float4* co, int64_t n, const FrameParams& fp,
                        RenderRec* rec, uint32_t* depth_key, uint32_t* ntiles, uint2* tilebox,
-                       uint32_t* tile_cnt, uint32_t* sc, cudaStream_t st);
+                       uint32_t* tile_cnt, uint32_t* sc, uint32_t* hist, uint32_t* hist_done,
+                       cudaStream_t st);
 
 // ---- tile-bucket binning (k_bin.cu) -------------------------------------------------------
 int64_t fill_scratch_words(int64_t n);  // + 1 zeroed u64 words of look-back scratch
@@ -111,6 +117,7 @@ void launch_scan_emit(const uint32_t* order, const uint32_t* ntiles, const uint2
                       uint32_t* tile_keys, uint32_t* emit_gid, int64_t key_cap,
                       unsigned long long* scratch, uint32_t* counter, uint32_t* n_keys,
                       unsigned long long* n_keys_total, uint2* ranges, int n_tiles,
+                      int tile_passes, uint32_t* tile_hist, uint32_t* tile_hist_done,
                       cudaStream_t st);
 // Empty tiles of the ranges the tile sort's epilogue wrote get (s, s), s = the start of the
 // next non-empty tile (n if none) — the position the tile would occupy, like the oracle.

@@ -2,13 +2,18 @@
 // (/root/reference/proj/src/splat3d.cpp:176-188 -> project_iso :59-64) and the per-splat
 // validation (IsoSplat3D::validate, splat3d.cpp:10-17).
 //
-// One thread per splat, coalesced float4 SoA loads (32 B/splat read), writes the 32-B render
-// record, the tile count (4 B) and, in radix binning mode, the depth key (4 B); in tile-bucket
-// mode it instead bumps one per-tile counter per touched tile.  Isotropic shortcut: the screen
+// One thread per splat (grid-stride over at most 8 blocks per SM), coalesced float4 SoA loads
+// (32 B/splat read), writes the 32-B render record, the tile count (4 B) and, in radix binning
+// mode, the depth key (4 B) plus the depth sort's digit histograms (radix_hist.cuh: one global
+// publish per block, so the sort needs no histogram pass); in tile-bucket mode it instead bumps
+// one per-tile counter per touched tile.  Isotropic shortcut: the screen
 // radius is 3*sigma*f/z directly — no 3x3 covariance, no eigen-solve.  Splats that are culled
 // (z <= near) or touch no tile get count 0 (and depth key 0xFFFFFFFF: they sort last and emit
 // nothing).
+#include <algorithm>
+
 #include "isg_math.cuh"
+#include "radix_hist.cuh"
 
 namespace isg {
 
@@ -19,59 +24,76 @@ __global__ void __launch_bounds__(256) k_preprocess(const float4* __restrict__ m
                                                     uint32_t* __restrict__ ntiles,
                                                     uint2* __restrict__ tilebox,
                                                     uint32_t* __restrict__ tile_cnt,
-                                                    uint32_t* __restrict__ sc) {
+                                                    uint32_t* __restrict__ sc,
+                                                    uint32_t* __restrict__ hist,
+                                                    uint32_t* __restrict__ hist_done) {
+  // radix mode: the depth sort's 4 digit histograms (radix_hist.cuh)
+  __shared__ uint32_t sh[kMaxPasses][256];
+  if (hist) {
+    hist_zero(sh);
+    __syncthreads();
+  }
   // sc: [1] 0xFFFFFFFF - first invalid splat (atomicMax, 0 = none: zero-initialised with the
   // other scalars), [2] visible splats, [4] n (device count)
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i == 0) sc[4] = (uint32_t)n;
-  uint32_t count = 0;
-  if (i < n) {
-    uint2 box = make_uint2(0u, 0u);
-    const float4 a = ms[i];
-    const float4 c = co[i];
-    // IsoSplat3D::validate (splat3d.cpp:10-17): finite mu, sigma > 0 finite, finite color,
-    // opacity in [0,1].  The host reports the first offending index with the reference message.
-    const bool ok = isfinite(a.x) && isfinite(a.y) && isfinite(a.z) && a.w > 0.0f &&
-                    isfinite(a.w) && isfinite(c.x) && isfinite(c.y) && isfinite(c.z) &&
-                    c.w >= 0.0f && c.w <= 1.0f;
-    if (!ok) atomicMax(&sc[1], 0xFFFFFFFFu - (uint32_t)i);
-    const Proj p = project(a, fp.cam);
-    if (p.vis && ok) {
-      int x0, x1, y0, y1;
-      if (tile_bbox(p.u, p.v, p.s, fp.tiles_x, fp.tiles_y, x0, x1, y0, y1)) {
-        const int bw = x1 - x0 + 1;
-        const bool small = bw * (y1 - y0 + 1) <= 32 && bw < 256 && x0 < 4096 && y0 < 4096;
-        uint32_t mask = 0;
-        for (int ty = y0; ty <= y1; ++ty)
-          for (int tx = x0; tx <= x1; ++tx) {
-            if (!tile_hit(p.u, p.v, p.r2max, tx, ty, fp.cam.width, fp.cam.height)) continue;
-            if (small) mask |= 1u << ((ty - y0) * bw + (tx - x0));
-            ++count;
-            if (tile_cnt) atomicAdd(&tile_cnt[ty * fp.tiles_x + tx], 1u);
-          }
-        // emission kernels iterate the hit bits instead of re-projecting (bw == 0: re-project)
-        if (small) box = make_uint2((uint32_t)x0 | ((uint32_t)y0 << 12) | ((uint32_t)bw << 24), mask);
+  if (blockIdx.x == 0 && threadIdx.x == 0) sc[4] = (uint32_t)n;
+  // grid-stride over block-sized chunks (few blocks: each publishes its histograms once)
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    uint32_t count = 0;
+    uint32_t key = 0xFFFFFFFFu;
+    if (i < n) {
+      uint2 box = make_uint2(0u, 0u);
+      const float4 a = ms[i];
+      const float4 c = co[i];
+      // IsoSplat3D::validate (splat3d.cpp:10-17): finite mu, sigma > 0 finite, finite color,
+      // opacity in [0,1].  The host reports the first offending index with the reference message.
+      const bool ok = isfinite(a.x) && isfinite(a.y) && isfinite(a.z) && a.w > 0.0f &&
+                      isfinite(a.w) && isfinite(c.x) && isfinite(c.y) && isfinite(c.z) &&
+                      c.w >= 0.0f && c.w <= 1.0f;
+      if (!ok) atomicMax(&sc[1], 0xFFFFFFFFu - (uint32_t)i);
+      const Proj p = project(a, fp.cam);
+      if (p.vis && ok) {
+        int x0, x1, y0, y1;
+        if (tile_bbox(p.u, p.v, p.s, fp.tiles_x, fp.tiles_y, x0, x1, y0, y1)) {
+          const int bw = x1 - x0 + 1;
+          const bool small = bw * (y1 - y0 + 1) <= 32 && bw < 256 && x0 < 4096 && y0 < 4096;
+          uint32_t mask = 0;
+          for (int ty = y0; ty <= y1; ++ty)
+            for (int tx = x0; tx <= x1; ++tx) {
+              if (!tile_hit(p.u, p.v, p.r2max, tx, ty, fp.cam.width, fp.cam.height)) continue;
+              if (small) mask |= 1u << ((ty - y0) * bw + (tx - x0));
+              ++count;
+              if (tile_cnt) atomicAdd(&tile_cnt[ty * fp.tiles_x + tx], 1u);
+            }
+          // emission kernels iterate the hit bits instead of re-projecting (bw == 0: re-project)
+          if (small) box = make_uint2((uint32_t)x0 | ((uint32_t)y0 << 12) | ((uint32_t)bw << 24), mask);
+        }
       }
+      tilebox[i] = box;
+      RenderRec r;  // (u, v, r2max, -log2(e)/sigma2d^2), (r, g, b, opacity)
+      r.geo = make_float4(p.u, p.v, p.r2max, __fdiv_rn(-1.4426950408889634f, __fmul_rn(p.s, p.s)));
+      r.col = c;
+      rec[i] = r;
+      key = count ? __float_as_uint(p.zc) : 0xFFFFFFFFu;
+      depth_key[i] = key;
+      ntiles[i] = count;
     }
-    tilebox[i] = box;
-    RenderRec r;  // (u, v, r2max, -log2(e)/sigma2d^2), (r, g, b, opacity)
-    r.geo = make_float4(p.u, p.v, p.r2max, __fdiv_rn(-1.4426950408889634f, __fmul_rn(p.s, p.s)));
-    r.col = c;
-    rec[i] = r;
-    depth_key[i] = count ? __float_as_uint(p.zc) : 0xFFFFFFFFu;
-    ntiles[i] = count;
+    // visible-splat count, one atomic per warp
+    const unsigned vis = __ballot_sync(0xffffffffu, count > 0);
+    if ((threadIdx.x & 31) == 0 && vis) atomicAdd(&sc[2], (uint32_t)__popc(vis));
+    if (hist) hist_add_warp(sh, key, i < n, kMaxPasses);
   }
-  // visible-splat count, one atomic per warp
-  const unsigned vis = __ballot_sync(0xffffffffu, count > 0);
-  if ((threadIdx.x & 31) == 0 && vis) atomicAdd(&sc[2], (uint32_t)__popc(vis));
+  if (hist) hist_publish(sh, kMaxPasses, hist, hist_done);
 }
 
 void launch_preprocess(const float4* ms, const float4* co, int64_t n, const FrameParams& fp,
                        RenderRec* rec, uint32_t* depth_key, uint32_t* ntiles, uint2* tilebox,
-                       uint32_t* tile_cnt, uint32_t* sc, cudaStream_t st) {
-  const int64_t blocks = n > 0 ? (n + 255) / 256 : 1;
+                       uint32_t* tile_cnt, uint32_t* sc, uint32_t* hist, uint32_t* hist_done,
+                       cudaStream_t st) {
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
   k_preprocess<<<(unsigned)blocks, 256, 0, st>>>(ms, co, n, fp, rec, depth_key, ntiles, tilebox,
-                                                 tile_cnt, sc);
+                                                 tile_cnt, sc, hist, hist_done);
 }
 
 // Parity hook: (tile << 32 | float_bits(depth)) and splat index for each sorted entry.

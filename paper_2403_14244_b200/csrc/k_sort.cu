@@ -20,6 +20,7 @@
 
 #include "isg_math.cuh"
 #include "lookback.cuh"
+#include "radix_hist.cuh"
 
 #ifndef ISG_HIST_MODE
 #define ISG_HIST_MODE 2
@@ -46,12 +47,6 @@ __device__ __forceinline__ void st_volatile(uint32_t* p, uint32_t v) {
   *(volatile uint32_t*)p = v;
 }
 
-__device__ __forceinline__ uint32_t lanemask_lt() {
-  uint32_t m;
-  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-  return m;
-}
-
 // Lanes of the warp holding the same 9-bit value (digit, or 256 = no item): 9 ballots instead of
 // one match.any (a slow MIO-pipe instruction on this part).
 __device__ __forceinline__ uint32_t warp_match9(uint32_t d) {
@@ -65,44 +60,18 @@ __device__ __forceinline__ uint32_t warp_match9(uint32_t d) {
   return peers;
 }
 
-// Exclusive scan of one u32 per thread over a 256-thread block.  s_warp: >= 8 words.
-__device__ __forceinline__ uint32_t block_excl_scan_256(uint32_t v, uint32_t* s_warp,
-                                                        uint32_t& total) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  uint32_t x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) s_warp[w] = x;
-  __syncthreads();
-  uint32_t wpre = 0, tot = 0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const uint32_t s = s_warp[i];
-    wpre += (i < w) ? s : 0u;
-    tot += s;
-  }
-  total = tot;
-  __syncthreads();
-  return wpre + x - v;
-}
-
 // ---- upfront histogram of all passes -------------------------------------------------------
+// (Not used by the frame's two sorts: their producers, k_preprocess and k_scan_emit, build the
+// same histograms while writing the keys; see radix_hist.cuh.)
 __global__ void __launch_bounds__(256) k_hist(const uint32_t* __restrict__ keys,
                                               const uint32_t* __restrict__ n_dev, int64_t cap,
                                               int passes, uint32_t* __restrict__ hist,
                                               uint32_t* __restrict__ done) {
   __shared__ uint32_t sh[kMaxPasses][256];
-  for (int i = threadIdx.x; i < kMaxPasses * 256; i += 256) (&sh[0][0])[i] = 0;
+  hist_zero(sh);
   __syncthreads();
   const int64_t n = min((int64_t)*n_dev, cap);
-  const uint32_t lt = lanemask_lt();
-  // grid-stride over whole warps, kHistUnroll keys per thread in flight at once.  A digit
-  // shared by the whole warp (the skewed high bytes: e.g. the exponent byte of positive
-  // depths, the top bits of tile ids) costs one shared atomic per warp instead of 32
-  // serialised ones.
+  // grid-stride over whole warps, kHistUnroll keys per thread in flight at once
   constexpr int kHistUnroll = 8;
   const int64_t stride = (int64_t)gridDim.x * 256 * kHistUnroll;
   for (int64_t i0 = ((int64_t)blockIdx.x * 256 + (threadIdx.x & ~31)) * kHistUnroll; i0 < n;
@@ -116,40 +85,9 @@ __global__ void __launch_bounds__(256) k_hist(const uint32_t* __restrict__ keys,
       k[u] = valid[u] ? keys[i] : 0u;
     }
 #pragma unroll
-    for (int u = 0; u < kHistUnroll; ++u) {
-      const bool full = __all_sync(0xffffffffu, valid[u]);
-      for (int p = 0; p < passes; ++p) {
-        const uint32_t d = (k[u] >> (8 * p)) & 255u;
-        const uint32_t d0 = __shfl_sync(0xffffffffu, d, 0);
-        if (full && __all_sync(0xffffffffu, d == d0)) {
-          if ((threadIdx.x & 31) == 0) atomicAdd(&sh[p][d0], 32u);
-        } else if (valid[u]) {
-          atomicAdd(&sh[p][d], 1u);
-        }
-      }
-    }
+    for (int u = 0; u < kHistUnroll; ++u) hist_add_warp(sh, k[u], valid[u], passes);
   }
-  __syncthreads();
-  for (int p = 0; p < passes; ++p) {
-    const uint32_t c = sh[p][threadIdx.x];
-    if (c) atomicAdd(&hist[p * 256 + threadIdx.x], c);
-  }
-  // the last block to finish turns the global histograms into exclusive digit offsets, once
-  // for all onesweep CTAs (done: a zeroed counter)
-  __shared__ bool s_last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(done, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  __shared__ uint32_t s_warp[8];
-  for (int p = 0; p < passes; ++p) {
-    const uint32_t c = __ldcg(&hist[p * 256 + threadIdx.x]);
-    uint32_t tot;
-    const uint32_t ex = block_excl_scan_256(c, s_warp, tot);
-    hist[p * 256 + threadIdx.x] = ex;
-  }
+  hist_publish(sh, passes, hist, done);
 }
 
 // ---- one onesweep digit pass -----------------------------------------------------------------
@@ -351,7 +289,9 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(
     uint32_t* __restrict__ emit_gid, int64_t key_cap,
     unsigned long long* __restrict__ lookback, uint32_t* __restrict__ counter,
     uint32_t* __restrict__ n_keys, unsigned long long* __restrict__ n_keys_total,
-    uint2* __restrict__ ranges, int n_tiles) {
+    uint2* __restrict__ ranges, int n_tiles, int tile_passes, uint32_t* __restrict__ tile_hist,
+    uint32_t* __restrict__ tile_hist_done) {
+  __shared__ uint32_t sh[kMaxPasses][256];  // the tile sort's digit histograms
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_warp[8];
   __shared__ unsigned long long s_excl;
@@ -359,6 +299,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(
   __shared__ uint32_t s_emit_gid[kEmitWindow];
   const int tid = threadIdx.x;
   if (tid == 0) s_tile = atomicAdd(counter, 1u);
+  hist_zero(sh);
   // empty ranges for the tile sort's epilogue (its atomics run after this kernel)
   for (int k = blockIdx.x * kScanThreads + tid; k < n_tiles; k += gridDim.x * kScanThreads)
     ranges[k] = make_uint2(0xFFFFFFFFu, 0u);
@@ -430,14 +371,19 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(
     __syncthreads();
     const uint32_t cnt = min(tot - w, (uint32_t)kEmitWindow);
     const unsigned long long o0 = cta0 + w;
-    for (uint32_t i = tid; i < cnt; i += kScanThreads) {
-      if (o0 + i < (unsigned long long)key_cap) {
-        tile_keys[o0 + i] = s_emit_key[i];
+    for (uint32_t i0 = 0; i0 < cnt; i0 += kScanThreads) {  // warp-uniform trip count
+      const uint32_t i = i0 + tid;
+      const bool ok = i < cnt && o0 + i < (unsigned long long)key_cap;
+      const uint32_t k = ok ? s_emit_key[i] : 0u;
+      if (ok) {
+        tile_keys[o0 + i] = k;
         emit_gid[o0 + i] = s_emit_gid[i];
       }
+      hist_add_warp(sh, k, ok, tile_passes);  // only keys that are written are counted
     }
     __syncthreads();
   }
+  hist_publish(sh, tile_passes, tile_hist, tile_hist_done);
 }
 
 }  // namespace
@@ -449,13 +395,15 @@ void launch_scan_emit(const uint32_t* order, const uint32_t* ntiles, const uint2
                       uint32_t* tile_keys, uint32_t* emit_gid, int64_t key_cap,
                       unsigned long long* scratch, uint32_t* counter, uint32_t* n_keys,
                       unsigned long long* n_keys_total, uint2* ranges, int n_tiles,
+                      int tile_passes, uint32_t* tile_hist, uint32_t* tile_hist_done,
                       cudaStream_t st) {
   const int64_t tiles = scan_emit_scratch_words(n);
   if (tiles == 0) return;  // caller zeroed the counts
   k_scan_emit<<<(unsigned)tiles, kScanThreads, 0, st>>>(order, ntiles, tilebox, ms, n, fp,
                                                         slot_off, tile_keys, emit_gid, key_cap,
                                                         scratch, counter, n_keys, n_keys_total,
-                                                        ranges, n_tiles);
+                                                        ranges, n_tiles, tile_passes, tile_hist,
+                                                        tile_hist_done);
 }
 
 void launch_ranges_fix(const uint32_t* n_keys, int64_t key_cap, int n_tiles, uint2* ranges,
@@ -465,18 +413,21 @@ void launch_ranges_fix(const uint32_t* n_keys, int64_t key_cap, int n_tiles, uin
 
 int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], bool iota_vals, const uint32_t* n_dev,
                      int64_t cap, int key_bits, SortScratch& s, cudaStream_t st,
-                     int64_t* launches, bool scratch_zeroed, const SortEpilogue& epi) {
+                     int64_t* launches, const SortOptions& opt) {
+  const SortEpilogue& epi = opt.epi;
   const int passes = (key_bits + 7) / 8;
   const int64_t tiles = (cap + kSortTileItems - 1) / kSortTileItems;
   // caller guarantees tiles <= s.max_tiles and passes <= kMaxPasses
-  if (!scratch_zeroed) {
+  if (!opt.scratch_zeroed) {
     cudaMemsetAsync(s.hist, 0, sizeof(uint32_t) * kMaxPasses * 256, st);
     cudaMemsetAsync(s.counters, 0, sizeof(uint32_t) * (kMaxPasses + 1), st);
     cudaMemsetAsync(s.lookback, 0, sizeof(uint32_t) * 256 * (size_t)tiles * passes, st);
   }
-  const int hist_blocks = (int)std::min<int64_t>(std::max<int64_t>(tiles, 1), 148 * 4);
-  k_hist<<<hist_blocks, 256, 0, st>>>(keys[0], n_dev, cap, passes, s.hist,
-                                      s.counters + kMaxPasses);
+  if (!opt.hist_ready) {
+    const int hist_blocks = (int)std::min<int64_t>(std::max<int64_t>(tiles, 1), 148 * 4);
+    k_hist<<<hist_blocks, 256, 0, st>>>(keys[0], n_dev, cap, passes, s.hist,
+                                        s.counters + kMaxPasses);
+  }
   int cur = 0;
   const size_t smem = sizeof(OnesweepSmem);
   static const bool attr_set = [&] {  // once, outside any graph capture
@@ -496,7 +447,7 @@ int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], bool iota_vals, const
         s.counters + p, fin ? epi : SortEpilogue());
     cur ^= 1;
   }
-  if (launches) *launches += 1 + passes;
+  if (launches) *launches += (opt.hist_ready ? 0 : 1) + passes;
   return cur;
 }
 
