@@ -41,6 +41,7 @@ constexpr int kBT = 64;      // threads per tile CTA: 2 warps x 8 four-lane grou
 #endif
 constexpr int kBatch = ISG_FWD_BATCH;  // records staged per batch
 constexpr int kWords = kBatch / 32;
+static_assert(kBatch < 256, "u8 list entries, sentinel index kBatch");
 constexpr int kListPitch = kBatch + 4;  // sub-quarter lists start in different banks
 
 // One row of a lane's 2x2 pixel quad: two horizontally adjacent pixels as packed f32x2 lanes
@@ -54,10 +55,10 @@ struct FwdPair {
 
 __device__ __forceinline__ float2 bc(float v) { return make_float2(v, v); }
 
-__device__ __forceinline__ void fwd_pair(FwdPair& p, bool has, float2 r2, const float4 g,
-                                         const float4 c, float t_min, uint32_t idx) {
-  const bool in0 = has && !(r2.x > g.z) && (p.T.x > t_min);
-  const bool in1 = has && !(r2.y > g.z) && (p.T.y > t_min);
+__device__ __forceinline__ void fwd_pair(FwdPair& p, float2 r2, const float4 g, const float4 c,
+                                         float t_min, uint32_t idx) {
+  const bool in0 = !(r2.x > g.z) && (p.T.x > t_min);
+  const bool in1 = !(r2.y > g.z) && (p.T.y > t_min);
   const float2 q = __fmul2_rn(r2, bc(g.w));
   const float2 e = __fmul2_rn(bc(c.w), make_float2(fast_exp2(q.x), fast_exp2(q.y)));
   const float2 a = make_float2(in0 ? e.x : 0.0f, in1 ? e.y : 0.0f);
@@ -78,9 +79,15 @@ __global__ void ISG_FWD_BOUNDS k_blend_fwd(
     const RenderRec* __restrict__ rec, const unsigned long long* __restrict__ total,
     int64_t key_cap, float* __restrict__ out, float* __restrict__ t_last,
     uint32_t* __restrict__ n_proc) {
-  __shared__ Stage<kBatch> st[2];
+  // entry kBatch of each stage is a sentinel no pixel is inside (r2max = -1): the groups'
+  // lists are padded with it to the warp's step count, so the walk needs no bounds test
+  __shared__ Stage<kBatch + 1> st[2];
   __shared__ uint8_t s_list[16][kListPitch];
   if (overflowed(total, key_cap)) return;
+  if (threadIdx.x < 2) {
+    st[threadIdx.x].geo[kBatch] = make_float4(0.0f, 0.0f, -1.0f, 0.0f);
+    st[threadIdx.x].col[kBatch] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+  }
   const int tile = blockIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int gq = lane >> 2, l4 = lane & 3;  // four-lane group = one 4x4 sub-quarter
@@ -127,7 +134,7 @@ __global__ void ISG_FWD_BOUNDS k_blend_fwd(
 
   if (n > 0) stage_batch<kBT>(st[0], sorted, rec, rg.x, min(kBatch, n));
   for (int b = 0, it = 0; b < n; b += kBatch, ++it) {
-    Stage<kBatch>& cur = st[it & 1];
+    Stage<kBatch + 1>& cur = st[it & 1];
     cp_async_wait_all();
     const bool live = P[0].T.x > t_min || P[0].T.y > t_min || P[1].T.x > t_min ||
                       P[1].T.y > t_min;
@@ -175,11 +182,11 @@ __global__ void ISG_FWD_BOUNDS k_blend_fwd(
       steps = max(steps, ck);
       if (k == gq) my_cnt = ck;
     }
+    for (int e = my_cnt + l4; e < steps; e += 4) s_list[sub][e] = (uint8_t)kBatch;
     __syncwarp();
     const uint8_t* my_list = s_list[sub];
     for (int i = 0; i < steps; ++i) {
-      const bool has = i < my_cnt;
-      const int jj = has ? my_list[i] : 0;
+      const int jj = my_list[i];
       const float4 g = cur.geo[jj], c = cur.col[jj];
       const float2 dx = __fadd2_rn(PX, bc(-g.x));
       const float2 dy = __fadd2_rn(PY, bc(-g.y));
@@ -191,7 +198,7 @@ __global__ void ISG_FWD_BOUNDS k_blend_fwd(
       for (int k = 0; k < 2; ++k) {
         const float dyk = k ? dy.y : dy.x;
         const float2 r2 = __fadd2_rn(ax, bc(__fmul_rn(dyk, dyk)));
-        fwd_pair(P[k], has, r2, g, c, t_min, idx);
+        fwd_pair(P[k], r2, g, c, t_min, idx);
       }
     }
   }
