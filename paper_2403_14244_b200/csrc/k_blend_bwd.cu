@@ -116,7 +116,9 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
     int64_t key_cap, const float* __restrict__ img, const float* __restrict__ target,
     const float* __restrict__ t_last, const uint32_t* __restrict__ n_proc, float loss_scale,
     float4* __restrict__ partial, double* __restrict__ tile_loss) {
-  __shared__ Stage<kBatch> st[2];
+  // entry kBatch of each stage is a sentinel no pixel is inside (r2max = -1): the groups'
+  // lists are padded with it to the warp's step count, so the walk needs no bounds test
+  __shared__ Stage<kBatch + 1> st[2];
   // [sub-quarter][value][entry]; rows padded so one entry's 8 values hit 8 different banks
   __shared__ float s_part[kSubs][8][kBatch + 1];
   __shared__ uint32_t s_rel[kSubs][kWords];  // relevance ballots of the batch per sub-quarter
@@ -127,6 +129,10 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
   if (overflowed(total, key_cap)) {
     if (threadIdx.x == 0) tile_loss[tile] = 0.0;
     return;
+  }
+  if (threadIdx.x < 2) {
+    st[threadIdx.x].geo[kBatch] = make_float4(0.0f, 0.0f, -1.0f, 0.0f);
+    st[threadIdx.x].col[kBatch] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
   }
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int gq = lane >> 2, l4 = lane & 3;  // four-lane group = one 4x4 sub-quarter
@@ -222,7 +228,7 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
   for (int it = 0; hi > 0; ++it) {
     const int lo = max(0, hi - kBatch);
     const int cnt = hi - lo;
-    Stage<kBatch>& cur = st[it & 1];
+    Stage<kBatch + 1>& cur = st[it & 1];
     cp_async_wait_all();
     __syncthreads();  // batch visible; previous batch's flush finished reading s_part
     if (lo > 0) {
@@ -255,7 +261,8 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
         const int c = (k >> 2) * 2 + (k & 1), r = (k >> 1) & 1;
         const bool hk = in && cv[c] && rv[r] && !(__fadd_rn(ax4[c], ay2[r]) > g.z);
         const uint32_t mk = __ballot_sync(0xffffffffu, hk);
-        if (hk) s_list[8 * w + k][base[k] + __popc(mk & lt)] = (uint8_t)j;
+        // stored in reverse depth order (one ballot word: the count is known here)
+        if (hk) s_list[8 * w + k][__popc(mk) - 1 - __popc(mk & lt)] = (uint8_t)j;
         if (lane == 0) s_rel[8 * w + k][wd] = mk;
         base[k] += __popc(mk);
       }
@@ -265,12 +272,13 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
       steps = max(steps, base[k]);
       if (k == gq) my_cnt = base[k];
     }
+    for (int e = my_cnt + l4; e < steps; e += 4) s_list[sub][e] = (uint8_t)kBatch;
     __syncwarp();
     const uint8_t* my_list = s_list[sub];
     for (int s = 0; s < steps; ++s) {
-      const int i = my_cnt - 1 - s;  // reverse depth order
-      const bool has = i >= 0;
-      const int jj = has ? my_list[i] : 0;
+      // reverse depth order; the sentinel has a = 0 for every pixel, so T (T / 1) and G.A stay
+      // exactly unchanged whatever j is, and its s_part column kBatch is padding
+      const int jj = my_list[s];
       const int j = lo + jj;
       const float4 g = cur.geo[jj];
       const float4 c = cur.col[jj];
@@ -288,8 +296,8 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
         const float dyk = k ? dy.y : dy.x;
         const float ay = __fmul_rn(dyk, dyk);
         const float2 r2 = __fadd2_rn(ax, bc(ay));
-        const bool act0 = has && j < P[k].np0 && !(r2.x > g.z);
-        const bool act1 = has && j < P[k].np1 && !(r2.y > g.z);
+        const bool act0 = j < P[k].np0 && !(r2.x > g.z);
+        const bool act1 = j < P[k].np1 && !(r2.y > g.z);
         bwd_pair(P[k], act0, act1, j, dx, dyk, r2, g, c, acc2);
       }
       float acc[8];
@@ -300,10 +308,8 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
       // the lane holds values vb, vb + 1 (vb = 4 (l4 >> 1) + 2 (l4 & 1)); the per-splat
       // scale factors are applied once per entry in the flush
       const int vb = 4 * (l4 >> 1) + 2 * (l4 & 1);
-      if (has) {
-        s_part[sub][vb][jj] = y[0];
-        s_part[sub][vb + 1][jj] = y[1];
-      }
+      s_part[sub][vb][jj] = y[0];  // the sentinel writes the padding column
+      s_part[sub][vb + 1][jj] = y[1];
     }
     __syncthreads();
     // combine the sub-quarters in a fixed order and write each (tile, splat) pair's slot:
