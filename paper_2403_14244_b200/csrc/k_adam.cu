@@ -149,7 +149,15 @@ __global__ void __launch_bounds__(256) k_project_backward(
   grad3d[2 * i + 1] = g1;
 }
 
-__global__ void __launch_bounds__(256) k_project_adam(
+#ifndef ISG_ADAM_MINB
+#define ISG_ADAM_MINB 0
+#endif
+#if ISG_ADAM_MINB > 0
+#define ISG_ADAM_BOUNDS __launch_bounds__(256, ISG_ADAM_MINB)
+#else
+#define ISG_ADAM_BOUNDS __launch_bounds__(256)
+#endif
+__global__ void ISG_ADAM_BOUNDS k_project_adam(
     float4* __restrict__ ms, float4* __restrict__ co, int64_t n, FrameParams fp,
     const uint32_t* __restrict__ slot_off, const uint32_t* __restrict__ slot_of,
     const uint32_t* __restrict__ ntiles, const float4* __restrict__ partial,
