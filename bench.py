@@ -382,6 +382,10 @@ def run_isg(args):
     flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if flush else None
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     ev_s = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)] if flush else None
+    if train:
+        # the stage-timing pass and the end-to-end region below restart from this state, so
+        # all three measure the same training trajectory (the scene evolves under Adam)
+        r.snapshot()
     barrier()
     launches_t0 = r.stats()["kernel_launches"]
     with ClockSampler(local) as clocks:
@@ -413,6 +417,8 @@ def run_isg(args):
     launches_timed = r.stats()["kernel_launches"] - launches_t0
 
     # ---- stage timing (separate pass, events per kernel, kernel by kernel) ----------------
+    if train:
+        r.restore()
     r.profile(True)
     r.profile_read()
     prof_steps = max(3, min(args.steps, 10))
@@ -467,6 +473,8 @@ def run_isg(args):
         ev_copy = [torch.cuda.Event() for _ in range(2)]
         ev_done = [torch.cuda.Event() for _ in range(2)]
         r.synchronize()
+    if train:
+        r.restore()
     barrier()
     l0 = r.stats()["kernel_launches"]
     t_start = time.perf_counter()
