@@ -48,19 +48,20 @@ METRIC = "fwd+bwd train iters/sec (1M isotropic Gaussians, 1080p)"
 FWD_FLOP_EVAL, FWD_FLOP_IN = 6, 12      # 3-sigma test; exp+alpha+composite+transmittance
 BWD_FLOP_EVAL, BWD_FLOP_IN = 6, 36      # same test; transmittance recovery + 7 gradients
 FP32_LANES = 148 * 128
-NCU_SUMMARY = "profiles/r1/ncu_full_blend.json"  # dram traffic per launch, --set full capture
+NCU_SUMMARY = "profiles/r1/ncu_full_step.json"  # dram traffic per launch, --set full capture
 
 
 def stage_bytes(n, keys, tiles):
     """Algorithmic DRAM bytes per step of the memory-bound stages:
-    K1 32 B read + 56 B written per splat; onesweep: 4 B histogram read + per pass 8 B read +
-    8 B written per item (depth: 4 passes over n, tiles: 2 passes over the keys); scan/emit:
+    K1 32 B read + 56 B written per splat (plus the depth histograms, negligible); depth sort:
+    per pass 8 B read + 8 B written per splat (4 passes; K1 built the histograms); scan/emit:
     order + tile count + tile box + slot offset (20 B) per splat, tile key + splat (8 B) per
-    key; ranges: 12 B read + 8 B written per key + 8 B per tile; K8: 96 B read + 96 B written
-    per splat + 32 B per gradient slot."""
-    return {"preprocess": 88 * n, "depth_sort": (4 + 4 * 16) * n,
-            "scan_emit": 20 * n + 8 * keys, "tile_sort": (4 + 2 * 16) * keys,
-            "ranges": 20 * keys + 8 * tiles, "project_adam": 192 * n + 32 * keys}
+    key, range init 8 B per tile; tile sort: pass 1 reads the key and writes key + index
+    (12 B), the last pass reads key + index, gathers the splat and writes the (splat, slot)
+    pair (20 B) per key; K8: 96 B read + 96 B written per splat + 32 B per gradient slot."""
+    return {"preprocess": 88 * n, "depth_sort": 4 * 16 * n,
+            "scan_emit": 20 * n + 8 * keys + 8 * tiles, "tile_sort": 32 * keys,
+            "project_adam": 192 * n + 32 * keys}
 
 
 def ncu_traffic(kernel: str):
