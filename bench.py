@@ -422,7 +422,7 @@ def run_isg(args):
         r.restore()
     r.profile(True)
     r.profile_read()
-    prof_steps = max(3, min(args.steps, 10))
+    prof_steps = args.steps  # the same trajectory as the timed region (the scene trains)
     for _ in range(prof_steps):
         step_eager()
     prof = r.profile_read()

@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "isg_internal.cuh"
+#include "pdl.cuh"
 
 // Stage timing (isg_profile_*): CUDA events around each kernel of a frame, on the launching
 // stream, so bench.py can report the dominant kernel's live launch duration.
@@ -1321,6 +1322,7 @@ isg_status isg_set_binning(isg_ctx* ctx, int mode) {
 isg_status isg_profile_enable(isg_ctx* ctx, int on) {
   if (!ctx) return ISG_E_ARG;
   ctx->prof = on != 0;
+  isg::g_pdl_enabled = !ctx->prof;
   return ISG_OK;
 }
 

@@ -5,6 +5,7 @@
 // tile keys, sort order, ranges and 3-sigma inclusion are bit-identical to it.
 #pragma once
 #include "isg_internal.cuh"
+#include "pdl.cuh"
 
 namespace isg {
 

@@ -114,6 +114,7 @@ __device__ __forceinline__ void adam_update(float4* __restrict__ ms, float4* __r
 // One thread: step counter, bias corrections (torch.optim.Adam: step_size = lr / (1 - b1^t),
 // denominator sqrt(v) / sqrt(1 - b2^t) + eps) and the loss hand-over of the step.
 __global__ void k_adam_tick(AdamParams in, AdamState* __restrict__ st, double* __restrict__ loss) {
+  pdl_enter();
   const long long t = st->t + 1;
   st->t = t;
   const double bc1 = 1.0 - pow((double)in.b1, (double)t);
@@ -164,6 +165,7 @@ __global__ void ISG_ADAM_BOUNDS k_project_adam(
     const unsigned long long* __restrict__ total, int64_t cap, float4* __restrict__ m,
     float4* __restrict__ v, const AdamState* __restrict__ state,
     unsigned long long* __restrict__ skipped) {
+  pdl_enter();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (*total > (unsigned long long)cap) return;  // overflowed frame: no update (host re-runs)
@@ -204,8 +206,8 @@ void launch_project_adam(float4* ms, float4* co, int64_t n, const FrameParams& f
                          const unsigned long long* total, int64_t cap, float4* m, float4* v,
                          const AdamState* ap, unsigned long long* skipped, cudaStream_t st) {
   if (n <= 0) return;
-  k_project_adam<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
-      ms, co, n, fp, slot_off, slot_of, ntiles, partial, total, cap, m, v, ap, skipped);
+  launch_pdl(k_project_adam, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, ms, co, n,
+             fp, slot_off, slot_of, ntiles, partial, total, cap, m, v, ap, skipped);
 }
 
 void launch_adam(float4* ms, float4* co, int64_t n, const float4* grad3d, float4* m, float4* v,
@@ -221,7 +223,7 @@ void launch_adam_tick(const float lr[4], float b1, float b2, float eps, AdamStat
   in.b1 = b1;
   in.b2 = b2;
   in.eps = eps;
-  k_adam_tick<<<1, 1, 0, st>>>(in, st_dev, loss);
+  launch_pdl(k_adam_tick, dim3(1), dim3(1), 0, st, in, st_dev, loss);
 }
 
 }  // namespace isg

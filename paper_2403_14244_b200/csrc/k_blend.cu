@@ -83,6 +83,7 @@ __global__ void ISG_FWD_BOUNDS k_blend_fwd(
   // lists are padded with it to the warp's step count, so the walk needs no bounds test
   __shared__ Stage<kBatch + 1> st[2];
   __shared__ uint8_t s_list[16][kListPitch];
+  pdl_enter();
   if (overflowed(total, key_cap)) return;
   if (threadIdx.x < 2) {
     st[threadIdx.x].geo[kBatch] = make_float4(0.0f, 0.0f, -1.0f, 0.0f);
@@ -225,8 +226,8 @@ __global__ void ISG_FWD_BOUNDS k_blend_fwd(
 void launch_blend_fwd(const FrameParams& fp, const uint2* ranges, const uint2* sorted,
                       const RenderRec* rec, const unsigned long long* total, int64_t key_cap,
                       float* out, float* t_last, uint32_t* n_proc, cudaStream_t st) {
-  k_blend_fwd<<<fp.n_tiles, kBT, 0, st>>>(fp, ranges, sorted, rec, total, key_cap, out, t_last,
-                                          n_proc);
+  launch_pdl(k_blend_fwd, dim3(fp.n_tiles), dim3(kBT), 0, st, fp, ranges, sorted, rec, total,
+             key_cap, out, t_last, n_proc);
 }
 
 }  // namespace isg

@@ -126,6 +126,7 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
   __shared__ float s_red[2];
   __shared__ int s_max[2];
   const int tile = blockIdx.x;
+  pdl_enter();
   if (overflowed(total, key_cap)) {
     if (threadIdx.x == 0) tile_loss[tile] = 0.0;
     return;
@@ -371,6 +372,7 @@ __global__ void __launch_bounds__(kTilePixels) k_l2_tiles(FrameParams fp,
 // scale * sum(tile_loss) in a fixed order: added to *accum (if not null), stored to *set.
 __global__ void k_loss_reduce(const double* __restrict__ tile_loss, int n_tiles, double scale,
                               double* __restrict__ accum, double* __restrict__ set) {
+  pdl_enter();
   __shared__ double s[256];
   double acc = 0.0;
   for (int i = threadIdx.x; i < n_tiles; i += 256) acc += tile_loss[i];
@@ -391,19 +393,15 @@ void launch_blend_bwd(const FrameParams& fp, const uint2* ranges, const uint2* s
                       const float* img, const float* target, const float* t_last,
                       const uint32_t* n_proc, float loss_scale, float4* partial,
                       double* tile_loss, bool given_dldc, cudaStream_t st) {
-  if (given_dldc)
-    k_blend_bwd<true><<<fp.n_tiles, kBT, 0, st>>>(fp, ranges, sorted, rec, total, key_cap, img,
-                                                  target, t_last, n_proc, loss_scale, partial,
-                                                  tile_loss);
-  else
-    k_blend_bwd<false><<<fp.n_tiles, kBT, 0, st>>>(fp, ranges, sorted, rec, total, key_cap, img,
-                                                   target, t_last, n_proc, loss_scale, partial,
-                                                   tile_loss);
+  launch_pdl(given_dldc ? k_blend_bwd<true> : k_blend_bwd<false>, dim3(fp.n_tiles), dim3(kBT),
+             0, st, fp, ranges, sorted, rec, total, key_cap, img, target, t_last, n_proc,
+             loss_scale, partial, tile_loss);
 }
 
 void launch_loss_reduce(const double* tile_loss, int n_tiles, double scale, double* accum,
                         double* set, cudaStream_t st) {
-  k_loss_reduce<<<1, 256, 0, st>>>(tile_loss, n_tiles, scale, accum, set);
+  launch_pdl(k_loss_reduce, dim3(1), dim3(256), 0, st, (const double*)tile_loss, n_tiles, scale,
+             accum, set);
 }
 
 void launch_l2_tiles(const FrameParams& fp, const float* img, const float* target,

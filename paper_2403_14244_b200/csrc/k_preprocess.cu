@@ -27,6 +27,7 @@ __global__ void __launch_bounds__(256) k_preprocess(const float4* __restrict__ m
                                                     uint32_t* __restrict__ sc,
                                                     uint32_t* __restrict__ hist,
                                                     uint32_t* __restrict__ hist_done) {
+  pdl_enter();
   // radix mode: the depth sort's 4 digit histograms (radix_hist.cuh)
   __shared__ uint32_t sh[kMaxPasses][256];
   if (hist) {
@@ -92,8 +93,8 @@ void launch_preprocess(const float4* ms, const float4* co, int64_t n, const Fram
                        uint32_t* tile_cnt, uint32_t* sc, uint32_t* hist, uint32_t* hist_done,
                        cudaStream_t st) {
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
-  k_preprocess<<<(unsigned)blocks, 256, 0, st>>>(ms, co, n, fp, rec, depth_key, ntiles, tilebox,
-                                                 tile_cnt, sc, hist, hist_done);
+  launch_pdl(k_preprocess, dim3((unsigned)blocks), dim3(256), 0, st, ms, co, n, fp, rec,
+             depth_key, ntiles, tilebox, tile_cnt, sc, hist, hist_done);
 }
 
 // Parity hook: (tile << 32 | float_bits(depth)) and splat index for each sorted entry.

@@ -67,6 +67,7 @@ __global__ void __launch_bounds__(256) k_hist(const uint32_t* __restrict__ keys,
                                               const uint32_t* __restrict__ n_dev, int64_t cap,
                                               int passes, uint32_t* __restrict__ hist,
                                               uint32_t* __restrict__ done) {
+  pdl_enter();
   __shared__ uint32_t sh[kMaxPasses][256];
   hist_zero(sh);
   __syncthreads();
@@ -109,6 +110,7 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
     const uint32_t* __restrict__ n_dev, int64_t cap, int shift,
     const uint32_t* __restrict__ hist, uint32_t* __restrict__ lookback,
     uint32_t* __restrict__ counter, SortEpilogue epi) {
+  pdl_enter();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   OnesweepSmem& S = *reinterpret_cast<OnesweepSmem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -291,6 +293,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(
     uint32_t* __restrict__ n_keys, unsigned long long* __restrict__ n_keys_total,
     uint2* __restrict__ ranges, int n_tiles, int tile_passes, uint32_t* __restrict__ tile_hist,
     uint32_t* __restrict__ tile_hist_done) {
+  pdl_enter();
   __shared__ uint32_t sh[kMaxPasses][256];  // the tile sort's digit histograms
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_warp[8];
@@ -399,11 +402,9 @@ void launch_scan_emit(const uint32_t* order, const uint32_t* ntiles, const uint2
                       cudaStream_t st) {
   const int64_t tiles = scan_emit_scratch_words(n);
   if (tiles == 0) return;  // caller zeroed the counts
-  k_scan_emit<<<(unsigned)tiles, kScanThreads, 0, st>>>(order, ntiles, tilebox, ms, n, fp,
-                                                        slot_off, tile_keys, emit_gid, key_cap,
-                                                        scratch, counter, n_keys, n_keys_total,
-                                                        ranges, n_tiles, tile_passes, tile_hist,
-                                                        tile_hist_done);
+  launch_pdl(k_scan_emit, dim3((unsigned)tiles), dim3(kScanThreads), 0, st, order, ntiles,
+             tilebox, ms, n, fp, slot_off, tile_keys, emit_gid, key_cap, scratch, counter, n_keys,
+             n_keys_total, ranges, n_tiles, tile_passes, tile_hist, tile_hist_done);
 }
 
 void launch_ranges_fix(const uint32_t* n_keys, int64_t key_cap, int n_tiles, uint2* ranges,
@@ -425,8 +426,8 @@ int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], bool iota_vals, const
   }
   if (!opt.hist_ready) {
     const int hist_blocks = (int)std::min<int64_t>(std::max<int64_t>(tiles, 1), 148 * 4);
-    k_hist<<<hist_blocks, 256, 0, st>>>(keys[0], n_dev, cap, passes, s.hist,
-                                        s.counters + kMaxPasses);
+    launch_pdl(k_hist, dim3(hist_blocks), dim3(256), 0, st, (const uint32_t*)keys[0], n_dev,
+               cap, passes, s.hist, s.counters + kMaxPasses);
   }
   int cur = 0;
   const size_t smem = sizeof(OnesweepSmem);
@@ -440,11 +441,12 @@ int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], bool iota_vals, const
   (void)attr_set;
   for (int p = 0; p < passes; ++p) {
     const bool fin = p == passes - 1 && epi.sorted;
-    (fin ? k_onesweep<true> : k_onesweep<false>)<<<(unsigned)std::max<int64_t>(tiles, 1),
-                                                  kSortThreads, smem, st>>>(
-        keys[cur], (p == 0 && iota_vals) ? nullptr : vals[cur], keys[cur ^ 1], vals[cur ^ 1],
-        n_dev, cap, 8 * p, s.hist + 256 * p, s.lookback + (size_t)256 * tiles * p,
-        s.counters + p, fin ? epi : SortEpilogue());
+    launch_pdl(fin ? k_onesweep<true> : k_onesweep<false>,
+               dim3((unsigned)std::max<int64_t>(tiles, 1)), dim3(kSortThreads), smem, st,
+               (const uint32_t*)keys[cur], (const uint32_t*)((p == 0 && iota_vals) ? nullptr : vals[cur]),
+               keys[cur ^ 1], vals[cur ^ 1], n_dev, cap, 8 * p, (const uint32_t*)(s.hist + 256 * p),
+               s.lookback + (size_t)256 * tiles * p, s.counters + p,
+               fin ? epi : SortEpilogue());
     cur ^= 1;
   }
   if (launches) *launches += (opt.hist_ready ? 0 : 1) + passes;
