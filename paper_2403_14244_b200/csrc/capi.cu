@@ -417,13 +417,15 @@ isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out) {
   const int64_t n = ctx->n;
   {
   ISG_STAGE(ST_MEMSET);
-  // scalars sc[0..7] and the frame's key total (contiguous): all zero
-  ISG_CUDA(cudaMemsetAsync(ctx->sc, 0, sizeof(uint32_t) * 8 + sizeof(unsigned long long), st));
-  // scan look-back + both sorts' histograms, counters and look-back statuses: one memset
+  // scan look-back + both sorts' histograms, counters and look-back statuses, and the scalars
+  // sc[0..7] + the frame's key total (contiguous): one zeroing kernel
   const size_t zero = radix ? (size_t)((unsigned char*)ctx->sort_tile.lookback - ctx->arena) +
                                   isg::sort_lookback_bytes(ctx->key_cap, 2)
                             : ctx->arena_depth_end;
-  ISG_CUDA(cudaMemsetAsync(ctx->arena, 0, zero, st));
+  isg::launch_zero2(ctx->arena, zero, ctx->sc, sizeof(uint32_t) * 8 + sizeof(unsigned long long),
+                    st);
+  ISG_CHECK_LAUNCH();
+  ctx->launches++;
   if (!radix) ISG_CUDA(cudaMemsetAsync(ctx->tile_cnt, 0, sizeof(uint32_t) * fp.n_tiles, st));
   }
   {

@@ -96,6 +96,9 @@ void launch_preprocess(const float4* ms, const float4* co, int64_t n, const Fram
                        uint32_t* tile_cnt, uint32_t* sc, uint32_t* hist, uint32_t* hist_done,
                        cudaStream_t st);
 
+// zero [a, a + a_bytes) and [b, b + b_bytes) (the frame's scratch reset)
+void launch_zero2(void* a, size_t a_bytes, void* b, size_t b_bytes, cudaStream_t st);
+
 // ---- tile-bucket binning (k_bin.cu) -------------------------------------------------------
 int64_t fill_scratch_words(int64_t n);  // + 1 zeroed u64 words of look-back scratch
 void launch_tile_scan(const uint32_t* cnt, int n_tiles, int64_t cap, uint2* ranges,

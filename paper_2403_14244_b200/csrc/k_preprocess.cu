@@ -97,6 +97,26 @@ void launch_preprocess(const float4* ms, const float4* co, int64_t n, const Fram
              depth_key, ntiles, tilebox, tile_cnt, sc, hist, hist_done);
 }
 
+// Frame scratch reset (the two regions a frame needs zeroed), as a kernel so that it joins the
+// programmatic-dependent-launch chain instead of breaking it like a memset node would.
+__global__ void __launch_bounds__(256) k_zero2(unsigned char* __restrict__ a, size_t a_bytes,
+                                               unsigned char* __restrict__ b, size_t b_bytes) {
+  pdl_enter();
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t a16 = ((uintptr_t)a & 15) ? 0 : a_bytes / 16;
+  for (size_t i = tid; i < a16; i += stride)
+    reinterpret_cast<uint4*>(a)[i] = make_uint4(0u, 0u, 0u, 0u);
+  for (size_t i = 16 * a16 + tid; i < a_bytes; i += stride) a[i] = 0;
+  for (size_t i = tid; i < b_bytes; i += stride) b[i] = 0;
+}
+
+void launch_zero2(void* a, size_t a_bytes, void* b, size_t b_bytes, cudaStream_t st) {
+  const size_t blocks = std::min<size_t>(std::max<size_t>((a_bytes / 16 + 255) / 256, 1), 148 * 4);
+  launch_pdl(k_zero2, dim3((unsigned)blocks), dim3(256), 0, st, (unsigned char*)a, a_bytes,
+             (unsigned char*)b, b_bytes);
+}
+
 // Parity hook: (tile << 32 | float_bits(depth)) and splat index for each sorted entry.
 __global__ void k_debug_keys(const uint2* __restrict__ ranges, const uint2* __restrict__ sorted,
                              const float4* __restrict__ ms, FrameParams fp,
