@@ -370,21 +370,34 @@ __global__ void __launch_bounds__(kTilePixels) k_l2_tiles(FrameParams fp,
 }
 
 // scale * sum(tile_loss) in a fixed order: added to *accum (if not null), stored to *set.
-__global__ void k_loss_reduce(const double* __restrict__ tile_loss, int n_tiles, double scale,
-                              double* __restrict__ accum, double* __restrict__ set) {
+constexpr int kReduceThreads = 1024;
+__global__ void __launch_bounds__(kReduceThreads) k_loss_reduce(
+    const double* __restrict__ tile_loss, int n_tiles, double scale, double* __restrict__ accum,
+    double* __restrict__ set) {
   pdl_enter();
-  __shared__ double s[256];
+  __shared__ double s[kReduceThreads / 32];
+  // fixed order: thread t sums tiles t, t + 1024, ... (8 loads in flight), then a fixed
+  // shuffle tree and a fixed sum over the warps
   double acc = 0.0;
-  for (int i = threadIdx.x; i < n_tiles; i += 256) acc += tile_loss[i];
-  s[threadIdx.x] = acc;
-  __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {
-    if ((int)threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
-    __syncthreads();
+  for (int i0 = 0; i0 < n_tiles; i0 += 8 * kReduceThreads) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u * kReduceThreads + (int)threadIdx.x;
+      v[u] = i < n_tiles ? tile_loss[i] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += v[u];
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = acc;
+  __syncthreads();
   if (threadIdx.x == 0) {
-    if (accum) *accum += s[0] * scale;
-    *set = s[0] * scale;
+    double t = 0.0;
+    for (int w = 0; w < kReduceThreads / 32; ++w) t += s[w];
+    if (accum) *accum += t * scale;
+    *set = t * scale;
   }
 }
 
@@ -400,8 +413,8 @@ void launch_blend_bwd(const FrameParams& fp, const uint2* ranges, const uint2* s
 
 void launch_loss_reduce(const double* tile_loss, int n_tiles, double scale, double* accum,
                         double* set, cudaStream_t st) {
-  launch_pdl(k_loss_reduce, dim3(1), dim3(256), 0, st, (const double*)tile_loss, n_tiles, scale,
-             accum, set);
+  launch_pdl(k_loss_reduce, dim3(1), dim3(kReduceThreads), 0, st, (const double*)tile_loss,
+             n_tiles, scale, accum, set);
 }
 
 void launch_l2_tiles(const FrameParams& fp, const float* img, const float* target,
