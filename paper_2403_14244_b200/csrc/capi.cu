@@ -26,13 +26,13 @@
 // Stage timing (isg_profile_*): CUDA events around each kernel of a frame, on the launching
 // stream, so bench.py can report the dominant kernel's live launch duration.
 enum Stage {
-  ST_MEMSET, ST_PREPROCESS, ST_DEPTH_SORT, ST_SCAN_EMIT, ST_TILE_SCAN, ST_FILL, ST_TILE_SORT,
-  ST_RANGES, ST_BLEND_FWD, ST_BLEND_BWD, ST_LOSS_REDUCE, ST_PROJECT_BWD, ST_PROJECT_ADAM, ST_ADAM,
+  ST_RESET, ST_PREPROCESS, ST_DEPTH_SORT, ST_SCAN_EMIT, ST_TILE_SCAN, ST_FILL, ST_TILE_SORT,
+  ST_BLEND_FWD, ST_BLEND_BWD, ST_LOSS_REDUCE, ST_PROJECT_BWD, ST_PROJECT_ADAM, ST_ADAM,
   ST_ALLREDUCE, ST_IMAGE_LOSS, ST_COUNT
 };
 static const char* kStageNames[ST_COUNT] = {
-    "memset", "preprocess", "depth_sort", "scan_emit", "tile_scan", "fill", "tile_sort",
-    "ranges", "blend_fwd", "blend_bwd", "loss_reduce", "project_bwd", "project_adam", "adam",
+    "frame_reset", "preprocess", "depth_sort", "scan_emit", "tile_scan", "fill", "tile_sort",
+    "blend_fwd", "blend_bwd", "loss_reduce", "project_bwd", "project_adam", "adam",
     "allreduce", "image_loss"};
 
 
@@ -416,7 +416,7 @@ isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out) {
   cudaStream_t st = ctx->stream;
   const int64_t n = ctx->n;
   {
-  ISG_STAGE(ST_MEMSET);
+  ISG_STAGE(ST_RESET);
   // scan look-back + both sorts' histograms, counters and look-back statuses, and the scalars
   // sc[0..7] + the frame's key total (contiguous): one zeroing kernel
   const size_t zero = radix ? (size_t)((unsigned char*)ctx->sort_tile.lookback - ctx->arena) +
