@@ -459,12 +459,15 @@ def run_isg(args):
         r.synchronize()
     if use_pipe:
         bufs = [[torch.empty_like(t) for t in targets] for _ in range(2)]
+        loss_host = torch.zeros(2, dtype=torch.float64).pin_memory()
+        step_losses = []
         graphs = []
         for b in range(2):
-            def step_b(bb=bufs[b]):
+            def step_b(bb=bufs[b], slot=loss_host[b:b + 1]):
                 for c, t in zip(cams, bb):
                     r.loss_backward_device(c, t.data_ptr(), opts, weight=1.0 / step_views)
                 r.adam_step(cfg)
+                r.step_loss_async(slot.data_ptr())  # the step's loss D2H, inside the graph
             for t, h in zip(bufs[b], pinned):
                 t.copy_(h)
             r.graph_begin()
@@ -497,7 +500,9 @@ def run_isg(args):
                     for t, h in zip(bufs[1 - b], pinned):
                         t.copy_(h, non_blocking=True)
                     ev_copy[1 - b].record(copy_stream)
-            r.last_step_loss()  # D2H of the step's loss (synchronises)
+            if i >= 1:  # step i-1's loss is on the host once its graph is done (step i queued)
+                ev_done[1 - b].synchronize()
+                step_losses.append(float(loss_host[1 - b]))
         elif train:
             for c, h in zip(cams, host_views):
                 r.loss_backward(c, h, opts, weight=1.0 / step_views)  # H2D target, D2H loss
@@ -516,6 +521,9 @@ def run_isg(args):
         else:
             r.render(cams[0], opts, out=host_out)  # D2H image into pinned memory
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    if use_pipe:
+        ev_done[(args.steps - 1) & 1].synchronize()
+        step_losses.append(float(loss_host[(args.steps - 1) & 1]))
     if use_rpipe:
         for e in ev_read:
             e.synchronize()  # the last frames' images are on the host
@@ -528,7 +536,7 @@ def run_isg(args):
         e2e_step = float(tt.item())
     e2e_value = (step_views if train else world) / (e2e_step / 1e3)
     h2d = sum(h.nbytes for h in host_views) if train else 0
-    d2h = 8 * len(host_views) if train else W * H * 3 * 4
+    d2h = (8 if use_pipe else 8 * len(host_views)) if train else W * H * 3 * 4
 
     st = r.stats()
     if rank != 0:
@@ -614,8 +622,12 @@ def run_isg(args):
         "e2e": {"value": e2e_value, "unit": "iters/s" if train else "frames/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_step,
+                **({"loss_first_last": [step_losses[0], step_losses[-1]],
+                    "losses_read": len(step_losses)} if use_pipe else {}),
                 "mode": ("cuda graph per step, next step's targets prefetched from pinned host "
-                         "memory on a copy stream, loss read back every step") if use_pipe else
+                         "memory on a copy stream; every step's loss copied D2H into pinned "
+                         "memory inside its graph and read by the host while the next step "
+                         "runs (all reads inside the timed region)") if use_pipe else
                         ("cuda graph per frame into a double-buffered device image, each image "
                          "copied to pinned host memory on a copy stream while the next renders")
                         if use_rpipe else

@@ -1010,6 +1010,14 @@ isg_status isg_last_step_loss(isg_ctx* ctx, double* loss_out) {
   return ISG_OK;
 }
 
+isg_status isg_step_loss_async(isg_ctx* ctx, double* host_dst) {
+  if (!ctx || !host_dst) return ISG_E_ARG;
+  cudaSetDevice(ctx->device);
+  ISG_CUDA(cudaMemcpyAsync(host_dst, ctx->loss + 2, sizeof(double), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  return ISG_OK;
+}
+
 isg_status isg_eval_loss(isg_ctx* ctx, const isg_camera* cam, const float bg[3], float t_min,
                          const float* target_dev, float weight, double* loss_out) {
   if (!ctx || !loss_out) return ISG_E_ARG;

@@ -92,6 +92,7 @@ def lib() -> C.CDLL:
         "isg_grads_device": ([P, C.POINTER(P)], C.c_int),
         "isg_adam_step": ([P, fp, F, F, F], C.c_int),
         "isg_last_step_loss": ([P, C.POINTER(C.c_double)], C.c_int),
+        "isg_step_loss_async": ([P, C.c_void_p], C.c_int),
         "isg_eval_loss": ([P, C.POINTER(CameraT), fp, F, P, F, C.POINTER(C.c_double)], C.c_int),
         "isg_snapshot": ([P], C.c_int),
         "isg_restore": ([P], C.c_int),
@@ -130,7 +131,7 @@ C_ABI_SYMBOLS = (
     "isg_set_stream", "isg_synchronize", "isg_get_stats", "isg_set_scene", "isg_set_scene_device",
     "isg_get_scene", "isg_render", "isg_render_device", "isg_loss_backward",
     "isg_loss_backward_device", "isg_read_loss", "isg_zero_grads", "isg_get_grads",
-    "isg_grads_device", "isg_adam_step", "isg_last_step_loss", "isg_eval_loss", "isg_snapshot",
+    "isg_grads_device", "isg_adam_step", "isg_last_step_loss", "isg_step_loss_async", "isg_eval_loss", "isg_snapshot",
     "isg_restore", "isg_set_loss", "isg_image_loss_device", "isg_adaptive_control",
     "isg_graph_begin", "isg_graph_end", "isg_graph_launch", "isg_graph_destroy", "isg_nccl_get_unique_id",
     "isg_nccl_init",
@@ -484,6 +485,11 @@ class Renderer:
         v = C.c_double()
         _check(self._h, lib().isg_last_step_loss(self._h, C.byref(v)))
         return v.value
+
+    def step_loss_async(self, host_ptr: int) -> None:
+        """Enqueue the last step's loss D2H into page-locked host memory at host_ptr (no sync;
+        capturable into a graph)."""
+        _check(self._h, lib().isg_step_loss_async(self._h, C.c_void_p(host_ptr)))
 
     # -- multi-GPU --------------------------------------------------------------------------
     @staticmethod

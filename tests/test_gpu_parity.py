@@ -502,3 +502,28 @@ def test_cuda_graph_with_nccl_single_rank():
     np.testing.assert_array_equal(out[0][0][0], out[1][0][0])
     np.testing.assert_array_equal(out[0][0][1], out[1][0][1])
     assert out[0][1] == out[1][1]
+
+
+def test_step_loss_async_in_graph_matches_sync_read():
+    """isg_step_loss_async captured in a step graph (the pipelined loop's D2H of each step's
+    loss) delivers the same value as the synchronous isg_last_step_loss."""
+    import torch
+    W, H = 128, 96
+    ms, co = isg.synth_scene(3000, W, H, seed=21)
+    tms, tco = isg.synth_scene(3000, W, H, seed=22)
+    cam = isg.Camera.synthetic(W, H)
+    target = torch.from_numpy(O.render32(tms, tco, cam)).cuda()
+    host = torch.zeros(1, dtype=torch.float64).pin_memory()
+    with isg.Renderer(0) as r:
+        r.set_scene(ms, co)
+        r.loss_backward(cam, target.cpu().numpy())  # sizes the buffers
+        r.zero_grads()
+        r.graph_begin()
+        r.loss_backward_device(cam, target.data_ptr())
+        r.adam_step(isg.AdamConfig())
+        r.step_loss_async(host.data_ptr())
+        g = r.graph_end()
+        for _ in range(3):
+            g.launch()
+            r.synchronize()
+            assert float(host[0]) == r.last_step_loss() > 0.0
