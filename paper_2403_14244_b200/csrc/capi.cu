@@ -415,12 +415,14 @@ isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out) {
   if (radix && (s = ensure_radix(ctx)) != ISG_OK) return s;
   cudaStream_t st = ctx->stream;
   const int64_t n = ctx->n;
+  // the tile sort uses ceil(tile bits / 8) passes: 2 up to 65536 tiles, 3 beyond
+  const int tile_passes = (bits_for(fp.n_tiles) + 7) / 8;
   {
   ISG_STAGE(ST_RESET);
   // scan look-back + both sorts' histograms, counters and look-back statuses, and the scalars
   // sc[0..7] + the frame's key total (contiguous): one zeroing kernel
   const size_t zero = radix ? (size_t)((unsigned char*)ctx->sort_tile.lookback - ctx->arena) +
-                                  isg::sort_lookback_bytes(ctx->key_cap, 2)
+                                  isg::sort_lookback_bytes(ctx->key_cap, tile_passes)
                             : ctx->arena_depth_end;
   isg::launch_zero2(ctx->arena, zero, ctx->sc, sizeof(uint32_t) * 8 + sizeof(unsigned long long),
                     st);
@@ -439,7 +441,6 @@ isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out) {
   ctx->launches++;
   }
   if (radix && n > 0) {
-    const int tile_passes = (bits_for(fp.n_tiles) + 7) / 8;
     {
     ISG_STAGE(ST_DEPTH_SORT);
     isg::SortOptions dopt;
