@@ -542,3 +542,44 @@ def test_three_pass_tile_sort_many_tiles():
             keys = check_bins(r, ms, co, cam)
         assert (keys >> 32).max() >= 65536  # tiles past the 16-bit boundary are populated
         assert np.abs(img - O.render32(ms, co, cam)).max() <= IMG_TOL
+
+
+@pytest.mark.parametrize("W,H", [(1, 1), (8, 8), (16, 16), (17, 1), (1, 33)])
+def test_degenerate_image_shapes(rend, W, H):
+    """One-tile and one-pixel-wide images (a 1-bit tile sort): bins, image and gradients."""
+    rng = np.random.default_rng(W * 100 + H)
+    ms, co, cam = random_scene(rng, 50, W, H, sigma2d=(0.3, 4.0))
+    rend.set_scene(ms, co)
+    img = rend.render(cam)
+    check_bins(rend, ms, co, cam)
+    assert np.abs(img - O.render32(ms, co, cam)).max() <= IMG_TOL
+    target = rng.uniform(0, 1, (H, W, 3)).astype(np.float32)
+    loss = rend.loss_backward(cam, target)
+    loss_ref, g_ref = O.loss_backward32(ms, co, cam, target)
+    assert abs(loss - loss_ref) <= 1e-6 * abs(loss_ref) + 1e-12
+    _grad_check(rend.grads(), g_ref)
+    rend.zero_grads()
+
+
+def test_all_splats_culled(rend):
+    """Every splat behind the near plane: no keys, background image, zero gradients, and the
+    Adam step leaves the (gradient-free) scene unchanged (up to the log-sigma / logit-opacity
+    round trip)."""
+    W, H = 96, 64
+    rng = np.random.default_rng(8)
+    ms, co, cam = random_scene(rng, 500, W, H)
+    ms[:, 2] = -np.abs(ms[:, 2])  # behind the camera
+    rend.set_scene(ms, co)
+    img = rend.render(cam, isg.RenderOptions(background=(0.1, 0.2, 0.3)))
+    keys, vals, ranges = rend.debug_bins()
+    assert len(keys) == 0 and np.all(ranges == 0)
+    assert np.array_equal(img, np.broadcast_to(np.float32([0.1, 0.2, 0.3]), img.shape))
+    target = rng.uniform(0, 1, (H, W, 3)).astype(np.float32)
+    rend.loss_backward(cam, target)
+    assert np.all(rend.grads() == 0)
+    rend.adam_step(isg.AdamConfig())
+    m2, c2 = rend.get_scene()
+    np.testing.assert_array_equal(m2[:, :3], ms[:, :3])
+    np.testing.assert_array_equal(c2[:, :3], co[:, :3])
+    np.testing.assert_allclose(m2[:, 3], ms[:, 3], rtol=1e-6)
+    np.testing.assert_allclose(c2[:, 3], co[:, 3], rtol=1e-5)
