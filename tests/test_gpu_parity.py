@@ -334,6 +334,27 @@ def test_full_size_c3_loss_backward():
     _grad_check(g, g_ref)
 
 
+def test_full_size_c5_bins_and_gradients():
+    """Config C5 (10M splats, 3840x2160, 33 M tile keys): bins bit-exact, then the L2 loss and
+    all 80 M gradients against the oracle (the target is the GPU render of a second scene: an
+    input to both sides, so it need not come from the oracle)."""
+    W, H, n = 3840, 2160, 10_000_000
+    ms, co = isg.synth_scene(n, W, H, seed=5)
+    tms, tco = isg.synth_scene(n, W, H, seed=6)
+    cam = isg.Camera.synthetic(W, H)
+    with isg.Renderer(0) as r:
+        r.set_scene(tms, tco)
+        target = r.render(cam)
+        r.set_scene(ms, co)
+        loss = r.loss_backward(cam, target)
+        g = r.grads()
+        keys = check_bins(r, ms, co, cam)
+        assert len(keys) > 30_000_000
+    loss_ref, g_ref = O.loss_backward32(ms, co, cam, target)
+    assert abs(loss - loss_ref) <= 1e-6 * abs(loss_ref)
+    _grad_check(g, g_ref)
+
+
 def test_binning_modes_bit_identical(rend):
     """Tile-bucket and onesweep-radix binning give identical lists, images and gradients."""
     W, H = 320, 200
