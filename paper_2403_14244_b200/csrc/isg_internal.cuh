@@ -3,8 +3,9 @@
 // Pipeline of one view (all on one stream, no host sync inside a frame):
 //   K1  k_preprocess      per splat: validate, project, 3-sigma radius, tile count, 32-B record
 //   binning (two interchangeable modes, identical output):
-//     radix (default)        onesweep depth sort -> k_scan_emit -> onesweep tile sort ->
-//                            k_ranges                                        (k_sort.cu)
+//     radix (default)        onesweep depth sort (histograms from K1) -> k_scan_emit (tile
+//                            histograms) -> onesweep tile sort whose last pass writes the
+//                            pairs and the ranges                            (k_sort.cu)
 //     tile-bucket            K2 k_tile_scan -> K3 k_fill -> K4 k_tile_sort   (k_bin.cu)
 //     output: per-tile ranges and, per list entry, (splat, gradient slot) in (depth, index)
 //     order; per splat, the list of its gradient slots.

@@ -4,16 +4,18 @@
 // test covers(ScreenIso) (:108-114).  Instead of every pixel visiting every splat
 // (O(W*H*N)), one CTA owns one tile and walks only that tile's depth-ordered list.
 //
-// Mapping: 128 threads per tile; warp w owns the 8x8 quarter-tile w, each 8-lane group one 4x4
-// sub-quarter and each lane a vertical pixel pair, so one shared-memory record feeds two pixels
-// that share dx.  Records are staged 128 at a time into shared memory with cp.async,
-// double-buffered (the next batch's copy is in flight while the current one is blended).
-// After each batch barrier every warp tests the staged splats' 3-sigma circles against its
-// quarter and then its four sub-quarters (conservative closest-point tests, exact rounding),
-// ballots, and compacts the relevant entry indices into four lists; the groups walk their own
-// lists in lockstep.  The 4x4 culling cuts the pixel-entry slots a circle does not cover
-// (a circle of the typical 6-px 3-sigma radius covers a 4x4 region far better than an 8x8).
-// Compositing is branch-free; the CTA stops once every pixel has transmittance <= t_min.
+// Mapping: 64 threads per tile (2 warps).  Each four-lane group owns one 4x4 sub-quarter and
+// each lane a 2x2 pixel quad, processed as two packed f32x2 pixel pairs (one row each), so one
+// shared-memory record feeds four pixels.  Records are staged 128 at a time into shared memory
+// with cp.async, double-buffered (the next batch's copy is in flight while the current one is
+// blended).  After each batch barrier every warp tests the staged splats' 3-sigma circles
+// against its eight sub-quarters (conservative closest-point tests sharing per-axis terms,
+// exact rounding), ballots, and compacts eight relevance lists; the groups walk their own
+// lists in lockstep, padded with a sentinel record to the warp's step count.  The 4x4 culling
+// cuts the pixel-entry slots a circle does not cover (a circle of the typical 6-px 3-sigma
+// radius covers a 4x4 region far better than an 8x8).  Compositing is branch-free; a
+// sub-quarter whose pixels all terminated walks nothing, and the CTA stops once every pixel
+// has transmittance <= t_min.
 //
 // The 3-sigma test is bit-identical to the FP32 oracle (explicit _rn arithmetic); exp uses
 // ex2.approx on a per-splat precomputed -log2(e)/sigma2d^2.
