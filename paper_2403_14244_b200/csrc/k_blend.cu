@@ -149,10 +149,13 @@ __global__ void ISG_FWD_BOUNDS k_blend_fwd(
     // share their per-axis terms (rounded squares of the distances to the 4 columns and 2
     // rows) and add one pair exactly as dist2_rn would at the sub-quarter's closest pixel
     // centre (bit-identical decisions; a conservative superset of the per-pixel test).
-    const int cnt = min(kBatch, n - b);
+    // a warp whose 128 pixels all terminated skips the tests (it still joins the barriers)
+    const uint32_t alive = __ballot_sync(0xffffffffu, live);
+    const int cnt = alive ? min(kBatch, n - b) : 0;
     int base[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
     for (int wd = 0; wd < kWords; ++wd) {
+      if (32 * wd >= cnt) break;  // warp-uniform
       const int j = 32 * wd + lane;
       const bool in = j < cnt;
       const float4 g = cur.geo[in ? j : 0];
@@ -177,7 +180,6 @@ __global__ void ISG_FWD_BOUNDS k_blend_fwd(
       }
     }
     // a sub-quarter whose 16 pixels have all terminated walks nothing
-    const uint32_t alive = __ballot_sync(0xffffffffu, live);
     int steps = 0, my_cnt = 0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
