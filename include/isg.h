@@ -210,8 +210,9 @@ isg_status isg_nccl_detach(isg_ctx* ctx);
 
 /* ---- parity hooks ---------------------------------------------------------------------- */
 /* After the last render/backward: sorted (tile<<32 | float_bits(depth)) keys, the splat
- * index of each key, and per-tile [start,end) ranges (n_tiles x 2).  Any output pointer may
- * be NULL; *n_keys always receives the key count. */
+ * index of each key, and per-tile [start,end) ranges (n_tiles x 2) in the oracle's form (an
+ * empty tile gets (s, s), s = the position it would occupy).  Any output pointer may be NULL;
+ * *n_keys always receives the key count. */
 isg_status isg_debug_bins(isg_ctx* ctx, uint64_t* keys, uint32_t* vals, int64_t* n_keys,
                           uint32_t* ranges);
 /* Per-pixel forward state of the last render: transmittance before the last contributor
@@ -227,7 +228,9 @@ isg_status isg_debug_pixel_state(isg_ctx* ctx, float* t_last, uint32_t* n_proc);
 #define ISG_BINNING_RADIX 1
 isg_status isg_set_binning(isg_ctx* ctx, int mode);
 
-/* ---- stage timing (CUDA events on the context stream; for bench.py's roofline) ---------- */
+/* ---- stage timing (CUDA events on the context stream; for bench.py's roofline) ----------
+ * While enabled, kernels are launched without programmatic dependent launch (process-wide),
+ * so that the events between them time each kernel alone. */
 isg_status isg_profile_enable(isg_ctx* ctx, int on);
 int isg_profile_num_stages(void);
 const char* isg_profile_stage_name(int stage);
