@@ -73,6 +73,7 @@ struct isg_ctx {
   uint32_t* tval[2] = {nullptr, nullptr};   // radix mode: emission indices
   uint32_t* emit_gid = nullptr;             // radix mode: splat of emission index e
   bool radix_alloc = false;
+  isg::AdaptScratch* adapt = nullptr;       // adaptive control's persistent scratch
 
   // sort / scan scratch
   isg::SortScratch sort{};  // adaptive control (zeroed per call)
@@ -708,6 +709,7 @@ void isg_destroy(isg_ctx* ctx) {
                  ctx->adam_state};
   for (void* p : dev)
     if (p) cudaFree(p);
+  isg::adapt_scratch_free(ctx->adapt);
   if (ctx->h_sc) cudaFreeHost(ctx->h_sc);
   if (ctx->h_total) cudaFreeHost(ctx->h_total);
   if (ctx->h_loss) cudaFreeHost(ctx->h_loss);
@@ -1133,17 +1135,13 @@ isg_status isg_adaptive_control(isg_ctx* ctx, const isg_adapt_params* prm, uint6
     if (s != ISG_OK) return s;
   }
   if ((s = ensure_sort_scratch(ctx, std::max(ctx->key_cap, ctx->n_alloc))) != ISG_OK) return s;
-  float4 *ms_tmp = nullptr, *co_tmp = nullptr;
-  ISG_CUDA(cudaMalloc(&ms_tmp, sizeof(float4) * ctx->n_alloc));
-  ISG_CUDA(cudaMalloc(&co_tmp, sizeof(float4) * ctx->n_alloc));
   isg::AdaptParamsDev p{prm->prune_threshold, prm->merge_distance_factor, prm->merge_color_tol,
                         prm->split_sigma_max, cap};
   isg::AdaptCounts c{};
-  const cudaError_t e = isg::adaptive_control(ctx->ms, ctx->co, n, p, seed, round, ctx->sort,
-                                              ctx->depth, ctx->order, ms_tmp, co_tmp, &c,
+  // (ctx->ms / ctx->co may come back swapped with the persistent scratch's temporaries)
+  const cudaError_t e = isg::adaptive_control(ctx->ms, ctx->co, n, ctx->n_alloc, p, seed, round,
+                                              ctx->sort, ctx->depth, ctx->order, ctx->adapt, &c,
                                               ctx->stream, &ctx->launches);
-  cudaFree(ms_tmp);  // the buffers not in use after the (possible) swaps
-  cudaFree(co_tmp);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "adaptive_control");
   // the optimizer restarts on the new set (the reference clears its momentum, optimize.cpp:344)
   ctx->n = c.n_after;

@@ -208,13 +208,18 @@ struct AdaptParamsDev {
 struct AdaptCounts {
   int64_t n_before, n_pruned, n_merged, n_split, n_after;
 };
-// Prune -> merge -> split of the n splats in (ms, co), in place; ms/co may be swapped with
-// ms_tmp/co_tmp (all four hold >= max(n, max_particles) records).  keys/vals: two ping-pong
-// pairs of >= n words; sort: radix scratch for >= n items.  Synchronises the stream.
-cudaError_t adaptive_control(float4*& ms, float4*& co, int64_t n, const AdaptParamsDev& p,
-                             uint64_t seed, uint64_t round, SortScratch& sort, uint32_t* keys[2],
-                             uint32_t* vals[2], float4* ms_tmp, float4* co_tmp,
-                             AdaptCounts* counts, cudaStream_t st, int64_t* launches);
+// Persistent device / pinned scratch of adaptive_control (grown on demand, reused across calls:
+// per-call allocations dominated a pass).  Owned by the context; free with adapt_scratch_free.
+struct AdaptScratch;
+void adapt_scratch_free(AdaptScratch* s);
+// Prune -> merge -> split of the n splats in (ms, co), in place; ms/co may be swapped with the
+// scratch's temporaries (all hold >= n_alloc >= max(n, max_particles) records).  keys/vals:
+// two ping-pong pairs of >= n words; sort: radix scratch for >= n items.  Synchronises.
+cudaError_t adaptive_control(float4*& ms, float4*& co, int64_t n, int64_t n_alloc,
+                             const AdaptParamsDev& p, uint64_t seed, uint64_t round,
+                             SortScratch& sort, uint32_t* keys[2], uint32_t* vals[2],
+                             AdaptScratch*& scratch, AdaptCounts* counts, cudaStream_t st,
+                             int64_t* launches);
 
 // ---- parity hook -------------------------------------------------------------------------
 void launch_debug_keys(const uint2* ranges, const uint2* sorted, const float4* ms,

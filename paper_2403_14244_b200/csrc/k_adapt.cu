@@ -428,54 +428,88 @@ static cudaError_t compact_positions(const uint8_t* flag, int64_t n, bool revers
   return cudaGetLastError();
 }
 
-cudaError_t adaptive_control(float4*& ms, float4*& co, int64_t n, const AdaptParamsDev& p,
-                             uint64_t seed, uint64_t round, SortScratch& sort, uint32_t* keys[2],
-                             uint32_t* vals[2], float4* ms_tmp, float4* co_tmp,
-                             AdaptCounts* counts, cudaStream_t st, int64_t* launches) {
+struct AdaptScratch {
+  int64_t n_cap = 0, alloc_cap = 0, edge_cap = 0;
+  uint32_t t_cap = 0;
+  uint8_t* flag = nullptr;
+  uint32_t *pos = nullptr, *scratch = nullptr, *partner = nullptr, *tk = nullptr, *tv = nullptr;
+  unsigned long long *best = nullptr, *bestd = nullptr, *bestij = nullptr;
+  unsigned int* acc = nullptr;
+  void* edges = nullptr;  // Edge[edge_cap]
+  float4 *ms_tmp = nullptr, *co_tmp = nullptr;
+  uint32_t* h = nullptr;  // pinned
+};
+
+void adapt_scratch_free(AdaptScratch* s) {
+  if (!s) return;
+  cudaFree(s->flag);
+  cudaFree(s->pos);
+  cudaFree(s->scratch);
+  cudaFree(s->partner);
+  cudaFree(s->tk);
+  cudaFree(s->tv);
+  cudaFree(s->best);
+  cudaFree(s->bestd);
+  cudaFree(s->bestij);
+  cudaFree(s->acc);
+  cudaFree(s->edges);
+  cudaFree(s->ms_tmp);
+  cudaFree(s->co_tmp);
+  cudaFreeHost(s->h);
+  delete s;
+}
+
+template <class T>
+static cudaError_t regrow(T*& p, size_t count) {
+  cudaFree(p);
+  p = nullptr;
+  return cudaMalloc(&p, count * sizeof(T));
+}
+
+cudaError_t adaptive_control(float4*& ms, float4*& co, int64_t n, int64_t n_alloc,
+                             const AdaptParamsDev& p, uint64_t seed, uint64_t round,
+                             SortScratch& sort, uint32_t* keys[2], uint32_t* vals[2],
+                             AdaptScratch*& S, AdaptCounts* counts, cudaStream_t st,
+                             int64_t* launches) {
   cudaError_t err = cudaSuccess;
   counts->n_before = n;
   counts->n_pruned = counts->n_merged = counts->n_split = 0;
   counts->n_after = n;
   if (n == 0) return cudaSuccess;
-  // device scratch for this call
-  uint8_t* flag = nullptr;
-  uint32_t *pos = nullptr, *scratch = nullptr, *partner = nullptr, *tk = nullptr, *tv = nullptr;
-  unsigned long long *best = nullptr, *bestd = nullptr, *bestij = nullptr;
-  unsigned int* acc = nullptr;
-  Edge* edges = nullptr;
-  uint32_t* h = nullptr;
-  const int64_t nb = (n + kT - 1) / kT;
-  auto cleanup = [&]() {
-    cudaFree(flag);
-    cudaFree(pos);
-    cudaFree(scratch);
-    cudaFree(partner);
-    cudaFree(tk);
-    cudaFree(tv);
-    cudaFree(best);
-    cudaFree(bestd);
-    cudaFree(bestij);
-    cudaFree(acc);
-    cudaFree(edges);
-    cudaFreeHost(h);
-  };
-#define ADAPT_CHECK(x)       \
-  do {                       \
-    err = (x);               \
+#define ADAPT_CHECK(x)        \
+  do {                        \
+    err = (x);                \
     if (err != cudaSuccess) { \
-      cleanup();             \
-      return err;            \
-    }                        \
+      return err;             \
+    }                         \
   } while (0)
-  ADAPT_CHECK(cudaMallocHost(&h, 16 * sizeof(uint32_t)));
-  ADAPT_CHECK(cudaMalloc(&flag, n));
-  ADAPT_CHECK(cudaMalloc(&pos, n * sizeof(uint32_t)));
-  ADAPT_CHECK(cudaMalloc(&scratch, (nb + 8) * sizeof(uint32_t)));
-  ADAPT_CHECK(cudaMalloc(&partner, n * sizeof(uint32_t)));
-  ADAPT_CHECK(cudaMalloc(&best, 4 * sizeof(unsigned long long)));
-  ADAPT_CHECK(cudaMalloc(&bestd, n * sizeof(unsigned long long)));
-  ADAPT_CHECK(cudaMalloc(&bestij, n * sizeof(unsigned long long)));
-  ADAPT_CHECK(cudaMalloc(&acc, 4 * sizeof(unsigned int)));
+  if (!S) S = new AdaptScratch();
+  const int64_t nb = (n + kT - 1) / kT;
+  if (!S->h) ADAPT_CHECK(cudaMallocHost(&S->h, 16 * sizeof(uint32_t)));
+  if (!S->best) {
+    ADAPT_CHECK(cudaMalloc(&S->best, 4 * sizeof(unsigned long long)));
+    ADAPT_CHECK(cudaMalloc(&S->acc, 4 * sizeof(unsigned int)));
+  }
+  if (n > S->n_cap) {
+    ADAPT_CHECK(regrow(S->flag, n));
+    ADAPT_CHECK(regrow(S->pos, n));
+    ADAPT_CHECK(regrow(S->scratch, nb + 8));
+    ADAPT_CHECK(regrow(S->partner, n));
+    ADAPT_CHECK(regrow(S->bestd, n));
+    ADAPT_CHECK(regrow(S->bestij, n));
+    S->n_cap = n;
+  }
+  if (n_alloc > S->alloc_cap) {
+    ADAPT_CHECK(regrow(S->ms_tmp, n_alloc));
+    ADAPT_CHECK(regrow(S->co_tmp, n_alloc));
+    S->alloc_cap = n_alloc;
+  }
+  uint8_t* flag = S->flag;
+  uint32_t *pos = S->pos, *scratch = S->scratch, *partner = S->partner;
+  unsigned long long *best = S->best, *bestd = S->bestd, *bestij = S->bestij;
+  unsigned int* acc = S->acc;
+  uint32_t* h = S->h;
+  float4 *ms_tmp = S->ms_tmp, *co_tmp = S->co_tmp;
   const int g = grid_for(n);
 
   // ---- prune --------------------------------------------------------------------------------
@@ -490,6 +524,8 @@ cudaError_t adaptive_control(float4*& ms, float4*& co, int64_t n, const AdaptPar
   k_gather_scene<<<g, kT, 0, st>>>(ms, co, n, pos, ms_tmp, co_tmp);
   std::swap(ms, ms_tmp);
   std::swap(co, co_tmp);
+  S->ms_tmp = ms_tmp;  // the scene's previous buffers become the scratch
+  S->co_tmp = co_tmp;
   counts->n_pruned = n - m;
   *launches += 6;
 
@@ -507,15 +543,24 @@ cudaError_t adaptive_control(float4*& ms, float4*& co, int64_t n, const AdaptPar
   const int sb = radix_sort_pairs(keys, vals, true, n_dev, m, 32, sort, st, launches);
   uint32_t tsize = 1;
   while (tsize < 2 * (uint64_t)m) tsize <<= 1;
-  ADAPT_CHECK(cudaMalloc(&tk, tsize * sizeof(uint32_t)));
-  ADAPT_CHECK(cudaMalloc(&tv, tsize * sizeof(uint32_t)));
+  if (tsize > S->t_cap) {
+    ADAPT_CHECK(regrow(S->tk, tsize));
+    ADAPT_CHECK(regrow(S->tv, tsize));
+    S->t_cap = tsize;
+  }
+  uint32_t *tk = S->tk, *tv = S->tv;
   cudaMemsetAsync(tk, 0xFF, tsize * sizeof(uint32_t), st);
   k_cell_table<<<gm, kT, 0, st>>>(keys[sb], m, tk, tv, tsize - 1);
-  int64_t edge_cap = std::max<int64_t>(4 * m, 1024);
+  int64_t edge_cap = std::max<int64_t>(S->edge_cap, std::max<int64_t>(4 * m, 1024));
   int64_t ne = 0;
   unsigned long long* n_edges = best + 2;
+  Edge* edges = static_cast<Edge*>(S->edges);
   for (int attempt = 0; attempt < 4; ++attempt) {
-    ADAPT_CHECK(cudaMalloc(&edges, edge_cap * sizeof(Edge)));
+    if (edge_cap > S->edge_cap) {
+      ADAPT_CHECK(regrow(edges, edge_cap));
+      S->edges = edges;
+      S->edge_cap = edge_cap;
+    }
     cudaMemsetAsync(n_edges, 0, sizeof(unsigned long long), st);
     k_find_pairs<<<gm, kT, 0, st>>>(ms, co, m, p.merge_distance_factor, p.merge_color_tol, smin,
                                     lmask, keys[sb], vals[sb], tk, tv, tsize - 1, edges, edge_cap,
@@ -526,8 +571,6 @@ cudaError_t adaptive_control(float4*& ms, float4*& co, int64_t n, const AdaptPar
     ADAPT_CHECK(cudaGetLastError());
     ne = (int64_t)ne_h;
     if (ne <= edge_cap) break;
-    cudaFree(edges);
-    edges = nullptr;
     edge_cap = ne + ne / 4 + 1024;
   }
   *launches += 5;
@@ -561,6 +604,8 @@ cudaError_t adaptive_control(float4*& ms, float4*& co, int64_t n, const AdaptPar
   k_gather_scene<<<gm, kT, 0, st>>>(ms, co, m, pos, ms_tmp, co_tmp);
   std::swap(ms, ms_tmp);
   std::swap(co, co_tmp);
+  S->ms_tmp = ms_tmp;
+  S->co_tmp = co_tmp;
   counts->n_merged = m - c;
   *launches += 5;
 
@@ -591,7 +636,6 @@ cudaError_t adaptive_control(float4*& ms, float4*& co, int64_t n, const AdaptPar
   ADAPT_CHECK(cudaStreamSynchronize(st));
   ADAPT_CHECK(cudaGetLastError());
   counts->n_after = count;
-  cleanup();
 #undef ADAPT_CHECK
   return cudaSuccess;
 }
