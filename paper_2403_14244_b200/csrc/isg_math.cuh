@@ -46,6 +46,17 @@ __device__ __forceinline__ float dist2_rn(float dx, float dy) {
   return __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
 }
 
+// One axis of tile_hit: the rounded squared distance from c (u or v) to the pixel-centre span of
+// tile t along an axis of lim pixels.  tile_hit == !(axis_d2(u, tx, W) + axis_d2(v, ty, H) >
+// r2max) with the sum rounded once, bit for bit, so a row's term can be hoisted.
+__device__ __forceinline__ float axis_d2(float c, int t, int lim) {
+  const float lo = (float)(t * kTile) + 0.5f;
+  const float hi = (float)(min(t * kTile + kTile, lim) - 1) + 0.5f;
+  const float q = c < lo ? lo : (c > hi ? hi : c);
+  const float d = __fsub_rn(q, c);
+  return __fmul_rn(d, d);
+}
+
 // Exact tile test (or32_tile_hit).
 __device__ __forceinline__ bool tile_hit(float u, float v, float r2max, int tx, int ty, int W,
                                          int H) {

@@ -60,13 +60,18 @@ __global__ void __launch_bounds__(256) k_preprocess(const float4* __restrict__ m
           const int bw = x1 - x0 + 1;
           const bool small = bw * (y1 - y0 + 1) <= 32 && bw < 256 && x0 < 4096 && y0 < 4096;
           uint32_t mask = 0;
-          for (int ty = y0; ty <= y1; ++ty)
-            for (int tx = x0; tx <= x1; ++tx) {
-              if (!tile_hit(p.u, p.v, p.r2max, tx, ty, fp.cam.width, fp.cam.height)) continue;
-              if (small) mask |= 1u << ((ty - y0) * bw + (tx - x0));
+          // tile_hit, separably: the row's y term once per row (bit-identical decisions)
+          uint32_t bit = 1u;
+          for (int ty = y0; ty <= y1; ++ty) {
+            const float ay = axis_d2(p.v, ty, fp.cam.height);
+            for (int tx = x0; tx <= x1; ++tx, bit <<= 1) {
+              if (__fadd_rn(axis_d2(p.u, tx, fp.cam.width), ay) > p.r2max) continue;
+              mask |= bit;  // (only meaningful when small: <= 32 tiles)
               ++count;
               if (tile_cnt) atomicAdd(&tile_cnt[ty * fp.tiles_x + tx], 1u);
             }
+          }
+          if (!small) mask = 0;
           // emission kernels iterate the hit bits instead of re-projecting (bw == 0: re-project)
           if (small) box = make_uint2((uint32_t)x0 | ((uint32_t)y0 << 12) | ((uint32_t)bw << 24), mask);
         }
