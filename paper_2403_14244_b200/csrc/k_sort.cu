@@ -284,7 +284,10 @@ constexpr int kScanItems = ISG_SCAN_ITEMS;
 constexpr int kScanTileItems = kScanThreads * kScanItems;
 constexpr int kEmitWindow = 4096;  // staged keys per window (32 KB of shared memory)
 
-__global__ void __launch_bounds__(kScanThreads) k_scan_emit(
+#ifndef ISG_SCAN_MINB
+#define ISG_SCAN_MINB 3
+#endif
+__global__ void __launch_bounds__(kScanThreads, ISG_SCAN_MINB) k_scan_emit(
     const uint32_t* __restrict__ order, const uint32_t* __restrict__ ntiles,
     const uint2* __restrict__ tilebox, const float4* __restrict__ ms, int64_t n, FrameParams fp,
     uint32_t* __restrict__ slot_off, uint32_t* __restrict__ tile_keys,
@@ -325,7 +328,10 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(
     sum += c[j];
   }
   uint32_t tot;
-  uint32_t texcl = block_excl_scan_256(sum, s_warp, tot);
+  const uint32_t t_begin = block_excl_scan_256(sum, s_warp, tot);
+  const uint32_t t_end = t_begin + sum;  // this thread's range, CTA-relative
+  // warp 0 runs the decoupled look-back for the CTA's global offset while the other warps
+  // already stage the first window (staging needs only CTA-relative positions)
   if (tid < 32) {
     const unsigned long long excl = lookback_warp(lookback, tile, tot);
     if (tid == 0) {
@@ -337,19 +343,20 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(
       }
     }
   }
-  __syncthreads();
+  unsigned long long cta0 = 0;
+#define ISG_WRITE_SLOT_OFFSETS()                                                   \
+  do {                                                                             \
+    cta0 = s_excl;                                                                 \
+    uint32_t pos_ = t_begin;                                                       \
+    _Pragma("unroll") for (int j = 0; j < kScanItems; ++j) {                       \
+      if (r0 + j < n) slot_off[g[j]] = (uint32_t)min(cta0 + pos_, 0xFFFFFFFFull); \
+      pos_ += c[j];                                                                \
+    }                                                                              \
+  } while (0)
   // Emission.  The CTA's keys occupy one contiguous range [s_excl, s_excl + tot) of the
   // output, so they are staged in shared memory window by window and written back coalesced
   // (per-thread emission straight to global memory scatters every store across 32 lines).
   // An item straddling a window boundary is enumerated again in the next window.
-  const unsigned long long cta0 = s_excl;
-#pragma unroll
-  for (int j = 0; j < kScanItems; ++j) {
-    if (r0 + j < n) slot_off[g[j]] = (uint32_t)min(cta0 + texcl, 0xFFFFFFFFull);
-    texcl += c[j];
-  }
-  // texcl is now the end of this thread's range (CTA-relative); its start is end - sum
-  const uint32_t t_end = texcl, t_begin = texcl - sum;
   for (uint32_t w = 0; w < tot; w += kEmitWindow) {
     const uint32_t wend = w + kEmitWindow;
     if (t_begin < wend && t_end > w) {
@@ -371,7 +378,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(
         });
       }
     }
-    __syncthreads();
+    __syncthreads();  // window staged (and, the first time, s_excl published)
+    if (w == 0) ISG_WRITE_SLOT_OFFSETS();
     const uint32_t cnt = min(tot - w, (uint32_t)kEmitWindow);
     const unsigned long long o0 = cta0 + w;
     for (uint32_t i0 = 0; i0 < cnt; i0 += kScanThreads) {  // warp-uniform trip count
@@ -386,6 +394,11 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(
     }
     __syncthreads();
   }
+  if (tot == 0) {  // (CTA-uniform) no keys: the offsets still need s_excl
+    __syncthreads();
+    ISG_WRITE_SLOT_OFFSETS();
+  }
+#undef ISG_WRITE_SLOT_OFFSETS
   hist_publish(sh, tile_passes, tile_hist, tile_hist_done);
 }
 
