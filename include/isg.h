@@ -194,7 +194,10 @@ isg_status isg_adaptive_control(isg_ctx* ctx, const isg_adapt_params* params, ui
  * entry points return ISG_E_STATE while capturing.  The Adam step counter lives on the device,
  * so replays apply the correct bias corrections; the learning rates, cameras and device
  * pointers are the captured ones.  A replayed frame that overflows the key capacity is skipped
- * and reported by the next synchronising call (re-capture after it grows the buffers). */
+ * and reported by the next synchronising call (re-capture after it grows the buffers).
+ * isg_graph_launch returns ISG_E_STATE for a graph captured before any device buffer it may
+ * use was reallocated (larger scene, key capacity or image, adaptive control); isg_graph_end
+ * returns it when a buffer grew inside the capture. */
 typedef struct isg_graph isg_graph;
 isg_status isg_graph_begin(isg_ctx* ctx);
 isg_status isg_graph_end(isg_ctx* ctx, isg_graph** out);

@@ -73,6 +73,7 @@ struct isg_ctx {
   uint32_t* tval[2] = {nullptr, nullptr};   // radix mode: emission indices
   uint32_t* emit_gid = nullptr;             // radix mode: splat of emission index e
   bool radix_alloc = false;
+  uint64_t buf_gen = 0;                     // bumped whenever a device buffer is reallocated
   isg::AdaptScratch* adapt = nullptr;       // adaptive control's persistent scratch
 
   // sort / scan scratch
@@ -140,6 +141,7 @@ struct isg_ctx {
   // CUDA-graph capture of the context stream (isg_graph_*)
   bool capturing = false;
   int64_t capture_launches0 = 0;
+  uint64_t capture_gen0 = 0;
 
   // profiling
   bool prof = false;
@@ -215,7 +217,10 @@ isg_status cuda_fail(isg_ctx* c, cudaError_t e, const char* where) {
   } while (0)
 
 template <class T>
-cudaError_t realloc_dev(T** p, size_t count) {
+cudaError_t realloc_dev(isg_ctx* ctx, T** p, size_t count, bool graph_visible = true) {
+  // captured graphs hold the old pointers (isg_graph_launch checks the generation); buffers
+  // no graph-captured kernel touches (the snapshot) pass graph_visible = false
+  if (graph_visible) ctx->buf_gen++;
   if (*p) cudaFree(*p);
   *p = nullptr;
   if (count == 0) count = 1;
@@ -231,18 +236,18 @@ int bits_for(int64_t v) {  // bits needed to represent values in [0, v)
 isg_status ensure_scene(isg_ctx* ctx, int64_t n) {
   if (n <= ctx->n_alloc) return ISG_OK;
   const int64_t a = std::max<int64_t>(n, 1);
-  ISG_CUDA(realloc_dev(&ctx->ms, a));
-  ISG_CUDA(realloc_dev(&ctx->co, a));
-  ISG_CUDA(realloc_dev(&ctx->m, 2 * a));
-  ISG_CUDA(realloc_dev(&ctx->v, 2 * a));
-  ISG_CUDA(realloc_dev(&ctx->rec, a));
-  ISG_CUDA(realloc_dev(&ctx->ntiles, a));
-  ISG_CUDA(realloc_dev(&ctx->slot_off, a));
-  ISG_CUDA(realloc_dev(&ctx->grad3d, 2 * a));
-  ISG_CUDA(realloc_dev(&ctx->tilebox, a));
+  ISG_CUDA(realloc_dev(ctx, &ctx->ms, a));
+  ISG_CUDA(realloc_dev(ctx, &ctx->co, a));
+  ISG_CUDA(realloc_dev(ctx, &ctx->m, 2 * a));
+  ISG_CUDA(realloc_dev(ctx, &ctx->v, 2 * a));
+  ISG_CUDA(realloc_dev(ctx, &ctx->rec, a));
+  ISG_CUDA(realloc_dev(ctx, &ctx->ntiles, a));
+  ISG_CUDA(realloc_dev(ctx, &ctx->slot_off, a));
+  ISG_CUDA(realloc_dev(ctx, &ctx->grad3d, 2 * a));
+  ISG_CUDA(realloc_dev(ctx, &ctx->tilebox, a));
   for (int i = 0; i < 2; ++i) {
-    ISG_CUDA(realloc_dev(&ctx->depth[i], a));
-    ISG_CUDA(realloc_dev(&ctx->order[i], a));
+    ISG_CUDA(realloc_dev(ctx, &ctx->depth[i], a));
+    ISG_CUDA(realloc_dev(ctx, &ctx->order[i], a));
   }
   ctx->n_alloc = a;
   return ISG_OK;
@@ -261,6 +266,7 @@ isg_status ensure_arena(isg_ctx* ctx) {
   const size_t bytes = scan + 2 * hist + lb_depth + lb_tile;
   if (ctx->arena) cudaFree(ctx->arena);
   ctx->arena = nullptr;
+  ctx->buf_gen++;
   ISG_CUDA(cudaMalloc(&ctx->arena, bytes));
   ISG_CUDA(cudaMemset(ctx->arena, 0, bytes));
   ctx->arena_bytes = bytes;
@@ -284,9 +290,9 @@ isg_status ensure_sort_scratch(isg_ctx* ctx, int64_t cap) {
   const int64_t tiles = isg::sort_tiles_for(cap);
   if (tiles <= ctx->sort_tiles_alloc && ctx->sort.hist) return ISG_OK;
   const int64_t t = std::max<int64_t>(tiles, 1);
-  ISG_CUDA(realloc_dev(&ctx->sort.hist, isg::kMaxPasses * 256));
-  ISG_CUDA(realloc_dev(&ctx->sort.counters, isg::kMaxPasses + 1));
-  ISG_CUDA(realloc_dev(&ctx->sort.lookback, (size_t)isg::kMaxPasses * 256 * t));
+  ISG_CUDA(realloc_dev(ctx, &ctx->sort.hist, isg::kMaxPasses * 256));
+  ISG_CUDA(realloc_dev(ctx, &ctx->sort.counters, isg::kMaxPasses + 1));
+  ISG_CUDA(realloc_dev(ctx, &ctx->sort.lookback, (size_t)isg::kMaxPasses * 256 * t));
   ctx->sort.max_tiles = t;
   ctx->sort_tiles_alloc = t;
   return ISG_OK;
@@ -294,16 +300,16 @@ isg_status ensure_sort_scratch(isg_ctx* ctx, int64_t cap) {
 
 isg_status ensure_keys(isg_ctx* ctx, int64_t cap) {
   if (cap <= ctx->key_cap) return ISG_OK;
-  ISG_CUDA(realloc_dev(&ctx->sorted, cap));
-  ISG_CUDA(realloc_dev(&ctx->partial, 2 * cap));
-  ISG_CUDA(realloc_dev(&ctx->bucket, cap));
-  ISG_CUDA(realloc_dev(&ctx->slot_of, cap));
+  ISG_CUDA(realloc_dev(ctx, &ctx->sorted, cap));
+  ISG_CUDA(realloc_dev(ctx, &ctx->partial, 2 * cap));
+  ISG_CUDA(realloc_dev(ctx, &ctx->bucket, cap));
+  ISG_CUDA(realloc_dev(ctx, &ctx->slot_of, cap));
   if (ctx->radix_alloc) {
     for (int i = 0; i < 2; ++i) {
-      ISG_CUDA(realloc_dev(&ctx->tkey[i], cap));
-      ISG_CUDA(realloc_dev(&ctx->tval[i], cap));
+      ISG_CUDA(realloc_dev(ctx, &ctx->tkey[i], cap));
+      ISG_CUDA(realloc_dev(ctx, &ctx->tval[i], cap));
     }
-    ISG_CUDA(realloc_dev(&ctx->emit_gid, cap));
+    ISG_CUDA(realloc_dev(ctx, &ctx->emit_gid, cap));
   }
   ctx->key_cap = cap;
   return ISG_OK;
@@ -316,10 +322,10 @@ isg_status ensure_radix(isg_ctx* ctx) {
   const int64_t cap = ctx->key_cap;
   if (cap > 0) {
     for (int i = 0; i < 2; ++i) {
-      ISG_CUDA(realloc_dev(&ctx->tkey[i], cap));
-      ISG_CUDA(realloc_dev(&ctx->tval[i], cap));
+      ISG_CUDA(realloc_dev(ctx, &ctx->tkey[i], cap));
+      ISG_CUDA(realloc_dev(ctx, &ctx->tval[i], cap));
     }
-    ISG_CUDA(realloc_dev(&ctx->emit_gid, cap));
+    ISG_CUDA(realloc_dev(ctx, &ctx->emit_gid, cap));
   }
   return ISG_OK;
 }
@@ -329,17 +335,17 @@ isg_status ensure_pixels(isg_ctx* ctx, int W, int H) {
   const int64_t tiles =
       (int64_t)((W + isg::kTile - 1) / isg::kTile) * ((H + isg::kTile - 1) / isg::kTile);
   if (pix > ctx->pix_alloc) {
-    ISG_CUDA(realloc_dev(&ctx->img, 3 * pix));
-    ISG_CUDA(realloc_dev(&ctx->target, 3 * pix));
-    ISG_CUDA(realloc_dev(&ctx->t_last, pix));
-    ISG_CUDA(realloc_dev(&ctx->n_proc, pix));
+    ISG_CUDA(realloc_dev(ctx, &ctx->img, 3 * pix));
+    ISG_CUDA(realloc_dev(ctx, &ctx->target, 3 * pix));
+    ISG_CUDA(realloc_dev(ctx, &ctx->t_last, pix));
+    ISG_CUDA(realloc_dev(ctx, &ctx->n_proc, pix));
     ctx->pix_alloc = pix;
   }
   if (tiles > ctx->tiles_alloc) {
-    ISG_CUDA(realloc_dev(&ctx->ranges, tiles));
-    ISG_CUDA(realloc_dev(&ctx->tile_cnt, tiles));
-    ISG_CUDA(realloc_dev(&ctx->cursor, tiles));
-    ISG_CUDA(realloc_dev(&ctx->tile_loss, tiles));
+    ISG_CUDA(realloc_dev(ctx, &ctx->ranges, tiles));
+    ISG_CUDA(realloc_dev(ctx, &ctx->tile_cnt, tiles));
+    ISG_CUDA(realloc_dev(ctx, &ctx->cursor, tiles));
+    ISG_CUDA(realloc_dev(ctx, &ctx->tile_loss, tiles));
     ctx->tiles_alloc = tiles;
   }
   return ISG_OK;
@@ -558,13 +564,13 @@ isg_status check_frame(isg_ctx* ctx, bool* overflow, bool with_loss = false) {
 isg_status ensure_image_loss(isg_ctx* ctx, int W, int H) {
   const int64_t pix = (int64_t)W * H;
   if (pix > ctx->ssim_pix_alloc) {
-    ISG_CUDA(realloc_dev(&ctx->coef, 9 * pix));
-    ISG_CUDA(realloc_dev(&ctx->dldc, 3 * pix));
+    ISG_CUDA(realloc_dev(ctx, &ctx->coef, 9 * pix));
+    ISG_CUDA(realloc_dev(ctx, &ctx->dldc, 3 * pix));
     ctx->ssim_pix_alloc = pix;
   }
   const int64_t parts = isg::ssim_part_count(W, H);
   if (parts > ctx->ssim_part_alloc) {
-    ISG_CUDA(realloc_dev(&ctx->ssim_part, parts));
+    ISG_CUDA(realloc_dev(ctx, &ctx->ssim_part, parts));
     ctx->ssim_part_alloc = parts;
   }
   return ISG_OK;
@@ -1062,7 +1068,7 @@ isg_status isg_snapshot(isg_ctx* ctx) {
   if (!ctx) return ISG_E_ARG;
   cudaSetDevice(ctx->device);
   if (ctx->snap_n < ctx->n) {
-    ISG_CUDA(realloc_dev(&ctx->snap, 6 * std::max<int64_t>(ctx->n, 1)));
+    ISG_CUDA(realloc_dev(ctx, &ctx->snap, 6 * std::max<int64_t>(ctx->n, 1), false));
     ctx->snap_n = ctx->n;
   }
   const size_t n = (size_t)ctx->n;
@@ -1142,6 +1148,7 @@ isg_status isg_adaptive_control(isg_ctx* ctx, const isg_adapt_params* prm, uint6
   const cudaError_t e = isg::adaptive_control(ctx->ms, ctx->co, n, ctx->n_alloc, p, seed, round,
                                               ctx->sort, ctx->depth, ctx->order, ctx->adapt, &c,
                                               ctx->stream, &ctx->launches);
+  ctx->buf_gen++;  // the scene may now live in the former scratch buffers
   if (e != cudaSuccess) return cuda_fail(ctx, e, "adaptive_control");
   // the optimizer restarts on the new set (the reference clears its momentum, optimize.cpp:344)
   ctx->n = c.n_after;
@@ -1174,6 +1181,7 @@ struct isg_graph {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   int64_t launches = 0;
+  uint64_t buf_gen = 0;  // the context's buffer generation the graph's pointers belong to
 };
 
 isg_status isg_graph_begin(isg_ctx* ctx) {
@@ -1185,6 +1193,7 @@ isg_status isg_graph_begin(isg_ctx* ctx) {
   ISG_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
   ctx->capturing = true;
   ctx->capture_launches0 = ctx->launches;
+  ctx->capture_gen0 = ctx->buf_gen;
   return ISG_OK;
 }
 
@@ -1203,6 +1212,15 @@ isg_status isg_graph_end(isg_ctx* ctx, isg_graph** out) {
     return cuda_fail(ctx, e, "graph capture");
   }
   g->launches = ctx->launches - ctx->capture_launches0;
+  g->buf_gen = ctx->buf_gen;
+  if (ctx->buf_gen != ctx->capture_gen0) {  // a buffer grew inside the capture
+    cudaGraphExecDestroy(g->exec);
+    cudaGraphDestroy(g->graph);
+    delete g;
+    return fail(ctx, ISG_E_STATE,
+                "graph_end: device buffers were reallocated during the capture; run the step "
+                "once outside a capture (it sizes the buffers), then capture it");
+  }
   *out = g;
   return ISG_OK;
 }
@@ -1210,6 +1228,10 @@ isg_status isg_graph_end(isg_ctx* ctx, isg_graph** out) {
 isg_status isg_graph_launch(isg_ctx* ctx, isg_graph* g) {
   if (!ctx || !g) return ISG_E_ARG;
   if (ctx->capturing) return fail(ctx, ISG_E_STATE, "graph_launch: inside a capture");
+  if (g->buf_gen != ctx->buf_gen)
+    return fail(ctx, ISG_E_STATE,
+                "graph_launch: device buffers were reallocated since the capture (scene size, "
+                "key capacity, image size or adaptive control); capture the step again");
   cudaSetDevice(ctx->device);
   ISG_CUDA(cudaGraphLaunch(g->exec, ctx->stream));
   ctx->launches += g->launches;

@@ -604,3 +604,40 @@ def test_all_splats_culled(rend):
     np.testing.assert_array_equal(c2[:, :3], co[:, :3])
     np.testing.assert_allclose(m2[:, 3], ms[:, 3], rtol=1e-6)
     np.testing.assert_allclose(c2[:, 3], co[:, 3], rtol=1e-5)
+
+
+def test_graph_replay_refused_after_reallocation():
+    """A captured step holds device pointers: after the scene grows (buffers reallocated) or
+    adaptive control swaps the scene buffers, replaying it is refused (ISG_E_STATE) instead
+    of touching freed memory; a fresh capture works."""
+    import torch
+    W, H = 96, 64
+    cam = isg.Camera.synthetic(W, H)
+    with isg.Renderer(0) as r:
+        ms, co = isg.synth_scene(2000, W, H, seed=41)
+        r.set_scene(ms, co)
+        target = torch.from_numpy(O.render32(ms, co, cam)).cuda()
+        r.loss_backward(cam, target.cpu().numpy())
+        r.zero_grads()
+
+        def capture():
+            r.graph_begin()
+            r.loss_backward_device(cam, target.data_ptr())
+            r.adam_step(isg.AdamConfig())
+            return r.graph_end()
+        g = capture()
+        g.launch()
+        r.synchronize()
+        big_ms, big_co = isg.synth_scene(50000, W, H, seed=42)
+        r.set_scene(big_ms, big_co)  # more splats than allocated: buffers regrow
+        with pytest.raises(isg.IsgError) as e:
+            g.launch()
+        assert e.value.status == isg.ISG_E_STATE
+        r.loss_backward(cam, target.cpu().numpy())  # sizes the key buffers for the new scene
+        r.zero_grads()
+        g2 = capture()
+        g2.launch()
+        r.synchronize()
+        r.adaptive_control(isg.AdaptParams(1e-3, 0.5, 0.05, 1e9, 0))
+        with pytest.raises(isg.IsgError):
+            g2.launch()
