@@ -343,44 +343,64 @@ __global__ void __launch_bounds__(kThreads) k_ssim_bwd(int W, int H, const float
     else if (c == 1) cp_async_wait<1>();
     else cp_async_wait<0>();
     __syncthreads();
+    // coefficients 0 and 1 as a packed f32x2 pair (FFMA2, same per-lane rounding as fmaf),
+    // coefficient 2 scalar
     for (int i = tid; i < kHItems; i += kThreads) {
       const int g = i / kR, r = i - g * kR;
-      float acc[kG][3];
+      float2 a01[kG];
+      float a2[kG];
 #pragma unroll
-      for (int o = 0; o < kG; ++o) acc[o][0] = acc[o][1] = acc[o][2] = 0.0f;
+      for (int o = 0; o < kG; ++o) {
+        a01[o] = make_float2(0.0f, 0.0f);
+        a2[o] = 0.0f;
+      }
 #pragma unroll
       for (int j = 0; j < kIn; ++j) {
-        const float v[3] = {S.c[c][0][r][g * kG + j], S.c[c][1][r][g * kG + j],
-                            S.c[c][2][r][g * kG + j]};
+        const float2 v01 = make_float2(S.c[c][0][r][g * kG + j], S.c[c][1][r][g * kG + j]);
+        const float v2 = S.c[c][2][r][g * kG + j];
 #pragma unroll
         for (int o = 0; o < kG; ++o) {
           const int d = j - o;
           if (d >= 0 && d < kWin) {
-#pragma unroll
-            for (int k = 0; k < 3; ++k) acc[o][k] = fmaf(tp.w[d], v[k], acc[o][k]);
+            a01[o] = __ffma2_rn(make_float2(tp.w[d], tp.w[d]), v01, a01[o]);
+            a2[o] = fmaf(tp.w[d], v2, a2[o]);
           }
         }
       }
 #pragma unroll
-      for (int o = 0; o < kG; ++o)
-#pragma unroll
-        for (int k = 0; k < 3; ++k) S.h[k][r][g * kG + o] = acc[o][k];
+      for (int o = 0; o < kG; ++o) {
+        S.h[0][r][g * kG + o] = a01[o].x;
+        S.h[1][r][g * kG + o] = a01[o].y;
+        S.h[2][r][g * kG + o] = a2[o];
+      }
     }
     __syncthreads();
-    float acc[kG][3];
+    float2 b01[kG];
+    float b2[kG];
 #pragma unroll
-    for (int o = 0; o < kG; ++o) acc[o][0] = acc[o][1] = acc[o][2] = 0.0f;
+    for (int o = 0; o < kG; ++o) {
+      b01[o] = make_float2(0.0f, 0.0f);
+      b2[o] = 0.0f;
+    }
 #pragma unroll
     for (int j = 0; j < kIn; ++j) {
-      const float v[3] = {S.h[0][y0 + j][x], S.h[1][y0 + j][x], S.h[2][y0 + j][x]};
+      const float2 v01 = make_float2(S.h[0][y0 + j][x], S.h[1][y0 + j][x]);
+      const float v2 = S.h[2][y0 + j][x];
 #pragma unroll
       for (int o = 0; o < kG; ++o) {
         const int d = j - o;
         if (d >= 0 && d < kWin) {
-#pragma unroll
-          for (int k = 0; k < 3; ++k) acc[o][k] = fmaf(tp.w[d], v[k], acc[o][k]);
+          b01[o] = __ffma2_rn(make_float2(tp.w[d], tp.w[d]), v01, b01[o]);
+          b2[o] = fmaf(tp.w[d], v2, b2[o]);
         }
       }
+    }
+    float acc[kG][3];
+#pragma unroll
+    for (int o = 0; o < kG; ++o) {
+      acc[o][0] = b01[o].x;
+      acc[o][1] = b01[o].y;
+      acc[o][2] = b2[o];
     }
     const int gx = bx + x;
 #pragma unroll
