@@ -641,3 +641,51 @@ def test_graph_replay_refused_after_reallocation():
         r.adaptive_control(isg.AdaptParams(1e-3, 0.5, 0.05, 1e9, 0))
         with pytest.raises(isg.IsgError):
             g2.launch()
+
+
+def _random_rotation(rng):
+    q = rng.normal(size=4)
+    q /= np.linalg.norm(q)
+    w, x, y, z = q
+    return np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)],
+                     [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
+                     [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)]])
+
+
+@pytest.mark.parametrize("seed", range(32))
+def test_randomized_configurations(rend, seed):
+    """Seeded random image sizes, splat counts and size ranges, arbitrary camera rotations,
+    translations, focal lengths, principal points, backgrounds and t_min: bins bit-exact,
+    image and gradients within the stated tolerances."""
+    rng = np.random.default_rng(1000 + seed)
+    W, H = int(rng.integers(1, 300)), int(rng.integers(1, 200))
+    n = int(rng.integers(1, 6000))
+    R = _random_rotation(rng)
+    f = float(rng.uniform(0.3, 2.0)) * max(W, H)
+    cam = isg.Camera(R, rng.normal(size=3) * 0.2, f,
+                     (float(rng.uniform(0, W)), float(rng.uniform(0, H))), W, H)
+    # splats in front of the camera in camera space, mapped back to world space
+    z = rng.uniform(0.5, 12.0, n)
+    u, v = rng.uniform(-0.2 * W, 1.2 * W, n), rng.uniform(-0.2 * H, 1.2 * H, n)
+    pc = np.stack([(u - cam.principal_point[0]) * z / f, (v - cam.principal_point[1]) * z / f,
+                   z], 1)
+    pc[rng.random(n) < 0.05, 2] *= -1  # some behind the camera
+    mu = (pc - cam.translation) @ R  # R^T (pc - t)
+    s2d = np.exp(rng.uniform(np.log(0.2), np.log(rng.uniform(1.0, 30.0)), n))
+    ms = np.concatenate([mu, (s2d * np.abs(z) / f)[:, None]], 1).astype(np.float32)
+    co = np.concatenate([rng.uniform(0, 1, (n, 3)), rng.uniform(0.0, 1.0, (n, 1))],
+                        1).astype(np.float32)
+    opts = isg.RenderOptions(background=tuple(rng.uniform(0, 1, 3)),
+                             t_min=float(rng.choice([0.0, 1e-5])))
+    bg = opts.background
+    rend.set_scene(ms, co)
+    img = rend.render(cam, opts)
+    check_bins(rend, ms, co, cam)
+    ref = O.render32(ms, co, cam, bg=bg, t_min=opts.t_min)
+    assert np.abs(img - ref).max() <= IMG_TOL + 2.0 * opts.t_min
+    target = rng.uniform(0, 1, (H, W, 3)).astype(np.float32)
+    loss = rend.loss_backward(cam, target, opts)
+    loss_ref, g_ref = O.loss_backward32(ms, co, cam, target, bg=bg, t_min=opts.t_min)
+    assert abs(loss - loss_ref) <= 1e-5 * abs(loss_ref) + 1e-12
+    _grad_check(rend.grads(), g_ref)
+    rend.zero_grads()
