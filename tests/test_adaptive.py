@@ -204,3 +204,29 @@ def test_gpu_prune_all_keeps_best_and_training_continues(rend):
     assert loss == pytest.approx(loss_ref, rel=1e-5)
     rend.adam_step(isg.AdamConfig())
     assert rend.stats()["adam_steps"] == 1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(8))
+def test_gpu_adaptive_control_randomized(rend, seed):
+    """Seeded random scenes and rule parameters: counts and the resulting splat set bit-exact
+    against the 3D oracle."""
+    rng = np.random.default_rng(500 + seed)
+    n = int(rng.integers(1, 6000))
+    ms, co = scene3d(rng, n, clusters=bool(rng.integers(0, 2)))
+    prm = isg.AdaptParams(prune_threshold=float(rng.choice([0.0, 1e-3, 0.05])),
+                          merge_distance_factor=float(rng.uniform(0.05, 2.5)),
+                          merge_color_tol=float(rng.uniform(0.0, 0.4)),
+                          split_sigma_max=float(rng.choice([1e9, rng.uniform(0.02, 0.2)])),
+                          max_particles=int(rng.choice([0, n + int(rng.integers(0, n + 1))])))
+    rend.set_scene(ms, co)
+    res = rend.adaptive_control(prm, seed=seed, round_=seed % 3)
+    cap = prm.max_particles if prm.max_particles > 0 else 2 * n
+    om, oc, counts = oracle3d(ms, co, isg.AdaptParams(prm.prune_threshold,
+                                                      prm.merge_distance_factor,
+                                                      prm.merge_color_tol, prm.split_sigma_max,
+                                                      cap), seed=seed, round_=seed % 3)
+    gm, gc = rend.get_scene()
+    assert (res["n_pruned"], res["n_merged"], res["n_split"]) == counts
+    np.testing.assert_array_equal(gm, om)
+    np.testing.assert_array_equal(gc, oc)
