@@ -187,3 +187,30 @@ def test_gpu_train_with_l1_dssim_matches_oracle(rend, lam):
     assert rend.eval_loss_device(cam, t.data_ptr(), weight=0.7) == pytest.approx(loss, rel=1e-12)
     rend.zero_grads()
     rend.set_loss(isg.LOSS_L2)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(12))
+def test_gpu_image_loss_randomized(rend, seed):
+    """Seeded random image sizes (from the 11-pixel window minimum to several ragged 32-pixel
+    tiles), lambdas, weights and image statistics: loss and dL/dfhat against the FP64 oracle."""
+    import torch
+    rng = np.random.default_rng(700 + seed)
+    H, W = int(rng.integers(11, 140)), int(rng.integers(11, 140))
+    lam = float(rng.choice([0.0, 0.2, float(rng.uniform(0, 1)), 1.0]))
+    weight = float(rng.uniform(0.1, 3.0))
+    f = rng.uniform(0, 1, (H, W, 3))
+    if seed % 3 == 0:  # smooth images: the SSIM terms dominate
+        f = np.cumsum(np.cumsum(rng.normal(0, 0.02, (H, W, 3)), 0), 1)
+        f = (f - f.min()) / max(f.max() - f.min(), 1e-6)
+    fh = np.clip(f + rng.normal(0, float(rng.uniform(0.01, 0.3)), f.shape), 0, 1)
+    f32, fh32 = f.astype(np.float32), fh.astype(np.float32)
+    exp_loss, exp_g = O.image_loss64(f32, fh32, lam, weight, grad=True)
+    tf, tfh = torch.from_numpy(f32).cuda(), torch.from_numpy(fh32).cuda()
+    g = torch.empty_like(tf)
+    rend.set_loss(isg.LOSS_L1_DSSIM, lam)
+    loss = rend.image_loss_device(W, H, tfh.data_ptr(), tf.data_ptr(), weight, g.data_ptr())
+    rend.set_loss(isg.LOSS_L2)
+    assert loss == pytest.approx(exp_loss, rel=LOSS_RTOL, abs=1e-9)
+    g = g.cpu().numpy()
+    assert np.abs(g - exp_g).max() <= PIXGRAD_TOL * np.abs(exp_g).max()
