@@ -370,7 +370,7 @@ def test_binning_modes_bit_identical(rend):
         bins = check_bins(rend, ms, co, cam)
         loss = rend.loss_backward(cam, target)
         out.append((img, bins, loss, rend.grads()))
-    rend.set_binning(isg.Renderer.BINNING_TILE_BUCKET)
+    rend.set_binning(isg.Renderer.BINNING_RADIX)  # the default, for the tests that follow
     (i0, b0, l0, g0), (i1, b1, l1, g1) = out
     assert np.array_equal(i0, i1) and np.array_equal(b0, b1)
     assert l0 == l1 and np.array_equal(g0, g1)
@@ -679,6 +679,10 @@ def test_randomized_configurations(rend, seed):
                              t_min=float(rng.choice([0.0, 1e-5])))
     bg = opts.background
     rend.set_scene(ms, co)
+    rend.set_binning(isg.Renderer.BINNING_TILE_BUCKET)  # the alternative binning: same lists
+    rend.render(cam, opts)
+    check_bins(rend, ms, co, cam)
+    rend.set_binning(isg.Renderer.BINNING_RADIX)
     img = rend.render(cam, opts)
     check_bins(rend, ms, co, cam)
     ref = O.render32(ms, co, cam, bg=bg, t_min=opts.t_min)
