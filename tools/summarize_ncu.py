@@ -44,7 +44,9 @@ def launches(path, out):
         d[metric] = float(val.replace(",", ""))
         d[metric + ".unit"] = unit
     ids = list(per)
-    last_pre = max(i for i in ids if per[i]["kernel"] == "k_preprocess")
+    # a step starts with the frame reset (k_zero2) when present, else with K1
+    first = "k_zero2" if any(per[i]["kernel"] == "k_zero2" for i in ids) else "k_preprocess"
+    last_pre = max(i for i in ids if per[i]["kernel"] == first)
     step = [per[i] for i in ids if i >= last_pre]
     agg = OrderedDict()
     for d in step:
