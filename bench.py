@@ -551,7 +551,13 @@ def run_isg(args):
     top_name, (top_ms_total, top_calls) = top
     top_ms = top_ms_total / max(top_calls, 1)
     roof = {"kernel": top_name, "stage_ms_per_step": {k: v[0] / prof_steps for k, v in prof.items()}}
-    pairs = None
+    # algorithmic work of the blend kernels (roofline): view 0 of the current scene, every
+    # pixel walking its list until termination, counted on the GPU (isg_count_pairs), outside
+    # every timed region
+    count_img = torch.empty((H, W, 3), dtype=torch.float32, device="cuda")
+    r.render_device(cams[0], opts, count_img.data_ptr())
+    pairs = r.count_pairs()
+    del count_img
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         import oracle as O
@@ -559,8 +565,7 @@ def run_isg(args):
         tgt0 = host_targets[0]
         ms_now, co_now = r.get_scene()
         t0 = time.perf_counter()
-        _, _, _, counts = O.render32(ms_now, co_now, cam0, t_min=T_MIN, want_state=True)
-        pairs = (int(counts[0]), int(counts[1]))
+        O.render32(ms_now, co_now, cam0, t_min=T_MIN)
         cores = host_threads()
         sec = cpu_oracle_train_step(ms_now, co_now, cam0, tgt0, 1, cores) if train else \
             (time.perf_counter() - t0)

@@ -218,6 +218,11 @@ isg_status isg_nccl_detach(isg_ctx* ctx);
  * *n_keys always receives the key count. */
 isg_status isg_debug_bins(isg_ctx* ctx, uint64_t* keys, uint32_t* vals, int64_t* n_keys,
                           uint32_t* ranges);
+/* Measurement hook (bench.py's roofline): the last frame's algorithmic work as the
+ * reference's per-pixel loop sees it -- each pixel walks its tile's depth-ordered list until
+ * its transmittance drops to t_min; *evaluated = entries visited, *inside = entries inside
+ * their 3-sigma circle (summed over pixels).  Slow (no culling): outside timed regions. */
+isg_status isg_count_pairs(isg_ctx* ctx, int64_t* evaluated, int64_t* inside);
 /* Per-pixel forward state of the last render: transmittance before the last contributor
  * and number of list entries processed (both H x W). */
 isg_status isg_debug_pixel_state(isg_ctx* ctx, float* t_last, uint32_t* n_proc);

@@ -1383,6 +1383,31 @@ isg_status isg_profile_read(isg_ctx* ctx, double* ms, int64_t* calls) {
   return ISG_OK;
 }
 
+isg_status isg_count_pairs(isg_ctx* ctx, int64_t* evaluated, int64_t* inside) {
+  if (!ctx || !evaluated || !inside) return ISG_E_ARG;
+  if (!ctx->have_frame) return fail(ctx, ISG_E_STATE, "count_pairs: no frame rendered yet");
+  cudaSetDevice(ctx->device);
+  bool ov = false;
+  isg_status s = check_frame(ctx, &ov);
+  if (s != ISG_OK) return s;
+  if (ov) return fail(ctx, ISG_E_OVERFLOW, "count_pairs: last frame overflowed");
+  const FrameParams& fp = ctx->last_fp;
+  if (ctx->binning == isg::kBinRadix)
+    isg::launch_ranges_fix(ctx->sc + 0, ctx->key_cap, fp.n_tiles, ctx->ranges, ctx->stream);
+  unsigned long long* d = nullptr;
+  ISG_CUDA(cudaMalloc(&d, 2 * sizeof(unsigned long long)));
+  ISG_CUDA(cudaMemsetAsync(d, 0, 2 * sizeof(unsigned long long), ctx->stream));
+  isg::launch_count_pairs(fp, ctx->ranges, ctx->sorted, ctx->rec, d, ctx->stream);
+  unsigned long long h[2] = {0, 0};
+  cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream);
+  const cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  cudaFree(d);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "count_pairs");
+  *evaluated = (int64_t)h[0];
+  *inside = (int64_t)h[1];
+  return ISG_OK;
+}
+
 isg_status isg_debug_pixel_state(isg_ctx* ctx, float* t_last, uint32_t* n_proc) {
   if (!ctx) return ISG_E_ARG;
   if (!ctx->have_frame) return fail(ctx, ISG_E_STATE, "debug_pixel_state: no frame rendered yet");

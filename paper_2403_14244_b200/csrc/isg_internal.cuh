@@ -221,6 +221,11 @@ cudaError_t adaptive_control(float4*& ms, float4*& co, int64_t n, int64_t n_allo
                              AdaptScratch*& scratch, AdaptCounts* counts, cudaStream_t st,
                              int64_t* launches);
 
+// measurement hook: per-pixel walk of the last frame's lists until termination; out[0] +=
+// entries evaluated, out[1] += entries inside their 3-sigma circle (out zeroed by the caller)
+void launch_count_pairs(const FrameParams& fp, const uint2* ranges, const uint2* sorted,
+                        const RenderRec* rec, unsigned long long* out, cudaStream_t st);
+
 // ---- parity hook -------------------------------------------------------------------------
 void launch_debug_keys(const uint2* ranges, const uint2* sorted, const float4* ms,
                        const FrameParams& fp, uint64_t* keys, uint32_t* gids, cudaStream_t st);

@@ -227,6 +227,60 @@ __global__ void ISG_FWD_BOUNDS k_blend_fwd(
   }
 }
 
+// Measurement hook (bench.py's roofline): the algorithmic work of the last frame, counted the
+// way the reference's per-pixel loop sees it -- every pixel walks its tile's list in depth
+// order until its transmittance drops to t_min, counting the entries it evaluates and those
+// inside their 3-sigma circle.  One thread per pixel, no culling; run outside timed regions.
+__global__ void __launch_bounds__(kTilePixels) k_count_pairs(
+    FrameParams fp, const uint2* __restrict__ ranges, const uint2* __restrict__ sorted,
+    const RenderRec* __restrict__ rec, unsigned long long* __restrict__ out) {
+  __shared__ unsigned long long s_ev[kTilePixels / 32], s_in[kTilePixels / 32];
+  const int tile = blockIdx.x;
+  const int tx = tile % fp.tiles_x, ty = tile / fp.tiles_x;
+  const int x = tx * kTile + (threadIdx.x & (kTile - 1)), y = ty * kTile + threadIdx.x / kTile;
+  unsigned long long ev = 0, in = 0;
+  if (x < fp.cam.width && y < fp.cam.height) {
+    const uint2 rg = ranges[tile];
+    const uint32_t n = rg.x == kEmptyRange ? 0u : rg.y - rg.x;
+    const float px = (float)x + 0.5f, py = (float)y + 0.5f;
+    float T = 1.0f;
+    for (uint32_t p = 0; p < n; ++p) {
+      const RenderRec r = rec[sorted[rg.x + p].x];
+      ++ev;
+      const float r2 = dist2_rn(__fsub_rn(px, r.geo.x), __fsub_rn(py, r.geo.y));
+      if (r2 > r.geo.z) continue;
+      ++in;
+      const float a = r.col.w * fast_exp2(r2 * r.geo.w);
+      T = T * (1.0f - a);
+      if (!(T > fp.t_min)) break;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ev += __shfl_xor_sync(0xffffffffu, ev, o);
+    in += __shfl_xor_sync(0xffffffffu, in, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s_ev[threadIdx.x >> 5] = ev;
+    s_in[threadIdx.x >> 5] = in;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long e = 0, i = 0;
+    for (int w = 0; w < kTilePixels / 32; ++w) {
+      e += s_ev[w];
+      i += s_in[w];
+    }
+    atomicAdd(&out[0], e);
+    atomicAdd(&out[1], i);
+  }
+}
+
+void launch_count_pairs(const FrameParams& fp, const uint2* ranges, const uint2* sorted,
+                        const RenderRec* rec, unsigned long long* out, cudaStream_t st) {
+  k_count_pairs<<<fp.n_tiles, kTilePixels, 0, st>>>(fp, ranges, sorted, rec, out);
+}
+
 void launch_blend_fwd(const FrameParams& fp, const uint2* ranges, const uint2* sorted,
                       const RenderRec* rec, const unsigned long long* total, int64_t key_cap,
                       float* out, float* t_last, uint32_t* n_proc, cudaStream_t st) {

@@ -109,6 +109,7 @@ def lib() -> C.CDLL:
         "isg_nccl_detach": ([P], C.c_int),
         "isg_debug_bins": ([P, P, P, C.POINTER(I64), P], C.c_int),
         "isg_debug_pixel_state": ([P, P, P], C.c_int),
+        "isg_count_pairs": ([P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)], C.c_int),
         "isg_set_binning": ([P, C.c_int], C.c_int),
         "isg_profile_enable": ([P, C.c_int], C.c_int),
         "isg_profile_num_stages": ([], C.c_int),
@@ -135,7 +136,7 @@ C_ABI_SYMBOLS = (
     "isg_restore", "isg_set_loss", "isg_image_loss_device", "isg_adaptive_control",
     "isg_graph_begin", "isg_graph_end", "isg_graph_launch", "isg_graph_destroy", "isg_nccl_get_unique_id",
     "isg_nccl_init",
-    "isg_nccl_detach", "isg_debug_bins", "isg_debug_pixel_state", "isg_set_binning",
+    "isg_nccl_detach", "isg_debug_bins", "isg_debug_pixel_state", "isg_count_pairs", "isg_set_binning",
     "isg_profile_enable",
     "isg_profile_num_stages", "isg_profile_stage_name", "isg_profile_read", "isg_synth_scene",
     "isg_synth_camera",
@@ -537,6 +538,12 @@ class Renderer:
         _check(self._h, lib().isg_debug_bins(self._h, _ptr(keys), _ptr(vals), C.byref(n),
                                              _ptr(ranges)))
         return keys, vals, ranges
+
+    def count_pairs(self):
+        """(evaluated, inside) pixel-entry pairs of the last frame (isg_count_pairs)."""
+        a, b = C.c_int64(), C.c_int64()
+        _check(self._h, lib().isg_count_pairs(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def debug_pixel_state(self, width: int, height: int):
         tl = np.empty((height, width), np.float32)

@@ -693,3 +693,18 @@ def test_randomized_configurations(rend, seed):
     assert abs(loss - loss_ref) <= 1e-5 * abs(loss_ref) + 1e-12
     _grad_check(rend.grads(), g_ref)
     rend.zero_grads()
+
+
+def test_count_pairs_matches_oracle_counts(rend):
+    """isg_count_pairs (the roofline's algorithmic work) against the FP32 oracle's own counts of
+    evaluated and in-circle pixel-entry pairs (termination at t_min: ex2.approx vs expf may
+    end a pixel's walk one entry apart, hence the small tolerance)."""
+    W, H = 320, 200
+    ms, co = isg.synth_scene(30000, W, H, seed=77)
+    cam = isg.Camera.synthetic(W, H)
+    rend.set_scene(ms, co)
+    rend.render(cam)
+    ev, inside = rend.count_pairs()
+    _, _, _, counts = O.render32(ms, co, cam, want_state=True)
+    assert ev == pytest.approx(int(counts[0]), rel=1e-3)
+    assert inside == pytest.approx(int(counts[1]), rel=1e-3)
