@@ -457,12 +457,13 @@ def run_isg(args):
         ev_done = [torch.cuda.Event() for _ in range(2)]
         ev_read = [torch.cuda.Event() for _ in range(2)]
         r.synchronize()
+    NB = 3  # target buffers: step i+2's upload may start once step i-1 is done
     if use_pipe:
-        bufs = [[torch.empty_like(t) for t in targets] for _ in range(2)]
-        loss_host = torch.zeros(2, dtype=torch.float64).pin_memory()
+        bufs = [[torch.empty_like(t) for t in targets] for _ in range(NB)]
+        loss_host = torch.zeros(NB, dtype=torch.float64).pin_memory()
         step_losses = []
         graphs = []
-        for b in range(2):
+        for b in range(NB):
             def step_b(bb=bufs[b], slot=loss_host[b:b + 1]):
                 for c, t in zip(cams, bb):
                     r.loss_backward_device(c, t.data_ptr(), opts, weight=1.0 / step_views)
@@ -474,8 +475,8 @@ def run_isg(args):
             step_b()
             graphs.append(r.graph_end())
         copy_stream = torch.cuda.Stream()
-        ev_copy = [torch.cuda.Event() for _ in range(2)]
-        ev_done = [torch.cuda.Event() for _ in range(2)]
+        ev_copy = [torch.cuda.Event() for _ in range(NB)]
+        ev_done = [torch.cuda.Event() for _ in range(NB)]
         r.synchronize()
     if train:
         r.restore()
@@ -484,25 +485,28 @@ def run_isg(args):
     t_start = time.perf_counter()
     if use_pipe:
         with torch.cuda.stream(copy_stream):
-            for t, h in zip(bufs[0], pinned):
-                t.copy_(h, non_blocking=True)
-            ev_copy[0].record(copy_stream)
+            for k in range(min(NB - 1, args.steps)):
+                for t, h in zip(bufs[k], pinned):
+                    t.copy_(h, non_blocking=True)
+                ev_copy[k].record(copy_stream)
     for i in range(args.steps):
         t0 = time.perf_counter()
         if use_pipe:
-            b = i & 1
+            b = i % NB
             stream.wait_event(ev_copy[b])
             graphs[b].launch()
             ev_done[b].record(stream)
-            if i + 1 < args.steps:  # prefetch the next step's inputs into the other buffer
+            if i + NB - 1 < args.steps:  # prefetch step i+2's inputs once step i-1 is done
+                nb = (i + NB - 1) % NB
                 with torch.cuda.stream(copy_stream):
-                    copy_stream.wait_event(ev_done[1 - b])
-                    for t, h in zip(bufs[1 - b], pinned):
+                    copy_stream.wait_event(ev_done[nb])
+                    for t, h in zip(bufs[nb], pinned):
                         t.copy_(h, non_blocking=True)
-                    ev_copy[1 - b].record(copy_stream)
+                    ev_copy[nb].record(copy_stream)
             if i >= 1:  # step i-1's loss is on the host once its graph is done (step i queued)
-                ev_done[1 - b].synchronize()
-                step_losses.append(float(loss_host[1 - b]))
+                pb = (i - 1) % NB
+                ev_done[pb].synchronize()
+                step_losses.append(float(loss_host[pb]))
         elif train:
             for c, h in zip(cams, host_views):
                 r.loss_backward(c, h, opts, weight=1.0 / step_views)  # H2D target, D2H loss
@@ -522,8 +526,8 @@ def run_isg(args):
             r.render(cams[0], opts, out=host_out)  # D2H image into pinned memory
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
     if use_pipe:
-        ev_done[(args.steps - 1) & 1].synchronize()
-        step_losses.append(float(loss_host[(args.steps - 1) & 1]))
+        ev_done[(args.steps - 1) % NB].synchronize()
+        step_losses.append(float(loss_host[(args.steps - 1) % NB]))
     if use_rpipe:
         for e in ev_read:
             e.synchronize()  # the last frames' images are on the host
@@ -630,8 +634,8 @@ def run_isg(args):
                 "ms_per_step": e2e_step,
                 **({"loss_first_last": [step_losses[0], step_losses[-1]],
                     "losses_read": len(step_losses)} if use_pipe else {}),
-                "mode": ("cuda graph per step, next step's targets prefetched from pinned host "
-                         "memory on a copy stream; every step's loss copied D2H into pinned "
+                "mode": ("cuda graph per step, targets prefetched two steps ahead from pinned host "
+                         "memory on a copy stream (3 buffers); every step's loss copied D2H into pinned "
                          "memory inside its graph and read by the host while the next step "
                          "runs (all reads inside the timed region)") if use_pipe else
                         ("cuda graph per frame into a double-buffered device image, each image "
