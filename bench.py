@@ -185,9 +185,10 @@ def cpu_oracle_train_step(ms, co, cam, target, steps=1, threads=0):
     m = np.zeros((ms.shape[0], 8), np.float32)
     v = np.zeros_like(m)
     t0 = time.perf_counter()
+    raw = O.raw_init32(ms, co)
     for s in range(1, steps + 1):
         _, g = O.loss_backward32(ms, co, cam, target, t_min=T_MIN, threads=threads)
-        O.adam32(ms, co, m, v, g, s, [1e-3, 5e-3, 1e-2, 1e-2], 0.9, 0.999, 1e-15)
+        O.adam32(ms, co, m, v, g, s, [1e-3, 5e-3, 1e-2, 1e-2], 0.9, 0.999, 1e-15, raw=raw)
     return (time.perf_counter() - t0) / steps
 
 

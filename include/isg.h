@@ -41,7 +41,7 @@ extern "C" {
 #endif
 
 #define ISG_TILE 16 /* screen tiles are ISG_TILE x ISG_TILE pixels */
-#define ISG_ABI_VERSION 1
+#define ISG_ABI_VERSION 2
 
 typedef struct isg_ctx isg_ctx; /* one per device: device buffers, a stream, Adam state. NOT thread-safe. */
 
@@ -76,6 +76,7 @@ typedef struct {
   int64_t skipped_updates;/* Gaussian updates skipped for non-finite gradients (optimize.cpp:87-90) */
   int64_t regrow_events;  /* frames re-run after key-capacity growth */
   int64_t kernel_launches;/* kernels launched by this context so far */
+  int64_t overflowed_frames;/* frames skipped for key-capacity overflow (each reported once) */
 } isg_stats;
 
 /* ---- lifetime -------------------------------------------------------------------------- */

@@ -58,9 +58,15 @@ def lib():
         L.or32_loss_backward.argtypes = [I64, P, P, C.POINTER(Cam32), P, C.c_float, P, C.c_float,
                                          C.c_int, C.POINTER(C.c_double), P, P]
         L.or32_loss_backward.restype = C.c_int
-        L.or32_adam.argtypes = [I64, P, P, P, P, P, I64, P, C.c_float, C.c_float, C.c_float,
+        L.or32_adam.argtypes = [I64, P, P, P, P, P, P, I64, P, C.c_float, C.c_float, C.c_float,
                                 C.POINTER(I64)]
         L.or32_adam.restype = None
+        L.or32_raw_init.argtypes = [I64, P, P, P]
+        L.or32_raw_init.restype = None
+        L.or_synth_scene.argtypes = [C.c_uint64, I64, C.c_int, C.c_int, P, P]
+        L.or_synth_scene.restype = None
+        L.or_synth_camera.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, P]
+        L.or_synth_camera.restype = None
         L.or32_backward_dldc.argtypes = [I64, P, P, C.POINTER(Cam32), P, C.c_float, P, C.c_int, P]
         L.or32_backward_dldc.restype = C.c_int
         L.or64_image_loss.argtypes = [C.c_int, C.c_int, P, P, C.c_double, C.c_double,
@@ -90,6 +96,35 @@ def cam64(camera) -> Cam64:
     c.cx, c.cy = map(float, camera.principal_point)
     c.width, c.height = int(camera.width), int(camera.height)
     return c
+
+
+class Camera:
+    """Plain camera record the oracle functions accept (any object with these attributes
+    does): rotation (3x3 world->camera), translation, focal, principal_point, width, height."""
+
+    def __init__(self, rotation, translation, focal, principal_point, width, height):
+        self.rotation = np.asarray(rotation, np.float64).reshape(3, 3)
+        self.translation = np.asarray(translation, np.float64).reshape(3)
+        self.focal = float(focal)
+        self.principal_point = (float(principal_point[0]), float(principal_point[1]))
+        self.width, self.height = int(width), int(height)
+
+
+def synth_scene(n, width, height, seed=2403):
+    """isg-synth v1 scene restated in the oracle: (mu_sigma, rgb_opacity), both
+    (n, 4) float32, byte-equal to the product's isg_synth_scene."""
+    ms = np.empty((n, 4), np.float32)
+    co = np.empty((n, 4), np.float32)
+    lib().or_synth_scene(seed, n, width, height, _p(ms), _p(co))
+    return ms, co
+
+
+def synth_camera(width, height, view=0, n_views=1) -> Camera:
+    """Camera `view` of an n-view isg-synth batch (the FP32 values of isg_synth_camera)."""
+    v = np.zeros(15, np.float32)
+    lib().or_synth_camera(width, height, view, n_views, _p(v))
+    return Camera(v[:9].astype(np.float64).reshape(3, 3), v[9:12].astype(np.float64),
+                  float(v[12]), (float(v[13]), float(v[14])), width, height)
 
 
 def cam32(camera) -> Cam32:
@@ -171,7 +206,7 @@ def bin32(ms, co, camera):
     return keys, vals, ranges, nvis.value
 
 
-def render32(ms, co, camera, bg=(0, 0, 0), t_min=1e-5, threads=0, want_state=False):
+def render32(ms, co, camera, bg=(0, 0, 0), t_min=0.0, threads=0, want_state=False):
     ms = np.ascontiguousarray(ms, np.float32)
     co = np.ascontiguousarray(co, np.float32)
     H, W = camera.height, camera.width
@@ -187,7 +222,7 @@ def render32(ms, co, camera, bg=(0, 0, 0), t_min=1e-5, threads=0, want_state=Fal
     return out
 
 
-def loss_backward32(ms, co, camera, target, bg=(0, 0, 0), t_min=1e-5, weight=1.0, threads=0,
+def loss_backward32(ms, co, camera, target, bg=(0, 0, 0), t_min=0.0, weight=1.0, threads=0,
                     grads=None, want_image=False):
     ms = np.ascontiguousarray(ms, np.float32)
     co = np.ascontiguousarray(co, np.float32)
@@ -205,17 +240,30 @@ def loss_backward32(ms, co, camera, target, bg=(0, 0, 0), t_min=1e-5, weight=1.0
     return loss.value, grads
 
 
-def adam32(ms, co, m, v, grads, step, lr, b1=0.9, b2=0.999, eps=1e-15):
-    """In place on ms, co, m, v (all float32, C-contiguous)."""
+def raw_init32(ms, co):
+    """Optimizer-space state (log sigma, logit clamp(opacity, 1e-6, 1 - 1e-6)), n x 2 float32."""
+    ms = np.ascontiguousarray(ms, np.float32)
+    co = np.ascontiguousarray(co, np.float32)
+    raw = np.zeros((ms.shape[0], 2), np.float32)
+    lib().or32_raw_init(ms.shape[0], _p(ms), _p(co), _p(raw))
+    return raw
+
+
+def adam32(ms, co, m, v, grads, step, lr, b1=0.9, b2=0.999, eps=1e-15, raw=None):
+    """In place on ms, co, m, v (all float32, C-contiguous) and raw, the persistent
+    (log sigma, logit opacity) optimizer state (n x 2; None = raw_init32(ms, co), i.e. the
+    first step after the splats were set).  Returns the number of skipped updates."""
     skipped = C.c_int64()
     lrs = np.asarray(lr, np.float32)
     g = np.ascontiguousarray(grads, np.float32)
-    lib().or32_adam(ms.shape[0], _p(ms), _p(co), _p(m), _p(v), _p(g), step, _p(lrs), b1, b2, eps,
-                    C.byref(skipped))
+    if raw is None:
+        raw = raw_init32(ms, co)
+    lib().or32_adam(ms.shape[0], _p(ms), _p(co), _p(raw), _p(m), _p(v), _p(g), step, _p(lrs), b1,
+                    b2, eps, C.byref(skipped))
     return skipped.value
 
 
-def backward_dldc32(ms, co, camera, dldc, bg=(0, 0, 0), t_min=1e-5, threads=0, grads=None):
+def backward_dldc32(ms, co, camera, dldc, bg=(0, 0, 0), t_min=0.0, threads=0, grads=None):
     """FP32 tiled backward for a given pixel gradient dL/dC (HWC3); accumulates into grads."""
     ms = np.ascontiguousarray(ms, np.float32)
     co = np.ascontiguousarray(co, np.float32)

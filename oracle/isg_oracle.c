@@ -855,12 +855,28 @@ int or64_image_loss(int W, int H, const double* f, const double* fhat, double la
   return 0;
 }
 
+/* Optimizer-space state of a set of splats: raw = (log sigma, logit opacity), the opacity
+ * first taken into [1e-6, 1 - 1e-6] (logit(0), logit(1) are infinite). */
+#define OR_OPACITY_EPS 1e-6f
+void or32_raw_init(int64_t n, const float* mu_sigma, const float* rgb_o, float* raw) {
+  for (int64_t i = 0; i < n; ++i) {
+    float op = rgb_o[4 * i + 3];
+    op = fminf(fmaxf(op, OR_OPACITY_EPS), 1.0f - OR_OPACITY_EPS);
+    raw[2 * i] = logf(mu_sigma[4 * i + 3]);
+    raw[2 * i + 1] = logf(op) - log1pf(-op);
+  }
+}
+
 /* Adam (torch.optim.Adam semantics, no weight decay) on the optimizer-space parameters
  * (mu, log sigma, rgb, logit opacity) with per-group learning rates lr[4].  sigma moves in
  * log space as in update_step (optimize.cpp:93,105); a Gaussian whose 8 gradients are not
- * all finite is skipped and counted (optimize.cpp:87-90).  m, v: n x 8; step >= 1. */
-void or32_adam(int64_t n, float* mu_sigma, float* rgb_o, float* m, float* v, const float* grads,
-               int64_t step, const float* lr, float b1, float b2, float eps, int64_t* skipped) {
+ * all finite is skipped and counted (optimize.cpp:87-90).  m, v: n x 8; step >= 1.
+ * raw (n x 2): the persistent (log sigma, logit opacity) -- like torch's own parameters, they
+ * are never re-derived from sigma / opacity; sigma = exp(raw.x), opacity = sigmoid(raw.y) are
+ * rewritten only when their raw value moved.  An update is exactly 0 when m is 0. */
+void or32_adam(int64_t n, float* mu_sigma, float* rgb_o, float* raw, float* m, float* v,
+               const float* grads, int64_t step, const float* lr, float b1, float b2, float eps,
+               int64_t* skipped) {
   const double bc1 = 1.0 - pow((double)b1, (double)step);
   const double bc2 = 1.0 - pow((double)b2, (double)step);
   const float bc2_sqrt = (float)sqrt(bc2);
@@ -878,25 +894,30 @@ void or32_adam(int64_t n, float* mu_sigma, float* rgb_o, float* m, float* v, con
     }
     float* ms = mu_sigma + 4 * (size_t)i;
     float* co = rgb_o + 4 * (size_t)i;
-    const float sigma = ms[3], op = co[3];
-    float p[8] = {ms[0], ms[1], ms[2], logf(sigma), co[0], co[1], co[2], logf(op) - log1pf(-op)};
-    float g[8] = {gr[0], gr[1], gr[2], gr[3] * sigma, gr[4], gr[5], gr[6], gr[7] * op * (1.0f - op)};
+    float* R = raw + 2 * (size_t)i;
+    const float sigma = ms[3];
+    const float s = 1.0f / (1.0f + expf(-R[1]));
+    float p[8] = {ms[0], ms[1], ms[2], R[0], co[0], co[1], co[2], R[1]};
+    float g[8] = {gr[0], gr[1], gr[2], gr[3] * sigma, gr[4], gr[5], gr[6], gr[7] * s * (1.0f - s)};
     for (int j = 0; j < 8; ++j) {
       float* mm = m + 8 * (size_t)i + j;
       float* vv = v + 8 * (size_t)i + j;
       *mm = *mm + (1.0f - b1) * (g[j] - *mm);
       *vv = b2 * *vv + (1.0f - b2) * g[j] * g[j];
       const float denom = sqrtf(*vv) / bc2_sqrt + eps;
-      p[j] = p[j] - step_size[group[j]] * (*mm / denom);
+      const float upd = *mm == 0.0f ? 0.0f : *mm / denom;
+      p[j] = p[j] - step_size[group[j]] * upd;
     }
     ms[0] = p[0];
     ms[1] = p[1];
     ms[2] = p[2];
-    ms[3] = expf(p[3]);
+    if (p[3] != R[0]) ms[3] = expf(p[3]);
     co[0] = p[4];
     co[1] = p[5];
     co[2] = p[6];
-    co[3] = 1.0f / (1.0f + expf(-p[7]));
+    if (p[7] != R[1]) co[3] = 1.0f / (1.0f + expf(-p[7]));
+    R[0] = p[3];
+    R[1] = p[7];
   }
   if (skipped) *skipped += skip;
 }
@@ -1157,4 +1178,61 @@ int64_t or_adaptive_control(int dims, int64_t n, const double* in, const or_adap
   free(pairs);
   free(a);
   return c;
+}
+
+/* ============================================================================================
+ * (5) The synthetic workload "isg-synth v1" -- restated here so the CPU arms of
+ * bench.py and the tests build the same scenes and cameras without the product library (pinned
+ * byte-equal to isg_synth_scene / isg_synth_camera in tests/test_oracle.py).  Counter-based:
+ * splitmix64 finaliser of seed * phi + 8 i + j, top 24 bits. */
+#ifndef M_PI
+#define M_PI 3.14159265358979323846
+#endif
+static uint64_t or_mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+static double or_u01(uint64_t seed, uint64_t i, int j) {
+  return (double)(or_mix64(seed * 0x9E3779B97F4A7C15ull + 8 * i + (uint64_t)j) >> 40) *
+         (1.0 / 16777216.0);
+}
+
+/* z ~ U[2,10]; u ~ U[-5%, 105%] W, v ~ U[-5%, 105%] H back-projected through the identity
+ * camera (f = 1000 W / 1920, principal point at the centre); sigma_2d ~ logU[0.5, 8] px;
+ * opacity ~ U[0.05, 0.95]; rgb ~ U[0,1]^3. */
+void or_synth_scene(uint64_t seed, int64_t n, int W, int H, float* ms, float* co) {
+  const double f = 1000.0 * W / 1920.0, cx = 0.5 * W, cy = 0.5 * H;
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) {
+    const double z = 2.0 + 8.0 * or_u01(seed, (uint64_t)i, 0);
+    const double u = W * (-0.05 + 1.1 * or_u01(seed, (uint64_t)i, 1));
+    const double v = H * (-0.05 + 1.1 * or_u01(seed, (uint64_t)i, 2));
+    const double s2d = 0.5 * pow(16.0, or_u01(seed, (uint64_t)i, 3));
+    ms[4 * i + 0] = (float)((u - cx) * z / f);
+    ms[4 * i + 1] = (float)((v - cy) * z / f);
+    ms[4 * i + 2] = (float)z;
+    ms[4 * i + 3] = (float)(s2d * z / f);
+    co[4 * i + 0] = (float)or_u01(seed, (uint64_t)i, 5);
+    co[4 * i + 1] = (float)or_u01(seed, (uint64_t)i, 6);
+    co[4 * i + 2] = (float)or_u01(seed, (uint64_t)i, 7);
+    co[4 * i + 3] = (float)(0.05 + 0.9 * or_u01(seed, (uint64_t)i, 4));
+  }
+}
+
+/* Camera k of an n-view batch: yaw (k - (n-1)/2) * 1.5 deg about y, t = (0.05 (k - (n-1)/2),
+ * 0, 0); out = R[9] (row-major), t[3], focal, cx, cy as FP32 values (the FP32 camera). */
+void or_synth_camera(int W, int H, int view, int n_views, float* out) {
+  const double k = view - 0.5 * (n_views - 1);
+  const double th = k * 1.5 * M_PI / 180.0;
+  const double cs = cos(th), sn = sin(th);
+  const double R[9] = {cs, 0, sn, 0, 1, 0, -sn, 0, cs};
+  for (int i = 0; i < 9; ++i) out[i] = (float)R[i];
+  out[9] = (float)(0.05 * k);
+  out[10] = 0.0f;
+  out[11] = 0.0f;
+  out[12] = (float)(1000.0 * W / 1920.0);
+  out[13] = (float)(0.5 * W);
+  out[14] = (float)(0.5 * H);
 }

@@ -12,6 +12,12 @@ constexpr uint32_t kEmptyRange = 0xFFFFFFFFu;
 __device__ __forceinline__ bool overflowed(const unsigned long long* total, int64_t cap) {
   return *total > (unsigned long long)cap;
 }
+// total[2] = max key count of any overflowed frame since the host's last check, total[3] =
+// frames skipped; the per-frame reset leaves both alone (isg_internal.cuh, kTotal*)
+__device__ __forceinline__ void note_overflow(unsigned long long* total) {
+  atomicMax(total + kTotalOverflowMax, total[kTotalKeys]);
+  atomicAdd(total + kTotalOverflowFrames, 1ull);
+}
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);

@@ -50,6 +50,7 @@ struct isg_ctx {
   float4* co = nullptr;
   float4* m = nullptr;
   float4* v = nullptr;
+  float2* raw = nullptr;  // optimizer space: (log sigma, logit opacity) per splat
   int64_t adam_t = 0;
 
   // per-splat work buffers
@@ -110,7 +111,7 @@ struct isg_ctx {
 
   // device scalars: [0] n_keys [1] first_bad [2] n_visible [3] scan tile counter [4] n
   uint32_t* sc = nullptr;
-  unsigned long long* total = nullptr;     // [0] total keys, [1] skipped updates
+  unsigned long long* total = nullptr;     // isg::TotalWord: keys, skipped, overflow record
   double* loss = nullptr;                  // [0] accumulated, [1] last view, [2] last step
   isg::AdamState* adam_state = nullptr;    // [0] live, [1] snapshot (step counter on device)
   // pinned readback
@@ -127,7 +128,7 @@ struct isg_ctx {
   bool frame_unchecked = false;  // frames launched since the last overflow check
 
   // stats
-  int64_t n_keys = 0, n_visible = 0, regrow = 0, launches = 0;
+  int64_t n_keys = 0, n_visible = 0, regrow = 0, launches = 0, overflowed_frames = 0;
 
   // snapshot of (scene, Adam moments, step) for reject-and-retry optimisation
   float4* snap = nullptr;  // ms | co | m (2n) | v (2n)
@@ -227,6 +228,11 @@ cudaError_t realloc_dev(isg_ctx* ctx, T** p, size_t count, bool graph_visible = 
   return cudaMalloc((void**)p, sizeof(T) * count);
 }
 
+// initial key capacity for a scene of n splats (grown on overflow up to kMaxItems)
+int64_t default_key_cap(int64_t n) {
+  return std::min<int64_t>(std::max<int64_t>(6 * n, 1 << 20), isg::kMaxItems);
+}
+
 int bits_for(int64_t v) {  // bits needed to represent values in [0, v)
   int b = 1;
   while (b < 32 && (int64_t(1) << b) < v) ++b;
@@ -240,6 +246,7 @@ isg_status ensure_scene(isg_ctx* ctx, int64_t n) {
   ISG_CUDA(realloc_dev(ctx, &ctx->co, a));
   ISG_CUDA(realloc_dev(ctx, &ctx->m, 2 * a));
   ISG_CUDA(realloc_dev(ctx, &ctx->v, 2 * a));
+  ISG_CUDA(realloc_dev(ctx, &ctx->raw, a));
   ISG_CUDA(realloc_dev(ctx, &ctx->rec, a));
   ISG_CUDA(realloc_dev(ctx, &ctx->ntiles, a));
   ISG_CUDA(realloc_dev(ctx, &ctx->slot_off, a));
@@ -415,7 +422,7 @@ isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out) {
   if ((s = ensure_pixels(ctx, fp.cam.width, fp.cam.height)) != ISG_OK) return s;
   if (!out) out = ctx->img;
   if (ctx->key_cap == 0) {
-    if ((s = ensure_keys(ctx, std::max<int64_t>(6 * ctx->n, 1 << 20))) != ISG_OK) return s;
+    if ((s = ensure_keys(ctx, default_key_cap(ctx->n))) != ISG_OK) return s;
   }
   if ((s = ensure_arena(ctx)) != ISG_OK) return s;
   const bool radix = ctx->binning == isg::kBinRadix;
@@ -532,7 +539,7 @@ isg_status check_frame(isg_ctx* ctx, bool* overflow, bool with_loss = false) {
   *overflow = false;
   ISG_CUDA(cudaMemcpyAsync(ctx->h_sc, ctx->sc, sizeof(uint32_t) * 8, cudaMemcpyDeviceToHost,
                            ctx->stream));
-  ISG_CUDA(cudaMemcpyAsync(ctx->h_total, ctx->total, sizeof(unsigned long long) * 2,
+  ISG_CUDA(cudaMemcpyAsync(ctx->h_total, ctx->total, sizeof(unsigned long long) * isg::kTotalWords,
                            cudaMemcpyDeviceToHost, ctx->stream));
   if (with_loss)
     ISG_CUDA(cudaMemcpyAsync(ctx->h_loss, ctx->loss, sizeof(double) * 4, cudaMemcpyDeviceToHost,
@@ -548,14 +555,40 @@ isg_status check_frame(isg_ctx* ctx, bool* overflow, bool with_loss = false) {
     ISG_CUDA(cudaMemcpy(c, ctx->co + bad, sizeof c, cudaMemcpyDeviceToHost));
     return fail(ctx, ISG_E_DOMAIN, splat_message(a, c));
   }
-  if (ctx->n_keys > ctx->key_cap) {
+  // the sticky record covers every frame since the last check, not only the last one
+  const unsigned long long need =
+      std::max<unsigned long long>(ctx->h_total[isg::kTotalOverflowMax], ctx->h_total[isg::kTotalKeys]);
+  if (ctx->h_total[isg::kTotalOverflowFrames] != 0 || need > (unsigned long long)ctx->key_cap) {
     *overflow = true;
-    const int64_t want = ctx->n_keys + ctx->n_keys / 4 + 1024;
-    if (want > (int64_t)0xFFFFFFF0ll)
-      return fail(ctx, ISG_E_OVERFLOW, "binning: more than 2^32 (tile, splat) pairs");
-    isg_status s = ensure_keys(ctx, want);
-    if (s != ISG_OK) return s;
-    ctx->regrow++;  // the frame arena follows the new capacity at the next launch
+    ctx->overflowed_frames += (int64_t)ctx->h_total[isg::kTotalOverflowFrames];
+    ISG_CUDA(cudaMemsetAsync(ctx->total + isg::kTotalOverflowMax, 0, sizeof(unsigned long long) * 2,
+                             ctx->stream));
+    const int64_t want = (int64_t)need + (int64_t)need / 4 + 1024;
+    if (want > isg::kMaxItems)
+      return fail(ctx, ISG_E_OVERFLOW, "binning: more than 2^30 (tile, splat) pairs");
+    if (want > ctx->key_cap) {
+      isg_status s = ensure_keys(ctx, want);
+      if (s != ISG_OK) return s;
+      ctx->regrow++;  // the frame arena follows the new capacity at the next launch
+    }
+  }
+  return ISG_OK;
+}
+
+// A host-synchronous entry point first settles the asynchronous frames issued since the last
+// check (isg_*_device calls, graph replays): if one of them overflowed the key capacity it was
+// skipped, along with any Adam step that followed it, and the caller must re-run them.
+isg_status check_async(isg_ctx* ctx) {
+  if (!ctx->frame_unchecked) return ISG_OK;
+  bool ov = false;
+  isg_status s = check_frame(ctx, &ov);
+  if (s != ISG_OK) return s;
+  if (ov) {
+    ctx->pending = false;  // a skipped view left no gradient slots to project
+    return fail(ctx, ISG_E_OVERFLOW,
+                "tile-key capacity was exceeded by an asynchronous frame; it was skipped (with "
+                "the Adam step after it) and capacity has been grown -- re-run the frames issued "
+                "since the last synchronisation");
   }
   return ISG_OK;
 }
@@ -676,15 +709,16 @@ isg_status isg_create(int device, int64_t max_gaussians, int32_t max_width, int3
   chk(cudaEventCreateWithFlags(&ctx->ev_main, cudaEventDisableTiming));
   chk(cudaEventCreateWithFlags(&ctx->ev_copy, cudaEventDisableTiming));
   // sc[0..7] followed by total[0..1] (one allocation: the per-frame part is zeroed at once)
-  chk(cudaMalloc(&ctx->sc, sizeof(uint32_t) * 8 + sizeof(unsigned long long) * 2));
+  chk(cudaMalloc(&ctx->sc, sizeof(uint32_t) * 8 + sizeof(unsigned long long) * isg::kTotalWords));
   if (s == ISG_OK) ctx->total = reinterpret_cast<unsigned long long*>(ctx->sc + 8);
   chk(cudaMalloc(&ctx->loss, sizeof(double) * 4));
   chk(cudaMalloc(&ctx->adam_state, sizeof(isg::AdamState) * 2));
   chk(cudaMallocHost(&ctx->h_sc, sizeof(uint32_t) * 8));
-  chk(cudaMallocHost(&ctx->h_total, sizeof(unsigned long long) * 2));
+  chk(cudaMallocHost(&ctx->h_total, sizeof(unsigned long long) * isg::kTotalWords));
   chk(cudaMallocHost(&ctx->h_loss, sizeof(double) * 4));
   if (s == ISG_OK) {
-    chk(cudaMemset(ctx->total, 0, sizeof(unsigned long long) * 2));
+    chk(cudaMemset(ctx->total, 0, sizeof(unsigned long long) * isg::kTotalWords));
+    std::memset(ctx->h_total, 0, sizeof(unsigned long long) * isg::kTotalWords);
     chk(cudaMemset(ctx->loss, 0, sizeof(double) * 4));
     chk(cudaMemset(ctx->adam_state, 0, sizeof(isg::AdamState) * 2));
   }
@@ -705,7 +739,7 @@ void isg_destroy(isg_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->nccl_comm) isg_nccl_detach(ctx);
-  void* dev[] = {ctx->ms, ctx->co, ctx->m, ctx->v, ctx->rec, ctx->ntiles, ctx->slot_off, ctx->tilebox,
+  void* dev[] = {ctx->ms, ctx->co, ctx->m, ctx->v, ctx->raw, ctx->rec, ctx->ntiles, ctx->slot_off, ctx->tilebox,
                  ctx->grad3d, ctx->depth[0], ctx->depth[1], ctx->order[0], ctx->order[1],
                  ctx->sorted, ctx->partial, ctx->bucket, ctx->slot_of, ctx->tkey[0], ctx->tkey[1],
                  ctx->tval[0], ctx->tval[1], ctx->emit_gid, ctx->sort.hist, ctx->sort.lookback,
@@ -754,16 +788,7 @@ isg_status isg_synchronize(isg_ctx* ctx) {
   if (!ctx) return ISG_E_ARG;
   ISG_NO_CAPTURE("isg_synchronize");
   cudaSetDevice(ctx->device);
-  if (ctx->frame_unchecked) {
-    bool ov = false;
-    isg_status s = check_frame(ctx, &ov);
-    if (s != ISG_OK) return s;
-    if (ov)
-      return fail(ctx, ISG_E_OVERFLOW,
-                  "tile-key capacity was exceeded by an asynchronous frame; capacity has been "
-                  "grown — re-run the frames issued since the last synchronisation");
-    return ISG_OK;
-  }
+  if (ctx->frame_unchecked) return check_async(ctx);
   ISG_CUDA(cudaStreamSynchronize(ctx->stream));
   return ISG_OK;
 }
@@ -779,6 +804,7 @@ isg_status isg_get_stats(const isg_ctx* ctx, isg_stats* out) {
   out->skipped_updates = ctx->h_total ? (int64_t)ctx->h_total[1] : 0;
   out->regrow_events = ctx->regrow;
   out->kernel_launches = ctx->launches;
+  out->overflowed_frames = ctx->overflowed_frames;
   return ISG_OK;
 }
 
@@ -786,7 +812,7 @@ static isg_status set_scene_impl(isg_ctx* ctx, int64_t n, const float* ms, const
                                  cudaMemcpyKind kind) {
   if (!ctx) return ISG_E_ARG;
   if (kind == cudaMemcpyHostToDevice) ISG_NO_CAPTURE("isg_set_scene");
-  if (n < 0 || n > 0xFFFFFFF0ll) return fail(ctx, ISG_E_ARG, "set_scene: bad splat count");
+  if (n < 0 || n > isg::kMaxItems) return fail(ctx, ISG_E_ARG, "set_scene: bad splat count (> 2^30)");
   if (n > 0 && (!ms || !co)) return fail(ctx, ISG_E_ARG, "set_scene: null pointer");
   cudaSetDevice(ctx->device);
   isg_status s = ensure_scene(ctx, n);
@@ -796,11 +822,18 @@ static isg_status set_scene_impl(isg_ctx* ctx, int64_t n, const float* ms, const
     ISG_CUDA(cudaMemcpyAsync(ctx->co, co, sizeof(float4) * n, kind, ctx->stream));
     ISG_CUDA(cudaMemsetAsync(ctx->m, 0, sizeof(float4) * 2 * n, ctx->stream));
     ISG_CUDA(cudaMemsetAsync(ctx->v, 0, sizeof(float4) * 2 * n, ctx->stream));
+    isg::launch_raw_init(ctx->ms, ctx->co, n, ctx->raw, ctx->stream);
+    ISG_CHECK_LAUNCH();
+    ctx->launches++;
   }
+  // frames of the previous scene are void: their overflow record with them
+  ISG_CUDA(cudaMemsetAsync(ctx->total + isg::kTotalOverflowMax, 0, sizeof(unsigned long long) * 2,
+                           ctx->stream));
+  ctx->frame_unchecked = false;
   if (ctx->n != n || ctx->key_cap < 4 * n) {
     // size the key buffers for the new scene on the next frame
-    if (ctx->key_cap < std::max<int64_t>(6 * n, 1 << 20)) {
-      s = ensure_keys(ctx, std::max<int64_t>(6 * n, 1 << 20));
+    if (ctx->key_cap < default_key_cap(n)) {
+      s = ensure_keys(ctx, default_key_cap(n));
       if (s != ISG_OK) return s;
     }
   }
@@ -856,6 +889,7 @@ isg_status isg_render(isg_ctx* ctx, const isg_camera* cam, const float bg[3], fl
   cudaSetDevice(ctx->device);
   isg_status s = validate_camera(ctx, cam);
   if (s != ISG_OK) return s;
+  if ((s = check_async(ctx)) != ISG_OK) return s;
   const FrameParams fp = make_fp(cam, bg, t_min);
   for (int attempt = 0; attempt < 3; ++attempt) {
     if ((s = launch_frame(ctx, fp, nullptr)) != ISG_OK) return s;
@@ -896,6 +930,7 @@ isg_status isg_loss_backward(isg_ctx* ctx, const isg_camera* cam, const float bg
   isg_status s = validate_camera(ctx, cam);
   if (s != ISG_OK) return s;
   if ((s = check_loss_size(ctx, cam->width, cam->height)) != ISG_OK) return s;
+  if ((s = check_async(ctx)) != ISG_OK) return s;
   if ((s = ensure_pixels(ctx, cam->width, cam->height)) != ISG_OK) return s;
   const FrameParams fp = make_fp(cam, bg, t_min);
   // The target upload runs on the copy stream, overlapped with binning and the forward blend;
@@ -982,10 +1017,10 @@ isg_status isg_adam_step(isg_ctx* ctx, const float lr[4], float b1, float b2, fl
   if (ctx->pending && !ctx->grad3d_valid && !ctx->nccl_comm) {
     // single view since the last step: projection backward fused with Adam (K8)
     ISG_STAGE(ST_PROJECT_ADAM);
-    isg::launch_adam_tick(lr, b1, b2, eps, ctx->adam_state, ctx->loss, ctx->stream);
+    isg::launch_adam_tick(lr, b1, b2, eps, ctx->adam_state, ctx->loss, ctx->total, ctx->stream);
     isg::launch_project_adam(ctx->ms, ctx->co, ctx->n, ctx->pending_fp, ctx->slot_off,
-                             slot_list(ctx), ctx->ntiles, ctx->partial, ctx->total, ctx->key_cap,
-                             ctx->m, ctx->v, ctx->adam_state, ctx->total + 1, ctx->stream);
+                             slot_list(ctx), ctx->ntiles, ctx->partial, ctx->total, ctx->raw,
+                             ctx->m, ctx->v, ctx->adam_state, ctx->stream);
     ISG_CHECK_LAUNCH();
     ctx->launches += 2;
     ctx->pending = false;
@@ -998,9 +1033,9 @@ isg_status isg_adam_step(isg_ctx* ctx, const float lr[4], float b1, float b2, fl
       if (s != ISG_OK) return s;
     }
     ISG_STAGE(ST_ADAM);
-    isg::launch_adam_tick(lr, b1, b2, eps, ctx->adam_state, ctx->loss, ctx->stream);
-    isg::launch_adam(ctx->ms, ctx->co, ctx->n, ctx->grad3d, ctx->m, ctx->v, ctx->adam_state,
-                     ctx->total + 1, ctx->stream);
+    isg::launch_adam_tick(lr, b1, b2, eps, ctx->adam_state, ctx->loss, ctx->total, ctx->stream);
+    isg::launch_adam(ctx->ms, ctx->co, ctx->n, ctx->grad3d, ctx->raw, ctx->m, ctx->v,
+                     ctx->adam_state, ctx->total, ctx->stream);
     ISG_CHECK_LAUNCH();
     ctx->launches += 2;
   }
@@ -1037,6 +1072,7 @@ isg_status isg_eval_loss(isg_ctx* ctx, const isg_camera* cam, const float bg[3],
   isg_status s = validate_camera(ctx, cam);
   if (s != ISG_OK) return s;
   if ((s = check_loss_size(ctx, cam->width, cam->height)) != ISG_OK) return s;
+  if ((s = check_async(ctx)) != ISG_OK) return s;
   const FrameParams fp = make_fp(cam, bg, t_min);
   const int W = cam->width, H = cam->height;
   if (ctx->loss_kind == ISG_LOSS_L1_DSSIM && (s = ensure_image_loss(ctx, W, H)) != ISG_OK) return s;
@@ -1068,7 +1104,8 @@ isg_status isg_snapshot(isg_ctx* ctx) {
   if (!ctx) return ISG_E_ARG;
   cudaSetDevice(ctx->device);
   if (ctx->snap_n < ctx->n) {
-    ISG_CUDA(realloc_dev(ctx, &ctx->snap, 6 * std::max<int64_t>(ctx->n, 1), false));
+    // ms | co | m (2n) | v (2n) | raw (n float2 = n/2 float4)
+    ISG_CUDA(realloc_dev(ctx, &ctx->snap, 7 * std::max<int64_t>(ctx->n, 1), false));
     ctx->snap_n = ctx->n;
   }
   const size_t n = (size_t)ctx->n;
@@ -1077,6 +1114,7 @@ isg_status isg_snapshot(isg_ctx* ctx) {
     ISG_CUDA(cudaMemcpyAsync(ctx->snap + n, ctx->co, sizeof(float4) * n, cudaMemcpyDeviceToDevice, ctx->stream));
     ISG_CUDA(cudaMemcpyAsync(ctx->snap + 2 * n, ctx->m, sizeof(float4) * 2 * n, cudaMemcpyDeviceToDevice, ctx->stream));
     ISG_CUDA(cudaMemcpyAsync(ctx->snap + 4 * n, ctx->v, sizeof(float4) * 2 * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    ISG_CUDA(cudaMemcpyAsync(ctx->snap + 6 * n, ctx->raw, sizeof(float2) * n, cudaMemcpyDeviceToDevice, ctx->stream));
   }
   ISG_CUDA(cudaMemcpyAsync(ctx->adam_state + 1, ctx->adam_state, sizeof(isg::AdamState),
                            cudaMemcpyDeviceToDevice, ctx->stream));
@@ -1096,6 +1134,7 @@ isg_status isg_restore(isg_ctx* ctx) {
     ISG_CUDA(cudaMemcpyAsync(ctx->co, ctx->snap + n, sizeof(float4) * n, cudaMemcpyDeviceToDevice, ctx->stream));
     ISG_CUDA(cudaMemcpyAsync(ctx->m, ctx->snap + 2 * n, sizeof(float4) * 2 * n, cudaMemcpyDeviceToDevice, ctx->stream));
     ISG_CUDA(cudaMemcpyAsync(ctx->v, ctx->snap + 4 * n, sizeof(float4) * 2 * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    ISG_CUDA(cudaMemcpyAsync(ctx->raw, ctx->snap + 6 * n, sizeof(float2) * n, cudaMemcpyDeviceToDevice, ctx->stream));
   }
   ISG_CUDA(cudaMemcpyAsync(ctx->adam_state, ctx->adam_state + 1, sizeof(isg::AdamState),
                            cudaMemcpyDeviceToDevice, ctx->stream));
@@ -1119,7 +1158,7 @@ isg_status isg_adaptive_control(isg_ctx* ctx, const isg_adapt_params* prm, uint6
   if (s != ISG_OK) return s;
   const int64_t n = ctx->n;
   const int64_t cap = prm->max_particles > 0 ? prm->max_particles : 2 * n;
-  if (cap > 0xFFFFFFF0ll) return fail(ctx, ISG_E_ARG, "max_particles: too large");
+  if (cap > isg::kMaxItems) return fail(ctx, ISG_E_ARG, "max_particles: too large (> 2^30)");
   // grow the scene buffers (preserving the splats) so the appended split children fit
   if (cap > ctx->n_alloc) {
     float4 *ms_keep = nullptr, *co_keep = nullptr;
@@ -1155,6 +1194,8 @@ isg_status isg_adaptive_control(isg_ctx* ctx, const isg_adapt_params* prm, uint6
   if (ctx->n > 0) {
     ISG_CUDA(cudaMemsetAsync(ctx->m, 0, sizeof(float4) * 2 * ctx->n, ctx->stream));
     ISG_CUDA(cudaMemsetAsync(ctx->v, 0, sizeof(float4) * 2 * ctx->n, ctx->stream));
+    isg::launch_raw_init(ctx->ms, ctx->co, ctx->n, ctx->raw, ctx->stream);
+    ctx->launches++;
   }
   ctx->adam_t = 0;
   ISG_CUDA(cudaMemsetAsync(ctx->adam_state, 0, sizeof(isg::AdamState), ctx->stream));
@@ -1164,8 +1205,8 @@ isg_status isg_adaptive_control(isg_ctx* ctx, const isg_adapt_params* prm, uint6
   ctx->have_frame = false;
   ISG_CUDA(cudaMemsetAsync(ctx->loss, 0, sizeof(double) * 2, ctx->stream));
   ISG_CUDA(cudaStreamSynchronize(ctx->stream));
-  if (ctx->key_cap < std::max<int64_t>(6 * ctx->n, 1 << 20)) {
-    if ((s = ensure_keys(ctx, std::max<int64_t>(6 * ctx->n, 1 << 20))) != ISG_OK) return s;
+  if (ctx->key_cap < default_key_cap(ctx->n)) {
+    if ((s = ensure_keys(ctx, default_key_cap(ctx->n))) != ISG_OK) return s;
   }
   if (out) {
     out->n_before = c.n_before;

@@ -29,6 +29,20 @@ constexpr float kNearPlane = 1e-3f;  // splat3d.hpp:55
 
 enum BinningMode { kBinTileBucket = 0, kBinRadix = 1 };
 
+// Device counters `total[kTotalWords]` (u64).  The frame reset zeroes only kTotalKeys; the
+// overflow record is sticky until the host's next check (capi.cu check_frame), so a skipped
+// frame is never lost behind later frames, and every Adam kernel refuses to step while it is
+// set (no update from a partial view batch).
+enum TotalWord {
+  kTotalKeys = 0,            // (tile, splat) pairs of the current frame
+  kTotalSkipped = 1,         // Adam updates skipped for non-finite gradients (cumulative)
+  kTotalOverflowMax = 2,     // max pairs needed by an overflowed frame since the last check
+  kTotalOverflowFrames = 3,  // frames skipped for overflow since the last check
+  kTotalWords = 4
+};
+// Largest key capacity / scene size: the onesweep look-back status words hold 30-bit counts.
+constexpr int64_t kMaxItems = int64_t(1) << 30;
+
 // ---- per-frame constant parameters --------------------------------------------------------
 struct FrameParams {
   isg_camera cam;
@@ -131,7 +145,7 @@ void launch_ranges_fix(const uint32_t* n_keys, int64_t key_cap, int n_tiles, uin
 // ---- blending (k_blend.cu) ----------------------------------------------------------------
 // sorted: per list entry (splat, gradient slot), tile-major, (depth, index) order per tile.
 void launch_blend_fwd(const FrameParams& fp, const uint2* ranges, const uint2* sorted,
-                      const RenderRec* rec, const unsigned long long* total, int64_t key_cap,
+                      const RenderRec* rec, unsigned long long* total, int64_t key_cap,
                       float* out, float* t_last, uint32_t* n_proc, cudaStream_t st);
 // Writes every pair's 2D gradient to partial[2 slot], partial[2 slot + 1].
 // given_dldc: `target` is dL/dC (G = loss_scale * target) and tile_loss is not meaningful;
@@ -180,8 +194,12 @@ struct AdamState {
 
 // t += 1, bias corrections of step t into st->p; moves the step's accumulated loss
 // (loss[0]) to loss[2] and restarts the accumulator.
+// A no-op (no tick) while total[kTotalOverflowMax] is set.
 void launch_adam_tick(const float lr[4], float b1, float b2, float eps, AdamState* st_dev,
-                      double* loss, cudaStream_t st);
+                      double* loss, const unsigned long long* total, cudaStream_t st);
+// Optimizer-space state raw[i] = (log sigma, logit clamp(opacity)) of the splats as set.
+constexpr float kOpacityEps = 1e-6f;
+void launch_raw_init(const float4* ms, const float4* co, int64_t n, float2* raw, cudaStream_t st);
 
 // Splat g's slots: slot_of[slot_off[g] + k] (or slot_off[g] + k when slot_of is null).
 // K8a: 2D grads of one view -> 3D grads (overwrite when `first`, else accumulate).
@@ -194,11 +212,11 @@ void launch_project_backward(const float4* ms, int64_t n, const FrameParams& fp,
 void launch_project_adam(float4* ms, float4* co, int64_t n, const FrameParams& fp,
                          const uint32_t* slot_off, const uint32_t* slot_of,
                          const uint32_t* ntiles, const float4* partial,
-                         const unsigned long long* total, int64_t cap, float4* m, float4* v,
-                         const AdamState* ap, unsigned long long* skipped, cudaStream_t st);
+                         unsigned long long* total, float2* raw, float4* m, float4* v,
+                         const AdamState* ap, cudaStream_t st);
 // K8b: Adam from accumulated 3D grads.
-void launch_adam(float4* ms, float4* co, int64_t n, const float4* grad3d, float4* m, float4* v,
-                 const AdamState* ap, unsigned long long* skipped, cudaStream_t st);
+void launch_adam(float4* ms, float4* co, int64_t n, const float4* grad3d, float2* raw, float4* m,
+                 float4* v, const AdamState* ap, unsigned long long* total, cudaStream_t st);
 
 // ---- adaptive control (k_adapt.cu) ----------------------------------------------------------
 struct AdaptParamsDev {

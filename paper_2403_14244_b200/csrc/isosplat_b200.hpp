@@ -158,7 +158,9 @@ inline Vector3d composite(std::span<const std::pair<Vector3d, double>> front_to_
 struct RenderOptions {
   Vector3d background{0.0, 0.0, 0.0};
   int threads = 1;       // accepted for source compatibility; the GPU ignores it
-  double t_min = 1e-5;   // early termination on transmittance (0 = exact reference semantics)
+  // early termination on transmittance: the default 0 is the reference's semantics (every
+  // covering splat composited, splat3d.cpp:134-141); training opts in (e.g. 1e-5)
+  double t_min = 0.0;
 };
 
 // image.hpp:11-31: row-major, interleaved channels, FP64

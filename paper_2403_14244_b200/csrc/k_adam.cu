@@ -74,9 +74,16 @@ __device__ __forceinline__ void grad3d_of(const float4 ms, const isg_camera& cam
   out[7] = a.w;
 }
 
+// Optimizer space (torch.optim.Adam on the parameters (mu, log sigma, rgb, logit opacity)):
+// log sigma and logit opacity live in `raw` (float2 per splat) and persist across steps, so
+// sigma = exp(raw.x) and opacity = sigmoid(raw.y) are never re-derived from the rendered
+// values (no log/exp round-trip drift; an opacity of exactly 0 or 1 is entered into the open
+// interval once, by k_raw_init).  A parameter whose update is exactly zero keeps its stored
+// value bit for bit (a zero-gradient step from zero moments is a no-op).
 __device__ __forceinline__ void adam_update(float4* __restrict__ ms, float4* __restrict__ co,
-                                            float4* __restrict__ m, float4* __restrict__ v,
-                                            int64_t i, const float gr[8], const AdamParams& ap,
+                                            float2* __restrict__ raw, float4* __restrict__ m,
+                                            float4* __restrict__ v, int64_t i, const float gr[8],
+                                            const AdamParams& ap,
                                             unsigned long long* skipped) {
   bool ok = true;
 #pragma unroll
@@ -86,10 +93,12 @@ __device__ __forceinline__ void adam_update(float4* __restrict__ ms, float4* __r
     return;
   }
   float4 P0 = ms[i], P1 = co[i];
-  const float sigma = P0.w, op = P1.w;
-  float p[8] = {P0.x, P0.y, P0.z, logf(sigma), P1.x, P1.y, P1.z, logf(op) - log1pf(-op)};
+  const float2 R = raw[i];
+  const float sigma = P0.w;
+  const float s = 1.0f / (1.0f + expf(-R.y));  // sigmoid(logit) of the optimizer state
+  float p[8] = {P0.x, P0.y, P0.z, R.x, P1.x, P1.y, P1.z, R.y};
   const float g[8] = {gr[0], gr[1], gr[2], gr[3] * sigma,
-                      gr[4], gr[5], gr[6], gr[7] * op * (1.0f - op)};
+                      gr[4], gr[5], gr[6], gr[7] * s * (1.0f - s)};
   float4 M0 = m[2 * i], M1 = m[2 * i + 1], V0 = v[2 * i], V1 = v[2 * i + 1];
   float mm[8] = {M0.x, M0.y, M0.z, M0.w, M1.x, M1.y, M1.z, M1.w};
   float vv[8] = {V0.x, V0.y, V0.z, V0.w, V1.x, V1.y, V1.z, V1.w};
@@ -99,22 +108,31 @@ __device__ __forceinline__ void adam_update(float4* __restrict__ ms, float4* __r
     mm[j] = mm[j] + (1.0f - ap.b1) * (g[j] - mm[j]);
     vv[j] = ap.b2 * vv[j] + (1.0f - ap.b2) * g[j] * g[j];
     const float denom = sqrtf(vv[j]) / ap.bc2_sqrt + ap.eps;
-    p[j] = p[j] - ap.step_size[group[j]] * (mm[j] / denom);
+    // m == 0 moves nothing (also with eps == 0 and v == 0, where m / denom would be 0 / 0)
+    const float upd = mm[j] == 0.0f ? 0.0f : mm[j] / denom;
+    p[j] = p[j] - ap.step_size[group[j]] * upd;
   }
   m[2 * i] = make_float4(mm[0], mm[1], mm[2], mm[3]);
   m[2 * i + 1] = make_float4(mm[4], mm[5], mm[6], mm[7]);
   v[2 * i] = make_float4(vv[0], vv[1], vv[2], vv[3]);
   v[2 * i + 1] = make_float4(vv[4], vv[5], vv[6], vv[7]);
-  ms[i] = make_float4(p[0], p[1], p[2], expf(p[3]));
-  co[i] = make_float4(p[4], p[5], p[6], 1.0f / (1.0f + expf(-p[7])));
+  raw[i] = make_float2(p[3], p[7]);
+  ms[i] = make_float4(p[0], p[1], p[2], p[3] == R.x ? sigma : expf(p[3]));
+  co[i] = make_float4(p[4], p[5], p[6], p[7] == R.y ? P1.w : 1.0f / (1.0f + expf(-p[7])));
 }
 
 }  // namespace
 
 // One thread: step counter, bias corrections (torch.optim.Adam: step_size = lr / (1 - b1^t),
 // denominator sqrt(v) / sqrt(1 - b2^t) + eps) and the loss hand-over of the step.
-__global__ void k_adam_tick(AdamParams in, AdamState* __restrict__ st, double* __restrict__ loss) {
+__global__ void k_adam_tick(AdamParams in, AdamState* __restrict__ st, double* __restrict__ loss,
+                            const unsigned long long* __restrict__ total) {
   pdl_enter();
+  loss[2] = loss[0];
+  loss[0] = 0.0;
+  // a view of this step was skipped (key-capacity overflow): the whole step is a no-op, the
+  // host reports it at its next check and the caller re-runs the step
+  if (total[kTotalOverflowMax] != 0ull) return;
   const long long t = st->t + 1;
   st->t = t;
   const double bc1 = 1.0 - pow((double)in.b1, (double)t);
@@ -123,8 +141,17 @@ __global__ void k_adam_tick(AdamParams in, AdamState* __restrict__ st, double* _
   for (int i = 0; i < 4; ++i) p.step_size[i] = (float)((double)in.lr[i] / bc1);
   p.bc2_sqrt = (float)sqrt(bc2);
   st->p = p;
-  loss[2] = loss[0];
-  loss[0] = 0.0;
+}
+
+// Optimizer state of freshly set splats: raw = (log sigma, logit opacity), the opacity taken
+// into [kOpacityEps, 1 - kOpacityEps] first (logit(0) and logit(1) are infinite).
+__global__ void __launch_bounds__(256) k_raw_init(const float4* __restrict__ ms,
+                                                  const float4* __restrict__ co, int64_t n,
+                                                  float2* __restrict__ raw) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float op = fminf(fmaxf(co[i].w, kOpacityEps), 1.0f - kOpacityEps);
+  raw[i] = make_float2(logf(ms[i].w), logf(op) - log1pf(-op));
 }
 
 __global__ void __launch_bounds__(256) k_project_backward(
@@ -162,32 +189,34 @@ __global__ void ISG_ADAM_BOUNDS k_project_adam(
     float4* __restrict__ ms, float4* __restrict__ co, int64_t n, FrameParams fp,
     const uint32_t* __restrict__ slot_off, const uint32_t* __restrict__ slot_of,
     const uint32_t* __restrict__ ntiles, const float4* __restrict__ partial,
-    const unsigned long long* __restrict__ total, int64_t cap, float4* __restrict__ m,
-    float4* __restrict__ v, const AdamState* __restrict__ state,
-    unsigned long long* __restrict__ skipped) {
+    unsigned long long* __restrict__ total, float2* __restrict__ raw, float4* __restrict__ m,
+    float4* __restrict__ v, const AdamState* __restrict__ state) {
   pdl_enter();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  if (*total > (unsigned long long)cap) return;  // overflowed frame: no update (host re-runs)
+  // an overflowed frame since the last host check: no update (the host re-runs the step)
+  if (total[kTotalOverflowMax] != 0ull) return;
   const AdamParams ap = state->p;
   float4 a, b;
   sum_slots(partial, slot_of, slot_off[i], ntiles[i], a, b);
   float o[8];
   grad3d_of(ms[i], fp.cam, a, b, o);
-  adam_update(ms, co, m, v, i, o, ap, skipped);
+  adam_update(ms, co, raw, m, v, i, o, ap, total + kTotalSkipped);
 }
 
 __global__ void __launch_bounds__(256) k_adam(float4* __restrict__ ms, float4* __restrict__ co,
                                               int64_t n, const float4* __restrict__ grad3d,
-                                              float4* __restrict__ m, float4* __restrict__ v,
+                                              float2* __restrict__ raw, float4* __restrict__ m,
+                                              float4* __restrict__ v,
                                               const AdamState* __restrict__ state,
-                                              unsigned long long* __restrict__ skipped) {
+                                              unsigned long long* __restrict__ total) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  if (total[kTotalOverflowMax] != 0ull) return;  // a view of the step was skipped
   const AdamParams ap = state->p;
   const float4 g0 = grad3d[2 * i], g1 = grad3d[2 * i + 1];
   const float o[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-  adam_update(ms, co, m, v, i, o, ap, skipped);
+  adam_update(ms, co, raw, m, v, i, o, ap, total + kTotalSkipped);
 }
 
 void launch_project_backward(const float4* ms, int64_t n, const FrameParams& fp,
@@ -203,27 +232,32 @@ void launch_project_backward(const float4* ms, int64_t n, const FrameParams& fp,
 void launch_project_adam(float4* ms, float4* co, int64_t n, const FrameParams& fp,
                          const uint32_t* slot_off, const uint32_t* slot_of,
                          const uint32_t* ntiles, const float4* partial,
-                         const unsigned long long* total, int64_t cap, float4* m, float4* v,
-                         const AdamState* ap, unsigned long long* skipped, cudaStream_t st) {
+                         unsigned long long* total, float2* raw, float4* m, float4* v,
+                         const AdamState* ap, cudaStream_t st) {
   if (n <= 0) return;
   launch_pdl(k_project_adam, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, ms, co, n,
-             fp, slot_off, slot_of, ntiles, partial, total, cap, m, v, ap, skipped);
+             fp, slot_off, slot_of, ntiles, partial, total, raw, m, v, ap);
 }
 
-void launch_adam(float4* ms, float4* co, int64_t n, const float4* grad3d, float4* m, float4* v,
-                 const AdamState* ap, unsigned long long* skipped, cudaStream_t st) {
+void launch_adam(float4* ms, float4* co, int64_t n, const float4* grad3d, float2* raw, float4* m,
+                 float4* v, const AdamState* ap, unsigned long long* total, cudaStream_t st) {
   if (n <= 0) return;
-  k_adam<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ms, co, n, grad3d, m, v, ap, skipped);
+  k_adam<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ms, co, n, grad3d, raw, m, v, ap, total);
+}
+
+void launch_raw_init(const float4* ms, const float4* co, int64_t n, float2* raw, cudaStream_t st) {
+  if (n <= 0) return;
+  k_raw_init<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ms, co, n, raw);
 }
 
 void launch_adam_tick(const float lr[4], float b1, float b2, float eps, AdamState* st_dev,
-                      double* loss, cudaStream_t st) {
+                      double* loss, const unsigned long long* total, cudaStream_t st) {
   AdamParams in{};
   for (int i = 0; i < 4; ++i) in.lr[i] = lr[i];
   in.b1 = b1;
   in.b2 = b2;
   in.eps = eps;
-  launch_pdl(k_adam_tick, dim3(1), dim3(1), 0, st, in, st_dev, loss);
+  launch_pdl(k_adam_tick, dim3(1), dim3(1), 0, st, in, st_dev, loss, total);
 }
 
 }  // namespace isg

@@ -78,7 +78,7 @@ __device__ __forceinline__ void fwd_pair(FwdPair& p, float2 r2, const float4 g, 
 
 __global__ void ISG_FWD_BOUNDS k_blend_fwd(
     FrameParams fp, const uint2* __restrict__ ranges, const uint2* __restrict__ sorted,
-    const RenderRec* __restrict__ rec, const unsigned long long* __restrict__ total,
+    const RenderRec* __restrict__ rec, unsigned long long* __restrict__ total,
     int64_t key_cap, float* __restrict__ out, float* __restrict__ t_last,
     uint32_t* __restrict__ n_proc) {
   // entry kBatch of each stage is a sentinel no pixel is inside (r2max = -1): the groups'
@@ -86,7 +86,12 @@ __global__ void ISG_FWD_BOUNDS k_blend_fwd(
   __shared__ Stage<kBatch + 1> st[2];
   __shared__ uint8_t s_list[16][kListPitch];
   pdl_enter();
-  if (overflowed(total, key_cap)) return;
+  if (overflowed(total, key_cap)) {
+    // sticky record for the host's next check (survives later frames' resets): the largest
+    // key count any frame since then needed, and how many frames were skipped
+    if (blockIdx.x == 0 && threadIdx.x == 0) note_overflow(total);
+    return;
+  }
   if (threadIdx.x < 2) {
     st[threadIdx.x].geo[kBatch] = make_float4(0.0f, 0.0f, -1.0f, 0.0f);
     st[threadIdx.x].col[kBatch] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
@@ -282,7 +287,7 @@ void launch_count_pairs(const FrameParams& fp, const uint2* ranges, const uint2*
 }
 
 void launch_blend_fwd(const FrameParams& fp, const uint2* ranges, const uint2* sorted,
-                      const RenderRec* rec, const unsigned long long* total, int64_t key_cap,
+                      const RenderRec* rec, unsigned long long* total, int64_t key_cap,
                       float* out, float* t_last, uint32_t* n_proc, cudaStream_t st) {
   launch_pdl(k_blend_fwd, dim3(fp.n_tiles), dim3(kBT), 0, st, fp, ranges, sorted, rec, total,
              key_cap, out, t_last, n_proc);

@@ -54,7 +54,7 @@ class AdaptResultT(C.Structure):
 class StatsT(C.Structure):
     _fields_ = [(n, C.c_int64) for n in ("n_gaussians", "n_visible", "n_keys", "key_capacity",
                                          "n_tiles", "adam_steps", "skipped_updates",
-                                         "regrow_events", "kernel_launches")]
+                                         "regrow_events", "kernel_launches", "overflowed_frames")]
 
 
 _lib = None
@@ -200,11 +200,13 @@ class Camera:
 
 @dataclass
 class RenderOptions:
-    """RenderOptions (splat3d.hpp:87-90) + t_min, the early-termination threshold (0 = the
-    reference's exact semantics).  `threads` is accepted for API parity and ignored."""
+    """RenderOptions (splat3d.hpp:87-90) + t_min, the early-termination threshold.  The default
+    0 is the reference's exact semantics (every covering splat composited, splat3d.cpp:134-141);
+    training configs opt in to early termination (e.g. 1e-5).  `threads` is accepted for API
+    parity and ignored."""
     background: tuple = (0.0, 0.0, 0.0)
     threads: int = 1
-    t_min: float = 1e-5
+    t_min: float = 0.0
 
 
 @dataclass

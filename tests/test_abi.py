@@ -33,7 +33,7 @@ def test_header_declarations_are_exported():
 
 def test_library_loads_and_reports_version():
     L = isg.lib()
-    assert L.isg_abi_version() == 1
+    assert L.isg_abi_version() == 2
     assert L.isg_status_string(1) == b"domain error"
 
 

@@ -27,6 +27,7 @@ class OracleFitBackend:
 
     def __init__(self, ms, co, cams, targets, cfg: FitConfig3D):
         self.ms, self.co = ms.copy(), co.copy()
+        self.raw = O.raw_init32(self.ms, self.co)
         self.m = np.zeros((ms.shape[0], 8), np.float32)
         self.v = np.zeros_like(self.m)
         self.g = np.zeros_like(self.m)
@@ -68,17 +69,18 @@ class OracleFitBackend:
               a.lr_opacity * rate_scale]
         self.t += 1
         self.skipped += O.adam32(self.ms, self.co, self.m, self.v, self.g, self.t, lr,
-                                 a.beta1, a.beta2, a.eps)
+                                 a.beta1, a.beta2, a.eps, raw=self.raw)
         self.g[:] = 0
         loss, self.loss = self.loss, 0.0
         return loss
 
     def snapshot(self):
-        self.snap = (self.ms.copy(), self.co.copy(), self.m.copy(), self.v.copy(), self.t)
+        self.snap = (self.ms.copy(), self.co.copy(), self.m.copy(), self.v.copy(),
+                     self.raw.copy(), self.t)
 
     def restore(self):
-        ms, co, m, v, self.t = self.snap
-        self.ms[:], self.co[:], self.m[:], self.v[:] = ms, co, m, v
+        ms, co, m, v, raw, self.t = self.snap
+        self.ms[:], self.co[:], self.m[:], self.v[:], self.raw[:] = ms, co, m, v, raw
 
     def skipped_updates(self):
         return self.skipped
@@ -91,6 +93,7 @@ class OracleFitBackend:
             dims=3, seed=seed, round_=round_)
         self.ms = np.ascontiguousarray(out[:, :4], np.float32)
         self.co = np.ascontiguousarray(out[:, 4:], np.float32)
+        self.raw = O.raw_init32(self.ms, self.co)
         self.m = np.zeros((self.ms.shape[0], 8), np.float32)
         self.v = np.zeros_like(self.m)
         self.g = np.zeros_like(self.m)
@@ -266,7 +269,7 @@ def test_gpu_eval_loss_keeps_pending_grads_and_restore():
     be.loss_backward(0, 0.5)
     g0 = be.r.grads().copy()
     l1 = be.eval_loss(1, 0.5)
-    lo, _ = O.loss_backward32(ms, co, cams[1], targets[1], weight=0.5)
+    lo, _ = O.loss_backward32(ms, co, cams[1], targets[1], t_min=cfg.t_min, weight=0.5)
     assert l1 == pytest.approx(lo, rel=1e-5)
     np.testing.assert_array_equal(be.r.grads(), g0)
     be.snapshot()

@@ -15,6 +15,7 @@ from paper_2403_14244_b200 import isg
 pytestmark = pytest.mark.gpu
 
 IMG_TOL = 1e-4
+T_MIN = 1e-5  # the training configs' early-termination threshold (full-size cases)
 GRAD_TOL = 1e-3
 GROUPS = {"mu": slice(0, 3), "sigma": slice(3, 4), "rgb": slice(4, 7), "opacity": slice(7, 8)}
 
@@ -223,11 +224,12 @@ def test_adam_matches_oracle_given_grads(rend):
     oms, oco = ms.copy(), co.copy()
     m = np.zeros((3000, 8), np.float32)
     v = np.zeros((3000, 8), np.float32)
+    raw = O.raw_init32(oms, oco)  # persistent optimizer-space (log sigma, logit opacity)
     for step in range(1, 4):
         rend.loss_backward(cam, target)
         g = rend.grads()
         rend.adam_step(cfg)
-        O.adam32(oms, oco, m, v, g, step, lrs, cfg.beta1, cfg.beta2, cfg.eps)
+        O.adam32(oms, oco, m, v, g, step, lrs, cfg.beta1, cfg.beta2, cfg.eps, raw=raw)
         gms, gco = rend.get_scene()
         assert np.abs(gms - oms).max() <= 1e-5
         assert np.abs(gco - oco).max() <= 1e-5
@@ -294,6 +296,52 @@ def test_key_capacity_regrow():
         assert np.abs(img - O.render32(ms, co, cam)).max() <= IMG_TOL
 
 
+def test_async_overflow_of_an_earlier_view_is_reported():
+    """Two asynchronous views, the FIRST overflowing the key capacity, then Adam: the step is
+    skipped as a whole (no update from the partial batch), the next synchronisation reports the
+    overflow once (sticky device record, not only the last frame's count), capacity has grown,
+    and the re-run step matches two synchronous views + Adam."""
+    import torch
+    W, H = 512, 512
+    rng = np.random.default_rng(3)
+    ms, co, cam_near = random_scene(rng, 2000, W, H, sigma2d=(60.0, 200.0))
+    cam_far = isg.Camera(np.eye(3), np.array([0.0, 0.0, 60.0]), cam_near.focal,
+                         (W / 2, H / 2), W, H)  # the same splats ~10x smaller: few keys
+    tms, tco, _ = random_scene(rng, 2000, W, H, sigma2d=(60.0, 200.0))
+    targets = [torch.from_numpy(O.render32(tms, tco, c)).cuda() for c in (cam_near, cam_far)]
+    torch.cuda.synchronize()
+    cams = (cam_near, cam_far)
+    with isg.Renderer(0) as r:
+        r.set_scene(ms, co)
+        cap0 = r.stats()["key_capacity"]
+        for c, t in zip(cams, targets):
+            r.loss_backward_device(c, t.data_ptr(), weight=0.5)
+        r.adam_step()
+        with pytest.raises(isg.IsgError) as ei:
+            r.synchronize()
+        assert ei.value.status == 5  # ISG_E_OVERFLOW
+        st = r.stats()
+        assert st["overflowed_frames"] == 1 and st["key_capacity"] > cap0
+        m1, c1 = r.get_scene()
+        np.testing.assert_array_equal(m1, ms)  # the step did not move anything
+        np.testing.assert_array_equal(c1, co)
+        r.synchronize()  # reported once
+        for c, t in zip(cams, targets):
+            r.loss_backward_device(c, t.data_ptr(), weight=0.5)
+        r.adam_step()
+        r.synchronize()
+        a_ms, a_co = r.get_scene()
+        assert r.stats()["adam_steps"] >= 1
+    with isg.Renderer(0) as r:
+        r.set_scene(ms, co)
+        for c, t in zip(cams, targets):
+            r.loss_backward(c, t.cpu().numpy(), weight=0.5)
+        r.adam_step()
+        b_ms, b_co = r.get_scene()
+    np.testing.assert_array_equal(a_ms, b_ms)
+    np.testing.assert_array_equal(a_co, b_co)
+
+
 def test_render_deterministic(rend):
     W, H = 256, 256
     ms, co = isg.synth_scene(10000, W, H)
@@ -311,10 +359,10 @@ def test_full_size_c2_render_parity():
     cam = isg.Camera.synthetic(W, H)
     with isg.Renderer(0) as r:
         r.set_scene(ms, co)
-        img = r.render(cam)
+        img = r.render(cam, isg.RenderOptions(t_min=T_MIN))
         keys = check_bins(r, ms, co, cam)
         assert np.all(np.diff(keys.astype(np.int64) >> 32) >= 0)
-        assert np.abs(img - O.render32(ms, co, cam)).max() <= IMG_TOL
+        assert np.abs(img - O.render32(ms, co, cam, t_min=T_MIN)).max() <= IMG_TOL
 
 
 def test_full_size_c3_loss_backward():
@@ -324,12 +372,12 @@ def test_full_size_c3_loss_backward():
     ms, co = isg.synth_scene(n, W, H, seed=1)
     tms, tco = isg.synth_scene(n, W, H, seed=2)
     cam = isg.Camera.synthetic(W, H)
-    target = O.render32(tms, tco, cam)
+    target = O.render32(tms, tco, cam, t_min=T_MIN)
     with isg.Renderer(0) as r:
         r.set_scene(ms, co)
-        loss = r.loss_backward(cam, target)
+        loss = r.loss_backward(cam, target, isg.RenderOptions(t_min=T_MIN))
         g = r.grads()
-    loss_ref, g_ref = O.loss_backward32(ms, co, cam, target)
+    loss_ref, g_ref = O.loss_backward32(ms, co, cam, target, t_min=T_MIN)
     assert abs(loss - loss_ref) <= 1e-6 * abs(loss_ref)
     _grad_check(g, g_ref)
 
@@ -344,13 +392,13 @@ def test_full_size_c5_bins_and_gradients():
     cam = isg.Camera.synthetic(W, H)
     with isg.Renderer(0) as r:
         r.set_scene(tms, tco)
-        target = r.render(cam)
+        target = r.render(cam, isg.RenderOptions(t_min=T_MIN))
         r.set_scene(ms, co)
-        loss = r.loss_backward(cam, target)
+        loss = r.loss_backward(cam, target, isg.RenderOptions(t_min=T_MIN))
         g = r.grads()
         keys = check_bins(r, ms, co, cam)
         assert len(keys) > 30_000_000
-    loss_ref, g_ref = O.loss_backward32(ms, co, cam, target)
+    loss_ref, g_ref = O.loss_backward32(ms, co, cam, target, t_min=T_MIN)
     assert abs(loss - loss_ref) <= 1e-6 * abs(loss_ref)
     _grad_check(g, g_ref)
 
@@ -584,8 +632,8 @@ def test_degenerate_image_shapes(rend, W, H):
 
 def test_all_splats_culled(rend):
     """Every splat behind the near plane: no keys, background image, zero gradients, and the
-    Adam step leaves the (gradient-free) scene unchanged (up to the log-sigma / logit-opacity
-    round trip)."""
+    Adam step leaves the (gradient-free) scene bitwise unchanged (optimizer-space state is
+    persistent; a zero update rewrites nothing)."""
     W, H = 96, 64
     rng = np.random.default_rng(8)
     ms, co, cam = random_scene(rng, 500, W, H)
@@ -598,12 +646,45 @@ def test_all_splats_culled(rend):
     target = rng.uniform(0, 1, (H, W, 3)).astype(np.float32)
     rend.loss_backward(cam, target)
     assert np.all(rend.grads() == 0)
-    rend.adam_step(isg.AdamConfig())
+    rend.adam_step(isg.AdamConfig(eps=0.0))  # eps 0: m == 0 must still move nothing
     m2, c2 = rend.get_scene()
-    np.testing.assert_array_equal(m2[:, :3], ms[:, :3])
-    np.testing.assert_array_equal(c2[:, :3], co[:, :3])
-    np.testing.assert_allclose(m2[:, 3], ms[:, 3], rtol=1e-6)
-    np.testing.assert_allclose(c2[:, 3], co[:, 3], rtol=1e-5)
+    np.testing.assert_array_equal(m2, ms)
+    np.testing.assert_array_equal(c2, co)
+
+
+def test_adam_opacity_at_interval_ends(rend):
+    """Opacity exactly 0 or 1 (IsoSplat3D::validate allows both, splat3d.cpp:14-16) enters the
+    optimizer's open interval once: the splat trains (finite logit, non-zero gradient factor)
+    instead of freezing, and matches the oracle's optimizer-space Adam."""
+    W, H = 64, 48
+    rng = np.random.default_rng(17)
+    ms, co, cam = random_scene(rng, 400, W, H)
+    co[::3, 3] = 1.0
+    co[1::3, 3] = 0.0
+    tms, tco, _ = random_scene(rng, 400, W, H)
+    target = O.render32(tms, tco, cam)
+    cfg = isg.AdamConfig(lr_mu=1e-3, lr_sigma=5e-3, lr_color=1e-2, lr_opacity=5e-2)
+    lrs = [cfg.lr_mu, cfg.lr_sigma, cfg.lr_color, cfg.lr_opacity]
+    rend.set_scene(ms, co)
+    oms, oco = ms.copy(), co.copy()
+    m = np.zeros((400, 8), np.float32)
+    v = np.zeros((400, 8), np.float32)
+    raw = O.raw_init32(oms, oco)
+    assert np.all(np.isfinite(raw))
+    for step in range(1, 4):
+        rend.loss_backward(cam, target)
+        g = rend.grads()
+        rend.adam_step(cfg)
+        O.adam32(oms, oco, m, v, g, step, lrs, cfg.beta1, cfg.beta2, cfg.eps, raw=raw)
+    gms, gco = rend.get_scene()
+    assert np.all(np.isfinite(gms)) and np.all(np.isfinite(gco))
+    np.testing.assert_allclose(gco, oco, atol=1e-5)
+    np.testing.assert_allclose(gms, oms, atol=1e-5)
+    covered = np.abs(g[:, 7]) > 0
+    moved = gco[:, 3] != co[:, 3]
+    # splats that started at exactly 0 or 1 and see a gradient move
+    ends = (co[:, 3] == 0.0) | (co[:, 3] == 1.0)
+    assert np.all(moved[ends & covered])
 
 
 def test_graph_replay_refused_after_reallocation():

@@ -28,6 +28,7 @@ class OracleBackend:
 
     def __init__(self, ms, co, cams, targets, world):
         self.ms, self.co = ms.copy(), co.copy()
+        self.raw = O.raw_init32(self.ms, self.co)
         self.m = np.zeros((ms.shape[0], 8), np.float32)
         self.v = np.zeros_like(self.m)
         self.g = np.zeros_like(self.m)
@@ -48,7 +49,8 @@ class OracleBackend:
             dist.all_reduce(lt)
             self.loss = float(lt.item())
         self.t += 1
-        O.adam32(self.ms, self.co, self.m, self.v, self.g, self.t, LR, 0.9, 0.999, 1e-15)
+        O.adam32(self.ms, self.co, self.m, self.v, self.g, self.t, LR, 0.9, 0.999, 1e-15,
+                 raw=self.raw)
         self.g[:] = 0
         loss, self.loss = self.loss, 0.0
         return loss

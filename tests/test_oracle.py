@@ -231,6 +231,7 @@ def test_adam_matches_torch():
     m = np.zeros((n, 8), np.float32)
     v = np.zeros((n, 8), np.float32)
     oms, oco = ms.copy(), co.copy()
+    raw = O.raw_init32(oms, oco)
     for step in range(1, 6):
         g = rng.normal(size=(n, 8)).astype(np.float32)  # dL/d(mu, sigma, rgb, opacity)
         sig = torch.exp(p_ls.detach())
@@ -240,8 +241,10 @@ def test_adam_matches_torch():
         p_c.grad = torch.tensor(g[:, 4:7])
         p_lo.grad = torch.tensor(g[:, 7]) * op * (1 - op)
         opt.step()
-        O.adam32(oms, oco, m, v, g, step, lr, b1, b2, eps)
+        O.adam32(oms, oco, m, v, g, step, lr, b1, b2, eps, raw=raw)
         assert np.allclose(oms[:, :3], p_mu.detach().numpy(), atol=2e-6)
+        assert np.allclose(raw[:, 0], p_ls.detach().numpy(), atol=2e-6)
+        assert np.allclose(raw[:, 1], p_lo.detach().numpy(), atol=2e-6)
         assert np.allclose(np.log(oms[:, 3]), p_ls.detach().numpy(), atol=2e-6)
         assert np.allclose(oco[:, :3], p_c.detach().numpy(), atol=2e-6)
         assert np.allclose(oco[:, 3], torch.sigmoid(p_lo.detach()).numpy(), atol=2e-6)
@@ -281,3 +284,25 @@ def test_reference_composite_and_errors():
     bad[1, 3] = -1.0
     with pytest.raises(ValueError, match="IsoSplat3D.sigma"):
         O.ref_render(bad, CAM32)
+
+
+# ---- the synthetic workload, restated in the oracle ------------------------------------------
+@pytest.mark.parametrize("n,W,H,seed", [(1000, 256, 256, 2403), (5000, 1920, 1080, 14244),
+                                        (777, 3840, 2160, 5)])
+def test_oracle_synth_scene_byte_equal_to_product(n, W, H, seed):
+    """bench.py's CPU arms build the isg-synth v1 scene and cameras from the oracle alone (no
+    libisg in that process); they must be the product's bytes (isg_synth_scene is host code,
+    callable without a GPU)."""
+    from paper_2403_14244_b200 import isg
+
+    ms, co = O.synth_scene(n, W, H, seed)
+    ms2, co2 = isg.synth_scene(n, W, H, seed)
+    assert ms.tobytes() == ms2.tobytes() and co.tobytes() == co2.tobytes()
+    for views in (1, 8):
+        for k in range(views):
+            a = O.synth_camera(W, H, k, views)
+            b = isg.Camera.synthetic(W, H, k, views)
+            assert np.array_equal(a.rotation, b.rotation)
+            assert np.array_equal(a.translation, b.translation)
+            assert (a.focal, a.principal_point, a.width, a.height) == \
+                (b.focal, b.principal_point, b.width, b.height)
