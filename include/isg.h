@@ -206,10 +206,25 @@ isg_status isg_graph_launch(isg_ctx* ctx, isg_graph* graph);
 void isg_graph_destroy(isg_graph* graph);
 
 /* ---- multi-GPU (one process per GPU, views sharded, NCCL all-reduce before Adam) -------- */
-/* NCCL is resolved at run time (dlopen libnccl.so.2, the copy torch already loaded if any). */
+/* NCCL is resolved at run time (dlopen libnccl.so.2, the copy torch already loaded if any).
+ * Once a communicator is attached, isg_adam_step sums the n x 8 gradient buffer over ranks
+ * (ncclAllReduce, in place) and every rank applies the identical Adam step, so replicas stay
+ * bitwise identical.  The exchange is pipelined over splat chunks on a second stream (the
+ * all-reduce of chunk c overlaps the projection backward of chunk c+1 and the Adam update of
+ * chunk c-1); the step loss and every rank's key-overflow flag travel in front of chunk 0, so
+ * a step is one all-reduce per chunk, and a view that overflowed on any rank skips the step
+ * on every rank.  At most 64 ranks. */
 isg_status isg_nccl_get_unique_id(void* out_128_bytes);
+/* Create and own a communicator (ncclCommInitRank); destroyed by isg_nccl_detach. */
 isg_status isg_nccl_init(isg_ctx* ctx, int nranks, int rank, const void* unique_id_128_bytes);
-/* Once attached, isg_adam_step all-reduces (sum) the gradient buffer and the loss first. */
+/* Use a caller-owned ncclComm_t (passed as void*); rank and size are read from it.  The
+ * caller keeps ownership: isg_nccl_detach / isg_destroy do not destroy it. */
+isg_status isg_nccl_attach(isg_ctx* ctx, void* nccl_comm);
+/* Size and rank as the attached communicator reports them (1, 0 without one), and the
+ * loaded NCCL's version code (0 if NCCL is not loadable); any pointer may be NULL. */
+isg_status isg_nccl_info(isg_ctx* ctx, int* nranks, int* rank, int* nccl_version);
+/* Pipeline depth of the exchange, 1..8 chunks (default 4; chunks are >= 128K splats). */
+isg_status isg_set_exchange_chunks(isg_ctx* ctx, int chunks);
 isg_status isg_nccl_detach(isg_ctx* ctx);
 
 /* ---- parity hooks ---------------------------------------------------------------------- */

@@ -207,7 +207,15 @@ void launch_project_backward(const float4* ms, int64_t n, const FrameParams& fp,
                              const uint32_t* slot_off, const uint32_t* slot_of,
                              const uint32_t* ntiles, const float4* partial,
                              const unsigned long long* total, int64_t cap, float4* grad3d,
-                             bool first, cudaStream_t st);
+                             bool first, cudaStream_t st, int64_t begin = 0, int64_t end = -1);
+// Multi-GPU exchange slots (kMaxRanks float4 ahead of the gradient buffer): pack this rank's
+// step loss (exact double as three floats) and overflow flag; unpack after the all-reduce.
+constexpr int kMaxRanks = 64;
+constexpr int kMaxExchangeChunks = 8;  // pipelined all-reduce chunks (isg_set_exchange_chunks)
+void launch_loss_pack(const double* loss, const unsigned long long* total, float4* slots,
+                      int rank, int nranks, cudaStream_t st);
+void launch_loss_unpack(double* loss, unsigned long long* total, const float4* slots, int nranks,
+                        cudaStream_t st);
 // K8 fused: 2D grads of one view -> 3D -> Adam.
 void launch_project_adam(float4* ms, float4* co, int64_t n, const FrameParams& fp,
                          const uint32_t* slot_off, const uint32_t* slot_of,

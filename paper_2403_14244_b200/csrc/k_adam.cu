@@ -159,8 +159,8 @@ __global__ void __launch_bounds__(256) k_project_backward(
     const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ ntiles,
     const float4* __restrict__ partial,
     const unsigned long long* __restrict__ total, int64_t cap, float4* __restrict__ grad3d,
-    bool first) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool first, int64_t begin) {
+  const int64_t i = begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const bool ov = *total > (unsigned long long)cap;  // frame was skipped: contributes nothing
   float4 a, b;
@@ -223,10 +223,60 @@ void launch_project_backward(const float4* ms, int64_t n, const FrameParams& fp,
                              const uint32_t* slot_off, const uint32_t* slot_of,
                              const uint32_t* ntiles, const float4* partial,
                              const unsigned long long* total, int64_t cap, float4* grad3d,
-                             bool first, cudaStream_t st) {
-  if (n <= 0) return;
-  k_project_backward<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
-      ms, n, fp, slot_off, slot_of, ntiles, partial, total, cap, grad3d, first);
+                             bool first, cudaStream_t st, int64_t begin, int64_t end) {
+  if (end < 0 || end > n) end = n;
+  if (end <= begin) return;
+  k_project_backward<<<(unsigned)((end - begin + 255) / 256), 256, 0, st>>>(
+      ms, end, fp, slot_off, slot_of, ntiles, partial, total, cap, grad3d, first, begin);
+}
+
+// ---- multi-GPU exchange: the step's loss and overflow state ride in the gradient all-reduce --
+// slots[r] = (hi, mid, lo, overflowed) for rank r, zero for every other rank: after the sum
+// every rank holds every rank's values unchanged (x + 0 = x), and hi + mid + lo reconstructs
+// the rank's double loss exactly (24 + 24 + <= 5 significant bits).
+__global__ void k_loss_pack(const double* __restrict__ loss,
+                            const unsigned long long* __restrict__ total, float4* __restrict__ slots,
+                            int rank, int nranks) {
+  const int r = threadIdx.x;
+  if (r >= nranks) return;
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (r == rank) {
+    const double L = loss[0];
+    const float hi = (float)L;
+    const double r1 = L - (double)hi;
+    const float mid = (float)r1;
+    s = make_float4(hi, mid, (float)(r1 - (double)mid),
+                    total[kTotalOverflowMax] != 0ull ? 1.0f : 0.0f);
+  }
+  slots[r] = s;
+}
+
+// After the exchange: loss[0] = the sum of the ranks' losses in rank order (identical on every
+// rank; k_adam_tick hands it over to loss[2]); any rank's overflow makes every rank skip the
+// step (replicas stay identical), recorded like a local overflow for the host's next check.
+__global__ void k_loss_unpack(double* __restrict__ loss, unsigned long long* __restrict__ total,
+                              const float4* __restrict__ slots, int nranks) {
+  double sum = 0.0;
+  bool ovf = false;
+  for (int r = 0; r < nranks; ++r) {
+    const float4 s = slots[r];
+    sum += ((double)s.x + (double)s.y) + (double)s.z;
+    ovf |= s.w != 0.0f;
+  }
+  loss[0] = sum;
+  if (ovf && total[kTotalOverflowMax] == 0ull) {
+    total[kTotalOverflowMax] = total[kTotalKeys];
+    total[kTotalOverflowFrames] += 1ull;
+  }
+}
+
+void launch_loss_pack(const double* loss, const unsigned long long* total, float4* slots,
+                      int rank, int nranks, cudaStream_t st) {
+  k_loss_pack<<<1, 64, 0, st>>>(loss, total, slots, rank, nranks);
+}
+void launch_loss_unpack(double* loss, unsigned long long* total, const float4* slots, int nranks,
+                        cudaStream_t st) {
+  k_loss_unpack<<<1, 1, 0, st>>>(loss, total, slots, nranks);
 }
 
 void launch_project_adam(float4* ms, float4* co, int64_t n, const FrameParams& fp,

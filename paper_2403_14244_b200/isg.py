@@ -107,6 +107,9 @@ def lib() -> C.CDLL:
         "isg_nccl_get_unique_id": ([P], C.c_int),
         "isg_nccl_init": ([P, C.c_int, C.c_int, P], C.c_int),
         "isg_nccl_detach": ([P], C.c_int),
+        "isg_nccl_attach": ([P, P], C.c_int),
+        "isg_nccl_info": ([P, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
+        "isg_set_exchange_chunks": ([P, C.c_int], C.c_int),
         "isg_debug_bins": ([P, P, P, C.POINTER(I64), P], C.c_int),
         "isg_debug_pixel_state": ([P, P, P], C.c_int),
         "isg_count_pairs": ([P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)], C.c_int),
@@ -135,7 +138,7 @@ C_ABI_SYMBOLS = (
     "isg_grads_device", "isg_adam_step", "isg_last_step_loss", "isg_step_loss_async", "isg_eval_loss", "isg_snapshot",
     "isg_restore", "isg_set_loss", "isg_image_loss_device", "isg_adaptive_control",
     "isg_graph_begin", "isg_graph_end", "isg_graph_launch", "isg_graph_destroy", "isg_nccl_get_unique_id",
-    "isg_nccl_init",
+    "isg_nccl_init", "isg_nccl_attach", "isg_nccl_info", "isg_set_exchange_chunks",
     "isg_nccl_detach", "isg_debug_bins", "isg_debug_pixel_state", "isg_count_pairs", "isg_set_binning",
     "isg_profile_enable",
     "isg_profile_num_stages", "isg_profile_stage_name", "isg_profile_read", "isg_synth_scene",
@@ -506,6 +509,20 @@ class Renderer:
         _process_nccl()
         buf = (C.c_char * 128).from_buffer_copy(uid)
         _check(self._h, lib().isg_nccl_init(self._h, nranks, rank, buf))
+
+    def nccl_attach(self, comm_ptr: int):
+        """Use a caller-owned ncclComm_t (its address as an int); the caller keeps ownership."""
+        _process_nccl()
+        _check(self._h, lib().isg_nccl_attach(self._h, C.c_void_p(comm_ptr)))
+
+    def nccl_info(self) -> dict:
+        """{'nranks', 'rank'} as the attached communicator reports them, and the NCCL version."""
+        n, r, v = C.c_int(), C.c_int(), C.c_int()
+        _check(self._h, lib().isg_nccl_info(self._h, C.byref(n), C.byref(r), C.byref(v)))
+        return {"nranks": n.value, "rank": r.value, "nccl_version": v.value}
+
+    def set_exchange_chunks(self, chunks: int):
+        _check(self._h, lib().isg_set_exchange_chunks(self._h, int(chunks)))
 
     def nccl_detach(self):
         _check(self._h, lib().isg_nccl_detach(self._h))

@@ -573,6 +573,91 @@ def test_cuda_graph_with_nccl_single_rank():
     assert out[0][1] == out[1][1]
 
 
+@pytest.mark.parametrize("chunks,graph", [(1, False), (4, False), (8, True)])
+def test_pipelined_exchange_matches_local_step(chunks, graph):
+    """The chunked exchange (projection backward, all-reduce and Adam pipelined over splat
+    ranges on two streams; loss and overflow flags in front of chunk 0) on one rank at a size
+    where it really splits (600K splats, 4-8 chunks): scene bitwise equal to the fused local
+    step, and the folded loss equal to the local double loss exactly."""
+    import torch
+    W, H, n = 320, 240, 600_000
+    ms, co = isg.synth_scene(n, W, H, seed=51)
+    tms, tco = isg.synth_scene(n, W, H, seed=52)
+    cams = [isg.Camera.synthetic(W, H, k, 2) for k in range(2)]
+    targets = [torch.from_numpy(O.render32(tms, tco, c, t_min=T_MIN)).cuda() for c in cams]
+    torch.cuda.synchronize()
+    opts = isg.RenderOptions(t_min=T_MIN)
+    out = []
+    for use_nccl in (False, True):
+        r = isg.Renderer(0)
+        r.set_scene(ms, co)
+        if use_nccl:
+            r.nccl_init(1, 0, isg.Renderer.nccl_unique_id())
+            r.set_exchange_chunks(chunks)
+            assert r.nccl_info()["nranks"] == 1
+
+        def step():
+            for c, t in zip(cams, targets):
+                r.loss_backward_device(c, t.data_ptr(), opts, weight=0.5)
+            r.adam_step()
+        step()
+        losses = [r.last_step_loss()]
+        if graph and use_nccl:
+            r.graph_begin()
+            step()
+            g = r.graph_end()
+            for _ in range(2):
+                g.launch()
+            g.close()
+        else:
+            for _ in range(2):
+                step()
+        losses.append(r.last_step_loss())
+        out.append((r.get_scene(), losses))
+        r.close()
+    (a, la), (b, lb) = out
+    np.testing.assert_array_equal(a[0], b[0])
+    np.testing.assert_array_equal(a[1], b[1])
+    assert la == lb
+
+
+def test_nccl_attach_caller_owned_communicator():
+    """isg_nccl_attach uses a communicator the caller created (here ncclCommInitRank called
+    directly through ctypes) and leaves it alive: the caller destroys it after the detach."""
+    import ctypes as C
+    import torch  # noqa: F401  (loads torch's libnccl.so.2, the copy libisg binds to)
+    nccl = C.CDLL("libnccl.so.2", mode=C.RTLD_GLOBAL)
+    W, H, n = 96, 64, 2000
+    ms, co = isg.synth_scene(n, W, H, seed=41)
+    tms, tco = isg.synth_scene(n, W, H, seed=42)
+    cam = isg.Camera.synthetic(W, H)
+    target = O.render32(tms, tco, cam)
+    out = []
+    for attach in (False, True):
+        with isg.Renderer(0) as r:
+            r.set_scene(ms, co)
+            comm = C.c_void_p()
+            if attach:
+                class UniqueId(C.Structure):  # ncclUniqueId is passed by value
+                    _fields_ = [("internal", C.c_char * 128)]
+                uid = UniqueId.from_buffer_copy(isg.Renderer.nccl_unique_id())
+                assert nccl.ncclCommInitRank(C.byref(comm), 1, uid, 0) == 0
+                r.nccl_attach(comm.value)
+                info = r.nccl_info()
+                assert info["nranks"] == 1 and info["rank"] == 0 and info["nccl_version"] > 0
+            for _ in range(2):
+                r.loss_backward(cam, target)
+                r.adam_step()
+            out.append(r.get_scene())
+            if attach:
+                r.nccl_detach()
+                assert r.nccl_info()["nranks"] == 1
+                # still alive: the caller's destroy succeeds exactly once
+                assert nccl.ncclCommDestroy(comm) == 0
+    np.testing.assert_array_equal(out[0][0], out[1][0])
+    np.testing.assert_array_equal(out[0][1], out[1][1])
+
+
 def test_step_loss_async_in_graph_matches_sync_read():
     """isg_step_loss_async captured in a step graph (the pipelined loop's D2H of each step's
     loss) delivers the same value as the synchronous isg_last_step_loss."""
