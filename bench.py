@@ -4,11 +4,17 @@
 Default workload (config C3, BASELINE.json configs[2]): 1M isotropic Gaussians
 (isg-synth v1, seed 2403), one 1920x1080 view per GPU per step, forward + L2 loss + backward
 + Adam, target = render of the seed-14244 scene.  One "step" = one view per GPU + one Adam
-step on every replica (gradients all-reduced over NCCL when N > 1): weak scaling.
+step on every replica (gradients all-reduced over NCCL when N > 1): weak scaling.  The same
+line carries a `render` object: C2 render FPS (BASELINE metric's second half) of the same
+scene and camera, with its own e2e and the reference's own render() beside it.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3|c2|c4|c5]
-  python bench.py --impl reference ...   # CPU reference arm (oracle port, all host cores)
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1|c2|c3|c4|c5]
+  python bench.py --impl reference ...   # CPU reference arm (oracle only, all host cores)
   python bench.py --loss l1_dssim        # train with the paper's 0.8 L1 + 0.2 D-SSIM loss
+
+--gpus N > 1 without torchrun's environment re-launches itself under
+`python -m torch.distributed.run --nproc-per-node N` (one rank per GPU, NCCL); under torchrun
+WORLD_SIZE must equal --gpus.
 
 `value` is device-resident throughput (inputs in HBM before the timed region); `e2e` is the
 same metric through the C-ABI with host buffers (target H2D + loss D2H inside the timed
@@ -42,7 +48,43 @@ CONFIGS = {
     "c5": (10_000_000, 3840, 2160, 1, True, "synthetic 10M isotropic Gaussians, 4K fwd+bwd+Adam"),
 }
 T_MIN = 1e-5
-METRIC = "fwd+bwd train iters/sec (1M isotropic Gaussians, 1080p)"
+METRICS = {  # BASELINE.json's metric, named per workload
+    "c1": ("fwd+bwd train iters/sec (10K isotropic Gaussians, 256x256)", "iters/s"),
+    "c2": ("render FPS (1M isotropic Gaussians, 1080p)", "frames/s"),
+    "c3": ("fwd+bwd train iters/sec (1M isotropic Gaussians, 1080p)", "iters/s"),
+    "c4": ("fwd+bwd train iters/sec (3M isotropic Gaussians, 1080p, 8-view batch per iter)",
+           "iters/s"),
+    "c5": ("fwd+bwd train iters/sec (10M isotropic Gaussians, 4K)", "iters/s"),
+}
+RENDER_METRIC = METRICS["c2"][0]
+LR = [1e-3, 5e-3, 1e-2, 1e-2]  # AdamConfig defaults (lr_mu, lr_sigma, lr_color, lr_opacity)
+
+
+def workload(config: str, world: int):
+    """Per-step work of `config` on `world` GPUs: (views of one step in camera order, the
+    number of views each rank renders, iterations one step counts).  C4 is one 8-view batch
+    per step split over the ranks (strong scaling, 1 iteration per step); the other configs
+    give every rank one view per step (weak scaling, `world` iterations per step)."""
+    n, W, H, views_total, train, _ = CONFIGS[config]
+    if config == "c4":
+        per_rank = max(1, views_total // world)
+        return [(v, per_rank * world) for v in range(per_rank * world)], per_rank, 1
+    return [(r, world) for r in range(world)], 1, world
+
+
+def config_dict(args, world: int) -> dict:
+    """The `config` object of both arms' JSON lines (identical for the same arguments)."""
+    n, W, H, views_total, train, desc = CONFIGS[args.config]
+    views, per_rank, _ = workload(args.config, world)
+    flush = args.config == "c1"
+    return {"workload": desc, "config": args.config, "n_gaussians": n, "width": W, "height": H,
+            "views_per_step": len(views), "t_min": T_MIN,
+            "loss": "L2 (mse)" if args.loss == "l2" else "0.8 L1 + 0.2 D-SSIM",
+            "binning": args.binning,
+            "launch": "eager" if args.no_graph else "cuda_graph (one graph launch per step)",
+            "parallelism": f"dp{world} (views sharded, scene replicated)",
+            "l2": ("L2 flushed between steps (256 MB memset outside the timed intervals)" if flush
+                   else "no flush: the per-step working set exceeds the 126 MB L2")}
 
 # Algorithmic FP32 work per (pixel, list entry) pair, FLOPs (FMA = 2), see DESIGN.md §Roofline:
 FWD_FLOP_EVAL, FWD_FLOP_IN = 6, 12      # 3-sigma test; exp+alpha+composite+transmittance
@@ -177,19 +219,32 @@ class ClockSampler:
                 "samples": len(self.rows), "source": self.source}
 
 
-def cpu_oracle_train_step(ms, co, cam, target, steps=1, threads=0):
-    """CPU oracle (FP32 tiled restatement, oracle/isg_oracle.c) train step: forward + L2 +
-    backward + Adam, timed.  Returns seconds per step."""
-    import oracle as O
-    ms, co = ms.copy(), co.copy()
-    m = np.zeros((ms.shape[0], 8), np.float32)
-    v = np.zeros_like(m)
-    t0 = time.perf_counter()
-    raw = O.raw_init32(ms, co)
-    for s in range(1, steps + 1):
-        _, g = O.loss_backward32(ms, co, cam, target, t_min=T_MIN, threads=threads)
-        O.adam32(ms, co, m, v, g, s, [1e-3, 5e-3, 1e-2, 1e-2], 0.9, 0.999, 1e-15, raw=raw)
-    return (time.perf_counter() - t0) / steps
+class CpuTrainer:
+    """CPU oracle (FP32 tiled restatement, oracle/isg_oracle.c) train steps: every view of the
+    step forward + L2 + backward (weight 1/V), then Adam on (mu, log sigma, rgb, logit o) with
+    its persistent optimizer state -- the GPU step's algorithm, on the host's threads."""
+
+    def __init__(self, ms, co, cams, targets, threads=0):
+        import oracle as O
+        self.O = O
+        self.ms, self.co = ms.copy(), co.copy()
+        self.m = np.zeros((ms.shape[0], 8), np.float32)
+        self.v = np.zeros_like(self.m)
+        self.raw = O.raw_init32(self.ms, self.co)
+        self.cams, self.targets, self.threads, self.t = cams, targets, threads, 0
+
+    def step(self) -> float:
+        """One step; returns its seconds."""
+        t0 = time.perf_counter()
+        g = np.zeros((self.ms.shape[0], 8), np.float32)
+        w = 1.0 / len(self.cams)
+        for c, tg in zip(self.cams, self.targets):
+            self.O.loss_backward32(self.ms, self.co, c, tg, t_min=T_MIN, weight=w,
+                                   threads=self.threads, grads=g)
+        self.t += 1
+        self.O.adam32(self.ms, self.co, self.m, self.v, g, self.t, LR, 0.9, 0.999, 1e-15,
+                      raw=self.raw)
+        return time.perf_counter() - t0
 
 
 def reference_render_fps(ms, co, cam, cores):
@@ -205,15 +260,14 @@ def reference_render_fps(ms, co, cam, cores):
         O.ref_lib()
     except Exception:
         return None
-    from paper_2403_14244_b200 import isg
     sp = np.concatenate([ms, co], 1).astype(np.float64)
     W, H = cam.width, cam.height
     cx, cy = cam.principal_point
     rows = max(1, min(cores, H))
 
     def sub(w, h, x0, y0):
-        c = isg.Camera(np.asarray(cam.rotation), np.asarray(cam.translation), cam.focal,
-                       (cx - x0, cy - y0), w, h)
+        c = O.Camera(np.asarray(cam.rotation), np.asarray(cam.translation), cam.focal,
+                     (cx - x0, cy - y0), w, h)
         t0 = time.perf_counter()
         O.ref_render(sp, c, threads=cores)
         return time.perf_counter() - t0
@@ -235,60 +289,144 @@ def host_threads():
         return os.cpu_count() or 1
 
 
-# ------------------------------------------------------------------------------------------
+
+
+def reference_train_line(args, world):
+    """The CPU oracle's train steps on this run's workload (all of a step's views + Adam),
+    bounded to ~60 s of timed steps.  Returns (iters/s, sample, steps timed, s/step)."""
+    import oracle as O
+    n, W, H, _, _, _ = CONFIGS[args.config]
+    views, _, iters = workload(args.config, world)
+    ms, co = O.synth_scene(n, W, H, seed=2403)
+    tms, tco = O.synth_scene(n, W, H, seed=14244)
+    cams = [O.synth_camera(W, H, v, nv) for v, nv in views]
+    cores = host_threads()
+    targets = [O.render32(tms, tco, c, t_min=T_MIN, threads=cores) for c in cams]
+    tr = CpuTrainer(ms, co, cams, targets, threads=cores)
+    first = tr.step()  # warm-up step
+    steps = max(1, min(args.steps, int(60.0 / max(first, 1e-3))))
+    sec = float(np.median([tr.step() for _ in range(steps)]))
+    sample = (f"{steps} full {args.config.upper()} train steps ({len(views)} view(s) of "
+              f"fwd+L2+bwd, then Adam) of the FP32 tiled CPU oracle, median; the reference "
+              f"itself has no 3D backward (SPEC.md:484)")
+    return iters / sec, sample, steps, sec
+
+
 def run_reference(args):
+    """--impl reference: the CPU path on the host cores, rank 0 only, from the oracle alone
+    (oracle/ restates the synthetic workload; the product library is not loaded)."""
     rank, world, _ = env_rank()
     if rank != 0:
         return
-    from paper_2403_14244_b200 import isg  # host-side synth only (no device work)
-    n, W, H, views, train, desc = CONFIGS[args.config]
-    ms, co = isg.synth_scene(n, W, H, seed=2403)
-    tms, tco = isg.synth_scene(n, W, H, seed=14244)
-    cam = isg.Camera.synthetic(W, H)
     import oracle as O
+    n, W, H, _, train, _ = CONFIGS[args.config]
+    metric, unit = METRICS[args.config]
     cores = host_threads()
+    base = {"impl": "reference", "metric": metric, "unit": unit, "n_gpus": world,
+            "warmup": 1, "higher_is_better": True,
+            "scaling": "strong" if args.config == "c4" else "weak", "vs_baseline": None,
+            "data": "synthetic (isg-synth v1: scene seed 2403, target seed 14244; oracle restatement)",
+            "config": config_dict(args, world), "gpu_launches": 0}
+    ref_render = None
+    if n <= 1_000_000 and W * H <= 1920 * 1080:
+        # the reference's own render() (FP64, every pixel tests every splat), extrapolated
+        ms, co = O.synth_scene(n, W, H, seed=2403)
+        ref_render = reference_render_fps(ms, co, O.synth_camera(W, H), cores)
     if not train:
-        res = reference_render_fps(ms, co, cam, cores)
-        if res is not None:
-            fps, sample = res
-            line = {"impl": "reference", "metric": "render FPS (1M isotropic Gaussians, 1080p)",
-                    "value": fps, "unit": "frames/s", "n_gpus": world, "steps": 1, "warmup": 0,
-                    "ms_per_step": 1e3 / fps, "higher_is_better": True, "scaling": "weak",
-                    "vs_baseline": None, "dtype": "f64",
-                    "data": "synthetic (isg-synth v1, seed 2403)",
-                    "config": {"workload": desc, "n_gaussians": n, "width": W, "height": H},
-                    "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores,
-                                     "kind": "reference", "sample": sample},
-                    "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0,
-                            "d2h_bytes_per_step": 0}}
-            print(json.dumps(line), flush=True)
+        if ref_render is None:
+            print(json.dumps({"impl": "reference", "unavailable":
+                              "oracle/_ref (the reference's render) was not built"}), flush=True)
             return
-    target = O.render32(tms, tco, cam, t_min=T_MIN)
-    # bounded: at most one warm-up step and ~60 s of timed steps, so that the arm ends within
-    # a few minutes for any --steps (the line reports the steps actually timed)
-    first = cpu_oracle_train_step(ms, co, cam, target, 1, cores)  # the warm-up step
-    steps = max(1, min(args.steps, int(60.0 / max(first, 1e-3))))
-    times = [cpu_oracle_train_step(ms, co, cam, target, 1, cores) for _ in range(steps)]
-    sec = float(np.median(times))
-    val = 1.0 / sec
-    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "iters/s",
-            "n_gpus": world, "steps": steps, "steps_requested": args.steps, "warmup": 1,
-            "ms_per_step": sec * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (isg-synth v1, seeds 2403/14244)",
-            "config": {"workload": desc, "n_gaussians": n, "width": W, "height": H,
-                       "t_min": T_MIN},
-            "cpu_baseline": {"value": val, "unit": "iters/s", "cores": cores, "kind": "port",
-                             "sample": f"{steps} full {args.config.upper()} train steps "
-                                       "(fwd+L2+bwd+Adam) of the "
-                                       "FP32 tiled CPU oracle; the reference itself has no 3D "
-                                       "backward (SPEC.md:484)"},
-            "e2e": {"value": val, "unit": "iters/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+        fps, sample = ref_render
+        line = dict(base, value=fps * world, steps=1, ms_per_step=1e3 / fps, dtype="f64",
+                    cpu_baseline={"value": fps * world, "unit": unit, "cores": cores,
+                                  "kind": "reference", "sample": sample},
+                    e2e={"value": fps * world, "unit": unit, "h2d_bytes_per_step": 0,
+                         "d2h_bytes_per_step": 0})
+        print(json.dumps(line), flush=True)
+        return
+    val, sample, steps, sec = reference_train_line(args, world)
+    line = dict(base, value=val, steps=steps, steps_requested=args.steps, ms_per_step=sec * 1e3,
+                dtype="f32",
+                cpu_baseline={"value": val, "unit": unit, "cores": cores, "kind": "port",
+                              "sample": sample},
+                e2e={"value": val, "unit": unit, "h2d_bytes_per_step": 0,
+                     "d2h_bytes_per_step": 0})
+    if ref_render is not None and args.config == "c3":
+        line["render"] = {"metric": RENDER_METRIC, "value": ref_render[0], "unit": "frames/s",
+                          "cpu_baseline": {"value": ref_render[0], "unit": "frames/s",
+                                           "cores": cores, "kind": "reference",
+                                           "sample": ref_render[1]}}
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------------------------------
+def time_render(r, cam, opts, steps, warmup, stream, barrier, world):
+    """C2-style render timing on the resident scene: device-resident FPS (one graph launch
+    per frame, CUDA events) and end-to-end FPS (each frame's image copied to pinned host
+    memory on a copy stream while the next frames render; NB images in flight).  Returns a
+    dict."""
+    import torch
+    import torch.distributed as dist
+    W, H = cam.width, cam.height
+    NB = 3
+    bufs = [torch.empty((H, W, 3), dtype=torch.float32, device="cuda") for _ in range(NB)]
+    host = [torch.empty((H, W, 3), dtype=torch.float32).pin_memory() for _ in range(NB)]
+    r.render(cam, opts)  # sizes the buffers (untimed)
+    graphs = []
+    for b in range(NB):
+        r.graph_begin()
+        r.render_device(cam, opts, bufs[b].data_ptr())
+        graphs.append(r.graph_end())
+    for _ in range(max(warmup, 3)):
+        graphs[0].launch()
+    r.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    l0 = r.stats()["kernel_launches"]
+    barrier()
+    ev[0].record(stream)
+    for i in range(steps):
+        graphs[i % NB].launch()
+    ev[1].record(stream)
+    barrier()
+    r.synchronize()
+    launches = r.stats()["kernel_launches"] - l0
+    dev_ms = ev[0].elapsed_time(ev[1]) / steps
+    # end to end: frame i into device image i % NB, its D2H into pinned host image i % NB
+    copy_stream = torch.cuda.Stream()
+    ev_done = [torch.cuda.Event() for _ in range(NB)]
+    ev_read = [torch.cuda.Event() for _ in range(NB)]
+    barrier()
+    t0 = time.perf_counter()
+    for i in range(steps):
+        b = i % NB
+        if i >= NB:
+            ev_read[b].synchronize()  # frame i - NB is on the host: its buffers are free
+        graphs[b].launch()
+        ev_done[b].record(stream)
+        with torch.cuda.stream(copy_stream):
+            copy_stream.wait_event(ev_done[b])
+            host[b].copy_(bufs[b], non_blocking=True)
+            ev_read[b].record(copy_stream)
+    for e in ev_read:
+        e.synchronize()
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / steps
+    for g in graphs:
+        g.close()
+    r.synchronize()
+    if world > 1:
+        tt = torch.tensor([dev_ms, e2e_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dev_ms, e2e_ms = (float(x) for x in tt.tolist())
+    return {"metric": RENDER_METRIC, "value": world * 1e3 / dev_ms, "unit": "frames/s",
+            "ms_per_frame": dev_ms, "frames": steps, "gpu_launches": int(launches),
+            "e2e": {"value": world * 1e3 / e2e_ms, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": W * H * 3 * 4,
+                    "mode": f"cuda graph per frame into one of {NB} device images, each image "
+                            "copied to pinned host memory on a copy stream while the next "
+                            "frames render (every copy complete inside the timed region)"}}
+
+
 def run_isg(args):
     import torch
     import torch.distributed as dist
@@ -296,14 +434,16 @@ def run_isg(args):
     from paper_2403_14244_b200 import isg
 
     rank, world, local = env_rank()
-    if world != args.gpus:
-        args.gpus = world
     torch.cuda.set_device(local)
     if world > 1:
+        # NCCL's communicator lines (rank count, transport) on stdout for the driver to check
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n, W, H, views_total, train, desc = CONFIGS[args.config]
-    views_per_rank = max(1, views_total // world) if args.config == "c4" else 1
-    step_views = views_per_rank * world
+    metric, unit = METRICS[args.config]
+    views, per_rank, iters_per_step = workload(args.config, world)
+    step_views = len(views)
     # a real (non-legacy) stream: the context launches on it and the events below time it
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
@@ -318,10 +458,8 @@ def run_isg(args):
         r.set_binning(r.BINNING_TILE_BUCKET)
     opts = isg.RenderOptions(t_min=T_MIN)
     cfg = isg.AdamConfig()
-    my_views = [rank * views_per_rank + i for i in range(views_per_rank)]
-    n_views_cam = views_total if args.config == "c4" else max(world, 1)
-    cams = [isg.Camera.synthetic(W, H, v % n_views_cam, n_views_cam) for v in
-            (my_views if args.config == "c4" else [rank])]
+    my_views = views[rank * per_rank:(rank + 1) * per_rank]
+    cams = [isg.Camera.synthetic(W, H, v, nv) for v, nv in my_views]
     # targets: renders of the target scene, resident in HBM
     targets = []
     r.set_scene(tms, tco)
@@ -331,11 +469,24 @@ def run_isg(args):
         targets.append(t)
     r.synchronize()
     r.set_scene(ms, co)
+    nccl = None
+    p = torch.cuda.get_device_properties(local)
+    devices = [f"{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}"]
     if world > 1:
         uid = r.nccl_unique_id() if rank == 0 else b"\0" * 128
         obj = [uid]
         dist.broadcast_object_list(obj, src=0)
         r.nccl_init(world, rank, obj[0])
+        info = r.nccl_info()
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (info, devices[0]))
+        nccl = {"comm_nranks": [g[0]["nranks"] for g in gathered],
+                "comm_ranks": [g[0]["rank"] for g in gathered],
+                "nccl_version": info["nccl_version"],
+                "exchange": "pipelined chunked all-reduce (isg_adam_step)"}
+        devices = [g[1] for g in gathered]
+        if any(c != world for c in nccl["comm_nranks"]):
+            raise SystemExit(f"bench: NCCL communicator size {nccl['comm_nranks']} != {world}")
 
     def step():
         if train:
@@ -357,8 +508,8 @@ def run_isg(args):
     step_eager = step
     graph = None
     if not args.no_graph:
-        # the whole step (every view's frame + backward, the all-reduce, Adam) as one CUDA
-        # graph launch; a replay re-runs every kernel on the live buffers
+        # the whole step (every view's frame + backward, the exchange, Adam) as one CUDA graph
+        # launch; a replay re-runs every kernel on the live buffers
         r.graph_begin()
         step_eager()
         graph = r.graph_end()
@@ -379,8 +530,8 @@ def run_isg(args):
     # per-pixel images) exceeds the 126 MB L2 runs back to back.  A smaller one (C1) gets an
     # L2 flush (a 256 MB memset) between steps, outside the per-step event pairs.
     n_keys = r.stats()["n_keys"]
-    working_set = n * 96 + n_keys * 24 + W * H * (3 * 4 * 2 + 8)
-    flush = working_set < 126e6
+    working_set = n * 104 + n_keys * 24 + W * H * (3 * 4 * 2 + 8)
+    flush = args.config == "c1"
     flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if flush else None
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     ev_s = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)] if flush else None
@@ -406,16 +557,12 @@ def run_isg(args):
     else:
         step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
         total_ms = ev[0].elapsed_time(ev[-1])
-    l2_note = (f"L2 flushed between steps (256 MB memset outside the timed intervals): working "
-               f"set {working_set / 1e6:.0f} MB < 126 MB L2" if flush else
-               f"no flush: per-step working set {working_set / 1e6:.0f} MB (scene + Adam "
-               f"state, {n_keys / 1e6:.2f} M keys and pairs, images) exceeds the 126 MB L2")
     if world > 1:
         tt = torch.tensor([total_ms], device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         total_ms = float(tt.item())
     ms_per_step = total_ms / args.steps
-    value = (step_views if train else 1 * world) / (ms_per_step / 1e3)
+    value = (iters_per_step if train else world) / (ms_per_step / 1e3)
     launches_timed = r.stats()["kernel_launches"] - launches_t0
 
     # ---- stage timing (separate pass, events per kernel, kernel by kernel) ----------------
@@ -428,41 +575,22 @@ def run_isg(args):
         step_eager()
     prof = r.profile_read()
     r.profile(False)
-    launches_per_step = None
 
     # ---- end to end through the public API with host buffers ------------------------------
-    # Every step uploads its targets from pinned host memory and reads its loss back.  With
-    # graphs (default) the upload of step i+1 runs on a copy stream into the other half of a
-    # double-buffered target while step i computes (the prefetch a training loop does); the
-    # loss read-back synchronises every step.  --no-graph: isg_loss_backward with the host
-    # target (its own H2D on a copy stream, overlapped with binning) per view.
+    # Train: every step uploads its targets from pinned host memory and reads its loss back;
+    # step i+2's upload runs on a copy stream into the third of three target buffers while
+    # step i computes (the prefetch a training loop does), and the host reads step i-1's loss
+    # (copied D2H inside step i-1's graph) while step i runs.  Render: time_render().
+    # --no-graph: isg_loss_backward with the host target per view + Adam + sync.
     host_targets = [t.cpu().numpy() for t in targets]
     pinned = [torch.from_numpy(h).pin_memory() for h in host_targets]
     host_views = [p.numpy() for p in pinned]
-    host_out = torch.empty((H, W, 3), dtype=torch.float32).pin_memory().numpy()
-    e2e_ms = []
     use_pipe = train and graph is not None
-    use_rpipe = (not train) and graph is not None
-    if use_rpipe:
-        # render: frame i into device image i % 2 (one graph each), its D2H into pinned host
-        # image i % 2 on a copy stream while frame i + 1 renders; frame i's read is complete
-        # (synchronised) before frame i + 2 reuses the buffers
-        rbufs = [torch.empty((H, W, 3), dtype=torch.float32, device="cuda") for _ in range(2)]
-        rhost = [torch.empty((H, W, 3), dtype=torch.float32).pin_memory() for _ in range(2)]
-        rgraphs = []
-        for b in range(2):
-            r.graph_begin()
-            r.render_device(cams[0], opts, rbufs[b].data_ptr())
-            rgraphs.append(r.graph_end())
-        copy_stream = torch.cuda.Stream()
-        ev_done = [torch.cuda.Event() for _ in range(2)]
-        ev_read = [torch.cuda.Event() for _ in range(2)]
-        r.synchronize()
     NB = 3  # target buffers: step i+2's upload may start once step i-1 is done
+    step_losses = []
     if use_pipe:
         bufs = [[torch.empty_like(t) for t in targets] for _ in range(NB)]
         loss_host = torch.zeros(NB, dtype=torch.float64).pin_memory()
-        step_losses = []
         graphs = []
         for b in range(NB):
             def step_b(bb=bufs[b], slot=loss_host[b:b + 1]):
@@ -479,70 +607,70 @@ def run_isg(args):
         ev_copy = [torch.cuda.Event() for _ in range(NB)]
         ev_done = [torch.cuda.Event() for _ in range(NB)]
         r.synchronize()
+    e2e = None
     if train:
         r.restore()
-    barrier()
-    l0 = r.stats()["kernel_launches"]
-    t_start = time.perf_counter()
-    if use_pipe:
-        with torch.cuda.stream(copy_stream):
-            for k in range(min(NB - 1, args.steps)):
-                for t, h in zip(bufs[k], pinned):
-                    t.copy_(h, non_blocking=True)
-                ev_copy[k].record(copy_stream)
-    for i in range(args.steps):
-        t0 = time.perf_counter()
+        barrier()
+        l0 = r.stats()["kernel_launches"]
+        t_start = time.perf_counter()
         if use_pipe:
-            b = i % NB
-            stream.wait_event(ev_copy[b])
-            graphs[b].launch()
-            ev_done[b].record(stream)
-            if i + NB - 1 < args.steps:  # prefetch step i+2's inputs once step i-1 is done
-                nb = (i + NB - 1) % NB
-                with torch.cuda.stream(copy_stream):
-                    copy_stream.wait_event(ev_done[nb])
-                    for t, h in zip(bufs[nb], pinned):
-                        t.copy_(h, non_blocking=True)
-                    ev_copy[nb].record(copy_stream)
-            if i >= 1:  # step i-1's loss is on the host once its graph is done (step i queued)
-                pb = (i - 1) % NB
-                ev_done[pb].synchronize()
-                step_losses.append(float(loss_host[pb]))
-        elif train:
-            for c, h in zip(cams, host_views):
-                r.loss_backward(c, h, opts, weight=1.0 / step_views)  # H2D target, D2H loss
-            r.adam_step(cfg)
-            r.synchronize()
-        elif use_rpipe:
-            b = i & 1
-            if i >= 2:
-                ev_read[b].synchronize()  # frame i - 2 is on the host: its buffers are free
-            rgraphs[b].launch()
-            ev_done[b].record(stream)
             with torch.cuda.stream(copy_stream):
-                copy_stream.wait_event(ev_done[b])
-                rhost[b].copy_(rbufs[b], non_blocking=True)
-                ev_read[b].record(copy_stream)
-        else:
-            r.render(cams[0], opts, out=host_out)  # D2H image into pinned memory
-        e2e_ms.append((time.perf_counter() - t0) * 1e3)
-    if use_pipe:
-        ev_done[(args.steps - 1) % NB].synchronize()
-        step_losses.append(float(loss_host[(args.steps - 1) % NB]))
-    if use_rpipe:
-        for e in ev_read:
-            e.synchronize()  # the last frames' images are on the host
-    e2e_total_ms = (time.perf_counter() - t_start) * 1e3
-    launches_per_step = (r.stats()["kernel_launches"] - l0) / args.steps
-    e2e_step = e2e_total_ms / args.steps
-    if world > 1:
-        tt = torch.tensor([e2e_step], device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_step = float(tt.item())
-    e2e_value = (step_views if train else world) / (e2e_step / 1e3)
-    h2d = sum(h.nbytes for h in host_views) if train else 0
-    d2h = (8 if use_pipe else 8 * len(host_views)) if train else W * H * 3 * 4
+                for k in range(min(NB - 1, args.steps)):
+                    for t, h in zip(bufs[k], pinned):
+                        t.copy_(h, non_blocking=True)
+                    ev_copy[k].record(copy_stream)
+        for i in range(args.steps):
+            if use_pipe:
+                b = i % NB
+                stream.wait_event(ev_copy[b])
+                graphs[b].launch()
+                ev_done[b].record(stream)
+                if i + NB - 1 < args.steps:  # prefetch step i+2's inputs once step i-1 is done
+                    nb = (i + NB - 1) % NB
+                    with torch.cuda.stream(copy_stream):
+                        copy_stream.wait_event(ev_done[nb])
+                        for t, h in zip(bufs[nb], pinned):
+                            t.copy_(h, non_blocking=True)
+                        ev_copy[nb].record(copy_stream)
+                if i >= 1:  # step i-1's loss is on the host once its graph is done
+                    pb = (i - 1) % NB
+                    ev_done[pb].synchronize()
+                    step_losses.append(float(loss_host[pb]))
+            else:
+                for c, h in zip(cams, host_views):
+                    r.loss_backward(c, h, opts, weight=1.0 / step_views)  # H2D target, D2H loss
+                r.adam_step(cfg)
+                r.synchronize()
+        if use_pipe:
+            ev_done[(args.steps - 1) % NB].synchronize()
+            step_losses.append(float(loss_host[(args.steps - 1) % NB]))
+        e2e_step = (time.perf_counter() - t_start) * 1e3 / args.steps
+        launches_per_step = (r.stats()["kernel_launches"] - l0) / args.steps
+        if world > 1:
+            tt = torch.tensor([e2e_step], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_step = float(tt.item())
+        e2e = {"value": iters_per_step / (e2e_step / 1e3), "unit": unit,
+               "h2d_bytes_per_step": sum(h.nbytes for h in host_views),
+               "d2h_bytes_per_step": 8 if use_pipe else 8 * len(host_views),
+               "ms_per_step": e2e_step, "gpu_launches_per_step": launches_per_step,
+               **({"loss_first_last": [step_losses[0], step_losses[-1]],
+                   "losses_read": len(step_losses)} if use_pipe else {}),
+               "mode": ("cuda graph per step, targets prefetched two steps ahead from pinned "
+                        "host memory on a copy stream (3 buffers); every step's loss copied "
+                        "D2H into pinned memory inside its graph and read by the host while "
+                        "the next step runs (all reads inside the timed region)") if use_pipe
+               else "isg_loss_backward with host targets per view + adam_step + sync"}
 
+    # ---- render FPS (C2): BASELINE's second metric on the same scene and camera ------------
+    render = None
+    if not train or args.config == "c3":
+        if train:
+            r.restore()  # the untrained seed-2403 scene: exactly C2's workload
+        render = time_render(r, cams[0], opts, max(args.steps, 50), args.warmup, stream,
+                             barrier, world)
+        if not train:  # C2 itself: `value` is the timed region above, e2e the pipelined frames
+            e2e = dict(render["e2e"], ms_per_step=1e3 * world / render["e2e"]["value"])
     st = r.stats()
     if rank != 0:
         r.close()
@@ -564,27 +692,25 @@ def run_isg(args):
     pairs = r.count_pairs()
     del count_img
     cpu = None
+    cores = host_threads()
     if rank == 0 and world == 1 and not args.no_cpu:
         import oracle as O
         cam0 = cams[0]
-        tgt0 = host_targets[0]
         ms_now, co_now = r.get_scene()
-        t0 = time.perf_counter()
-        O.render32(ms_now, co_now, cam0, t_min=T_MIN)
-        cores = host_threads()
-        sec = cpu_oracle_train_step(ms_now, co_now, cam0, tgt0, 1, cores) if train else \
-            (time.perf_counter() - t0)
-        cpu = {"value": 1.0 / sec, "unit": "iters/s" if train else "frames/s", "cores": cores,
-               "kind": "port",
-               "sample": (f"1 full {args.config.upper()} train step (fwd+L2+bwd+Adam) of the FP32 "
-                          "tiled CPU oracle" if train else
-                          f"1 full {args.config.upper()} frame of the FP32 tiled CPU oracle")}
-        if not train:  # the reference's own renderer exists: it is the baseline, the port aside
-            res = reference_render_fps(ms_now, co_now, cam0, cores)
+        if train:
+            tr = CpuTrainer(ms_now, co_now, [cam0], [host_targets[0]], threads=cores)
+            sec = tr.step()
+            cpu = {"value": 1.0 / sec, "unit": unit, "cores": cores, "kind": "port",
+                   "sample": f"1 full {args.config.upper()} train step (fwd+L2+bwd+Adam, one "
+                             "view) of the FP32 tiled CPU oracle"}
+        if render is not None and n <= 1_000_000:
+            # the reference's own renderer is the render baseline
+            res = reference_render_fps(ms, co, cam0, cores)
             if res is not None:
-                port = cpu
-                cpu = {"value": res[0], "unit": "frames/s", "cores": cores, "kind": "reference",
-                       "sample": res[1], "port": port}
+                render["cpu_baseline"] = {"value": res[0], "unit": "frames/s", "cores": cores,
+                                          "kind": "reference", "sample": res[1]}
+                if not train:
+                    cpu = render["cpu_baseline"]
     sm_mhz = peaks.get("sm_max_mhz", 1965.0)
     if top_name in ("blend_fwd", "blend_bwd") and pairs:
         ev_p, in_p = pairs
@@ -616,37 +742,19 @@ def run_isg(args):
 
     clk = clocks.summary()
     line = {
-        "metric": METRIC if train else "render FPS (1M isotropic Gaussians, 1080p)",
-        "value": value, "unit": "iters/s" if train else "frames/s", "n_gpus": world,
+        "metric": metric, "value": value, "unit": unit, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "ms_per_step_median": float(np.median(step_ms)),
-        "higher_is_better": True, "scaling": "weak" if args.config != "c4" else "strong",
+        "higher_is_better": True, "scaling": "strong" if args.config == "c4" else "weak",
         "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (isg-synth v1: scene seed 2403, target seed 14244)",
-        "config": {"workload": desc, "config": args.config, "n_gaussians": n, "width": W,
-                   "height": H, "views_per_step": step_views, "t_min": T_MIN,
-                   "loss": "L2 (mse)" if args.loss == "l2" else "0.8 L1 + 0.2 D-SSIM",
-                   "binning": args.binning,
-                   "launch": "eager" if args.no_graph else "cuda_graph (one graph launch per step)",
-                   "parallelism": f"dp{world} (views sharded, scene replicated)",
-                   "l2": l2_note},
-        "e2e": {"value": e2e_value, "unit": "iters/s" if train else "frames/s",
-                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": e2e_step,
-                **({"loss_first_last": [step_losses[0], step_losses[-1]],
-                    "losses_read": len(step_losses)} if use_pipe else {}),
-                "mode": ("cuda graph per step, targets prefetched two steps ahead from pinned host "
-                         "memory on a copy stream (3 buffers); every step's loss copied D2H into pinned "
-                         "memory inside its graph and read by the host while the next step "
-                         "runs (all reads inside the timed region)") if use_pipe else
-                        ("cuda graph per frame into a double-buffered device image, each image "
-                         "copied to pinned host memory on a copy stream while the next renders")
-                        if use_rpipe else
-                        ("isg_loss_backward with host targets per view + adam_step + sync"
-                         if train else "isg_render into pinned host memory")},
+        "config": config_dict(args, world),
+        "l2_working_set_mb": working_set / 1e6,
+        "iters_per_step": iters_per_step, "views_per_step": step_views,
+        "e2e": e2e,
         "gpu_launches": int(launches_timed),
         "gpu_launches_per_step": launches_timed / args.steps,
-        "e2e_gpu_launches_per_step": launches_per_step,
+        "gpus_active": world, "devices": devices,
         "roofline": roof,
         "cpu_baseline": cpu,
         "clocks": clk,
@@ -654,13 +762,33 @@ def run_isg(args):
                   "pairs_evaluated": pairs[0] if pairs else None,
                   "pairs_in_circle": pairs[1] if pairs else None},
     }
+    if args.config == "c4":
+        line["views_per_s"] = step_views / (ms_per_step / 1e3)
+    if train and render is not None:
+        line["render"] = render
+    if nccl is not None:
+        line["nccl"] = nccl
     print(json.dumps(line), flush=True)
     r.close()
     if world > 1:
         dist.destroy_process_group()
 
 
-def main():
+def free_port() -> int:
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_command(argv, gpus: int, port: int):
+    """The torchrun command a `--gpus N` run without torchrun's environment re-launches."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+            f"--nproc-per-node={gpus}", "--master-addr", "127.0.0.1", f"--master-port={port}",
+            str(Path(__file__).resolve()), *argv]
+
+
+def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
@@ -674,12 +802,28 @@ def main():
                     help="binning strategy (identical tile lists)")
     ap.add_argument("--loss", default="l2", choices=["l2", "l1_dssim"],
                     help="training loss (BASELINE configs use L2; l1_dssim = the paper's loss)")
-    args = ap.parse_args()
+    argv = sys.argv[1:] if argv is None else argv
+    args = ap.parse_args(argv)
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if "WORLD_SIZE" in os.environ:
+        world = int(os.environ["WORLD_SIZE"])
+        if world != args.gpus:
+            print(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU "
+                  f"(torchrun --nproc-per-node {args.gpus}) or drop --gpus", file=sys.stderr)
+            return 2
+    elif args.gpus > 1:
+        # one process per GPU: re-launch under torchrun (rank 0 prints the line)
+        env = dict(os.environ)
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        return subprocess.call(spawn_command(argv, args.gpus, free_port()), env=env)
     if args.impl == "reference":
         run_reference(args)
     else:
         run_isg(args)
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())
