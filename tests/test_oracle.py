@@ -306,3 +306,40 @@ def test_oracle_synth_scene_byte_equal_to_product(n, W, H, seed):
             assert np.array_equal(a.translation, b.translation)
             assert (a.focal, a.principal_point, a.width, a.height) == \
                 (b.focal, b.principal_point, b.width, b.height)
+
+
+# ---- the reference's own renders, committed (tests/golden/make_golden.py) ------------------
+def _golden(name):
+    import sys
+    sys.path.insert(0, str(O.ROOT / "tests" / "golden"))
+    from make_golden import load_scenes
+    return load_scenes(name)
+
+
+@pytest.mark.parametrize("name", ["reference_scenes.npz", "reference_scenes_large.npz"])
+def test_restatement_equals_committed_reference_renders(name):
+    """The FP64 restatement reproduces the reference's own render() (oracle/_ref output
+    committed as fixtures) on rotated + translated cameras, shifted principal points, splats
+    behind / at the near plane and off screen, opacity exactly 1 and non-zero backgrounds; the
+    FP32 tiled oracle (the GPU's bit-level model) at t_min = 0 lies within the north star's
+    1e-4 image tolerance of it (FP32 accumulation over up to ~1K-entry lists: <= 3e-5 here)."""
+    for sp, cam, bg, img in _golden(name):
+        assert np.abs(O.render64(sp, cam, bg) - img).max() <= 1e-12
+        ms, co = sp[:, :4].astype(np.float32), sp[:, 4:].astype(np.float32)
+        assert np.abs(O.render32(ms, co, cam, bg=bg, t_min=0.0) - img).max() <= 1e-4
+        if sp.shape[0] <= 120:
+            assert np.abs(O.brute_force64(sp, cam, bg) - img).max() <= 1e-12
+
+
+@ref
+@pytest.mark.parametrize("seed", range(6))
+def test_restatement_equals_reference_render_random_cameras(seed):
+    """Live against the reference's render(): random rotations, translations, focal lengths,
+    principal points, backgrounds, opacity exactly 1, splats behind the camera."""
+    import sys
+    sys.path.insert(0, str(O.ROOT / "tests" / "golden"))
+    from make_golden import random_scene
+    rng = np.random.default_rng(1000 + seed)
+    W, H = int(rng.integers(8, 97)), int(rng.integers(8, 81))
+    sp, cam, bg = random_scene(rng, W, H, int(rng.integers(1, 400)), seed)
+    assert np.abs(O.render64(sp, cam, bg) - O.ref_render(sp, cam, bg, threads=4)).max() <= 1e-12
