@@ -81,6 +81,9 @@ def config_dict(args, world: int) -> dict:
             "views_per_step": len(views), "t_min": T_MIN,
             "loss": "L2 (mse)" if args.loss == "l2" else "0.8 L1 + 0.2 D-SSIM",
             "binning": args.binning,
+            "gradients": ("deterministic (per-pair slots, fixed-order sums)" if
+                          getattr(args, "deterministic", False) else
+                          "direct (warp pre-reduced, red.global.add into per-splat sums)"),
             "launch": "eager" if args.no_graph else "cuda_graph (one graph launch per step)",
             "parallelism": f"dp{world} (views sharded, scene replicated)",
             "l2": ("L2 flushed between steps (256 MB memset outside the timed intervals)" if flush
@@ -456,6 +459,8 @@ def run_isg(args):
         r.set_loss(isg.LOSS_L1_DSSIM, 0.2)
     if args.binning == "bucket":
         r.set_binning(r.BINNING_TILE_BUCKET)
+    if args.deterministic:
+        r.set_deterministic(True)
     opts = isg.RenderOptions(t_min=T_MIN)
     cfg = isg.AdamConfig()
     my_views = views[rank * per_rank:(rank + 1) * per_rank]
@@ -800,6 +805,8 @@ def main(argv=None):
                     help="launch the device-resident step kernel by kernel (no CUDA graph)")
     ap.add_argument("--binning", default="radix", choices=["radix", "bucket"],
                     help="binning strategy (identical tile lists)")
+    ap.add_argument("--deterministic", action="store_true",
+                    help="slot-mode gradient accumulation (bitwise deterministic, slower)")
     ap.add_argument("--loss", default="l2", choices=["l2", "l1_dssim"],
                     help="training loss (BASELINE configs use L2; l1_dssim = the paper's loss)")
     argv = sys.argv[1:] if argv is None else argv

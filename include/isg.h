@@ -252,6 +252,16 @@ isg_status isg_debug_pixel_state(isg_ctx* ctx, float* t_last, uint32_t* n_proc);
 #define ISG_BINNING_RADIX 1
 isg_status isg_set_binning(isg_ctx* ctx, int mode);
 
+/* ---- gradient accumulation mode ---------------------------------------------------------
+ * 0 (default, "direct"): the blend backward pre-reduces each (tile, splat) pair's gradients
+ *   over warp lanes and adds them straight into a per-splat n x 8 buffer in L2
+ *   (red.global.add.v2.f32); the projection backward / Adam read it densely.  Fastest; the
+ *   summation order of a splat's tile contributions varies run to run (last-bit differences).
+ * 1 ("deterministic"): every pair writes its own gradient slot and the projection backward
+ *   sums a splat's slots in a fixed order -- bitwise-identical gradients and trajectories
+ *   across runs, binning modes and CUDA-graph replays. */
+isg_status isg_set_deterministic(isg_ctx* ctx, int on);
+
 /* ---- stage timing (CUDA events on the context stream; for bench.py's roofline) ----------
  * While enabled, kernels are launched without programmatic dependent launch (process-wide),
  * so that the events between them time each kernel alone. */

@@ -26,6 +26,11 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
+// L2 reduction of two consecutive floats (REDG.E.ADD.F32x2): fire-and-forget, no return value
+__device__ __forceinline__ void red_add_v2(float* p, float a, float b) {
+  asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(a), "f"(b) : "memory");
+}
+
 __device__ __forceinline__ float fast_rcp(float x) {
   float y;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -43,20 +48,24 @@ struct Stage {
   float4 geo[B];     // u, v, r2max, -log2e / sigma2d^2
   float4 col[B];     // r, g, b, opacity
   uint32_t slot[B];  // gradient slot of the (tile, splat) pair
+  uint16_t mask[B];  // the pair's sub-quarter mask (sub_mask16)
 };
 
 // Stage list entries [beg, beg+cnt) of the sorted (splat, slot) array (thread t: entries t,
 // t + NT, ...).  The 32-B record gathers are issued as cp.async; the caller waits + barriers
 // before use.
-template <int NT, int B>
+// kSplat: st.slot holds the splat index instead of the pair's gradient slot.
+template <int NT, int B, bool kSplat = false>
 __device__ __forceinline__ void stage_batch(Stage<B>& st, const uint2* __restrict__ sorted,
+                                            const uint16_t* __restrict__ submask,
                                             const RenderRec* __restrict__ rec, uint32_t beg,
                                             int cnt) {
 #pragma unroll
   for (int t = threadIdx.x; t < B; t += NT) {
     if (t < cnt) {
       const uint2 gs = sorted[beg + t];  // (splat, gradient slot)
-      st.slot[t] = gs.y;
+      st.slot[t] = kSplat ? gs.x : gs.y;
+      st.mask[t] = submask[beg + t];
       cp_async16(&st.geo[t], &rec[gs.x].geo);
       cp_async16(&st.col[t], &rec[gs.x].col);
     }

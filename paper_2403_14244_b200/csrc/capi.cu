@@ -59,6 +59,9 @@ struct isg_ctx {
   uint32_t* slot_off = nullptr;   // start of splat g's gradient-slot list
   float4* gradx = nullptr;        // [kMaxRanks exchange slots | grad3d]: one all-reduce buffer
   float4* grad3d = nullptr;       // n x 2, indexed by splat (= gradx + kMaxRanks)
+  float* grad2d = nullptr;        // n x 8 direct-mode 2D gradient sums (zero between views)
+  bool deterministic = false;     // slot mode (bitwise deterministic) instead of direct mode
+  bool pending_direct = false;    // the pending view's K7 ran in direct mode
   uint2* tilebox = nullptr;                 // compact tile bbox + hit mask per splat
   uint32_t* depth[2] = {nullptr, nullptr};  // depth keys (+ radix ping-pong) / depth order
   uint32_t* order[2] = {nullptr, nullptr};
@@ -68,6 +71,7 @@ struct isg_ctx {
   int binning = isg::kBinRadix;
   int64_t key_cap = 0;
   uint2* sorted = nullptr;                  // per list entry: (splat, gradient slot)
+  uint16_t* submask = nullptr;              // per list entry: sub-quarters reached (16 bits)
   float4* partial = nullptr;                // gradient slot: 2D grads of one pair (2 x float4)
   unsigned long long* bucket = nullptr;     // tile-bucket mode: (depth << 32 | splat), unsorted
   uint32_t* slot_of = nullptr;              // tile-bucket mode: slot lists per splat
@@ -252,6 +256,8 @@ isg_status ensure_scene(isg_ctx* ctx, int64_t n) {
   ISG_CUDA(realloc_dev(ctx, &ctx->m, 2 * a));
   ISG_CUDA(realloc_dev(ctx, &ctx->v, 2 * a));
   ISG_CUDA(realloc_dev(ctx, &ctx->raw, a));
+  ISG_CUDA(realloc_dev(ctx, &ctx->grad2d, 8 * a));
+  ISG_CUDA(cudaMemset(ctx->grad2d, 0, sizeof(float) * 8 * a));
   ISG_CUDA(realloc_dev(ctx, &ctx->rec, a));
   ISG_CUDA(realloc_dev(ctx, &ctx->ntiles, a));
   ISG_CUDA(realloc_dev(ctx, &ctx->slot_off, a));
@@ -314,6 +320,7 @@ isg_status ensure_sort_scratch(isg_ctx* ctx, int64_t cap) {
 isg_status ensure_keys(isg_ctx* ctx, int64_t cap) {
   if (cap <= ctx->key_cap) return ISG_OK;
   ISG_CUDA(realloc_dev(ctx, &ctx->sorted, cap));
+  ISG_CUDA(realloc_dev(ctx, &ctx->submask, cap));
   ISG_CUDA(realloc_dev(ctx, &ctx->partial, 2 * cap));
   ISG_CUDA(realloc_dev(ctx, &ctx->bucket, cap));
   ISG_CUDA(realloc_dev(ctx, &ctx->slot_of, cap));
@@ -406,13 +413,26 @@ const uint32_t* slot_list(const isg_ctx* ctx) {
   return ctx->binning == isg::kBinRadix ? nullptr : ctx->slot_of;
 }
 
+// The pending view's direct-mode 2D gradient sums (nullptr: slot mode).
+float* pending_grad2d(const isg_ctx* ctx) { return ctx->pending_direct ? ctx->grad2d : nullptr; }
+
+// Drop a pending view's 2D gradients unprojected (its direct-mode sums are zeroed for the
+// next view; slot-mode slots are simply overwritten by the next backward).
+isg_status drop_pending(isg_ctx* ctx) {
+  if (ctx->pending && ctx->pending_direct && ctx->n_alloc > 0)
+    ISG_CUDA(cudaMemsetAsync(ctx->grad2d, 0, sizeof(float) * 8 * ctx->n_alloc, ctx->stream));
+  ctx->pending = false;
+  return ISG_OK;
+}
+
 // Project a pending view's 2D gradients into the 3D accumulator (K8a).
 isg_status flush_pending(isg_ctx* ctx) {
   if (!ctx->pending) return ISG_OK;
   ISG_STAGE(ST_PROJECT_BWD);
-  isg::launch_project_backward(ctx->ms, ctx->n, ctx->pending_fp, ctx->slot_off, slot_list(ctx),
-                               ctx->ntiles, ctx->partial, ctx->total, ctx->key_cap, ctx->grad3d,
-                               !ctx->grad3d_valid, ctx->stream);
+  isg::launch_project_backward(ctx->ms, ctx->co, ctx->n, ctx->pending_fp, ctx->slot_off,
+                               slot_list(ctx), ctx->ntiles, ctx->partial, pending_grad2d(ctx),
+                               ctx->total, ctx->key_cap, ctx->grad3d, !ctx->grad3d_valid,
+                               ctx->stream);
   ISG_CHECK_LAUNCH();
   ctx->launches++;
   ctx->grad3d_valid = true;
@@ -486,6 +506,9 @@ isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out) {
     topt.epi.emit_gid = ctx->emit_gid;
     topt.epi.sorted = ctx->sorted;
     topt.epi.ranges = ctx->ranges;
+    topt.epi.rec = ctx->rec;
+    topt.epi.submask = ctx->submask;
+    topt.epi.fp = fp;
     isg::radix_sort_pairs(ctx->tkey, ctx->tval, true, ctx->sc + 0, ctx->key_cap,
                           bits_for(fp.n_tiles), ctx->sort_tile, st, &ctx->launches, topt);
     ISG_CHECK_LAUNCH();
@@ -511,7 +534,7 @@ isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out) {
     {
     ISG_STAGE(ST_TILE_SORT);
     isg::launch_tile_sort(fp, ctx->ranges, ctx->bucket, ctx->total, ctx->key_cap, ctx->sorted,
-                          ctx->partial, st);
+                          ctx->partial, ctx->rec, ctx->submask, st);
     ISG_CHECK_LAUNCH();
     ctx->launches++;
     }
@@ -519,7 +542,7 @@ isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out) {
     ISG_CUDA(cudaMemsetAsync(ctx->ranges, 0, sizeof(uint2) * fp.n_tiles, st));
   }
   ISG_STAGE(ST_BLEND_FWD);
-  isg::launch_blend_fwd(fp, ctx->ranges, ctx->sorted, ctx->rec, ctx->total, ctx->key_cap, out,
+  isg::launch_blend_fwd(fp, ctx->ranges, ctx->sorted, ctx->submask, ctx->rec, ctx->total, ctx->key_cap, out,
                         ctx->t_last, ctx->n_proc, st);
   ISG_CHECK_LAUNCH();
   ctx->launches++;
@@ -590,7 +613,7 @@ isg_status check_async(isg_ctx* ctx) {
   isg_status s = check_frame(ctx, &ov);
   if (s != ISG_OK) return s;
   if (ov) {
-    ctx->pending = false;  // a skipped view left no gradient slots to project
+    if ((s = drop_pending(ctx)) != ISG_OK) return s;  // the step is re-run as a whole
     return fail(ctx, ISG_E_OVERFLOW,
                 "tile-key capacity was exceeded by an asynchronous frame; it was skipped (with "
                 "the Adam step after it) and capacity has been grown -- re-run the frames issued "
@@ -638,18 +661,20 @@ isg_status run_backward(isg_ctx* ctx, const FrameParams& fp, const float* target
     ISG_CHECK_LAUNCH();
     }
     ISG_STAGE(ST_BLEND_BWD);
-    isg::launch_blend_bwd(fp, ctx->ranges, ctx->sorted, ctx->rec, ctx->total, ctx->key_cap,
+    isg::launch_blend_bwd(fp, ctx->ranges, ctx->sorted, ctx->submask, ctx->rec, ctx->total, ctx->key_cap,
                           ctx->img, ctx->dldc, ctx->t_last, ctx->n_proc, 1.0f, ctx->partial,
-                          ctx->tile_loss, true, ctx->stream);
+                          ctx->tile_loss, true, ctx->deterministic ? nullptr : ctx->grad2d,
+                          ctx->stream);
     ISG_CHECK_LAUNCH();
     ctx->launches += 1;
   } else {
     const float scale = weight / (3.0f * (float)W * (float)H);
     {
     ISG_STAGE(ST_BLEND_BWD);
-    isg::launch_blend_bwd(fp, ctx->ranges, ctx->sorted, ctx->rec, ctx->total, ctx->key_cap,
+    isg::launch_blend_bwd(fp, ctx->ranges, ctx->sorted, ctx->submask, ctx->rec, ctx->total, ctx->key_cap,
                           ctx->img, target_dev, ctx->t_last, ctx->n_proc, scale, ctx->partial,
-                          ctx->tile_loss, false, ctx->stream);
+                          ctx->tile_loss, false, ctx->deterministic ? nullptr : ctx->grad2d,
+                          ctx->stream);
     ISG_CHECK_LAUNCH();
     }
     ISG_STAGE(ST_LOSS_REDUCE);
@@ -660,6 +685,7 @@ isg_status run_backward(isg_ctx* ctx, const FrameParams& fp, const float* target
   }
   ctx->pending = true;
   ctx->pending_fp = fp;
+  ctx->pending_direct = !ctx->deterministic;
   return ISG_OK;
 }
 
@@ -748,9 +774,9 @@ void isg_destroy(isg_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->nccl_comm) isg_nccl_detach(ctx);
-  void* dev[] = {ctx->ms, ctx->co, ctx->m, ctx->v, ctx->raw, ctx->rec, ctx->ntiles, ctx->slot_off, ctx->tilebox,
+  void* dev[] = {ctx->ms, ctx->co, ctx->m, ctx->v, ctx->raw, ctx->grad2d, ctx->rec, ctx->ntiles, ctx->slot_off, ctx->tilebox,
                  ctx->gradx, ctx->depth[0], ctx->depth[1], ctx->order[0], ctx->order[1],
-                 ctx->sorted, ctx->partial, ctx->bucket, ctx->slot_of, ctx->tkey[0], ctx->tkey[1],
+                 ctx->sorted, ctx->submask, ctx->partial, ctx->bucket, ctx->slot_of, ctx->tkey[0], ctx->tkey[1],
                  ctx->tval[0], ctx->tval[1], ctx->emit_gid, ctx->sort.hist, ctx->sort.lookback,
                  ctx->sort.counters, ctx->arena, ctx->img, ctx->target, ctx->t_last,
                  ctx->n_proc, ctx->ranges, ctx->tile_cnt, ctx->cursor, ctx->tile_loss, ctx->sc,
@@ -855,7 +881,7 @@ static isg_status set_scene_impl(isg_ctx* ctx, int64_t n, const float* ms, const
   ctx->adam_t = 0;
   ISG_CUDA(cudaMemsetAsync(ctx->adam_state, 0, sizeof(isg::AdamState), ctx->stream));
   ctx->snap_valid = false;
-  ctx->pending = false;
+  if ((s = drop_pending(ctx)) != ISG_OK) return s;
   ctx->grad3d_valid = false;
   ctx->have_frame = false;
   ISG_CUDA(cudaMemsetAsync(ctx->loss, 0, sizeof(double) * 2, ctx->stream));
@@ -985,7 +1011,8 @@ isg_status isg_read_loss(isg_ctx* ctx, double* loss_out) {
 isg_status isg_zero_grads(isg_ctx* ctx) {
   if (!ctx) return ISG_E_ARG;
   cudaSetDevice(ctx->device);
-  ctx->pending = false;  // the pending view's per-pair slots are simply dropped
+  isg_status s = drop_pending(ctx);  // the pending view's gradients are simply dropped
+  if (s != ISG_OK) return s;
   ctx->grad3d_valid = false;
   ISG_CUDA(cudaMemsetAsync(ctx->loss, 0, sizeof(double) * 2, ctx->stream));
   return ISG_OK;
@@ -1032,7 +1059,8 @@ isg_status isg_adam_step(isg_ctx* ctx, const float lr[4], float b1, float b2, fl
     ISG_STAGE(ST_PROJECT_ADAM);
     isg::launch_adam_tick(lr, b1, b2, eps, ctx->adam_state, ctx->loss, ctx->total, ctx->stream);
     isg::launch_project_adam(ctx->ms, ctx->co, ctx->n, ctx->pending_fp, ctx->slot_off,
-                             slot_list(ctx), ctx->ntiles, ctx->partial, ctx->total, ctx->raw,
+                             slot_list(ctx), ctx->ntiles, ctx->partial, pending_grad2d(ctx),
+                             ctx->total, ctx->raw,
                              ctx->m, ctx->v, ctx->adam_state, ctx->stream);
     ISG_CHECK_LAUNCH();
     ctx->launches += 2;
@@ -1211,7 +1239,7 @@ isg_status isg_adaptive_control(isg_ctx* ctx, const isg_adapt_params* prm, uint6
   ctx->adam_t = 0;
   ISG_CUDA(cudaMemsetAsync(ctx->adam_state, 0, sizeof(isg::AdamState), ctx->stream));
   ctx->snap_valid = false;
-  ctx->pending = false;
+  if ((s = drop_pending(ctx)) != ISG_OK) return s;
   ctx->grad3d_valid = false;
   ctx->have_frame = false;
   ISG_CUDA(cudaMemsetAsync(ctx->loss, 0, sizeof(double) * 2, ctx->stream));
@@ -1387,6 +1415,16 @@ isg_status isg_debug_bins(isg_ctx* ctx, uint64_t* keys, uint32_t* vals, int64_t*
                              ctx->stream));
   ISG_CUDA(cudaStreamSynchronize(ctx->stream));
   ISG_CUDA(cudaGetLastError());
+  return ISG_OK;
+}
+
+isg_status isg_set_deterministic(isg_ctx* ctx, int on) {
+  if (!ctx) return ISG_E_ARG;
+  ISG_NO_CAPTURE("isg_set_deterministic");
+  cudaSetDevice(ctx->device);
+  isg_status s = flush_pending(ctx);  // the pending view keeps the mode it was computed in
+  if (s != ISG_OK) return s;
+  ctx->deterministic = on != 0;
   return ISG_OK;
 }
 
@@ -1583,9 +1621,10 @@ isg_status exchange_and_adam(isg_ctx* ctx, const float lr[4], float b1, float b2
     for (int c = 0; c < chunks; ++c) {
       const int64_t b = bound(c), e = bound(c + 1);
       if (project && e > b) {
-        isg::launch_project_backward(ctx->ms, n, ctx->pending_fp, ctx->slot_off, slot_list(ctx),
-                                     ctx->ntiles, ctx->partial, ctx->total, ctx->key_cap,
-                                     ctx->grad3d, first, st, b, e);
+        isg::launch_project_backward(ctx->ms, ctx->co, n, ctx->pending_fp, ctx->slot_off,
+                                     slot_list(ctx), ctx->ntiles, ctx->partial,
+                                     pending_grad2d(ctx), ctx->total, ctx->key_cap, ctx->grad3d,
+                                     first, st, b, e);
         ctx->launches++;
       }
       ISG_CHECK_LAUNCH();

@@ -87,6 +87,9 @@ struct SortEpilogue {
   const uint32_t* emit_gid = nullptr;
   uint2* sorted = nullptr;
   uint2* ranges = nullptr;
+  const RenderRec* rec = nullptr;  // + the pairs' sub-quarter masks (sub_mask16)
+  uint16_t* submask = nullptr;
+  FrameParams fp{};
 };
 struct SortOptions {
   bool scratch_zeroed = false;  // hist / counters / look-back already zero (one frame memset)
@@ -124,9 +127,10 @@ void launch_fill(const float4* ms, const uint32_t* ntiles, const uint2* tilebox,
                  unsigned long long* bucket, uint32_t* slot_of, uint32_t* slot_off, int64_t cap,
                  unsigned long long* lookback, uint32_t* counter, cudaStream_t st);
 // scratch: the gradient-slot buffer (2 float4 per key), used only for tiles > 2048 entries.
+// Also writes each pair's sub-quarter mask (sub_mask16) to submask.
 void launch_tile_sort(const FrameParams& fp, const uint2* ranges, const unsigned long long* bucket,
                       const unsigned long long* total, int64_t cap, uint2* sorted, float4* scratch,
-                      cudaStream_t st);
+                      const RenderRec* rec, uint16_t* submask, cudaStream_t st);
 
 // ---- radix binning (k_sort.cu) ------------------------------------------------------------
 int64_t scan_emit_scratch_words(int64_t n);  // + 1 zeroed u64 words
@@ -143,18 +147,24 @@ void launch_ranges_fix(const uint32_t* n_keys, int64_t key_cap, int n_tiles, uin
                        cudaStream_t st);
 
 // ---- blending (k_blend.cu) ----------------------------------------------------------------
-// sorted: per list entry (splat, gradient slot), tile-major, (depth, index) order per tile.
+// sorted: per list entry (splat, gradient slot), tile-major, (depth, index) order per tile;
+// submask: per list entry, the 4x4 sub-quarters of the tile the splat reaches (sub_mask16).
 void launch_blend_fwd(const FrameParams& fp, const uint2* ranges, const uint2* sorted,
+                      const uint16_t* submask,
                       const RenderRec* rec, unsigned long long* total, int64_t key_cap,
                       float* out, float* t_last, uint32_t* n_proc, cudaStream_t st);
 // Writes every pair's 2D gradient to partial[2 slot], partial[2 slot + 1].
 // given_dldc: `target` is dL/dC (G = loss_scale * target) and tile_loss is not meaningful;
 // otherwise G = 2 loss_scale (img - target) and tile_loss[t] = sum over the tile of |d|^2.
 void launch_blend_bwd(const FrameParams& fp, const uint2* ranges, const uint2* sorted,
-                      const RenderRec* rec, const unsigned long long* total, int64_t key_cap,
+                      const uint16_t* submask, const RenderRec* rec, const unsigned long long* total, int64_t key_cap,
                       const float* img, const float* target, const float* t_last,
                       const uint32_t* n_proc, float loss_scale, float4* partial,
-                      double* tile_loss, bool given_dldc, cudaStream_t st);
+                      double* tile_loss, bool given_dldc, float* grad2d, cudaStream_t st);
+// grad2d != nullptr: "direct" accumulation -- each sub-quarter's pre-reduced gradients are
+// added (red.global.add.v2.f32) into grad2d[splat] (n x 8: sum go dx, sum go dy, sum go r2,
+// sum go, drgb, 0; unscaled), which K8 reads densely, scales and re-zeroes.  Not bitwise
+// deterministic (L2 reduction order); the slot mode (grad2d == nullptr) is.
 
 // ---- L1 + D-SSIM image loss (k_ssim.cu) ---------------------------------------------------
 constexpr int kSsimHalf = 5;  // 11-tap window
@@ -186,6 +196,7 @@ struct AdamParams {
   float b1, b2, eps;
   float step_size[4];  // lr / (1 - b1^t)
   float bc2_sqrt;      // sqrt(1 - b2^t)
+  float inv_bc2_sqrt;  // 1 / sqrt(1 - b2^t)
 };
 struct AdamState {
   AdamParams p;
@@ -203,9 +214,11 @@ void launch_raw_init(const float4* ms, const float4* co, int64_t n, float2* raw,
 
 // Splat g's slots: slot_of[slot_off[g] + k] (or slot_off[g] + k when slot_of is null).
 // K8a: 2D grads of one view -> 3D grads (overwrite when `first`, else accumulate).
-void launch_project_backward(const float4* ms, int64_t n, const FrameParams& fp,
-                             const uint32_t* slot_off, const uint32_t* slot_of,
-                             const uint32_t* ntiles, const float4* partial,
+// grad2d != nullptr: direct mode (dense sums, read and re-zeroed; co supplies the opacity).
+void launch_project_backward(const float4* ms, const float4* co, int64_t n,
+                             const FrameParams& fp, const uint32_t* slot_off,
+                             const uint32_t* slot_of, const uint32_t* ntiles,
+                             const float4* partial, float* grad2d,
                              const unsigned long long* total, int64_t cap, float4* grad3d,
                              bool first, cudaStream_t st, int64_t begin = 0, int64_t end = -1);
 // Multi-GPU exchange slots (kMaxRanks float4 ahead of the gradient buffer): pack this rank's
@@ -219,7 +232,7 @@ void launch_loss_unpack(double* loss, unsigned long long* total, const float4* s
 // K8 fused: 2D grads of one view -> 3D -> Adam.
 void launch_project_adam(float4* ms, float4* co, int64_t n, const FrameParams& fp,
                          const uint32_t* slot_off, const uint32_t* slot_of,
-                         const uint32_t* ntiles, const float4* partial,
+                         const uint32_t* ntiles, const float4* partial, float* grad2d,
                          unsigned long long* total, float2* raw, float4* m, float4* v,
                          const AdamState* ap, cudaStream_t st);
 // K8b: Adam from accumulated 3D grads.

@@ -20,6 +20,19 @@ namespace isg {
 
 namespace {
 
+// MUFU approximations (~2 ulp) for K8's arithmetic: the optimizer and the chain rule are
+// compared with tolerances, never bit for bit (and nothing is binned from them)
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ void sum_slots(const float4* __restrict__ partial,
                                           const uint32_t* __restrict__ slot_of, uint32_t off,
                                           uint32_t cnt, float4& a, float4& b) {
@@ -53,17 +66,55 @@ __device__ __forceinline__ void sum_slots(const float4* __restrict__ partial,
   }
 }
 
+// Splat i's 2D gradient sums of one view: its gradient slots (slot mode, already scaled by
+// K7's flush) or, in direct mode (grad2d != null), the dense L2-reduced sums, read and zeroed
+// for the next view (the caller scales them, see grad3d_of).
+__device__ __forceinline__ void load_2d(int64_t i, float* __restrict__ grad2d,
+                                        const float4* __restrict__ partial,
+                                        const uint32_t* __restrict__ slot_of,
+                                        const uint32_t* __restrict__ slot_off,
+                                        const uint32_t* __restrict__ ntiles, bool skip,
+                                        float4& a, float4& b) {
+  if (grad2d) {
+    float4* g = reinterpret_cast<float4*>(grad2d) + 2 * i;
+    a = g[0];
+    b = g[1];
+    g[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+    g[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  } else {
+    sum_slots(partial, slot_of, slot_off[i], skip ? 0u : ntiles[i], a, b);
+  }
+}
+
+// opacity >= 0 (direct mode): a holds the unscaled sums (sum go dx, sum go dy, sum go r2,
+// sum go); kernels.hpp:219-220: dg/du = g 2 dx / s^2, dg/ds = g 2 r^2 / s^3, times opacity,
+// so (du, dv) scale by 2 o / s^2 and dsigma2d by 2 o / s^3 (s = sigma2d of this projection).
+// The chain rule needs only the camera-space centre and 1 / z: no exact-rounding projection
+// here (nothing is binned from it), one fast reciprocal instead of K1's three IEEE divisions.
 __device__ __forceinline__ void grad3d_of(const float4 ms, const isg_camera& cam, float4 a,
-                                          float4 b, float out[8]) {
-  const Proj p = project(ms, cam);
-  if (!p.vis) {
+                                          float4 b, float out[8], float opacity = -1.0f) {
+  const float xc = cam.R[0] * ms.x + cam.R[1] * ms.y + cam.R[2] * ms.z + cam.t[0];
+  const float yc = cam.R[3] * ms.x + cam.R[4] * ms.y + cam.R[5] * ms.z + cam.t[1];
+  const float zc = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(cam.R[6], ms.x), __fmul_rn(cam.R[7], ms.y)),
+                                       __fmul_rn(cam.R[8], ms.z)),
+                             cam.t[2]);  // K1's rounding: the same near-plane decision
+  if (!(zc > kNearPlane)) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) out[j] = 0.f;
     return;
   }
-  const float fz = cam.focal / p.zc;
+  const float iz = rcp_approx(zc);
+  const float fz = cam.focal * iz;
+  if (opacity >= 0.0f) {
+    // s = sigma f / z; (du, dv) scale by 2 o / s^2, dsigma2d by 2 o / s^3
+    const float inv_s = rcp_approx(ms.w * fz);
+    const float k2 = 2.0f * opacity * inv_s * inv_s;
+    a.x *= k2;
+    a.y *= k2;
+    a.z *= k2 * inv_s;
+  }
   const float gx = a.x * fz, gy = a.y * fz;
-  const float gz = -(((a.x * p.xc + a.y * p.yc) + a.z * ms.w) * fz) / p.zc;
+  const float gz = -(((a.x * xc + a.y * yc) + a.z * ms.w) * fz) * iz;
   out[0] = (cam.R[0] * gx + cam.R[3] * gy) + cam.R[6] * gz;
   out[1] = (cam.R[1] * gx + cam.R[4] * gy) + cam.R[7] * gz;
   out[2] = (cam.R[2] * gx + cam.R[5] * gy) + cam.R[8] * gz;
@@ -80,11 +131,35 @@ __device__ __forceinline__ void grad3d_of(const float4 ms, const isg_camera& cam
 // values (no log/exp round-trip drift; an opacity of exactly 0 or 1 is entered into the open
 // interval once, by k_raw_init).  A parameter whose update is exactly zero keeps its stored
 // value bit for bit (a zero-gradient step from zero moments is a no-op).
-__device__ __forceinline__ void adam_update(float4* __restrict__ ms, float4* __restrict__ co,
-                                            float2* __restrict__ raw, float4* __restrict__ m,
-                                            float4* __restrict__ v, int64_t i, const float gr[8],
-                                            const AdamParams& ap,
-                                            unsigned long long* skipped) {
+//
+// A splat's optimizer inputs, loaded together up front (every load in flight at once: the
+// kernels are HBM streams whose only limit is memory-level parallelism).
+struct AdamIn {
+  float4 P0, P1;          // (mu, sigma), (rgb, opacity)
+  float2 R;               // (log sigma, logit opacity)
+  float4 M0, M1, V0, V1;  // moments
+};
+__device__ __forceinline__ AdamIn adam_load(const float4* __restrict__ ms,
+                                            const float4* __restrict__ co,
+                                            const float2* __restrict__ raw,
+                                            const float4* __restrict__ m,
+                                            const float4* __restrict__ v, int64_t i) {
+  AdamIn a;
+  a.P0 = ms[i];
+  a.P1 = co[i];
+  a.R = raw[i];
+  a.M0 = m[2 * i];
+  a.M1 = m[2 * i + 1];
+  a.V0 = v[2 * i];
+  a.V1 = v[2 * i + 1];
+  return a;
+}
+
+__device__ __forceinline__ void adam_apply(const AdamIn& in, float4* __restrict__ ms,
+                                           float4* __restrict__ co, float2* __restrict__ raw,
+                                           float4* __restrict__ m, float4* __restrict__ v,
+                                           int64_t i, const float gr[8], const AdamParams& ap,
+                                           unsigned long long* skipped) {
   bool ok = true;
 #pragma unroll
   for (int j = 0; j < 8; ++j) ok &= isfinite(gr[j]);
@@ -92,24 +167,22 @@ __device__ __forceinline__ void adam_update(float4* __restrict__ ms, float4* __r
     atomicAdd(skipped, 1ull);
     return;
   }
-  float4 P0 = ms[i], P1 = co[i];
-  const float2 R = raw[i];
-  const float sigma = P0.w;
-  const float s = 1.0f / (1.0f + expf(-R.y));  // sigmoid(logit) of the optimizer state
-  float p[8] = {P0.x, P0.y, P0.z, R.x, P1.x, P1.y, P1.z, R.y};
+  const float sigma = in.P0.w;
+  const float s = rcp_approx(1.0f + __expf(-in.R.y));  // sigmoid(logit) of the optimizer state
+  float p[8] = {in.P0.x, in.P0.y, in.P0.z, in.R.x, in.P1.x, in.P1.y, in.P1.z, in.R.y};
   const float g[8] = {gr[0], gr[1], gr[2], gr[3] * sigma,
                       gr[4], gr[5], gr[6], gr[7] * s * (1.0f - s)};
-  float4 M0 = m[2 * i], M1 = m[2 * i + 1], V0 = v[2 * i], V1 = v[2 * i + 1];
-  float mm[8] = {M0.x, M0.y, M0.z, M0.w, M1.x, M1.y, M1.z, M1.w};
-  float vv[8] = {V0.x, V0.y, V0.z, V0.w, V1.x, V1.y, V1.z, V1.w};
+  float mm[8] = {in.M0.x, in.M0.y, in.M0.z, in.M0.w, in.M1.x, in.M1.y, in.M1.z, in.M1.w};
+  float vv[8] = {in.V0.x, in.V0.y, in.V0.z, in.V0.w, in.V1.x, in.V1.y, in.V1.z, in.V1.w};
   const int group[8] = {0, 0, 0, 1, 2, 2, 2, 3};
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     mm[j] = mm[j] + (1.0f - ap.b1) * (g[j] - mm[j]);
     vv[j] = ap.b2 * vv[j] + (1.0f - ap.b2) * g[j] * g[j];
-    const float denom = sqrtf(vv[j]) / ap.bc2_sqrt + ap.eps;
+    // MUFU square root and reciprocal (~2 ulp; the oracle's IEEE forms agree to ~1e-7 rel)
+    const float denom = sqrt_approx(vv[j]) * ap.inv_bc2_sqrt + ap.eps;
     // m == 0 moves nothing (also with eps == 0 and v == 0, where m / denom would be 0 / 0)
-    const float upd = mm[j] == 0.0f ? 0.0f : mm[j] / denom;
+    const float upd = mm[j] == 0.0f ? 0.0f : mm[j] * rcp_approx(denom);
     p[j] = p[j] - ap.step_size[group[j]] * upd;
   }
   m[2 * i] = make_float4(mm[0], mm[1], mm[2], mm[3]);
@@ -117,8 +190,9 @@ __device__ __forceinline__ void adam_update(float4* __restrict__ ms, float4* __r
   v[2 * i] = make_float4(vv[0], vv[1], vv[2], vv[3]);
   v[2 * i + 1] = make_float4(vv[4], vv[5], vv[6], vv[7]);
   raw[i] = make_float2(p[3], p[7]);
-  ms[i] = make_float4(p[0], p[1], p[2], p[3] == R.x ? sigma : expf(p[3]));
-  co[i] = make_float4(p[4], p[5], p[6], p[7] == R.y ? P1.w : 1.0f / (1.0f + expf(-p[7])));
+  ms[i] = make_float4(p[0], p[1], p[2], p[3] == in.R.x ? sigma : __expf(p[3]));
+  co[i] = make_float4(p[4], p[5], p[6],
+                      p[7] == in.R.y ? in.P1.w : rcp_approx(1.0f + __expf(-p[7])));
 }
 
 }  // namespace
@@ -140,6 +214,7 @@ __global__ void k_adam_tick(AdamParams in, AdamState* __restrict__ st, double* _
   AdamParams p = in;
   for (int i = 0; i < 4; ++i) p.step_size[i] = (float)((double)in.lr[i] / bc1);
   p.bc2_sqrt = (float)sqrt(bc2);
+  p.inv_bc2_sqrt = (float)(1.0 / sqrt(bc2));
   st->p = p;
 }
 
@@ -155,18 +230,20 @@ __global__ void __launch_bounds__(256) k_raw_init(const float4* __restrict__ ms,
 }
 
 __global__ void __launch_bounds__(256) k_project_backward(
-    const float4* __restrict__ ms, int64_t n, FrameParams fp, const uint32_t* __restrict__ slot_off,
-    const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ ntiles,
-    const float4* __restrict__ partial,
-    const unsigned long long* __restrict__ total, int64_t cap, float4* __restrict__ grad3d,
-    bool first, int64_t begin) {
+    const float4* __restrict__ ms, const float4* __restrict__ co, int64_t n, FrameParams fp,
+    const uint32_t* __restrict__ slot_off, const uint32_t* __restrict__ slot_of,
+    const uint32_t* __restrict__ ntiles, const float4* __restrict__ partial,
+    float* __restrict__ grad2d, const unsigned long long* __restrict__ total, int64_t cap,
+    float4* __restrict__ grad3d, bool first, int64_t begin) {
   const int64_t i = begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const bool ov = *total > (unsigned long long)cap;  // frame was skipped: contributes nothing
+  const float4 P0 = ms[i];
+  const float op = grad2d ? co[i].w : -1.0f;
   float4 a, b;
-  sum_slots(partial, slot_of, slot_off[i], ov ? 0u : ntiles[i], a, b);
+  load_2d(i, grad2d, partial, slot_of, slot_off, ntiles, ov, a, b);
   float o[8];
-  grad3d_of(ms[i], fp.cam, a, b, o);
+  grad3d_of(P0, fp.cam, a, b, o, op);
   float4 g0 = make_float4(o[0], o[1], o[2], o[3]), g1 = make_float4(o[4], o[5], o[6], o[7]);
   if (!first) {
     const float4 h0 = grad3d[2 * i], h1 = grad3d[2 * i + 1];
@@ -189,19 +266,23 @@ __global__ void ISG_ADAM_BOUNDS k_project_adam(
     float4* __restrict__ ms, float4* __restrict__ co, int64_t n, FrameParams fp,
     const uint32_t* __restrict__ slot_off, const uint32_t* __restrict__ slot_of,
     const uint32_t* __restrict__ ntiles, const float4* __restrict__ partial,
-    unsigned long long* __restrict__ total, float2* __restrict__ raw, float4* __restrict__ m,
-    float4* __restrict__ v, const AdamState* __restrict__ state) {
+    float* __restrict__ grad2d, unsigned long long* __restrict__ total,
+    float2* __restrict__ raw, float4* __restrict__ m, float4* __restrict__ v,
+    const AdamState* __restrict__ state) {
   pdl_enter();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  // an overflowed frame since the last host check: no update (the host re-runs the step)
-  if (total[kTotalOverflowMax] != 0ull) return;
-  const AdamParams ap = state->p;
+  // an overflowed frame since the last host check: no update (the host re-runs the step);
+  // the direct-mode sums are consumed (zeroed) either way
+  const bool skip = total[kTotalOverflowMax] != 0ull;
+  const AdamIn in = adam_load(ms, co, raw, m, v, i);
   float4 a, b;
-  sum_slots(partial, slot_of, slot_off[i], ntiles[i], a, b);
+  load_2d(i, grad2d, partial, slot_of, slot_off, ntiles, skip, a, b);
+  if (skip) return;
+  const AdamParams ap = state->p;
   float o[8];
-  grad3d_of(ms[i], fp.cam, a, b, o);
-  adam_update(ms, co, raw, m, v, i, o, ap, total + kTotalSkipped);
+  grad3d_of(in.P0, fp.cam, a, b, o, grad2d ? in.P1.w : -1.0f);
+  adam_apply(in, ms, co, raw, m, v, i, o, ap, total + kTotalSkipped);
 }
 
 __global__ void __launch_bounds__(256) k_adam(float4* __restrict__ ms, float4* __restrict__ co,
@@ -213,21 +294,24 @@ __global__ void __launch_bounds__(256) k_adam(float4* __restrict__ ms, float4* _
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (total[kTotalOverflowMax] != 0ull) return;  // a view of the step was skipped
-  const AdamParams ap = state->p;
+  const AdamIn in = adam_load(ms, co, raw, m, v, i);
   const float4 g0 = grad3d[2 * i], g1 = grad3d[2 * i + 1];
+  const AdamParams ap = state->p;
   const float o[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-  adam_update(ms, co, raw, m, v, i, o, ap, total + kTotalSkipped);
+  adam_apply(in, ms, co, raw, m, v, i, o, ap, total + kTotalSkipped);
 }
 
-void launch_project_backward(const float4* ms, int64_t n, const FrameParams& fp,
-                             const uint32_t* slot_off, const uint32_t* slot_of,
-                             const uint32_t* ntiles, const float4* partial,
+void launch_project_backward(const float4* ms, const float4* co, int64_t n,
+                             const FrameParams& fp, const uint32_t* slot_off,
+                             const uint32_t* slot_of, const uint32_t* ntiles,
+                             const float4* partial, float* grad2d,
                              const unsigned long long* total, int64_t cap, float4* grad3d,
                              bool first, cudaStream_t st, int64_t begin, int64_t end) {
   if (end < 0 || end > n) end = n;
   if (end <= begin) return;
   k_project_backward<<<(unsigned)((end - begin + 255) / 256), 256, 0, st>>>(
-      ms, end, fp, slot_off, slot_of, ntiles, partial, total, cap, grad3d, first, begin);
+      ms, co, end, fp, slot_off, slot_of, ntiles, partial, grad2d, total, cap, grad3d, first,
+      begin);
 }
 
 // ---- multi-GPU exchange: the step's loss and overflow state ride in the gradient all-reduce --
@@ -281,12 +365,12 @@ void launch_loss_unpack(double* loss, unsigned long long* total, const float4* s
 
 void launch_project_adam(float4* ms, float4* co, int64_t n, const FrameParams& fp,
                          const uint32_t* slot_off, const uint32_t* slot_of,
-                         const uint32_t* ntiles, const float4* partial,
+                         const uint32_t* ntiles, const float4* partial, float* grad2d,
                          unsigned long long* total, float2* raw, float4* m, float4* v,
                          const AdamState* ap, cudaStream_t st) {
   if (n <= 0) return;
   launch_pdl(k_project_adam, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, ms, co, n,
-             fp, slot_off, slot_of, ntiles, partial, total, raw, m, v, ap);
+             fp, slot_off, slot_of, ntiles, partial, grad2d, total, raw, m, v, ap);
 }
 
 void launch_adam(float4* ms, float4* co, int64_t n, const float4* grad3d, float2* raw, float4* m,

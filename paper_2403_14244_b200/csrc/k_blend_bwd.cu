@@ -31,6 +31,10 @@ constexpr int kBT = 64;      // threads per tile CTA: 2 warps x 8 four-lane grou
 #ifndef ISG_BWD_BATCH
 #define ISG_BWD_BATCH 32
 #endif
+#ifndef ISG_BWD_UNROLL
+#define ISG_BWD_UNROLL 1
+#endif
+constexpr int kUnroll = ISG_BWD_UNROLL;  // walk steps per loop iteration
 constexpr int kBatch = ISG_BWD_BATCH;  // records staged per batch (32: one ballot per sub-quarter)
 constexpr int kWords = kBatch / 32;
 constexpr int kSubs = 16;    // 4x4 sub-quarters per tile (one per four-lane group)
@@ -107,20 +111,22 @@ __device__ __forceinline__ void reduce_scatter8_quad(const float v[8], float out
 #else
 #define ISG_BWD_BOUNDS __launch_bounds__(kBT)
 #endif
-template <bool kGivenG>
+template <bool kGivenG, bool kDirect>
 // (a minimum-blocks bound that caps registers for more resident warps — 10, 12, 14 or 16 CTAs
 // per SM — measured 12-27% slower: ptxas then trades ILP for registers)
 __global__ void ISG_BWD_BOUNDS k_blend_bwd(
     FrameParams fp, const uint2* __restrict__ ranges, const uint2* __restrict__ sorted,
+    const uint16_t* __restrict__ submask,
     const RenderRec* __restrict__ rec, const unsigned long long* __restrict__ total,
     int64_t key_cap, const float* __restrict__ img, const float* __restrict__ target,
     const float* __restrict__ t_last, const uint32_t* __restrict__ n_proc, float loss_scale,
-    float4* __restrict__ partial, double* __restrict__ tile_loss) {
+    float4* __restrict__ partial, double* __restrict__ tile_loss, float* __restrict__ grad2d) {
   // entry kBatch of each stage is a sentinel no pixel is inside (r2max = -1): the groups'
   // lists are padded with it to the warp's step count, so the walk needs no bounds test
   __shared__ Stage<kBatch + 1> st[2];
   // [sub-quarter][value][entry]; rows padded so one entry's 8 values hit 8 different banks
-  __shared__ float s_part[kSubs][8][kBatch + 1];
+  // (slot mode only: the direct mode reduces into grad2d in L2 instead)
+  __shared__ float s_part[kDirect ? 1 : kSubs][8][kBatch + 1];
   __shared__ uint32_t s_rel[kSubs][kWords];  // relevance ballots of the batch per sub-quarter
   __shared__ uint8_t s_list[kSubs][kListPitch];
   __shared__ float s_red[2];
@@ -145,23 +151,6 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
   const int y0 = ty * kTile + (q >> 1) * 8 + (sq >> 1) * 4 + 2 * (l4 >> 1);
   const float2 PX = make_float2((float)x0 + 0.5f, (float)x0 + 1.5f);
   const float2 PY = make_float2((float)y0 + 0.5f, (float)y0 + 1.5f);
-  // the warp's 8 sub-quarters: 4 columns of the tile (x = 4c) x 2 rows (y = 8w + 4r)
-  float cx0[4], cx1[4], ry0[2], ry1[2];
-  bool cv[4], rv[2];
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const int xs = tx * kTile + 4 * c;
-    cv[c] = xs < W;
-    cx0[c] = (float)xs + 0.5f;
-    cx1[c] = (float)(min(xs + 4, W) - 1) + 0.5f;
-  }
-#pragma unroll
-  for (int r = 0; r < 2; ++r) {
-    const int ys = ty * kTile + 8 * w + 4 * r;
-    rv[r] = ys < H;
-    ry0[r] = (float)ys + 0.5f;
-    ry1[r] = (float)(min(ys + 4, H) - 1) + 0.5f;
-  }
   const uint2 rg = ranges[tile];
   const int n = rg.x == kEmptyRange ? 0 : (int)(rg.y - rg.x);
 
@@ -215,8 +204,8 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
   __syncthreads();
   const int m = max(s_max[0], s_max[1]);  // entries [0, m) are walked
   if (threadIdx.x == 0) tile_loss[tile] = (double)s_red[0] + (double)s_red[1];
-  // entries never reached by any pixel get zero gradient slots
-  for (int j = m + (int)threadIdx.x; j < n; j += kBT) {
+  // entries never reached by any pixel get zero gradient slots (slot mode)
+  for (int j = m + (int)threadIdx.x; !kDirect && j < n; j += kBT) {
     const uint32_t e = sorted[rg.x + j].y;
     partial[2 * (size_t)e] = make_float4(0.f, 0.f, 0.f, 0.f);
     partial[2 * (size_t)e + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -225,7 +214,8 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
 
   const uint32_t lt = (1u << lane) - 1u;
   int hi = m;
-  stage_batch<kBT>(st[0], sorted, rec, rg.x + max(0, hi - kBatch), min(kBatch, hi));
+  stage_batch<kBT, kBatch + 1, kDirect>(st[0], sorted, submask, rec, rg.x + max(0, hi - kBatch),
+                                        min(kBatch, hi));
   for (int it = 0; hi > 0; ++it) {
     const int lo = max(0, hi - kBatch);
     const int cnt = hi - lo;
@@ -234,37 +224,24 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
     __syncthreads();  // batch visible; previous batch's flush finished reading s_part
     if (lo > 0) {
       const int nlo = max(0, lo - kBatch);
-      stage_batch<kBT>(st[(it + 1) & 1], sorted, rec, rg.x + nlo, lo - nlo);
+      stage_batch<kBT, kBatch + 1, kDirect>(st[(it + 1) & 1], sorted, submask, rec, rg.x + nlo,
+                                            lo - nlo);
     }
-    // relevance of the batch for the warp's 8 sub-quarters -> 8 compacted lists.  The tests
-    // share their per-axis terms (rounded squares of the distances to the 4 columns and 2
-    // rows) and add one pair exactly as dist2_rn would at the sub-quarter's closest pixel centre.
+    // relevance of the batch for the warp's 8 sub-quarters -> 8 compacted lists, from the
+    // pairs' precomputed sub-quarter masks (sub_mask16, the binning's closest-point tests)
     int my_cnt = 0, steps = 0;
     int base[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
     for (int wd = 0; wd < kWords; ++wd) {
       const int j = 32 * wd + lane;
-      const bool in = j < cnt;
-      const float4 g = cur.geo[in ? j : 0];
-      float ax4[4], ay2[2];
+      const uint32_t mw = j < cnt ? ((uint32_t)cur.mask[j] >> (8 * w)) & 0xFFu : 0u;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const float d = __fsub_rn(fminf(fmaxf(g.x, cx0[c]), cx1[c]), g.x);
-        ax4[c] = __fmul_rn(d, d);
-      }
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const float d = __fsub_rn(fminf(fmaxf(g.y, ry0[r]), ry1[r]), g.y);
-        ay2[r] = __fmul_rn(d, d);
-      }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {  // group k: quarter 2w + (k >> 2), sub (k & 3)
-        const int c = (k >> 2) * 2 + (k & 1), r = (k >> 1) & 1;
-        const bool hk = in && cv[c] && rv[r] && !(__fadd_rn(ax4[c], ay2[r]) > g.z);
+      for (int k = 0; k < 8; ++k) {  // group k = sub-quarter 8 w + k
+        const bool hk = (mw >> k) & 1u;
         const uint32_t mk = __ballot_sync(0xffffffffu, hk);
         // stored in reverse depth order (one ballot word: the count is known here)
         if (hk) s_list[8 * w + k][__popc(mk) - 1 - __popc(mk & lt)] = (uint8_t)j;
-        if (lane == 0) s_rel[8 * w + k][wd] = mk;
+        if (!kDirect && lane == 0) s_rel[8 * w + k][wd] = mk;
         base[k] += __popc(mk);
       }
     }
@@ -276,6 +253,7 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
     for (int e = my_cnt + l4; e < steps; e += 4) s_list[sub][e] = (uint8_t)kBatch;
     __syncwarp();
     const uint8_t* my_list = s_list[sub];
+#pragma unroll kUnroll
     for (int s = 0; s < steps; ++s) {
       // reverse depth order; the sentinel has a = 0 for every pixel, so T (T / 1) and G.A stay
       // exactly unchanged whatever j is, and its s_part column kBatch is padding
@@ -307,10 +285,21 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
       float y[2];
       reduce_scatter8_quad(acc, y);
       // the lane holds values vb, vb + 1 (vb = 4 (l4 >> 1) + 2 (l4 & 1)); the per-splat
-      // scale factors are applied once per entry in the flush
+      // scale factors are applied once per entry in the flush (slot mode) or per splat by K8
       const int vb = 4 * (l4 >> 1) + 2 * (l4 & 1);
-      s_part[sub][vb][jj] = y[0];  // the sentinel writes the padding column
-      s_part[sub][vb + 1][jj] = y[1];
+      if constexpr (kDirect) {
+        // the sub-quarter's pre-reduced share goes straight to the splat's 2D gradient in L2
+        // (4 lanes = one 32-B sector); the sentinel and exact zeros send nothing
+        if (jj < kBatch && (y[0] != 0.0f || y[1] != 0.0f))
+          red_add_v2(grad2d + 8 * (size_t)cur.slot[jj] + vb, y[0], y[1]);
+      } else {
+        s_part[sub][vb][jj] = y[0];  // the sentinel writes the padding column
+        s_part[sub][vb + 1][jj] = y[1];
+      }
+    }
+    if constexpr (kDirect) {
+      hi = lo;  // the next batch's barrier orders the staging buffers
+      continue;
     }
     __syncthreads();
     // combine the sub-quarters in a fixed order and write each (tile, splat) pair's slot:
@@ -402,13 +391,15 @@ __global__ void __launch_bounds__(kReduceThreads) k_loss_reduce(
 }
 
 void launch_blend_bwd(const FrameParams& fp, const uint2* ranges, const uint2* sorted,
-                      const RenderRec* rec, const unsigned long long* total, int64_t key_cap,
+                      const uint16_t* submask, const RenderRec* rec,
+                      const unsigned long long* total, int64_t key_cap,
                       const float* img, const float* target, const float* t_last,
                       const uint32_t* n_proc, float loss_scale, float4* partial,
-                      double* tile_loss, bool given_dldc, cudaStream_t st) {
-  launch_pdl(given_dldc ? k_blend_bwd<true> : k_blend_bwd<false>, dim3(fp.n_tiles), dim3(kBT),
-             0, st, fp, ranges, sorted, rec, total, key_cap, img, target, t_last, n_proc,
-             loss_scale, partial, tile_loss);
+                      double* tile_loss, bool given_dldc, float* grad2d, cudaStream_t st) {
+  auto k = grad2d ? (given_dldc ? k_blend_bwd<true, true> : k_blend_bwd<false, true>)
+                  : (given_dldc ? k_blend_bwd<true, false> : k_blend_bwd<false, false>);
+  launch_pdl(k, dim3(fp.n_tiles), dim3(kBT), 0, st, fp, ranges, sorted, submask, rec, total,
+             key_cap, img, target, t_last, n_proc, loss_scale, partial, tile_loss, grad2d);
 }
 
 void launch_loss_reduce(const double* tile_loss, int n_tiles, double scale, double* accum,

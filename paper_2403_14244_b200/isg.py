@@ -114,6 +114,7 @@ def lib() -> C.CDLL:
         "isg_debug_pixel_state": ([P, P, P], C.c_int),
         "isg_count_pairs": ([P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)], C.c_int),
         "isg_set_binning": ([P, C.c_int], C.c_int),
+        "isg_set_deterministic": ([P, C.c_int], C.c_int),
         "isg_profile_enable": ([P, C.c_int], C.c_int),
         "isg_profile_num_stages": ([], C.c_int),
         "isg_profile_stage_name": ([C.c_int], C.c_char_p),
@@ -140,6 +141,7 @@ C_ABI_SYMBOLS = (
     "isg_graph_begin", "isg_graph_end", "isg_graph_launch", "isg_graph_destroy", "isg_nccl_get_unique_id",
     "isg_nccl_init", "isg_nccl_attach", "isg_nccl_info", "isg_set_exchange_chunks",
     "isg_nccl_detach", "isg_debug_bins", "isg_debug_pixel_state", "isg_count_pairs", "isg_set_binning",
+    "isg_set_deterministic",
     "isg_profile_enable",
     "isg_profile_num_stages", "isg_profile_stage_name", "isg_profile_read", "isg_synth_scene",
     "isg_synth_camera",
@@ -528,6 +530,11 @@ class Renderer:
         _check(self._h, lib().isg_nccl_detach(self._h))
 
     BINNING_TILE_BUCKET, BINNING_RADIX = 0, 1
+
+    def set_deterministic(self, on: bool = True):
+        """Slot-mode gradient accumulation (bitwise deterministic) instead of the default
+        direct L2 reduction (isg_set_deterministic)."""
+        _check(self._h, lib().isg_set_deterministic(self._h, int(bool(on))))
 
     def set_binning(self, mode: int):
         """0 = tile-bucket, 1 = onesweep radix (default); bit-identical tile lists."""
