@@ -126,6 +126,7 @@ struct isg_ctx {
 
   // frame state
   bool have_frame = false;
+  bool last_tracked = false;  // the last frame recorded t_last / n_proc
   isg::FrameParams last_fp{};
   bool pending = false;  // `partial` holds an un-projected view
   isg::FrameParams pending_fp{};
@@ -442,7 +443,8 @@ isg_status flush_pending(isg_ctx* ctx) {
 
 // Launch one frame: K1, depth sort, scan/emit, tile sort, ranges, K6 into `out` (nullptr =
 // the context's own image buffer, resolved after it is sized for this camera).
-isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out) {
+// track: the forward also records the per-pixel state the backward starts from.
+isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out, bool track) {
   isg_status s = flush_pending(ctx);
   if (s != ISG_OK) return s;
   if ((s = ensure_pixels(ctx, fp.cam.width, fp.cam.height)) != ISG_OK) return s;
@@ -542,10 +544,11 @@ isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out) {
     ISG_CUDA(cudaMemsetAsync(ctx->ranges, 0, sizeof(uint2) * fp.n_tiles, st));
   }
   ISG_STAGE(ST_BLEND_FWD);
-  isg::launch_blend_fwd(fp, ctx->ranges, ctx->sorted, ctx->submask, ctx->rec, ctx->total, ctx->key_cap, out,
-                        ctx->t_last, ctx->n_proc, st);
+  isg::launch_blend_fwd(fp, ctx->ranges, ctx->sorted, ctx->submask, ctx->rec, ctx->total,
+                        ctx->key_cap, out, ctx->t_last, ctx->n_proc, track, st);
   ISG_CHECK_LAUNCH();
   ctx->launches++;
+  ctx->last_tracked = track;
   ctx->have_frame = true;
   ctx->last_fp = fp;
   ctx->frame_unchecked = true;
@@ -917,7 +920,7 @@ isg_status isg_render_device(isg_ctx* ctx, const isg_camera* cam, const float bg
   cudaSetDevice(ctx->device);
   isg_status s = validate_camera(ctx, cam);
   if (s != ISG_OK) return s;
-  return launch_frame(ctx, make_fp(cam, bg, t_min), out_dev);
+  return launch_frame(ctx, make_fp(cam, bg, t_min), out_dev, false);
 }
 
 isg_status isg_render(isg_ctx* ctx, const isg_camera* cam, const float bg[3], float t_min,
@@ -932,7 +935,7 @@ isg_status isg_render(isg_ctx* ctx, const isg_camera* cam, const float bg[3], fl
   if ((s = check_async(ctx)) != ISG_OK) return s;
   const FrameParams fp = make_fp(cam, bg, t_min);
   for (int attempt = 0; attempt < 3; ++attempt) {
-    if ((s = launch_frame(ctx, fp, nullptr)) != ISG_OK) return s;
+    if ((s = launch_frame(ctx, fp, nullptr, false)) != ISG_OK) return s;
     // image read-back queued behind the frame; one synchronisation covers both
     ISG_CUDA(cudaMemcpyAsync(out_hwc3, ctx->img, sizeof(float) * 3 * (size_t)cam->width * cam->height,
                              cudaMemcpyDeviceToHost, ctx->stream));
@@ -955,7 +958,7 @@ isg_status isg_loss_backward_device(isg_ctx* ctx, const isg_camera* cam, const f
   if (s != ISG_OK) return s;
   if ((s = check_loss_size(ctx, cam->width, cam->height)) != ISG_OK) return s;
   const FrameParams fp = make_fp(cam, bg, t_min);
-  if ((s = launch_frame(ctx, fp, nullptr)) != ISG_OK) return s;
+  if ((s = launch_frame(ctx, fp, nullptr, true)) != ISG_OK) return s;
   return run_backward(ctx, fp, target_dev, weight);
 }
 
@@ -982,7 +985,7 @@ isg_status isg_loss_backward(isg_ctx* ctx, const isg_camera* cam, const float bg
                            cudaMemcpyHostToDevice, ctx->copy_stream));
   ISG_CUDA(cudaEventRecord(ctx->ev_copy, ctx->copy_stream));
   for (int attempt = 0; attempt < 3; ++attempt) {
-    if ((s = launch_frame(ctx, fp, nullptr)) != ISG_OK) return s;
+    if ((s = launch_frame(ctx, fp, nullptr, true)) != ISG_OK) return s;
     ISG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_copy, 0));
     if ((s = run_backward(ctx, fp, ctx->target, weight)) != ISG_OK) return s;
     bool ov = false;
@@ -1116,7 +1119,7 @@ isg_status isg_eval_loss(isg_ctx* ctx, const isg_camera* cam, const float bg[3],
   const int W = cam->width, H = cam->height;
   if (ctx->loss_kind == ISG_LOSS_L1_DSSIM && (s = ensure_image_loss(ctx, W, H)) != ISG_OK) return s;
   for (int attempt = 0; attempt < 3; ++attempt) {
-    if ((s = launch_frame(ctx, fp, nullptr)) != ISG_OK) return s;
+    if ((s = launch_frame(ctx, fp, nullptr, false)) != ISG_OK) return s;
     if (ctx->loss_kind == ISG_LOSS_L1_DSSIM) {
       ISG_STAGE(ST_IMAGE_LOSS);
       ctx->launches += isg::launch_image_loss(W, H, ctx->img, target_dev, ctx->lambda,
@@ -1502,6 +1505,13 @@ isg_status isg_debug_pixel_state(isg_ctx* ctx, float* t_last, uint32_t* n_proc) 
   if (!ctx) return ISG_E_ARG;
   if (!ctx->have_frame) return fail(ctx, ISG_E_STATE, "debug_pixel_state: no frame rendered yet");
   cudaSetDevice(ctx->device);
+  if (!ctx->last_tracked) {
+    // render-only frames skip the per-pixel bookkeeping: re-run the last frame with it (into
+    // the context's own image)
+    isg_status s = flush_pending(ctx);
+    if (s != ISG_OK) return s;
+    if ((s = launch_frame(ctx, ctx->last_fp, nullptr, true)) != ISG_OK) return s;
+  }
   const size_t pix = (size_t)ctx->last_fp.cam.width * ctx->last_fp.cam.height;
   if (t_last) ISG_CUDA(cudaMemcpyAsync(t_last, ctx->t_last, sizeof(float) * pix, cudaMemcpyDeviceToHost, ctx->stream));
   if (n_proc) ISG_CUDA(cudaMemcpyAsync(n_proc, ctx->n_proc, sizeof(uint32_t) * pix, cudaMemcpyDeviceToHost, ctx->stream));

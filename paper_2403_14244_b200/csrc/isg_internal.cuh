@@ -152,7 +152,9 @@ void launch_ranges_fix(const uint32_t* n_keys, int64_t key_cap, int n_tiles, uin
 void launch_blend_fwd(const FrameParams& fp, const uint2* ranges, const uint2* sorted,
                       const uint16_t* submask,
                       const RenderRec* rec, unsigned long long* total, int64_t key_cap,
-                      float* out, float* t_last, uint32_t* n_proc, cudaStream_t st);
+                      float* out, float* t_last, uint32_t* n_proc, bool track, cudaStream_t st);
+// (track: also write t_last / n_proc, the backward's per-pixel state; render-only frames
+// skip that bookkeeping)
 // Writes every pair's 2D gradient to partial[2 slot], partial[2 slot + 1].
 // given_dldc: `target` is dL/dC (G = loss_scale * target) and tile_loss is not meaningful;
 // otherwise G = 2 loss_scale (img - target) and tile_loss[t] = sum over the tile of |d|^2.

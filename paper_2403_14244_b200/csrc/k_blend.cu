@@ -61,6 +61,9 @@ struct FwdPair {
 
 __device__ __forceinline__ float2 bc(float v) { return make_float2(v, v); }
 
+// kTrack: also record, per pixel, the transmittance before and the index of the last
+// contributor (the backward's starting state); a render-only frame skips it.
+template <bool kTrack>
 __device__ __forceinline__ void fwd_pair(FwdPair& p, float2 r2, const float4 g, const float4 c,
                                          float t_min, uint32_t idx) {
   const bool in0 = !(r2.x > g.z) && (p.T.x > t_min);
@@ -72,14 +75,17 @@ __device__ __forceinline__ void fwd_pair(FwdPair& p, float2 r2, const float4 g, 
   p.Cr = __ffma2_rn(wgt, bc(c.x), p.Cr);
   p.Cg = __ffma2_rn(wgt, bc(c.y), p.Cg);
   p.Cb = __ffma2_rn(wgt, bc(c.z), p.Cb);
-  p.Tl = make_float2(in0 ? p.T.x : p.Tl.x, in1 ? p.T.y : p.Tl.y);
-  p.np0 = in0 ? idx : p.np0;
-  p.np1 = in1 ? idx : p.np1;
+  if constexpr (kTrack) {
+    p.Tl = make_float2(in0 ? p.T.x : p.Tl.x, in1 ? p.T.y : p.Tl.y);
+    p.np0 = in0 ? idx : p.np0;
+    p.np1 = in1 ? idx : p.np1;
+  }
   p.T = __fmul2_rn(p.T, __fadd2_rn(bc(1.0f), make_float2(-a.x, -a.y)));  // T (1 - a)
 }
 
 }  // namespace
 
+template <bool kTrack>
 __global__ void ISG_FWD_BOUNDS k_blend_fwd(
     FrameParams fp, const uint2* __restrict__ ranges, const uint2* __restrict__ sorted,
     const uint16_t* __restrict__ submask,
@@ -183,7 +189,7 @@ __global__ void ISG_FWD_BOUNDS k_blend_fwd(
       for (int k = 0; k < 2; ++k) {
         const float dyk = k ? dy.y : dy.x;
         const float2 r2 = __fadd2_rn(ax, bc(__fmul_rn(dyk, dyk)));
-        fwd_pair(P[k], r2, g, c, t_min, idx);
+        fwd_pair<kTrack>(P[k], r2, g, c, t_min, idx);
       }
     }
   }
@@ -201,8 +207,10 @@ __global__ void ISG_FWD_BOUNDS k_blend_fwd(
       out[3 * pix + 0] = (i ? P[k].Cr.y : P[k].Cr.x) + T * fp.bg[0];
       out[3 * pix + 1] = (i ? P[k].Cg.y : P[k].Cg.x) + T * fp.bg[1];
       out[3 * pix + 2] = (i ? P[k].Cb.y : P[k].Cb.x) + T * fp.bg[2];
-      t_last[pix] = i ? P[k].Tl.y : P[k].Tl.x;
-      n_proc[pix] = i ? P[k].np1 : P[k].np0;
+      if constexpr (kTrack) {
+        t_last[pix] = i ? P[k].Tl.y : P[k].Tl.x;
+        n_proc[pix] = i ? P[k].np1 : P[k].np0;
+      }
     }
   }
 }
@@ -263,10 +271,10 @@ void launch_count_pairs(const FrameParams& fp, const uint2* ranges, const uint2*
 
 void launch_blend_fwd(const FrameParams& fp, const uint2* ranges, const uint2* sorted,
                       const uint16_t* submask, const RenderRec* rec, unsigned long long* total,
-                      int64_t key_cap, float* out, float* t_last, uint32_t* n_proc,
+                      int64_t key_cap, float* out, float* t_last, uint32_t* n_proc, bool track,
                       cudaStream_t st) {
-  launch_pdl(k_blend_fwd, dim3(fp.n_tiles), dim3(kBT), 0, st, fp, ranges, sorted, submask, rec,
-             total, key_cap, out, t_last, n_proc);
+  launch_pdl(track ? k_blend_fwd<true> : k_blend_fwd<false>, dim3(fp.n_tiles), dim3(kBT), 0, st,
+             fp, ranges, sorted, submask, rec, total, key_cap, out, t_last, n_proc);
 }
 
 }  // namespace isg
