@@ -54,8 +54,9 @@ struct Stage {
 // Stage list entries [beg, beg+cnt) of the sorted (splat, slot) array (thread t: entries t,
 // t + NT, ...).  The 32-B record gathers are issued as cp.async; the caller waits + barriers
 // before use.
-// kSplat: st.slot holds the splat index instead of the pair's gradient slot.
-template <int NT, int B, bool kSplat = false>
+// kSplat: st.slot holds the splat index instead of the pair's gradient slot.  kMask: also stage
+// the entries' sub-quarter masks.
+template <int NT, int B, bool kSplat = false, bool kMask = true>
 __device__ __forceinline__ void stage_batch(Stage<B>& st, const uint2* __restrict__ sorted,
                                             const uint16_t* __restrict__ submask,
                                             const RenderRec* __restrict__ rec, uint32_t beg,
@@ -65,7 +66,7 @@ __device__ __forceinline__ void stage_batch(Stage<B>& st, const uint2* __restric
     if (t < cnt) {
       const uint2 gs = sorted[beg + t];  // (splat, gradient slot)
       st.slot[t] = kSplat ? gs.x : gs.y;
-      st.mask[t] = submask[beg + t];
+      if (kMask) st.mask[t] = submask[beg + t];
       cp_async16(&st.geo[t], &rec[gs.x].geo);
       cp_async16(&st.col[t], &rec[gs.x].col);
     }

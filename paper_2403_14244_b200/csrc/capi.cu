@@ -508,9 +508,7 @@ isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out, bool tr
     topt.epi.emit_gid = ctx->emit_gid;
     topt.epi.sorted = ctx->sorted;
     topt.epi.ranges = ctx->ranges;
-    topt.epi.rec = ctx->rec;
-    topt.epi.submask = ctx->submask;
-    topt.epi.fp = fp;
+
     isg::radix_sort_pairs(ctx->tkey, ctx->tval, true, ctx->sc + 0, ctx->key_cap,
                           bits_for(fp.n_tiles), ctx->sort_tile, st, &ctx->launches, topt);
     ISG_CHECK_LAUNCH();
@@ -536,7 +534,7 @@ isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out, bool tr
     {
     ISG_STAGE(ST_TILE_SORT);
     isg::launch_tile_sort(fp, ctx->ranges, ctx->bucket, ctx->total, ctx->key_cap, ctx->sorted,
-                          ctx->partial, ctx->rec, ctx->submask, st);
+                          ctx->partial, st);
     ISG_CHECK_LAUNCH();
     ctx->launches++;
     }

@@ -87,9 +87,6 @@ struct SortEpilogue {
   const uint32_t* emit_gid = nullptr;
   uint2* sorted = nullptr;
   uint2* ranges = nullptr;
-  const RenderRec* rec = nullptr;  // + the pairs' sub-quarter masks (sub_mask16)
-  uint16_t* submask = nullptr;
-  FrameParams fp{};
 };
 struct SortOptions {
   bool scratch_zeroed = false;  // hist / counters / look-back already zero (one frame memset)
@@ -127,10 +124,9 @@ void launch_fill(const float4* ms, const uint32_t* ntiles, const uint2* tilebox,
                  unsigned long long* bucket, uint32_t* slot_of, uint32_t* slot_off, int64_t cap,
                  unsigned long long* lookback, uint32_t* counter, cudaStream_t st);
 // scratch: the gradient-slot buffer (2 float4 per key), used only for tiles > 2048 entries.
-// Also writes each pair's sub-quarter mask (sub_mask16) to submask.
 void launch_tile_sort(const FrameParams& fp, const uint2* ranges, const unsigned long long* bucket,
                       const unsigned long long* total, int64_t cap, uint2* sorted, float4* scratch,
-                      const RenderRec* rec, uint16_t* submask, cudaStream_t st);
+                      cudaStream_t st);
 
 // ---- radix binning (k_sort.cu) ------------------------------------------------------------
 int64_t scan_emit_scratch_words(int64_t n);  // + 1 zeroed u64 words
@@ -148,13 +144,15 @@ void launch_ranges_fix(const uint32_t* n_keys, int64_t key_cap, int n_tiles, uin
 
 // ---- blending (k_blend.cu) ----------------------------------------------------------------
 // sorted: per list entry (splat, gradient slot), tile-major, (depth, index) order per tile;
-// submask: per list entry, the 4x4 sub-quarters of the tile the splat reaches (sub_mask16).
+// submask: per list entry, the 4x4 sub-quarters of the tile the splat's 3-sigma circle reaches
+// (bit 8 w + k: group k of warp w; the closest-point tests K6 makes anyway), written by a
+// tracked forward for the backward of the same frame.
 void launch_blend_fwd(const FrameParams& fp, const uint2* ranges, const uint2* sorted,
-                      const uint16_t* submask,
+                      uint16_t* submask,
                       const RenderRec* rec, unsigned long long* total, int64_t key_cap,
                       float* out, float* t_last, uint32_t* n_proc, bool track, cudaStream_t st);
-// (track: also write t_last / n_proc, the backward's per-pixel state; render-only frames
-// skip that bookkeeping)
+// (track: also write t_last / n_proc and submask, the backward's per-pixel and per-entry
+// state; render-only frames skip that bookkeeping)
 // Writes every pair's 2D gradient to partial[2 slot], partial[2 slot + 1].
 // given_dldc: `target` is dL/dC (G = loss_scale * target) and tile_loss is not meaningful;
 // otherwise G = 2 loss_scale (img - target) and tile_loss[t] = sum over the tile of |d|^2.

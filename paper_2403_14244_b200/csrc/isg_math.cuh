@@ -91,44 +91,6 @@ __device__ __forceinline__ bool tile_bbox(float u, float v, float s, int tiles_x
   return true;
 }
 
-// Sub-quarter relevance of a (tile, splat) pair, computed once per pair by the binning and
-// read by both blend kernels: bit s is set when the splat's 3-sigma circle (centre (u, v),
-// r2max = 9 sigma2d^2) reaches the pixel-centre box of the tile's 4x4 sub-quarter s inside the
-// image (closest-point test, exact rounding: a conservative superset of the per-pixel test).
-// s is the blend kernels' group numbering, s = 8 w + k for group k of warp w: column
-// c = 2 ((s >> 2) & 1) + (s & 1), row r = 2 (s >> 3) + ((s >> 1) & 1).
-__device__ __forceinline__ uint32_t sub_mask16(float u, float v, float r2max, int tile,
-                                               const FrameParams& fp) {
-  const int tx = tile % fp.tiles_x, ty = tile / fp.tiles_x;
-  const int W = fp.cam.width, H = fp.cam.height;
-  float ax[4], ay[4];
-  uint32_t cv = 0, rv = 0;
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const int xs = tx * kTile + 4 * c;
-    cv |= (xs < W ? 1u : 0u) << c;
-    const float lo = (float)xs + 0.5f, hi = (float)(min(xs + 4, W) - 1) + 0.5f;
-    const float d = __fsub_rn(fminf(fmaxf(u, lo), hi), u);
-    ax[c] = __fmul_rn(d, d);
-  }
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int ys = ty * kTile + 4 * r;
-    rv |= (ys < H ? 1u : 0u) << r;
-    const float lo = (float)ys + 0.5f, hi = (float)(min(ys + 4, H) - 1) + 0.5f;
-    const float d = __fsub_rn(fminf(fmaxf(v, lo), hi), v);
-    ay[r] = __fmul_rn(d, d);
-  }
-  uint32_t mask = 0;
-#pragma unroll
-  for (int s = 0; s < 16; ++s) {
-    const int c = 2 * ((s >> 2) & 1) + (s & 1), r = 2 * (s >> 3) + ((s >> 1) & 1);
-    const bool hit = ((cv >> c) & (rv >> r) & 1u) && !(__fadd_rn(ax[c], ay[r]) > r2max);
-    mask |= (hit ? 1u : 0u) << s;
-  }
-  return mask;
-}
-
 // Visit the tiles a splat touches, in row-major order (the order K1 counted them).  `box` is
 // K1's compact record: x0 | y0 << 12 | bw << 24 and a hit mask over the (<= 32-tile) bbox; for
 // bigger boxes (bw == 0) the projection and the exact tile tests are recomputed from `ms`.

@@ -169,9 +169,7 @@ __device__ __forceinline__ void bitonic_smem(unsigned long long* key, uint32_t* 
 // (not yet used) gradient-slot storage of this tile's range.
 __device__ void long_list_sort(const unsigned long long* __restrict__ bucket, uint32_t start,
                                int L, unsigned long long* skey, uint32_t* sidx,
-                               ulonglong2* bufA, ulonglong2* bufB, uint2* __restrict__ sorted,
-                               const RenderRec* __restrict__ rec, uint16_t* __restrict__ submask,
-                               const FrameParams& fp) {
+                               ulonglong2* bufA, ulonglong2* bufB, uint2* __restrict__ sorted) {
   for (int r0 = 0; r0 < L; r0 += kSortCap) {
     const int m = min(kSortCap, L - r0);
     int P = 1;
@@ -217,16 +215,13 @@ __device__ void long_list_sort(const unsigned long long* __restrict__ bucket, ui
   for (int i = threadIdx.x; i < L; i += blockDim.x) {
     const ulonglong2 e = src[i];
     sorted[start + i] = make_uint2((uint32_t)e.x, start + (uint32_t)e.y);
-    const float4 geo = rec[(uint32_t)e.x].geo;
-    submask[start + i] = (uint16_t)sub_mask16(geo.x, geo.y, geo.z, (int)blockIdx.x, fp);
   }
 }
 
 __global__ void __launch_bounds__(kTsThreads) k_tile_sort(
     const uint2* __restrict__ ranges, const unsigned long long* __restrict__ bucket,
     const unsigned long long* __restrict__ total, int64_t cap, uint2* __restrict__ sorted,
-    float4* __restrict__ scratch, const RenderRec* __restrict__ rec,
-    uint16_t* __restrict__ submask, FrameParams fp) {
+    float4* __restrict__ scratch) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned long long* skey = reinterpret_cast<unsigned long long*>(smem_raw);
   uint32_t* sidx = reinterpret_cast<uint32_t*>(skey + kSortCap);
@@ -236,7 +231,7 @@ __global__ void __launch_bounds__(kTsThreads) k_tile_sort(
   if (L == 0) return;
   if (L > kSortCap) {
     ulonglong2* bufA = reinterpret_cast<ulonglong2*>(scratch + 2 * (size_t)rg.x);
-    long_list_sort(bucket, rg.x, L, skey, sidx, bufA, bufA + L, sorted, rec, submask, fp);
+    long_list_sort(bucket, rg.x, L, skey, sidx, bufA, bufA + L, sorted);
     return;
   }
   int P = 1;
@@ -247,12 +242,8 @@ __global__ void __launch_bounds__(kTsThreads) k_tile_sort(
   }
   __syncthreads();
   bitonic_smem(skey, sidx, P);
-  for (int i = threadIdx.x; i < L; i += blockDim.x) {
-    const uint32_t g = (uint32_t)skey[i];
-    sorted[rg.x + i] = make_uint2(g, rg.x + sidx[i]);
-    const float4 geo = rec[g].geo;
-    submask[rg.x + i] = (uint16_t)sub_mask16(geo.x, geo.y, geo.z, (int)blockIdx.x, fp);
-  }
+  for (int i = threadIdx.x; i < L; i += blockDim.x)
+    sorted[rg.x + i] = make_uint2((uint32_t)skey[i], rg.x + sidx[i]);
 }
 
 // ---- launchers --------------------------------------------------------------------------------
@@ -277,10 +268,9 @@ void launch_fill(const float4* ms, const uint32_t* ntiles, const uint2* tilebox,
 
 void launch_tile_sort(const FrameParams& fp, const uint2* ranges, const unsigned long long* bucket,
                       const unsigned long long* total, int64_t cap, uint2* sorted, float4* scratch,
-                      const RenderRec* rec, uint16_t* submask, cudaStream_t st) {
+                      cudaStream_t st) {
   const size_t smem = kSortCap * (sizeof(unsigned long long) + sizeof(uint32_t));
-  k_tile_sort<<<fp.n_tiles, kTsThreads, smem, st>>>(ranges, bucket, total, cap, sorted, scratch,
-                                                    rec, submask, fp);
+  k_tile_sort<<<fp.n_tiles, kTsThreads, smem, st>>>(ranges, bucket, total, cap, sorted, scratch);
 }
 
 }  // namespace isg

@@ -88,7 +88,7 @@ __device__ __forceinline__ void fwd_pair(FwdPair& p, float2 r2, const float4 g, 
 template <bool kTrack>
 __global__ void ISG_FWD_BOUNDS k_blend_fwd(
     FrameParams fp, const uint2* __restrict__ ranges, const uint2* __restrict__ sorted,
-    const uint16_t* __restrict__ submask,
+    uint16_t* __restrict__ submask,
     const RenderRec* __restrict__ rec, unsigned long long* __restrict__ total,
     int64_t key_cap, float* __restrict__ out, float* __restrict__ t_last,
     uint32_t* __restrict__ n_proc) {
@@ -118,6 +118,25 @@ __global__ void ISG_FWD_BOUNDS k_blend_fwd(
   const int y0 = ty * kTile + (q >> 1) * 8 + (sq >> 1) * 4 + 2 * (l4 >> 1);
   const float2 PX = make_float2((float)x0 + 0.5f, (float)x0 + 1.5f);
   const float2 PY = make_float2((float)y0 + 0.5f, (float)y0 + 1.5f);
+  // the warp's 8 sub-quarters: 4 columns of the tile (x = 4c) x 2 rows (y = 8w + 4r)
+  float cx0[4], cx1[4], ry0[2], ry1[2];
+  bool cv[4], rv[2];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int xs = tx * kTile + 4 * c;
+    cv[c] = xs < W;
+    cx0[c] = (float)xs + 0.5f;
+    cx1[c] = (float)(min(xs + 4, W) - 1) + 0.5f;
+  }
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int ys = ty * kTile + 8 * w + 4 * r;
+    rv[r] = ys < H;
+    ry0[r] = (float)ys + 0.5f;
+    ry1[r] = (float)(min(ys + 4, H) - 1) + 0.5f;
+  }
+  // tracked frames leave each entry's relevance bits for the backward: byte w of submask[e]
+  uint8_t* const mask_bytes = reinterpret_cast<uint8_t*>(submask);
   const uint2 rg = ranges[tile];
   const int n = rg.x == kEmptyRange ? 0 : (int)(rg.y - rg.x);
   const float t_min = fp.t_min;
@@ -134,7 +153,7 @@ __global__ void ISG_FWD_BOUNDS k_blend_fwd(
   }
   const uint32_t lt = (1u << lane) - 1u;
 
-  if (n > 0) stage_batch<kBT>(st[0], sorted, submask, rec, rg.x, min(kBatch, n));
+  if (n > 0) stage_batch<kBT, kBatch + 1, false, false>(st[0], sorted, submask, rec, rg.x, min(kBatch, n));
   for (int b = 0, it = 0; b < n; b += kBatch, ++it) {
     Stage<kBatch + 1>& cur = st[it & 1];
     cp_async_wait_all();
@@ -142,12 +161,15 @@ __global__ void ISG_FWD_BOUNDS k_blend_fwd(
                       P[1].T.y > t_min;
     if (__syncthreads_count(live) == 0) break;  // barrier: batch visible, previous consumed
     if (b + kBatch < n)
-      stage_batch<kBT>(st[(it + 1) & 1], sorted, submask, rec, rg.x + b + kBatch,
+      stage_batch<kBT, kBatch + 1, false, false>(st[(it + 1) & 1], sorted, submask, rec, rg.x + b + kBatch,
                        min(kBatch, n - b - kBatch));
-    // relevance of the batch for the warp's 8 sub-quarters -> 8 compacted lists, from the
-    // pairs' precomputed sub-quarter masks (sub_mask16: the binning's closest-point tests,
-    // bit-identical decisions; a conservative superset of the per-pixel test).
-    // a warp whose 128 pixels all terminated skips the lists (it still joins the barriers)
+    // relevance of the batch for the warp's 8 sub-quarters -> 8 compacted lists.  The tests
+    // share their per-axis terms (rounded squares of the distances to the 4 columns and 2
+    // rows) and add one pair exactly as dist2_rn would at the sub-quarter's closest pixel
+    // centre (bit-identical decisions; a conservative superset of the per-pixel test).
+    // a warp whose 128 pixels all terminated skips the tests (it still joins the barriers;
+    // its mask bytes stay unwritten, which the backward tolerates: those pixels' walks ended
+    // before the batch, so any bits only add entries that contribute exact zeros)
     const uint32_t alive = __ballot_sync(0xffffffffu, live);
     const int cnt = alive ? min(kBatch, n - b) : 0;
     int base[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -155,14 +177,30 @@ __global__ void ISG_FWD_BOUNDS k_blend_fwd(
     for (int wd = 0; wd < kWords; ++wd) {
       if (32 * wd >= cnt) break;  // warp-uniform
       const int j = 32 * wd + lane;
-      const uint32_t mw = j < cnt ? ((uint32_t)cur.mask[j] >> (8 * w)) & 0xFFu : 0u;
+      const bool in = j < cnt;
+      const float4 g = cur.geo[in ? j : 0];
+      float ax4[4], ay2[2];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {  // group k = sub-quarter 8 w + k
-        const bool hk = (mw >> k) & 1u;
+      for (int c = 0; c < 4; ++c) {
+        const float d = __fsub_rn(fminf(fmaxf(g.x, cx0[c]), cx1[c]), g.x);
+        ax4[c] = __fmul_rn(d, d);
+      }
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const float d = __fsub_rn(fminf(fmaxf(g.y, ry0[r]), ry1[r]), g.y);
+        ay2[r] = __fmul_rn(d, d);
+      }
+      uint32_t mw = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {  // group k: quarter 2w + (k >> 2), sub (k & 3)
+        const int c = (k >> 2) * 2 + (k & 1), r = (k >> 1) & 1;
+        const bool hk = in && cv[c] && rv[r] && !(__fadd_rn(ax4[c], ay2[r]) > g.z);
+        mw |= (hk ? 1u : 0u) << k;
         const uint32_t mk = __ballot_sync(0xffffffffu, hk);
         if (hk) s_list[8 * w + k][base[k] + __popc(mk & lt)] = (uint8_t)j;
         base[k] += __popc(mk);
       }
+      if (kTrack && in) mask_bytes[2 * ((size_t)rg.x + b + j) + w] = (uint8_t)mw;
     }
     // a sub-quarter whose 16 pixels have all terminated walks nothing
     int steps = 0, my_cnt = 0;
@@ -270,7 +308,7 @@ void launch_count_pairs(const FrameParams& fp, const uint2* ranges, const uint2*
 }
 
 void launch_blend_fwd(const FrameParams& fp, const uint2* ranges, const uint2* sorted,
-                      const uint16_t* submask, const RenderRec* rec, unsigned long long* total,
+                      uint16_t* submask, const RenderRec* rec, unsigned long long* total,
                       int64_t key_cap, float* out, float* t_last, uint32_t* n_proc, bool track,
                       cudaStream_t st) {
   launch_pdl(track ? k_blend_fwd<true> : k_blend_fwd<false>, dim3(fp.n_tiles), dim3(kBT), 0, st,

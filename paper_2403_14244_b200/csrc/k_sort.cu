@@ -221,10 +221,7 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
       const uint32_t k = S.keys[i];
       const uint32_t o = S.bin_base[(k >> shift) & 255u] + (uint32_t)i;
       const uint32_t v = S.vals[i];
-      const uint32_t g = ISG_EPI_PREFETCH ? S.gids[i] : epi.emit_gid[v];
-      epi.sorted[o] = make_uint2(g, v);
-      const float4 geo = epi.rec[g].geo;
-      epi.submask[o] = (uint16_t)sub_mask16(geo.x, geo.y, geo.z, (int)k, epi.fp);
+      epi.sorted[o] = make_uint2(ISG_EPI_PREFETCH ? S.gids[i] : epi.emit_gid[v], v);
       if (i == 0 || S.keys[i - 1] != k) atomicMin(&epi.ranges[k].x, o);
       if (i == nvalid - 1 || S.keys[i + 1] != k) atomicMax(&epi.ranges[k].y, o + 1u);
     }
