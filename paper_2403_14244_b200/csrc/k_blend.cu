@@ -30,11 +30,11 @@ constexpr int kBT = 64;      // threads per tile CTA: 2 warps x 8 four-lane grou
 #ifndef ISG_FWD_BATCH
 #define ISG_FWD_BATCH 128
 #endif
-// An explicit minimum of 1 CTA/SM lets ptxas use 106 registers instead of its default 80:
-// measured 4.5% faster (C3 0.263 vs 0.275 ms); capping for occupancy (72 / 64 registers) is
-// slower.
+// Register budget: a 12-CTA/SM minimum (80 registers) measured fastest for the relevance-testing
+// forward of a train step (0.259 vs 0.275 ms at 116 registers with a 1-CTA minimum; 8 and 10
+// CTAs in between).
 #ifndef ISG_FWD_MINB
-#define ISG_FWD_MINB 1
+#define ISG_FWD_MINB 12
 #endif
 #if ISG_FWD_MINB > 0
 #define ISG_FWD_BOUNDS __launch_bounds__(kBT, ISG_FWD_MINB)
