@@ -93,7 +93,7 @@ def config_dict(args, world: int) -> dict:
 FWD_FLOP_EVAL, FWD_FLOP_IN = 6, 12      # 3-sigma test; exp+alpha+composite+transmittance
 BWD_FLOP_EVAL, BWD_FLOP_IN = 6, 36      # same test; transmittance recovery + 7 gradients
 FP32_LANES = 148 * 128
-NCU_SUMMARY = "profiles/r1/ncu_full_step.json"  # dram traffic per launch, --set full capture
+NCU_SUMMARY = "profiles/r2/ncu_full_step.json"  # dram traffic per launch, --set full capture
 
 
 def stage_bytes(n, keys, tiles):

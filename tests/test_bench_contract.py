@@ -9,9 +9,9 @@ from pathlib import Path
 
 import pytest
 
-PROFILES = Path(__file__).resolve().parents[1] / "profiles" / "r1"
+PROFILES = Path(__file__).resolve().parents[1] / "profiles" / "r2"
 ARM_FILES = ["bench_c1.jsonl", "bench_c2.jsonl", "bench_c3.jsonl", "bench_c4.jsonl",
-             "bench_c5.jsonl", "bench_c3_dssim.jsonl"]
+             "bench_c5.jsonl"]
 
 
 def last_line(name):
@@ -40,6 +40,7 @@ def test_isg_arm_line(name):
     assert 0 < r["frac"] < 1 and r["achieved"] > 0
     assert r["frac"] == pytest.approx(r["achieved"] / r["peak"], rel=1e-9)
     c = d["cpu_baseline"]
+    assert c is not None, name
     for k in ("value", "unit", "cores", "kind", "sample"):
         assert k in c, (name, k)
     assert c["kind"] in ("reference", "port") and c["cores"] >= 1
@@ -66,3 +67,18 @@ def test_headline_is_c3_train():
     assert d["metric"] in base["metric"]
     assert d["config"]["n_gaussians"] == 1_000_000
     assert (d["config"]["width"], d["config"]["height"]) == (1920, 1080)
+
+
+def test_headline_carries_render_fps():
+    """The default line also reports BASELINE's second metric (C2 render FPS) with its own e2e
+    and the reference's own render() beside it."""
+    d = last_line("bench_c3.jsonl")
+    r = d["render"]
+    assert r["unit"] == "frames/s" and r["value"] > 0 and r["e2e"]["value"] > 0
+    assert r["e2e"]["d2h_bytes_per_step"] == 1920 * 1080 * 3 * 4
+    assert r["cpu_baseline"]["kind"] == "reference" and r["cpu_baseline"]["value"] > 0
+
+
+def test_reference_arm_shares_the_config():
+    a, b = last_line("bench_c3.jsonl"), last_line("bench_reference.jsonl")
+    assert a["config"] == b["config"] and a["metric"] == b["metric"] and a["unit"] == b["unit"]

@@ -24,6 +24,10 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(SIZES))
     ap.add_argument("--render", action="store_true", help="forward only")
     ap.add_argument("--loss", default="l2", choices=["l2", "l1_dssim"])
+    ap.add_argument("--const-target", action="store_true",
+                    help="a constant target image (no target render frame: the capture then "
+                         "holds only train-step kernels)")
+    ap.add_argument("--deterministic", action="store_true")
     a = ap.parse_args()
     n, W, H = SIZES[a.config]
     ms, co = isg.synth_scene(n, W, H, seed=2403)
@@ -36,9 +40,14 @@ def main():
     r.set_stream(stream.cuda_stream)
     if a.loss == "l1_dssim":
         r.set_loss(isg.LOSS_L1_DSSIM, 0.2)
+    if a.deterministic:
+        r.set_deterministic(True)
     target = torch.empty((H, W, 3), dtype=torch.float32, device="cuda")
-    r.set_scene(tms, tco)
-    r.render_device(cam, opts, target.data_ptr())
+    if a.const_target:
+        target.fill_(0.5)
+    else:
+        r.set_scene(tms, tco)
+        r.render_device(cam, opts, target.data_ptr())
     r.set_scene(ms, co)
     out = torch.empty_like(target)
     for _ in range(a.steps):

@@ -27,6 +27,9 @@ FULL_METRICS = [
     "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
     "smsp__thread_inst_executed_per_inst_executed.ratio", "sm__cycles_elapsed.avg.per_second",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+    "sm__warps_active.avg.per_cycle_active", "smsp__warps_eligible.avg.per_cycle_active",
+    "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem",
+    "lts__t_sectors_op_red.sum", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
 ]
 
 
@@ -73,14 +76,16 @@ def full(rep, out, regex=None):
     rows = list(csv.reader(txt.splitlines()))
     h, units = rows[0], rows[1]
     res = OrderedDict()
+    seen = {}
     for r in rows[2:]:
         d = dict(zip(h, r))
         k = short(d["Kernel Name"])
         if regex and not re.search(regex, k):
             continue
-        if k in res:
-            continue
-        res[k] = {m: f"{d[m]} {units[h.index(m)]}".strip() for m in FULL_METRICS if m in d}
+        # repeated kernels (the sorts' passes) are numbered in launch order: k_onesweep#0, ...
+        seen[k] = seen.get(k, -1) + 1
+        key = k if seen[k] == 0 else f"{k}#{seen[k]}"
+        res[key] = {m: f"{d[m]} {units[h.index(m)]}".strip() for m in FULL_METRICS if m in d}
     json.dump({"source": f"ncu --set full --clock-control none --import-source on, report {rep} "
                          "(not committed)", "kernels": res}, open(out, "w"), indent=1)
     print(json.dumps(res, indent=1)[:2000])
