@@ -36,10 +36,6 @@ constexpr int kBT = 64;      // threads per tile CTA: 2 warps x 8 four-lane grou
 #define ISG_BWD_UNROLL 4
 #endif
 constexpr int kUnroll = ISG_BWD_UNROLL;  // walk steps per loop iteration
-#ifndef ISG_BWD_XCH
-#define ISG_BWD_XCH 0
-#endif
-constexpr bool kXch = ISG_BWD_XCH;  // the 4-lane reduction via shared memory instead of shuffles
 constexpr int kBatch = ISG_BWD_BATCH;  // records staged per batch (32: one ballot per sub-quarter)
 constexpr int kWords = kBatch / 32;
 constexpr int kSubs = 16;    // 4x4 sub-quarters per tile (one per four-lane group)
@@ -134,9 +130,6 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
   __shared__ float s_part[kDirect ? 1 : kSubs][8][kBatch + 1];
   __shared__ uint32_t s_rel[kSubs][kWords];  // relevance ballots of the batch per sub-quarter
   __shared__ uint8_t s_list[kSubs][kListPitch];
-  // direct mode, shared-memory reduction variant: per warp, two step buffers of 2 x 32 float4
-  __shared__ float4 s_xch[kXch ? 2 : 1][2][kXch ? 64 : 1];
-  int xpar = 0;
   __shared__ float s_red[2];
   __shared__ int s_max[2];
   const int tile = blockIdx.x;
@@ -291,24 +284,7 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
 #pragma unroll
       for (int k = 0; k < 8; ++k) acc[k] = acc2[k].x + acc2[k].y;
       float y[2];
-      if constexpr (kDirect && kXch) {
-        // 4-lane reduction through a per-warp shared-memory transpose: every lane stores its 8
-        // values (two conflict-free 16-B stores), then sums values 2 l4, 2 l4 + 1 of the
-        // group's 4 lanes (double-buffered by step parity: one __syncwarp per step)
-        float4* xb = s_xch[w][xpar];
-        xb[lane] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-        xb[32 + lane] = make_float4(acc[4], acc[5], acc[6], acc[7]);
-        __syncwarp();
-        const float2* xb2 = reinterpret_cast<const float2*>(xb) + (l4 >> 1) * 64 + (l4 & 1);
-        float2 t = xb2[2 * (4 * gq)];
-#pragma unroll
-        for (int q = 1; q < 4; ++q) t = __fadd2_rn(t, xb2[2 * (4 * gq + q)]);
-        y[0] = t.x;
-        y[1] = t.y;
-        xpar ^= 1;
-      } else {
-        reduce_scatter8_quad(acc, y);
-      }
+      reduce_scatter8_quad(acc, y);
       // the lane holds values vb, vb + 1 (vb = 4 (l4 >> 1) + 2 (l4 & 1)); the per-splat
       // scale factors are applied once per entry in the flush (slot mode) or per splat by K8
       const int vb = 4 * (l4 >> 1) + 2 * (l4 & 1);
