@@ -239,8 +239,9 @@ isg_status isg_debug_bins(isg_ctx* ctx, uint64_t* keys, uint32_t* vals, int64_t*
  * its transmittance drops to t_min; *evaluated = entries visited, *inside = entries inside
  * their 3-sigma circle (summed over pixels).  Slow (no culling): outside timed regions. */
 isg_status isg_count_pairs(isg_ctx* ctx, int64_t* evaluated, int64_t* inside);
-/* Per-pixel forward state of the last render: transmittance before the last contributor
- * and number of list entries processed (both H x W). */
+/* Per-pixel forward state of the last render (both H x W): the final transmittance — or,
+ * negated, the transmittance before the last contributor in a tile where some pixel's final
+ * transmittance is not a normal float — and 1 + the index of the last contributor. */
 isg_status isg_debug_pixel_state(isg_ctx* ctx, float* t_last, uint32_t* n_proc);
 
 /* ---- binning strategy (both produce bit-identical tile lists) ----------------------------

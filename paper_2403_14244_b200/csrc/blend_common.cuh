@@ -1,11 +1,15 @@
 // blend_common.cuh — pieces shared by the tile blend kernels (k_blend.cu, k_blend_bwd.cu).
 #pragma once
+#include <type_traits>
+
 #include "isg_math.cuh"
 
 namespace isg {
 namespace blend {
 
 constexpr float kLn2 = 0.6931471805599453f;
+// smallest normal float: a final transmittance below it cannot be divided back up (k_blend.cu)
+constexpr float kMinNormal = 1.17549435e-38f;
 // start of an empty tile's range as the tile sort leaves it (isg_debug_bins fixes it up)
 constexpr uint32_t kEmptyRange = 0xFFFFFFFFu;
 

@@ -55,15 +55,17 @@ constexpr int kListPitch = kBatch + 4;  // sub-quarter lists start in different 
 struct FwdPair {
   float2 T;           // transmittance
   float2 Cr, Cg, Cb;  // accumulated colour
-  float2 Tl;          // transmittance before the last contributor (read by the backward)
+  float2 Tl;          // transmittance before the last contributor (the rare re-walk only)
   uint32_t np0, np1;  // 1 + index of the last contributor (entries the backward walks)
 };
 
 __device__ __forceinline__ float2 bc(float v) { return make_float2(v, v); }
 
-// kTrack: also record, per pixel, the transmittance before and the index of the last
-// contributor (the backward's starting state); a render-only frame skips it.
-template <bool kTrack>
+// kTrack: also record, per pixel, the index of the last contributor (where the backward starts
+// its walk); a render-only frame skips it.  kTl: also record the transmittance *before* the last
+// contributor (the backward's starting state for pixels whose final transmittance is not a
+// normal float, see k_blend_fwd).
+template <bool kTrack, bool kTl>
 __device__ __forceinline__ void fwd_pair(FwdPair& p, float2 r2, const float4 g, const float4 c,
                                          float t_min, uint32_t idx) {
   const bool in0 = !(r2.x > g.z) && (p.T.x > t_min);
@@ -75,8 +77,8 @@ __device__ __forceinline__ void fwd_pair(FwdPair& p, float2 r2, const float4 g, 
   p.Cr = __ffma2_rn(wgt, bc(c.x), p.Cr);
   p.Cg = __ffma2_rn(wgt, bc(c.y), p.Cg);
   p.Cb = __ffma2_rn(wgt, bc(c.z), p.Cb);
+  if constexpr (kTl) p.Tl = make_float2(in0 ? p.T.x : p.Tl.x, in1 ? p.T.y : p.Tl.y);
   if constexpr (kTrack) {
-    p.Tl = make_float2(in0 ? p.T.x : p.Tl.x, in1 ? p.T.y : p.Tl.y);
     p.np0 = in0 ? idx : p.np0;
     p.np1 = in1 ? idx : p.np1;
   }
@@ -141,8 +143,13 @@ __global__ void ISG_FWD_BOUNDS k_blend_fwd(
   const int n = rg.x == kEmptyRange ? 0 : (int)(rg.y - rg.x);
   const float t_min = fp.t_min;
 
-  // Invalid pixels start "terminated" (T = 0 <= t_min) and never contribute.
+  const uint32_t lt = (1u << lane) - 1u;
   FwdPair P[2];
+  // One walk over the tile's list.  kTl = false is every frame's walk; kTl = true the rare
+  // re-walk of a tracked frame that also records the transmittance before the last contributor.
+  auto walk = [&](auto tl_tag) {
+  constexpr bool kTl = decltype(tl_tag)::value;
+  // Invalid pixels start "terminated" (T = 0 <= t_min) and never contribute.
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     P[k].T = make_float2(x0 < W && y0 + k < H ? 1.0f : 0.0f,
@@ -151,7 +158,6 @@ __global__ void ISG_FWD_BOUNDS k_blend_fwd(
     P[k].Tl = bc(1.0f);
     P[k].np0 = P[k].np1 = 0u;
   }
-  const uint32_t lt = (1u << lane) - 1u;
 
   if (n > 0) stage_batch<kBT, kBatch + 1, false, false>(st[0], sorted, submask, rec, rg.x, min(kBatch, n));
   for (int b = 0, it = 0; b < n; b += kBatch, ++it) {
@@ -200,7 +206,7 @@ __global__ void ISG_FWD_BOUNDS k_blend_fwd(
         if (hk) s_list[8 * w + k][base[k] + __popc(mk & lt)] = (uint8_t)j;
         base[k] += __popc(mk);
       }
-      if (kTrack && in) mask_bytes[2 * ((size_t)rg.x + b + j) + w] = (uint8_t)mw;
+      if (kTrack && !kTl && in) mask_bytes[2 * ((size_t)rg.x + b + j) + w] = (uint8_t)mw;
     }
     // a sub-quarter whose 16 pixels have all terminated walks nothing
     int steps = 0, my_cnt = 0;
@@ -227,9 +233,27 @@ __global__ void ISG_FWD_BOUNDS k_blend_fwd(
       for (int k = 0; k < 2; ++k) {
         const float dyk = k ? dy.y : dy.x;
         const float2 r2 = __fadd2_rn(ax, bc(__fmul_rn(dyk, dyk)));
-        fwd_pair<kTrack>(P[k], r2, g, c, t_min, idx);
+        fwd_pair<kTrack, kTl>(P[k], r2, g, c, t_min, idx);
       }
     }
+  }
+  };
+  walk(std::false_type{});
+  // Tracked frames hand the backward each pixel's final transmittance, from which it recovers
+  // T before every contributor by division (k_blend_bwd.cu).  A pixel whose final
+  // transmittance is not a normal float (an opacity-1 splat at its centre gives T = 0; t_min = 0
+  // lets T underflow) cannot be recovered that way: if the tile has one, it is walked again,
+  // recording T before the last contributor, stored negated so the backward takes its slower,
+  // select-based start for this tile.
+  bool rewalk = false;
+  if constexpr (kTrack) {
+    bool bad = false;
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      bad |= (P[k].np0 != 0u && !(P[k].T.x >= kMinNormal)) ||
+             (P[k].np1 != 0u && !(P[k].T.y >= kMinNormal));
+    rewalk = __syncthreads_or(bad) != 0;
+    if (rewalk) walk(std::true_type{});
   }
   cp_async_wait_all();
 #pragma unroll
@@ -246,7 +270,7 @@ __global__ void ISG_FWD_BOUNDS k_blend_fwd(
       out[3 * pix + 1] = (i ? P[k].Cg.y : P[k].Cg.x) + T * fp.bg[1];
       out[3 * pix + 2] = (i ? P[k].Cb.y : P[k].Cb.x) + T * fp.bg[2];
       if constexpr (kTrack) {
-        t_last[pix] = i ? P[k].Tl.y : P[k].Tl.x;
+        t_last[pix] = rewalk ? -(i ? P[k].Tl.y : P[k].Tl.x) : T;
         n_proc[pix] = i ? P[k].np1 : P[k].np0;
       }
     }

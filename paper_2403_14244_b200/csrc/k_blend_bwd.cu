@@ -29,17 +29,21 @@ using namespace blend;
 
 constexpr int kBT = 64;      // threads per tile CTA: 2 warps x 8 four-lane groups
 #ifndef ISG_BWD_BATCH
-#define ISG_BWD_BATCH 32
+#define ISG_BWD_BATCH 128
 #endif
 // 4 walk steps per loop iteration (0.578 vs 0.595 ms unrolled by 1 at C3, direct mode)
 #ifndef ISG_BWD_UNROLL
 #define ISG_BWD_UNROLL 4
 #endif
 constexpr int kUnroll = ISG_BWD_UNROLL;  // walk steps per loop iteration
-constexpr int kBatch = ISG_BWD_BATCH;  // records staged per batch (32: one ballot per sub-quarter)
-constexpr int kWords = kBatch / 32;
+// Records staged per batch.  The 8 groups of a warp walk a batch in lockstep, so a warp's step
+// count per batch is the longest of its 8 relevance lists: larger batches pad less (C3 walk
+// steps, tools/sim_bwd_lists.py: 3.36M at 32, 3.20M at 64, 3.09M at 128).  Slot mode keeps 32
+// (its flush maps entry = lane).
+constexpr int kBatchDirect = ISG_BWD_BATCH;
+constexpr int kBatchSlot = 32;
+static_assert(kBatchDirect % 32 == 0 && kBatchDirect < 256, "u8 list entries, sentinel index");
 constexpr int kSubs = 16;    // 4x4 sub-quarters per tile (one per four-lane group)
-constexpr int kListPitch = kBatch + 4;  // sub-quarter lists start in different banks
 
 // Two horizontally adjacent pixels (same row) as packed f32x2 lanes: .x = (x0, y), .y = (x0+1, y).
 // Packed FFMA2/FMUL2/FADD2 issue once for both pixels.
@@ -57,6 +61,10 @@ __device__ __forceinline__ float2 bc(float v) { return make_float2(v, v); }
 //   dL/da_k = T_k G.(c_k - A_k);  A <- a c + (1 - a) A  =>  G.A <- G.A + a (G.c - G.A)
 // so the colour behind is carried as the single scalar G.A per pixel.  An inactive pixel gets
 // e = 0, hence a = 0: T and G.A stay exactly unchanged and every contribution is an exact zero.
+// kFast: p.T starts as the pixel's final transmittance and every contributor divides it back
+// up, T_k = T_{k+1} / (1 - a_k).  Otherwise (a tile the forward re-walked, k_blend.cu) p.T
+// starts as the transmittance before the last contributor, which therefore does not divide.
+template <bool kFast>
 __device__ __forceinline__ void bwd_pair(BwdPair& p, bool act0, bool act1, int j, float2 dx,
                                          float dy, float2 r2, const float4 g, const float4 c,
                                          float2 acc[8]) {
@@ -65,7 +73,9 @@ __device__ __forceinline__ void bwd_pair(BwdPair& p, bool act0, bool act1, int j
   const float2 a = __fmul2_rn(bc(c.w), e);
   const float2 om = __fadd2_rn(bc(1.0f), make_float2(-a.x, -a.y));  // 1 - a (FADD2 imm)
   const float2 Tr = __fmul2_rn(p.T, make_float2(fast_rcp(om.x), fast_rcp(om.y)));
-  const float2 Tk = make_float2(j == p.np0 - 1 ? p.T.x : Tr.x, j == p.np1 - 1 ? p.T.y : Tr.y);
+  float2 Tk = Tr;
+  if constexpr (!kFast)
+    Tk = make_float2(j == p.np0 - 1 ? p.T.x : Tr.x, j == p.np1 - 1 ? p.T.y : Tr.y);
   p.T = Tk;
   const float2 Gc = __ffma2_rn(p.G2, bc(c.z), __ffma2_rn(p.G1, bc(c.y), __fmul2_rn(p.G0, bc(c.x))));
   const float2 gd = __fadd2_rn(Gc, make_float2(-p.GA.x, -p.GA.y));  // G.(c - A)
@@ -122,13 +132,16 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
     int64_t key_cap, const float* __restrict__ img, const float* __restrict__ target,
     const float* __restrict__ t_last, const uint32_t* __restrict__ n_proc, float loss_scale,
     float4* __restrict__ partial, double* __restrict__ tile_loss, float* __restrict__ grad2d) {
-  // entry kBatch of each stage is a sentinel no pixel is inside (r2max = -1): the groups'
+  constexpr int kB = kDirect ? kBatchDirect : kBatchSlot;
+  constexpr int kW = kB / 32;
+  constexpr int kListPitch = kB + 4;  // sub-quarter lists start in different banks
+  // entry kB of each stage is a sentinel no pixel is inside (r2max = -1): the groups'
   // lists are padded with it to the warp's step count, so the walk needs no bounds test
-  __shared__ Stage<kBatch + 1> st[2];
+  __shared__ Stage<kB + 1> st[2];
   // [sub-quarter][value][entry]; rows padded so one entry's 8 values hit 8 different banks
   // (slot mode only: the direct mode reduces into grad2d in L2 instead)
-  __shared__ float s_part[kDirect ? 1 : kSubs][8][kBatch + 1];
-  __shared__ uint32_t s_rel[kSubs][kWords];  // relevance ballots of the batch per sub-quarter
+  __shared__ float s_part[kDirect ? 1 : kSubs][8][kB + 1];
+  __shared__ uint32_t s_rel[kSubs][kW];  // relevance ballots of the batch per sub-quarter
   __shared__ uint8_t s_list[kSubs][kListPitch];
   __shared__ float s_red[2];
   __shared__ int s_max[2];
@@ -139,8 +152,8 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
     return;
   }
   if (threadIdx.x < 2) {
-    st[threadIdx.x].geo[kBatch] = make_float4(0.0f, 0.0f, -1.0f, 0.0f);
-    st[threadIdx.x].col[kBatch] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    st[threadIdx.x].geo[kB] = make_float4(0.0f, 0.0f, -1.0f, 0.0f);
+    st[threadIdx.x].col[kB] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
   }
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int gq = lane >> 2, l4 = lane & 3;  // four-lane group = one 4x4 sub-quarter
@@ -157,6 +170,7 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
 
   BwdPair P[2];  // P[k]: the quad's row k
   float dsq = 0.0f;
+  bool slow_px = false;
   int npmax = 0;
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
@@ -178,7 +192,9 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
             G[i][ch] = 2.0f * d * loss_scale;
           }
         }
-        T[i] = t_last[pix];
+        const float tl = t_last[pix];  // negative: the tile's select-based start (k_blend.cu)
+        slow_px |= tl < 0.0f;
+        T[i] = fabsf(tl);
         np[i] = (int)n_proc[pix];
         npmax = max(npmax, np[i]);
       }
@@ -202,7 +218,7 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
     s_red[w] = dsq;
     s_max[w] = npmax;
   }
-  __syncthreads();
+  const bool slow = __syncthreads_or(slow_px) != 0;
   const int m = max(s_max[0], s_max[1]);  // entries [0, m) are walked
   if (threadIdx.x == 0) tile_loss[tile] = (double)s_red[0] + (double)s_red[1];
   // entries never reached by any pixel get zero gradient slots (slot mode)
@@ -213,35 +229,37 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
   }
   if (m == 0) return;
 
-  const uint32_t lt = (1u << lane) - 1u;
+  const uint32_t gt = ~((2u << lane) - 1u);  // lanes above this one
   int hi = m;
-  stage_batch<kBT, kBatch + 1, kDirect>(st[0], sorted, submask, rec, rg.x + max(0, hi - kBatch),
-                                        min(kBatch, hi));
+  stage_batch<kBT, kB + 1, kDirect>(st[0], sorted, submask, rec, rg.x + max(0, hi - kB),
+                                        min(kB, hi));
   for (int it = 0; hi > 0; ++it) {
-    const int lo = max(0, hi - kBatch);
+    const int lo = max(0, hi - kB);
     const int cnt = hi - lo;
-    Stage<kBatch + 1>& cur = st[it & 1];
+    Stage<kB + 1>& cur = st[it & 1];
     cp_async_wait_all();
     __syncthreads();  // batch visible; previous batch's flush finished reading s_part
     if (lo > 0) {
-      const int nlo = max(0, lo - kBatch);
-      stage_batch<kBT, kBatch + 1, kDirect>(st[(it + 1) & 1], sorted, submask, rec, rg.x + nlo,
+      const int nlo = max(0, lo - kB);
+      stage_batch<kBT, kB + 1, kDirect>(st[(it + 1) & 1], sorted, submask, rec, rg.x + nlo,
                                             lo - nlo);
     }
     // relevance of the batch for the warp's 8 sub-quarters -> 8 compacted lists, from the
     // pairs' precomputed sub-quarter masks (sub_mask16, the binning's closest-point tests)
     int my_cnt = 0, steps = 0;
     int base[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    // words from the last to the first and, within a word, lanes from high to low: the lists
+    // come out in reverse depth order
 #pragma unroll
-    for (int wd = 0; wd < kWords; ++wd) {
+    for (int wd = kW - 1; wd >= 0; --wd) {
+      if (32 * wd >= cnt) continue;  // warp-uniform: the batch's partial end
       const int j = 32 * wd + lane;
       const uint32_t mw = j < cnt ? ((uint32_t)cur.mask[j] >> (8 * w)) & 0xFFu : 0u;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {  // group k = sub-quarter 8 w + k
         const bool hk = (mw >> k) & 1u;
         const uint32_t mk = __ballot_sync(0xffffffffu, hk);
-        // stored in reverse depth order (one ballot word: the count is known here)
-        if (hk) s_list[8 * w + k][__popc(mk) - 1 - __popc(mk & lt)] = (uint8_t)j;
+        if (hk) s_list[8 * w + k][base[k] + __popc(mk & gt)] = (uint8_t)j;
         if (!kDirect && lane == 0) s_rel[8 * w + k][wd] = mk;
         base[k] += __popc(mk);
       }
@@ -251,13 +269,15 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
       steps = max(steps, base[k]);
       if (k == gq) my_cnt = base[k];
     }
-    for (int e = my_cnt + l4; e < steps; e += 4) s_list[sub][e] = (uint8_t)kBatch;
+    for (int e = my_cnt + l4; e < steps; e += 4) s_list[sub][e] = (uint8_t)kB;
     __syncwarp();
     const uint8_t* my_list = s_list[sub];
+    auto walk = [&](auto fast_tag) {
+    constexpr bool kFast = decltype(fast_tag)::value;
 #pragma unroll kUnroll
     for (int s = 0; s < steps; ++s) {
       // reverse depth order; the sentinel has a = 0 for every pixel, so T (T / 1) and G.A stay
-      // exactly unchanged whatever j is, and its s_part column kBatch is padding
+      // exactly unchanged whatever j is, and its s_part column kB is padding
       const int jj = my_list[s];
       const int j = lo + jj;
       const float4 g = cur.geo[jj];
@@ -278,7 +298,7 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
         const float2 r2 = __fadd2_rn(ax, bc(ay));
         const bool act0 = j < P[k].np0 && !(r2.x > g.z);
         const bool act1 = j < P[k].np1 && !(r2.y > g.z);
-        bwd_pair(P[k], act0, act1, j, dx, dyk, r2, g, c, acc2);
+        bwd_pair<kFast>(P[k], act0, act1, j, dx, dyk, r2, g, c, acc2);
       }
       float acc[8];
 #pragma unroll
@@ -291,13 +311,18 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
       if constexpr (kDirect) {
         // the sub-quarter's pre-reduced share goes straight to the splat's 2D gradient in L2
         // (4 lanes = one 32-B sector); the sentinel and exact zeros send nothing
-        if (jj < kBatch && (y[0] != 0.0f || y[1] != 0.0f))
+        if (jj < kB && (y[0] != 0.0f || y[1] != 0.0f))
           red_add_v2(grad2d + 8 * (size_t)cur.slot[jj] + vb, y[0], y[1]);
       } else {
         s_part[sub][vb][jj] = y[0];  // the sentinel writes the padding column
         s_part[sub][vb + 1][jj] = y[1];
       }
     }
+    };
+    if (slow)
+      walk(std::false_type{});
+    else
+      walk(std::true_type{});
     if constexpr (kDirect) {
       hi = lo;  // the next batch's barrier orders the staging buffers
       continue;
@@ -305,7 +330,7 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
     __syncthreads();
     // combine the sub-quarters in a fixed order and write each (tile, splat) pair's slot:
     // warp h sums values 4h .. 4h+3 of entry `lane` (h = 1: drgb; value 7 is unused)
-    static_assert(kBatch == 32 && kBT == 64, "flush maps entry = lane, half = warp");
+    static_assert(kDirect || (kB == 32 && kBT == 64), "flush maps entry = lane, half = warp");
     if (lane < cnt) {
       const int jj = lane;
       float v[4] = {0.f, 0.f, 0.f, 0.f};

@@ -189,6 +189,50 @@ def test_backward_vs_fp64_reference(rend):
     _grad_check(g, g64)
 
 
+@pytest.mark.parametrize("case", ["alpha_one", "underflow"])
+def test_backward_through_zero_final_transmittance(rend, case):
+    """The backward recovers every contributor's transmittance by dividing the pixel's final
+    transmittance back up.  Where that is 0 or not a normal float -- an opacity-1 splat whose
+    centre falls exactly on a pixel centre (alpha = 1), or t_min = 0 with a stack of opaque
+    splats (T underflows) -- the forward re-walks the tile and hands over T before the last
+    contributor instead (negated, debug_pixel_state); gradients must match the oracle either
+    way, and ordinary tiles must keep the fast start."""
+    rng = np.random.default_rng(7 if case == "alpha_one" else 8)
+    W, H = 64, 48
+    ms, co, cam = random_scene(rng, 400, W, H)
+    if case == "alpha_one":
+        # principal point on pixel centres: x = y = 0 projects exactly to (cx, cy)
+        cam = isg.Camera(np.eye(3), np.zeros(3), cam.focal, (20.5, 12.5), W, H)
+        extra_ms = np.array([[0.0, 0.0, 1.5, 0.004], [0.0, 0.0, 1.6, 0.01]], np.float32)
+        extra_co = np.array([[0.9, 0.2, 0.1, 1.0], [0.1, 0.8, 0.3, 1.0]], np.float32)
+        t_mins = (0.0, 1e-5)
+    else:
+        # 150 near-opaque splats over the same pixels: T falls below the smallest normal float
+        k = 150
+        z = np.linspace(1.2, 1.9, k, dtype=np.float32)
+        extra_ms = np.stack([np.full(k, 0.01), np.full(k, -0.01), z, 0.02 * z], 1).astype(np.float32)
+        extra_co = np.concatenate([rng.uniform(0, 1, (k, 3)), np.full((k, 1), 0.9)], 1).astype(np.float32)
+        t_mins = (0.0,)
+    ms = np.concatenate([ms, extra_ms]).astype(np.float32)
+    co = np.concatenate([co, extra_co]).astype(np.float32)
+    tms, tco, _ = random_scene(rng, 400, W, H)
+    target = O.render32(tms, tco, cam)
+    rend.set_scene(ms, co)
+    for t_min in t_mins:
+        opts = isg.RenderOptions(t_min=t_min)
+        rend.zero_grads()
+        loss = rend.loss_backward(cam, target, opts, weight=1.0)
+        g = rend.grads()
+        tl, _ = rend.debug_pixel_state(W, H)
+        assert (tl < 0).any(), "no tile took the re-walk"
+        assert (tl >= 0).any(), "every tile took the re-walk"
+        loss_ref, g_ref = O.loss_backward32(ms, co, cam, target, t_min=t_min)
+        assert abs(loss - loss_ref) <= 1e-6 * abs(loss_ref)
+        # (the FP32 oracle, not the FP64 backward: a pixel stops where T reaches exactly 0,
+        # so the splats behind an alpha-1 splat are not its "colour behind" here)
+        _grad_check(g, g_ref)
+
+
 def _golden(name):
     import sys
     from pathlib import Path

@@ -67,3 +67,25 @@ for name,RR in (('8x4',rel84),('4x8',rel48)):
     C8=np.zeros((len(uk),8),np.int64)
     for s_ in range(8): C8[:,s_]=np.bincount(inv,weights=RR[:,s_],minlength=len(uk))
     print(name,'sum max8',C8.max(1).sum(),'cost (190/step)',C8.max(1).sum()*190/1e6)
+
+# Cumulative (carry-over) walk: each group walks its whole tile list without per-batch lockstep;
+# a warp's step count is then the max over its groups of the group's TOTAL relevant entries.
+tb = uk // 100000  # tile of each (tile, batch) row
+for name, cols in (('top', slice(0, 8)), ('bot', slice(8, 16))):
+    pass
+tot_top = np.zeros(T, np.int64); tot_bot = np.zeros(T, np.int64)
+G = np.zeros((T, 16), np.int64)
+np.add.at(G, tb, C)
+cum = G[:, :8].max(1).sum() + G[:, 8:].max(1).sum()
+print('lockstep per batch', (top + bot).sum(), 'cumulative per tile', cum,
+      'ideal (mean)', C.sum() / 8)
+
+# lockstep window size: steps = sum over (tile, window) of the max over a warp's 8 groups
+for Wn in (32, 64, 96, 128, 256):
+    bw = (m[tile] - 1 - pos) // Wn
+    key2 = tile * 100000 + bw
+    uk2, inv2 = np.unique(key2, return_inverse=True)
+    C2 = np.zeros((len(uk2), 16), np.int64)
+    for s_ in range(16): C2[:, s_] = np.bincount(inv2, weights=rel[:, s_], minlength=len(uk2))
+    print('window', Wn, 'lockstep steps', C2[:, :8].max(1).sum() + C2[:, 8:].max(1).sum(),
+          'windows', len(uk2))
