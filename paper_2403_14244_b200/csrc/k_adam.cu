@@ -14,6 +14,9 @@
 // Adam rule of torch.optim.Adam on (mu, log sigma, rgb, logit opacity).
 //
 // One thread per splat; params, moments and 3D grads are float4 SoA, coalesced.
+#include <algorithm>
+#include <cstdlib>
+
 #include "isg_math.cuh"
 
 namespace isg {
@@ -285,6 +288,129 @@ __global__ void ISG_ADAM_BOUNDS k_project_adam(
   adam_apply(in, ms, co, raw, m, v, i, o, ap, total + kTotalSkipped);
 }
 
+// ---- K8, direct mode: a persistent HBM stream ------------------------------------------------
+// The fused step is a pure stream (136 B read + 136 B written per splat) whose speed is set by
+// how many bytes are in flight.  Each CTA owns chunks of kAS splats; one thread issues 1D bulk
+// copies (cp.async.bulk, TMA) of a chunk's six input arrays into a shared-memory stage that
+// completes on an mbarrier, two stages deep, so the next chunk's 17 KB are in flight while the
+// current one is computed and stored (one splat per thread, coalesced float4 stores).  The
+// partial last chunk is read directly.
+constexpr int kAS = 128;  // splats per chunk = threads per CTA
+struct AdamStage {
+  float4 ms[kAS], co[kAS];
+  float4 m[2 * kAS], v[2 * kAS], g[2 * kAS];
+  float2 raw[kAS];
+};
+constexpr uint32_t kAdamStageBytes = sizeof(AdamStage);
+static_assert(kAdamStageBytes == kAS * 136, "stage = the chunk's input bytes");
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kAS) k_project_adam_stream(
+    float4* __restrict__ ms, float4* __restrict__ co, int64_t n, FrameParams fp,
+    float* __restrict__ grad2d, unsigned long long* __restrict__ total, float2* __restrict__ raw,
+    float4* __restrict__ m, float4* __restrict__ v, const AdamState* __restrict__ state) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  AdamStage* S = reinterpret_cast<AdamStage*>(smem_raw);
+  __shared__ uint64_t bar[2];
+  const int tid = threadIdx.x;
+  float4* g2 = reinterpret_cast<float4*>(grad2d);
+  pdl_enter();
+  // an overflowed frame since the last host check: no update (the host re-runs the step);
+  // the direct-mode sums are consumed (zeroed) either way
+  if (total[kTotalOverflowMax] != 0ull) {
+    for (int64_t i = (int64_t)blockIdx.x * kAS + tid; i < n; i += (int64_t)gridDim.x * kAS) {
+      g2[2 * i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      g2[2 * i + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    return;
+  }
+  const AdamParams ap = state->p;
+  const int64_t nfull = n / kAS;
+  const int64_t G = gridDim.x;
+  auto issue = [&](int s, int64_t c) {  // thread 0: chunk c into stage s
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[s])),
+                 "r"(kAdamStageBytes)
+                 : "memory");
+    const int64_t b = c * kAS;
+    bulk_load(S[s].ms, ms + b, kAS * 16, &bar[s]);
+    bulk_load(S[s].co, co + b, kAS * 16, &bar[s]);
+    bulk_load(S[s].m, m + 2 * b, kAS * 32, &bar[s]);
+    bulk_load(S[s].v, v + 2 * b, kAS * 32, &bar[s]);
+    bulk_load(S[s].g, g2 + 2 * b, kAS * 32, &bar[s]);
+    bulk_load(S[s].raw, raw + b, kAS * 8, &bar[s]);
+  };
+  if (tid == 0) {
+    mbar_init(&bar[0]);
+    mbar_init(&bar[1]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (blockIdx.x < nfull) issue(0, blockIdx.x);
+    if (blockIdx.x + G < nfull) issue(1, blockIdx.x + G);
+  }
+  __syncthreads();
+  uint32_t phase = 0;  // bit s: parity of stage s's next completion
+  int it = 0;
+  for (int64_t c = blockIdx.x; c < nfull; c += G, ++it) {
+    const int s = it & 1;
+    mbar_wait(&bar[s], (phase >> s) & 1u);
+    phase ^= 1u << s;
+    AdamIn in;
+    in.P0 = S[s].ms[tid];
+    in.P1 = S[s].co[tid];
+    in.R = S[s].raw[tid];
+    in.M0 = S[s].m[2 * tid];
+    in.M1 = S[s].m[2 * tid + 1];
+    in.V0 = S[s].v[2 * tid];
+    in.V1 = S[s].v[2 * tid + 1];
+    const float4 a = S[s].g[2 * tid], b = S[s].g[2 * tid + 1];
+    // stage s consumed: refill it with the chunk two ahead (the generic-proxy reads of the
+    // stage are ordered before the async-proxy writes of the refill)
+    __syncthreads();
+    if (tid == 0 && c + 2 * G < nfull) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(s, c + 2 * G);
+    }
+    const int64_t i = c * kAS + tid;
+    g2[2 * i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    g2[2 * i + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    float o[8];
+    grad3d_of(in.P0, fp.cam, a, b, o, in.P1.w);
+    adam_apply(in, ms, co, raw, m, v, i, o, ap, total + kTotalSkipped);
+  }
+  // the partial last chunk: the CTA that would own it reads it directly
+  if (nfull % G == blockIdx.x) {
+    const int64_t i = nfull * kAS + tid;
+    if (i < n) {
+      const AdamIn in = adam_load(ms, co, raw, m, v, i);
+      const float4 a = g2[2 * i], b = g2[2 * i + 1];
+      g2[2 * i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      g2[2 * i + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+      float o[8];
+      grad3d_of(in.P0, fp.cam, a, b, o, in.P1.w);
+      adam_apply(in, ms, co, raw, m, v, i, o, ap, total + kTotalSkipped);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) k_adam(float4* __restrict__ ms, float4* __restrict__ co,
                                               int64_t n, const float4* __restrict__ grad3d,
                                               float2* __restrict__ raw, float4* __restrict__ m,
@@ -369,6 +495,26 @@ void launch_project_adam(float4* ms, float4* co, int64_t n, const FrameParams& f
                          unsigned long long* total, float2* raw, float4* m, float4* v,
                          const AdamState* ap, cudaStream_t st) {
   if (n <= 0) return;
+  static const bool use_stream = [] {
+    const char* e = std::getenv("ISG_K8_STREAM");
+    return !(e && e[0] == '0');
+  }();
+  if (grad2d && use_stream) {
+    static const int grid_max = [] {
+      int dev = 0, sms = 0, per_sm = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaFuncSetAttribute(k_project_adam_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(2 * kAdamStageBytes));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_project_adam_stream, kAS,
+                                                    2 * kAdamStageBytes);
+      return std::max(1, sms * std::max(1, per_sm));
+    }();
+    const int64_t chunks = (n + kAS - 1) / kAS;
+    launch_pdl(k_project_adam_stream, dim3((unsigned)std::min<int64_t>(chunks, grid_max)),
+               dim3(kAS), 2 * kAdamStageBytes, st, ms, co, n, fp, grad2d, total, raw, m, v, ap);
+    return;
+  }
   launch_pdl(k_project_adam, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, ms, co, n,
              fp, slot_off, slot_of, ntiles, partial, grad2d, total, raw, m, v, ap);
 }
