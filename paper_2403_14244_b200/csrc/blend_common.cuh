@@ -34,6 +34,14 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 __device__ __forceinline__ void red_add_v2(float* p, float a, float b) {
   asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(a), "f"(b) : "memory");
 }
+// ... predicated in place (no branch around it: the walk loop stays one basic block).  The
+// address is only formed, never dereferenced, when `on` is false.
+__device__ __forceinline__ void red_add_v2_if(bool on, float* p, float a, float b) {
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.u32 q, %3, 0;\n @q red.global.add.v2.f32 [%0], {%1, %2};\n}" ::"l"(p),
+      "f"(a), "f"(b), "r"((unsigned)on)
+      : "memory");
+}
 
 __device__ __forceinline__ float fast_rcp(float x) {
   float y;

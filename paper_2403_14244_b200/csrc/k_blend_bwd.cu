@@ -67,7 +67,7 @@ __device__ __forceinline__ float2 bc(float v) { return make_float2(v, v); }
 template <bool kFast>
 __device__ __forceinline__ void bwd_pair(BwdPair& p, bool act0, bool act1, int j, float2 dx,
                                          float dy, float2 r2, const float4 g, const float4 c,
-                                         float2 acc[8]) {
+                                         float2 acc[8], float2& go) {
   const float2 q = __fmul2_rn(r2, bc(g.w));
   const float2 e = make_float2(act0 ? fast_exp2(q.x) : 0.0f, act1 ? fast_exp2(q.y) : 0.0f);
   const float2 a = __fmul2_rn(bc(c.w), e);
@@ -85,24 +85,27 @@ __device__ __forceinline__ void bwd_pair(BwdPair& p, bool act0, bool act1, int j
   acc[4] = __ffma2_rn(p.G0, Ta, acc[4]);
   acc[5] = __ffma2_rn(p.G1, Ta, acc[5]);
   acc[6] = __ffma2_rn(p.G2, Ta, acc[6]);
-  const float2 go = __fmul2_rn(dLda, e);
-  acc[3] = __fadd2_rn(acc[3], go);
+  go = __fmul2_rn(dLda, e);  // the caller sums the two rows' go into acc[3]
   acc[0] = __ffma2_rn(go, dx, acc[0]);
   acc[1] = __ffma2_rn(go, bc(dy), acc[1]);
   acc[2] = __ffma2_rn(go, r2, acc[2]);
 }
 
-// reduce-scatter of 8 values over a 4-lane group in 6 shuffles: lane l (l4 = l & 3) returns the
-// group sums of values 4*(l4>>1) + 2*(l4&1) + {0, 1} in out[0], out[1].
+// reduce-scatter of 8 values (v[7] == 0) over a 4-lane group in 6 shuffles: lane l (l4 = l & 3)
+// returns the group sums of values 4*(l4>>1) + 2*(l4&1) + {0, 1} in out[0], out[1].
 __device__ __forceinline__ void reduce_scatter8_quad(const float v[8], float out[2]) {
   const int lane = threadIdx.x & 31;
   const bool b1 = lane & 2, b0 = lane & 1;
   float w[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < 3; ++i) {
     const float send = b1 ? v[i] : v[i + 4];
     const float keep = b1 ? v[i + 4] : v[i];
     w[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  }
+  {  // value 7 is zero: the upper lanes' share of this pair is 0, the lower lanes add v[3]
+    const float t = __shfl_xor_sync(0xffffffffu, v[3], 2);
+    w[3] = b1 ? 0.0f : v[3] + t;
   }
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
@@ -291,6 +294,7 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
       float2 acc2[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) acc2[k] = bc(0.0f);
+      float2 go[2];
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
         const float dyk = k ? dy.y : dy.x;
@@ -298,8 +302,9 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
         const float2 r2 = __fadd2_rn(ax, bc(ay));
         const bool act0 = j < P[k].np0 && !(r2.x > g.z);
         const bool act1 = j < P[k].np1 && !(r2.y > g.z);
-        bwd_pair<kFast>(P[k], act0, act1, j, dx, dyk, r2, g, c, acc2);
+        bwd_pair<kFast>(P[k], act0, act1, j, dx, dyk, r2, g, c, acc2, go[k]);
       }
+      acc2[3] = __fadd2_rn(go[0], go[1]);
       float acc[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) acc[k] = acc2[k].x + acc2[k].y;
@@ -311,8 +316,8 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
       if constexpr (kDirect) {
         // the sub-quarter's pre-reduced share goes straight to the splat's 2D gradient in L2
         // (4 lanes = one 32-B sector); the sentinel and exact zeros send nothing
-        if (jj < kB && (y[0] != 0.0f || y[1] != 0.0f))
-          red_add_v2(grad2d + 8 * (size_t)cur.slot[jj] + vb, y[0], y[1]);
+        red_add_v2_if(jj < kB && (y[0] != 0.0f || y[1] != 0.0f),
+                      grad2d + 8 * (size_t)cur.slot[jj] + vb, y[0], y[1]);
       } else {
         s_part[sub][vb][jj] = y[0];  // the sentinel writes the padding column
         s_part[sub][vb + 1][jj] = y[1];
