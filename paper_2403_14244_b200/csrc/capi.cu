@@ -493,8 +493,9 @@ isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out, bool tr
     }
     {
     ISG_STAGE(ST_SCAN_EMIT);
+    // slot lists (slot_off) only for the deterministic backward; direct mode needs none
     isg::launch_scan_emit(ctx->order[ctx->order_buf], ctx->ntiles, ctx->tilebox, ctx->ms, n, fp,
-                          ctx->slot_off, ctx->tkey[0], ctx->emit_gid, ctx->key_cap,
+                          ctx->deterministic ? ctx->slot_off : nullptr, ctx->tkey[0], ctx->emit_gid, ctx->key_cap,
                           ctx->scan_scratch, ctx->sc + 3, ctx->sc + 0, ctx->total, ctx->ranges,
                           fp.n_tiles, tile_passes, ctx->sort_tile.hist,
                           ctx->sort_tile.counters + isg::kMaxPasses, st);

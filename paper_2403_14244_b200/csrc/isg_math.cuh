@@ -91,6 +91,12 @@ __device__ __forceinline__ bool tile_bbox(float u, float v, float s, int tiles_x
   return true;
 }
 
+// Tiles a splat touches, from K1's compact box record (small box: popc of the hit mask; bigger
+// box, bw == 0: the count itself in .y).
+__device__ __forceinline__ uint32_t tilebox_count(uint2 box) {
+  return (box.x >> 24) ? (uint32_t)__popc(box.y) : box.y;
+}
+
 // Visit the tiles a splat touches, in row-major order (the order K1 counted them).  `box` is
 // K1's compact record: x0 | y0 << 12 | bw << 24 and a hit mask over the (<= 32-tile) bbox; for
 // bigger boxes (bw == 0) the projection and the exact tile tests are recomputed from `ms`.

@@ -71,9 +71,11 @@ __global__ void __launch_bounds__(256) k_preprocess(const float4* __restrict__ m
               if (tile_cnt) atomicAdd(&tile_cnt[ty * fp.tiles_x + tx], 1u);
             }
           }
-          if (!small) mask = 0;
-          // emission kernels iterate the hit bits instead of re-projecting (bw == 0: re-project)
-          if (small) box = make_uint2((uint32_t)x0 | ((uint32_t)y0 << 12) | ((uint32_t)bw << 24), mask);
+          // emission kernels iterate the hit bits instead of re-projecting; a bigger box
+          // (bw == 0: re-project) carries the tile count instead, so one 8-B gather gives the
+          // emission every splat's count (popc of the mask, or box.y)
+          box = small ? make_uint2((uint32_t)x0 | ((uint32_t)y0 << 12) | ((uint32_t)bw << 24), mask)
+                      : make_uint2(0u, count);
         }
       }
       tilebox[i] = box;

@@ -323,8 +323,8 @@ __global__ void __launch_bounds__(kScanThreads, ISG_SCAN_MINB) k_scan_emit(
 #pragma unroll
   for (int j = 0; j < kScanItems; ++j) {
     const bool ok = r0 + j < n;
-    c[j] = ok ? ntiles[g[j]] : 0u;
     box[j] = ok ? tilebox[g[j]] : make_uint2(0u, 0u);
+    c[j] = tilebox_count(box[j]);
     sum += c[j];
   }
   uint32_t tot;
@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(kScanThreads, ISG_SCAN_MINB) k_scan_emit(
     cta0 = s_excl;                                                                 \
     uint32_t pos_ = t_begin;                                                       \
     _Pragma("unroll") for (int j = 0; j < kScanItems; ++j) {                       \
-      if (r0 + j < n) slot_off[g[j]] = (uint32_t)min(cta0 + pos_, 0xFFFFFFFFull); \
+      if (slot_off && r0 + j < n) slot_off[g[j]] = (uint32_t)min(cta0 + pos_, 0xFFFFFFFFull); \
       pos_ += c[j];                                                                \
     }                                                                              \
   } while (0)
