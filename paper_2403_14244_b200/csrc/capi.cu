@@ -509,9 +509,18 @@ isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out, bool tr
     topt.epi.emit_gid = ctx->emit_gid;
     topt.epi.sorted = ctx->sorted;
     topt.epi.ranges = ctx->ranges;
-
-    isg::radix_sort_pairs(ctx->tkey, ctx->tval, true, ctx->sc + 0, ctx->key_cap,
-                          bits_for(fp.n_tiles), ctx->sort_tile, st, &ctx->launches, topt);
+    if (ctx->deterministic) {
+      // values: emission indices (a pair's gradient slot), splat ids gathered at the end
+      isg::radix_sort_pairs(ctx->tkey, ctx->tval, true, ctx->sc + 0, ctx->key_cap,
+                            bits_for(fp.n_tiles), ctx->sort_tile, st, &ctx->launches, topt);
+    } else {
+      // direct mode needs no slot: the values are the splat ids themselves (read in emission
+      // order by the first pass), no random gather of emit_gid in the last one
+      topt.epi.vals_are_gids = true;
+      uint32_t* vals[2] = {ctx->emit_gid, ctx->tval[1]};
+      isg::radix_sort_pairs(ctx->tkey, vals, false, ctx->sc + 0, ctx->key_cap,
+                            bits_for(fp.n_tiles), ctx->sort_tile, st, &ctx->launches, topt);
+    }
     ISG_CHECK_LAUNCH();
     }
     // empty tiles keep (0xFFFFFFFF, 0): the blend kernels read them as empty, and only the

@@ -87,6 +87,9 @@ struct SortEpilogue {
   const uint32_t* emit_gid = nullptr;
   uint2* sorted = nullptr;
   uint2* ranges = nullptr;
+  // the sorted values are splat ids already (the direct-mode backward needs no gradient slot):
+  // sorted[o] = (val, o), no emit_gid gather
+  bool vals_are_gids = false;
 };
 struct SortOptions {
   bool scratch_zeroed = false;  // hist / counters / look-back already zero (one frame memset)

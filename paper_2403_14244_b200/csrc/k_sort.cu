@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
   if constexpr (kEpi) {
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j)
-      gid[j] = ISG_EPI_PREFETCH && dig[j] < 256u ? epi.emit_gid[val[j]] : 0u;
+      gid[j] = ISG_EPI_PREFETCH && !epi.vals_are_gids && dig[j] < 256u ? epi.emit_gid[val[j]] : 0u;
   }
   // stable warp multisplit: rank = items of the same digit earlier in (iteration, lane) order
   const uint32_t lt = lanemask_lt();
@@ -221,7 +221,9 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
       const uint32_t k = S.keys[i];
       const uint32_t o = S.bin_base[(k >> shift) & 255u] + (uint32_t)i;
       const uint32_t v = S.vals[i];
-      epi.sorted[o] = make_uint2(ISG_EPI_PREFETCH ? S.gids[i] : epi.emit_gid[v], v);
+      epi.sorted[o] = epi.vals_are_gids
+                          ? make_uint2(v, o)
+                          : make_uint2(ISG_EPI_PREFETCH ? S.gids[i] : epi.emit_gid[v], v);
       if (i == 0 || S.keys[i - 1] != k) atomicMin(&epi.ranges[k].x, o);
       if (i == nvalid - 1 || S.keys[i + 1] != k) atomicMax(&epi.ranges[k].y, o + 1u);
     }
