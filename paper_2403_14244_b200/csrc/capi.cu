@@ -312,7 +312,7 @@ isg_status ensure_sort_scratch(isg_ctx* ctx, int64_t cap) {
   const int64_t t = std::max<int64_t>(tiles, 1);
   ISG_CUDA(realloc_dev(ctx, &ctx->sort.hist, isg::kMaxPasses * 256));
   ISG_CUDA(realloc_dev(ctx, &ctx->sort.counters, isg::kMaxPasses + 1));
-  ISG_CUDA(realloc_dev(ctx, &ctx->sort.lookback, (size_t)isg::kMaxPasses * 256 * t));
+  ISG_CUDA(realloc_dev(ctx, &ctx->sort.lookback, (size_t)isg::kMaxPasses * isg::sort_lookback_words(t)));
   ctx->sort.max_tiles = t;
   ctx->sort_tiles_alloc = t;
   return ISG_OK;

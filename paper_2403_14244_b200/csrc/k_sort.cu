@@ -29,13 +29,18 @@
 #define ISG_EPI_PREFETCH 1
 #endif
 #ifndef ISG_LOOKBACK_WIN
-#define ISG_LOOKBACK_WIN 16
+#define ISG_LOOKBACK_WIN 8
+#endif
+#ifndef ISG_LOOKBACK_GROUP
+#define ISG_LOOKBACK_GROUP 8
 #endif
 
 namespace isg {
 
 namespace {
 
+constexpr int kLbWin = ISG_LOOKBACK_WIN;      // level-2 rows read per round trip
+constexpr int kLbGroup = ISG_LOOKBACK_GROUP;  // tiles per level-2 group
 constexpr uint32_t kFlagAgg = 1u << 30;
 constexpr uint32_t kFlagInc = 2u << 30;
 constexpr uint32_t kCountMask = (1u << 30) - 1;
@@ -165,8 +170,8 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
     cnt += c;
   }
   // publish this tile's aggregate (or inclusive prefix for tile 0) as early as possible
-  uint32_t* my = lookback + (int64_t)tile * 256 + tid;
-  st_volatile(my, (tile == 0 ? kFlagInc : kFlagAgg) | cnt);
+  // level 1: this tile's per-digit count, published as early as possible (never upgraded)
+  st_volatile(lookback + (int64_t)tile * 256 + tid, kFlagAgg | cnt);
   uint32_t tot;
   const uint32_t local_start = block_excl_scan_256(cnt, S.warp_tmp, tot);
   S.local_start[tid] = local_start;
@@ -184,30 +189,53 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
     }
   }
   const uint32_t gpre = hist[tid];  // exclusive digit offset (k_hist's last block scanned)
-  // decoupled look-back for digit `tid`
+  // Two-level decoupled look-back for digit `tid`.  Tiles form groups of kLbGroup; a tile sums
+  // the counts of the earlier tiles of its own group (level 1, one round of loads), and the
+  // prefix of all earlier groups from the level-2 words: each group's last tile publishes the
+  // group's count (AGG) as soon as it has read its group, and the inclusive prefix through the
+  // group (INC) once it knows the group's start.  A tile therefore reads at most kLbGroup - 1
+  // level-1 rows and one row per earlier group back to the nearest inclusive one, instead of
+  // every earlier tile's row when the whole pass is resident at once (one wave: small sorts).
   uint32_t excl = 0;
-  if (tile > 0) {
-    // walk back kWin predecessors per round trip, all loads in flight at once (statuses only
-    // move 0 -> AGG -> INC, so a stale aggregate is still a correct partial sum); the
-    // inclusive-prefix frontier then advances kWin tiles per L2 round trip
-    constexpr int kWin = ISG_LOOKBACK_WIN;
-    int64_t p = (int64_t)tile - 1;
-    bool found = false;
-    while (!found) {
-      uint32_t sw[kWin];
+  {
+    uint32_t* const l2 = lookback + 256 * ((cap + kSortTileItems - 1) / kSortTileItems);
+    const int64_t g = (int64_t)tile / kLbGroup;
+    const int r = (int)((int64_t)tile - g * kLbGroup);
+    uint32_t sw[kLbGroup - 1];
 #pragma unroll
-      for (int q = 0; q < kWin; ++q)
-        sw[q] = p - q >= 0 ? ld_volatile(lookback + (p - q) * 256 + tid) : kFlagInc;
+    for (int q = 0; q < kLbGroup - 1; ++q)
+      sw[q] = q < r ? ld_volatile(lookback + ((int64_t)tile - 1 - q) * 256 + tid) : kFlagAgg;
 #pragma unroll
-      for (int q = 0; q < kWin; ++q) {
-        if (found) break;
-        while ((sw[q] & ~kCountMask) == 0) sw[q] = ld_volatile(lookback + (p - q) * 256 + tid);
+    for (int q = 0; q < kLbGroup - 1; ++q) {
+      if (q < r) {
+        while ((sw[q] & ~kCountMask) == 0)
+          sw[q] = ld_volatile(lookback + ((int64_t)tile - 1 - q) * 256 + tid);
         excl += sw[q] & kCountMask;
-        found = (sw[q] & ~kCountMask) == kFlagInc;
       }
-      p -= kWin;
     }
-    st_volatile(my, kFlagInc | (excl + cnt));
+    const bool last = r == kLbGroup - 1;
+    if (last) st_volatile(l2 + g * 256 + tid, (g == 0 ? kFlagInc : kFlagAgg) | (excl + cnt));
+    if (g > 0) {
+      uint32_t gp = 0;
+      int64_t p = g - 1;
+      bool found = false;
+      while (!found) {
+        uint32_t w2[kLbWin];
+#pragma unroll
+        for (int q = 0; q < kLbWin; ++q)
+          w2[q] = p - q >= 0 ? ld_volatile(l2 + (p - q) * 256 + tid) : kFlagInc;
+#pragma unroll
+        for (int q = 0; q < kLbWin; ++q) {
+          if (found) break;
+          while ((w2[q] & ~kCountMask) == 0) w2[q] = ld_volatile(l2 + (p - q) * 256 + tid);
+          gp += w2[q] & kCountMask;
+          found = (w2[q] & ~kCountMask) == kFlagInc;
+        }
+        p -= kLbWin;
+      }
+      if (last) st_volatile(l2 + g * 256 + tid, kFlagInc | (gp + excl + cnt));
+      excl += gp;
+    }
   }
   S.bin_base[tid] = gpre + excl - local_start;
   __syncthreads();
@@ -437,7 +465,7 @@ int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], bool iota_vals, const
   if (!opt.scratch_zeroed) {
     cudaMemsetAsync(s.hist, 0, sizeof(uint32_t) * kMaxPasses * 256, st);
     cudaMemsetAsync(s.counters, 0, sizeof(uint32_t) * (kMaxPasses + 1), st);
-    cudaMemsetAsync(s.lookback, 0, sizeof(uint32_t) * 256 * (size_t)tiles * passes, st);
+    cudaMemsetAsync(s.lookback, 0, sizeof(uint32_t) * sort_lookback_words(tiles) * passes, st);
   }
   if (!opt.hist_ready) {
     const int hist_blocks = (int)std::min<int64_t>(std::max<int64_t>(tiles, 1), 148 * 4);
@@ -460,7 +488,7 @@ int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], bool iota_vals, const
                dim3((unsigned)std::max<int64_t>(tiles, 1)), dim3(kSortThreads), smem, st,
                (const uint32_t*)keys[cur], (const uint32_t*)((p == 0 && iota_vals) ? nullptr : vals[cur]),
                keys[cur ^ 1], vals[cur ^ 1], n_dev, cap, 8 * p, (const uint32_t*)(s.hist + 256 * p),
-               s.lookback + (size_t)256 * tiles * p, s.counters + p,
+               s.lookback + sort_lookback_words(tiles) * p, s.counters + p,
                fin ? epi : SortEpilogue());
     cur ^= 1;
   }
