@@ -71,8 +71,10 @@ __device__ __forceinline__ void fwd_pair(FwdPair& p, float2 r2, const float4 g, 
   const bool in0 = !(r2.x > g.z) && (p.T.x > t_min);
   const bool in1 = !(r2.y > g.z) && (p.T.y > t_min);
   const float2 q = __fmul2_rn(r2, bc(g.w));
-  const float2 e = __fmul2_rn(bc(c.w), make_float2(fast_exp2(q.x), fast_exp2(q.y)));
-  const float2 a = make_float2(in0 ? e.x : 0.0f, in1 ? e.y : 0.0f);
+  // an excluded pixel's exponential is never evaluated (predicated MUFU into a zeroed pair), so
+  // a = o * 0 = 0 exactly, the same value the select after the product gave
+  const float2 a = __fmul2_rn(bc(c.w), make_float2(in0 ? fast_exp2(q.x) : 0.0f,
+                                                   in1 ? fast_exp2(q.y) : 0.0f));
   const float2 wgt = __fmul2_rn(p.T, a);
   p.Cr = __ffma2_rn(wgt, bc(c.x), p.Cr);
   p.Cg = __ffma2_rn(wgt, bc(c.y), p.Cg);

@@ -89,3 +89,21 @@ for Wn in (32, 64, 96, 128, 256):
     for s_ in range(16): C2[:, s_] = np.bincount(inv2, weights=rel[:, s_], minlength=len(uk2))
     print('window', Wn, 'lockstep steps', C2[:, :8].max(1).sum() + C2[:, 8:].max(1).sum(),
           'windows', len(uk2))
+
+# Entries past a sub-quarter's own last contributor (j >= max np over its 16 pixels) contribute
+# exact zeros: lists that skip them (batch 128 lockstep)
+sqmax = npr_p.reshape(ty_n, 4, 4, tx_n, 4, 4).max(axis=(2, 5))  # [ty, r4, tx, c4]
+G16 = np.zeros((len(g), 16), np.int64)
+for r4 in range(4):
+    for c4 in range(4):
+        G16[:, 4 * r4 + c4] = sqmax[ty, r4, tx, c4]
+relx = rel & (pos[:, None] < G16)
+print('relevant pairs', rel.sum(), 'before own max np', relx.sum())
+for Wn in (128,):
+    bw = (m[tile] - 1 - pos) // Wn
+    key2 = tile * 100000 + bw
+    uk2, inv2 = np.unique(key2, return_inverse=True)
+    for nm, RR in (('all', rel), ('trimmed', relx)):
+        C2 = np.zeros((len(uk2), 16), np.int64)
+        for s_ in range(16): C2[:, s_] = np.bincount(inv2, weights=RR[:, s_], minlength=len(uk2))
+        print(nm, 'window', Wn, 'lockstep steps', C2[:, :8].max(1).sum() + C2[:, 8:].max(1).sum())
