@@ -15,7 +15,7 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
 OBJS = {"k_blend_fwd": "build/isg/k_blend.o", "k_blend_bwd": "build/isg/k_blend_bwd.o",
-        "k_project_adam": "build/isg/k_adam.o", "k_preprocess": "build/isg/k_preprocess.o"}
+        "k_adam_stream": "build/isg/k_adam.o", "k_preprocess": "build/isg/k_preprocess.o"}
 CLASSES = {  # opcode -> class
     "FFMA2": "fp32x2", "FMUL2": "fp32x2", "FADD2": "fp32x2", "FFMA": "fp32", "FMUL": "fp32",
     "FADD": "fp32", "MUFU": "mufu", "SHFL": "shuffle", "FSEL": "select", "SEL": "select",

@@ -30,6 +30,12 @@ FULL_METRICS = [
     "sm__warps_active.avg.per_cycle_active", "smsp__warps_eligible.avg.per_cycle_active",
     "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem",
     "lts__t_sectors_op_red.sum", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+    "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_not_selected_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
 ]
 
 
