@@ -2,24 +2,29 @@
 //
 // The backward the reference does not have (its 2D analogue is loss_gradients,
 // /root/reference/proj/src/loss.cpp:259-300).  Per pixel it walks the tile's depth-ordered
-// list in reverse from the last processed entry (n_proc - 1), recovering the transmittance
-// T_k = T_{k+1} / (1 - a_k) (the forward stores T *before* the last contributor, so a = 1 is
-// never divided by), and accumulating with A = colour behind:
+// list in reverse from the last contributor (n_proc - 1), recovering the transmittance
+// T_k = T_{k+1} / (1 - a_k) from the pixel's final transmittance (a tile where that is not a
+// normal float — alpha = 1 or underflow — gets T before the last contributor instead, see
+// k_blend.cu, and does not divide for it), and accumulating with A = colour behind (SURVEY
+// Appendix A):
 //     dL/da_k = T_k G.(c_k - A_k),  dL/dc_k = G T_k a_k,  A <- a c + (1 - a) A
 // with G = dL/dC = 2 w (C - target) / (3 W H) (mse, src/image.cpp:50-58) computed in the
 // prologue — or, for the L1 + D-SSIM loss, read from the dL/dC image k_ssim.cu wrote — and the
 // kernel closed forms of include/isosplat/kernels.hpp:208-222.
 //
 // Mapping: 64 threads per tile.  Each four-lane group owns one 4x4 sub-quarter and each lane a
-// 2x2 pixel quad (two packed f32x2 pixel pairs).  Per staged batch of 32 records every warp
-// tests the records against its 8 sub-quarters (shared per-axis terms), ballots, and compacts 8
-// relevance lists; the 8 groups then walk their OWN lists in lockstep in reverse — eight
-// different splats per warp step — so culling is at 4x4 granularity (a typical 6-px 3-sigma
-// circle covers a 4x4 region far better than an 8x8 one) and the per-entry reduction runs
-// over only 4 lanes.  The 7 gradients of a pair are summed over the lane's 4 pixels,
-// reduce-scattered over the group in 6 shuffles, combined over the 16 sub-quarters in shared
-// memory in a fixed order and written — no atomics — to the pair's gradient slot; K8 sums each
-// splat's slots in a fixed order, so gradients are bitwise deterministic.
+// 2x2 pixel quad (two packed f32x2 pixel pairs).  Per staged batch (128 records in direct
+// mode, 32 in slot mode) every warp turns the entries' sub-quarter masks (written by the
+// forward) into 8 relevance lists by ballots; the 8 groups then walk their OWN lists in
+// lockstep in reverse — eight different splats per warp step — so culling is at 4x4
+// granularity (a typical 6-px 3-sigma circle covers a 4x4 region far better than an 8x8 one)
+// and the per-entry reduction runs over only 4 lanes.  The 7 gradients of a pair are summed
+// over the lane's 4 pixels and reduce-scattered over the group in 6 shuffles.  Direct mode
+// (default): each lane adds its 2 values to the splat's 2D sums with one L2 reduction
+// (red.global.add.v2.f32; the 4 lanes cover one 32-B sector).  Slot mode (deterministic): the
+// 16 sub-quarters are combined in shared memory in a fixed order and written — no atomics —
+// to the pair's gradient slot; K8 sums each splat's slots in a fixed order, so gradients are
+// bitwise deterministic.
 #include "blend_common.cuh"
 
 namespace isg {
