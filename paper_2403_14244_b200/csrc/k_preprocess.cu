@@ -60,15 +60,39 @@ __global__ void __launch_bounds__(256) k_preprocess(const float4* __restrict__ m
           const int bw = x1 - x0 + 1;
           const bool small = bw * (y1 - y0 + 1) <= 32 && bw < 256 && x0 < 4096 && y0 < 4096;
           uint32_t mask = 0;
-          // tile_hit, separably: the row's y term once per row (bit-identical decisions)
+          // tile_hit, separably (bit-identical decisions): the row's y term once per row and,
+          // for boxes up to kCols tiles wide (all but the largest splats), every column's x
+          // term once per splat instead of once per tile
           uint32_t bit = 1u;
-          for (int ty = y0; ty <= y1; ++ty) {
-            const float ay = axis_d2(p.v, ty, fp.cam.height);
-            for (int tx = x0; tx <= x1; ++tx, bit <<= 1) {
-              if (__fadd_rn(axis_d2(p.u, tx, fp.cam.width), ay) > p.r2max) continue;
-              mask |= bit;  // (only meaningful when small: <= 32 tiles)
-              ++count;
-              if (tile_cnt) atomicAdd(&tile_cnt[ty * fp.tiles_x + tx], 1u);
+          constexpr int kCols = 8;
+          if (bw <= kCols) {
+            float ax[kCols];
+#pragma unroll
+            for (int c = 0; c < kCols; ++c)
+              ax[c] = c < bw ? axis_d2(p.u, x0 + c, fp.cam.width) : 0.0f;
+            for (int ty = y0; ty <= y1; ++ty) {
+              const float ay = axis_d2(p.v, ty, fp.cam.height);
+#pragma unroll
+              for (int c = 0; c < kCols; ++c) {
+                if (c < bw) {
+                  if (!(__fadd_rn(ax[c], ay) > p.r2max)) {
+                    mask |= bit;  // (only meaningful when small: <= 32 tiles)
+                    ++count;
+                    if (tile_cnt) atomicAdd(&tile_cnt[ty * fp.tiles_x + x0 + c], 1u);
+                  }
+                  bit <<= 1;
+                }
+              }
+            }
+          } else {
+            for (int ty = y0; ty <= y1; ++ty) {
+              const float ay = axis_d2(p.v, ty, fp.cam.height);
+              for (int tx = x0; tx <= x1; ++tx, bit <<= 1) {
+                if (__fadd_rn(axis_d2(p.u, tx, fp.cam.width), ay) > p.r2max) continue;
+                mask |= bit;
+                ++count;
+                if (tile_cnt) atomicAdd(&tile_cnt[ty * fp.tiles_x + tx], 1u);
+              }
             }
           }
           // emission kernels iterate the hit bits instead of re-projecting; a bigger box
@@ -80,7 +104,10 @@ __global__ void __launch_bounds__(256) k_preprocess(const float4* __restrict__ m
       }
       tilebox[i] = box;
       RenderRec r;  // (u, v, r2max, -log2(e)/sigma2d^2), (r, g, b, opacity)
-      r.geo = make_float4(p.u, p.v, p.r2max, __fdiv_rn(-1.4426950408889634f, __fmul_rn(p.s, p.s)));
+      // -log2(e) / sigma2d^2 feeds only ex2.approx (no inclusion decision): a MUFU reciprocal
+      float inv_s2;
+      asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv_s2) : "f"(__fmul_rn(p.s, p.s)));
+      r.geo = make_float4(p.u, p.v, p.r2max, -1.4426950408889634f * inv_s2);
       r.col = c;
       rec[i] = r;
       key = count ? __float_as_uint(p.zc) : 0xFFFFFFFFu;
