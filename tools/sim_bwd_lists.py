@@ -107,3 +107,23 @@ for Wn in (128,):
         C2 = np.zeros((len(uk2), 16), np.int64)
         for s_ in range(16): C2[:, s_] = np.bincount(inv2, weights=RR[:, s_], minlength=len(uk2))
         print(nm, 'window', Wn, 'lockstep steps', C2[:, :8].max(1).sum() + C2[:, 8:].max(1).sum())
+
+# 2-lane groups over 4x2 half sub-quarters (16 groups per warp): finer culling, 2-lane reduce,
+# lockstep over 16 lists per warp.  rel8[:, 2*s + h]: sub-quarter s, half h (top/bottom 2 rows)
+rel8 = np.zeros((len(g), 32), bool)
+for r4 in range(4):
+    for c4 in range(4):
+        for h in range(2):
+            y0 = ty * 16 + 4 * r4 + 2 * h + 0.5; y1 = np.minimum(ty * 16 + 4 * r4 + 2 * h + 2, H) - 1 + 0.5
+            dy = np.clip(v[g], y0, y1) - v[g]
+            x0 = tx * 16 + 4 * c4 + 0.5; x1 = np.minimum(tx * 16 + 4 * c4 + 4, W) - 1 + 0.5
+            dx = np.clip(u[g], x0, x1) - u[g]
+            rel8[:, 2 * (4 * r4 + c4) + h] = (dx * dx + dy * dy <= r2m[g]) & (ty * 16 + 4 * r4 + 2 * h < H) & (tx * 16 + 4 * c4 < W)
+bw = (m[tile] - 1 - pos) // 128
+key2 = tile * 100000 + bw
+uk2, inv2 = np.unique(key2, return_inverse=True)
+C32 = np.zeros((len(uk2), 32), np.int64)
+for s_ in range(32): C32[:, s_] = np.bincount(inv2, weights=rel8[:, s_], minlength=len(uk2))
+steps8 = C32[:, :16].max(1).sum() + C32[:, 16:].max(1).sum()
+print('4x2 groups: relevant group-entry pairs', rel8.sum(), '(x8 px =', rel8.sum() * 8, 'slots) vs 4x4', rel.sum() * 16,
+      '; lockstep warp steps', steps8, '(x 16 groups x 8 px =', steps8 * 128, 'slots)')
