@@ -582,90 +582,172 @@ def run_isg(args):
     r.profile(False)
 
     # ---- end to end through the public API with host buffers ------------------------------
-    # Train: every step uploads its targets from pinned host memory and reads its loss back;
-    # step i+2's upload runs on a copy stream into the third of three target buffers while
-    # step i computes (the prefetch a training loop does), and the host reads step i-1's loss
-    # (copied D2H inside step i-1's graph) while step i runs.  Render: time_render().
-    # --no-graph: isg_loss_backward with the host target per view + Adam + sync.
-    host_targets = [t.cpu().numpy() for t in targets]
-    pinned = [torch.from_numpy(h).pin_memory() for h in host_targets]
-    host_views = [p.numpy() for p in pinned]
-    use_pipe = train and graph is not None
-    NB = 3  # target buffers: step i+2's upload may start once step i-1 is done
-    step_losses = []
-    if use_pipe:
-        bufs = [[torch.empty_like(t) for t in targets] for _ in range(NB)]
-        loss_host = torch.zeros(NB, dtype=torch.float64).pin_memory()
-        graphs = []
-        for b in range(NB):
-            def step_b(bb=bufs[b], slot=loss_host[b:b + 1]):
-                for c, t in zip(cams, bb):
-                    r.loss_backward_device(c, t.data_ptr(), opts, weight=1.0 / step_views)
-                r.adam_step(cfg)
-                r.step_loss_async(slot.data_ptr())  # the step's loss D2H, inside the graph
-            for t, h in zip(bufs[b], pinned):
-                t.copy_(h)
-            r.graph_begin()
-            step_b()
-            graphs.append(r.graph_end())
-        copy_stream = torch.cuda.Stream()
-        ev_copy = [torch.cuda.Event() for _ in range(NB)]
-        ev_done = [torch.cuda.Event() for _ in range(NB)]
-        r.synchronize()
-    e2e = None
-    if train:
-        r.restore()
-        barrier()
-        l0 = r.stats()["kernel_launches"]
-        t_start = time.perf_counter()
+    # --e2e ring (default): the C-ABI target ring, no torch copies; --e2e graph: one CUDA
+    # graph per step with torch copies of the targets on a side stream (round-2 first session).
+    if args.e2e == "graph":
+        # Train: every step uploads its targets from pinned host memory and reads its loss back;
+        # step i+2's upload runs on a copy stream into the third of three target buffers while
+        # step i computes (the prefetch a training loop does), and the host reads step i-1's loss
+        # (copied D2H inside step i-1's graph) while step i runs.  Render: time_render().
+        # --no-graph: isg_loss_backward with the host target per view + Adam + sync.
+        host_targets = [t.cpu().numpy() for t in targets]
+        pinned = [torch.from_numpy(h).pin_memory() for h in host_targets]
+        host_views = [p.numpy() for p in pinned]
+        use_pipe = train and graph is not None
+        NB = 3  # target buffers: step i+2's upload may start once step i-1 is done
+        step_losses = []
         if use_pipe:
-            with torch.cuda.stream(copy_stream):
-                for k in range(min(NB - 1, args.steps)):
-                    for t, h in zip(bufs[k], pinned):
-                        t.copy_(h, non_blocking=True)
-                    ev_copy[k].record(copy_stream)
-        for i in range(args.steps):
+            bufs = [[torch.empty_like(t) for t in targets] for _ in range(NB)]
+            loss_host = torch.zeros(NB, dtype=torch.float64).pin_memory()
+            graphs = []
+            for b in range(NB):
+                def step_b(bb=bufs[b], slot=loss_host[b:b + 1]):
+                    for c, t in zip(cams, bb):
+                        r.loss_backward_device(c, t.data_ptr(), opts, weight=1.0 / step_views)
+                    r.adam_step(cfg)
+                    r.step_loss_async(slot.data_ptr())  # the step's loss D2H, inside the graph
+                for t, h in zip(bufs[b], pinned):
+                    t.copy_(h)
+                r.graph_begin()
+                step_b()
+                graphs.append(r.graph_end())
+            copy_stream = torch.cuda.Stream()
+            ev_copy = [torch.cuda.Event() for _ in range(NB)]
+            ev_done = [torch.cuda.Event() for _ in range(NB)]
+            r.synchronize()
+        e2e = None
+        if train:
+            r.restore()
+            barrier()
+            l0 = r.stats()["kernel_launches"]
+            t_start = time.perf_counter()
             if use_pipe:
-                b = i % NB
-                stream.wait_event(ev_copy[b])
-                graphs[b].launch()
-                ev_done[b].record(stream)
-                if i + NB - 1 < args.steps:  # prefetch step i+2's inputs once step i-1 is done
-                    nb = (i + NB - 1) % NB
-                    with torch.cuda.stream(copy_stream):
-                        copy_stream.wait_event(ev_done[nb])
-                        for t, h in zip(bufs[nb], pinned):
+                with torch.cuda.stream(copy_stream):
+                    for k in range(min(NB - 1, args.steps)):
+                        for t, h in zip(bufs[k], pinned):
                             t.copy_(h, non_blocking=True)
-                        ev_copy[nb].record(copy_stream)
-                if i >= 1:  # step i-1's loss is on the host once its graph is done
-                    pb = (i - 1) % NB
-                    ev_done[pb].synchronize()
-                    step_losses.append(float(loss_host[pb]))
-            else:
-                for c, h in zip(cams, host_views):
-                    r.loss_backward(c, h, opts, weight=1.0 / step_views)  # H2D target, D2H loss
-                r.adam_step(cfg)
-                r.synchronize()
+                        ev_copy[k].record(copy_stream)
+            for i in range(args.steps):
+                if use_pipe:
+                    b = i % NB
+                    stream.wait_event(ev_copy[b])
+                    graphs[b].launch()
+                    ev_done[b].record(stream)
+                    if i + NB - 1 < args.steps:  # prefetch step i+2's inputs once step i-1 is done
+                        nb = (i + NB - 1) % NB
+                        with torch.cuda.stream(copy_stream):
+                            copy_stream.wait_event(ev_done[nb])
+                            for t, h in zip(bufs[nb], pinned):
+                                t.copy_(h, non_blocking=True)
+                            ev_copy[nb].record(copy_stream)
+                    if i >= 1:  # step i-1's loss is on the host once its graph is done
+                        pb = (i - 1) % NB
+                        ev_done[pb].synchronize()
+                        step_losses.append(float(loss_host[pb]))
+                else:
+                    for c, h in zip(cams, host_views):
+                        r.loss_backward(c, h, opts, weight=1.0 / step_views)  # H2D target, D2H loss
+                    r.adam_step(cfg)
+                    r.synchronize()
+            if use_pipe:
+                ev_done[(args.steps - 1) % NB].synchronize()
+                step_losses.append(float(loss_host[(args.steps - 1) % NB]))
+            e2e_step = (time.perf_counter() - t_start) * 1e3 / args.steps
+            launches_per_step = (r.stats()["kernel_launches"] - l0) / args.steps
+            if world > 1:
+                tt = torch.tensor([e2e_step], device="cuda")
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                e2e_step = float(tt.item())
+            e2e = {"value": iters_per_step / (e2e_step / 1e3), "unit": unit,
+                   "h2d_bytes_per_step": sum(h.nbytes for h in host_views),
+                   "d2h_bytes_per_step": 8 if use_pipe else 8 * len(host_views),
+                   "ms_per_step": e2e_step, "gpu_launches_per_step": launches_per_step,
+                   **({"loss_first_last": [step_losses[0], step_losses[-1]],
+                       "losses_read": len(step_losses)} if use_pipe else {}),
+                   "mode": ("cuda graph per step, targets prefetched two steps ahead from pinned "
+                            "host memory on a copy stream (3 buffers); every step's loss copied "
+                            "D2H into pinned memory inside its graph and read by the host while "
+                            "the next step runs (all reads inside the timed region)") if use_pipe
+                   else "isg_loss_backward with host targets per view + adam_step + sync"}
+
+    else:
+        # Train: every step uploads its targets from pinned host memory through the C-ABI's target
+        # ring (isg_upload_target_async: step i+2's views on the library's copy stream while step i
+        # computes; isg_loss_backward_slot: only the backward waits for its upload) and reads its
+        # loss back (isg_step_loss_async into pinned memory; the host reads step i-1's loss while
+        # step i runs).  No torch copy is involved (torch events only tell the host when a loss
+        # landed).  Render: time_render().  --no-graph: isg_loss_backward (synchronous) per view.
+        host_targets = [t.cpu().numpy() for t in targets]
+        pinned = [torch.from_numpy(h).pin_memory() for h in host_targets]
+        host_views = [p.numpy() for p in pinned]
+        use_pipe = train and graph is not None
+        NB = 3  # ring slots per view: step i+2's upload may start once step i-1 has read its slot
+        step_losses = []
         if use_pipe:
-            ev_done[(args.steps - 1) % NB].synchronize()
-            step_losses.append(float(loss_host[(args.steps - 1) % NB]))
-        e2e_step = (time.perf_counter() - t_start) * 1e3 / args.steps
-        launches_per_step = (r.stats()["kernel_launches"] - l0) / args.steps
-        if world > 1:
-            tt = torch.tensor([e2e_step], device="cuda")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e_step = float(tt.item())
-        e2e = {"value": iters_per_step / (e2e_step / 1e3), "unit": unit,
-               "h2d_bytes_per_step": sum(h.nbytes for h in host_views),
-               "d2h_bytes_per_step": 8 if use_pipe else 8 * len(host_views),
-               "ms_per_step": e2e_step, "gpu_launches_per_step": launches_per_step,
-               **({"loss_first_last": [step_losses[0], step_losses[-1]],
-                   "losses_read": len(step_losses)} if use_pipe else {}),
-               "mode": ("cuda graph per step, targets prefetched two steps ahead from pinned "
-                        "host memory on a copy stream (3 buffers); every step's loss copied "
-                        "D2H into pinned memory inside its graph and read by the host while "
-                        "the next step runs (all reads inside the timed region)") if use_pipe
-               else "isg_loss_backward with host targets per view + adam_step + sync"}
+            loss_host = torch.zeros(NB, dtype=torch.float64).pin_memory()
+            ev_done = [torch.cuda.Event() for _ in range(NB)]
+
+            def upload(i):  # step i's views into ring slots (i % NB) * views + v
+                for v, h in enumerate(host_views):
+                    r.upload_target_async((i % NB) * len(host_views) + v, h)
+
+            def ring_step(i):
+                for v, c in enumerate(cams):
+                    r.loss_backward_slot(c, (i % NB) * len(cams) + v, opts, weight=1.0 / step_views)
+                r.adam_step(cfg)
+                r.step_loss_async(loss_host[i % NB:i % NB + 1].data_ptr())
+            if len(host_views) * NB > isg.TARGET_SLOTS:
+                raise SystemExit(f"bench: {len(host_views)} views need {len(host_views) * NB} target "
+                                 f"ring slots (ISG_TARGET_SLOTS = {isg.TARGET_SLOTS})")
+            for i in range(NB):  # allocate the slots outside the timed region
+                upload(i)
+            r.synchronize()
+        e2e = None
+        if train:
+            r.restore()
+            barrier()
+            l0 = r.stats()["kernel_launches"]
+            t_start = time.perf_counter()
+            if use_pipe:
+                for k in range(min(NB - 1, args.steps)):
+                    upload(k)
+            for i in range(args.steps):
+                if use_pipe:
+                    if i + NB - 1 < args.steps:  # step i+2's upload waits for step i-1's reads
+                        upload(i + NB - 1)
+                    ring_step(i)
+                    ev_done[i % NB].record(stream)
+                    if i >= 1:  # step i-1's loss is on the host once its work is done
+                        pb = (i - 1) % NB
+                        ev_done[pb].synchronize()
+                        step_losses.append(float(loss_host[pb]))
+                else:
+                    for c, h in zip(cams, host_views):
+                        r.loss_backward(c, h, opts, weight=1.0 / step_views)  # H2D target, D2H loss
+                    r.adam_step(cfg)
+                    r.synchronize()
+            if use_pipe:
+                ev_done[(args.steps - 1) % NB].synchronize()
+                step_losses.append(float(loss_host[(args.steps - 1) % NB]))
+            e2e_step = (time.perf_counter() - t_start) * 1e3 / args.steps
+            launches_per_step = (r.stats()["kernel_launches"] - l0) / args.steps
+            if world > 1:
+                tt = torch.tensor([e2e_step], device="cuda")
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                e2e_step = float(tt.item())
+            e2e = {"value": iters_per_step / (e2e_step / 1e3), "unit": unit,
+                   "h2d_bytes_per_step": sum(h.nbytes for h in host_views),
+                   "d2h_bytes_per_step": 8 if use_pipe else 8 * len(host_views),
+                   "ms_per_step": e2e_step, "gpu_launches_per_step": launches_per_step,
+                   **({"loss_first_last": [step_losses[0], step_losses[-1]],
+                       "losses_read": len(step_losses)} if use_pipe else {}),
+                   "mode": ("C-ABI only: targets uploaded from pinned host memory two steps ahead "
+                            "into the library's target ring (isg_upload_target_async on its copy "
+                            "stream, isg_loss_backward_slot), every step's loss copied D2H into "
+                            "pinned memory (isg_step_loss_async) and read by the host while the "
+                            "next step runs (all reads inside the timed region); kernel by kernel, "
+                            "no graph") if use_pipe
+                   else "isg_loss_backward with host targets per view + adam_step + sync"}
 
     # ---- render FPS (C2): BASELINE's second metric on the same scene and camera ------------
     render = None
@@ -799,6 +881,9 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="isg", choices=["isg", "reference"])
+    ap.add_argument("--e2e", default="ring", choices=["ring", "graph"],
+                    help="end-to-end path: the C-ABI target ring (default) or CUDA graphs with "
+                         "torch-side target copies")
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-graph", action="store_true",

@@ -118,6 +118,19 @@ isg_status isg_loss_backward(isg_ctx* ctx, const isg_camera* cam, const float bg
 /* Device target pointer; asynchronous; the loss accumulates on device (isg_read_loss). */
 isg_status isg_loss_backward_device(isg_ctx* ctx, const isg_camera* cam, const float bg[3],
                                     float t_min, const float* target_hwc3_dev, float weight);
+/* Host-buffer training without a host sync per view: a ring of ISG_TARGET_SLOTS device
+ * target images owned by the context (each allocated on its first upload).  isg_upload_target_async enqueues the host-to-device copy
+ * of one view's HWC3 target into ring slot `slot` on the context's copy stream and returns at
+ * once (`host_hwc3` should be page-locked and stay unchanged until the copy has run; the copy
+ * first waits for the last enqueued frame that read the slot).  isg_loss_backward_slot is
+ * isg_loss_backward_device on that slot: binning and the forward blend run while the upload
+ * may still be in flight, only the backward waits for it.  A caller uploads view i + 2 while
+ * view i trains (the pattern bench.py's end-to-end number uses: 3 slots per view of a step). */
+#define ISG_TARGET_SLOTS 32
+isg_status isg_upload_target_async(isg_ctx* ctx, int32_t slot, const float* host_hwc3,
+                                   int32_t width, int32_t height);
+isg_status isg_loss_backward_slot(isg_ctx* ctx, const isg_camera* cam, const float bg[3],
+                                  float t_min, int32_t slot, float weight);
 /* Sum of losses of the views since the last isg_adam_step/isg_zero_grads (syncs). */
 isg_status isg_read_loss(isg_ctx* ctx, double* loss_out);
 isg_status isg_zero_grads(isg_ctx* ctx);

@@ -42,6 +42,12 @@ struct isg_ctx {
   bool own_stream = false;
   cudaStream_t copy_stream = nullptr;  // host<->device uploads overlapped with compute
   cudaEvent_t ev_main = nullptr, ev_copy = nullptr;
+  // target ring for host-buffer training (isg_upload_target_async / isg_loss_backward_slot):
+  // per slot the device image, the event of its last upload and of the last frame that read it
+  float* tring[ISG_TARGET_SLOTS] = {};
+  size_t tring_floats[ISG_TARGET_SLOTS] = {};
+  cudaEvent_t ev_tup[ISG_TARGET_SLOTS] = {}, ev_tread[ISG_TARGET_SLOTS] = {};
+  bool tring_read[ISG_TARGET_SLOTS] = {};
   std::string err;
 
   // scene (SoA float4) and Adam moments (n x 2 float4 each)
@@ -811,6 +817,11 @@ void isg_destroy(isg_ctx* ctx) {
   }
   if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
   if (ctx->ev_copy) cudaEventDestroy(ctx->ev_copy);
+  for (int k = 0; k < ISG_TARGET_SLOTS; ++k) {
+    if (ctx->ev_tup[k]) cudaEventDestroy(ctx->ev_tup[k]);
+    if (ctx->ev_tread[k]) cudaEventDestroy(ctx->ev_tread[k]);
+    if (ctx->tring[k]) cudaFree(ctx->tring[k]);
+  }
   if (ctx->copy_stream) {
     cudaStreamSynchronize(ctx->copy_stream);
     cudaStreamDestroy(ctx->copy_stream);
@@ -968,6 +979,62 @@ isg_status isg_loss_backward_device(isg_ctx* ctx, const isg_camera* cam, const f
   const FrameParams fp = make_fp(cam, bg, t_min);
   if ((s = launch_frame(ctx, fp, nullptr, true)) != ISG_OK) return s;
   return run_backward(ctx, fp, target_dev, weight);
+}
+
+isg_status isg_upload_target_async(isg_ctx* ctx, int32_t slot, const float* host_hwc3,
+                                   int32_t width, int32_t height) {
+  if (!ctx) return ISG_E_ARG;
+  ISG_NO_CAPTURE("isg_upload_target_async");
+  if (slot < 0 || slot >= ISG_TARGET_SLOTS) return fail(ctx, ISG_E_ARG, "upload_target: bad slot");
+  if (!host_hwc3 || width <= 0 || height <= 0)
+    return fail(ctx, ISG_E_ARG, "upload_target: null target or empty image");
+  cudaSetDevice(ctx->device);
+  const size_t floats = 3 * (size_t)width * (size_t)height;
+  if (floats > ctx->tring_floats[slot]) {
+    // (re)allocating the slot: nothing may still read or fill it
+    if (ctx->tring[slot]) {
+      ISG_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+      ISG_CUDA(cudaStreamSynchronize(ctx->stream));
+      cudaFree(ctx->tring[slot]);
+      ctx->tring[slot] = nullptr;
+    }
+    ctx->tring_floats[slot] = 0;
+    ctx->tring_read[slot] = false;
+    ISG_CUDA(cudaMalloc(&ctx->tring[slot], sizeof(float) * floats));
+    if (!ctx->ev_tup[slot]) ISG_CUDA(cudaEventCreateWithFlags(&ctx->ev_tup[slot], cudaEventDisableTiming));
+    if (!ctx->ev_tread[slot]) ISG_CUDA(cudaEventCreateWithFlags(&ctx->ev_tread[slot], cudaEventDisableTiming));
+    ctx->tring_floats[slot] = floats;
+  }
+  // the slot's previous image may still be read by a frame enqueued earlier
+  if (ctx->tring_read[slot]) ISG_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_tread[slot], 0));
+  ISG_CUDA(cudaMemcpyAsync(ctx->tring[slot], host_hwc3, sizeof(float) * floats,
+                           cudaMemcpyHostToDevice, ctx->copy_stream));
+  ISG_CUDA(cudaEventRecord(ctx->ev_tup[slot], ctx->copy_stream));
+  return ISG_OK;
+}
+
+isg_status isg_loss_backward_slot(isg_ctx* ctx, const isg_camera* cam, const float bg[3],
+                                  float t_min, int32_t slot, float weight) {
+  if (!ctx) return ISG_E_ARG;
+  ISG_NO_CAPTURE("isg_loss_backward_slot");
+  if (slot < 0 || slot >= ISG_TARGET_SLOTS || !ctx->tring[slot])
+    return fail(ctx, ISG_E_ARG, "loss_backward_slot: slot has no uploaded target");
+  if (!(t_min >= 0.0f) || !(t_min < 1.0f)) return fail(ctx, ISG_E_ARG, "loss_backward: t_min must be in [0,1)");
+  if (!std::isfinite(weight)) return fail(ctx, ISG_E_ARG, "loss_backward: non-finite weight");
+  if (!cam || 3 * (size_t)cam->width * (size_t)cam->height > ctx->tring_floats[slot])
+    return fail(ctx, ISG_E_ARG, "loss_backward_slot: camera larger than the uploaded target");
+  cudaSetDevice(ctx->device);
+  isg_status s = validate_camera(ctx, cam);
+  if (s != ISG_OK) return s;
+  if ((s = check_loss_size(ctx, cam->width, cam->height)) != ISG_OK) return s;
+  const FrameParams fp = make_fp(cam, bg, t_min);
+  // binning and the forward do not need the target: only the backward waits for the upload
+  if ((s = launch_frame(ctx, fp, nullptr, true)) != ISG_OK) return s;
+  ISG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_tup[slot], 0));
+  if ((s = run_backward(ctx, fp, ctx->tring[slot], weight)) != ISG_OK) return s;
+  ISG_CUDA(cudaEventRecord(ctx->ev_tread[slot], ctx->stream));
+  ctx->tring_read[slot] = true;
+  return ISG_OK;
 }
 
 isg_status isg_loss_backward(isg_ctx* ctx, const isg_camera* cam, const float bg[3], float t_min,

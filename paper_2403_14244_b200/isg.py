@@ -86,6 +86,8 @@ def lib() -> C.CDLL:
         "isg_render_device": ([P, C.POINTER(CameraT), fp, F, P], C.c_int),
         "isg_loss_backward": ([P, C.POINTER(CameraT), fp, F, P, F, C.POINTER(C.c_double)], C.c_int),
         "isg_loss_backward_device": ([P, C.POINTER(CameraT), fp, F, P, F], C.c_int),
+        "isg_upload_target_async": ([P, C.c_int32, P, C.c_int32, C.c_int32], C.c_int),
+        "isg_loss_backward_slot": ([P, C.POINTER(CameraT), fp, F, C.c_int32, F], C.c_int),
         "isg_read_loss": ([P, C.POINTER(C.c_double)], C.c_int),
         "isg_zero_grads": ([P], C.c_int),
         "isg_get_grads": ([P, P], C.c_int),
@@ -135,7 +137,7 @@ C_ABI_SYMBOLS = (
     "isg_abi_version", "isg_status_string", "isg_last_error", "isg_create", "isg_destroy",
     "isg_set_stream", "isg_synchronize", "isg_get_stats", "isg_set_scene", "isg_set_scene_device",
     "isg_get_scene", "isg_render", "isg_render_device", "isg_loss_backward",
-    "isg_loss_backward_device", "isg_read_loss", "isg_zero_grads", "isg_get_grads",
+    "isg_loss_backward_device", "isg_upload_target_async", "isg_loss_backward_slot", "isg_read_loss", "isg_zero_grads", "isg_get_grads",
     "isg_grads_device", "isg_adam_step", "isg_last_step_loss", "isg_step_loss_async", "isg_eval_loss", "isg_snapshot",
     "isg_restore", "isg_set_loss", "isg_image_loss_device", "isg_adaptive_control",
     "isg_graph_begin", "isg_graph_end", "isg_graph_launch", "isg_graph_destroy", "isg_nccl_get_unique_id",
@@ -201,6 +203,9 @@ class Camera:
         c = CameraT()
         _check(None, lib().isg_synth_camera(width, height, view, n_views, C.byref(c)))
         return Camera.from_c(c)
+
+
+TARGET_SLOTS = 32  # ISG_TARGET_SLOTS (include/isg.h)
 
 
 @dataclass
@@ -415,6 +420,25 @@ class Renderer:
         _check(self._h, lib().isg_loss_backward_device(self._h, C.byref(c), self._bg(options),
                                                        float(options.t_min),
                                                        C.c_void_p(target_ptr), float(weight)))
+
+    def upload_target_async(self, slot: int, target: np.ndarray):
+        """isg_upload_target_async: enqueue the H2D copy of an H x W x 3 float32 target into ring
+        slot `slot` (< TARGET_SLOTS) on the context's copy stream.  The array must stay alive and
+        unchanged until the copy has run (page-locked memory makes it truly asynchronous)."""
+        t = np.ascontiguousarray(target, dtype=np.float32)
+        if t is not target:
+            raise ValueError("upload_target_async: target must be a C-contiguous float32 array "
+                             "(a temporary copy would be freed before the asynchronous upload)")
+        H, W = t.shape[:2]
+        _check(self._h, lib().isg_upload_target_async(self._h, int(slot), _ptr(t), W, H))
+
+    def loss_backward_slot(self, camera, slot: int, options: RenderOptions = RenderOptions(),
+                           weight: float = 1.0):
+        """isg_loss_backward_slot: loss_backward_device on target ring slot `slot`."""
+        c = self._cam(camera)
+        _check(self._h, lib().isg_loss_backward_slot(self._h, C.byref(c), self._bg(options),
+                                                     float(options.t_min), int(slot),
+                                                     float(weight)))
 
     def read_loss(self) -> float:
         v = C.c_double()
