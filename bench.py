@@ -702,6 +702,11 @@ def run_isg(args):
             for i in range(NB):  # allocate the slots outside the timed region
                 upload(i)
             r.synchronize()
+            ring_graphs = []  # step b of the ring, captured once per slot set (slot fixed)
+            for b in range(NB):
+                r.graph_begin()
+                ring_step(b)
+                ring_graphs.append(r.graph_end())
         e2e = None
         if train:
             r.restore()
@@ -715,7 +720,7 @@ def run_isg(args):
                 if use_pipe:
                     if i + NB - 1 < args.steps:  # step i+2's upload waits for step i-1's reads
                         upload(i + NB - 1)
-                    ring_step(i)
+                    ring_graphs[i % NB].launch()
                     ev_done[i % NB].record(stream)
                     if i >= 1:  # step i-1's loss is on the host once its work is done
                         pb = (i - 1) % NB
@@ -745,8 +750,8 @@ def run_isg(args):
                             "into the library's target ring (isg_upload_target_async on its copy "
                             "stream, isg_loss_backward_slot), every step's loss copied D2H into "
                             "pinned memory (isg_step_loss_async) and read by the host while the "
-                            "next step runs (all reads inside the timed region); kernel by kernel, "
-                            "no graph") if use_pipe
+                            "next step runs (all reads inside the timed region); one CUDA graph "
+                            "launch per step, captured once per ring slot set") if use_pipe
                    else "isg_loss_backward with host targets per view + adam_step + sync"}
 
     # ---- render FPS (C2): BASELINE's second metric on the same scene and camera ------------

@@ -125,7 +125,9 @@ isg_status isg_loss_backward_device(isg_ctx* ctx, const isg_camera* cam, const f
  * first waits for the last enqueued frame that read the slot).  isg_loss_backward_slot is
  * isg_loss_backward_device on that slot: binning and the forward blend run while the upload
  * may still be in flight, only the backward waits for it.  A caller uploads view i + 2 while
- * view i trains (the pattern bench.py's end-to-end number uses: 3 slots per view of a step). */
+ * view i trains (the pattern bench.py's end-to-end number uses: 3 slots per view of a step).
+ * isg_loss_backward_slot may be captured (isg_graph_begin/end): the slot is fixed in the graph,
+ * each replay waits for that slot's latest upload enqueued before the launch. */
 #define ISG_TARGET_SLOTS 32
 isg_status isg_upload_target_async(isg_ctx* ctx, int32_t slot, const float* host_hwc3,
                                    int32_t width, int32_t height);

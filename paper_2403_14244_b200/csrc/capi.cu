@@ -1016,7 +1016,6 @@ isg_status isg_upload_target_async(isg_ctx* ctx, int32_t slot, const float* host
 isg_status isg_loss_backward_slot(isg_ctx* ctx, const isg_camera* cam, const float bg[3],
                                   float t_min, int32_t slot, float weight) {
   if (!ctx) return ISG_E_ARG;
-  ISG_NO_CAPTURE("isg_loss_backward_slot");
   if (slot < 0 || slot >= ISG_TARGET_SLOTS || !ctx->tring[slot])
     return fail(ctx, ISG_E_ARG, "loss_backward_slot: slot has no uploaded target");
   if (!(t_min >= 0.0f) || !(t_min < 1.0f)) return fail(ctx, ISG_E_ARG, "loss_backward: t_min must be in [0,1)");
@@ -1030,9 +1029,15 @@ isg_status isg_loss_backward_slot(isg_ctx* ctx, const isg_camera* cam, const flo
   const FrameParams fp = make_fp(cam, bg, t_min);
   // binning and the forward do not need the target: only the backward waits for the upload
   if ((s = launch_frame(ctx, fp, nullptr, true)) != ISG_OK) return s;
-  ISG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_tup[slot], 0));
+  // Inside a graph capture the wait and the record become external event nodes: each replay
+  // waits for the slot's most recent upload enqueued before the launch, and marks the slot
+  // read for the next upload into it (so a step can be captured once per slot and replayed
+  // while the uploads run outside the graph).
+  ISG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_tup[slot],
+                               ctx->capturing ? cudaEventWaitExternal : 0));
   if ((s = run_backward(ctx, fp, ctx->tring[slot], weight)) != ISG_OK) return s;
-  ISG_CUDA(cudaEventRecord(ctx->ev_tread[slot], ctx->stream));
+  ISG_CUDA(cudaEventRecordWithFlags(ctx->ev_tread[slot], ctx->stream,
+                                    ctx->capturing ? cudaEventRecordExternal : 0));
   ctx->tring_read[slot] = true;
   return ISG_OK;
 }

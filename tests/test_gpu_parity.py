@@ -249,31 +249,45 @@ def test_target_ring_matches_device_targets():
     host = [p.numpy() for p in pinned]
     opts = isg.RenderOptions(t_min=1e-5)
     adam = isg.AdamConfig()
-    steps = 7
+    steps = 8  # graphs replayed twice; targets cycle with period 4, so slots get new data
     results = []
-    for use_ring in (False, True):
+    for mode in ("device", "ring", "ring_graph"):
         with isg.Renderer(0) as r:
             r.set_deterministic(True)
             r.set_scene(ms, co)
             dev = [torch.from_numpy(t).cuda() for t in targets]
             torch.cuda.synchronize()
             losses = []
-            if use_ring:
+            if mode != "device":
                 for s_ in range(min(2, steps)):  # three slots, reused: the WAR waits matter
                     r.upload_target_async(s_ % 3, host[s_ % 4])
+            graphs = {}
+            if mode == "ring_graph":
+                r.render(cams[0], opts)  # buffers sized before any capture (captures cannot grow them)
             for s_ in range(steps):
-                if use_ring:
+                if mode == "device":
+                    r.loss_backward_device(cams[s_ % 3], dev[s_ % 4].data_ptr(), opts)
+                    r.adam_step(adam)
+                else:
                     if s_ + 2 < steps:
                         r.upload_target_async((s_ + 2) % 3, host[(s_ + 2) % 4])
-                    r.loss_backward_slot(cams[s_ % 4], s_ % 3, opts)
-                else:
-                    r.loss_backward_device(cams[s_ % 4], dev[s_ % 4].data_ptr(), opts)
-                r.adam_step(adam)
+                    if mode == "ring":
+                        r.loss_backward_slot(cams[s_ % 3], s_ % 3, opts)
+                        r.adam_step(adam)
+                    else:  # one graph per slot (camera s % 3), replayed on new uploads
+                        key = s_ % 3
+                        if key not in graphs:
+                            r.graph_begin()
+                            r.loss_backward_slot(cams[s_ % 3], s_ % 3, opts)
+                            r.adam_step(adam)
+                            graphs[key] = r.graph_end()
+                        graphs[key].launch()
                 losses.append(r.last_step_loss())
             results.append((np.array(losses), r.get_scene()))
-    (l0, (a0, b0)), (l1, (a1, b1)) = results
-    assert np.array_equal(l0, l1)
-    assert np.array_equal(a0, a1) and np.array_equal(b0, b1)
+    (l0, (a0, b0)) = results[0]
+    for l1, (a1, b1) in results[1:]:
+        assert np.array_equal(l0, l1)
+        assert np.array_equal(a0, a1) and np.array_equal(b0, b1)
     with isg.Renderer(0) as r:
         r.set_scene(ms, co)
         with pytest.raises(ValueError):
