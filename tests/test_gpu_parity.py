@@ -408,6 +408,38 @@ def test_adam_fused_equals_unfused(rend):
     assert np.all(d[big] <= (1e-2 * step_tol + 1e-6)[np.nonzero(big)[1]])
 
 
+@pytest.mark.parametrize("n", [1, 127, 128, 129, 230_077])
+def test_adam_stream_sizes(n):
+    """K8's TMA stream (direct mode) updates every splat exactly once at sizes around its
+    128-splat chunks and with more chunks than resident CTAs: the fused step's first Adam move
+    (+-lr for any nonzero gradient) equals the un-fused one wherever the gradient is nonzero."""
+    W, H = 96, 64
+    ms, co = isg.synth_scene(n, W, H, seed=21)
+    tms, tco = isg.synth_scene(max(n, 64), W, H, seed=22)
+    cam = isg.Camera.synthetic(W, H)
+    target = O.render32(tms, tco, cam)
+    cfg = isg.AdamConfig(lr_mu=1e-3, lr_sigma=5e-3, lr_color=1e-2, lr_opacity=1e-2, eps=1e-15)
+    out = []
+    with isg.Renderer(0) as r:
+        for fused in (True, False):
+            r.set_scene(ms, co)
+            r.loss_backward(cam, target)
+            g = None if fused else r.grads()
+            r.adam_step(cfg)
+            out.append((r.get_scene(), g))
+    (ams, aco), _ = out[0]
+    (bms, bco), g = out[1]
+    lr = np.array([cfg.lr_mu] * 3 + [cfg.lr_sigma] + [cfg.lr_color] * 3 + [cfg.lr_opacity])
+    pa = np.concatenate([ams[:, :3], np.log(ams[:, 3:4]), aco[:, :3],
+                         np.log(aco[:, 3:4] / (1 - aco[:, 3:4]))], 1)
+    pb = np.concatenate([bms[:, :3], np.log(bms[:, 3:4]), bco[:, :3],
+                         np.log(bco[:, 3:4] / (1 - bco[:, 3:4]))], 1)
+    moved = np.abs(g) > 1e-6 * np.abs(g).max(axis=0, keepdims=True)
+    d = np.abs(pa - pb)
+    assert np.all(d[moved] <= (0.1 * lr + 1e-6)[np.nonzero(moved)[1]])
+    assert np.all(d[~moved] <= (2.001 * lr + 1e-6)[np.nonzero(~moved)[1]])
+
+
 def test_validation_errors(rend):
     cam = isg.Camera(np.eye(3), np.zeros(3), 32.0, (16, 16), 32, 32)
     good = np.array([[0, 0, 2, .25, 1, .2, .1, .5]] * 3, np.float64)
