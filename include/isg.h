@@ -109,6 +109,17 @@ isg_status isg_render(isg_ctx* ctx, const isg_camera* cam, const float bg[3], fl
 isg_status isg_render_device(isg_ctx* ctx, const isg_camera* cam, const float bg[3], float t_min,
                              float* out_hwc3_dev);
 
+/* Host-buffer rendering without a host sync per frame: render into the context's image ring
+ * slot `slot` (0..ISG_IMAGE_SLOTS-1, each allocated on first use) and enqueue the frame's
+ * device-to-host copy into `host_dst` (page-locked H x W x 3) on the context's copy stream;
+ * returns at once, so the next frames render while this one travels.  isg_image_wait blocks
+ * until slot `slot`'s last copy has landed (then `host_dst` may be read or reused).  Overflow
+ * of a frame's key capacity surfaces at the next synchronising call, as for the device form. */
+#define ISG_IMAGE_SLOTS 8
+isg_status isg_render_host_async(isg_ctx* ctx, const isg_camera* cam, const float bg[3],
+                                 float t_min, int32_t slot, float* host_dst);
+isg_status isg_image_wait(isg_ctx* ctx, int32_t slot);
+
 /* ---- training -------------------------------------------------------------------------- */
 /* Forward + L2 loss (weight * mse, image.cpp:50-58) + backward for one view.  Gradients
  * ACCUMULATE into the context's n x 8 buffer until isg_adam_step / isg_zero_grads.

@@ -48,6 +48,11 @@ struct isg_ctx {
   size_t tring_floats[ISG_TARGET_SLOTS] = {};
   cudaEvent_t ev_tup[ISG_TARGET_SLOTS] = {}, ev_tread[ISG_TARGET_SLOTS] = {};
   bool tring_read[ISG_TARGET_SLOTS] = {};
+  // image ring for host-buffer rendering (isg_render_host_async / isg_image_wait)
+  float* iring[ISG_IMAGE_SLOTS] = {};
+  size_t iring_floats[ISG_IMAGE_SLOTS] = {};
+  cudaEvent_t ev_irend[ISG_IMAGE_SLOTS] = {}, ev_icopy[ISG_IMAGE_SLOTS] = {};
+  bool iring_copied[ISG_IMAGE_SLOTS] = {};
   std::string err;
 
   // scene (SoA float4) and Adam moments (n x 2 float4 each)
@@ -817,6 +822,11 @@ void isg_destroy(isg_ctx* ctx) {
   }
   if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
   if (ctx->ev_copy) cudaEventDestroy(ctx->ev_copy);
+  for (int k = 0; k < ISG_IMAGE_SLOTS; ++k) {
+    if (ctx->ev_irend[k]) cudaEventDestroy(ctx->ev_irend[k]);
+    if (ctx->ev_icopy[k]) cudaEventDestroy(ctx->ev_icopy[k]);
+    if (ctx->iring[k]) cudaFree(ctx->iring[k]);
+  }
   for (int k = 0; k < ISG_TARGET_SLOTS; ++k) {
     if (ctx->ev_tup[k]) cudaEventDestroy(ctx->ev_tup[k]);
     if (ctx->ev_tread[k]) cudaEventDestroy(ctx->ev_tread[k]);
@@ -940,6 +950,53 @@ isg_status isg_render_device(isg_ctx* ctx, const isg_camera* cam, const float bg
   isg_status s = validate_camera(ctx, cam);
   if (s != ISG_OK) return s;
   return launch_frame(ctx, make_fp(cam, bg, t_min), out_dev, false);
+}
+
+isg_status isg_render_host_async(isg_ctx* ctx, const isg_camera* cam, const float bg[3],
+                                 float t_min, int32_t slot, float* host_dst) {
+  if (!ctx) return ISG_E_ARG;
+  ISG_NO_CAPTURE("isg_render_host_async");
+  if (slot < 0 || slot >= ISG_IMAGE_SLOTS) return fail(ctx, ISG_E_ARG, "render_host_async: bad slot");
+  if (!host_dst) return fail(ctx, ISG_E_ARG, "render: null output");
+  if (!(t_min >= 0.0f) || !(t_min < 1.0f)) return fail(ctx, ISG_E_ARG, "render: t_min must be in [0,1)");
+  cudaSetDevice(ctx->device);
+  isg_status s = validate_camera(ctx, cam);
+  if (s != ISG_OK) return s;
+  const size_t floats = 3 * (size_t)cam->width * (size_t)cam->height;
+  if (floats > ctx->iring_floats[slot]) {
+    if (ctx->iring[slot]) {  // nothing may still write or read the old image
+      ISG_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+      ISG_CUDA(cudaStreamSynchronize(ctx->stream));
+      cudaFree(ctx->iring[slot]);
+      ctx->iring[slot] = nullptr;
+    }
+    ctx->iring_floats[slot] = 0;
+    ctx->iring_copied[slot] = false;
+    ISG_CUDA(cudaMalloc(&ctx->iring[slot], sizeof(float) * floats));
+    if (!ctx->ev_irend[slot]) ISG_CUDA(cudaEventCreateWithFlags(&ctx->ev_irend[slot], cudaEventDisableTiming));
+    if (!ctx->ev_icopy[slot]) ISG_CUDA(cudaEventCreateWithFlags(&ctx->ev_icopy[slot], cudaEventDisableTiming));
+    ctx->iring_floats[slot] = floats;
+  }
+  // the slot's previous image may still be on its way to the host
+  if (ctx->iring_copied[slot]) ISG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_icopy[slot], 0));
+  if ((s = launch_frame(ctx, make_fp(cam, bg, t_min), ctx->iring[slot], false)) != ISG_OK) return s;
+  ISG_CUDA(cudaEventRecord(ctx->ev_irend[slot], ctx->stream));
+  ISG_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_irend[slot], 0));
+  ISG_CUDA(cudaMemcpyAsync(host_dst, ctx->iring[slot], sizeof(float) * floats,
+                           cudaMemcpyDeviceToHost, ctx->copy_stream));
+  ISG_CUDA(cudaEventRecord(ctx->ev_icopy[slot], ctx->copy_stream));
+  ctx->iring_copied[slot] = true;
+  return ISG_OK;
+}
+
+isg_status isg_image_wait(isg_ctx* ctx, int32_t slot) {
+  if (!ctx) return ISG_E_ARG;
+  ISG_NO_CAPTURE("isg_image_wait");
+  if (slot < 0 || slot >= ISG_IMAGE_SLOTS) return fail(ctx, ISG_E_ARG, "image_wait: bad slot");
+  if (!ctx->iring_copied[slot]) return ISG_OK;
+  cudaSetDevice(ctx->device);
+  ISG_CUDA(cudaEventSynchronize(ctx->ev_icopy[slot]));
+  return ISG_OK;
 }
 
 isg_status isg_render(isg_ctx* ctx, const isg_camera* cam, const float bg[3], float t_min,

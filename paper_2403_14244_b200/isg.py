@@ -87,6 +87,8 @@ def lib() -> C.CDLL:
         "isg_loss_backward": ([P, C.POINTER(CameraT), fp, F, P, F, C.POINTER(C.c_double)], C.c_int),
         "isg_loss_backward_device": ([P, C.POINTER(CameraT), fp, F, P, F], C.c_int),
         "isg_upload_target_async": ([P, C.c_int32, P, C.c_int32, C.c_int32], C.c_int),
+        "isg_render_host_async": ([P, C.POINTER(CameraT), fp, F, C.c_int32, P], C.c_int),
+        "isg_image_wait": ([P, C.c_int32], C.c_int),
         "isg_loss_backward_slot": ([P, C.POINTER(CameraT), fp, F, C.c_int32, F], C.c_int),
         "isg_read_loss": ([P, C.POINTER(C.c_double)], C.c_int),
         "isg_zero_grads": ([P], C.c_int),
@@ -137,6 +139,7 @@ C_ABI_SYMBOLS = (
     "isg_abi_version", "isg_status_string", "isg_last_error", "isg_create", "isg_destroy",
     "isg_set_stream", "isg_synchronize", "isg_get_stats", "isg_set_scene", "isg_set_scene_device",
     "isg_get_scene", "isg_render", "isg_render_device", "isg_loss_backward",
+    "isg_render_host_async", "isg_image_wait",
     "isg_loss_backward_device", "isg_upload_target_async", "isg_loss_backward_slot", "isg_read_loss", "isg_zero_grads", "isg_get_grads",
     "isg_grads_device", "isg_adam_step", "isg_last_step_loss", "isg_step_loss_async", "isg_eval_loss", "isg_snapshot",
     "isg_restore", "isg_set_loss", "isg_image_loss_device", "isg_adaptive_control",
@@ -206,6 +209,7 @@ class Camera:
 
 
 TARGET_SLOTS = 32  # ISG_TARGET_SLOTS (include/isg.h)
+IMAGE_SLOTS = 8  # ISG_IMAGE_SLOTS
 
 
 @dataclass
@@ -420,6 +424,20 @@ class Renderer:
         _check(self._h, lib().isg_loss_backward_device(self._h, C.byref(c), self._bg(options),
                                                        float(options.t_min),
                                                        C.c_void_p(target_ptr), float(weight)))
+
+    def render_host_async(self, camera, slot: int, out: np.ndarray,
+                          options: RenderOptions = RenderOptions()):
+        """isg_render_host_async: render into image ring slot `slot` and enqueue the copy into
+        `out` (a C-contiguous H x W x 3 float32 array that stays alive; page-locked memory makes
+        the copy truly asynchronous).  image_wait(slot) before reading `out`."""
+        if not (out.flags.c_contiguous and out.dtype == np.float32):
+            raise ValueError("render_host_async: out must be a C-contiguous float32 array")
+        c = self._cam(camera)
+        _check(self._h, lib().isg_render_host_async(self._h, C.byref(c), self._bg(options),
+                                                    float(options.t_min), int(slot), _ptr(out)))
+
+    def image_wait(self, slot: int):
+        _check(self._h, lib().isg_image_wait(self._h, int(slot)))
 
     def upload_target_async(self, slot: int, target: np.ndarray):
         """isg_upload_target_async: enqueue the H2D copy of an H x W x 3 float32 target into ring

@@ -296,6 +296,33 @@ def test_target_ring_matches_device_targets():
             r.upload_target_async(isg.TARGET_SLOTS, host[0])
 
 
+def test_image_ring_render_to_host(rend):
+    """isg_render_host_async + isg_image_wait (frames rendered into the image ring while earlier
+    frames travel to the host) return the same images as the synchronous render, slots reused."""
+    import torch
+    W, H, n = 80, 56, 2500
+    ms, co = isg.synth_scene(n, W, H, seed=31)
+    cams = [isg.Camera.synthetic(W, H, v, 5) for v in range(5)]
+    opts = isg.RenderOptions(t_min=0.0)
+    rend.set_scene(ms, co)
+    ref = [rend.render(c, opts) for c in cams]
+    pinned = [torch.empty((H, W, 3), dtype=torch.float32).pin_memory() for _ in range(3)]
+    outs = [p.numpy() for p in pinned]
+    got = []
+    for i in range(9):  # 3 slots, each reused three times
+        if i >= 3:
+            rend.image_wait(i % 3)
+            got.append(outs[i % 3].copy())
+        rend.render_host_async(cams[i % 5], i % 3, outs[i % 3], opts)
+    for i in range(6, 9):
+        rend.image_wait(i % 3)
+        got.append(outs[i % 3].copy())
+    for i, img in enumerate(got):
+        assert np.array_equal(img, ref[i % 5]), i
+    with pytest.raises(ValueError):
+        rend.render_host_async(cams[0], isg.IMAGE_SLOTS, outs[0], opts)
+
+
 def _golden(name):
     import sys
     from pathlib import Path
