@@ -148,6 +148,10 @@ isg_status isg_loss_backward_slot(isg_ctx* ctx, const isg_camera* cam, const flo
 isg_status isg_read_loss(isg_ctx* ctx, double* loss_out);
 isg_status isg_zero_grads(isg_ctx* ctx);
 isg_status isg_get_grads(isg_ctx* ctx, float* grads_nx8);
+/* Replace the accumulated gradients with a host n x 8 buffer (a pending view is projected
+ * first and then overwritten), e.g. after a reduction the caller ran itself; the next
+ * isg_adam_step applies them.  Synchronous. */
+isg_status isg_set_grads(isg_ctx* ctx, const float* grads_nx8);
 /* Device pointer of the n x 8 gradient buffer (flushes pending per-view work first), e.g.
  * for an external all-reduce.  Valid until the next isg_set_scene. */
 isg_status isg_grads_device(isg_ctx* ctx, float** grads_dev);

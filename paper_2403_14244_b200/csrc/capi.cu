@@ -1182,6 +1182,17 @@ isg_status isg_get_grads(isg_ctx* ctx, float* grads) {
   return ISG_OK;
 }
 
+isg_status isg_set_grads(isg_ctx* ctx, const float* grads) {
+  if (!ctx || !grads) return ISG_E_ARG;
+  ISG_NO_CAPTURE("isg_set_grads");
+  float* d = nullptr;
+  isg_status s = isg_grads_device(ctx, &d);  // projects a pending view first
+  if (s != ISG_OK) return s;
+  if (ctx->n > 0)
+    ISG_CUDA(cudaMemcpyAsync(d, grads, sizeof(float) * 8 * ctx->n, cudaMemcpyHostToDevice, ctx->stream));
+  ISG_CUDA(cudaStreamSynchronize(ctx->stream));
+  return ISG_OK;
+}
 
 isg_status isg_adam_step(isg_ctx* ctx, const float lr[4], float b1, float b2, float eps) {
   if (!ctx || !lr) return ISG_E_ARG;

@@ -93,6 +93,7 @@ def lib() -> C.CDLL:
         "isg_read_loss": ([P, C.POINTER(C.c_double)], C.c_int),
         "isg_zero_grads": ([P], C.c_int),
         "isg_get_grads": ([P, P], C.c_int),
+        "isg_set_grads": ([P, P], C.c_int),
         "isg_grads_device": ([P, C.POINTER(P)], C.c_int),
         "isg_adam_step": ([P, fp, F, F, F], C.c_int),
         "isg_last_step_loss": ([P, C.POINTER(C.c_double)], C.c_int),
@@ -140,7 +141,7 @@ C_ABI_SYMBOLS = (
     "isg_set_stream", "isg_synchronize", "isg_get_stats", "isg_set_scene", "isg_set_scene_device",
     "isg_get_scene", "isg_render", "isg_render_device", "isg_loss_backward",
     "isg_render_host_async", "isg_image_wait",
-    "isg_loss_backward_device", "isg_upload_target_async", "isg_loss_backward_slot", "isg_read_loss", "isg_zero_grads", "isg_get_grads",
+    "isg_loss_backward_device", "isg_upload_target_async", "isg_loss_backward_slot", "isg_read_loss", "isg_zero_grads", "isg_get_grads", "isg_set_grads",
     "isg_grads_device", "isg_adam_step", "isg_last_step_loss", "isg_step_loss_async", "isg_eval_loss", "isg_snapshot",
     "isg_restore", "isg_set_loss", "isg_image_loss_device", "isg_adaptive_control",
     "isg_graph_begin", "isg_graph_end", "isg_graph_launch", "isg_graph_destroy", "isg_nccl_get_unique_id",
@@ -470,6 +471,11 @@ class Renderer:
         g = np.empty((self.n, 8), np.float32)
         _check(self._h, lib().isg_get_grads(self._h, _ptr(g)))
         return g
+
+    def set_grads(self, grads: np.ndarray):
+        """isg_set_grads: replace the accumulated gradients (n x 8, host)."""
+        g = np.ascontiguousarray(grads, dtype=np.float32)
+        _check(self._h, lib().isg_set_grads(self._h, _ptr(g)))
 
     def grads_device_ptr(self) -> int:
         p = C.c_void_p()
