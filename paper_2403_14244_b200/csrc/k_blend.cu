@@ -65,11 +65,14 @@ __device__ __forceinline__ float2 bc(float v) { return make_float2(v, v); }
 // its walk); a render-only frame skips it.  kTl: also record the transmittance *before* the last
 // contributor (the backward's starting state for pixels whose final transmittance is not a
 // normal float, see k_blend_fwd).
-template <bool kTrack, bool kTl>
+// kTerm = false (an untracked frame at t_min = 0): the per-pixel termination test is dropped —
+// once T reaches 0 every later contribution T a c and T (1 - a) is an exact zero anyway, so the
+// image is bit-identical.
+template <bool kTrack, bool kTl, bool kTerm = true>
 __device__ __forceinline__ void fwd_pair(FwdPair& p, float2 r2, const float4 g, const float4 c,
                                          float t_min, uint32_t idx) {
-  const bool in0 = !(r2.x > g.z) && (p.T.x > t_min);
-  const bool in1 = !(r2.y > g.z) && (p.T.y > t_min);
+  const bool in0 = !(r2.x > g.z) && (!kTerm || p.T.x > t_min);
+  const bool in1 = !(r2.y > g.z) && (!kTerm || p.T.y > t_min);
   const float2 q = __fmul2_rn(r2, bc(g.w));
   // an excluded pixel's exponential is never evaluated (predicated MUFU into a zeroed pair), so
   // a = o * 0 = 0 exactly, the same value the select after the product gave
@@ -89,7 +92,7 @@ __device__ __forceinline__ void fwd_pair(FwdPair& p, float2 r2, const float4 g, 
 
 }  // namespace
 
-template <bool kTrack>
+template <bool kTrack, bool kTerm>
 __global__ void ISG_FWD_BOUNDS k_blend_fwd(
     FrameParams fp, const uint2* __restrict__ ranges, const uint2* __restrict__ sorted,
     uint16_t* __restrict__ submask,
@@ -235,7 +238,7 @@ __global__ void ISG_FWD_BOUNDS k_blend_fwd(
       for (int k = 0; k < 2; ++k) {
         const float dyk = k ? dy.y : dy.x;
         const float2 r2 = __fadd2_rn(ax, bc(__fmul_rn(dyk, dyk)));
-        fwd_pair<kTrack, kTl>(P[k], r2, g, c, t_min, idx);
+        fwd_pair<kTrack, kTl, kTerm>(P[k], r2, g, c, t_min, idx);
       }
     }
   }
@@ -337,7 +340,11 @@ void launch_blend_fwd(const FrameParams& fp, const uint2* ranges, const uint2* s
                       uint16_t* submask, const RenderRec* rec, unsigned long long* total,
                       int64_t key_cap, float* out, float* t_last, uint32_t* n_proc, bool track,
                       cudaStream_t st) {
-  launch_pdl(track ? k_blend_fwd<true> : k_blend_fwd<false>, dim3(fp.n_tiles), dim3(kBT), 0, st,
+  // a tracked frame needs the termination test (the last contributor it records); an untracked
+  // one only when t_min > 0
+  auto k = track ? k_blend_fwd<true, true>
+                 : (fp.t_min > 0.0f ? k_blend_fwd<false, true> : k_blend_fwd<false, false>);
+  launch_pdl(k, dim3(fp.n_tiles), dim3(kBT), 0, st,
              fp, ranges, sorted, submask, rec, total, key_cap, out, t_last, n_proc);
 }
 
