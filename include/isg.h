@@ -130,9 +130,9 @@ isg_status isg_loss_backward(isg_ctx* ctx, const isg_camera* cam, const float bg
 isg_status isg_loss_backward_device(isg_ctx* ctx, const isg_camera* cam, const float bg[3],
                                     float t_min, const float* target_hwc3_dev, float weight);
 /* Host-buffer training without a host sync per view: a ring of ISG_TARGET_SLOTS device
- * target images owned by the context (each allocated on its first upload).  isg_upload_target_async enqueues the host-to-device copy
- * of one view's HWC3 target into ring slot `slot` on the context's copy stream and returns at
- * once (`host_hwc3` should be page-locked and stay unchanged until the copy has run; the copy
+ * target images owned by the context (each allocated on its first upload).
+ * isg_upload_target_async enqueues the host-to-device copy of one view's HWC3 target into ring
+ * slot `slot` on the context's copy stream and returns at once (`host_hwc3` should be page-locked and stay unchanged until the copy has run; the copy
  * first waits for the last enqueued frame that read the slot).  isg_loss_backward_slot is
  * isg_loss_backward_device on that slot: binning and the forward blend run while the upload
  * may still be in flight, only the backward waits for it.  A caller uploads view i + 2 while
