@@ -1,3 +1,6 @@
+"""GPU vs FP32-oracle gradients on scenes whose final transmittance is 0 or underflows (an
+opacity-1 splat centred on a pixel; a stack of opaque splats at t_min = 0): the K6 re-walk /
+K7 select-based start.  Run on the GPU box: python tools/dbg_alpha.py"""
 import numpy as np, sys, os
 sys.path.insert(0,'tests'); sys.path.insert(0,'.')
 import oracle as O

@@ -1,3 +1,5 @@
+"""Render FPS of the C2 workload at t_min = 1e-5 and at t_min = 0 (one-frame graphs replayed).
+Run on the GPU box: python tools/render_tmin.py"""
 import sys
 sys.path.insert(0, '.')
 import torch
