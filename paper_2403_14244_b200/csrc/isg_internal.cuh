@@ -49,6 +49,11 @@ struct FrameParams {
   int tiles_x, tiles_y, n_tiles;
   float bg[3];
   float t_min;
+  // pure render (isg_render*): K1 writes log2(opacity) into the records' col.w and K6 forms
+  // alpha as ex2(r2 (-log2 e / s^2) + log2 o) (one fused op instead of two products); tracked
+  // frames (K7 needs alpha exactly as the forward formed it, and o) and the evaluation loss
+  // (equal to the training loss) keep the opacity itself
+  int rec_log2o = 0;
 };
 
 // Render record of one splat, indexed by splat (32 B, two float4):

@@ -109,6 +109,11 @@ __global__ void __launch_bounds__(256) k_preprocess(const float4* __restrict__ m
       asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv_s2) : "f"(__fmul_rn(p.s, p.s)));
       r.geo = make_float4(p.u, p.v, p.r2max, -1.4426950408889634f * inv_s2);
       r.col = c;
+      if (fp.rec_log2o) {  // render-only frame (FrameParams::rec_log2o); log2(0) = -inf -> alpha 0
+        float l2;
+        asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2) : "f"(c.w));
+        r.col.w = l2;
+      }
       rec[i] = r;
       key = count ? __float_as_uint(p.zc) : 0xFFFFFFFFu;
       depth_key[i] = key;
