@@ -153,6 +153,7 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
   __shared__ uint8_t s_list[kSubs][kListPitch];
   __shared__ float s_red[2];
   __shared__ int s_max[2];
+  __shared__ __align__(16) int s_sqmax[kSubs];  // per sub-quarter: max entries processed over its 16 pixels
   const int tile = blockIdx.x;
   pdl_enter();
   if (overflowed(total, key_cap)) {
@@ -217,10 +218,16 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
     s.GA = make_float2(G[0][0] * fp.bg[0] + G[0][1] * fp.bg[1] + G[0][2] * fp.bg[2],
                        G[1][0] * fp.bg[0] + G[1][1] * fp.bg[1] + G[1][2] * fp.bg[2]);
   }
+  // the sub-quarter's own last entry: entries at or past it are exact zeros for all of its
+  // pixels, so its lists stop there (dense scenes terminate sub-quarters at very different
+  // depths within one tile)
+  npmax = max(npmax, __shfl_xor_sync(0xffffffffu, npmax, 1));
+  npmax = max(npmax, __shfl_xor_sync(0xffffffffu, npmax, 2));
+  if (l4 == 0) s_sqmax[sub] = npmax;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     dsq += __shfl_xor_sync(0xffffffffu, dsq, o);
-    npmax = max(npmax, __shfl_xor_sync(0xffffffffu, npmax, o));
+    if (o >= 4) npmax = max(npmax, __shfl_xor_sync(0xffffffffu, npmax, o));
   }
   if (lane == 0) {
     s_red[w] = dsq;
@@ -256,6 +263,10 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
     // pairs' precomputed sub-quarter masks (sub_mask16, the binning's closest-point tests)
     int my_cnt = 0, steps = 0;
     int base[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    // (re-read per batch: two broadcast loads, no registers held across the walk)
+    const int4 sq0 = reinterpret_cast<const int4*>(s_sqmax)[2 * w];
+    const int4 sq1 = reinterpret_cast<const int4*>(s_sqmax)[2 * w + 1];
+    const int sqm[8] = {sq0.x, sq0.y, sq0.z, sq0.w, sq1.x, sq1.y, sq1.z, sq1.w};
     // words from the last to the first and, within a word, lanes from high to low: the lists
     // come out in reverse depth order
 #pragma unroll
@@ -265,7 +276,7 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
       const uint32_t mw = j < cnt ? ((uint32_t)cur.mask[j] >> (8 * w)) & 0xFFu : 0u;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {  // group k = sub-quarter 8 w + k
-        const bool hk = (mw >> k) & 1u;
+        const bool hk = ((mw >> k) & 1u) && lo + j < sqm[k];
         const uint32_t mk = __ballot_sync(0xffffffffu, hk);
         if (hk) s_list[8 * w + k][base[k] + __popc(mk & gt)] = (uint8_t)j;
         if (!kDirect && lane == 0) s_rel[8 * w + k][wd] = mk;
