@@ -455,12 +455,7 @@ isg_status flush_pending(isg_ctx* ctx) {
 // Launch one frame: K1, depth sort, scan/emit, tile sort, ranges, K6 into `out` (nullptr =
 // the context's own image buffer, resolved after it is sized for this camera).
 // track: the forward also records the per-pixel state the backward starts from.
-// fast: a pure render (isg_render*): K6 forms alpha with one fused op (FrameParams::rec_log2o);
-// tracked frames and the evaluation loss keep the training arithmetic exactly.
-isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp_in, float* out, bool track,
-                        bool fast = false) {
-  FrameParams fp = fp_in;
-  fp.rec_log2o = (fast && !track) ? 1 : 0;
+isg_status launch_frame(isg_ctx* ctx, const FrameParams& fp, float* out, bool track) {
   isg_status s = flush_pending(ctx);
   if (s != ISG_OK) return s;
   if ((s = ensure_pixels(ctx, fp.cam.width, fp.cam.height)) != ISG_OK) return s;
@@ -954,7 +949,7 @@ isg_status isg_render_device(isg_ctx* ctx, const isg_camera* cam, const float bg
   cudaSetDevice(ctx->device);
   isg_status s = validate_camera(ctx, cam);
   if (s != ISG_OK) return s;
-  return launch_frame(ctx, make_fp(cam, bg, t_min), out_dev, false, true);
+  return launch_frame(ctx, make_fp(cam, bg, t_min), out_dev, false);
 }
 
 isg_status isg_render_host_async(isg_ctx* ctx, const isg_camera* cam, const float bg[3],
@@ -984,8 +979,7 @@ isg_status isg_render_host_async(isg_ctx* ctx, const isg_camera* cam, const floa
   }
   // the slot's previous image may still be on its way to the host
   if (ctx->iring_copied[slot]) ISG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_icopy[slot], 0));
-  if ((s = launch_frame(ctx, make_fp(cam, bg, t_min), ctx->iring[slot], false, true)) != ISG_OK)
-    return s;
+  if ((s = launch_frame(ctx, make_fp(cam, bg, t_min), ctx->iring[slot], false)) != ISG_OK) return s;
   ISG_CUDA(cudaEventRecord(ctx->ev_irend[slot], ctx->stream));
   ISG_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_irend[slot], 0));
   ISG_CUDA(cudaMemcpyAsync(host_dst, ctx->iring[slot], sizeof(float) * floats,
@@ -1017,7 +1011,7 @@ isg_status isg_render(isg_ctx* ctx, const isg_camera* cam, const float bg[3], fl
   if ((s = check_async(ctx)) != ISG_OK) return s;
   const FrameParams fp = make_fp(cam, bg, t_min);
   for (int attempt = 0; attempt < 3; ++attempt) {
-    if ((s = launch_frame(ctx, fp, nullptr, false, true)) != ISG_OK) return s;
+    if ((s = launch_frame(ctx, fp, nullptr, false)) != ISG_OK) return s;
     // image read-back queued behind the frame; one synchronisation covers both
     ISG_CUDA(cudaMemcpyAsync(out_hwc3, ctx->img, sizeof(float) * 3 * (size_t)cam->width * cam->height,
                              cudaMemcpyDeviceToHost, ctx->stream));

@@ -26,6 +26,9 @@ namespace isg {
 constexpr int kTile = ISG_TILE;
 constexpr int kTilePixels = kTile * kTile;
 constexpr float kNearPlane = 1e-3f;  // splat3d.hpp:55
+// Opacity floor of the render record's log2(opacity) (k_preprocess.cu): alpha / o stays defined
+// in the backward, and an alpha of at most 2^-60 is an exact no-op on 1 - alpha
+constexpr float kOpacityFloor = 0x1p-60f;
 
 enum BinningMode { kBinTileBucket = 0, kBinRadix = 1 };
 
@@ -49,15 +52,10 @@ struct FrameParams {
   int tiles_x, tiles_y, n_tiles;
   float bg[3];
   float t_min;
-  // pure render (isg_render*): K1 writes log2(opacity) into the records' col.w and K6 forms
-  // alpha as ex2(r2 (-log2 e / s^2) + log2 o) (one fused op instead of two products); tracked
-  // frames (K7 needs alpha exactly as the forward formed it, and o) and the evaluation loss
-  // (equal to the training loss) keep the opacity itself
-  int rec_log2o = 0;
 };
 
 // Render record of one splat, indexed by splat (32 B, two float4):
-//   geo = (u, v, r2max = (9*sigma2d)*sigma2d, -log2(e)/sigma2d^2),  col = (r, g, b, opacity)
+//   geo = (u, v, r2max = (9*sigma2d)*sigma2d, -log2(e)/sigma2d^2),  col = (r, g, b, log2 opacity)
 struct __align__(16) RenderRec {
   float4 geo;
   float4 col;

@@ -89,13 +89,14 @@ __device__ __forceinline__ void load_2d(int64_t i, float* __restrict__ grad2d,
   }
 }
 
-// opacity >= 0 (direct mode): a holds the unscaled sums (sum go dx, sum go dy, sum go r2,
-// sum go); kernels.hpp:219-220: dg/du = g 2 dx / s^2, dg/ds = g 2 r^2 / s^3, times opacity,
-// so (du, dv) scale by 2 o / s^2 and dsigma2d by 2 o / s^3 (s = sigma2d of this projection).
+// a = (sum go dx, sum go dy, sum go r2, sum go) with go = dL/dalpha * alpha (K7), so alpha's
+// opacity factor is already in: sum go = o dL/do.  Direct mode (!scaled): kernels.hpp:219-220,
+// dg/du = g 2 dx / s^2, dg/ds = g 2 r^2 / s^3, so (du, dv) scale by 2 / s^2 and dsigma2d by
+// 2 / s^3 (s = sigma2d of this projection); slot mode: K7's flush scaled them.
 // The chain rule needs only the camera-space centre and 1 / z: no exact-rounding projection
 // here (nothing is binned from it), one fast reciprocal instead of K1's three IEEE divisions.
 __device__ __forceinline__ void grad3d_of(const float4 ms, const isg_camera& cam, float4 a,
-                                          float4 b, float out[8], float opacity = -1.0f) {
+                                          float4 b, float out[8], float opacity, bool scaled) {
   const float xc = cam.R[0] * ms.x + cam.R[1] * ms.y + cam.R[2] * ms.z + cam.t[0];
   const float yc = cam.R[3] * ms.x + cam.R[4] * ms.y + cam.R[5] * ms.z + cam.t[1];
   const float zc = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(cam.R[6], ms.x), __fmul_rn(cam.R[7], ms.y)),
@@ -108,10 +109,10 @@ __device__ __forceinline__ void grad3d_of(const float4 ms, const isg_camera& cam
   }
   const float iz = rcp_approx(zc);
   const float fz = cam.focal * iz;
-  if (opacity >= 0.0f) {
-    // s = sigma f / z; (du, dv) scale by 2 o / s^2, dsigma2d by 2 o / s^3
+  if (!scaled) {
+    // s = sigma f / z; (du, dv) scale by 2 / s^2, dsigma2d by 2 / s^3
     const float inv_s = rcp_approx(ms.w * fz);
-    const float k2 = 2.0f * opacity * inv_s * inv_s;
+    const float k2 = 2.0f * inv_s * inv_s;
     a.x *= k2;
     a.y *= k2;
     a.z *= k2 * inv_s;
@@ -125,7 +126,7 @@ __device__ __forceinline__ void grad3d_of(const float4 ms, const isg_camera& cam
   out[4] = b.x;
   out[5] = b.y;
   out[6] = b.z;
-  out[7] = a.w;
+  out[7] = a.w * rcp_approx(fmaxf(opacity, kOpacityFloor));  // K1's floored opacity
 }
 
 // Optimizer space (torch.optim.Adam on the parameters (mu, log sigma, rgb, logit opacity)):
@@ -242,11 +243,11 @@ __global__ void __launch_bounds__(256) k_project_backward(
   if (i >= n) return;
   const bool ov = *total > (unsigned long long)cap;  // frame was skipped: contributes nothing
   const float4 P0 = ms[i];
-  const float op = grad2d ? co[i].w : -1.0f;
+  const float op = co[i].w;
   float4 a, b;
   load_2d(i, grad2d, partial, slot_of, slot_off, ntiles, ov, a, b);
   float o[8];
-  grad3d_of(P0, fp.cam, a, b, o, op);
+  grad3d_of(P0, fp.cam, a, b, o, op, !grad2d);
   float4 g0 = make_float4(o[0], o[1], o[2], o[3]), g1 = make_float4(o[4], o[5], o[6], o[7]);
   if (!first) {
     const float4 h0 = grad3d[2 * i], h1 = grad3d[2 * i + 1];
@@ -284,7 +285,7 @@ __global__ void ISG_ADAM_BOUNDS k_project_adam(
   if (skip) return;
   const AdamParams ap = state->p;
   float o[8];
-  grad3d_of(in.P0, fp.cam, a, b, o, grad2d ? in.P1.w : -1.0f);
+  grad3d_of(in.P0, fp.cam, a, b, o, in.P1.w, !grad2d);
   adam_apply(in, ms, co, raw, m, v, i, o, ap, total + kTotalSkipped);
 }
 
@@ -405,7 +406,7 @@ __global__ void __launch_bounds__(kAS) k_adam_stream(
     if constexpr (kProject) {
       g[2 * i] = make_float4(0.f, 0.f, 0.f, 0.f);
       g[2 * i + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
-      grad3d_of(r.in.P0, fp.cam, r.a, r.b, o, r.in.P1.w);
+      grad3d_of(r.in.P0, fp.cam, r.a, r.b, o, r.in.P1.w, false);
     } else {
       o[0] = r.a.x; o[1] = r.a.y; o[2] = r.a.z; o[3] = r.a.w;
       o[4] = r.b.x; o[5] = r.b.y; o[6] = r.b.z; o[7] = r.b.w;
@@ -464,7 +465,7 @@ __global__ void __launch_bounds__(kAS) k_project_stream(
     g2[2 * i] = make_float4(0.f, 0.f, 0.f, 0.f);
     g2[2 * i + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
     float o[8];
-    grad3d_of(r.P0, fp.cam, r.a, r.b, o, r.op);
+    grad3d_of(r.P0, fp.cam, r.a, r.b, o, r.op, false);
     float4 q0 = make_float4(o[0], o[1], o[2], o[3]), q1 = make_float4(o[4], o[5], o[6], o[7]);
     if constexpr (!kFirst) {
       q0 = make_float4(q0.x + r.h0.x, q0.y + r.h0.y, q0.z + r.h0.z, q0.w + r.h0.w);

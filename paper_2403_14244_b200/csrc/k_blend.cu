@@ -70,21 +70,17 @@ __device__ __forceinline__ float2 bc(float v) { return make_float2(v, v); }
 // kTerm = false (an untracked frame at t_min = 0): the per-pixel termination test is dropped —
 // once T reaches 0 every later contribution T a c and T (1 - a) is an exact zero anyway, so the
 // image is bit-identical.
-template <bool kTrack, bool kTl, bool kTerm = true, bool kFast = false>
+template <bool kTrack, bool kTl, bool kTerm = true>
 __device__ __forceinline__ void fwd_pair(FwdPair& p, float2 r2, const float4 g, const float4 c,
                                          float t_min, uint32_t idx) {
   const bool in0 = !(r2.x > g.z) && (!kTerm || p.T.x > t_min);
   const bool in1 = !(r2.y > g.z) && (!kTerm || p.T.y > t_min);
   // an excluded pixel's exponential is never evaluated (predicated MUFU into a zeroed pair), so
   // its alpha is an exact 0
-  float2 a;
-  if constexpr (!kFast) {
-    const float2 q = __fmul2_rn(r2, bc(g.w));
-    a = __fmul2_rn(bc(c.w), make_float2(in0 ? fast_exp2(q.x) : 0.0f, in1 ? fast_exp2(q.y) : 0.0f));
-  } else {  // pure render: c.w holds log2(opacity), alpha = ex2(r2 g.w + log2 o)
-    const float2 q = __ffma2_rn(r2, bc(g.w), bc(c.w));
-    a = make_float2(in0 ? fast_exp2(q.x) : 0.0f, in1 ? fast_exp2(q.y) : 0.0f);
-  }
+  // c.w holds log2(opacity) (K1): alpha = o exp(-r2 / (2 s^2)) = ex2(r2 g.w + log2 o), one
+  // fused op (the backward forms it the same way)
+  const float2 q = __ffma2_rn(r2, bc(g.w), bc(c.w));
+  const float2 a = make_float2(in0 ? fast_exp2(q.x) : 0.0f, in1 ? fast_exp2(q.y) : 0.0f);
   const float2 wgt = __fmul2_rn(p.T, a);
   p.Cr = __ffma2_rn(wgt, bc(c.x), p.Cr);
   p.Cg = __ffma2_rn(wgt, bc(c.y), p.Cg);
@@ -94,18 +90,14 @@ __device__ __forceinline__ void fwd_pair(FwdPair& p, float2 r2, const float4 g, 
     p.np0 = in0 ? idx : p.np0;
     p.np1 = in1 ? idx : p.np1;
   }
-  if constexpr (!kFast) {
-    p.T = __fmul2_rn(p.T, __fadd2_rn(bc(1.0f), make_float2(-a.x, -a.y)));  // T (1 - a)
-  } else {
-    // pure render: T - T a (one op; its rounding differs from T (1 - a) only in the last bits,
-    // and no backward divides by 1 - a for this frame)
-    p.T = __fadd2_rn(p.T, make_float2(-wgt.x, -wgt.y));
-  }
+  // T (1 - a) as T - T a: one op on the product already formed (the backward recovers
+  // T_k = T_{k+1} / (1 - a_k) up to the same rounding either way)
+  p.T = __fadd2_rn(p.T, make_float2(-wgt.x, -wgt.y));
 }
 
 }  // namespace
 
-template <bool kTrack, bool kTerm, bool kFast>
+template <bool kTrack, bool kTerm>
 __global__ void ISG_FWD_BOUNDS k_blend_fwd(
     FrameParams fp, const uint2* __restrict__ ranges, const uint2* __restrict__ sorted,
     uint16_t* __restrict__ submask,
@@ -251,7 +243,7 @@ __global__ void ISG_FWD_BOUNDS k_blend_fwd(
       for (int k = 0; k < 2; ++k) {
         const float dyk = k ? dy.y : dy.x;
         const float2 r2 = __fadd2_rn(ax, bc(__fmul_rn(dyk, dyk)));
-        fwd_pair<kTrack, kTl, kTerm, kFast>(P[k], r2, g, c, t_min, idx);
+        fwd_pair<kTrack, kTl, kTerm>(P[k], r2, g, c, t_min, idx);
       }
     }
   }
@@ -318,8 +310,7 @@ __global__ void __launch_bounds__(kTilePixels) k_count_pairs(
       const float r2 = dist2_rn(__fsub_rn(px, r.geo.x), __fsub_rn(py, r.geo.y));
       if (r2 > r.geo.z) continue;
       ++in;
-      const float a = fp.rec_log2o ? fast_exp2(__fmaf_rn(r2, r.geo.w, r.col.w))
-                                   : r.col.w * fast_exp2(r2 * r.geo.w);
+      const float a = fast_exp2(__fmaf_rn(r2, r.geo.w, r.col.w));  // K6's alpha
       T = T * (1.0f - a);
       if (!(T > fp.t_min)) break;
     }
@@ -356,11 +347,8 @@ void launch_blend_fwd(const FrameParams& fp, const uint2* ranges, const uint2* s
                       cudaStream_t st) {
   // a tracked frame needs the termination test (the last contributor it records); an untracked
   // one only when t_min > 0
-  auto k = track ? k_blend_fwd<true, true, false>
-         : fp.rec_log2o ? (fp.t_min > 0.0f ? k_blend_fwd<false, true, true>
-                                           : k_blend_fwd<false, false, true>)
-                        : (fp.t_min > 0.0f ? k_blend_fwd<false, true, false>
-                                           : k_blend_fwd<false, false, false>);
+  auto k = track ? k_blend_fwd<true, true>
+                 : (fp.t_min > 0.0f ? k_blend_fwd<false, true> : k_blend_fwd<false, false>);
   launch_pdl(k, dim3(fp.n_tiles), dim3(kBT), 0, st,
              fp, ranges, sorted, submask, rec, total, key_cap, out, t_last, n_proc);
 }

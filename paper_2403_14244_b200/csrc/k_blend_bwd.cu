@@ -61,8 +61,9 @@ struct BwdPair {
 
 __device__ __forceinline__ float2 bc(float v) { return make_float2(v, v); }
 
-// acc: [0] sum go*dx, [1] sum go*dy, [2] sum go*r2 (scaled per entry into du, dv, dsigma2d),
-// [3] dopacity, [4..6] drgb;  go = dL/dalpha * g; summed per lane of the pair.
+// acc: [0] sum go*dx, [1] sum go*dy, [2] sum go*r2 (scaled per splat into du, dv, dsigma2d),
+// [3] sum go (= o dL/dopacity), [4..6] drgb;  go = dL/dalpha * alpha; summed per lane of the
+// pair.  alpha = ex2(r2 g.w + log2 o) exactly as the forward formed it (c.w = log2 o, K1).
 //   dL/da_k = T_k G.(c_k - A_k);  A <- a c + (1 - a) A  =>  G.A <- G.A + a (G.c - G.A)
 // so the colour behind is carried as the single scalar G.A per pixel.  An inactive pixel gets
 // e = 0, hence a = 0: T and G.A stay exactly unchanged and every contribution is an exact zero.
@@ -73,9 +74,8 @@ template <bool kFast>
 __device__ __forceinline__ void bwd_pair(BwdPair& p, bool act0, bool act1, int j, float2 dx,
                                          float dy, float2 r2, const float4 g, const float4 c,
                                          float2 acc[8], float2& go) {
-  const float2 q = __fmul2_rn(r2, bc(g.w));
-  const float2 e = make_float2(act0 ? fast_exp2(q.x) : 0.0f, act1 ? fast_exp2(q.y) : 0.0f);
-  const float2 a = __fmul2_rn(bc(c.w), e);
+  const float2 q = __ffma2_rn(r2, bc(g.w), bc(c.w));
+  const float2 a = make_float2(act0 ? fast_exp2(q.x) : 0.0f, act1 ? fast_exp2(q.y) : 0.0f);
   const float2 om = __fadd2_rn(bc(1.0f), make_float2(-a.x, -a.y));  // 1 - a (FADD2 imm)
   const float2 Tr = __fmul2_rn(p.T, make_float2(fast_rcp(om.x), fast_rcp(om.y)));
   float2 Tk = Tr;
@@ -90,7 +90,7 @@ __device__ __forceinline__ void bwd_pair(BwdPair& p, bool act0, bool act1, int j
   acc[4] = __ffma2_rn(p.G0, Ta, acc[4]);
   acc[5] = __ffma2_rn(p.G1, Ta, acc[5]);
   acc[6] = __ffma2_rn(p.G2, Ta, acc[6]);
-  go = __fmul2_rn(dLda, e);  // the caller sums the two rows' go into acc[3]
+  go = __fmul2_rn(dLda, a);  // the caller sums the two rows' go into acc[3]
   acc[0] = __ffma2_rn(go, dx, acc[0]);
   acc[1] = __ffma2_rn(go, bc(dy), acc[1]);
   acc[2] = __ffma2_rn(go, r2, acc[2]);
@@ -363,10 +363,10 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
       }
       const size_t e = cur.slot[jj];
       if (w == 0) {
-        // kernels.hpp:219-220: dg/du = g 2 dx / s^2, dg/ds = g 2 r^2 / s^3, times opacity:
-        // (du, dv) scale by 2 o / s^2, dsigma2d by 2 o / s^3
+        // kernels.hpp:219-220: dg/du = g 2 dx / s^2, dg/ds = g 2 r^2 / s^3 (go already carries
+        // the opacity): (du, dv) scale by 2 / s^2, dsigma2d by 2 / s^3
         const float inv_s2 = cur.geo[jj].w * -kLn2;  // 1 / sigma2d^2
-        const float k2 = 2.0f * cur.col[jj].w * inv_s2;
+        const float k2 = 2.0f * inv_s2;
         partial[2 * e] = make_float4(v[0] * k2, v[1] * k2, v[2] * (k2 * fast_sqrt(inv_s2)), v[3]);
       } else {
         partial[2 * e + 1] = make_float4(v[0], v[1], v[2], 0.0f);

@@ -117,17 +117,17 @@ __global__ void __launch_bounds__(256) k_preprocess(const float4* __restrict__ m
         }
       }
       tilebox[i] = box;
-      RenderRec r;  // (u, v, r2max, -log2(e)/sigma2d^2), (r, g, b, opacity)
+      RenderRec r;  // (u, v, r2max, -log2(e)/sigma2d^2), (r, g, b, log2 opacity)
       // -log2(e) / sigma2d^2 feeds only ex2.approx (no inclusion decision): a MUFU reciprocal
       float inv_s2;
       asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv_s2) : "f"(__fmul_rn(p.s, p.s)));
       r.geo = make_float4(p.u, p.v, p.r2max, -1.4426950408889634f * inv_s2);
       r.col = c;
-      if (fp.rec_log2o) {  // render-only frame (FrameParams::rec_log2o); log2(0) = -inf -> alpha 0
-        float l2;
-        asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2) : "f"(c.w));
-        r.col.w = l2;
-      }
+      // log2(opacity): the blend kernels form alpha as one ex2(r2 g + log2 o).  Opacity is
+      // floored at kOpacityFloor (2^-60) so that alpha / o stays defined for the backward: an
+      // opacity-0 splat keeps its opacity gradient, and its alpha (<= 2^-60) leaves every
+      // 1 - alpha at exactly 1
+      asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r.col.w) : "f"(fmaxf(c.w, kOpacityFloor)));
       rec[i] = r;
       key = count ? __float_as_uint(p.zc) : 0xFFFFFFFFu;
       depth_key[i] = key;
