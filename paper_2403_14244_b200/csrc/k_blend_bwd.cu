@@ -61,9 +61,9 @@ struct BwdPair {
 
 __device__ __forceinline__ float2 bc(float v) { return make_float2(v, v); }
 
-// acc: [0] sum go*dx, [1] sum go*dy, [2] sum go*r2 (scaled per splat into du, dv, dsigma2d),
-// [3] sum go (= o dL/dopacity), [4..6] drgb;  go = dL/dalpha * alpha; summed per lane of the
-// pair.  alpha = ex2(r2 g.w + log2 o) exactly as the forward formed it (c.w = log2 o, K1).
+// acc: [2] sum go*r2, [4..6] drgb, summed per lane of the pair; go = dL/dalpha * alpha is
+// returned per pixel (the caller forms [0] sum go*dx, [1] sum go*dy and [3] sum go = o dL/do
+// from the quad's row and column sums).  alpha = ex2(r2 g.w + log2 o) exactly as the forward formed it (c.w = log2 o, K1).
 //   dL/da_k = T_k G.(c_k - A_k);  A <- a c + (1 - a) A  =>  G.A <- G.A + a (G.c - G.A)
 // so the colour behind is carried as the single scalar G.A per pixel.  An inactive pixel gets
 // e = 0, hence a = 0: T and G.A stay exactly unchanged and every contribution is an exact zero.
@@ -71,9 +71,9 @@ __device__ __forceinline__ float2 bc(float v) { return make_float2(v, v); }
 // up, T_k = T_{k+1} / (1 - a_k).  Otherwise (a tile the forward re-walked, k_blend.cu) p.T
 // starts as the transmittance before the last contributor, which therefore does not divide.
 template <bool kFast>
-__device__ __forceinline__ void bwd_pair(BwdPair& p, bool act0, bool act1, int j, float2 dx,
-                                         float dy, float2 r2, const float4 g, const float4 c,
-                                         float2 acc[8], float2& go) {
+__device__ __forceinline__ void bwd_pair(BwdPair& p, bool act0, bool act1, int j, float2 r2,
+                                         const float4 g, const float4 c, float2 acc[8],
+                                         float2& go) {
   const float2 q = __ffma2_rn(r2, bc(g.w), bc(c.w));
   const float2 a = make_float2(act0 ? fast_exp2(q.x) : 0.0f, act1 ? fast_exp2(q.y) : 0.0f);
   const float2 om = __fadd2_rn(bc(1.0f), make_float2(-a.x, -a.y));  // 1 - a (FADD2 imm)
@@ -91,8 +91,6 @@ __device__ __forceinline__ void bwd_pair(BwdPair& p, bool act0, bool act1, int j
   acc[5] = __ffma2_rn(p.G1, Ta, acc[5]);
   acc[6] = __ffma2_rn(p.G2, Ta, acc[6]);
   go = __fmul2_rn(dLda, a);  // the caller sums the two rows' go into acc[3]
-  acc[0] = __ffma2_rn(go, dx, acc[0]);
-  acc[1] = __ffma2_rn(go, bc(dy), acc[1]);
   acc[2] = __ffma2_rn(go, r2, acc[2]);
 }
 
@@ -318,12 +316,18 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
         const float2 r2 = __fadd2_rn(ax, bc(ay));
         const bool act0 = j < P[k].np0 && !(r2.x > g.z);
         const bool act1 = j < P[k].np1 && !(r2.y > g.z);
-        bwd_pair<kFast>(P[k], act0, act1, j, dx, dyk, r2, g, c, acc2, go[k]);
+        bwd_pair<kFast>(P[k], act0, act1, j, r2, g, c, acc2, go[k]);
       }
       acc2[3] = __fadd2_rn(go[0], go[1]);
+      // sum go dx and sum go dy over the 2x2 quad from its row and column sums: the right
+      // column's dx and the bottom row's dy are the top-left pixel's + 1, so
+      //   sum go dx = dx00 sum go + sum_right go,  sum go dy = dy00 sum go + sum_bottom go
+      const float s_go = acc2[3].x + acc2[3].y;
       float acc[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) acc[k] = acc2[k].x + acc2[k].y;
+      for (int k = 2; k < 8; ++k) acc[k] = k == 3 ? s_go : acc2[k].x + acc2[k].y;
+      acc[0] = __fmaf_rn(dx.x, s_go, go[0].y + go[1].y);
+      acc[1] = __fmaf_rn(dy.x, s_go, go[1].x + go[1].y);
       float y[2];
       reduce_scatter8_quad(acc, y);
       // the lane holds values vb, vb + 1 (vb = 4 (l4 >> 1) + 2 (l4 & 1)); the per-splat

@@ -233,6 +233,43 @@ def test_backward_through_zero_final_transmittance(rend, case):
         _grad_check(g, g_ref)
 
 
+@pytest.mark.parametrize("deterministic", [False, True], ids=["direct", "slot"])
+def test_opacity_zero_keeps_its_gradient(rend, deterministic):
+    """The blend kernels form alpha as ex2(r2 g + log2 o) and the backward accumulates
+    dL/dalpha * alpha, dividing by the opacity per splat; the opacity is floored at 2^-60 for
+    that, so a splat of opacity exactly 0 (valid input, IsoSplat3D::validate) still renders as
+    alpha ~ 0 and still gets its opacity gradient sum(dL/dalpha * exp(...)) -- as does
+    opacity 1."""
+    rng = np.random.default_rng(21)
+    W, H = 64, 48
+    ms, co, cam = random_scene(rng, 500, W, H)
+    co[::5, 3] = 0.0
+    co[1::7, 3] = 1.0
+    tms, tco, _ = random_scene(rng, 500, W, H)
+    target = O.render32(tms, tco, cam)
+    rend.set_deterministic(deterministic)
+    try:
+        rend.set_scene(ms, co)
+        rend.zero_grads()
+        img = rend.render(cam)
+        assert np.abs(img - O.render32(ms, co, cam)).max() <= IMG_TOL
+        loss = rend.loss_backward(cam, target, isg.RenderOptions(t_min=1e-5), weight=1.0)
+        g = rend.grads()
+    finally:
+        rend.set_deterministic(False)
+    loss_ref, g_ref = O.loss_backward32(ms, co, cam, target, t_min=1e-5)
+    assert abs(loss - loss_ref) <= 1e-6 * abs(loss_ref)
+    zero = co[:, 3] == 0.0
+    assert np.abs(g_ref[zero, 7]).max() > 0  # the case is exercised
+    _grad_check(g, g_ref)
+    # the zero-opacity splats: their opacity gradient matches the oracle; the others are the
+    # floor's 2^-60-scaled copies of an ordinary gradient where the oracle has exact zeros
+    og, oref = g[zero, 7], g_ref[zero, 7]
+    assert np.linalg.norm(og - oref) / np.linalg.norm(oref) <= GRAD_TOL
+    assert np.abs(og - oref).max() <= GRAD_TOL * np.abs(oref).max()
+    assert np.abs(g[zero, :7]).max() <= 1e-15 * np.abs(g_ref[:, :7]).max()
+
+
 def test_target_ring_matches_device_targets():
     """Host-buffer training through the C-ABI target ring (isg_upload_target_async +
     isg_loss_backward_slot, uploads two views ahead, no host sync per step) gives the same
