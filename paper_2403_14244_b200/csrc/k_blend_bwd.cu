@@ -63,7 +63,8 @@ __device__ __forceinline__ float2 bc(float v) { return make_float2(v, v); }
 
 // acc: [2] sum go*r2, [4..6] drgb, summed per lane of the pair; go = dL/dalpha * alpha is
 // returned per pixel (the caller forms [0] sum go*dx, [1] sum go*dy and [3] sum go = o dL/do
-// from the quad's row and column sums).  alpha = ex2(r2 g.w + log2 o) exactly as the forward formed it (c.w = log2 o, K1).
+// from the quad's row and column sums).  alpha = ex2(r2 g.w + log2 o) exactly as the forward
+// formed it (c.w = log2 o, K1).
 //   dL/da_k = T_k G.(c_k - A_k);  A <- a c + (1 - a) A  =>  G.A <- G.A + a (G.c - G.A)
 // so the colour behind is carried as the single scalar G.A per pixel.  An inactive pixel gets
 // e = 0, hence a = 0: T and G.A stay exactly unchanged and every contribution is an exact zero.
