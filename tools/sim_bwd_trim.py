@@ -101,3 +101,27 @@ np.add.at(G, tb, C)
 Cg = np.take_along_axis(C, np.argsort(-G, axis=1, kind="stable")[tb], axis=1)
 lock_g = Cg[:, :8].max(1).sum() + Cg[:, 8:].max(1).sum()
 print(f"sorted by relevant entries: lockstep {lock_g:,} warp steps ({lock_g / lock:.3f})")
+
+# one batch of lookahead: a group whose list of the current batch is done walks on into its
+# list of the next staged batch while the warp's longest list finishes
+nb = np.zeros(len(uk), np.int64)
+tile_of = uk // 100000
+b_of = uk % 100000
+tot_la = 0
+tot_lock = 0
+order_rows = np.lexsort((b_of, tile_of))
+rows_t = tile_of[order_rows]
+bounds = np.flatnonzero(np.diff(rows_t)) + 1
+for seg in np.split(order_rows, bounds):
+    Cseg = C[seg]  # batches of one tile, in walk order (batch 0 = the top of the list)
+    for w in range(2):
+        L = Cseg[:, 8 * w:8 * w + 8].astype(np.int64)
+        rem = L[0].copy()
+        for b in range(len(L)):
+            steps = rem.max()
+            tot_lock += L[b].max()
+            tot_la += steps
+            if b + 1 < len(L):
+                adv = np.minimum(steps - rem, L[b + 1])
+                rem = L[b + 1] - adv
+print(f"one-batch lookahead: {tot_la:,} warp steps ({tot_la / tot_lock:.3f} of lockstep {tot_lock:,})")
