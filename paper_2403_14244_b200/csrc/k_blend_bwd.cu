@@ -34,7 +34,7 @@ using namespace blend;
 
 constexpr int kBT = 64;      // threads per tile CTA: 2 warps x 8 four-lane groups
 #ifndef ISG_BWD_BATCH
-#define ISG_BWD_BATCH 128
+#define ISG_BWD_BATCH 160
 #endif
 // 4 walk steps per loop iteration (0.578 vs 0.595 ms unrolled by 1 at C3, direct mode)
 #ifndef ISG_BWD_UNROLL
@@ -43,7 +43,9 @@ constexpr int kBT = 64;      // threads per tile CTA: 2 warps x 8 four-lane grou
 constexpr int kUnroll = ISG_BWD_UNROLL;  // walk steps per loop iteration
 // Records staged per batch.  The 8 groups of a warp walk a batch in lockstep, so a warp's step
 // count per batch is the longest of its 8 relevance lists: larger batches pad less (C3 walk
-// steps, tools/sim_bwd_lists.py: 3.36M at 32, 3.20M at 64, 3.09M at 128).  Slot mode keeps 32
+// steps, tools/sim_bwd_lists.py / sim_bwd_trim.py: 3.36M at 32, 3.20M at 64, 3.08M at 128,
+// 3.03M at 192), until the staging's shared memory costs resident CTAs: 0.485 ms at 128,
+// 0.475 at 160, 0.488 at 192 (11 CTAs / SM), 0.491 at 224 (96 registers).  Slot mode keeps 32
 // (its flush maps entry = lane).
 constexpr int kBatchDirect = ISG_BWD_BATCH;
 constexpr int kBatchSlot = 32;

@@ -19,7 +19,8 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
 view = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 nv = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 t_min = float(sys.argv[4]) if len(sys.argv) > 4 else 1e-5
-W, H, B = 1920, 1080, 128
+W, H = 1920, 1080
+B = int(__import__("os").environ.get("SIM_BATCH", 128))
 ms, co = isg.synth_scene(n, W, H, seed=2403)
 cam = isg.Camera.synthetic(W, H, view, nv)
 keys, vals, ranges, nvis = O.bin32(ms, co, cam)
