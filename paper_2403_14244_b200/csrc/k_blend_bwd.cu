@@ -149,8 +149,9 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
   __shared__ Stage<kB + 1> st[2];
   // [sub-quarter][value][entry]; rows padded so one entry's 8 values hit 8 different banks
   // (slot mode only: the direct mode reduces into grad2d in L2 instead)
-  __shared__ float s_part[kDirect ? 1 : kSubs][8][kB + 1];
-  __shared__ uint32_t s_rel[kSubs][kW];  // relevance ballots of the batch per sub-quarter
+  // (direct mode: one-element placeholders, no shared memory spent)
+  __shared__ float s_part[kDirect ? 1 : kSubs][kDirect ? 1 : 8][kDirect ? 1 : kB + 1];
+  __shared__ uint32_t s_rel[kDirect ? 1 : kSubs][kDirect ? 1 : kW];  // relevance ballots
   __shared__ uint8_t s_list[kSubs][kListPitch];
   __shared__ float s_red[2];
   __shared__ int s_max[2];
