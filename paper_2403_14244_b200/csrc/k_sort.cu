@@ -109,7 +109,11 @@ struct OnesweepSmem {
 };
 
 template <bool kEpi>
-__global__ void __launch_bounds__(kSortThreads) k_onesweep(
+// (a 5- or 6-CTA minimum per SM for more resident tiles: equal / slower at C3, 72-88 B spills)
+#ifndef ISG_SORT_MINB
+#define ISG_SORT_MINB 1
+#endif
+__global__ void __launch_bounds__(kSortThreads, ISG_SORT_MINB) k_onesweep(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
     uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
     const uint32_t* __restrict__ n_dev, int64_t cap, int shift,
