@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """Minimal driver for ncu captures: C3 (1M splats, 1080p) train steps through the C-ABI with
 device-resident inputs, no timing and no CPU work, so `ncu -k regex:...` sees only our
-kernels.  Usage: python tools/profile_step.py [--steps 3] [--config c3|c2|c5] [--render]
+kernels.  Usage: python tools/profile_step.py [--steps 3] [--config c3|c2|c4|c5] [--render]
 [--loss l2|l1_dssim]"""
 import argparse
 import sys
@@ -15,7 +15,8 @@ import torch  # noqa: E402
 from paper_2403_14244_b200 import isg  # noqa: E402
 
 SIZES = {"c2": (1_000_000, 1920, 1080), "c3": (1_000_000, 1920, 1080),
-         "c5": (10_000_000, 3840, 2160), "small": (10_000, 256, 256)}
+         "c4": (3_000_000, 1920, 1080), "c5": (10_000_000, 3840, 2160),
+         "small": (10_000, 256, 256)}
 
 
 def main():
@@ -32,7 +33,8 @@ def main():
     n, W, H = SIZES[a.config]
     ms, co = isg.synth_scene(n, W, H, seed=2403)
     tms, tco = isg.synth_scene(n, W, H, seed=14244)
-    cam = isg.Camera.synthetic(W, H)
+    # c4: the first view of the 8-view batch (one view pass; the batch repeats it 8 times)
+    cam = isg.Camera.synthetic(W, H, 0, 8) if a.config == "c4" else isg.Camera.synthetic(W, H)
     opts = isg.RenderOptions(t_min=1e-5)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
