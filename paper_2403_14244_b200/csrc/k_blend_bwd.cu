@@ -293,8 +293,11 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
     for (int e = my_cnt + l4; e < steps; e += 4) s_list[sub][e] = (uint8_t)kB;
     __syncwarp();
     const uint8_t* my_list = s_list[sub];
-    auto walk = [&](auto fast_tag) {
+    // kNp: some pixel of the warp has its last entry inside this batch, so each pixel tests
+    // j < n_proc; below every pixel's last entry (most batches) the test is dropped
+    auto walk = [&](auto fast_tag, auto np_tag) {
     constexpr bool kFast = decltype(fast_tag)::value;
+    constexpr bool kNp = decltype(np_tag)::value;
 #pragma unroll kUnroll
     for (int s = 0; s < steps; ++s) {
       // reverse depth order; the sentinel has a = 0 for every pixel, so T (T / 1) and G.A stay
@@ -318,8 +321,8 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
         const float dyk = k ? dy.y : dy.x;
         const float ay = __fmul_rn(dyk, dyk);
         const float2 r2 = __fadd2_rn(ax, bc(ay));
-        const bool act0 = j < P[k].np0 && !(r2.x > g.z);
-        const bool act1 = j < P[k].np1 && !(r2.y > g.z);
+        const bool act0 = (!kNp || j < P[k].np0) && !(r2.x > g.z);
+        const bool act1 = (!kNp || j < P[k].np1) && !(r2.y > g.z);
         bwd_pair<kFast>(P[k], act0, act1, j, r2, g, c, acc2, go[k]);
       }
       acc2[3] = __fadd2_rn(go[0], go[1]);
@@ -348,10 +351,14 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
       }
     }
     };
+    const bool np_in = !__all_sync(0xffffffffu, P[0].np0 >= hi && P[0].np1 >= hi &&
+                                                  P[1].np0 >= hi && P[1].np1 >= hi);
     if (slow)
-      walk(std::false_type{});
+      walk(std::false_type{}, std::true_type{});
+    else if (np_in)
+      walk(std::true_type{}, std::true_type{});
     else
-      walk(std::true_type{});
+      walk(std::true_type{}, std::false_type{});
     if constexpr (kDirect) {
       hi = lo;  // the next batch's barrier orders the staging buffers
       continue;
