@@ -54,14 +54,35 @@ __device__ __forceinline__ void st_volatile(uint32_t* p, uint32_t v) {
 
 // Lanes of the warp holding the same 9-bit value (digit, or 256 = no item): 9 ballots instead of
 // one match.any (a slow MIO-pipe instruction on this part).
+#ifndef ISG_MATCH_PTX
+#define ISG_MATCH_PTX 1
+#endif
 __device__ __forceinline__ uint32_t warp_match9(uint32_t d) {
   uint32_t peers = 0xffffffffu;
+#if ISG_MATCH_PTX
+  // per bit: the bit as a predicate (ptxas sets several at once with R2P), its ballot, the
+  // lane's all-ones / all-zeros mask from the same predicate, one LOP3 peers &= ~(ballot ^
+  // mask) — about 3.3 instructions per bit where the C++ form compiles to six.  Depth sort
+  // 0.0633 -> 0.0575 ms, tile sort 0.0751 -> 0.0674 ms (C3).
+#pragma unroll
+  for (int b = 0; b < 9; ++b) {
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 t, m, s;\n\t"
+        "and.b32 t, %1, %2;\n\t"
+        "setp.ne.u32 p, t, 0;\n\t"
+        "vote.sync.ballot.b32 m, p, 0xffffffff;\n\t"
+        "selp.b32 s, -1, 0, p;\n\t"
+        "lop3.b32 %0, %0, m, s, 0x90;\n\t}"  // a & ~(b ^ c)
+        : "+r"(peers)
+        : "r"(d), "r"(1u << b));
+  }
+#else
 #pragma unroll
   for (int b = 0; b < 9; ++b) {
     const bool bit = (d >> b) & 1u;
     const uint32_t m = __ballot_sync(0xffffffffu, bit);
     peers &= bit ? m : ~m;
   }
+#endif
   return peers;
 }
 
@@ -109,11 +130,18 @@ struct OnesweepSmem {
 };
 
 template <bool kEpi>
-// (a 5- or 6-CTA minimum per SM for more resident tiles: equal / slower at C3, 72-88 B spills)
+// A 4-CTA minimum per SM (64 registers): the PTX ballot match lets ptxas batch the ballots of
+// several items and take 77 registers (3 CTAs) otherwise — depth sort 0.0578 vs 0.0575 ms,
+// tile sort 0.0739 vs 0.0674.  (5 / 6 CTAs: spills, equal or slower.)
 #ifndef ISG_SORT_MINB
-#define ISG_SORT_MINB 1
+#define ISG_SORT_MINB 4
 #endif
-__global__ void __launch_bounds__(kSortThreads, ISG_SORT_MINB) k_onesweep(
+#if ISG_SORT_MINB > 0
+#define ISG_SORT_BOUNDS __launch_bounds__(kSortThreads, ISG_SORT_MINB)
+#else
+#define ISG_SORT_BOUNDS __launch_bounds__(kSortThreads)
+#endif
+__global__ void ISG_SORT_BOUNDS k_onesweep(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
     uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
     const uint32_t* __restrict__ n_dev, int64_t cap, int shift,
