@@ -161,10 +161,12 @@ isg_status isg_grads_device(isg_ctx* ctx, float** grads_dev);
 isg_status isg_adam_step(isg_ctx* ctx, const float lr[4], float beta1, float beta2, float eps);
 /* Loss of the last Adam step's views (all-reduced over ranks when NCCL is attached; syncs). */
 isg_status isg_last_step_loss(isg_ctx* ctx, double* loss_out);
-/* Asynchronous form: enqueues the device-to-host copy of the last Adam step's loss into
+/* Asynchronous form: enqueues the device-to-host transfer of the last Adam step's loss into
  * `host_dst` on the context stream and returns at once (no sync, no frame check; it can be
- * captured into a graph).  `host_dst` should be page-locked; the value is valid once the stream
- * has passed the copy — the pipelined training loop reads step i's loss while step i + 1 runs. */
+ * captured into a graph).  Page-locked `host_dst` is written by a one-thread kernel through its
+ * mapped device address (no copy engine); pageable memory falls back to cudaMemcpyAsync.  The
+ * value is valid once the stream has passed the transfer — the pipelined training loop reads
+ * step i's loss while step i + 1 runs. */
 isg_status isg_step_loss_async(isg_ctx* ctx, double* host_dst);
 /* weight * mse of one view without gradients (forward + loss only; device target; syncs).
  * Pending per-view gradients are preserved. */

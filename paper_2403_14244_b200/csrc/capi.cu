@@ -1244,9 +1244,28 @@ isg_status isg_last_step_loss(isg_ctx* ctx, double* loss_out) {
   return ISG_OK;
 }
 
+namespace {
+// The step loss straight into mapped pinned host memory: one thread's store over PCIe, chained
+// to the Adam kernel by programmatic dependent launch (a D2H memcpy node would go through a copy
+// engine and cost the next graph launch ~10 us of latency).
+__global__ void k_store_loss(const double* __restrict__ src, double* __restrict__ dst) {
+  isg::pdl_enter();
+  *dst = *src;
+}
+}  // namespace
+
 isg_status isg_step_loss_async(isg_ctx* ctx, double* host_dst) {
   if (!ctx || !host_dst) return ISG_E_ARG;
   cudaSetDevice(ctx->device);
+  cudaPointerAttributes pa{};
+  if (cudaPointerGetAttributes(&pa, host_dst) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+      pa.devicePointer != nullptr) {
+    ISG_CUDA(isg::launch_pdl(k_store_loss, dim3(1), dim3(1), 0, ctx->stream,
+                             (const double*)(ctx->loss + 2), (double*)pa.devicePointer));
+    ctx->launches++;
+    return ISG_OK;
+  }
+  cudaGetLastError();  // (pageable memory: cudaPointerGetAttributes reports it unregistered)
   ISG_CUDA(cudaMemcpyAsync(host_dst, ctx->loss + 2, sizeof(double), cudaMemcpyDeviceToHost,
                            ctx->stream));
   return ISG_OK;
