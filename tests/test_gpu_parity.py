@@ -983,6 +983,14 @@ def test_step_loss_async_in_graph_matches_sync_read():
             g.launch()
             r.synchronize()
             assert float(host[0]) == r.last_step_loss() > 0.0
+        # page-locked memory is written by a kernel through its mapped address; pageable
+        # memory takes the cudaMemcpyAsync path (not capturable, so outside a graph)
+        pageable = np.zeros(1, np.float64)
+        r.loss_backward_device(cam, target.data_ptr())
+        r.adam_step(isg.AdamConfig())
+        r.step_loss_async(pageable.ctypes.data)
+        r.synchronize()
+        assert pageable[0] == r.last_step_loss() > 0.0
 
 
 def test_three_pass_tile_sort_many_tiles():
