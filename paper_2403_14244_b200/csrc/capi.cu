@@ -1266,7 +1266,7 @@ isg_status isg_step_loss_async(isg_ctx* ctx, double* host_dst) {
     return ISG_OK;
   }
   cudaGetLastError();  // (pageable memory: cudaPointerGetAttributes reports it unregistered)
-  ISG_CUDA(cudaMemcpyAsync(host_dst, ctx->loss + 2, sizeof(double), cudaMemcpyDeviceToHost,
+  ISG_CUDA(cudaMemcpyAsync(host_dst, ctx->loss + 2, sizeof(double), cudaMemcpyDefault,
                            ctx->stream));
   return ISG_OK;
 }
