@@ -17,8 +17,18 @@
 
 namespace isg {
 
+// 5 CTAs / SM (47 registers, no spills): C3 0.0389 vs 0.0391 ms, C5 0.391 vs 0.398 ms against
+// ptxas's own 58; 6 / 8 spill and are slower
+#ifndef ISG_K1_MINB
+#define ISG_K1_MINB 5
+#endif
+#if ISG_K1_MINB > 0
+#define ISG_K1_BOUNDS __launch_bounds__(256, ISG_K1_MINB)
+#else
+#define ISG_K1_BOUNDS __launch_bounds__(256)
+#endif
 template <bool kBucket>  // tile-bucket binning: also bump the per-tile counters
-__global__ void __launch_bounds__(256) k_preprocess(const float4* __restrict__ ms,
+__global__ void ISG_K1_BOUNDS k_preprocess(const float4* __restrict__ ms,
                                                     const float4* __restrict__ co, int64_t n,
                                                     FrameParams fp, RenderRec* __restrict__ rec,
                                                     uint32_t* __restrict__ depth_key,
