@@ -18,7 +18,7 @@
 // has transmittance <= t_min.
 //
 // The 3-sigma test is bit-identical to the FP32 oracle (explicit _rn arithmetic); exp uses
-// ex2.approx on a per-splat precomputed -log2(e)/sigma2d^2.
+// ex2.approx of r2 * (-log2(e)/sigma2d^2) + log2(opacity), both precomputed per splat by K1.
 #include "blend_common.cuh"
 
 namespace isg {
@@ -77,7 +77,7 @@ __device__ __forceinline__ void fwd_pair(FwdPair& p, float2 r2, const float4 g, 
   const bool in1 = !(r2.y > g.z) && (!kTerm || p.T.y > t_min);
   // an excluded pixel's exponential is never evaluated (predicated MUFU into a zeroed pair), so
   // its alpha is an exact 0
-  // c.w holds log2(opacity) (K1): alpha = o exp(-r2 / (2 s^2)) = ex2(r2 g.w + log2 o), one
+  // c.w holds log2(opacity) (K1): alpha = o exp(-r2 / s^2) = ex2(r2 g.w + log2 o), one
   // fused op (the backward forms it the same way)
   const float2 q = __ffma2_rn(r2, bc(g.w), bc(c.w));
   const float2 a = make_float2(in0 ? fast_exp2(q.x) : 0.0f, in1 ? fast_exp2(q.y) : 0.0f);
