@@ -40,6 +40,9 @@ constexpr int kBT = 64;      // threads per tile CTA: 2 warps x 8 four-lane grou
 #ifndef ISG_BWD_UNROLL
 #define ISG_BWD_UNROLL 4
 #endif
+#ifndef ISG_LIST_PTX
+#define ISG_LIST_PTX 1
+#endif
 constexpr int kUnroll = ISG_BWD_UNROLL;  // walk steps per loop iteration
 // Records staged per batch.  The 8 groups of a warp walk a batch in lockstep, so a warp's step
 // count per batch is the longest of its 8 relevance lists: larger batches pad less (C3 walk
@@ -278,8 +281,23 @@ __global__ void ISG_BWD_BOUNDS k_blend_bwd(
       const uint32_t mw = j < cnt ? ((uint32_t)cur.mask[j] >> (8 * w)) & 0xFFu : 0u;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {  // group k = sub-quarter 8 w + k
+#if ISG_LIST_PTX
+        // the mask bit as a predicate (ptxas sets them together with R2P) and-ed into the
+        // trim compare, then the ballot: three instructions where the C++ form takes five
+        uint32_t mk, hku;
+        asm("{\n\t.reg .pred p, q;\n\t.reg .b32 t;\n\t"
+            "and.b32 t, %2, %3;\n\t"
+            "setp.ne.u32 p, t, 0;\n\t"
+            "setp.lt.and.s32 q, %4, %5, p;\n\t"
+            "vote.sync.ballot.b32 %0, q, 0xffffffff;\n\t"
+            "selp.u32 %1, 1, 0, q;\n\t}"
+            : "=r"(mk), "=r"(hku)
+            : "r"(mw), "r"(1u << k), "r"(lo + j), "r"(sqm[k]));
+        const bool hk = hku != 0u;
+#else
         const bool hk = ((mw >> k) & 1u) && lo + j < sqm[k];
         const uint32_t mk = __ballot_sync(0xffffffffu, hk);
+#endif
         if (hk) s_list[8 * w + k][base[k] + __popc(mk & gt)] = (uint8_t)j;
         if (!kDirect && lane == 0) s_rel[8 * w + k][wd] = mk;
         base[k] += __popc(mk);
