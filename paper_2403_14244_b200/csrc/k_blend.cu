@@ -131,21 +131,25 @@ __global__ void ISG_FWD_BOUNDS k_blend_fwd(
   const float2 PX = make_float2((float)x0 + 0.5f, (float)x0 + 1.5f);
   const float2 PY = make_float2((float)y0 + 0.5f, (float)y0 + 1.5f);
   // the warp's 8 sub-quarters: 4 columns of the tile (x = 4c) x 2 rows (y = 8w + 4r)
+  // Untracked frames give a column or row of sub-quarters outside the image the span 1e30:
+  // the rounded square of the distance is +inf and no record tests relevant to it, so the
+  // per-record tests need no validity predicates (render 0.1995 -> 0.1974 ms).  Tracked frames
+  // keep the predicates (without them ptxas spills in that variant).
   float cx0[4], cx1[4], ry0[2], ry1[2];
   bool cv[4], rv[2];
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
     const int xs = tx * kTile + 4 * c;
     cv[c] = xs < W;
-    cx0[c] = (float)xs + 0.5f;
-    cx1[c] = (float)(min(xs + 4, W) - 1) + 0.5f;
+    cx0[c] = (kTrack || xs < W) ? (float)xs + 0.5f : 1e30f;
+    cx1[c] = (kTrack || xs < W) ? (float)(min(xs + 4, W) - 1) + 0.5f : 1e30f;
   }
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
     const int ys = ty * kTile + 8 * w + 4 * r;
     rv[r] = ys < H;
-    ry0[r] = (float)ys + 0.5f;
-    ry1[r] = (float)(min(ys + 4, H) - 1) + 0.5f;
+    ry0[r] = (kTrack || ys < H) ? (float)ys + 0.5f : 1e30f;
+    ry1[r] = (kTrack || ys < H) ? (float)(min(ys + 4, H) - 1) + 0.5f : 1e30f;
   }
   // tracked frames leave each entry's relevance bits for the backward: byte w of submask[e]
   uint8_t* const mask_bytes = reinterpret_cast<uint8_t*>(submask);
@@ -194,7 +198,8 @@ __global__ void ISG_FWD_BOUNDS k_blend_fwd(
       if (32 * wd >= cnt) break;  // warp-uniform
       const int j = 32 * wd + lane;
       const bool in = j < cnt;
-      const float4 g = cur.geo[in ? j : 0];
+      // past the batch: the sentinel, never relevant (tracked frames test `in` explicitly)
+      const float4 g = cur.geo[in ? j : (kTrack ? 0 : kBatch)];
       float ax4[4], ay2[2];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -210,7 +215,7 @@ __global__ void ISG_FWD_BOUNDS k_blend_fwd(
 #pragma unroll
       for (int k = 0; k < 8; ++k) {  // group k: quarter 2w + (k >> 2), sub (k & 3)
         const int c = (k >> 2) * 2 + (k & 1), r = (k >> 1) & 1;
-        const bool hk = in && cv[c] && rv[r] && !(__fadd_rn(ax4[c], ay2[r]) > g.z);
+        const bool hk = (!kTrack || (in && cv[c] && rv[r])) && !(__fadd_rn(ax4[c], ay2[r]) > g.z);
         mw |= (hk ? 1u : 0u) << k;
         const uint32_t mk = __ballot_sync(0xffffffffu, hk);
         if (hk) s_list[8 * w + k][base[k] + __popc(mk & lt)] = (uint8_t)j;
