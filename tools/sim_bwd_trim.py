@@ -126,3 +126,27 @@ for seg in np.split(order_rows, bounds):
                 adv = np.minimum(steps - rem, L[b + 1])
                 rem = L[b + 1] - adv
 print(f"one-batch lookahead: {tot_la:,} warp steps ({tot_la / tot_lock:.3f} of lockstep {tot_lock:,})")
+
+# exact masks: a sub-quarter is listed for an entry only if one of its 16 pixel centres is
+# inside the circle and the pixel has not finished before the entry (what K6 could record
+# from its own walk instead of the closest-point box test)
+ex = np.zeros((len(g), 16), bool)
+for r4 in range(4):
+    for c4 in range(4):
+        hit = np.zeros(len(g), bool)
+        for rr in range(4):
+            for cc in range(4):
+                y = ty * 16 + 4 * r4 + rr
+                x = tx * 16 + 4 * c4 + cc
+                ok = (y < H) & (x < W)
+                yy, xx = np.minimum(y, H - 1), np.minimum(x, W - 1)
+                d2 = (xx + 0.5 - u[g]) ** 2 + (yy + 0.5 - v[g]) ** 2
+                hit |= ok & (d2 <= r2m[g]) & (pos < npr[yy, xx])
+        ex[:, 4 * r4 + c4] = hit
+ex = ex[:, order]
+Ce = np.zeros((len(uk), 16), np.int64)
+for k in range(16):
+    Ce[:, k] = np.bincount(inv, weights=ex[:, k], minlength=len(uk))
+lock_e = Ce[:, :8].max(1).sum() + Ce[:, 8:].max(1).sum()
+print(f"exact per-sub-quarter masks: lockstep {lock_e:,} warp steps ({lock_e / lock:.3f} of the box masks'); "
+      f"listed group-entries {ex.sum():,} vs {rel.sum():,}")
