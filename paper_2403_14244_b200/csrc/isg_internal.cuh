@@ -107,9 +107,12 @@ int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], bool iota_vals, const
 // Byte size of a sort's look-back region for `passes` passes over up to `cap` items.
 // Per pass: one status row (256 words) per tile (level 1) and one per group of tiles (level 2,
 // k_sort.cu's two-level look-back; rows for groups of 8 tiles or more).
+#ifndef ISG_LOOKBACK_GROUP
+#define ISG_LOOKBACK_GROUP 8
+#endif
 inline size_t sort_lookback_words(int64_t tiles) {
   const int64_t t = std::max<int64_t>(tiles, 1);
-  return (size_t)256 * (t + (t + 7) / 8);
+  return (size_t)256 * (t + (t + ISG_LOOKBACK_GROUP - 1) / ISG_LOOKBACK_GROUP);
 }
 inline size_t sort_lookback_bytes(int64_t cap, int passes) {
   return sizeof(uint32_t) * sort_lookback_words(sort_tiles_for(cap)) * passes;
